@@ -1,0 +1,35 @@
+# Build of every native artefact, in-tree (the .so files travel to the GPU box).
+#   libsbdt_gpu.so   : sm_100a kernels + the C ABI (include/sbdt_gpu.h)        [product]
+#   libsbdt_host.so  : host setup (generators, DT builder, partitioner)        [setup]
+#   oracle/liboracle.so : CPU restatement of the path (tests / cpu baseline)   [checker]
+#   oracle/_ref/*    : reference sources compiled by path (only where /root/reference exists)
+PKG      := paper_1902_07554_b200
+CSRC     := $(PKG)/csrc
+NVCC     ?= nvcc
+CXX      ?= g++
+# FP64 bit-exactness: no contraction anywhere.
+CXXFLAGS := -O3 -std=c++20 -fPIC -ffp-contract=off -Wall -Wextra -Wno-unused-parameter
+NVFLAGS  := -O3 -std=c++20 -gencode arch=compute_100a,code=sm_100a -lineinfo -fmad=false \
+            -Xcompiler -fPIC -Xcompiler -ffp-contract=off --expt-relaxed-constexpr -Xptxas -v
+
+GPU_SRC  := $(wildcard $(CSRC)/gpu/*.cu)
+GPU_HDR  := $(wildcard $(CSRC)/gpu/*.cuh) $(wildcard $(CSRC)/common/*.hpp) include/sbdt_gpu.h
+HOST_SRC := $(CSRC)/host/delaunay.cpp $(CSRC)/host/setup.cpp $(CSRC)/host/host_capi.cpp
+HOST_HDR := $(wildcard $(CSRC)/host/*.hpp) $(CSRC)/common/predicates.hpp
+
+all: $(PKG)/libsbdt_gpu.so $(PKG)/libsbdt_host.so oracle
+
+$(PKG)/libsbdt_host.so: $(HOST_SRC) $(HOST_HDR)
+	$(CXX) $(CXXFLAGS) -shared -o $@ $(HOST_SRC) -lpthread
+
+$(PKG)/libsbdt_gpu.so: $(GPU_SRC) $(GPU_HDR)
+	$(NVCC) $(NVFLAGS) -Iinclude -shared -o $@ $(GPU_SRC) 2> $(PKG)/ptxas.log || (cat $(PKG)/ptxas.log; exit 1)
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -f $(PKG)/*.so $(PKG)/ptxas.log
+	$(MAKE) -C oracle clean
+
+.PHONY: all oracle clean

@@ -1,0 +1,152 @@
+/*
+ * sbdt_gpu.h — C ABI of libsbdt_gpu.so, the B200 (sm_100a) implementation of
+ * the sample-based divide step's data-parallel core (arXiv 1902.07554):
+ *
+ *   sbdt_gpu_assign_points*  replaces  sample-partition `assign_points`
+ *       (Alg. 2 lines "find nearest
+ *       sample point" / "assign p to v_n's partition") and the
+ *       Partitioning.parts bucketing.
+ *   sbdt_gpu_find_border*    replaces  dc-engine `find_border` with the
+ *       border-geom `GridIndex` / `intersects_{bbox,grid}` queries
+ *       (Alg. 1 border block) on the
+ *       reference's Triangulation<D> records (proj/include/sbdt/triangulation.hpp:17-68).
+ *
+ * Neither reference operation ships as code; the C++
+ * drop-in headers include/sbdt/sample_partition.hpp and include/sbdt/border.hpp
+ * declare them with the SPEC's signatures and call this ABI. Conventions:
+ *   - plain pointers and sizes only; no exception crosses the ABI;
+ *   - status 0 = ok; nonzero codes below map to the reference's exception
+ *     types (common.hpp:22-65) in the C++ wrapper; sbdt_gpu_last_error() has
+ *     the message;
+ *   - *_dev entry points take DEVICE pointers and are asynchronous on the
+ *     context's stream; the plain entry points take HOST buffers (H2D/D2H
+ *     inside) and are synchronous;
+ *   - one host thread per context.
+ * Results are bit-identical to the CPU oracle: labels, positive flags,
+ * hull-reachable border flags and border-vertex ids; circumcentres/radii are
+ * the reference's binary64 expressions evaluated in the same order.
+ */
+#ifndef SBDT_GPU_H_
+#define SBDT_GPU_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sbdt_gpu_ctx sbdt_gpu_ctx;
+
+enum sbdt_status {
+  SBDT_OK = 0,
+  SBDT_ERR_INVALID = 1,    /* std::invalid_argument                     */
+  SBDT_ERR_DEGENERATE = 2, /* sbdt::DegenerateSimplex (geometry.cpp:281) */
+  SBDT_ERR_CUDA = 3,       /* std::runtime_error                        */
+  SBDT_ERR_OOM = 4,        /* std::bad_alloc                            */
+  SBDT_ERR_RANGE = 5       /* grid larger than 4 n / c_G^D cells         */
+};
+
+/* IntersectionPolicy::Kind */
+enum sbdt_policy { SBDT_POLICY_BBOX = 0, SBDT_POLICY_GRID = 1, SBDT_POLICY_EXACT = 2 };
+
+/* find_border flags */
+enum sbdt_border_flags {
+  SBDT_BORDER_HULL_BFS = 1u /* also compute the SPEC find_border BFS subset (border_out) */
+};
+
+int sbdt_gpu_create(int device, sbdt_gpu_ctx** out);
+void sbdt_gpu_destroy(sbdt_gpu_ctx* ctx);
+const char* sbdt_gpu_last_error(const sbdt_gpu_ctx* ctx);
+/* Use an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream);
+ * NULL restores the context's own stream. */
+int sbdt_gpu_set_stream(sbdt_gpu_ctx* ctx, void* cuda_stream);
+int sbdt_gpu_synchronize(sbdt_gpu_ctx* ctx);
+/* Number of kernels launched by this context so far. */
+unsigned long long sbdt_gpu_launch_count(const sbdt_gpu_ctx* ctx);
+/* Reads and clears the device status word; returns the mapped status. */
+int sbdt_gpu_check_status(sbdt_gpu_ctx* ctx);
+
+/* ---- assign_points -------------------------------------
+ * coords: n points, AoS binary64 (PointSet::raw(), geometry.hpp:94-95).
+ * sample_ids: m global PointIds; sample_labels: m labels < k.
+ * labels_out[i] = sample_labels[argmin_s squared_distance(p_i, p_s)], ties
+ * toward the lowest sample PointId.
+ * part_offsets_out (k+1, optional) and part_ids_out (n, optional) receive
+ * Partitioning.parts as CSR, ids ascending within each part.
+ * bbox_out (optional, 2*dim doubles: lo[], hi[]) receives the global point
+ * bounding box, fused into the same pass. */
+int sbdt_gpu_assign_points(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint64_t n,
+                           const uint32_t* sample_ids, const uint32_t* sample_labels, uint32_t m,
+                           uint32_t k, uint32_t* labels_out, uint64_t* part_offsets_out,
+                           uint32_t* part_ids_out, double* bbox_out);
+
+/* Device-pointer variant. d_bbox_ordered_out (optional) receives 2*dim
+ * order-preserving uint64 keys of the bbox (input of sbdt_gpu_find_border_dev). */
+int sbdt_gpu_assign_points_dev(sbdt_gpu_ctx* ctx, int dim, const double* d_coords, uint64_t n,
+                               const uint32_t* d_sample_ids, const uint32_t* d_sample_labels,
+                               uint32_t m, uint32_t k, uint32_t* d_labels_out,
+                               uint64_t* d_part_offsets_out, uint32_t* d_part_ids_out,
+                               uint64_t* d_bbox_ordered_out);
+
+/* ---- find_border ---------------------------------------
+ * The k partial triangulations are concatenated: part p owns simplex rows
+ * [offsets[p], offsets[p+1]). Per row s, in vertex-major SoA (row j holds
+ * Simplex::vertices[j] / neighbors[j] of every simplex):
+ *   verts[j*S + s]  global PointId, ascending, kInfiniteVertex (0xFFFFFFFF) last
+ *   nbrs[j*S + s]   part-local SimplexId sharing the facet opposite verts[j]
+ *   parity[s]       Simplex::parity (orientation sign of the stored order)
+ * labels[i] is the partition of point i (the GridIndex of part j is built from
+ * the points labelled j; cell edge c_G (V/n)^(1/D) over the global bbox).
+ * Outputs (caller buffers):
+ *   positive_out[s]  1 iff the (inflated) circumsphere / hull halfspace of s
+ *                    reaches a cell occupied by another part (full scan);
+ *   border_out[s]    (optional; needs SBDT_BORDER_HULL_BFS) the SPEC BFS
+ *                    subset: positive simplices connected through positive
+ *                    simplices to a hull simplex (hull_simplices,
+ *                    triangulation.cpp:34-53);
+ *   vertex_ids_out   sorted unique finite vertices of positive simplices
+ *                    (capacity n), count in *n_vertices_out;
+ *   bfs_vertex_ids_out / n_bfs_vertices_out (optional): same for border_out;
+ *   spheres_out      (optional) (dim+1) doubles per row: inflated centre, r^2
+ *                    (zeros for infinite rows). */
+int sbdt_gpu_find_border(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint64_t n,
+                         const uint32_t* labels, uint32_t k, const uint64_t* offsets,
+                         const uint32_t* verts, const uint32_t* nbrs, const int8_t* parity,
+                         int policy, double c_G, uint32_t flags, uint8_t* positive_out,
+                         uint8_t* border_out, uint32_t* vertex_ids_out, uint64_t* n_vertices_out,
+                         uint32_t* bfs_vertex_ids_out, uint64_t* n_bfs_vertices_out,
+                         double* spheres_out);
+
+typedef struct sbdt_border_args {
+  int dim;
+  const double* d_xyz;
+  uint64_t n;
+  const uint32_t* d_labels;
+  uint32_t k;
+  const uint64_t* d_offsets; /* k+1 */
+  const uint32_t* d_verts;
+  const uint32_t* d_nbrs;
+  const int8_t* d_parity;
+  uint64_t S;
+  int policy;
+  double c_G;
+  uint32_t flags;
+  const uint64_t* d_bbox_ordered; /* optional: from sbdt_gpu_assign_points_dev */
+  uint8_t* d_positive;            /* S */
+  uint8_t* d_border;              /* S, optional (HULL_BFS) */
+  uint8_t* d_vertex_flags;        /* n scratch */
+  uint32_t* d_vertex_ids;         /* n */
+  uint64_t* d_vertex_count;       /* 1 */
+  uint8_t* d_bfs_vertex_flags;    /* n scratch, optional */
+  uint32_t* d_bfs_vertex_ids;     /* n, optional */
+  uint64_t* d_bfs_vertex_count;   /* 1, optional */
+  double* d_spheres;              /* S*(dim+1), optional */
+} sbdt_border_args;
+
+int sbdt_gpu_find_border_dev(sbdt_gpu_ctx* ctx, const sbdt_border_args* args);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SBDT_GPU_H_ */

@@ -1,0 +1,399 @@
+// K1/K2/K3 — point-to-partition assignment (Alg. 2 line
+// "find nearest sample point") on sm_100a.
+//
+// label(p) = sample_labels[argmin_s squared_distance(p, s)], ties -> lowest
+// sample PointId, with squared_distance evaluated exactly as
+// geometry.hpp:102-110 (binary64, left-to-right, no contraction), so labels
+// are bit-identical to a brute-force scan.
+//
+// K1  sample grid: samples gathered into 32-byte records {x,y,z,pid,label}
+//     bucketed by a uniform grid (~2 samples/cell) -> CSR. O(m), L2 resident.
+// K2  per-point exact search: own cell, then Chebyshev rings; a ring is
+//     pruned only when a rigorous lower bound (binning error + rounding
+//     margin) proves every unvisited sample strictly farther in binary64.
+//     Fused: global point bbox (min/max) for the grid index that follows.
+// K3  stable counting sort by label -> Partitioning.parts (ascending ids).
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "context.cuh"
+#include "scan.cuh"
+#include "sbdt_gpu.h"
+
+namespace sbdt_gpu {
+
+struct __align__(16) SampleRec {
+  double x[3];
+  std::uint32_t pid;
+  std::uint32_t label;
+};
+
+template <int D>
+struct SampleGrid {
+  Grid<D> g;
+  double margin;         // binning + rounding slack in coordinate units
+  unsigned long long cells;
+};
+
+constexpr int kBlock = 256;
+
+// Block-reduce local bbox then one atomic per block per coordinate.
+template <int D>
+__device__ __forceinline__ void bbox_flush(const double* lo, const double* hi, unsigned long long* bbox) {
+  __shared__ unsigned long long s_lo[D], s_hi[D];
+  if (threadIdx.x < D) {
+    s_lo[threadIdx.x] = 0xFFFFFFFFFFFFFFFFULL;
+    s_hi[threadIdx.x] = 0ULL;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    double a = lo[d], b = hi[d];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
+      b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+    }
+    if (lane_id() == 0) {
+      atomicMin(&s_lo[d], dbl_to_ordered(a));
+      atomicMax(&s_hi[d], dbl_to_ordered(b));
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < D) {
+    atomicMin(&bbox[threadIdx.x], s_lo[threadIdx.x]);
+    atomicMax(&bbox[D + threadIdx.x], s_hi[threadIdx.x]);
+  }
+}
+
+__global__ void k_bbox_init(unsigned long long* bbox, int dim) {
+  if (threadIdx.x < static_cast<unsigned>(dim)) {
+    bbox[threadIdx.x] = 0xFFFFFFFFFFFFFFFFULL;
+    bbox[dim + threadIdx.x] = 0ULL;
+  }
+}
+
+template <int D>
+__global__ void k_sample_gather(const double* __restrict__ xyz, const std::uint32_t* __restrict__ sample_ids,
+                                const std::uint32_t* __restrict__ sample_labels, std::uint32_t m,
+                                SampleRec* __restrict__ recs, unsigned long long* bbox) {
+  double lo[D], hi[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) lo[d] = INFINITY, hi[d] = -INFINITY;
+  for (std::uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < m; s += gridDim.x * blockDim.x) {
+    const std::uint32_t pid = sample_ids[s];
+    SampleRec r;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) r.x[d] = 0.0;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      r.x[d] = xyz[std::size_t(pid) * D + d];
+      lo[d] = fmin(lo[d], r.x[d]);
+      hi[d] = fmax(hi[d], r.x[d]);
+    }
+    r.pid = pid;
+    r.label = sample_labels[s];
+    recs[s] = r;
+  }
+  bbox_flush<D>(lo, hi, bbox);
+}
+
+// Sample-grid parameters: ~2 samples per cell, cell count capped at cap.
+template <int D>
+__global__ void k_sample_grid_params(const unsigned long long* bbox, std::uint32_t m, unsigned long long cap,
+                                     SampleGrid<D>* sg) {
+  double lo[D], hi[D], vol = 1.0, ext_max = 0.0, mag = 0.0;
+  for (int d = 0; d < D; ++d) {
+    lo[d] = ordered_to_dbl(bbox[d]);
+    hi[d] = ordered_to_dbl(bbox[D + d]);
+    const double ext = hi[d] - lo[d];
+    vol *= ext;
+    ext_max = fmax(ext_max, ext);
+    mag = fmax(mag, fmax(fabs(lo[d]), fabs(hi[d])));
+  }
+  const double per = 2.0 * vol / static_cast<double>(m > 0 ? m : 1);
+  double e = (D == 2) ? sqrt(per) : cbrt_det(per);
+  if (!(e > 0.0)) e = ext_max > 0.0 ? ext_max / 64.0 : 1.0;
+  unsigned long long cells;
+  long long dims[D];
+  for (;;) {
+    cells = 1;
+    for (int d = 0; d < D; ++d) {
+      dims[d] = static_cast<long long>(floor((hi[d] - lo[d]) / e)) + 1;
+      cells *= static_cast<unsigned long long>(dims[d]);
+    }
+    if (cells <= cap) break;
+    e *= 2.0;
+  }
+  for (int d = 0; d < D; ++d) {
+    sg->g.lo[d] = lo[d];
+    sg->g.dims[d] = dims[d];
+  }
+  sg->g.edge = e;
+  sg->cells = cells;
+  sg->margin = 1e-12 * (mag + ext_max + e);
+}
+
+template <int D>
+__device__ __forceinline__ long long linear(const Grid<D>& g, const long long* c) {
+  long long id = c[D - 1];
+#pragma unroll
+  for (int d = D - 2; d >= 0; --d) id = id * g.dims[d] + c[d];
+  return id;
+}
+
+template <int D>
+__global__ void k_sample_count(const SampleRec* __restrict__ recs, std::uint32_t m, const SampleGrid<D>* sgp,
+                               std::uint32_t* __restrict__ counts, std::uint32_t* __restrict__ cell_of) {
+  const Grid<D> g = sgp->g;
+  for (std::uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < m; s += gridDim.x * blockDim.x) {
+    long long c[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) c[d] = cell_coord<D>(g, recs[s].x[d], d);
+    const std::uint32_t cell = static_cast<std::uint32_t>(linear<D>(g, c));
+    cell_of[s] = cell;
+    atomicAdd(&counts[cell], 1u);
+  }
+}
+
+__global__ void k_sample_scatter(const SampleRec* __restrict__ recs, std::uint32_t m,
+                                 const std::uint32_t* __restrict__ cell_of, const std::uint32_t* __restrict__ starts,
+                                 std::uint32_t* __restrict__ fill, SampleRec* __restrict__ sorted) {
+  for (std::uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < m; s += gridDim.x * blockDim.x) {
+    const std::uint32_t c = cell_of[s];
+    sorted[starts[c] + atomicAdd(&fill[c], 1u)] = recs[s];
+  }
+}
+
+// K2: exact nearest-sample search, one thread per point.
+template <int D>
+__global__ void __launch_bounds__(kBlock) k_assign(const double* __restrict__ xyz, std::uint64_t n,
+                                                   const SampleGrid<D>* __restrict__ sgp,
+                                                   const std::uint32_t* __restrict__ starts,
+                                                   const SampleRec* __restrict__ sorted,
+                                                   std::uint32_t* __restrict__ labels,
+                                                   unsigned long long* bbox) {
+  __shared__ SampleGrid<D> s_sg;
+  if (threadIdx.x == 0) s_sg = *sgp;
+  __syncthreads();
+  const Grid<D>& g = s_sg.g;
+  const double margin = s_sg.margin;
+  double blo[D], bhi[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) blo[d] = INFINITY, bhi[d] = -INFINITY;
+
+  for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += std::uint64_t(gridDim.x) * blockDim.x) {
+    double x[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      x[d] = xyz[i * D + d];
+      blo[d] = fmin(blo[d], x[d]);
+      bhi[d] = fmax(bhi[d], x[d]);
+    }
+    long long ci[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) ci[d] = cell_coord<D>(g, x[d], d);
+    double best = INFINITY;
+    std::uint32_t best_pid = 0xFFFFFFFFu, best_label = 0;
+    for (long long r = 0;; ++r) {
+      long long lo_c[D], hi_c[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        lo_c[d] = ci[d] - r < 0 ? 0 : ci[d] - r;
+        hi_c[d] = ci[d] + r > g.dims[d] - 1 ? g.dims[d] - 1 : ci[d] + r;
+      }
+      long long c[D];
+      // enumerate the clamped cube, visiting only cells at Chebyshev distance r
+      if constexpr (D == 2) {
+        for (c[1] = lo_c[1]; c[1] <= hi_c[1]; ++c[1])
+          for (c[0] = lo_c[0]; c[0] <= hi_c[0]; ++c[0]) {
+            const long long cheb = max(llabs(c[0] - ci[0]), llabs(c[1] - ci[1]));
+            if (cheb != r) continue;
+            const long long cell = linear<D>(g, c);
+            for (std::uint32_t s = starts[cell], e = starts[cell + 1]; s < e; ++s) {
+              const SampleRec rec = sorted[s];
+              const double d2 = sqdist<D>(x, rec.x);
+              if (d2 < best || (d2 == best && rec.pid < best_pid)) {
+                best = d2;
+                best_pid = rec.pid;
+                best_label = rec.label;
+              }
+            }
+          }
+      } else {
+        for (c[2] = lo_c[2]; c[2] <= hi_c[2]; ++c[2])
+          for (c[1] = lo_c[1]; c[1] <= hi_c[1]; ++c[1])
+            for (c[0] = lo_c[0]; c[0] <= hi_c[0]; ++c[0]) {
+              const long long cheb = max(max(llabs(c[0] - ci[0]), llabs(c[1] - ci[1])), llabs(c[2] - ci[2]));
+              if (cheb != r) continue;
+              const long long cell = linear<D>(g, c);
+              for (std::uint32_t s = starts[cell], e = starts[cell + 1]; s < e; ++s) {
+                const SampleRec rec = sorted[s];
+                const double d2 = sqdist<D>(x, rec.x);
+                if (d2 < best || (d2 == best && rec.pid < best_pid)) {
+                  best = d2;
+                  best_pid = rec.pid;
+                  best_label = rec.label;
+                }
+              }
+            }
+      }
+      // lower bound on the distance to any sample in a cell at Chebyshev distance > r
+      double lb = INFINITY;
+      bool any = false;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        if (ci[d] - r > 0) {
+          lb = fmin(lb, x[d] - cell_lo<D>(g, ci[d] - r, d));
+          any = true;
+        }
+        if (ci[d] + r < g.dims[d] - 1) {
+          lb = fmin(lb, cell_lo<D>(g, ci[d] + r + 1, d) - x[d]);
+          any = true;
+        }
+      }
+      if (!any) break;
+      lb -= margin;
+      if (lb > 0.0 && (lb * lb) * (1.0 - 1e-12) > best) break;
+    }
+    labels[i] = best_label;
+  }
+  bbox_flush<D>(blo, bhi, bbox);
+}
+
+// ---- K3: stable bucketing of point ids by label ------------------------------
+constexpr int kBucketTile = 4096;  // points per CTA tile
+constexpr int kBucketThreads = 256;
+
+__global__ void k_bucket_count(const std::uint32_t* __restrict__ labels, std::uint64_t n, std::uint32_t k,
+                               std::uint32_t* __restrict__ tile_counts /* [k][tiles] */, std::uint32_t tiles) {
+  extern __shared__ std::uint32_t hist[];
+  for (std::uint32_t j = threadIdx.x; j < k; j += blockDim.x) hist[j] = 0;
+  __syncthreads();
+  const std::uint64_t base = std::uint64_t(blockIdx.x) * kBucketTile;
+  for (int t = threadIdx.x; t < kBucketTile; t += blockDim.x) {
+    const std::uint64_t i = base + t;
+    if (i < n) atomicAdd(&hist[labels[i]], 1u);
+  }
+  __syncthreads();
+  for (std::uint32_t j = threadIdx.x; j < k; j += blockDim.x) tile_counts[std::uint64_t(j) * tiles + blockIdx.x] = hist[j];
+}
+
+// Stable scatter: each warp owns a contiguous slice of the tile; per-warp
+// label histograms give exact in-order ranks.
+__global__ void __launch_bounds__(kBucketThreads) k_bucket_scatter(const std::uint32_t* __restrict__ labels,
+                                                                   std::uint64_t n, std::uint32_t k,
+                                                                   const std::uint32_t* __restrict__ tile_offsets,
+                                                                   std::uint32_t tiles,
+                                                                   std::uint32_t* __restrict__ part_ids) {
+  extern __shared__ std::uint32_t sh[];  // [warps][k]
+  constexpr int kWarps = kBucketThreads / 32;
+  constexpr int kSlice = kBucketTile / kWarps;
+  const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  for (std::uint32_t j = threadIdx.x; j < k * kWarps; j += blockDim.x) sh[j] = 0;
+  __syncthreads();
+  const std::uint64_t base = std::uint64_t(blockIdx.x) * kBucketTile + std::uint64_t(warp) * kSlice;
+  for (int t = lane; t < kSlice; t += 32) {
+    const std::uint64_t i = base + t;
+    if (i < n) atomicAdd(&sh[warp * k + labels[i]], 1u);
+  }
+  __syncthreads();
+  // exclusive scan across warps per label, plus the tile's global offset
+  for (std::uint32_t j = threadIdx.x; j < k; j += blockDim.x) {
+    std::uint32_t run = tile_offsets[std::uint64_t(j) * tiles + blockIdx.x];
+    for (int w = 0; w < kWarps; ++w) {
+      const std::uint32_t c = sh[w * k + j];
+      sh[w * k + j] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  for (int t0 = 0; t0 < kSlice; t0 += 32) {
+    const std::uint64_t i = base + t0 + lane;
+    const bool valid = i < n;
+    const std::uint32_t lab = valid ? labels[i] : 0xFFFFFFFFu;
+    const unsigned peers = __match_any_sync(0xffffffffu, lab);
+    const unsigned rank = __popc(peers & ((1u << lane) - 1u));
+    const int leader = __ffs(peers) - 1;
+    std::uint32_t basepos = 0;
+    if (valid) basepos = sh[warp * k + lab];
+    __syncwarp();
+    if (valid) part_ids[basepos + rank] = static_cast<std::uint32_t>(i);
+    if (valid && static_cast<int>(lane) == leader) sh[warp * k + lab] = basepos + __popc(peers);
+    __syncwarp();
+  }
+}
+
+// tile_offsets[j][t] = part_offset[j] + sum_{t'<t} counts[j][t'] via one flat
+// exclusive scan over the label-major [k][tiles] matrix.
+__global__ void k_part_offsets(const std::uint32_t* __restrict__ tile_offsets, std::uint32_t k, std::uint32_t tiles,
+                               std::uint64_t n, std::uint64_t* __restrict__ part_offsets) {
+  for (std::uint32_t j = threadIdx.x; j <= k; j += blockDim.x)
+    part_offsets[j] = (j == k) ? n : tile_offsets[std::uint64_t(j) * tiles];
+}
+
+// ---------------------------------------------------------------------------
+template <int D>
+int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const std::uint32_t* d_sample_ids,
+                const std::uint32_t* d_sample_labels, std::uint32_t m, std::uint32_t* d_labels,
+                unsigned long long* d_bbox) {
+  cudaStream_t st = ctx->stream;
+  const unsigned long long cap = 4ULL * m + 64;
+  SBDT_WS(recs, SampleRec, "assign.recs", m);
+  SBDT_WS(sorted, SampleRec, "assign.sorted", m);
+  SBDT_WS(sbbox, unsigned long long, "assign.sbbox", 2 * D);
+  SBDT_WS(sg, SampleGrid<D>, "assign.sg", 1);
+  SBDT_WS(counts, std::uint32_t, "assign.counts", cap + 1);
+  SBDT_WS(starts, std::uint32_t, "assign.starts", cap + 1);
+  SBDT_WS(cell_of, std::uint32_t, "assign.cell_of", m);
+  SBDT_WS(blocksums, std::uint32_t, "assign.blocksums", (cap + 1) / kScanTile + 2);
+
+  k_bbox_init<<<1, 32, 0, st>>>(sbbox, D);
+  k_bbox_init<<<1, 32, 0, st>>>(d_bbox, D);
+  const unsigned sblocks = static_cast<unsigned>((m + kBlock - 1) / kBlock);
+  k_sample_gather<D><<<sblocks, kBlock, 0, st>>>(d_xyz, d_sample_ids, d_sample_labels, m, recs, sbbox);
+  k_sample_grid_params<D><<<1, 1, 0, st>>>(sbbox, m, cap, sg);
+  SBDT_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(std::uint32_t) * (cap + 1), st));
+  k_sample_count<D><<<sblocks, kBlock, 0, st>>>(recs, m, sg, counts, cell_of);
+  exclusive_scan(counts, starts, cap + 1, blocksums, nullptr, st, &ctx->launches);
+  SBDT_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(std::uint32_t) * (cap + 1), st));
+  k_sample_scatter<<<sblocks, kBlock, 0, st>>>(recs, m, cell_of, starts, counts, sorted);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  const std::uint64_t want = (n + kBlock - 1) / kBlock;
+  const unsigned blocks = static_cast<unsigned>(want < std::uint64_t(sms) * 16 ? want : std::uint64_t(sms) * 16);
+  if (blocks > 0)
+    k_assign<D><<<blocks, kBlock, 0, st>>>(d_xyz, n, sg, starts, sorted, d_labels, d_bbox);
+  ctx->launches += 7 + (blocks > 0);
+  SBDT_CUDA_TRY(cudaGetLastError());
+  return kOk;
+}
+
+int bucket_impl(sbdt_gpu_ctx* ctx, const std::uint32_t* d_labels, std::uint64_t n, std::uint32_t k,
+                std::uint64_t* d_part_offsets, std::uint32_t* d_part_ids) {
+  cudaStream_t st = ctx->stream;
+  const std::uint32_t tiles = static_cast<std::uint32_t>((n + kBucketTile - 1) / kBucketTile);
+  if (tiles == 0) {
+    SBDT_CUDA_TRY(cudaMemsetAsync(d_part_offsets, 0, sizeof(std::uint64_t) * (k + 1), st));
+    return kOk;
+  }
+  const std::uint64_t cells = std::uint64_t(k) * tiles;
+  SBDT_WS(tc, std::uint32_t, "bucket.tc", cells + 1);
+  SBDT_WS(bs, std::uint32_t, "bucket.bs", (cells + 1) / kScanTile + 2);
+  k_bucket_count<<<tiles, kBucketThreads, sizeof(std::uint32_t) * k, st>>>(d_labels, n, k, tc, tiles);
+  exclusive_scan(tc, tc, cells, bs, nullptr, st, &ctx->launches);
+  k_part_offsets<<<1, 256, 0, st>>>(tc, k, tiles, n, d_part_offsets);
+  k_bucket_scatter<<<tiles, kBucketThreads, sizeof(std::uint32_t) * k * (kBucketThreads / 32), st>>>(
+      d_labels, n, k, tc, tiles, d_part_ids);
+  ctx->launches += 3;
+  SBDT_CUDA_TRY(cudaGetLastError());
+  return kOk;
+}
+
+template int assign_impl<2>(sbdt_gpu_ctx*, const double*, std::uint64_t, const std::uint32_t*, const std::uint32_t*,
+                            std::uint32_t, std::uint32_t*, unsigned long long*);
+template int assign_impl<3>(sbdt_gpu_ctx*, const double*, std::uint64_t, const std::uint32_t*, const std::uint32_t*,
+                            std::uint32_t, std::uint32_t*, unsigned long long*);
+
+}  // namespace sbdt_gpu

@@ -1,0 +1,275 @@
+// C ABI (include/sbdt_gpu.h): context management, host-buffer entry points
+// (H2D -> kernels -> D2H, synchronous) and device-pointer entry points
+// (asynchronous on the context stream). No exception crosses this boundary.
+#include <cuda_runtime.h>
+
+#include <new>
+#include <string>
+
+#include "common.cuh"
+#include "context.cuh"
+#include "sbdt_gpu.h"
+
+namespace sbdt_gpu {
+template <int D>
+int assign_impl(sbdt_gpu_ctx*, const double*, std::uint64_t, const std::uint32_t*, const std::uint32_t*,
+                std::uint32_t, std::uint32_t*, unsigned long long*);
+int bucket_impl(sbdt_gpu_ctx*, const std::uint32_t*, std::uint64_t, std::uint32_t, std::uint64_t*, std::uint32_t*);
+template <int D>
+int border_impl(sbdt_gpu_ctx*, const sbdt_border_args*);
+int reach_impl(sbdt_gpu_ctx*, const sbdt_border_args*);
+}  // namespace sbdt_gpu
+
+using namespace sbdt_gpu;
+
+namespace {
+
+template <typename T>
+int dalloc(sbdt_gpu_ctx* ctx, const char* name, std::size_t count, T** out) {
+  cudaError_t e = cudaSuccess;
+  *out = static_cast<T*>(workspace(ctx, name, sizeof(T) * (count ? count : 1), &e));
+  if (!*out) return fail_cuda(ctx, e, name);
+  return kOk;
+}
+
+int finish(sbdt_gpu_ctx* ctx) {
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) return fail_cuda(ctx, e, "cudaStreamSynchronize");
+  return sbdt_gpu_check_status(ctx);
+}
+
+}  // namespace
+
+#define TRY(x)                 \
+  do {                         \
+    const int rc_ = (x);       \
+    if (rc_ != kOk) return rc_; \
+  } while (0)
+
+extern "C" {
+
+int sbdt_gpu_create(int device, sbdt_gpu_ctx** out) {
+  if (!out) return SBDT_ERR_INVALID;
+  *out = nullptr;
+  sbdt_gpu_ctx* ctx = new (std::nothrow) sbdt_gpu_ctx();
+  if (!ctx) return SBDT_ERR_OOM;
+  ctx->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->d_status, sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaMemset(ctx->d_status, 0, sizeof(unsigned));
+  if (e != cudaSuccess) {
+    const int code = (e == cudaErrorMemoryAllocation) ? SBDT_ERR_OOM : SBDT_ERR_CUDA;
+    delete ctx;
+    return code;
+  }
+  ctx->own_stream = true;
+  *out = ctx;
+  return SBDT_OK;
+}
+
+void sbdt_gpu_destroy(sbdt_gpu_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  for (auto& kv : ctx->bufs)
+    if (kv.second.ptr) cudaFree(kv.second.ptr);
+  if (ctx->d_status) cudaFree(ctx->d_status);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* sbdt_gpu_last_error(const sbdt_gpu_ctx* ctx) { return ctx ? ctx->last_error.c_str() : "null context"; }
+
+int sbdt_gpu_set_stream(sbdt_gpu_ctx* ctx, void* stream) {
+  if (!ctx) return SBDT_ERR_INVALID;
+  if (ctx->own_stream && ctx->stream) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaStreamDestroy(ctx->stream);
+  }
+  if (stream) {
+    ctx->stream = static_cast<cudaStream_t>(stream);
+    ctx->own_stream = false;
+  } else {
+    cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return fail_cuda(ctx, e, "cudaStreamCreate");
+    ctx->own_stream = true;
+  }
+  return SBDT_OK;
+}
+
+int sbdt_gpu_synchronize(sbdt_gpu_ctx* ctx) {
+  if (!ctx) return SBDT_ERR_INVALID;
+  return finish(ctx);
+}
+
+unsigned long long sbdt_gpu_launch_count(const sbdt_gpu_ctx* ctx) { return ctx ? ctx->launches : 0ULL; }
+
+int sbdt_gpu_check_status(sbdt_gpu_ctx* ctx) {
+  if (!ctx) return SBDT_ERR_INVALID;
+  unsigned st = 0;
+  cudaError_t e = cudaMemcpy(&st, ctx->d_status, sizeof(unsigned), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return fail_cuda(ctx, e, "status readback");
+  if (st) cudaMemset(ctx->d_status, 0, sizeof(unsigned));
+  if (st & kStDegenerate) return fail(ctx, SBDT_ERR_DEGENERATE, "degenerate simplex (parity 0) in a partial triangulation");
+  if (st & kStGridCap) return fail(ctx, SBDT_ERR_RANGE, "grid index would exceed 4 n / c_G^D cells (degenerate bbox?)");
+  if (st & kStQueueOverflow) return fail(ctx, SBDT_ERR_RANGE, "escalation queue overflow");
+  return SBDT_OK;
+}
+
+int sbdt_gpu_assign_points_dev(sbdt_gpu_ctx* ctx, int dim, const double* d_coords, uint64_t n,
+                               const uint32_t* d_sample_ids, const uint32_t* d_sample_labels, uint32_t m,
+                               uint32_t k, uint32_t* d_labels_out, uint64_t* d_part_offsets_out,
+                               uint32_t* d_part_ids_out, uint64_t* d_bbox_ordered_out) {
+  if (!ctx) return SBDT_ERR_INVALID;
+  if (dim != 2 && dim != 3) return fail(ctx, SBDT_ERR_INVALID, "dim must be 2 or 3");
+  if (m == 0 || k == 0 || k >= 0xFFFE) return fail(ctx, SBDT_ERR_INVALID, "need m >= 1 and 1 <= k < 65534");
+  if (n > 0xFFFFFFFFull) return fail(ctx, SBDT_ERR_INVALID, "n exceeds the 32-bit PointId range");
+  unsigned long long* bbox = reinterpret_cast<unsigned long long*>(d_bbox_ordered_out);
+  if (!bbox) {
+    SBDT_WS(tmp, unsigned long long, "capi.bbox", 6);
+    bbox = tmp;
+  }
+  int rc = (dim == 2) ? assign_impl<2>(ctx, d_coords, n, d_sample_ids, d_sample_labels, m, d_labels_out, bbox)
+                      : assign_impl<3>(ctx, d_coords, n, d_sample_ids, d_sample_labels, m, d_labels_out, bbox);
+  if (rc != kOk) return rc;
+  if (d_part_offsets_out && d_part_ids_out)
+    return bucket_impl(ctx, d_labels_out, n, k, d_part_offsets_out, d_part_ids_out);
+  return kOk;
+}
+
+int sbdt_gpu_assign_points(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint64_t n,
+                           const uint32_t* sample_ids, const uint32_t* sample_labels, uint32_t m, uint32_t k,
+                           uint32_t* labels_out, uint64_t* part_offsets_out, uint32_t* part_ids_out,
+                           double* bbox_out) {
+  if (!ctx || !coords || !sample_ids || !sample_labels || !labels_out) return SBDT_ERR_INVALID;
+  cudaStream_t st = ctx->stream;
+  double* d_xyz;
+  uint32_t *d_sid, *d_slab, *d_lab, *d_pids = nullptr;
+  uint64_t *d_poff = nullptr, *d_bbox;
+  TRY(dalloc(ctx, "h.xyz", n * dim, &d_xyz));
+  TRY(dalloc(ctx, "h.sid", m, &d_sid));
+  TRY(dalloc(ctx, "h.slab", m, &d_slab));
+  TRY(dalloc(ctx, "h.lab", n, &d_lab));
+  TRY(dalloc(ctx, "h.bbox", 6, &d_bbox));
+  const bool parts = part_offsets_out && part_ids_out;
+  if (parts) {
+    TRY(dalloc(ctx, "h.poff", k + 1, &d_poff));
+    TRY(dalloc(ctx, "h.pids", n, &d_pids));
+  }
+  SBDT_CUDA_TRY(cudaMemcpyAsync(d_xyz, coords, sizeof(double) * n * dim, cudaMemcpyHostToDevice, st));
+  SBDT_CUDA_TRY(cudaMemcpyAsync(d_sid, sample_ids, sizeof(uint32_t) * m, cudaMemcpyHostToDevice, st));
+  SBDT_CUDA_TRY(cudaMemcpyAsync(d_slab, sample_labels, sizeof(uint32_t) * m, cudaMemcpyHostToDevice, st));
+  TRY(sbdt_gpu_assign_points_dev(ctx, dim, d_xyz, n, d_sid, d_slab, m, k, d_lab, d_poff, d_pids, d_bbox));
+  SBDT_CUDA_TRY(cudaMemcpyAsync(labels_out, d_lab, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, st));
+  if (parts) {
+    SBDT_CUDA_TRY(cudaMemcpyAsync(part_offsets_out, d_poff, sizeof(uint64_t) * (k + 1), cudaMemcpyDeviceToHost, st));
+    SBDT_CUDA_TRY(cudaMemcpyAsync(part_ids_out, d_pids, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, st));
+  }
+  unsigned long long hb[6] = {0, 0, 0, 0, 0, 0};
+  if (bbox_out) SBDT_CUDA_TRY(cudaMemcpyAsync(hb, d_bbox, sizeof(uint64_t) * 2 * dim, cudaMemcpyDeviceToHost, st));
+  TRY(finish(ctx));
+  if (bbox_out)
+    for (int i = 0; i < 2 * dim; ++i) bbox_out[i] = ordered_to_dbl(hb[i]);
+  return SBDT_OK;
+}
+
+int sbdt_gpu_find_border_dev(sbdt_gpu_ctx* ctx, const sbdt_border_args* a) {
+  if (!ctx || !a) return SBDT_ERR_INVALID;
+  if (a->dim != 2 && a->dim != 3) return fail(ctx, SBDT_ERR_INVALID, "dim must be 2 or 3");
+  if (a->k == 0 || a->k >= 0xFFFE) return fail(ctx, SBDT_ERR_INVALID, "need 1 <= k < 65534");
+  if (a->policy != SBDT_POLICY_BBOX && a->policy != SBDT_POLICY_GRID)
+    return fail(ctx, SBDT_ERR_INVALID, "policy not supported by this build (bbox, grid)");
+  if (!a->d_positive || !a->d_vertex_flags || !a->d_vertex_ids || !a->d_vertex_count)
+    return fail(ctx, SBDT_ERR_INVALID, "missing output buffers");
+  if (a->S > 0xFFFFFFFFull) return fail(ctx, SBDT_ERR_INVALID, "S exceeds the 32-bit SimplexId range");
+  int rc = (a->dim == 2) ? border_impl<2>(ctx, a) : border_impl<3>(ctx, a);
+  if (rc != kOk) return rc;
+  if ((a->flags & SBDT_BORDER_HULL_BFS) && a->d_border) return reach_impl(ctx, a);
+  return kOk;
+}
+
+int sbdt_gpu_find_border(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint64_t n, const uint32_t* labels,
+                         uint32_t k, const uint64_t* offsets, const uint32_t* verts, const uint32_t* nbrs,
+                         const int8_t* parity, int policy, double c_G, uint32_t flags, uint8_t* positive_out,
+                         uint8_t* border_out, uint32_t* vertex_ids_out, uint64_t* n_vertices_out,
+                         uint32_t* bfs_vertex_ids_out, uint64_t* n_bfs_vertices_out, double* spheres_out) {
+  if (!ctx || !coords || !labels || !offsets || !verts || !nbrs || !parity || !positive_out || !vertex_ids_out ||
+      !n_vertices_out)
+    return SBDT_ERR_INVALID;
+  if (dim != 2 && dim != 3) return fail(ctx, SBDT_ERR_INVALID, "dim must be 2 or 3");
+  const uint64_t S = offsets[k];
+  cudaStream_t st = ctx->stream;
+  sbdt_border_args a{};
+  a.dim = dim;
+  a.n = n;
+  a.k = k;
+  a.S = S;
+  a.policy = policy;
+  a.c_G = c_G;
+  a.flags = flags;
+  double* d_xyz;
+  uint32_t *d_lab, *d_verts, *d_nbrs, *d_vids, *d_bvids = nullptr;
+  uint64_t *d_off, *d_cnt, *d_bcnt = nullptr;
+  int8_t* d_par;
+  uint8_t *d_pos, *d_bor = nullptr, *d_vf, *d_bvf = nullptr;
+  double* d_sph = nullptr;
+  TRY(dalloc(ctx, "h.xyz", n * dim, &d_xyz));
+  TRY(dalloc(ctx, "h.lab", n, &d_lab));
+  TRY(dalloc(ctx, "h.off", k + 1, &d_off));
+  TRY(dalloc(ctx, "h.verts", S * (dim + 1), &d_verts));
+  TRY(dalloc(ctx, "h.nbrs", S * (dim + 1), &d_nbrs));
+  TRY(dalloc(ctx, "h.par", S, &d_par));
+  TRY(dalloc(ctx, "h.pos", S, &d_pos));
+  TRY(dalloc(ctx, "h.vf", n + 64, &d_vf));
+  TRY(dalloc(ctx, "h.vids", n, &d_vids));
+  TRY(dalloc(ctx, "h.cnt", 1, &d_cnt));
+  const bool bfs = (flags & SBDT_BORDER_HULL_BFS) && border_out;
+  if (bfs) {
+    TRY(dalloc(ctx, "h.bor", S, &d_bor));
+    TRY(dalloc(ctx, "h.bvf", n + 64, &d_bvf));
+    TRY(dalloc(ctx, "h.bvids", n, &d_bvids));
+    TRY(dalloc(ctx, "h.bcnt", 1, &d_bcnt));
+  }
+  if (spheres_out) TRY(dalloc(ctx, "h.sph", S * (dim + 1), &d_sph));
+  SBDT_CUDA_TRY(cudaMemcpyAsync(d_xyz, coords, sizeof(double) * n * dim, cudaMemcpyHostToDevice, st));
+  SBDT_CUDA_TRY(cudaMemcpyAsync(d_lab, labels, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, st));
+  SBDT_CUDA_TRY(cudaMemcpyAsync(d_off, offsets, sizeof(uint64_t) * (k + 1), cudaMemcpyHostToDevice, st));
+  SBDT_CUDA_TRY(cudaMemcpyAsync(d_verts, verts, sizeof(uint32_t) * S * (dim + 1), cudaMemcpyHostToDevice, st));
+  SBDT_CUDA_TRY(cudaMemcpyAsync(d_nbrs, nbrs, sizeof(uint32_t) * S * (dim + 1), cudaMemcpyHostToDevice, st));
+  SBDT_CUDA_TRY(cudaMemcpyAsync(d_par, parity, S, cudaMemcpyHostToDevice, st));
+  a.d_xyz = d_xyz;
+  a.d_labels = d_lab;
+  a.d_offsets = d_off;
+  a.d_verts = d_verts;
+  a.d_nbrs = d_nbrs;
+  a.d_parity = d_par;
+  a.d_positive = d_pos;
+  a.d_border = d_bor;
+  a.d_vertex_flags = d_vf;
+  a.d_vertex_ids = d_vids;
+  a.d_vertex_count = d_cnt;
+  a.d_bfs_vertex_flags = d_bvf;
+  a.d_bfs_vertex_ids = d_bvids;
+  a.d_bfs_vertex_count = d_bcnt;
+  a.d_spheres = d_sph;
+  TRY(sbdt_gpu_find_border_dev(ctx, &a));
+  uint64_t nv = 0, nb = 0;
+  SBDT_CUDA_TRY(cudaMemcpyAsync(positive_out, d_pos, S, cudaMemcpyDeviceToHost, st));
+  SBDT_CUDA_TRY(cudaMemcpyAsync(&nv, d_cnt, 8, cudaMemcpyDeviceToHost, st));
+  if (bfs) {
+    SBDT_CUDA_TRY(cudaMemcpyAsync(border_out, d_bor, S, cudaMemcpyDeviceToHost, st));
+    SBDT_CUDA_TRY(cudaMemcpyAsync(&nb, d_bcnt, 8, cudaMemcpyDeviceToHost, st));
+  }
+  if (spheres_out)
+    SBDT_CUDA_TRY(cudaMemcpyAsync(spheres_out, d_sph, sizeof(double) * S * (dim + 1), cudaMemcpyDeviceToHost, st));
+  TRY(finish(ctx));
+  SBDT_CUDA_TRY(cudaMemcpy(vertex_ids_out, d_vids, sizeof(uint32_t) * nv, cudaMemcpyDeviceToHost));
+  *n_vertices_out = nv;
+  if (bfs) {
+    if (bfs_vertex_ids_out) SBDT_CUDA_TRY(cudaMemcpy(bfs_vertex_ids_out, d_bvids, sizeof(uint32_t) * nb, cudaMemcpyDeviceToHost));
+    if (n_bfs_vertices_out) *n_bfs_vertices_out = nb;
+  }
+  return SBDT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,83 @@
+// Device context owned by the C ABI: stream, grow-only workspace, error word.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <string>
+
+#include "common.cuh"
+
+struct sbdt_gpu_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string last_error;
+  unsigned long long launches = 0;
+  struct Buf {
+    void* ptr = nullptr;
+    std::size_t bytes = 0;
+  };
+  std::map<std::string, Buf> bufs;
+  // device-side status word: bit0 degenerate simplex, bit1 grid cap exceeded,
+  // bit2 escalation overflow
+  unsigned* d_status = nullptr;
+  // last find_border statistics (read back by the host after a call)
+  unsigned long long stats[8] = {0};
+};
+
+namespace sbdt_gpu {
+
+enum Status : int {
+  kOk = 0,
+  kErrInvalid = 1,
+  kErrDegenerate = 2,
+  kErrCuda = 3,
+  kErrOom = 4,
+  kErrRange = 5,
+};
+
+enum DeviceStatusBits : unsigned {
+  kStDegenerate = 1u,
+  kStGridCap = 2u,
+  kStQueueOverflow = 4u,
+};
+
+inline int fail(sbdt_gpu_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->last_error = msg;
+  return code;
+}
+inline int fail_cuda(sbdt_gpu_ctx* ctx, cudaError_t e, const char* what) {
+  const int code = (e == cudaErrorMemoryAllocation) ? kErrOom : kErrCuda;
+  return fail(ctx, code, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Grow-only named workspace buffer (contents undefined on growth).
+inline void* workspace(sbdt_gpu_ctx* ctx, const char* name, std::size_t bytes, cudaError_t* err) {
+  auto& b = ctx->bufs[name];
+  if (b.bytes >= bytes && b.ptr) return b.ptr;
+  if (b.ptr) cudaFree(b.ptr);
+  b.ptr = nullptr;
+  b.bytes = 0;
+  std::size_t want = bytes + bytes / 8 + 256;
+  cudaError_t e = cudaMalloc(&b.ptr, want);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *err = e;
+    return nullptr;
+  }
+  b.bytes = want;
+  return b.ptr;
+}
+
+}  // namespace sbdt_gpu
+
+#define SBDT_WS(var, type, name, count)                                                         \
+  type* var = nullptr;                                                                          \
+  do {                                                                                          \
+    cudaError_t e_ = cudaSuccess;                                                               \
+    var = static_cast<type*>(::sbdt_gpu::workspace(ctx, name, sizeof(type) * (std::size_t)(count), &e_)); \
+    if (!var) return ::sbdt_gpu::fail_cuda(ctx, e_, "workspace " name);                        \
+  } while (0)

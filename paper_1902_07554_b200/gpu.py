@@ -1,0 +1,225 @@
+"""Python mirror of the reference's divide-step interface over the C ABI
+(include/sbdt_gpu.h -> libsbdt_gpu.so, sm_100a kernels).
+
+Names and argument meaning follow SPEC.md's operations:
+  assign_points(P, sample_ids, sample_labels, k) -> Partitioning
+  find_border(P, labels, partials, policy)        -> BorderSet
+  IntersectionPolicy(kind, c_G)
+Errors map like the reference's exceptions (common.hpp:22-65). There is no
+CPU fallback: a missing library or device raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_lib = None
+
+SBDT_OK, SBDT_ERR_INVALID, SBDT_ERR_DEGENERATE, SBDT_ERR_CUDA, SBDT_ERR_OOM, SBDT_ERR_RANGE = range(6)
+POLICY = {"bbox": 0, "grid": 1, "exact": 2}
+HULL_BFS = 1
+
+
+class DegenerateSimplex(RuntimeError):
+    """sbdt::DegenerateSimplex (common.hpp:22-25)."""
+
+
+class SbdtGpuError(RuntimeError):
+    pass
+
+
+class BorderArgs(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int), ("d_xyz", C.c_void_p), ("n", C.c_uint64), ("d_labels", C.c_void_p), ("k", C.c_uint32),
+        ("d_offsets", C.c_void_p), ("d_verts", C.c_void_p), ("d_nbrs", C.c_void_p), ("d_parity", C.c_void_p),
+        ("S", C.c_uint64), ("policy", C.c_int), ("c_G", C.c_double), ("flags", C.c_uint32),
+        ("d_bbox_ordered", C.c_void_p), ("d_positive", C.c_void_p), ("d_border", C.c_void_p),
+        ("d_vertex_flags", C.c_void_p), ("d_vertex_ids", C.c_void_p), ("d_vertex_count", C.c_void_p),
+        ("d_bfs_vertex_flags", C.c_void_p), ("d_bfs_vertex_ids", C.c_void_p), ("d_bfs_vertex_count", C.c_void_p),
+        ("d_spheres", C.c_void_p),
+    ]
+
+
+EXPORTS = [
+    "sbdt_gpu_create", "sbdt_gpu_destroy", "sbdt_gpu_last_error", "sbdt_gpu_set_stream", "sbdt_gpu_synchronize",
+    "sbdt_gpu_launch_count", "sbdt_gpu_check_status", "sbdt_gpu_assign_points", "sbdt_gpu_assign_points_dev",
+    "sbdt_gpu_find_border", "sbdt_gpu_find_border_dev",
+]
+
+
+def lib_path() -> str:
+    return os.path.join(_HERE, "libsbdt_gpu.so")
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        path = lib_path()
+        if not os.path.exists(path):
+            raise SbdtGpuError(f"{path} missing: the CUDA extension is not built (run __graft_entry__.build())")
+        L = C.CDLL(path)
+        vp, u64, u32, u32p, u64p, dp, i8p, u8p = (C.c_void_p, C.c_uint64, C.c_uint32, C.POINTER(C.c_uint32),
+                                                  C.POINTER(C.c_uint64), C.POINTER(C.c_double), C.POINTER(C.c_int8),
+                                                  C.POINTER(C.c_uint8))
+        L.sbdt_gpu_create.argtypes = [C.c_int, C.POINTER(vp)]
+        L.sbdt_gpu_destroy.argtypes = [vp]
+        L.sbdt_gpu_destroy.restype = None
+        L.sbdt_gpu_last_error.argtypes = [vp]
+        L.sbdt_gpu_last_error.restype = C.c_char_p
+        L.sbdt_gpu_set_stream.argtypes = [vp, vp]
+        L.sbdt_gpu_synchronize.argtypes = [vp]
+        L.sbdt_gpu_launch_count.argtypes = [vp]
+        L.sbdt_gpu_launch_count.restype = C.c_ulonglong
+        L.sbdt_gpu_check_status.argtypes = [vp]
+        L.sbdt_gpu_assign_points.argtypes = [vp, C.c_int, dp, u64, u32p, u32p, u32, u32, u32p, u64p, u32p, dp]
+        L.sbdt_gpu_assign_points_dev.argtypes = [vp, C.c_int, vp, u64, vp, vp, u32, u32, vp, vp, vp, vp]
+        L.sbdt_gpu_find_border.argtypes = [vp, C.c_int, dp, u64, u32p, u32, u64p, u32p, u32p, i8p, C.c_int, C.c_double,
+                                           u32, u8p, u8p, u32p, u64p, u32p, u64p, dp]
+        L.sbdt_gpu_find_border_dev.argtypes = [vp, C.POINTER(BorderArgs)]
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray, t):
+    return a.ctypes.data_as(C.POINTER(t))
+
+
+class Context:
+    """One device context (stream + workspace) per host thread."""
+
+    def __init__(self, device: int = 0):
+        self._h = C.c_void_p()
+        rc = lib().sbdt_gpu_create(device, C.byref(self._h))
+        if rc != SBDT_OK:
+            raise SbdtGpuError(f"sbdt_gpu_create(device={device}) failed with status {rc} (no CUDA device?)")
+
+    @property
+    def handle(self):
+        return self._h
+
+    def check(self, rc: int, what: str):
+        if rc == SBDT_OK:
+            return
+        msg = lib().sbdt_gpu_last_error(self._h).decode()
+        if rc == SBDT_ERR_DEGENERATE:
+            raise DegenerateSimplex(msg)
+        if rc == SBDT_ERR_INVALID:
+            raise ValueError(f"{what}: {msg}")
+        raise SbdtGpuError(f"{what}: status {rc}: {msg}")
+
+    def set_stream(self, stream_handle: int | None):
+        self.check(lib().sbdt_gpu_set_stream(self._h, C.c_void_p(stream_handle or 0)), "set_stream")
+
+    def synchronize(self):
+        self.check(lib().sbdt_gpu_synchronize(self._h), "synchronize")
+
+    @property
+    def launches(self) -> int:
+        return int(lib().sbdt_gpu_launch_count(self._h))
+
+    def close(self):
+        if self._h:
+            lib().sbdt_gpu_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx: Context | None = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+@dataclass
+class Partitioning:
+    """labels, parts (CSR: parts_offsets, parts_ids), sample ids/labels."""
+    labels: np.ndarray
+    parts_offsets: np.ndarray
+    parts_ids: np.ndarray
+    sample_point_ids: np.ndarray
+    sample_labels: np.ndarray
+    bbox: np.ndarray
+
+    def part(self, i: int) -> np.ndarray:
+        return self.parts_ids[self.parts_offsets[i]:self.parts_offsets[i + 1]]
+
+
+def assign_points(points: np.ndarray, sample_ids: np.ndarray, sample_labels: np.ndarray, k: int,
+                  ctx: Context | None = None) -> Partitioning:
+    """assign_points through the host-buffer C ABI entry point."""
+    ctx = ctx or default_context()
+    pts = np.ascontiguousarray(points, np.float64)
+    n, dim = pts.shape
+    sid = np.ascontiguousarray(sample_ids, np.uint32)
+    slab = np.ascontiguousarray(sample_labels, np.uint32)
+    labels = np.empty(n, np.uint32)
+    poff = np.empty(k + 1, np.uint64)
+    pids = np.empty(n, np.uint32)
+    bbox = np.empty(2 * dim, np.float64)
+    rc = lib().sbdt_gpu_assign_points(ctx.handle, dim, _p(pts, C.c_double), n, _p(sid, C.c_uint32),
+                                      _p(slab, C.c_uint32), len(sid), k, _p(labels, C.c_uint32),
+                                      _p(poff, C.c_uint64), _p(pids, C.c_uint32), _p(bbox, C.c_double))
+    ctx.check(rc, "assign_points")
+    return Partitioning(labels, poff, pids, sid, slab, bbox)
+
+
+@dataclass
+class IntersectionPolicy:
+    """kind in {bbox, grid, exact}, c_G > 0."""
+    kind: str = "grid"
+    c_G: float = 1.0
+
+
+@dataclass
+class BorderSet:
+    """SPEC.md:472-476 plus the north_star full-scan flags."""
+    positive: np.ndarray              # per simplex row: full-scan positive flag
+    border: np.ndarray | None         # per simplex row: SPEC BFS border flag
+    border_vertex_ids: np.ndarray     # vertices(border) (SPEC BorderSet), sorted
+    positive_vertex_ids: np.ndarray   # vertices(positive) (north_star), sorted
+    spheres: np.ndarray | None = None
+
+    def simplex_ids(self, partials, part: int, which: str = "border") -> np.ndarray:
+        flags = self.border if which == "border" else self.positive
+        lo, hi = int(partials.offsets[part]), int(partials.offsets[part + 1])
+        return np.nonzero(flags[lo:hi])[0].astype(np.uint32)
+
+
+def find_border(points: np.ndarray, labels: np.ndarray, partials, policy: IntersectionPolicy | None = None,
+                hull_bfs: bool = True, spheres: bool = False, ctx: Context | None = None) -> BorderSet:
+    """find_border through the host-buffer C ABI entry point."""
+    ctx = ctx or default_context()
+    policy = policy or IntersectionPolicy()
+    pts = np.ascontiguousarray(points, np.float64)
+    n, dim = pts.shape
+    lab = np.ascontiguousarray(labels, np.uint32)
+    S, k = partials.S, partials.k
+    pos = np.empty(S, np.uint8)
+    bor = np.empty(S, np.uint8) if hull_bfs else None
+    vids = np.empty(n, np.uint32)
+    bvids = np.empty(n, np.uint32) if hull_bfs else None
+    nv, nb = C.c_uint64(0), C.c_uint64(0)
+    sph = np.empty((S, dim + 1), np.float64) if spheres else None
+    rc = lib().sbdt_gpu_find_border(
+        ctx.handle, dim, _p(pts, C.c_double), n, _p(lab, C.c_uint32), k, _p(partials.offsets, C.c_uint64),
+        _p(partials.verts, C.c_uint32), _p(partials.nbrs, C.c_uint32), _p(partials.parity, C.c_int8),
+        POLICY[policy.kind], policy.c_G, HULL_BFS if hull_bfs else 0, _p(pos, C.c_uint8),
+        _p(bor, C.c_uint8) if hull_bfs else None, _p(vids, C.c_uint32), C.byref(nv),
+        _p(bvids, C.c_uint32) if hull_bfs else None, C.byref(nb) if hull_bfs else None,
+        _p(sph, C.c_double) if spheres else None)
+    ctx.check(rc, "find_border")
+    return BorderSet(pos, bor, bvids[:nb.value].copy() if hull_bfs else vids[:nv.value].copy(),
+                     vids[:nv.value].copy(), sph)
