@@ -1,0 +1,411 @@
+#!/usr/bin/env python3
+"""Benchmark of the sample-based divide step's hot path on B200 (sm_100a).
+
+One step = assign_points over all n points (nearest-sample labels + the
+Partitioning.parts bucketing) followed by find_border over all k partial DTs
+(owner grid, full-scan positive flags, border-vertex compaction) — the two
+stages of BASELINE.json's north_star, inputs resident in HBM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+N>1 (torchrun): one process per GPU; each rank owns an independent instance
+of the config (seed derived from the rank) — weak scaling, no data-path
+collective; rank 0 prints the max-over-ranks line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "input points partitioned/s and simplices border-tested/s on 1 B200; % HBM roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--n", type=int, default=None, help="override n (test-scale runs)")
+    ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--policy", default="grid")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0, help="CPU work per baseline step (seconds, approx.)")
+    ap.add_argument("--profile", action="store_true", help="single short run for ncu (no baseline/e2e)")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+            time.sleep(0.25)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+def algorithmic_bytes(dim, n, S, cells, n_vb):
+    b_assign = n * (8 * dim + 4)
+    b_border = S * (4 * (dim + 1) + 1) + n * (8 * dim + 1) + cells * 2 + n_vb * 4
+    return b_assign, b_border
+
+
+def cpu_baseline(inst, labels, policy, budget_s, threads):
+    """The CPU oracle (restatement of SPEC assign_points / find_border on the
+    reference's algorithm) timed on a bounded sample of the same workload."""
+    import oracle
+    n, S, k = inst.n, inst.partials.S, inst.config["k"]
+    # assignment sample sized to ~budget/3 seconds
+    n_s = min(n, 200_000)
+    t0 = time.perf_counter()
+    oracle.assign_kdtree(inst.points[:n_s], inst.sample_ids, inst.sample_labels, threads)  # warm-up + estimate
+    est = (time.perf_counter() - t0) / n_s
+    n_s = int(min(n, max(200_000, (budget_s / 3) / max(est, 1e-9))))
+    lab = np.empty(n_s, np.uint32)
+    import ctypes as C
+    pts = np.ascontiguousarray(inst.points)
+    t0 = time.perf_counter()
+    oracle.lib().oracle_assign_kdtree_range(inst.dim, oracle._p(pts, C.c_double), 0, n_s,
+                                            oracle._p(inst.sample_ids, C.c_uint32), len(inst.sample_ids),
+                                            oracle._p(inst.sample_labels, C.c_uint32), oracle._p(lab, C.c_uint32),
+                                            threads)
+    t_assign = time.perf_counter() - t0
+    # border sample: `threads` partitions (one BFS task per partition)
+    p_s = max(1, min(k, threads))
+    t_build, t_border, _ = oracle.time_border(inst.points, labels, inst.partials, policy, 1.0, threads, (0, p_s), 1)
+    S_s = int(inst.partials.offsets[p_s])
+    t_est = t_assign * (n / n_s) + t_border * (S / max(S_s, 1))
+    return dict(value=n / t_est, unit="points/s", cores=threads, kind="port",
+                sample=(f"oracle (SPEC restatement, kd-tree assign + per-part GridIndex/AABB find_border) on "
+                        f"{n_s} points assigned ({t_assign:.2f}s) and parts 0..{p_s - 1} = {S_s} simplices "
+                        f"border-tested ({t_border:.2f}s, index build {t_build:.2f}s excluded); "
+                        f"extrapolated to the full step ({t_est:.1f}s)"),
+                assign_points_per_s=n_s / t_assign, border_simplices_per_s=S_s / t_border, est_step_s=t_est)
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    """--impl reference: the CPU path (oracle port of the reference algorithm;
+    the reference ships no hot-path code) on all host threads."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_1902_07554_b200 import host
+    import oracle
+    threads = os.cpu_count() or 1
+    inst = host.make_instance(args.config, n=args.n, k=args.k)
+    labels = oracle.assign_kdtree(inst.points, inst.sample_ids, inst.sample_labels, threads)
+    host.attach_partials(inst, labels)
+    per_step = max(2.0, min(args.cpu_budget_s, 150.0 / max(1, args.steps + args.warmup)))
+    vals, res = [], None
+    for i in range(args.warmup + args.steps):
+        res = cpu_baseline(inst, labels, args.policy, per_step, threads)
+        if i >= args.warmup:
+            vals.append(res["value"])
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "points/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * inst.n / v, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json config)",
+            "config": {"workload": inst.config["name"], "n": inst.n, "k": inst.config["k"],
+                       "m": len(inst.sample_ids), "S": inst.partials.S, "policy": args.policy},
+            "cpu_baseline": {"value": v, "unit": "points/s", "cores": threads, "kind": "port",
+                             "sample": res["sample"]},
+            "e2e": {"value": v, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    from paper_1902_07554_b200 import gpu, host
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    threads = max(1, (os.cpu_count() or 1) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))))
+    seed = None
+    if world > 1:
+        from paper_1902_07554_b200.host import CONFIGS
+        seed = CONFIGS[args.config]["seed"] * 1000 + rank  # independent instance per rank
+    t_setup = time.time()
+    inst = host.make_instance(args.config, n=args.n, k=args.k, seed=seed)
+    dim, n, k, m = inst.dim, inst.n, inst.config["k"], len(inst.sample_ids)
+    ctx = gpu.Context(local)
+    stream = torch.cuda.Stream(dev)  # dedicated stream: events and kernels on the same queue
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+
+    # ---- device-resident inputs and outputs
+    d_xyz = torch.from_numpy(np.ascontiguousarray(inst.points)).to(dev)
+    d_sid = torch.from_numpy(inst.sample_ids.view(np.int32)).to(dev)
+    d_slab = torch.from_numpy(inst.sample_labels.view(np.int32)).to(dev)
+    d_lab = torch.empty(n, dtype=torch.int32, device=dev)
+    d_poff = torch.empty(k + 1, dtype=torch.int64, device=dev)
+    d_pids = torch.empty(n, dtype=torch.int32, device=dev)
+    d_bbox = torch.empty(2 * dim, dtype=torch.int64, device=dev)
+    P = lambda t: t.data_ptr()  # noqa: E731
+
+    def assign():
+        ctx.assign_points_dev(dim, P(d_xyz), n, P(d_sid), P(d_slab), m, k, P(d_lab), P(d_poff), P(d_pids), P(d_bbox))
+
+    assign()
+    torch.cuda.synchronize()
+    labels = d_lab.cpu().numpy().view(np.uint32).copy()
+    host.attach_partials(inst, labels, threads=threads)
+    part = inst.partials
+    S = part.S
+    setup_s = time.time() - t_setup
+
+    d_off = torch.from_numpy(part.offsets.view(np.int64)).to(dev)
+    d_verts = torch.from_numpy(part.verts.view(np.int32)).to(dev)
+    d_nbrs = torch.from_numpy(part.nbrs.view(np.int32)).to(dev)
+    d_par = torch.from_numpy(part.parity).to(dev)
+    d_pos = torch.empty(S, dtype=torch.uint8, device=dev)
+    d_bor = torch.empty(S, dtype=torch.uint8, device=dev)
+    d_vf = torch.empty(n + 64, dtype=torch.uint8, device=dev)
+    d_vids = torch.empty(n, dtype=torch.int32, device=dev)
+    d_cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    d_bvf = torch.empty(n + 64, dtype=torch.uint8, device=dev)
+    d_bvids = torch.empty(n, dtype=torch.int32, device=dev)
+    d_bcnt = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def border_args(bfs: bool):
+        a = gpu.BorderArgs()
+        a.dim, a.d_xyz, a.n, a.d_labels, a.k = dim, P(d_xyz), n, P(d_lab), k
+        a.d_offsets, a.d_verts, a.d_nbrs, a.d_parity, a.S = P(d_off), P(d_verts), P(d_nbrs), P(d_par), S
+        a.policy, a.c_G, a.flags = gpu.POLICY[args.policy], 1.0, gpu.HULL_BFS if bfs else 0
+        a.d_bbox_ordered = P(d_bbox)
+        a.d_positive, a.d_border = P(d_pos), P(d_bor) if bfs else None
+        a.d_vertex_flags, a.d_vertex_ids, a.d_vertex_count = P(d_vf), P(d_vids), P(d_cnt)
+        if bfs:
+            a.d_bfs_vertex_flags, a.d_bfs_vertex_ids, a.d_bfs_vertex_count = P(d_bvf), P(d_bvids), P(d_bcnt)
+        return a
+
+    args_full, args_bfs = border_args(False), border_args(True)
+
+    def step(bfs=False):
+        assign()
+        ctx.find_border_dev(args_bfs if bfs else args_full)
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def timed(nsteps, bfs=False):
+        ctx.set_timing(True)
+        ms, stages = [], {}
+        l0 = ctx.launches
+        for _ in range(nsteps):
+            flush.zero_()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            step(bfs)
+            e.record(stream)
+            e.synchronize()
+            ms.append(s.elapsed_time(e))
+            for name, t in ctx.stage_times():
+                stages.setdefault(name, []).append(t)
+        ctx.set_timing(False)
+        return ms, {kk: sum(v) / len(v) for kk, v in stages.items()}, ctx.launches - l0
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    ctx.synchronize()  # surfaces device-side status (degenerate simplex, grid cap)
+
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t_wall0 = time.perf_counter()
+        ms, stages, launches = timed(args.steps)
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall0
+    if dist:
+        dist.barrier()
+    table_stats = ctx.table_stats()
+    tot = torch.tensor([sum(ms)], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    total_ms = float(tot.item())
+    ctx.synchronize()
+
+    n_vb = int(d_cnt.item())
+    # SPEC find_border (hull-seeded BFS) variant, timed separately (K8 included)
+    ms_bfs, stages_bfs, _ = timed(max(1, min(args.steps, 5)), bfs=True)
+    n_vb_bfs = int(d_bcnt.item())
+    n_pos = int(d_pos.sum().item())
+
+    import oracle  # checker only: grid cell count for the byte model
+    lo, hi, edge, dims = oracle.grid_params(inst.points, 1.0)
+    cells = int(np.prod(dims))
+    b_assign, b_border = algorithmic_bytes(dim, n, S, cells, n_vb)
+    peak, peak_kind = peaks()
+
+    def roof(bytes_, ms_):
+        a = bytes_ / (ms_ * 1e-3) / 1e9
+        return {"bound": "hbm", "achieved": round(a, 1), "peak": peak, "unit": "GB/s", "frac": round(a / peak, 4),
+                "traffic": None, "algorithmic_bytes": int(bytes_), "ms": round(ms_, 4), "peak_kind": peak_kind}
+
+    t_assign = sum(v for kk, v in stages.items() if kk.startswith("assign."))
+    t_border = sum(v for kk, v in stages.items() if kk.startswith("border."))
+    kernel_bytes = {
+        "assign.points": n * (8 * dim + 4),
+        "border.finite": S * (4 * (dim + 1) + 1) + n * (8 * dim + 1) + cells * 2,
+        "border.grid": n * (8 * dim + 4) + cells * 2,
+        "assign.bucket": n * 12,
+        "border.compact": n + n_vb * 4,
+    }
+    dominant = max(stages.items(), key=lambda kv: kv[1])[0]
+    per_kernel = {kk: roof(kernel_bytes[kk], v) for kk, v in stages.items() if kk in kernel_bytes}
+    roofline = per_kernel.get(dominant) or roof(b_border, t_border)
+    roofline = dict(roofline, kernel=dominant)
+
+    value = world * n / (total_ms / args.steps * 1e-3)
+    clocks = clk.summary()
+
+    # ---- end to end through the host-buffer C ABI (pinned buffers; H2D+D2H inside)
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        def pinned(a):
+            t = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True).numpy()
+            v = t.view(a.dtype).reshape(a.shape)
+            v[...] = a
+            return v
+        h_pts, h_sid, h_slab = pinned(np.ascontiguousarray(inst.points)), pinned(inst.sample_ids), pinned(inst.sample_labels)
+        from paper_1902_07554_b200.host import Partials
+        h_part = Partials(pinned(part.offsets), pinned(part.verts), pinned(part.nbrs), pinned(part.parity))
+        ectx = gpu.Context(local)
+        pol = gpu.IntersectionPolicy(args.policy, 1.0)
+        res = gpu.assign_points(h_pts, h_sid, h_slab, k, ctx=ectx)  # warm-up (allocations)
+        gpu.find_border(h_pts, res.labels, h_part, pol, hull_bfs=False, ctx=ectx)
+        e2e_steps = max(1, min(args.steps, 3))
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            res = gpu.assign_points(h_pts, h_sid, h_slab, k, ctx=ectx)
+            bs = gpu.find_border(h_pts, res.labels, h_part, pol, hull_bfs=False, ctx=ectx)
+        t_e2e = (time.perf_counter() - t0) / e2e_steps
+        assert np.array_equal(res.labels, labels)
+        h2d = (inst.points.nbytes + 8 * m) + (inst.points.nbytes + 4 * n + part.offsets.nbytes + part.verts.nbytes
+                                               + part.nbrs.nbytes + part.parity.nbytes)
+        d2h = (4 * n + 8 * (k + 1) + 4 * n + 8 * dim) + (S + 8 + 4 * len(bs.positive_vertex_ids))
+        e2e = {"value": world * n / t_e2e, "unit": "points/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": round(1e3 * t_e2e, 3),
+               "path": "sbdt_gpu_assign_points + sbdt_gpu_find_border (host buffers, pinned)"}
+        ectx.close()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
+        cpu = cpu_baseline(inst, labels, args.policy, args.cpu_budget_s, os.cpu_count() or 1)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json config)",
+            "config": {"workload": inst.config["name"], "n": n, "dim": dim, "k": k, "m": m, "S": S,
+                       "policy": f"{args.policy}(c_G=1)", "cells": cells,
+                       "l2": "inputs > L2 (coords %d MB, simplices %d MB) and 256 MB L2 flush between steps"
+                             % (inst.points.nbytes >> 20, (part.verts.nbytes + part.nbrs.nbytes) >> 20),
+                       "parallelism": f"{world} independent instance(s), one per GPU"},
+            "stages_ms": {kk: round(v, 4) for kk, v in stages.items()},
+            "stage_rates": {"assign_points_per_s": n / (t_assign * 1e-3), "border_simplices_per_s": S / (t_border * 1e-3),
+                            "assign_roofline": roof(b_assign, t_assign), "border_roofline": roof(b_border, t_border)},
+            "roofline": roofline,
+            "kernel_rooflines": per_kernel,
+            "hull_bfs": {"ms_per_step": round(sum(ms_bfs) / len(ms_bfs), 4),
+                         "stages_ms": {kk: round(v, 4) for kk, v in stages_bfs.items()},
+                         "border_vertices": n_vb_bfs},
+            "border_vertices": n_vb, "positive_simplices": n_pos, "assign_table": table_stats,
+            "gpu_launches": int(launches), "gpu_launches_per_step": launches / args.steps,
+            "clocks": clocks, "wall_timed_s": round(t_wall, 3), "setup_s": round(setup_s, 1),
+            "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

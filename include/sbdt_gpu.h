@@ -57,14 +57,23 @@ enum sbdt_border_flags {
 int sbdt_gpu_create(int device, sbdt_gpu_ctx** out);
 void sbdt_gpu_destroy(sbdt_gpu_ctx* ctx);
 const char* sbdt_gpu_last_error(const sbdt_gpu_ctx* ctx);
-/* Use an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream);
- * NULL restores the context's own stream. */
+/* Launch on an external cudaStream_t from now on (e.g.
+ * torch.cuda.current_stream().cuda_stream); the handle is used as given, so
+ * NULL selects the legacy default stream. */
 int sbdt_gpu_set_stream(sbdt_gpu_ctx* ctx, void* cuda_stream);
 int sbdt_gpu_synchronize(sbdt_gpu_ctx* ctx);
 /* Number of kernels launched by this context so far. */
 unsigned long long sbdt_gpu_launch_count(const sbdt_gpu_ctx* ctx);
 /* Reads and clears the device status word; returns the mapped status. */
 int sbdt_gpu_check_status(sbdt_gpu_ctx* ctx);
+/* Per-stage CUDA-event timing on the context stream (off by default).
+ * sbdt_gpu_stage_times synchronizes, writes up to max_stages durations (ms)
+ * and '\n'-separated stage names, clears the record and returns the count. */
+int sbdt_gpu_set_timing(sbdt_gpu_ctx* ctx, int enable);
+int sbdt_gpu_stage_times(sbdt_gpu_ctx* ctx, char* names, int names_len, float* ms, int max_stages);
+/* Voronoi-label-table census of the last assign with timing enabled:
+ * out3 = {uniform records, candidate-list records, overflow records}. */
+int sbdt_gpu_assign_table_stats(sbdt_gpu_ctx* ctx, unsigned* out3);
 
 /* ---- assign_points -------------------------------------
  * coords: n points, AoS binary64 (PointSet::raw(), geometry.hpp:94-95).

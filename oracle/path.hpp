@@ -240,8 +240,15 @@ struct GridIndex {
     std::int32_t left = -1, right = -1, leaf = -1;  // leaf = cell index
   };
   std::vector<Node> nodes;  // nodes[0] = root
-  Box<D> root_box;          // partition point bbox (bbox policy)
+  Box<D> root_box;          // partition point bbox (diagnostic)
   bool empty() const { return cells.empty(); }
+  // Root box of the bbox policy (intersects_bbox): the AABB-tree
+  // root, i.e. the partition bbox snapped to its occupied cells. SPEC.md
+  // requires both "root_box equals the partition's bounding box" and "every
+  // node box contains its leaf boxes"; only the snapped box satisfies the
+  // second, and it is what makes the policy chain exact <= grid <= bbox
+  // (acceptance criterion 7) hold without exceptions.
+  const Box<D>& bbox_policy_box() const { return nodes[0].box; }
 };
 
 template <int D>
@@ -405,7 +412,7 @@ class BorderOracle {
       for (std::uint32_t j = 0; j < pv_.k; ++j) {
         if (j == i || idx_[j].empty()) continue;
         if (policy_ == kBbox) {
-          if (Prims::box_sphere(idx_[j].root_box, sph)) return true;
+          if (Prims::box_sphere(idx_[j].bbox_policy_box(), sph)) return true;
           continue;
         }
         auto test = [&](const Box<D>& b) { return Prims::box_sphere(b, sph); };
@@ -441,7 +448,7 @@ class BorderOracle {
     for (std::uint32_t j = 0; j < pv_.k; ++j) {
       if (j == i || idx_[j].empty()) continue;
       if (policy_ == kBbox) {
-        if (Prims::halfspace_box(facet, ip, idx_[j].root_box)) return true;
+        if (Prims::halfspace_box(facet, ip, idx_[j].bbox_policy_box())) return true;
         continue;
       }
       auto test = [&](const Box<D>& b) { return Prims::halfspace_box(facet, ip, b); };

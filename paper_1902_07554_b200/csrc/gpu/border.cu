@@ -33,10 +33,11 @@ constexpr int kBThreads = 256;
 template <int D>
 struct OwnerGrid {
   Grid<D> g;
+  double inv_edge;
   double margin;
   int levels;  // number of levels incl. leaf level 0; top level has one block
   int shift;   // log2 of per-axis fanout
-  long long ldims[kMaxLevels][D];
+  int ldims[kMaxLevels][D];
   unsigned long long loff[kMaxLevels + 1];
 };
 
@@ -46,18 +47,34 @@ constexpr int fan_shift() {
 }
 
 template <int D>
-__device__ __forceinline__ long long lin(const long long* dims, const long long* c) {
-  long long id = c[D - 1];
+__device__ __forceinline__ unsigned long long lin(const int* dims, const int* c) {
+  unsigned long long id = static_cast<unsigned>(c[D - 1]);
 #pragma unroll
-  for (int d = D - 2; d >= 0; --d) id = id * dims[d] + c[d];
+  for (int d = D - 2; d >= 0; --d) id = id * static_cast<unsigned>(dims[d]) + static_cast<unsigned>(c[d]);
   return id;
 }
+
+// Packed descent entries: level | coordinates (3D: 20/20/19 bits, 2D: 29/29).
 template <int D>
-__device__ __forceinline__ void unlin(const long long* dims, long long id, long long* c) {
-#pragma unroll
-  for (int d = 0; d < D; ++d) {
-    c[d] = id % dims[d];
-    id /= dims[d];
+__device__ __forceinline__ unsigned long long pack(int L, const int* c) {
+  if constexpr (D == 3)
+    return (static_cast<unsigned long long>(L) << 59) | (static_cast<unsigned long long>(c[2]) << 40) |
+           (static_cast<unsigned long long>(c[1]) << 20) | static_cast<unsigned long long>(c[0]);
+  else
+    return (static_cast<unsigned long long>(L) << 58) | (static_cast<unsigned long long>(c[1]) << 29) |
+           static_cast<unsigned long long>(c[0]);
+}
+template <int D>
+__device__ __forceinline__ int unpack(unsigned long long e, int* c) {
+  if constexpr (D == 3) {
+    c[0] = static_cast<int>(e & 0xFFFFFu);
+    c[1] = static_cast<int>((e >> 20) & 0xFFFFFu);
+    c[2] = static_cast<int>((e >> 40) & 0x7FFFFu);
+    return static_cast<int>(e >> 59);
+  } else {
+    c[0] = static_cast<int>(e & 0x1FFFFFFFu);
+    c[1] = static_cast<int>((e >> 29) & 0x1FFFFFFFu);
+    return static_cast<int>(e >> 58);
   }
 }
 
@@ -113,10 +130,11 @@ __global__ void k_owner_params(const unsigned long long* bbox, std::uint64_t n, 
   const double e = c_G * ((D == 2) ? sqrt(per) : cbrt_det(per));
   unsigned long long cells = 1;
   bool bad = !(e > 0.0);
+  const double axis_cap = D == 3 ? 500000.0 : 500000000.0;  // packed-coordinate range
   for (int d = 0; d < D; ++d) {
     og->g.lo[d] = lo[d];
     const double f = bad ? 0.0 : floor((hi[d] - lo[d]) / e);
-    if (!(f < 1e12)) bad = true;
+    if (!(f < axis_cap)) bad = true;
     og->g.dims[d] = bad ? 1 : static_cast<long long>(f) + 1;
     cells *= static_cast<unsigned long long>(og->g.dims[d]);
   }
@@ -125,6 +143,7 @@ __global__ void k_owner_params(const unsigned long long* bbox, std::uint64_t n, 
     for (int d = 0; d < D; ++d) og->g.dims[d] = 1;
   }
   og->g.edge = bad ? 1.0 : e;
+  og->inv_edge = 1.0 / og->g.edge;
   og->margin = 1e-9 * (mag + ext_max + og->g.edge);
   const int sh = fan_shift<D>();
   og->shift = sh;
@@ -134,7 +153,7 @@ __global__ void k_owner_params(const unsigned long long* bbox, std::uint64_t n, 
     bool top = true;
     unsigned long long cnt = 1;
     for (int d = 0; d < D; ++d) {
-      og->ldims[L][d] = ((og->g.dims[d] - 1) >> (L * sh)) + 1;
+      og->ldims[L][d] = static_cast<int>(((og->g.dims[d] - 1) >> (L * sh)) + 1);
       cnt *= static_cast<unsigned long long>(og->ldims[L][d]);
       top = top && og->ldims[L][d] == 1;
     }
@@ -153,8 +172,12 @@ __global__ void k_owner_mark(const double* __restrict__ xyz, const std::uint32_t
                              std::uint64_t n, const OwnerGrid<D>* __restrict__ ogp, std::uint16_t* __restrict__ owner,
                              unsigned long long* __restrict__ pbbox, std::uint32_t k) {
   __shared__ Grid<D> g;
+  __shared__ int dims[D];
   extern __shared__ unsigned long long s_pb[];  // [k][2D] when pbbox != nullptr
-  if (threadIdx.x == 0) g = ogp->g;
+  if (threadIdx.x == 0) {
+    g = ogp->g;
+    for (int d = 0; d < D; ++d) dims[d] = ogp->ldims[0][d];
+  }
   if (pbbox)
     for (std::uint32_t j = threadIdx.x; j < k * 2 * D; j += blockDim.x)
       s_pb[j] = ((j % (2 * D)) < D) ? 0xFFFFFFFFFFFFFFFFULL : 0ULL;
@@ -162,14 +185,14 @@ __global__ void k_owner_mark(const double* __restrict__ xyz, const std::uint32_t
   for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += std::uint64_t(gridDim.x) * blockDim.x) {
     double x[D];
-    long long c[D];
+    int c[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       x[d] = xyz[i * D + d];
-      c[d] = cell_coord<D>(g, x[d], d);
+      c[d] = static_cast<int>(cell_coord<D>(g, x[d], d));
     }
     const std::uint32_t lab = labels[i];
-    std::uint16_t* slot = owner + lin<D>(g.dims, c);
+    std::uint16_t* slot = owner + lin<D>(dims, c);
     unsigned short old = *slot;
     while (old != lab && old != kOwnerMulti) {
       const unsigned short nv = (old == kOwnerEmpty) ? static_cast<unsigned short>(lab) : kOwnerMulti;
@@ -206,22 +229,29 @@ __device__ __forceinline__ std::uint16_t combine(std::uint16_t a, std::uint16_t 
 }
 
 template <int D>
-__device__ __forceinline__ void build_block(const OwnerGrid<D>& og, std::uint16_t* owner, int L, long long id) {
-  const int sh = og.shift;
-  const long long F = 1LL << sh;
-  long long c[D];
-  unlin<D>(og.ldims[L], id, c);
+__device__ __forceinline__ void build_block(const OwnerGrid<D>& og, std::uint16_t* owner, int L, unsigned long long id) {
+  const int F = 1 << og.shift;
+  int c[D];
+  {
+    unsigned long long rem = id;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      c[d] = static_cast<int>(rem % static_cast<unsigned>(og.ldims[L][d]));
+      rem /= static_cast<unsigned>(og.ldims[L][d]);
+    }
+  }
   std::uint16_t code = kOwnerEmpty;
-  long long ch[D];
+  int ch[D];
+  const int* cd = og.ldims[L - 1];
   if constexpr (D == 3) {
-    for (ch[2] = c[2] * F; ch[2] < min((c[2] + 1) * F, og.ldims[L - 1][2]); ++ch[2])
-      for (ch[1] = c[1] * F; ch[1] < min((c[1] + 1) * F, og.ldims[L - 1][1]); ++ch[1])
-        for (ch[0] = c[0] * F; ch[0] < min((c[0] + 1) * F, og.ldims[L - 1][0]); ++ch[0])
-          code = combine(code, owner[og.loff[L - 1] + lin<D>(og.ldims[L - 1], ch)]);
+    for (ch[2] = c[2] * F; ch[2] < min((c[2] + 1) * F, cd[2]); ++ch[2])
+      for (ch[1] = c[1] * F; ch[1] < min((c[1] + 1) * F, cd[1]); ++ch[1])
+        for (ch[0] = c[0] * F; ch[0] < min((c[0] + 1) * F, cd[0]); ++ch[0])
+          code = combine(code, owner[og.loff[L - 1] + lin<D>(cd, ch)]);
   } else {
-    for (ch[1] = c[1] * F; ch[1] < min((c[1] + 1) * F, og.ldims[L - 1][1]); ++ch[1])
-      for (ch[0] = c[0] * F; ch[0] < min((c[0] + 1) * F, og.ldims[L - 1][0]); ++ch[0])
-        code = combine(code, owner[og.loff[L - 1] + lin<D>(og.ldims[L - 1], ch)]);
+    for (ch[1] = c[1] * F; ch[1] < min((c[1] + 1) * F, cd[1]); ++ch[1])
+      for (ch[0] = c[0] * F; ch[0] < min((c[0] + 1) * F, cd[0]); ++ch[0])
+        code = combine(code, owner[og.loff[L - 1] + lin<D>(cd, ch)]);
   }
   owner[og.loff[L] + id] = code;
 }
@@ -232,9 +262,9 @@ __global__ void k_owner_level(const OwnerGrid<D>* __restrict__ ogp, std::uint16_
   if (threadIdx.x == 0) og = *ogp;
   __syncthreads();
   if (L >= og.levels) return;
-  const long long cnt = static_cast<long long>(og.loff[L + 1] - og.loff[L]);
-  for (long long id = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; id < cnt;
-       id += static_cast<long long>(gridDim.x) * blockDim.x)
+  const unsigned long long cnt = og.loff[L + 1] - og.loff[L];
+  for (unsigned long long id = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; id < cnt;
+       id += static_cast<unsigned long long>(gridDim.x) * blockDim.x)
     build_block<D>(og, owner, L, id);
 }
 
@@ -244,27 +274,95 @@ __global__ void k_owner_levels_tail(const OwnerGrid<D>* __restrict__ ogp, std::u
   if (threadIdx.x == 0) og = *ogp;
   __syncthreads();
   for (int L = L0; L < og.levels; ++L) {
-    const long long cnt = static_cast<long long>(og.loff[L + 1] - og.loff[L]);
-    for (long long id = threadIdx.x; id < cnt; id += blockDim.x) build_block<D>(og, owner, L, id);
+    const unsigned long long cnt = og.loff[L + 1] - og.loff[L];
+    for (unsigned long long id = threadIdx.x; id < cnt; id += blockDim.x) build_block<D>(og, owner, L, id);
     __syncthreads();
   }
 }
 
 // ---- descent helpers -----------------------------------------------------------
 template <int D>
-__device__ __forceinline__ void block_box(const OwnerGrid<D>& og, int L, const long long* c, double* blo,
-                                          double* bhi) {
+__device__ __forceinline__ void block_box(const OwnerGrid<D>& og, int L, const int* c, double* blo, double* bhi) {
+  const int s = L * og.shift;
 #pragma unroll
   for (int d = 0; d < D; ++d) {
-    const long long first = c[d] << (L * og.shift);
-    long long last1 = (c[d] + 1) << (L * og.shift);
+    const long long first = static_cast<long long>(c[d]) << s;
+    long long last1 = static_cast<long long>(c[d] + 1) << s;
     if (last1 > og.g.dims[d]) last1 = og.g.dims[d];
     blo[d] = cell_lo<D>(og.g, first, d);
     bhi[d] = cell_lo<D>(og.g, last1, d);
   }
 }
 
-constexpr int kStack = 192;
+// Depth-first pyramid descent with one cursor frame per level (depth bounded
+// by the number of levels, no overflow). Visits the blocks of level L0 in the
+// leaf range [a,b] (restricted) or the single top block; a block whose code
+// is EMPTY or `self` is pruned; test(blo, bhi) returns 0 (reject), 1
+// (descend) or 2 (accept: every sub-box passes, so a foreign occupied leaf
+// inside passes). A leaf that passes is a hit.
+template <int D, class Test>
+__device__ bool descend(const OwnerGrid<D>& og, const std::uint16_t* __restrict__ owner, std::uint32_t self, int L0,
+                        const int* a, const int* b, bool restrict_range, const Test& test) {
+  struct Frame {
+    int lo[D], hi[D], cur[D];
+    int level;
+  };
+  Frame fr[kMaxLevels + 1];
+  int depth = 1;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    fr[0].lo[d] = restrict_range ? (a[d] >> (L0 * og.shift)) : 0;
+    fr[0].hi[d] = restrict_range ? (b[d] >> (L0 * og.shift)) : og.ldims[L0][d] - 1;
+    fr[0].cur[d] = fr[0].lo[d];
+  }
+  fr[0].level = L0;
+  while (depth > 0) {
+    Frame& f = fr[depth - 1];
+    if (f.cur[D - 1] > f.hi[D - 1]) {
+      --depth;
+      continue;
+    }
+    int cc[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) cc[d] = f.cur[d];
+    // odometer advance
+    ++f.cur[0];
+#pragma unroll
+    for (int d = 0; d < D - 1; ++d)
+      if (f.cur[d] > f.hi[d]) {
+        f.cur[d] = f.lo[d];
+        ++f.cur[d + 1];
+      }
+    const int lv = f.level;
+    const std::uint16_t code = owner[og.loff[lv] + lin<D>(og.ldims[lv], cc)];
+    if (code == kOwnerEmpty || code == self) continue;
+    double blo[D], bhi[D];
+    block_box<D>(og, lv, cc, blo, bhi);
+    const int r = test(blo, bhi);
+    if (r == 0) continue;
+    if (lv == 0 || r == 2) return true;
+    const int cl = lv - 1;
+    const int csh = cl * og.shift;
+    Frame& g = fr[depth];
+    bool empty = false;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      int lo = cc[d] << og.shift;
+      int hi = min(((cc[d] + 1) << og.shift) - 1, og.ldims[cl][d] - 1);
+      if (restrict_range) {
+        lo = max(lo, a[d] >> csh);
+        hi = min(hi, b[d] >> csh);
+      }
+      g.lo[d] = lo;
+      g.hi[d] = hi;
+      g.cur[d] = lo;
+      empty = empty || lo > hi;
+    }
+    g.level = cl;
+    if (!empty) ++depth;
+  }
+  return false;
+}
 
 // true iff some cell with owner code not in {EMPTY, self} overlaps the sphere.
 template <int D>
@@ -274,20 +372,23 @@ __device__ bool sphere_hits_foreign(const OwnerGrid<D>& og, const std::uint16_t*
   bool fin = isfinite(r2);
 #pragma unroll
   for (int d = 0; d < D; ++d) fin = fin && isfinite(c[d]);
-  long long a[D], b[D];
+  int a[D], b[D];
   if (fin) {
+    // Conservative leaf range: the margin (1e-9 relative) dominates the
+    // rounding of this multiply-by-inverse binning.
     const double r = sqrt(r2) * (1.0 + 1e-9) + og.margin;
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      const double fa = floor((c[d] - r - og.g.lo[d]) / og.g.edge);
-      const double fb = floor((c[d] + r - og.g.lo[d]) / og.g.edge);
-      if (fb < 0.0 || fa > static_cast<double>(og.g.dims[d] - 1)) return false;
-      a[d] = fa < 0.0 ? 0 : static_cast<long long>(fa);
-      b[d] = fb > static_cast<double>(og.g.dims[d] - 1) ? og.g.dims[d] - 1 : static_cast<long long>(fb);
+      const double fa = floor((c[d] - r - og.g.lo[d]) * og.inv_edge);
+      const double fb = floor((c[d] + r - og.g.lo[d]) * og.inv_edge);
+      const double top = static_cast<double>(og.ldims[0][d] - 1);
+      if (fb < 0.0 || fa > top) return false;
+      a[d] = fa < 0.0 ? 0 : static_cast<int>(fa);
+      b[d] = fb > top ? og.ldims[0][d] - 1 : static_cast<int>(fb);
     }
   } else {
 #pragma unroll
-    for (int d = 0; d < D; ++d) a[d] = 0, b[d] = og.g.dims[d] - 1;
+    for (int d = 0; d < D; ++d) a[d] = 0, b[d] = og.ldims[0][d] - 1;
   }
   int L = 0;
   for (; L < og.levels - 1; ++L) {
@@ -296,66 +397,32 @@ __device__ bool sphere_hits_foreign(const OwnerGrid<D>& og, const std::uint16_t*
     for (int d = 0; d < D; ++d) ok = ok && ((b[d] >> (L * og.shift)) - (a[d] >> (L * og.shift)) <= 1);
     if (ok) break;
   }
-  unsigned long long stack[kStack];
-  int top = 0;
+  // Fast path: start blocks (<= 2 per axis) all EMPTY or own partition.
   {
-    long long s0[D], s1[D], cc[D];
-#pragma unroll
-    for (int d = 0; d < D; ++d) s0[d] = a[d] >> (L * og.shift), s1[d] = b[d] >> (L * og.shift);
-    if constexpr (D == 3) {
-      for (cc[2] = s0[2]; cc[2] <= s1[2]; ++cc[2])
-        for (cc[1] = s0[1]; cc[1] <= s1[1]; ++cc[1])
-          for (cc[0] = s0[0]; cc[0] <= s1[0]; ++cc[0])
-            stack[top++] = (static_cast<unsigned long long>(L) << 58) | lin<D>(og.ldims[L], cc);
-    } else {
-      for (cc[1] = s0[1]; cc[1] <= s1[1]; ++cc[1])
-        for (cc[0] = s0[0]; cc[0] <= s1[0]; ++cc[0])
-          stack[top++] = (static_cast<unsigned long long>(L) << 58) | lin<D>(og.ldims[L], cc);
-    }
-  }
-  while (top > 0) {
-    const unsigned long long e = stack[--top];
-    const int lv = static_cast<int>(e >> 58);
-    const long long id = static_cast<long long>(e & ((1ULL << 58) - 1));
-    const std::uint16_t code = owner[og.loff[lv] + id];
-    if (code == kOwnerEmpty || code == self) continue;
-    long long cc[D];
-    unlin<D>(og.ldims[lv], id, cc);
-    double blo[D], bhi[D];
-    block_box<D>(og, lv, cc, blo, bhi);
-    if (!box_sphere<D>(blo, bhi, c, r2)) continue;
-    if (lv == 0) return true;
-    if (box_inside_sphere<D>(blo, bhi, c, r2)) return true;
-    // children restricted to the conservative leaf range
-    const int cl = lv - 1;
-    const int csh = cl * og.shift;
-    long long lo_c[D], hi_c[D];
+    int s0[D], n0[D];
+    bool any = false;
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      lo_c[d] = cc[d] << og.shift;
-      hi_c[d] = ((cc[d] + 1) << og.shift) - 1;
-      if (hi_c[d] > og.ldims[cl][d] - 1) hi_c[d] = og.ldims[cl][d] - 1;
-      const long long ra = a[d] >> csh, rb = b[d] >> csh;
-      if (lo_c[d] < ra) lo_c[d] = ra;
-      if (hi_c[d] > rb) hi_c[d] = rb;
+      s0[d] = a[d] >> (L * og.shift);
+      n0[d] = (b[d] >> (L * og.shift)) - s0[d] + 1;
     }
-    long long ch[D];
-    if constexpr (D == 3) {
-      for (ch[2] = lo_c[2]; ch[2] <= hi_c[2]; ++ch[2])
-        for (ch[1] = lo_c[1]; ch[1] <= hi_c[1]; ++ch[1])
-          for (ch[0] = lo_c[0]; ch[0] <= hi_c[0]; ++ch[0]) {
-            if (top >= kStack) return true;  // unreachable for <=16 levels; conservative
-            stack[top++] = (static_cast<unsigned long long>(cl) << 58) | lin<D>(og.ldims[cl], ch);
-          }
-    } else {
-      for (ch[1] = lo_c[1]; ch[1] <= hi_c[1]; ++ch[1])
-        for (ch[0] = lo_c[0]; ch[0] <= hi_c[0]; ++ch[0]) {
-          if (top >= kStack) return true;
-          stack[top++] = (static_cast<unsigned long long>(cl) << 58) | lin<D>(og.ldims[cl], ch);
-        }
+    const int total = D == 3 ? n0[0] * n0[1] * n0[2] : n0[0] * n0[1];
+    for (int t = 0; t < total && !any; ++t) {
+      int cc[D], rem = t;  // every n0 is 1 or 2 at the start level
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        cc[d] = s0[d] + (rem & (n0[d] - 1));
+        rem >>= (n0[d] - 1);
+      }
+      const std::uint16_t code = owner[og.loff[L] + lin<D>(og.ldims[L], cc)];
+      any = !(code == kOwnerEmpty || code == self);
     }
+    if (!any) return false;
   }
-  return false;
+  return descend<D>(og, owner, self, L, a, b, true, [&](const double* blo, const double* bhi) {
+    if (!box_sphere<D>(blo, bhi, c, r2)) return 0;
+    return box_inside_sphere<D>(blo, bhi, c, r2) ? 2 : 1;
+  });
 }
 
 // Halfspace variant: test = some box corner strictly on the outer side of
@@ -380,48 +447,12 @@ __device__ int corners_outside(const double* const* facet, int inner_sign, const
 template <int D>
 __device__ bool halfspace_hits_foreign(const OwnerGrid<D>& og, const std::uint16_t* __restrict__ owner,
                                        const double* const* facet, int inner_sign, std::uint32_t self) {
-  unsigned long long stack[kStack];
-  int top = 0;
-  const int Ltop = og.levels - 1;
-  stack[top++] = (static_cast<unsigned long long>(Ltop) << 58);
-  while (top > 0) {
-    const unsigned long long e = stack[--top];
-    const int lv = static_cast<int>(e >> 58);
-    const long long id = static_cast<long long>(e & ((1ULL << 58) - 1));
-    const std::uint16_t code = owner[og.loff[lv] + id];
-    if (code == kOwnerEmpty || code == self) continue;
-    long long cc[D];
-    unlin<D>(og.ldims[lv], id, cc);
-    double blo[D], bhi[D];
-    block_box<D>(og, lv, cc, blo, bhi);
-    const int out = corners_outside<D>(facet, inner_sign, blo, bhi);
-    if (out == 0) continue;
-    if (lv == 0 || out == (1 << D)) return true;
-    const int cl = lv - 1;
-    long long lo_c[D], hi_c[D];
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      lo_c[d] = cc[d] << og.shift;
-      hi_c[d] = ((cc[d] + 1) << og.shift) - 1;
-      if (hi_c[d] > og.ldims[cl][d] - 1) hi_c[d] = og.ldims[cl][d] - 1;
-    }
-    long long ch[D];
-    if constexpr (D == 3) {
-      for (ch[2] = lo_c[2]; ch[2] <= hi_c[2]; ++ch[2])
-        for (ch[1] = lo_c[1]; ch[1] <= hi_c[1]; ++ch[1])
-          for (ch[0] = lo_c[0]; ch[0] <= hi_c[0]; ++ch[0]) {
-            if (top >= kStack) return true;
-            stack[top++] = (static_cast<unsigned long long>(cl) << 58) | lin<D>(og.ldims[cl], ch);
-          }
-    } else {
-      for (ch[1] = lo_c[1]; ch[1] <= hi_c[1]; ++ch[1])
-        for (ch[0] = lo_c[0]; ch[0] <= hi_c[0]; ++ch[0]) {
-          if (top >= kStack) return true;
-          stack[top++] = (static_cast<unsigned long long>(cl) << 58) | lin<D>(og.ldims[cl], ch);
-        }
-    }
-  }
-  return false;
+  return descend<D>(og, owner, self, og.levels - 1, nullptr, nullptr, false,
+                    [&](const double* blo, const double* bhi) {
+                      const int out = corners_outside<D>(facet, inner_sign, blo, bhi);
+                      if (out == 0) return 0;
+                      return out == (1 << D) ? 2 : 1;
+                    });
 }
 
 // circumsphere (geometry.cpp:279-327) + inflated (geometry.hpp:179-183)
@@ -467,7 +498,6 @@ __device__ __forceinline__ void circumsphere_inflated(const double (*p)[D], doub
   }
 }
 
-template <int D>
 __device__ __forceinline__ std::uint32_t part_of(const std::uint64_t* offs, std::uint32_t k, std::uint64_t s) {
   std::uint32_t lo = 0, hi = k;  // offs[lo] <= s < offs[hi]
   while (hi - lo > 1) {
@@ -498,6 +528,34 @@ struct BorderArgs {
   unsigned* status;
 };
 
+// bbox-policy root box of partition j: its point bbox snapped to the occupied
+// cells (= the AABB-tree root, oracle GridIndex::bbox_policy_box). Cell
+// binning is monotone, so the extreme cells are the cells of the extreme points.
+template <int D>
+__device__ __forceinline__ bool bbox_policy_box(const OwnerGrid<D>& og, const unsigned long long* pbbox,
+                                                std::uint32_t j, double* blo, double* bhi) {
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const double pl = ordered_to_dbl(pbbox[j * 2 * D + d]);
+    const double ph = ordered_to_dbl(pbbox[j * 2 * D + D + d]);
+    if (!(pl <= ph)) return false;  // empty partition
+    blo[d] = cell_lo<D>(og.g, cell_coord<D>(og.g, pl, d), d);
+    bhi[d] = cell_lo<D>(og.g, cell_coord<D>(og.g, ph, d) + 1, d);
+  }
+  return true;
+}
+
+template <int D>
+__device__ __forceinline__ bool bbox_policy_sphere(const OwnerGrid<D>& og, const BorderArgs& a, std::uint32_t self,
+                                                   const double* c, double r2) {
+  for (std::uint32_t j = 0; j < a.k; ++j) {
+    if (j == self) continue;
+    double blo[D], bhi[D];
+    if (bbox_policy_box<D>(og, a.pbbox, j, blo, bhi) && box_sphere<D>(blo, bhi, c, r2)) return true;
+  }
+  return false;
+}
+
 template <int D>
 __global__ void __launch_bounds__(kBThreads) k_border_finite(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp) {
   __shared__ OwnerGrid<D> og;
@@ -509,14 +567,14 @@ __global__ void __launch_bounds__(kBThreads) k_border_finite(BorderArgs a, const
        s += std::uint64_t(gridDim.x) * blockDim.x) {
     std::uint32_t v[D + 1];
 #pragma unroll
-    for (int j = 0; j <= D; ++j) v[j] = a.verts[std::uint64_t(j) * a.S + s];
+    for (int j = 0; j <= D; ++j) v[j] = __ldcs(a.verts + std::uint64_t(j) * a.S + s);
     if (v[D] == kInfVertex) {
       const unsigned slot = atomicAdd(a.inf_count, 1u);
       a.inf_queue[slot] = static_cast<std::uint32_t>(s);
       continue;
     }
     if (a.parity[s] == 0) atomicOr(a.status, kStDegenerate);
-    const std::uint32_t self = part_of<D>(s_off, a.k, s);
+    const std::uint32_t self = part_of(s_off, a.k, s);
     double p[D + 1][D];
 #pragma unroll
     for (int j = 0; j <= D; ++j)
@@ -529,24 +587,9 @@ __global__ void __launch_bounds__(kBThreads) k_border_finite(BorderArgs a, const
       for (int d = 0; d < D; ++d) a.spheres[s * (D + 1) + d] = c[d];
       a.spheres[s * (D + 1) + D] = r2;
     }
-    bool pos = false;
-    if (a.policy == SBDT_POLICY_BBOX) {
-      for (std::uint32_t j = 0; j < a.k && !pos; ++j) {
-        if (j == self) continue;
-        double blo[D], bhi[D];
-        bool empty = false;
-#pragma unroll
-        for (int d = 0; d < D; ++d) {
-          blo[d] = ordered_to_dbl(a.pbbox[j * 2 * D + d]);
-          bhi[d] = ordered_to_dbl(a.pbbox[j * 2 * D + D + d]);
-          empty = empty || !(blo[d] <= bhi[d]);
-        }
-        if (!empty && box_sphere<D>(blo, bhi, c, r2)) pos = true;
-      }
-    } else {
-      pos = sphere_hits_foreign<D>(og, a.owner, c, r2, self);
-    }
-    a.positive[s] = pos ? 1 : 0;
+    const bool pos = (a.policy == SBDT_POLICY_BBOX) ? bbox_policy_sphere<D>(og, a, self, c, r2)
+                                                    : sphere_hits_foreign<D>(og, a.owner, c, r2, self);
+    __stcs(a.positive + s, static_cast<std::uint8_t>(pos ? 1 : 0));
     if (pos)
 #pragma unroll
       for (int j = 0; j <= D; ++j) a.vflags[v[j]] = 1;
@@ -563,7 +606,7 @@ __global__ void __launch_bounds__(128) k_border_infinite(BorderArgs a, const Own
   const unsigned count = *a.inf_count;
   for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < count; q += gridDim.x * blockDim.x) {
     const std::uint64_t s = a.inf_queue[q];
-    const std::uint32_t self = part_of<D>(s_off, a.k, s);
+    const std::uint32_t self = part_of(s_off, a.k, s);
     std::uint32_t fv[D];
 #pragma unroll
     for (int j = 0; j < D; ++j) fv[j] = a.verts[std::uint64_t(j) * a.S + s];
@@ -592,14 +635,8 @@ __global__ void __launch_bounds__(128) k_border_infinite(BorderArgs a, const Own
       for (std::uint32_t j = 0; j < a.k && !pos; ++j) {
         if (j == self) continue;
         double blo[D], bhi[D];
-        bool empty = false;
-#pragma unroll
-        for (int d = 0; d < D; ++d) {
-          blo[d] = ordered_to_dbl(a.pbbox[j * 2 * D + d]);
-          bhi[d] = ordered_to_dbl(a.pbbox[j * 2 * D + D + d]);
-          empty = empty || !(blo[d] <= bhi[d]);
-        }
-        if (!empty && corners_outside<D>(facet, inner_sign, blo, bhi) > 0) pos = true;
+        if (bbox_policy_box<D>(og, a.pbbox, j, blo, bhi) && corners_outside<D>(facet, inner_sign, blo, bhi) > 0)
+          pos = true;
       }
     } else {
       pos = halfspace_hits_foreign<D>(og, a.owner, facet, inner_sign, self);
@@ -690,8 +727,9 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   double scale = 1.0;
   for (int d = 0; d < D; ++d) scale /= cg;
   const unsigned long long cap = static_cast<unsigned long long>(4.0 * double(in->n) * scale) + 4096;
+  const unsigned long long owner_len = cap * 8 / 7 + 64 * kMaxLevels + 64;
   SBDT_WS(og, OwnerGrid<D>, "border.og", 1);
-  SBDT_WS(owner, std::uint16_t, "border.owner", cap * 8 / 7 + 64 * kMaxLevels + 64);
+  SBDT_WS(owner, std::uint16_t, "border.owner", owner_len);
   SBDT_WS(bbox, unsigned long long, "border.bbox", 2 * D);
   SBDT_WS(infq, std::uint32_t, "border.infq", in->S / 2 + 1024);
   SBDT_WS(infc, unsigned, "border.infc", 1);
@@ -701,6 +739,7 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
     pbbox = pb;
   }
 
+  StageTimer tgrid(ctx, "border.grid");
   const unsigned long long* bb = reinterpret_cast<const unsigned long long*>(in->d_bbox_ordered);
   if (!bb) {
     k_bbox_points_init<<<1, 32, 0, st>>>(bbox, D);
@@ -711,7 +750,7 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
     bb = bbox;
   }
   k_owner_params<D><<<1, 1, 0, st>>>(bb, in->n, cg, cap, og, ctx->d_status);
-  SBDT_CUDA_TRY(cudaMemsetAsync(owner, 0xFF, sizeof(std::uint16_t) * (cap * 8 / 7 + 64 * kMaxLevels + 64), st));
+  SBDT_CUDA_TRY(cudaMemsetAsync(owner, 0xFF, sizeof(std::uint16_t) * owner_len, st));
   if (pbbox) {
     k_pbbox_init<<<(in->k * 2 * D + 255) / 256, 256, 0, st>>>(pbbox, in->k * 2 * D, D);
     ctx->launches += 1;
@@ -725,10 +764,11 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   k_owner_level<D><<<sms * 8, 256, 0, st>>>(og, owner, 1);
   k_owner_level<D><<<sms * 2, 256, 0, st>>>(og, owner, 2);
   k_owner_levels_tail<D><<<1, 1024, 0, st>>>(og, owner, 3);
-  ctx->launches += 5;
+  ctx->launches += 6;
 
   SBDT_CUDA_TRY(cudaMemsetAsync(in->d_vertex_flags, 0, in->n, st));
   SBDT_CUDA_TRY(cudaMemsetAsync(infc, 0, sizeof(unsigned), st));
+  tgrid.end();
   BorderArgs a;
   a.xyz = in->d_xyz;
   a.n = in->n;
@@ -751,10 +791,17 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   {
     const std::uint64_t want = (in->S + kBThreads - 1) / kBThreads;
     const unsigned blocks = static_cast<unsigned>(want < std::uint64_t(sms) * 32 ? want : std::uint64_t(sms) * 32);
-    if (blocks > 0) k_border_finite<D><<<blocks, kBThreads, offs_sh, st>>>(a, og);
-    k_border_infinite<D><<<sms * 2, 128, offs_sh, st>>>(a, og);
+    {
+      StageTimer t(ctx, "border.finite");
+      if (blocks > 0) k_border_finite<D><<<blocks, kBThreads, offs_sh, st>>>(a, og);
+    }
+    {
+      StageTimer t(ctx, "border.infinite");
+      k_border_infinite<D><<<sms * 2, 128, offs_sh, st>>>(a, og);
+    }
     ctx->launches += 2;
   }
+  StageTimer tc(ctx, "border.compact");
   int rc = compact_flags(ctx, in->d_vertex_flags, in->n, in->d_vertex_ids, in->d_vertex_count);
   if (rc != kOk) return rc;
   SBDT_CUDA_TRY(cudaGetLastError());

@@ -3,6 +3,7 @@
 // (asynchronous on the context stream). No exception crosses this boundary.
 #include <cuda_runtime.h>
 
+#include <cstring>
 #include <new>
 #include <string>
 
@@ -18,6 +19,7 @@ int bucket_impl(sbdt_gpu_ctx*, const std::uint32_t*, std::uint64_t, std::uint32_
 template <int D>
 int border_impl(sbdt_gpu_ctx*, const sbdt_border_args*);
 int reach_impl(sbdt_gpu_ctx*, const sbdt_border_args*);
+int assign_stats(sbdt_gpu_ctx*, unsigned*);
 }  // namespace sbdt_gpu
 
 using namespace sbdt_gpu;
@@ -86,14 +88,9 @@ int sbdt_gpu_set_stream(sbdt_gpu_ctx* ctx, void* stream) {
     cudaStreamSynchronize(ctx->stream);
     cudaStreamDestroy(ctx->stream);
   }
-  if (stream) {
-    ctx->stream = static_cast<cudaStream_t>(stream);
-    ctx->own_stream = false;
-  } else {
-    cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
-    if (e != cudaSuccess) return fail_cuda(ctx, e, "cudaStreamCreate");
-    ctx->own_stream = true;
-  }
+  // used as given: NULL is the legacy default stream (torch's default stream)
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  ctx->own_stream = false;
   return SBDT_OK;
 }
 
@@ -103,6 +100,43 @@ int sbdt_gpu_synchronize(sbdt_gpu_ctx* ctx) {
 }
 
 unsigned long long sbdt_gpu_launch_count(const sbdt_gpu_ctx* ctx) { return ctx ? ctx->launches : 0ULL; }
+
+int sbdt_gpu_set_timing(sbdt_gpu_ctx* ctx, int enable) {
+  if (!ctx) return SBDT_ERR_INVALID;
+  ctx->timing = enable != 0;
+  ctx->stages.clear();
+  ctx->events_used = 0;
+  return SBDT_OK;
+}
+
+int sbdt_gpu_stage_times(sbdt_gpu_ctx* ctx, char* names, int names_len, float* ms, int max_stages) {
+  if (!ctx) return -SBDT_ERR_INVALID;
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) return -fail_cuda(ctx, e, "stage_times sync");
+  int count = 0;
+  std::string all;
+  for (const auto& s : ctx->stages) {
+    if (count >= max_stages) break;
+    float t = 0.f;
+    cudaEventElapsedTime(&t, s.start, s.stop);
+    ms[count++] = t;
+    all += s.name;
+    all += '\n';
+  }
+  if (names && names_len > 0) {
+    const std::size_t nb = all.size() < static_cast<std::size_t>(names_len - 1) ? all.size() : names_len - 1;
+    std::memcpy(names, all.data(), nb);
+    names[nb] = 0;
+  }
+  ctx->stages.clear();
+  ctx->events_used = 0;
+  return count;
+}
+
+int sbdt_gpu_assign_table_stats(sbdt_gpu_ctx* ctx, unsigned* out3) {
+  if (!ctx || !out3) return SBDT_ERR_INVALID;
+  return assign_stats(ctx, out3) == kOk ? SBDT_OK : SBDT_ERR_INVALID;
+}
 
 int sbdt_gpu_check_status(sbdt_gpu_ctx* ctx) {
   if (!ctx) return SBDT_ERR_INVALID;

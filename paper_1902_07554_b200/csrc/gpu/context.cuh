@@ -7,6 +7,7 @@
 #include <cstring>
 #include <map>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 
@@ -26,6 +27,15 @@ struct sbdt_gpu_ctx {
   unsigned* d_status = nullptr;
   // last find_border statistics (read back by the host after a call)
   unsigned long long stats[8] = {0};
+  // optional per-stage CUDA-event timing (bench.py: live per-kernel durations)
+  bool timing = false;
+  struct Stage {
+    std::string name;
+    cudaEvent_t start = nullptr, stop = nullptr;
+  };
+  std::vector<Stage> stages;
+  std::vector<cudaEvent_t> event_pool;
+  std::size_t events_used = 0;
 };
 
 namespace sbdt_gpu {
@@ -71,6 +81,36 @@ inline void* workspace(sbdt_gpu_ctx* ctx, const char* name, std::size_t bytes, c
   b.bytes = want;
   return b.ptr;
 }
+
+inline cudaEvent_t pooled_event(sbdt_gpu_ctx* ctx) {
+  if (ctx->events_used == ctx->event_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    ctx->event_pool.push_back(e);
+  }
+  return ctx->event_pool[ctx->events_used++];
+}
+
+// RAII stage marker: records events around the enclosed launches when timing is on.
+struct StageTimer {
+  sbdt_gpu_ctx* ctx;
+  std::size_t idx = static_cast<std::size_t>(-1);
+  StageTimer(sbdt_gpu_ctx* c, const char* name) : ctx(c) {
+    if (!ctx->timing) return;
+    sbdt_gpu_ctx::Stage s;
+    s.name = name;
+    s.start = pooled_event(ctx);
+    s.stop = pooled_event(ctx);
+    cudaEventRecord(s.start, ctx->stream);
+    idx = ctx->stages.size();
+    ctx->stages.push_back(s);
+  }
+  void end() {
+    if (idx != static_cast<std::size_t>(-1)) cudaEventRecord(ctx->stages[idx].stop, ctx->stream);
+    idx = static_cast<std::size_t>(-1);
+  }
+  ~StageTimer() { end(); }
+};
 
 }  // namespace sbdt_gpu
 

@@ -139,6 +139,7 @@ int reach_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   cudaStream_t st = ctx->stream;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  StageTimer timer(ctx, "border.hull_bfs");
   SBDT_WS(pos_ids, std::uint32_t, "reach.pos_ids", in->S + 1);
   SBDT_WS(pos_count, std::uint64_t, "reach.pos_count", 1);
   SBDT_WS(cidx, std::uint32_t, "reach.cidx", in->S + 1);

@@ -80,6 +80,9 @@ def lib():
         L.sbdt_gpu_find_border.argtypes = [vp, C.c_int, dp, u64, u32p, u32, u64p, u32p, u32p, i8p, C.c_int, C.c_double,
                                            u32, u8p, u8p, u32p, u64p, u32p, u64p, dp]
         L.sbdt_gpu_find_border_dev.argtypes = [vp, C.POINTER(BorderArgs)]
+        L.sbdt_gpu_set_timing.argtypes = [vp, C.c_int]
+        L.sbdt_gpu_stage_times.argtypes = [vp, C.c_char_p, C.c_int, C.POINTER(C.c_float), C.c_int]
+        L.sbdt_gpu_assign_table_stats.argtypes = [vp, C.POINTER(C.c_uint)]
         _lib = L
     return _lib
 
@@ -120,6 +123,35 @@ class Context:
     @property
     def launches(self) -> int:
         return int(lib().sbdt_gpu_launch_count(self._h))
+
+    def set_timing(self, enable: bool):
+        self.check(lib().sbdt_gpu_set_timing(self._h, 1 if enable else 0), "set_timing")
+
+    def stage_times(self) -> list[tuple[str, float]]:
+        """(stage, ms) pairs recorded since the last call (CUDA events on the context stream)."""
+        names = C.create_string_buffer(1 << 16)
+        ms = (C.c_float * 4096)()
+        cnt = lib().sbdt_gpu_stage_times(self._h, names, 1 << 16, ms, 4096)
+        if cnt < 0:
+            self.check(-cnt, "stage_times")
+        labels = names.value.decode().split("\n")[:cnt]
+        return [(labels[i], float(ms[i])) for i in range(cnt)]
+
+    def table_stats(self) -> dict:
+        out = (C.c_uint * 3)()
+        if lib().sbdt_gpu_assign_table_stats(self._h, out) != SBDT_OK:
+            return {}
+        return {"uniform": int(out[0]), "list": int(out[1]), "overflow": int(out[2])}
+
+    # ---- device-pointer entry points (inputs resident in HBM; async on the stream)
+    def assign_points_dev(self, dim, d_xyz, n, d_sample_ids, d_sample_labels, m, k, d_labels, d_part_offsets=None,
+                          d_part_ids=None, d_bbox=None):
+        rc = lib().sbdt_gpu_assign_points_dev(self._h, dim, d_xyz, n, d_sample_ids, d_sample_labels, m, k, d_labels,
+                                              d_part_offsets, d_part_ids, d_bbox)
+        self.check(rc, "assign_points_dev")
+
+    def find_border_dev(self, args: "BorderArgs"):
+        self.check(lib().sbdt_gpu_find_border_dev(self._h, C.byref(args)), "find_border_dev")
 
     def close(self):
         if self._h:
