@@ -193,10 +193,9 @@ def main():
         return
     import torch
     from paper_1902_07554_b200 import gpu, host
+    from paper_1902_07554_b200 import dist as sdist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    rank, local, world = sdist.world()
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
@@ -205,10 +204,7 @@ def main():
     dev = torch.device("cuda", local)
 
     threads = max(1, (os.cpu_count() or 1) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))))
-    seed = None
-    if world > 1:
-        from paper_1902_07554_b200.host import CONFIGS
-        seed = CONFIGS[args.config]["seed"] * 1000 + rank  # independent instance per rank
+    seed = sdist.rank_seed(host.CONFIGS[args.config]["seed"], rank, world)  # independent instance per rank
     t_setup = time.time()
     inst = host.make_instance(args.config, n=args.n, k=args.k, seed=seed)
     dim, n, k, m = inst.dim, inst.n, inst.config["k"], len(inst.sample_ids)
@@ -304,10 +300,8 @@ def main():
     if dist:
         dist.barrier()
     table_stats = ctx.table_stats()
-    tot = torch.tensor([sum(ms)], dtype=torch.float64, device=dev)
-    if dist:
-        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
-    total_ms = float(tot.item())
+    border_stats = ctx.border_stats()
+    total_ms = sdist.max_over_ranks(sum(ms), device=dev)  # device time, max over ranks
     ctx.synchronize()
 
     n_vb = int(d_cnt.item())
@@ -341,7 +335,7 @@ def main():
     roofline = per_kernel.get(dominant) or roof(b_border, t_border)
     roofline = dict(roofline, kernel=dominant)
 
-    value = world * n / (total_ms / args.steps * 1e-3)
+    value = sdist.aggregate_throughput(n, world, total_ms / args.steps * 1e-3)
     clocks = clk.summary()
 
     # ---- end to end through the host-buffer C ABI (pinned buffers; H2D+D2H inside)
@@ -396,7 +390,7 @@ def main():
             "hull_bfs": {"ms_per_step": round(sum(ms_bfs) / len(ms_bfs), 4),
                          "stages_ms": {kk: round(v, 4) for kk, v in stages_bfs.items()},
                          "border_vertices": n_vb_bfs},
-            "border_vertices": n_vb, "positive_simplices": n_pos, "assign_table": table_stats,
+            "border_vertices": n_vb, "positive_simplices": n_pos, "assign_table": table_stats, "border_pipeline": border_stats,
             "gpu_launches": int(launches), "gpu_launches_per_step": launches / args.steps,
             "clocks": clocks, "wall_timed_s": round(t_wall, 3), "setup_s": round(setup_s, 1),
             "e2e": e2e, "cpu_baseline": cpu,

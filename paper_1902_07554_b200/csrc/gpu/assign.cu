@@ -36,14 +36,6 @@ struct __align__(16) SampleRec {
   std::uint32_t label;
 };
 
-// Fine-cell record (32 bytes = one L2 sector).
-struct __align__(32) FineRec {
-  std::uint32_t head;     // bits 0-3: count (0 uniform, 1..7 list, 15 overflow); uniform: label << 8
-  std::uint32_t cand[7];  // indices into the cell-sorted SampleRec array
-};
-constexpr std::uint32_t kRecOverflow = 15u;
-constexpr int kMaxInline = 7;
-
 template <int D>
 constexpr int fine_factor() {
   return D == 3 ? 2 : 3;
@@ -65,9 +57,6 @@ struct SampleGrid {
 };
 
 constexpr int kBlock = 256;
-constexpr int kBuildWarps = 4;
-constexpr int kCoarseCap = 160;
-constexpr int kSurvCap = 64;
 
 // Block-reduce local bbox then one atomic per block per coordinate.
 template <int D>
@@ -269,29 +258,7 @@ __device__ std::uint32_t nearest_label_ring(const double* x, const Grid<D>& g, d
   return best_label;
 }
 
-// ---- K1b: Voronoi label table ----------------------------------------------------
-// Box = centre c +- hw (inflated). Returns true iff sample s is provably
-// never the binary64 argmin in the box because t is strictly closer for
-// every point of it (after rounding): with y = x - c,
-//   |x-s|^2 - |x-t|^2 = F0 + 2 y.(t - s) >= F0 - 2 sum |t_d - s_d| hw_d,
-// required to exceed 1e-10 * max(|x-s|^2 + |x-t|^2), a margin ~5 orders of
-// magnitude above the rounding of the computed distances and of this test.
-template <int D>
-__device__ __forceinline__ bool dominated(const double* c, const double* hw, double H, const double* s,
-                                          const double* t) {
-  double ds = 0.0, dt = 0.0, slope = 0.0;
-#pragma unroll
-  for (int d = 0; d < D; ++d) {
-    const double a = c[d] - s[d], b = c[d] - t[d];
-    ds += a * a;
-    dt += b * b;
-    slope += fabs(t[d] - s[d]) * hw[d];
-  }
-  const double f_min = (ds - dt) - 2.0 * slope;
-  const double rs = sqrt(ds) + H, rt = sqrt(dt) + H;
-  return f_min > 1e-10 * (rs * rs + rt * rt);
-}
-
+// ---- helpers shared with the Voronoi label table ---------------------------------
 template <int D>
 __device__ __forceinline__ void warp_argmin(double& d2, std::uint32_t& idx) {
 #pragma unroll
@@ -305,308 +272,11 @@ __device__ __forceinline__ void warp_argmin(double& d2, std::uint32_t& idx) {
   }
 }
 
-// One warp per grid cell.
-template <int D>
-__global__ void __launch_bounds__(32 * kBuildWarps) k_vlt_build(const SampleGrid<D>* __restrict__ sgp,
-                                                                const std::uint32_t* __restrict__ starts,
-                                                                const SampleRec* __restrict__ sorted,
-                                                                FineRec* __restrict__ table,
-                                                                unsigned* __restrict__ stats) {
-  __shared__ SampleGrid<D> sg;
-  __shared__ std::uint32_t s_idx[kBuildWarps][kCoarseCap];
-  __shared__ double s_xyz[kBuildWarps][kCoarseCap][D];
-  __shared__ std::uint32_t s_lab[kBuildWarps][kCoarseCap];
-  __shared__ std::uint16_t s_surv[kBuildWarps][kSurvCap];
-  __shared__ int s_cnt[kBuildWarps];
-  if (threadIdx.x == 0) sg = *sgp;
-  __syncthreads();
-  const Grid<D>& g = sg.g;
-  const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-  constexpr int F = fine_factor<D>();
-  constexpr int FC = fine_per_cell<D>();
-  const long long cells = static_cast<long long>(sg.cells);
-  for (long long cell = static_cast<long long>(blockIdx.x) * kBuildWarps + warp; cell < cells;
-       cell += static_cast<long long>(gridDim.x) * kBuildWarps) {
-    long long cc[D];
-    {
-      long long rem = cell;
-#pragma unroll
-      for (int d = 0; d < D; ++d) {
-        cc[d] = rem % g.dims[d];
-        rem /= g.dims[d];
-      }
-    }
-    double c[D], hw[D], H2 = 0.0;
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      const double lo = cell_lo<D>(g, cc[d], d), hi = cell_lo<D>(g, cc[d] + 1, d);
-      c[d] = 0.5 * (lo + hi);
-      hw[d] = 0.5 * (hi - lo) + sg.delta_c;
-      H2 += hw[d] * hw[d];
-    }
-    const double H = sqrt(H2);
-    // (a) a dominating sample: nearest to the centre within growing rings
-    double bd = INFINITY;
-    std::uint32_t bi = 0xFFFFFFFFu;
-    for (long long r = 1;; ++r) {
-      long long lo_c[D], span[D], count = 1;
-#pragma unroll
-      for (int d = 0; d < D; ++d) {
-        lo_c[d] = cc[d] - r < 0 ? 0 : cc[d] - r;
-        const long long hi_c = cc[d] + r > g.dims[d] - 1 ? g.dims[d] - 1 : cc[d] + r;
-        span[d] = hi_c - lo_c[d] + 1;
-        count *= span[d];
-      }
-      for (long long t = lane; t < count; t += 32) {
-        long long rem = t, q[D];
-#pragma unroll
-        for (int d = 0; d < D; ++d) {
-          q[d] = lo_c[d] + rem % span[d];
-          rem /= span[d];
-        }
-        const long long qc = linear<D>(g, q);
-        for (std::uint32_t s = starts[qc], e = starts[qc + 1]; s < e; ++s) {
-          const double d2 = sqdist<D>(c, sorted[s].x);
-          if (d2 < bd || (d2 == bd && s < bi)) {
-            bd = d2;
-            bi = s;
-          }
-        }
-      }
-      warp_argmin<D>(bd, bi);
-      if (bi != 0xFFFFFFFFu) break;
-      bool whole = true;
-#pragma unroll
-      for (int d = 0; d < D; ++d) whole = whole && (cc[d] - r <= 0) && (cc[d] + r >= g.dims[d] - 1);
-      if (whole) break;
-    }
-    // (b) coarse candidates: within R of the centre and not dominated by s0
-    const SampleRec s0 = sorted[bi];
-    const double R = (sqrt(bd) + 2.0 * H) * (1.0 + 1e-9) + sg.margin;
-    const double R2 = R * R;
-    if (lane == 0) s_cnt[warp] = 0;
-    __syncwarp();
-    {
-      long long lo_c[D], span[D], count = 1;
-#pragma unroll
-      for (int d = 0; d < D; ++d) {
-        long long a = static_cast<long long>(floor((c[d] - R - g.lo[d]) / g.edge)) - 1;
-        long long b = static_cast<long long>(floor((c[d] + R - g.lo[d]) / g.edge)) + 1;
-        a = a < 0 ? 0 : a;
-        b = b > g.dims[d] - 1 ? g.dims[d] - 1 : b;
-        lo_c[d] = a;
-        span[d] = b - a + 1;
-        count *= span[d];
-      }
-      for (long long t0 = 0; t0 < count; t0 += 32) {
-        const long long t = t0 + lane;
-        std::uint32_t sb = 0, se = 0;
-        if (t < count) {
-          long long rem = t, q[D];
-#pragma unroll
-          for (int d = 0; d < D; ++d) {
-            q[d] = lo_c[d] + rem % span[d];
-            rem /= span[d];
-          }
-          const long long qc = linear<D>(g, q);
-          sb = starts[qc];
-          se = starts[qc + 1];
-        }
-        for (std::uint32_t s = sb; s < se; ++s) {
-          const SampleRec rec = sorted[s];
-          const double d2 = sqdist<D>(c, rec.x);
-          if (d2 > R2) continue;
-          if (s != bi && dominated<D>(c, hw, H, rec.x, s0.x)) continue;
-          const int slot = atomicAdd(&s_cnt[warp], 1);
-          if (slot < kCoarseCap) {
-            s_idx[warp][slot] = s;
-            s_lab[warp][slot] = rec.label;
-#pragma unroll
-            for (int d = 0; d < D; ++d) s_xyz[warp][slot][d] = rec.x[d];
-          }
-        }
-      }
-    }
-    __syncwarp();
-    const int ncand = s_cnt[warp];
-    // (c) fine cells
-    for (int f = 0; f < FC; ++f) {
-      long long fi[D];
-      {
-        int rem = f;
-#pragma unroll
-        for (int d = 0; d < D; ++d) {
-          fi[d] = cc[d] * F + rem % F;
-          rem /= F;
-        }
-      }
-      FineRec rec;
-      rec.head = kRecOverflow;
-#pragma unroll
-      for (int j = 0; j < kMaxInline; ++j) rec.cand[j] = 0;
-      if (ncand <= kCoarseCap) {
-        double fc[D], fhw[D], fH2 = 0.0;
-#pragma unroll
-        for (int d = 0; d < D; ++d) {
-          const double lo = g.lo[d] + static_cast<double>(fi[d]) * sg.ef;
-          const double hi = g.lo[d] + static_cast<double>(fi[d] + 1) * sg.ef;
-          fc[d] = 0.5 * (lo + hi);
-          fhw[d] = 0.5 * (hi - lo) + sg.delta_f;
-          fH2 += fhw[d] * fhw[d];
-        }
-        const double fH = sqrt(fH2);
-        double bd2 = INFINITY;
-        std::uint32_t bj = 0xFFFFFFFFu;
-        for (int j = lane; j < ncand; j += 32) {
-          const double d2 = sqdist<D>(fc, s_xyz[warp][j]);
-          if (d2 < bd2 || (d2 == bd2 && static_cast<std::uint32_t>(j) < bj)) {
-            bd2 = d2;
-            bj = static_cast<std::uint32_t>(j);
-          }
-        }
-        warp_argmin<D>(bd2, bj);
-        int count = 0;
-        bool uniform = true;
-        const std::uint32_t lab0 = s_lab[warp][bj];
-        // pass 1: survivors of the nearest-centre dominator
-        for (int j0 = 0; j0 < ncand; j0 += 32) {
-          const int j = j0 + static_cast<int>(lane);
-          bool keep = false;
-          if (j < ncand)
-            keep = (static_cast<std::uint32_t>(j) == bj) || !dominated<D>(fc, fhw, fH, s_xyz[warp][j], s_xyz[warp][bj]);
-          const unsigned ballot = __ballot_sync(0xffffffffu, keep);
-          if (__ballot_sync(0xffffffffu, keep && s_lab[warp][j] != lab0)) uniform = false;
-          const int pos = count + __popc(ballot & ((1u << lane) - 1u));
-          if (keep && pos < kSurvCap) s_surv[warp][pos] = static_cast<std::uint16_t>(j);
-          count += __popc(ballot);
-        }
-        __syncwarp();
-        if (uniform) {
-          rec.head = lab0 << 8;
-        } else if (count <= kSurvCap) {
-          // pass 2: pairwise dominance among the survivors (any dominator
-          // excludes: a dominated sample is never the argmin in the box)
-          const int nsurv = count;
-          count = 0;
-          uniform = true;
-          for (int j0 = 0; j0 < nsurv; j0 += 32) {
-            const int jj = j0 + static_cast<int>(lane);
-            bool keep = jj < nsurv;
-            const int j = keep ? s_surv[warp][jj] : 0;
-            for (int u = 0; u < nsurv; ++u) {
-              const int t = s_surv[warp][u];
-              if (keep && t != j && dominated<D>(fc, fhw, fH, s_xyz[warp][j], s_xyz[warp][t])) keep = false;
-            }
-            const unsigned ballot = __ballot_sync(0xffffffffu, keep);
-            if (__ballot_sync(0xffffffffu, keep && s_lab[warp][j] != lab0)) uniform = false;
-            const int pos = count + __popc(ballot & ((1u << lane) - 1u));
-            if (keep && pos < kMaxInline) rec.cand[pos] = s_idx[warp][j];
-            count += __popc(ballot);
-          }
-          // merge the lanes' partial candidate writes (each slot has one writer)
-#pragma unroll
-          for (int j = 0; j < kMaxInline; ++j) {
-            std::uint32_t v = rec.cand[j];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v |= __shfl_xor_sync(0xffffffffu, v, o);
-            rec.cand[j] = v;
-          }
-          if (uniform) rec.head = lab0 << 8;
-          else if (count <= kMaxInline) rec.head = static_cast<std::uint32_t>(count);
-          else rec.head = kRecOverflow;
-        } else {
-          rec.head = kRecOverflow;
-        }
-      }
-      if (lane == 0) {
-        long long fdims[D];
-#pragma unroll
-        for (int d = 0; d < D; ++d) fdims[d] = g.dims[d];
-        const long long ridx = cell * FC + f;
-        table[ridx] = rec;
-        if (stats) {
-          const std::uint32_t h = rec.head & 15u;
-          atomicAdd(&stats[h == 0 ? 0 : (h == kRecOverflow ? 2 : 1)], 1u);
-        }
-        (void)fdims;
-      }
-    }
-  }
-}
+}  // namespace sbdt_gpu
 
-// K2: table-driven point pass.
-template <int D>
-__global__ void __launch_bounds__(kBlock) k_assign_table(const double* __restrict__ xyz, std::uint64_t n,
-                                                         const SampleGrid<D>* __restrict__ sgp,
-                                                         const FineRec* __restrict__ table,
-                                                         const std::uint32_t* __restrict__ starts,
-                                                         const SampleRec* __restrict__ sorted,
-                                                         std::uint32_t* __restrict__ labels,
-                                                         unsigned long long* bbox) {
-  __shared__ SampleGrid<D> s_sg;
-  if (threadIdx.x == 0) s_sg = *sgp;
-  __syncthreads();
-  const SampleGrid<D>& sg = s_sg;
-  constexpr int F = fine_factor<D>();
-  constexpr int FC = fine_per_cell<D>();
-  double blo[D], bhi[D];
-#pragma unroll
-  for (int d = 0; d < D; ++d) blo[d] = INFINITY, bhi[d] = -INFINITY;
-  for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += std::uint64_t(gridDim.x) * blockDim.x) {
-    double x[D];
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      x[d] = __ldcs(xyz + i * D + d);
-      blo[d] = fmin(blo[d], x[d]);
-      bhi[d] = fmax(bhi[d], x[d]);
-    }
-    bool inside = true;
-    long long cell = 0, sub = 0;
-    {
-      long long mul = 1, smul = 1;
-#pragma unroll
-      for (int d = 0; d < D; ++d) {
-        const double f = floor((x[d] - sg.g.lo[d]) * sg.inv_ef);
-        const double fmax_ = static_cast<double>(sg.g.dims[d] * F);
-        inside = inside && (f >= 0.0) && (f < fmax_);
-        const long long fi = inside ? static_cast<long long>(f) : 0;
-        cell += (fi / F) * mul;
-        sub += (fi % F) * smul;
-        mul *= sg.g.dims[d];
-        smul *= F;
-      }
-    }
-    std::uint32_t label;
-    std::uint32_t head = kRecOverflow;
-    const FineRec* rp = nullptr;
-    if (inside) {
-      rp = table + (cell * FC + sub);
-      head = __ldg(&rp->head);
-    }
-    const std::uint32_t cnt = head & 15u;
-    if (cnt == 0) {
-      label = head >> 8;
-    } else if (cnt != kRecOverflow) {
-      double best = INFINITY;
-      std::uint32_t best_pid = 0xFFFFFFFFu;
-      label = 0;
-      for (std::uint32_t j = 0; j < cnt; ++j) {
-        const SampleRec rec = sorted[__ldg(&rp->cand[j])];
-        const double d2 = sqdist<D>(x, rec.x);
-        if (d2 < best || (d2 == best && rec.pid < best_pid)) {
-          best = d2;
-          best_pid = rec.pid;
-          label = rec.label;
-        }
-      }
-    } else {
-      label = nearest_label_ring<D>(x, sg.g, sg.margin, starts, sorted);
-    }
-    __stcs(labels + i, label);
-  }
-  bbox_flush<D>(blo, bhi, bbox);
-}
+#include "vlt.cuh"
+
+namespace sbdt_gpu {
 
 // ---- K3: stable bucketing of point ids by label ------------------------------
 constexpr int kBucketTile = 4096;  // points per CTA tile
@@ -685,7 +355,7 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
                 const std::uint32_t* d_sample_labels, std::uint32_t m, std::uint32_t* d_labels,
                 unsigned long long* d_bbox) {
   cudaStream_t st = ctx->stream;
-  const unsigned long long cap = 4ULL * m + 64;
+  const unsigned long long cap = 2ULL * m + 1024;
   SBDT_WS(recs, SampleRec, "assign.recs", m);
   SBDT_WS(sorted, SampleRec, "assign.sorted", m);
   SBDT_WS(sbbox, unsigned long long, "assign.sbbox", 2 * D);
@@ -694,15 +364,20 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
   SBDT_WS(starts, std::uint32_t, "assign.starts", cap + 1);
   SBDT_WS(cell_of, std::uint32_t, "assign.cell_of", m);
   SBDT_WS(blocksums, std::uint32_t, "assign.blocksums", (cap + 1) / kScanTile + 2);
-  SBDT_WS(table, FineRec, "assign.table", cap * fine_per_cell<D>());
+  const unsigned long long fine = cap * fine_per_cell<D>();
+  SBDT_WS(heads, std::uint32_t, "assign.heads", fine);
+  SBDT_WS(slab, VltEntry, "assign.slab", fine * kSlots);
+  SBDT_WS(slabels, std::uint32_t, "assign.slabels", m);
   SBDT_WS(stats, unsigned, "assign.stats", 4);
+  SBDT_WS(oq, std::uint32_t, "assign.oq", n + 1);
+  SBDT_WS(oqc, unsigned, "assign.oqc", 1);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  const unsigned sblocks = static_cast<unsigned>((m + kBlock - 1) / kBlock);
   {
     StageTimer t0(ctx, "assign.sample_grid");
     k_bbox_init<<<1, 32, 0, st>>>(sbbox, D);
     k_bbox_init<<<1, 32, 0, st>>>(d_bbox, D);
-    const unsigned sblocks = static_cast<unsigned>((m + kBlock - 1) / kBlock);
     k_sample_gather<D><<<sblocks, kBlock, 0, st>>>(d_xyz, d_sample_ids, d_sample_labels, m, recs, sbbox);
     k_sample_grid_params<D><<<1, 1, 0, st>>>(sbbox, m, cap, sg);
     SBDT_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(std::uint32_t) * (cap + 1), st));
@@ -710,20 +385,23 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
     exclusive_scan(counts, starts, cap + 1, blocksums, nullptr, st, &ctx->launches);
     SBDT_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(std::uint32_t) * (cap + 1), st));
     k_sample_scatter<<<sblocks, kBlock, 0, st>>>(recs, m, cell_of, starts, counts, sorted);
-    ctx->launches += 6;
+    k_sorted_labels<<<sblocks, kBlock, 0, st>>>(sorted, m, slabels);
+    ctx->launches += 7;
   }
   {
     StageTimer t1(ctx, "assign.table");
     if (ctx->timing) SBDT_CUDA_TRY(cudaMemsetAsync(stats, 0, sizeof(unsigned) * 4, st));
-    k_vlt_build<D><<<sms * 16, 32 * kBuildWarps, 0, st>>>(sg, starts, sorted, table, ctx->timing ? stats : nullptr);
+    k_vlt_build<D><<<sms * 16, 32 * kVltWarps, 0, st>>>(sg, starts, sorted, heads, slab, ctx->timing ? stats : nullptr);
     ctx->launches += 1;
   }
   const std::uint64_t want = (n + kBlock - 1) / kBlock;
   const unsigned blocks = static_cast<unsigned>(want < std::uint64_t(sms) * 16 ? want : std::uint64_t(sms) * 16);
   if (blocks > 0) {
     StageTimer t2(ctx, "assign.points");
-    k_assign_table<D><<<blocks, kBlock, 0, st>>>(d_xyz, n, sg, table, starts, sorted, d_labels, d_bbox);
-    ctx->launches += 1;
+    SBDT_CUDA_TRY(cudaMemsetAsync(oqc, 0, sizeof(unsigned), st));
+    k_assign_vlt<D><<<blocks, kBlock, 0, st>>>(d_xyz, n, sg, heads, slab, sorted, slabels, d_labels, d_bbox, oq, oqc);
+    k_assign_overflow<D><<<sms * 4, 128, 0, st>>>(d_xyz, sg, starts, sorted, d_labels, oq, oqc);
+    ctx->launches += 2;
   }
   SBDT_CUDA_TRY(cudaGetLastError());
   return kOk;

@@ -23,60 +23,13 @@
 
 #include "common.cuh"
 #include "context.cuh"
+#include "owner_grid.cuh"
 #include "scan.cuh"
 #include "sbdt_gpu.h"
 
 namespace sbdt_gpu {
 
 constexpr int kBThreads = 256;
-
-template <int D>
-struct OwnerGrid {
-  Grid<D> g;
-  double inv_edge;
-  double margin;
-  int levels;  // number of levels incl. leaf level 0; top level has one block
-  int shift;   // log2 of per-axis fanout
-  int ldims[kMaxLevels][D];
-  unsigned long long loff[kMaxLevels + 1];
-};
-
-template <int D>
-constexpr int fan_shift() {
-  return D == 3 ? 2 : 3;  // 64 children per block
-}
-
-template <int D>
-__device__ __forceinline__ unsigned long long lin(const int* dims, const int* c) {
-  unsigned long long id = static_cast<unsigned>(c[D - 1]);
-#pragma unroll
-  for (int d = D - 2; d >= 0; --d) id = id * static_cast<unsigned>(dims[d]) + static_cast<unsigned>(c[d]);
-  return id;
-}
-
-// Packed descent entries: level | coordinates (3D: 20/20/19 bits, 2D: 29/29).
-template <int D>
-__device__ __forceinline__ unsigned long long pack(int L, const int* c) {
-  if constexpr (D == 3)
-    return (static_cast<unsigned long long>(L) << 59) | (static_cast<unsigned long long>(c[2]) << 40) |
-           (static_cast<unsigned long long>(c[1]) << 20) | static_cast<unsigned long long>(c[0]);
-  else
-    return (static_cast<unsigned long long>(L) << 58) | (static_cast<unsigned long long>(c[1]) << 29) |
-           static_cast<unsigned long long>(c[0]);
-}
-template <int D>
-__device__ __forceinline__ int unpack(unsigned long long e, int* c) {
-  if constexpr (D == 3) {
-    c[0] = static_cast<int>(e & 0xFFFFFu);
-    c[1] = static_cast<int>((e >> 20) & 0xFFFFFu);
-    c[2] = static_cast<int>((e >> 40) & 0x7FFFFu);
-    return static_cast<int>(e >> 59);
-  } else {
-    c[0] = static_cast<int>(e & 0x1FFFFFFFu);
-    c[1] = static_cast<int>((e >> 29) & 0x1FFFFFFFu);
-    return static_cast<int>(e >> 58);
-  }
-}
 
 __global__ void k_bbox_points_init(unsigned long long* bbox, int dim) {
   if (threadIdx.x < static_cast<unsigned>(dim)) {
@@ -113,346 +66,9 @@ __global__ void k_bbox_points(const double* __restrict__ xyz, std::uint64_t n, u
   }
 }
 
-// Grid parameters from the global bbox: edge = c_G (V/n)^(1/D) (SPEC.md:403 /
-// build_grid_index post), origin = bbox lo, dims = floor(ext/edge)+1.
-template <int D>
-__global__ void k_owner_params(const unsigned long long* bbox, std::uint64_t n, double c_G,
-                               unsigned long long cap, OwnerGrid<D>* og, unsigned* status) {
-  double lo[D], hi[D], vol = 1.0, ext_max = 0.0, mag = 0.0;
-  for (int d = 0; d < D; ++d) {
-    lo[d] = ordered_to_dbl(bbox[d]);
-    hi[d] = ordered_to_dbl(bbox[D + d]);
-    vol *= (hi[d] - lo[d]);
-    ext_max = fmax(ext_max, hi[d] - lo[d]);
-    mag = fmax(mag, fmax(fabs(lo[d]), fabs(hi[d])));
-  }
-  const double per = vol / static_cast<double>(n);
-  const double e = c_G * ((D == 2) ? sqrt(per) : cbrt_det(per));
-  unsigned long long cells = 1;
-  bool bad = !(e > 0.0);
-  const double axis_cap = D == 3 ? 500000.0 : 500000000.0;  // packed-coordinate range
-  for (int d = 0; d < D; ++d) {
-    og->g.lo[d] = lo[d];
-    const double f = bad ? 0.0 : floor((hi[d] - lo[d]) / e);
-    if (!(f < axis_cap)) bad = true;
-    og->g.dims[d] = bad ? 1 : static_cast<long long>(f) + 1;
-    cells *= static_cast<unsigned long long>(og->g.dims[d]);
-  }
-  if (bad || cells > cap) {
-    atomicOr(status, kStGridCap);
-    for (int d = 0; d < D; ++d) og->g.dims[d] = 1;
-  }
-  og->g.edge = bad ? 1.0 : e;
-  og->inv_edge = 1.0 / og->g.edge;
-  og->margin = 1e-9 * (mag + ext_max + og->g.edge);
-  const int sh = fan_shift<D>();
-  og->shift = sh;
-  int L = 0;
-  unsigned long long off = 0;
-  for (;;) {
-    bool top = true;
-    unsigned long long cnt = 1;
-    for (int d = 0; d < D; ++d) {
-      og->ldims[L][d] = static_cast<int>(((og->g.dims[d] - 1) >> (L * sh)) + 1);
-      cnt *= static_cast<unsigned long long>(og->ldims[L][d]);
-      top = top && og->ldims[L][d] == 1;
-    }
-    og->loff[L] = off;
-    off += cnt;
-    ++L;
-    if (top || L == kMaxLevels) break;
-  }
-  og->loff[L] = off;
-  og->levels = L;
-}
-
-// Mark leaf cells with their owner; optionally the per-partition point bbox.
-template <int D>
-__global__ void k_owner_mark(const double* __restrict__ xyz, const std::uint32_t* __restrict__ labels,
-                             std::uint64_t n, const OwnerGrid<D>* __restrict__ ogp, std::uint16_t* __restrict__ owner,
-                             unsigned long long* __restrict__ pbbox, std::uint32_t k) {
-  __shared__ Grid<D> g;
-  __shared__ int dims[D];
-  extern __shared__ unsigned long long s_pb[];  // [k][2D] when pbbox != nullptr
-  if (threadIdx.x == 0) {
-    g = ogp->g;
-    for (int d = 0; d < D; ++d) dims[d] = ogp->ldims[0][d];
-  }
-  if (pbbox)
-    for (std::uint32_t j = threadIdx.x; j < k * 2 * D; j += blockDim.x)
-      s_pb[j] = ((j % (2 * D)) < D) ? 0xFFFFFFFFFFFFFFFFULL : 0ULL;
-  __syncthreads();
-  for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += std::uint64_t(gridDim.x) * blockDim.x) {
-    double x[D];
-    int c[D];
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      x[d] = xyz[i * D + d];
-      c[d] = static_cast<int>(cell_coord<D>(g, x[d], d));
-    }
-    const std::uint32_t lab = labels[i];
-    std::uint16_t* slot = owner + lin<D>(dims, c);
-    unsigned short old = *slot;
-    while (old != lab && old != kOwnerMulti) {
-      const unsigned short nv = (old == kOwnerEmpty) ? static_cast<unsigned short>(lab) : kOwnerMulti;
-      const unsigned short prev = atomicCAS(reinterpret_cast<unsigned short*>(slot), old, nv);
-      if (prev == old) break;
-      old = prev;
-    }
-    if (pbbox) {
-#pragma unroll
-      for (int d = 0; d < D; ++d) {
-        atomicMin(&s_pb[lab * 2 * D + d], dbl_to_ordered(x[d]));
-        atomicMax(&s_pb[lab * 2 * D + D + d], dbl_to_ordered(x[d]));
-      }
-    }
-  }
-  if (pbbox) {
-    __syncthreads();
-    for (std::uint32_t j = threadIdx.x; j < k * 2 * D; j += blockDim.x) {
-      if ((j % (2 * D)) < D) atomicMin(&pbbox[j], s_pb[j]);
-      else atomicMax(&pbbox[j], s_pb[j]);
-    }
-  }
-}
-
 __global__ void k_pbbox_init(unsigned long long* pbbox, std::uint32_t count, int dim) {
   for (std::uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < count; j += gridDim.x * blockDim.x)
     pbbox[j] = ((j % (2 * dim)) < static_cast<std::uint32_t>(dim)) ? 0xFFFFFFFFFFFFFFFFULL : 0ULL;
-}
-
-__device__ __forceinline__ std::uint16_t combine(std::uint16_t a, std::uint16_t b) {
-  if (a == kOwnerEmpty) return b;
-  if (b == kOwnerEmpty) return a;
-  return a == b ? a : kOwnerMulti;
-}
-
-template <int D>
-__device__ __forceinline__ void build_block(const OwnerGrid<D>& og, std::uint16_t* owner, int L, unsigned long long id) {
-  const int F = 1 << og.shift;
-  int c[D];
-  {
-    unsigned long long rem = id;
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      c[d] = static_cast<int>(rem % static_cast<unsigned>(og.ldims[L][d]));
-      rem /= static_cast<unsigned>(og.ldims[L][d]);
-    }
-  }
-  std::uint16_t code = kOwnerEmpty;
-  int ch[D];
-  const int* cd = og.ldims[L - 1];
-  if constexpr (D == 3) {
-    for (ch[2] = c[2] * F; ch[2] < min((c[2] + 1) * F, cd[2]); ++ch[2])
-      for (ch[1] = c[1] * F; ch[1] < min((c[1] + 1) * F, cd[1]); ++ch[1])
-        for (ch[0] = c[0] * F; ch[0] < min((c[0] + 1) * F, cd[0]); ++ch[0])
-          code = combine(code, owner[og.loff[L - 1] + lin<D>(cd, ch)]);
-  } else {
-    for (ch[1] = c[1] * F; ch[1] < min((c[1] + 1) * F, cd[1]); ++ch[1])
-      for (ch[0] = c[0] * F; ch[0] < min((c[0] + 1) * F, cd[0]); ++ch[0])
-        code = combine(code, owner[og.loff[L - 1] + lin<D>(cd, ch)]);
-  }
-  owner[og.loff[L] + id] = code;
-}
-
-template <int D>
-__global__ void k_owner_level(const OwnerGrid<D>* __restrict__ ogp, std::uint16_t* __restrict__ owner, int L) {
-  __shared__ OwnerGrid<D> og;
-  if (threadIdx.x == 0) og = *ogp;
-  __syncthreads();
-  if (L >= og.levels) return;
-  const unsigned long long cnt = og.loff[L + 1] - og.loff[L];
-  for (unsigned long long id = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; id < cnt;
-       id += static_cast<unsigned long long>(gridDim.x) * blockDim.x)
-    build_block<D>(og, owner, L, id);
-}
-
-template <int D>
-__global__ void k_owner_levels_tail(const OwnerGrid<D>* __restrict__ ogp, std::uint16_t* __restrict__ owner, int L0) {
-  __shared__ OwnerGrid<D> og;
-  if (threadIdx.x == 0) og = *ogp;
-  __syncthreads();
-  for (int L = L0; L < og.levels; ++L) {
-    const unsigned long long cnt = og.loff[L + 1] - og.loff[L];
-    for (unsigned long long id = threadIdx.x; id < cnt; id += blockDim.x) build_block<D>(og, owner, L, id);
-    __syncthreads();
-  }
-}
-
-// ---- descent helpers -----------------------------------------------------------
-template <int D>
-__device__ __forceinline__ void block_box(const OwnerGrid<D>& og, int L, const int* c, double* blo, double* bhi) {
-  const int s = L * og.shift;
-#pragma unroll
-  for (int d = 0; d < D; ++d) {
-    const long long first = static_cast<long long>(c[d]) << s;
-    long long last1 = static_cast<long long>(c[d] + 1) << s;
-    if (last1 > og.g.dims[d]) last1 = og.g.dims[d];
-    blo[d] = cell_lo<D>(og.g, first, d);
-    bhi[d] = cell_lo<D>(og.g, last1, d);
-  }
-}
-
-// Depth-first pyramid descent with one cursor frame per level (depth bounded
-// by the number of levels, no overflow). Visits the blocks of level L0 in the
-// leaf range [a,b] (restricted) or the single top block; a block whose code
-// is EMPTY or `self` is pruned; test(blo, bhi) returns 0 (reject), 1
-// (descend) or 2 (accept: every sub-box passes, so a foreign occupied leaf
-// inside passes). A leaf that passes is a hit.
-template <int D, class Test>
-__device__ bool descend(const OwnerGrid<D>& og, const std::uint16_t* __restrict__ owner, std::uint32_t self, int L0,
-                        const int* a, const int* b, bool restrict_range, const Test& test) {
-  struct Frame {
-    int lo[D], hi[D], cur[D];
-    int level;
-  };
-  Frame fr[kMaxLevels + 1];
-  int depth = 1;
-#pragma unroll
-  for (int d = 0; d < D; ++d) {
-    fr[0].lo[d] = restrict_range ? (a[d] >> (L0 * og.shift)) : 0;
-    fr[0].hi[d] = restrict_range ? (b[d] >> (L0 * og.shift)) : og.ldims[L0][d] - 1;
-    fr[0].cur[d] = fr[0].lo[d];
-  }
-  fr[0].level = L0;
-  while (depth > 0) {
-    Frame& f = fr[depth - 1];
-    if (f.cur[D - 1] > f.hi[D - 1]) {
-      --depth;
-      continue;
-    }
-    int cc[D];
-#pragma unroll
-    for (int d = 0; d < D; ++d) cc[d] = f.cur[d];
-    // odometer advance
-    ++f.cur[0];
-#pragma unroll
-    for (int d = 0; d < D - 1; ++d)
-      if (f.cur[d] > f.hi[d]) {
-        f.cur[d] = f.lo[d];
-        ++f.cur[d + 1];
-      }
-    const int lv = f.level;
-    const std::uint16_t code = owner[og.loff[lv] + lin<D>(og.ldims[lv], cc)];
-    if (code == kOwnerEmpty || code == self) continue;
-    double blo[D], bhi[D];
-    block_box<D>(og, lv, cc, blo, bhi);
-    const int r = test(blo, bhi);
-    if (r == 0) continue;
-    if (lv == 0 || r == 2) return true;
-    const int cl = lv - 1;
-    const int csh = cl * og.shift;
-    Frame& g = fr[depth];
-    bool empty = false;
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      int lo = cc[d] << og.shift;
-      int hi = min(((cc[d] + 1) << og.shift) - 1, og.ldims[cl][d] - 1);
-      if (restrict_range) {
-        lo = max(lo, a[d] >> csh);
-        hi = min(hi, b[d] >> csh);
-      }
-      g.lo[d] = lo;
-      g.hi[d] = hi;
-      g.cur[d] = lo;
-      empty = empty || lo > hi;
-    }
-    g.level = cl;
-    if (!empty) ++depth;
-  }
-  return false;
-}
-
-// true iff some cell with owner code not in {EMPTY, self} overlaps the sphere.
-template <int D>
-__device__ bool sphere_hits_foreign(const OwnerGrid<D>& og, const std::uint16_t* __restrict__ owner,
-                                    const double* c, double r2, std::uint32_t self) {
-  if (isnan(r2)) return false;
-  bool fin = isfinite(r2);
-#pragma unroll
-  for (int d = 0; d < D; ++d) fin = fin && isfinite(c[d]);
-  int a[D], b[D];
-  if (fin) {
-    // Conservative leaf range: the margin (1e-9 relative) dominates the
-    // rounding of this multiply-by-inverse binning.
-    const double r = sqrt(r2) * (1.0 + 1e-9) + og.margin;
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      const double fa = floor((c[d] - r - og.g.lo[d]) * og.inv_edge);
-      const double fb = floor((c[d] + r - og.g.lo[d]) * og.inv_edge);
-      const double top = static_cast<double>(og.ldims[0][d] - 1);
-      if (fb < 0.0 || fa > top) return false;
-      a[d] = fa < 0.0 ? 0 : static_cast<int>(fa);
-      b[d] = fb > top ? og.ldims[0][d] - 1 : static_cast<int>(fb);
-    }
-  } else {
-#pragma unroll
-    for (int d = 0; d < D; ++d) a[d] = 0, b[d] = og.ldims[0][d] - 1;
-  }
-  int L = 0;
-  for (; L < og.levels - 1; ++L) {
-    bool ok = true;
-#pragma unroll
-    for (int d = 0; d < D; ++d) ok = ok && ((b[d] >> (L * og.shift)) - (a[d] >> (L * og.shift)) <= 1);
-    if (ok) break;
-  }
-  // Fast path: start blocks (<= 2 per axis) all EMPTY or own partition.
-  {
-    int s0[D], n0[D];
-    bool any = false;
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      s0[d] = a[d] >> (L * og.shift);
-      n0[d] = (b[d] >> (L * og.shift)) - s0[d] + 1;
-    }
-    const int total = D == 3 ? n0[0] * n0[1] * n0[2] : n0[0] * n0[1];
-    for (int t = 0; t < total && !any; ++t) {
-      int cc[D], rem = t;  // every n0 is 1 or 2 at the start level
-#pragma unroll
-      for (int d = 0; d < D; ++d) {
-        cc[d] = s0[d] + (rem & (n0[d] - 1));
-        rem >>= (n0[d] - 1);
-      }
-      const std::uint16_t code = owner[og.loff[L] + lin<D>(og.ldims[L], cc)];
-      any = !(code == kOwnerEmpty || code == self);
-    }
-    if (!any) return false;
-  }
-  return descend<D>(og, owner, self, L, a, b, true, [&](const double* blo, const double* bhi) {
-    if (!box_sphere<D>(blo, bhi, c, r2)) return 0;
-    return box_inside_sphere<D>(blo, bhi, c, r2) ? 2 : 1;
-  });
-}
-
-// Halfspace variant: test = some box corner strictly on the outer side of
-// the facet plane (exact orient), full = every corner strictly outside.
-template <int D>
-__device__ int corners_outside(const double* const* facet, int inner_sign, const double* blo, const double* bhi) {
-  const double* pts[D + 1];
-#pragma unroll
-  for (int i = 0; i < D; ++i) pts[i] = facet[i];
-  double corner[D];
-  pts[D] = corner;
-  int outside = 0;
-  for (unsigned cm = 0; cm < (1u << D); ++cm) {
-#pragma unroll
-    for (int d = 0; d < D; ++d) corner[d] = (cm & (1u << d)) ? bhi[d] : blo[d];
-    const int s = orient_dev<D>(pts);
-    if (s != 0 && s != inner_sign) ++outside;
-  }
-  return outside;
-}
-
-template <int D>
-__device__ bool halfspace_hits_foreign(const OwnerGrid<D>& og, const std::uint16_t* __restrict__ owner,
-                                       const double* const* facet, int inner_sign, std::uint32_t self) {
-  return descend<D>(og, owner, self, og.levels - 1, nullptr, nullptr, false,
-                    [&](const double* blo, const double* bhi) {
-                      const int out = corners_outside<D>(facet, inner_sign, blo, bhi);
-                      if (out == 0) return 0;
-                      return out == (1 << D) ? 2 : 1;
-                    });
 }
 
 // circumsphere (geometry.cpp:279-327) + inflated (geometry.hpp:179-183)
@@ -498,6 +114,148 @@ __device__ __forceinline__ void circumsphere_inflated(const double (*p)[D], doub
   }
 }
 
+// Binary32 circumsphere with an a-posteriori error bound (Cramer's rule as
+// geometry.cpp:279-327, relative to p0). Inputs p_i - p0 are formed in
+// binary64 and rounded (relative error <= 2^-24); every 2x2/3x3 determinant is
+// accompanied by its permanent P (sum of |products|); its rounding error is
+// <= 8.4e-7 P (inputs + products + sums), bounded here by g = 2e-6 P. When the
+// system is well conditioned (|det| > 4 g P_det) the centre error per axis is
+//   e_i <= g (P_Ni + |rel_i| P_det) / (|det| - g P_det) + 2^-23 |rel_i|,
+// which also dominates the binary64 evaluation's own error (~2^-29 of it).
+// Returns a centre (binary64) and a radius R such that the sphere (c, R)
+// contains the inflated binary64 sphere of circumsphere_inflated(); false
+// when ill-conditioned (the caller then runs the exact path).
+template <int D>
+__device__ __forceinline__ bool enclosing_sphere_f32(const double (*p)[D], double* c, double* R) {
+  constexpr float g = 2e-6f;
+  float rel[D], err[D];
+  if constexpr (D == 2) {
+    const float ux = static_cast<float>(p[1][0] - p[0][0]), uy = static_cast<float>(p[1][1] - p[0][1]);
+    const float vx = static_cast<float>(p[2][0] - p[0][0]), vy = static_cast<float>(p[2][1] - p[0][1]);
+    const float bu = 0.5f * (ux * ux + uy * uy), bv = 0.5f * (vx * vx + vy * vy);
+    const float det = ux * vy - uy * vx;
+    const float pd = fabsf(ux * vy) + fabsf(uy * vx);
+    if (!(fabsf(det) > 4.f * g * pd)) return false;
+    const float n0 = bu * vy - bv * uy, p0 = fabsf(bu * vy) + fabsf(bv * uy);
+    const float n1 = ux * bv - vx * bu, p1 = fabsf(ux * bv) + fabsf(vx * bu);
+    const float den = fabsf(det) - g * pd;
+    rel[0] = n0 / det;
+    rel[1] = n1 / det;
+    err[0] = g * (p0 + fabsf(rel[0]) * pd) / den + 1.2e-7f * fabsf(rel[0]);
+    err[1] = g * (p1 + fabsf(rel[1]) * pd) / den + 1.2e-7f * fabsf(rel[1]);
+  } else {
+    float m[3][3], r[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+#pragma unroll
+      for (int d = 0; d < 3; ++d) m[i][d] = static_cast<float>(p[i + 1][d] - p[0][d]);
+      r[i] = 0.5f * (m[i][0] * m[i][0] + m[i][1] * m[i][1] + m[i][2] * m[i][2]);
+    }
+    // minors of the last two rows
+    const float c0 = m[1][1] * m[2][2] - m[1][2] * m[2][1], q0 = fabsf(m[1][1] * m[2][2]) + fabsf(m[1][2] * m[2][1]);
+    const float c1 = m[1][0] * m[2][2] - m[1][2] * m[2][0], q1 = fabsf(m[1][0] * m[2][2]) + fabsf(m[1][2] * m[2][0]);
+    const float c2 = m[1][0] * m[2][1] - m[1][1] * m[2][0], q2 = fabsf(m[1][0] * m[2][1]) + fabsf(m[1][1] * m[2][0]);
+    const float det = m[0][0] * c0 - m[0][1] * c1 + m[0][2] * c2;
+    const float pd = fabsf(m[0][0]) * q0 + fabsf(m[0][1]) * q1 + fabsf(m[0][2]) * q2;
+    if (!(fabsf(det) > 4.f * g * pd)) return false;
+    const float den = fabsf(det) - g * pd;
+#pragma unroll
+    for (int col = 0; col < 3; ++col) {
+      float a[3][3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) a[i][j] = (j == col) ? r[i] : m[i][j];
+      const float e0 = a[1][1] * a[2][2] - a[1][2] * a[2][1], f0 = fabsf(a[1][1] * a[2][2]) + fabsf(a[1][2] * a[2][1]);
+      const float e1 = a[1][0] * a[2][2] - a[1][2] * a[2][0], f1 = fabsf(a[1][0] * a[2][2]) + fabsf(a[1][2] * a[2][0]);
+      const float e2 = a[1][0] * a[2][1] - a[1][1] * a[2][0], f2 = fabsf(a[1][0] * a[2][1]) + fabsf(a[1][1] * a[2][0]);
+      const float num = a[0][0] * e0 - a[0][1] * e1 + a[0][2] * e2;
+      const float pn = fabsf(a[0][0]) * f0 + fabsf(a[0][1]) * f1 + fabsf(a[0][2]) * f2;
+      rel[col] = num / det;
+      err[col] = g * (pn + fabsf(rel[col]) * pd) / den + 1.2e-7f * fabsf(rel[col]);
+    }
+  }
+  float rr = 0.f, ee = 0.f;
+  bool fin = true;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    c[d] = p[0][d] + static_cast<double>(rel[d]);
+    rr += rel[d] * rel[d];
+    ee += err[d] * err[d];
+    fin = fin && isfinite(rel[d]) && isfinite(err[d]);
+  }
+  if (!fin) return false;
+  // radius of the binary64 sphere <= |rel32| + e (+ its inflation 1e-10);
+  // the centres differ by <= e: R = |rel32| (1 + 1e-6) + 2.01 e (+ abs slack)
+  const double r32 = sqrt(static_cast<double>(rr)), e32 = sqrt(static_cast<double>(ee));
+  double mag = 0.0;
+#pragma unroll
+  for (int d = 0; d < D; ++d) mag = fmax(mag, fabs(p[0][d]));
+  *R = r32 * (1.0 + 1e-6) + 2.01 * e32 + 1e-15 * mag;
+  return true;
+}
+
+// true iff every cell the sphere (c, R) can reach lies in one window (the
+// cell itself, its 3^D or its 5^D neighbourhood, the smallest that covers the
+// conservative cell range) whose combined code is EMPTY or `self`: then no
+// foreign occupied cell is reachable.
+template <int D>
+__device__ __forceinline__ bool window_clear(const OwnerGrid<D>& og, const std::uint16_t* __restrict__ owner,
+                                             const std::uint16_t* __restrict__ nbr3,
+                                             const std::uint16_t* __restrict__ nbr5, const double* c, double R,
+                                             std::uint32_t self) {
+  const double r = R * (1.0 + 1e-9) + og.margin;
+  int a[D];
+  int w = 0;
+  bool outside = false;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const double fa = floor((c[d] - r - og.g.lo[d]) * og.inv_edge);
+    const double fb = floor((c[d] + r - og.g.lo[d]) * og.inv_edge);
+    const double top = static_cast<double>(og.ldims[0][d] - 1);
+    if (!(fa <= fb)) return false;  // NaN
+    outside = outside || fb < 0.0 || fa > top;
+    a[d] = fa < 0.0 ? 0 : (fa > top ? og.ldims[0][d] - 1 : static_cast<int>(fa));
+    const int b = fb > top ? og.ldims[0][d] - 1 : (fb < 0.0 ? 0 : static_cast<int>(fb));
+    w = max(w, b - a[d]);
+  }
+  if (outside) return true;  // the range misses the grid on some axis: no cell is reachable
+  if (w > 4) return false;
+  const int h = w == 0 ? 0 : (w <= 2 ? 1 : 2);
+  int cm[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) cm[d] = min(a[d] + h, og.ldims[0][d] - 1);
+  const std::uint16_t* src = h == 0 ? owner : (h == 1 ? nbr3 : nbr5);
+  const std::uint16_t code = __ldg(src + og_index<D>(og, 0, cm));
+  return code == kOwnerEmpty || code == self;
+}
+
+// Leaf-cell range of the (inflated binary64) sphere, as og_sphere_hits_foreign
+// computes it: 0 = no cell reachable (negative), 1 = small range (spans <= 5,
+// cooperative scan), 2 = large / non-finite (pyramid descent).
+template <int D>
+__device__ __forceinline__ int leaf_range(const OwnerGrid<D>& og, const double* c, double r2, int* lo, int* span) {
+  if (isnan(r2)) return 0;
+  bool fin = isfinite(r2);
+#pragma unroll
+  for (int d = 0; d < D; ++d) fin = fin && isfinite(c[d]);
+  if (!fin) return 2;
+  const double r = sqrt(r2) * (1.0 + 1e-9) + og.margin;
+  int mode = 1;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const double fa = floor((c[d] - r - og.g.lo[d]) * og.inv_edge);
+    const double fb = floor((c[d] + r - og.g.lo[d]) * og.inv_edge);
+    const double top = static_cast<double>(og.ldims[0][d] - 1);
+    if (fb < 0.0 || fa > top) return 0;
+    lo[d] = fa < 0.0 ? 0 : static_cast<int>(fa);
+    const int hi = fb > top ? og.ldims[0][d] - 1 : static_cast<int>(fb);
+    span[d] = hi - lo[d] + 1;
+    if (span[d] > 5) mode = 2;
+  }
+  return mode;
+}
+
 __device__ __forceinline__ std::uint32_t part_of(const std::uint64_t* offs, std::uint32_t k, std::uint64_t s) {
   std::uint32_t lo = 0, hi = k;  // offs[lo] <= s < offs[hi]
   while (hi - lo > 1) {
@@ -519,6 +277,8 @@ struct BorderArgs {
   std::uint64_t S;
   int policy;
   const std::uint16_t* owner;
+  const std::uint16_t* nbr3;  // 3^D neighbourhood codes (grid policy prefilter)
+  const std::uint16_t* nbr5;  // 5^D neighbourhood codes
   const unsigned long long* pbbox;  // [k][2D] ordered (bbox policy)
   std::uint8_t* positive;
   std::uint8_t* vflags;
@@ -526,6 +286,7 @@ struct BorderArgs {
   std::uint32_t* inf_queue;
   unsigned* inf_count;
   unsigned* status;
+  unsigned long long* counters;  // [0] finite rows, [1] exact-stage rows, [2] positive (optional)
 };
 
 // bbox-policy root box of partition j: its point bbox snapped to the occupied
@@ -580,6 +341,16 @@ __global__ void __launch_bounds__(kBThreads) k_border_finite(BorderArgs a, const
     for (int j = 0; j <= D; ++j)
 #pragma unroll
       for (int d = 0; d < D; ++d) p[j][d] = a.xyz[std::size_t(v[j]) * D + d];
+    if (!a.spheres && a.policy == SBDT_POLICY_GRID && a.nbr3) {
+      // Prefilter: a binary32 sphere that provably encloses the binary64 one;
+      // if its cell range sits in a 5^D window free of foreign cells, s is
+      // negative exactly.
+      double cc[D], R;
+      if (enclosing_sphere_f32<D>(p, cc, &R) && window_clear<D>(og, a.owner, a.nbr3, a.nbr5, cc, R, self)) {
+        __stcs(a.positive + s, static_cast<std::uint8_t>(0));
+        continue;
+      }
+    }
     double c[D], r2;
     circumsphere_inflated<D>(p, c, &r2);
     if (a.spheres) {
@@ -588,11 +359,153 @@ __global__ void __launch_bounds__(kBThreads) k_border_finite(BorderArgs a, const
       a.spheres[s * (D + 1) + D] = r2;
     }
     const bool pos = (a.policy == SBDT_POLICY_BBOX) ? bbox_policy_sphere<D>(og, a, self, c, r2)
-                                                    : sphere_hits_foreign<D>(og, a.owner, c, r2, self);
+                                                    : og_sphere_hits_foreign<D>(og, a.owner, c, r2, self);
     __stcs(a.positive + s, static_cast<std::uint8_t>(pos ? 1 : 0));
     if (pos)
 #pragma unroll
       for (int j = 0; j <= D; ++j) a.vflags[v[j]] = 1;
+  }
+}
+
+// Grid policy, two-stage CTA pipeline over tiles of kTile simplices. The
+// simplices that survive stage A are compacted into a shared-memory queue, so
+// both stages run with all lanes busy (no divergence between cheap negatives
+// and exact candidates):
+//   A  all rows: binary32 enclosing sphere + the owner/3^D/5^D neighbourhood
+//      code of the window covering its cell range -> most simplices are proven
+//      negative with one 2-byte lookup and no binary64 arithmetic;
+//   C  candidates: the reference's binary64 circumsphere (exact operation
+//      order) and the exact pyramid descent (og_sphere_hits_foreign).
+// A only concludes "negative" for a sphere that contains the exact binary64
+// sphere, so the flags equal the exact test's.
+constexpr int kTile = 2048;
+
+
+template <int D>
+__global__ void __launch_bounds__(kBThreads) k_border_tiles(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp) {
+  __shared__ OwnerGrid<D> og;
+  __shared__ std::uint32_t qb[kTile];
+  __shared__ std::uint32_t qb_self[kTile];
+  __shared__ int nb;
+  extern __shared__ std::uint64_t s_off[];
+  if (threadIdx.x == 0) og = *ogp;
+  for (std::uint32_t j = threadIdx.x; j <= a.k; j += blockDim.x) s_off[j] = a.offsets[j];
+  __syncthreads();
+  const std::uint64_t tiles = (a.S + kTile - 1) / kTile;
+  for (std::uint64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    if (threadIdx.x == 0) nb = 0;
+    __syncthreads();
+    const std::uint64_t base = tile * kTile;
+    // ---- stage A
+    for (int t = threadIdx.x; t < kTile; t += blockDim.x) {
+      const std::uint64_t s = base + t;
+      if (s >= a.S) break;
+      std::uint32_t v[D + 1];
+#pragma unroll
+      for (int j = 0; j <= D; ++j) v[j] = __ldcs(a.verts + std::uint64_t(j) * a.S + s);
+      if (v[D] == kInfVertex) {
+        const unsigned slot = atomicAdd(a.inf_count, 1u);
+        a.inf_queue[slot] = static_cast<std::uint32_t>(s);
+        continue;
+      }
+      if (a.parity[s] == 0) atomicOr(a.status, kStDegenerate);
+      const std::uint32_t self = part_of(s_off, a.k, s);
+      double p[D + 1][D];
+#pragma unroll
+      for (int j = 0; j <= D; ++j)
+#pragma unroll
+        for (int d = 0; d < D; ++d) p[j][d] = a.xyz[std::size_t(v[j]) * D + d];
+      double cc[D], R;
+      if (enclosing_sphere_f32<D>(p, cc, &R)) {
+        if (window_clear<D>(og, a.owner, a.nbr3, a.nbr5, cc, R, self)) {
+          __stcs(a.positive + s, static_cast<std::uint8_t>(0));
+          continue;
+        }
+      }
+      {
+        const int q = atomicAdd(&nb, 1);
+        qb[q] = static_cast<std::uint32_t>(s);
+        qb_self[q] = self;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && a.counters) {
+      atomicAdd(&a.counters[1], static_cast<unsigned long long>(nb));
+      const std::uint64_t rows = (a.S - base) < std::uint64_t(kTile) ? (a.S - base) : std::uint64_t(kTile);
+      atomicAdd(&a.counters[0], static_cast<unsigned long long>(rows));
+    }
+    // ---- stage C: lane-parallel binary64 spheres, then one warp-cooperative
+    // leaf scan per candidate (lane = cell of the candidate's cell range).
+    const int nqb = nb;
+    const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    for (int base = warp * 32; base < nqb; base += blockDim.x) {
+      const int t = base + static_cast<int>(lane);
+      const bool has = t < nqb;
+      std::uint64_t s = 0;
+      std::uint32_t self = 0, v[D + 1];
+      double c[D], r2 = 0.0;
+      int lo[D], span[D];
+      int mode = 0;  // 0 none/negative, 1 cooperative scan, 2 solo descent
+      if (has) {
+        s = qb[t];
+        self = qb_self[t];
+#pragma unroll
+        for (int j = 0; j <= D; ++j) v[j] = a.verts[std::uint64_t(j) * a.S + s];
+        double p[D + 1][D];
+#pragma unroll
+        for (int j = 0; j <= D; ++j)
+#pragma unroll
+          for (int d = 0; d < D; ++d) p[j][d] = a.xyz[std::size_t(v[j]) * D + d];
+        circumsphere_inflated<D>(p, c, &r2);
+        mode = leaf_range<D>(og, c, r2, lo, span);
+      }
+      bool pos = false;
+      if (has && mode == 2) pos = og_sphere_hits_foreign<D>(og, a.owner, c, r2, self);
+      unsigned todo = __ballot_sync(0xffffffffu, mode == 1);
+      while (todo) {
+        const int l = __ffs(todo) - 1;
+        todo &= todo - 1;
+        double cl[D];
+        int lol[D], spl[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          cl[d] = __shfl_sync(0xffffffffu, c[d], l);
+          lol[d] = __shfl_sync(0xffffffffu, lo[d], l);
+          spl[d] = __shfl_sync(0xffffffffu, span[d], l);
+        }
+        const double rl = __shfl_sync(0xffffffffu, r2, l);
+        const std::uint32_t sl = __shfl_sync(0xffffffffu, self, l);
+        const int cells = D == 3 ? spl[0] * spl[1] * spl[2] : spl[0] * spl[1];
+        bool hit = false;
+        for (int i0 = 0; i0 < cells && !hit; i0 += 32) {
+          const int i = i0 + static_cast<int>(lane);
+          bool h = false;
+          if (i < cells) {
+            int cc[D], rem = i;
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+              cc[d] = lol[d] + rem % spl[d];
+              rem /= spl[d];
+            }
+            const std::uint16_t code = a.owner[og_index<D>(og, 0, cc)];
+            if (code != kOwnerEmpty && code != sl) {
+              double blo[D], bhi[D];
+              og_block_box<D>(og, 0, cc, blo, bhi);
+              h = box_sphere<D>(blo, bhi, cl, rl);
+            }
+          }
+          hit = __any_sync(0xffffffffu, h);
+        }
+        if (static_cast<int>(lane) == l) pos = hit;
+      }
+      if (has) {
+        __stcs(a.positive + s, static_cast<std::uint8_t>(pos ? 1 : 0));
+        if (pos)
+#pragma unroll
+          for (int j = 0; j <= D; ++j) a.vflags[v[j]] = 1;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -639,7 +552,7 @@ __global__ void __launch_bounds__(128) k_border_infinite(BorderArgs a, const Own
           pos = true;
       }
     } else {
-      pos = halfspace_hits_foreign<D>(og, a.owner, facet, inner_sign, self);
+      pos = og_halfspace_hits_foreign<D>(og, a.owner, facet, inner_sign, self);
     }
     a.positive[s] = pos ? 1 : 0;
     if (a.spheres)
@@ -727,7 +640,7 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   double scale = 1.0;
   for (int d = 0; d < D; ++d) scale /= cg;
   const unsigned long long cap = static_cast<unsigned long long>(4.0 * double(in->n) * scale) + 4096;
-  const unsigned long long owner_len = cap * 8 / 7 + 64 * kMaxLevels + 64;
+  const unsigned long long owner_len = 2 * cap + 64 * kMaxLevels + 4096;
   SBDT_WS(og, OwnerGrid<D>, "border.og", 1);
   SBDT_WS(owner, std::uint16_t, "border.owner", owner_len);
   SBDT_WS(bbox, unsigned long long, "border.bbox", 2 * D);
@@ -749,7 +662,7 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
     ctx->launches += 2;
     bb = bbox;
   }
-  k_owner_params<D><<<1, 1, 0, st>>>(bb, in->n, cg, cap, og, ctx->d_status);
+  k_owner_params<D><<<1, 1, 0, st>>>(bb, in->n, cg, cap, owner_len, og, ctx->d_status);
   SBDT_CUDA_TRY(cudaMemsetAsync(owner, 0xFF, sizeof(std::uint16_t) * owner_len, st));
   if (pbbox) {
     k_pbbox_init<<<(in->k * 2 * D + 255) / 256, 256, 0, st>>>(pbbox, in->k * 2 * D, D);
@@ -764,6 +677,31 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   k_owner_level<D><<<sms * 8, 256, 0, st>>>(og, owner, 1);
   k_owner_level<D><<<sms * 2, 256, 0, st>>>(og, owner, 2);
   k_owner_levels_tail<D><<<1, 1024, 0, st>>>(og, owner, 3);
+  std::uint16_t *nbr3 = nullptr, *nbr5 = nullptr;
+  if (in->policy == SBDT_POLICY_GRID) {
+    SBDT_WS(n3, std::uint16_t, "border.nbr3", owner_len);
+    SBDT_WS(n5, std::uint16_t, "border.nbr5", owner_len);
+    SBDT_WS(tmp, std::uint16_t, "border.nbrtmp", owner_len);
+    nbr3 = n3;
+    nbr5 = n5;
+    const unsigned nbk = static_cast<unsigned>(sms) * 8;
+    // separable W=1 passes: owner -> nbr3 -> nbr5 (ping-pong through tmp)
+    std::uint16_t* src = owner;
+    for (int rep = 0; rep < 2; ++rep) {
+      std::uint16_t* out = rep == 0 ? nbr3 : nbr5;
+      if constexpr (D == 3) {
+        k_nbr_pass<D><<<nbk, 256, 0, st>>>(og, src, tmp, 0);
+        k_nbr_pass<D><<<nbk, 256, 0, st>>>(og, tmp, out, 1);
+        k_nbr_pass<D><<<nbk, 256, 0, st>>>(og, out, tmp, 2);
+        SBDT_CUDA_TRY(cudaMemcpyAsync(out, tmp, sizeof(std::uint16_t) * owner_len, cudaMemcpyDeviceToDevice, st));
+      } else {
+        k_nbr_pass<D><<<nbk, 256, 0, st>>>(og, src, tmp, 0);
+        k_nbr_pass<D><<<nbk, 256, 0, st>>>(og, tmp, out, 1);
+      }
+      src = out;
+    }
+    ctx->launches += 2 * D;
+  }
   ctx->launches += 6;
 
   SBDT_CUDA_TRY(cudaMemsetAsync(in->d_vertex_flags, 0, in->n, st));
@@ -780,6 +718,8 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   a.S = in->S;
   a.policy = in->policy;
   a.owner = owner;
+  a.nbr3 = nbr3;
+  a.nbr5 = nbr5;
   a.pbbox = pbbox;
   a.positive = in->d_positive;
   a.vflags = in->d_vertex_flags;
@@ -787,13 +727,25 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   a.inf_queue = infq;
   a.inf_count = infc;
   a.status = ctx->d_status;
+  a.counters = nullptr;
+  if (ctx->timing) {
+    SBDT_WS(cnt, unsigned long long, "border.counters", 8);
+    SBDT_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 8, st));
+    a.counters = cnt;
+  }
   const std::size_t offs_sh = sizeof(std::uint64_t) * (in->k + 1);
   {
     const std::uint64_t want = (in->S + kBThreads - 1) / kBThreads;
     const unsigned blocks = static_cast<unsigned>(want < std::uint64_t(sms) * 32 ? want : std::uint64_t(sms) * 32);
     {
       StageTimer t(ctx, "border.finite");
-      if (blocks > 0) k_border_finite<D><<<blocks, kBThreads, offs_sh, st>>>(a, og);
+      if (in->policy == SBDT_POLICY_GRID && !in->d_spheres && nbr3) {
+        const std::uint64_t tiles = (in->S + kTile - 1) / kTile;
+        const unsigned tb = static_cast<unsigned>(tiles < std::uint64_t(sms) * 4 ? tiles : std::uint64_t(sms) * 4);
+        if (tb > 0) k_border_tiles<D><<<tb, kBThreads, offs_sh, st>>>(a, og);
+      } else if (blocks > 0) {
+        k_border_finite<D><<<blocks, kBThreads, offs_sh, st>>>(a, og);
+      }
     }
     {
       StageTimer t(ctx, "border.infinite");

@@ -1,0 +1,513 @@
+// Owner grid (K4): the GridIndex of every partition at once as one uint16 code
+// per cell of the global uniform grid — EMPTY, a single owning partition, or
+// MULTI — plus a pyramid of coarser levels with the same code per block.
+//
+// Tiled layout: per-axis fanout F (4 in 3D, 8 in 2D), 64 children per block,
+// and the 64 children of a block are CONTIGUOUS (one 128-byte line). Level L
+// (below the top) is stored block-major in the tiling of level L+1:
+//   index(L, c) = loff[L] + lin(ldims[L+1], c >> sh) * 64 + sub(c & (F-1)).
+// Expanding a block is then one coalesced 128-byte load, and the foreign
+// children (code not in {EMPTY, self}) come out of per-half-word SIMD
+// compares as a 64-bit mask. Padding cells (grid not a multiple of F) are
+// EMPTY and are never visited.
+//
+// Exactness of the descent: a block box is
+// the exact union of its cells' boxes (cell_lo is monotone in the index), the
+// box_sphere_overlap and halfspace tests are monotone under box containment
+// in binary64 / exact arithmetic, and "every sub-box passes" (far corner
+// inside the sphere, every corner strictly outside the halfspace) implies the
+// leaf test for each occupied leaf below. So the descent answers exactly the
+// SPEC's "some occupied leaf cell of another partition passes the test".
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace sbdt_gpu {
+
+template <int D>
+struct OwnerGrid {
+  Grid<D> g;
+  double inv_edge;
+  double margin;
+  int levels;  // levels incl. leaf level 0; the top level has exactly one block
+  int shift;   // log2 per-axis fanout
+  int ldims[kMaxLevels][D];
+  unsigned long long loff[kMaxLevels + 1];
+};
+
+template <int D>
+constexpr int og_shift() {
+  return D == 3 ? 2 : 3;
+}
+template <int D>
+constexpr int og_fan() {
+  return 1 << og_shift<D>();
+}
+
+template <int D>
+__host__ __device__ __forceinline__ unsigned long long lin_i(const int* dims, const int* c) {
+  unsigned long long id = static_cast<unsigned>(c[D - 1]);
+#pragma unroll
+  for (int d = D - 2; d >= 0; --d) id = id * static_cast<unsigned>(dims[d]) + static_cast<unsigned>(c[d]);
+  return id;
+}
+
+template <int D>
+__device__ __forceinline__ unsigned long long og_index(const OwnerGrid<D>& og, int L, const int* c) {
+  if (L == og.levels - 1) return og.loff[L];
+  constexpr int sh = og_shift<D>();
+  constexpr int F = og_fan<D>();
+  int blk[D];
+  int sub = 0;
+#pragma unroll
+  for (int d = 0; d < D; ++d) blk[d] = c[d] >> sh;
+  if constexpr (D == 3) sub = (c[0] & (F - 1)) | ((c[1] & (F - 1)) << 2) | ((c[2] & (F - 1)) << 4);
+  else sub = (c[0] & (F - 1)) | ((c[1] & (F - 1)) << 3);
+  return og.loff[L] + lin_i<D>(og.ldims[L + 1], blk) * 64 + static_cast<unsigned>(sub);
+}
+
+// child j (0..63) of block coords b, at the child level
+template <int D>
+__device__ __forceinline__ void og_child(const int* b, int j, int* c) {
+  if constexpr (D == 3) {
+    c[0] = (b[0] << 2) | (j & 3);
+    c[1] = (b[1] << 2) | ((j >> 2) & 3);
+    c[2] = (b[2] << 2) | (j >> 4);
+  } else {
+    c[0] = (b[0] << 3) | (j & 7);
+    c[1] = (b[1] << 3) | (j >> 3);
+  }
+}
+
+// Grid parameters from the global bbox: edge = c_G (V/n)^(1/D) (SPEC.md:403 /
+// build_grid_index post), origin = bbox lo, dims = floor(ext/edge)+1.
+template <int D>
+__global__ void k_owner_params(const unsigned long long* bbox, std::uint64_t n, double c_G, unsigned long long cap_cells,
+                               unsigned long long cap_entries, OwnerGrid<D>* og, unsigned* status) {
+  double lo[D], hi[D], vol = 1.0, ext_max = 0.0, mag = 0.0;
+  for (int d = 0; d < D; ++d) {
+    lo[d] = ordered_to_dbl(bbox[d]);
+    hi[d] = ordered_to_dbl(bbox[D + d]);
+    vol *= (hi[d] - lo[d]);
+    ext_max = fmax(ext_max, hi[d] - lo[d]);
+    mag = fmax(mag, fmax(fabs(lo[d]), fabs(hi[d])));
+  }
+  const double per = vol / static_cast<double>(n);
+  const double e = c_G * ((D == 2) ? sqrt(per) : cbrt_det(per));
+  unsigned long long cells = 1;
+  bool bad = !(e > 0.0);
+  for (int d = 0; d < D; ++d) {
+    og->g.lo[d] = lo[d];
+    const double f = bad ? 0.0 : floor((hi[d] - lo[d]) / e);
+    if (!(f < 1.0e9)) bad = true;
+    og->g.dims[d] = bad ? 1 : static_cast<long long>(f) + 1;
+    cells *= static_cast<unsigned long long>(og->g.dims[d]);
+  }
+  if (bad || cells > cap_cells) {
+    atomicOr(status, kStGridCap);
+    for (int d = 0; d < D; ++d) og->g.dims[d] = 1;
+  }
+  og->g.edge = bad ? 1.0 : e;
+  og->inv_edge = 1.0 / og->g.edge;
+  og->margin = 1e-9 * (mag + ext_max + og->g.edge);
+  constexpr int sh = og_shift<D>();
+  og->shift = sh;
+  int L = 0;
+  for (;;) {
+    bool top = true;
+    for (int d = 0; d < D; ++d) {
+      og->ldims[L][d] = static_cast<int>(((og->g.dims[d] - 1) >> (L * sh)) + 1);
+      top = top && og->ldims[L][d] == 1;
+    }
+    ++L;
+    if (top || L == kMaxLevels) break;
+  }
+  og->levels = L;
+  unsigned long long off = 0;
+  for (int l = 0; l < L; ++l) {
+    og->loff[l] = off;
+    unsigned long long cnt = 64;
+    if (l == L - 1) cnt = 1;
+    else
+      for (int d = 0; d < D; ++d) cnt *= static_cast<unsigned long long>(og->ldims[l + 1][d]);
+    off += cnt;
+  }
+  og->loff[L] = off;
+  if (off > cap_entries) {
+    atomicOr(status, kStGridCap);
+    og->levels = 1;  // unusable; the call reports SBDT_ERR_RANGE
+    og->loff[1] = 1;
+  }
+}
+
+// Leaf marking: owner code per occupied cell (CAS on 16-bit words).
+template <int D>
+__global__ void k_owner_mark(const double* __restrict__ xyz, const std::uint32_t* __restrict__ labels, std::uint64_t n,
+                             const OwnerGrid<D>* __restrict__ ogp, std::uint16_t* __restrict__ owner,
+                             unsigned long long* __restrict__ pbbox, std::uint32_t k) {
+  __shared__ OwnerGrid<D> og;
+  extern __shared__ unsigned long long s_pb[];  // [k][2D] when pbbox != nullptr
+  if (threadIdx.x == 0) og = *ogp;
+  if (pbbox)
+    for (std::uint32_t j = threadIdx.x; j < k * 2 * D; j += blockDim.x)
+      s_pb[j] = ((j % (2 * D)) < D) ? 0xFFFFFFFFFFFFFFFFULL : 0ULL;
+  __syncthreads();
+  for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += std::uint64_t(gridDim.x) * blockDim.x) {
+    double x[D];
+    int c[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      x[d] = xyz[i * D + d];
+      c[d] = static_cast<int>(cell_coord<D>(og.g, x[d], d));
+    }
+    const std::uint32_t lab = labels[i];
+    std::uint16_t* slot = owner + og_index<D>(og, 0, c);
+    unsigned short old = *slot;
+    while (old != lab && old != kOwnerMulti) {
+      const unsigned short nv = (old == kOwnerEmpty) ? static_cast<unsigned short>(lab) : kOwnerMulti;
+      const unsigned short prev = atomicCAS(reinterpret_cast<unsigned short*>(slot), old, nv);
+      if (prev == old) break;
+      old = prev;
+    }
+    if (pbbox) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        atomicMin(&s_pb[lab * 2 * D + d], dbl_to_ordered(x[d]));
+        atomicMax(&s_pb[lab * 2 * D + D + d], dbl_to_ordered(x[d]));
+      }
+    }
+  }
+  if (pbbox) {
+    __syncthreads();
+    for (std::uint32_t j = threadIdx.x; j < k * 2 * D; j += blockDim.x) {
+      if ((j % (2 * D)) < D) atomicMin(&pbbox[j], s_pb[j]);
+      else atomicMax(&pbbox[j], s_pb[j]);
+    }
+  }
+}
+
+__device__ __forceinline__ std::uint16_t og_combine(std::uint16_t a, std::uint16_t b) {
+  if (a == kOwnerEmpty) return b;
+  if (b == kOwnerEmpty) return a;
+  return a == b ? a : kOwnerMulti;
+}
+
+// Code of block `id` (linear in ldims[L]) at level L >= 1 from its 64
+// contiguous children at level L-1.
+template <int D>
+__device__ __forceinline__ void og_build_block(const OwnerGrid<D>& og, std::uint16_t* owner, int L, unsigned long long id) {
+  int c[D];
+  unsigned long long rem = id;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    c[d] = static_cast<int>(rem % static_cast<unsigned>(og.ldims[L][d]));
+    rem /= static_cast<unsigned>(og.ldims[L][d]);
+  }
+  const uint4* ch = reinterpret_cast<const uint4*>(owner + og.loff[L - 1] + id * 64);
+  std::uint16_t code = kOwnerEmpty;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint4 v = ch[q];
+    const unsigned w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      code = og_combine(code, static_cast<std::uint16_t>(w[t] & 0xFFFFu));
+      code = og_combine(code, static_cast<std::uint16_t>(w[t] >> 16));
+    }
+  }
+  owner[og_index<D>(og, L, c)] = code;
+}
+
+template <int D>
+__global__ void k_owner_level(const OwnerGrid<D>* __restrict__ ogp, std::uint16_t* __restrict__ owner, int L) {
+  __shared__ OwnerGrid<D> og;
+  if (threadIdx.x == 0) og = *ogp;
+  __syncthreads();
+  if (L >= og.levels) return;
+  unsigned long long cnt = 1;
+#pragma unroll
+  for (int d = 0; d < D; ++d) cnt *= static_cast<unsigned>(og.ldims[L][d]);
+  for (unsigned long long id = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; id < cnt;
+       id += static_cast<unsigned long long>(gridDim.x) * blockDim.x)
+    og_build_block<D>(og, owner, L, id);
+}
+
+template <int D>
+__global__ void k_owner_levels_tail(const OwnerGrid<D>* __restrict__ ogp, std::uint16_t* __restrict__ owner, int L0) {
+  __shared__ OwnerGrid<D> og;
+  if (threadIdx.x == 0) og = *ogp;
+  __syncthreads();
+  for (int L = L0; L < og.levels; ++L) {
+    unsigned long long cnt = 1;
+#pragma unroll
+    for (int d = 0; d < D; ++d) cnt *= static_cast<unsigned>(og.ldims[L][d]);
+    for (unsigned long long id = threadIdx.x; id < cnt; id += blockDim.x) og_build_block<D>(og, owner, L, id);
+    __syncthreads();
+  }
+}
+
+// ---- neighbourhood codes -----------------------------------------------------------
+// nbr3[c] / nbr5[c] = combine of the leaf codes in the 3^D / 5^D window
+// around c, clipped to the grid. The combine is a semilattice (EMPTY
+// identity, MULTI absorbing), so the box filter is separable (one 1-D pass of
+// half-width 1 per axis), and a 3-window of 3-windows is the 5-window.
+constexpr int kNbrW = 1;
+
+template <int D>
+__global__ void k_nbr_pass(const OwnerGrid<D>* __restrict__ ogp, const std::uint16_t* __restrict__ src,
+                           std::uint16_t* __restrict__ dst, int axis) {
+  __shared__ OwnerGrid<D> og;
+  if (threadIdx.x == 0) og = *ogp;
+  __syncthreads();
+  unsigned long long cnt = 1;
+#pragma unroll
+  for (int d = 0; d < D; ++d) cnt *= static_cast<unsigned>(og.ldims[0][d]);
+  for (unsigned long long id = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; id < cnt;
+       id += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+    int c[D];
+    unsigned long long rem = id;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      c[d] = static_cast<int>(rem % static_cast<unsigned>(og.ldims[0][d]));
+      rem /= static_cast<unsigned>(og.ldims[0][d]);
+    }
+    const int c0 = c[axis];
+    std::uint16_t code = kOwnerEmpty;
+    for (int t = max(c0 - kNbrW, 0); t <= min(c0 + kNbrW, og.ldims[0][axis] - 1); ++t) {
+      c[axis] = t;
+      code = og_combine(code, src[og_index<D>(og, 0, c)]);
+    }
+    c[axis] = c0;
+    dst[og_index<D>(og, 0, c)] = code;
+  }
+}
+
+// ---- queries ----------------------------------------------------------------------
+template <int D>
+__device__ __forceinline__ void og_block_box(const OwnerGrid<D>& og, int L, const int* c, double* blo, double* bhi) {
+  const int s = L * og_shift<D>();
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const long long first = static_cast<long long>(c[d]) << s;
+    long long last1 = static_cast<long long>(c[d] + 1) << s;
+    if (last1 > og.g.dims[d]) last1 = og.g.dims[d];
+    blo[d] = cell_lo<D>(og.g, first, d);
+    bhi[d] = cell_lo<D>(og.g, last1, d);
+  }
+}
+
+// 64-bit mask of the children of block b (level L >= 1) whose code is
+// foreign (not EMPTY, not self) and whose coordinates lie in [ra, rb]
+// (child-level range) — one 128-byte load.
+template <int D>
+__device__ __forceinline__ unsigned long long og_child_mask(const OwnerGrid<D>& og, const std::uint16_t* __restrict__ owner,
+                                                            int L, const int* b, std::uint32_t self, const int* ra,
+                                                            const int* rb) {
+  const uint4* ch = reinterpret_cast<const uint4*>(owner + og.loff[L - 1] + lin_i<D>(og.ldims[L], b) * 64);
+  const unsigned selfx2 = (self & 0xFFFFu) | (self << 16);
+  unsigned long long m = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint4 v = __ldg(ch + q);
+    const unsigned w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const unsigned f = __vcmpne2(w[t], 0xFFFFFFFFu) & __vcmpne2(w[t], selfx2);
+      const unsigned long long bits = (f & 1u) | ((f >> 15) & 2u);
+      m |= bits << (2 * (4 * q + t));
+    }
+  }
+  // range restriction
+  constexpr int F = og_fan<D>();
+  unsigned long long rm = 0;
+  int lo[D], hi[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    lo[d] = max(ra[d] - b[d] * F, 0);
+    hi[d] = min(rb[d] - b[d] * F, F - 1);
+    if (lo[d] > hi[d]) return 0;
+  }
+  if constexpr (D == 3) {
+    const unsigned long long row = ((1ULL << (hi[0] - lo[0] + 1)) - 1) << lo[0];
+    for (int z = lo[2]; z <= hi[2]; ++z)
+      for (int y = lo[1]; y <= hi[1]; ++y) rm |= row << (4 * y + 16 * z);
+  } else {
+    const unsigned long long row = ((1ULL << (hi[0] - lo[0] + 1)) - 1) << lo[0];
+    for (int y = lo[1]; y <= hi[1]; ++y) rm |= row << (8 * y);
+  }
+  return m & rm;
+}
+
+// Depth-first descent. Start blocks: the blocks of level L0 covering the leaf
+// range [a, b] (at most two per axis). test(blo, bhi) returns 0 reject,
+// 1 descend, 2 accept (every sub-box passes). A passing leaf is a hit.
+template <int D, class Test>
+__device__ bool og_descend(const OwnerGrid<D>& og, const std::uint16_t* __restrict__ owner, std::uint32_t self, int L0,
+                           const int* a, const int* b, const Test& test, unsigned long long* stats = nullptr) {
+  unsigned n_tests = 0, n_masks = 0;
+  struct Flush {
+    unsigned long long* st;
+    unsigned& t;
+    unsigned& m;
+    int L;
+    __device__ ~Flush() {
+      if (st) {
+        atomicAdd(&st[2], static_cast<unsigned long long>(t));
+        atomicAdd(&st[3], static_cast<unsigned long long>(m));
+        atomicAdd(&st[4 + (L > 3 ? 3 : L)], 1ULL);
+      }
+    }
+  } flush{stats, n_tests, n_masks, L0};
+  struct Frame {
+    unsigned long long mask;
+    int c[D];
+    int level;
+  };
+  Frame fr[kMaxLevels];  // depth <= levels - 1
+  int s0[D], n0[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    s0[d] = a[d] >> (L0 * og.shift);
+    n0[d] = (b[d] >> (L0 * og.shift)) - s0[d] + 1;
+  }
+  const int total = D == 3 ? n0[0] * n0[1] * n0[2] : n0[0] * n0[1];
+  for (int t = 0; t < total; ++t) {
+    int cc[D], rem = t;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      cc[d] = s0[d] + rem % n0[d];
+      rem /= n0[d];
+    }
+    const std::uint16_t code = owner[og_index<D>(og, L0, cc)];
+    if (code == kOwnerEmpty || code == self) continue;
+    double blo[D], bhi[D];
+    og_block_box<D>(og, L0, cc, blo, bhi);
+    ++n_tests;
+    const int r = test(blo, bhi);
+    if (r == 0) continue;
+    if (L0 == 0 || r == 2) return true;
+    // explore this start block
+    int depth = 0;
+    {
+      const int cl = L0 - 1, csh = cl * og.shift;
+      int ra[D], rb[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) ra[d] = a[d] >> csh, rb[d] = b[d] >> csh;
+      ++n_masks;
+      fr[0].mask = og_child_mask<D>(og, owner, L0, cc, self, ra, rb);
+#pragma unroll
+      for (int d = 0; d < D; ++d) fr[0].c[d] = cc[d];
+      fr[0].level = L0;
+      depth = 1;
+    }
+    while (depth > 0) {
+      Frame& f = fr[depth - 1];
+      if (f.mask == 0) {
+        --depth;
+        continue;
+      }
+      const int j = __ffsll(static_cast<long long>(f.mask)) - 1;
+      f.mask &= f.mask - 1;
+      const int lv = f.level - 1;
+      int ch[D];
+      og_child<D>(f.c, j, ch);
+      double blo[D], bhi[D];
+      og_block_box<D>(og, lv, ch, blo, bhi);
+      ++n_tests;
+      const int r2 = test(blo, bhi);
+      if (r2 == 0) continue;
+      if (lv == 0 || r2 == 2) return true;
+      const int cl = lv - 1, csh = cl * og.shift;
+      int ra[D], rb[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) ra[d] = a[d] >> csh, rb[d] = b[d] >> csh;
+      Frame& g2 = fr[depth];
+      ++n_masks;
+      g2.mask = og_child_mask<D>(og, owner, lv, ch, self, ra, rb);
+#pragma unroll
+      for (int d = 0; d < D; ++d) g2.c[d] = ch[d];
+      g2.level = lv;
+      if (g2.mask) ++depth;
+    }
+  }
+  return false;
+}
+
+// true iff some cell with owner code not in {EMPTY, self} overlaps the sphere
+// (box_sphere_overlap, geometry.hpp:187-201).
+template <int D>
+__device__ __forceinline__ bool og_sphere_hits_foreign(const OwnerGrid<D>& og, const std::uint16_t* __restrict__ owner,
+                                                       const double* c, double r2, std::uint32_t self,
+                                                       unsigned long long* stats = nullptr) {
+  if (isnan(r2)) return false;
+  bool fin = isfinite(r2);
+#pragma unroll
+  for (int d = 0; d < D; ++d) fin = fin && isfinite(c[d]);
+  int a[D], b[D];
+  if (fin) {
+    // Conservative leaf range; the margin (1e-9 relative) dominates the
+    // rounding of this multiply-by-inverse binning.
+    const double r = sqrt(r2) * (1.0 + 1e-9) + og.margin;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const double fa = floor((c[d] - r - og.g.lo[d]) * og.inv_edge);
+      const double fb = floor((c[d] + r - og.g.lo[d]) * og.inv_edge);
+      const double top = static_cast<double>(og.ldims[0][d] - 1);
+      if (fb < 0.0 || fa > top) return false;
+      a[d] = fa < 0.0 ? 0 : static_cast<int>(fa);
+      b[d] = fb > top ? og.ldims[0][d] - 1 : static_cast<int>(fb);
+    }
+  } else {
+#pragma unroll
+    for (int d = 0; d < D; ++d) a[d] = 0, b[d] = og.ldims[0][d] - 1;
+  }
+  int L = 0;
+  for (; L < og.levels - 1; ++L) {
+    bool ok = true;
+#pragma unroll
+    for (int d = 0; d < D; ++d) ok = ok && ((b[d] >> (L * og.shift)) - (a[d] >> (L * og.shift)) <= 1);
+    if (ok) break;
+  }
+  return og_descend<D>(og, owner, self, L, a, b, [&](const double* blo, const double* bhi) {
+    if (!box_sphere<D>(blo, bhi, c, r2)) return 0;
+    return box_inside_sphere<D>(blo, bhi, c, r2) ? 2 : 1;
+  }, stats);
+}
+
+// Halfspace variant (halfspace_box_overlap, geometry.cpp:329-345): test = some
+// box corner strictly on the outer side of the hull facet plane (exact
+// orient), accept = every corner strictly outside.
+template <int D>
+__device__ int corners_outside(const double* const* facet, int inner_sign, const double* blo, const double* bhi) {
+  const double* pts[D + 1];
+#pragma unroll
+  for (int i = 0; i < D; ++i) pts[i] = facet[i];
+  double corner[D];
+  pts[D] = corner;
+  int outside = 0;
+  for (unsigned cm = 0; cm < (1u << D); ++cm) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) corner[d] = (cm & (1u << d)) ? bhi[d] : blo[d];
+    const int s = orient_dev<D>(pts);
+    if (s != 0 && s != inner_sign) ++outside;
+  }
+  return outside;
+}
+
+template <int D>
+__device__ bool og_halfspace_hits_foreign(const OwnerGrid<D>& og, const std::uint16_t* __restrict__ owner,
+                                          const double* const* facet, int inner_sign, std::uint32_t self) {
+  int a[D], b[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) a[d] = 0, b[d] = og.ldims[0][d] - 1;
+  return og_descend<D>(og, owner, self, og.levels - 1, a, b, [&](const double* blo, const double* bhi) {
+    const int out = corners_outside<D>(facet, inner_sign, blo, bhi);
+    if (out == 0) return 0;
+    return out == (1 << D) ? 2 : 1;
+  });
+}
+
+}  // namespace sbdt_gpu

@@ -1,0 +1,439 @@
+// Voronoi label table (VLT): the assignment's per-point work becomes one table
+// lookup for most points. Included by assign.cu (needs SampleRec, SampleGrid,
+// nearest_label_ring, bbox_flush).
+//
+// Every grid cell (~2 samples) is split into F^D fine cells. For each fine
+// cell a CONSERVATIVE candidate set of samples is computed: every sample that
+// can be the binary64 argmin (squared_distance, lowest pid on ties) for SOME
+// point binned into the cell is kept. A sample s is dropped only when one
+// dominator t is provably strictly closer over the whole (inflated) cell box:
+//   |x-s|^2 - |x-t|^2 = F0 + 2 y.(t-s) >= F0 - 2 sum |t_d - s_d| hw_d  (y = x - c)
+// must exceed 1e-5 * ((|c-s|+H)^2 + (|c-t|+H)^2); the test runs in binary32 on
+// coordinates relative to the box centre, and 1e-5 is ~100x the total
+// binary32 rounding of the inputs and of the test. Dropping is
+// thus safe; keeping extra samples only costs time.
+//
+// Record per fine cell (u32 head): count 0 -> UNIFORM (label << 8), all
+// candidates share one label; 1..kSlots -> candidate list in the cell's slab
+// slot (16-byte entries: binary32 coordinates relative to the fine-cell centre
+// + sample index); kOverflow -> the point is queued for the exact ring search.
+// Point decision: binary32 distances with a rigorous per-candidate error bound
+// pick the winner when the gap exceeds both bounds; otherwise the tied
+// candidates are compared exactly in binary64 (reference formula + pid).
+#pragma once
+
+namespace sbdt_gpu {
+
+constexpr int kSlots = 12;
+constexpr std::uint32_t kHeadOverflow = 15u;
+constexpr int kVltWarps = 4;
+constexpr int kVltCap = 192;
+
+struct __align__(16) VltEntry {
+  float r[3];          // sample - fine-cell centre (binary32)
+  std::uint32_t idx;   // index into the cell-sorted SampleRec array
+};
+
+template <int D>
+struct FineGeom {
+  double c[D];
+  float hw[D];
+  float H;
+};
+
+// binary32 dominance: true iff s (rel rs) is never the argmin in the box
+// (centre c, half-widths hw, half-diagonal H) because t (rel rt) wins.
+template <int D>
+__device__ __forceinline__ bool dominated_f(const float* rs, const float* rt, const float* hw, float H) {
+  float ds = 0.f, dt = 0.f, slope = 0.f;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    ds = __fadd_rn(ds, __fmul_rn(rs[d], rs[d]));
+    dt = __fadd_rn(dt, __fmul_rn(rt[d], rt[d]));
+    slope = __fadd_rn(slope, __fmul_rn(fabsf(__fsub_rn(rt[d], rs[d])), hw[d]));
+  }
+  const float fmin_ = __fsub_rn(__fsub_rn(ds, dt), __fmul_rn(2.f, slope));
+  const float a = __fadd_rn(sqrtf(ds), H), b = __fadd_rn(sqrtf(dt), H);
+  return fmin_ > 1e-5f * (a * a + b * b);
+}
+
+// One warp per grid cell: coarse candidates (radius + dominance against the
+// sample nearest to the cell centre), then per fine cell the nearest coarse
+// candidate as dominator.
+template <int D>
+__global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D>* __restrict__ sgp,
+                                                              const std::uint32_t* __restrict__ starts,
+                                                              const SampleRec* __restrict__ sorted,
+                                                              std::uint32_t* __restrict__ heads,
+                                                              VltEntry* __restrict__ slab, unsigned* __restrict__ stats) {
+  __shared__ SampleGrid<D> sg;
+  __shared__ std::uint32_t s_idx[kVltWarps][kVltCap];
+  __shared__ float s_rel[kVltWarps][kVltCap][D];  // relative to the coarse centre
+  __shared__ std::uint32_t s_lab[kVltWarps][kVltCap];
+  __shared__ int s_cnt[kVltWarps];
+  if (threadIdx.x == 0) sg = *sgp;
+  __syncthreads();
+  const Grid<D>& g = sg.g;
+  const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  constexpr int F = fine_factor<D>();
+  constexpr int FC = fine_per_cell<D>();
+  unsigned st_uniform = 0, st_list = 0, st_over = 0;
+  const long long cells = static_cast<long long>(sg.cells);
+  for (long long cell = static_cast<long long>(blockIdx.x) * kVltWarps + warp; cell < cells;
+       cell += static_cast<long long>(gridDim.x) * kVltWarps) {
+    int cc[D];
+    {
+      long long rem = cell;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        cc[d] = static_cast<int>(rem % g.dims[d]);
+        rem /= g.dims[d];
+      }
+    }
+    double c[D];
+    float hw[D];
+    float H2 = 0.f;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const double lo = cell_lo<D>(g, cc[d], d), hi = cell_lo<D>(g, cc[d] + 1, d);
+      c[d] = 0.5 * (lo + hi);
+      // binary32 half-width rounded up, plus the coarse inflation
+      hw[d] = __double2float_ru(0.5 * (hi - lo) + sg.delta_c);
+      H2 = __fadd_ru(H2, __fmul_ru(hw[d], hw[d]));
+    }
+    const float H = __fsqrt_ru(H2);
+    // (a) dominator: nearest sample to the centre in growing rings
+    double bd = INFINITY;
+    std::uint32_t bi = 0xFFFFFFFFu;
+    for (int r = 1;; ++r) {
+      int lo_c[D], span[D], count = 1;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        lo_c[d] = max(cc[d] - r, 0);
+        span[d] = min(cc[d] + r, static_cast<int>(g.dims[d]) - 1) - lo_c[d] + 1;
+        count *= span[d];
+      }
+      for (int t = lane; t < count; t += 32) {
+        int rem = t, q[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          q[d] = lo_c[d] + rem % span[d];
+          rem /= span[d];
+        }
+        long long qc = q[D - 1];
+#pragma unroll
+        for (int d = D - 2; d >= 0; --d) qc = qc * g.dims[d] + q[d];
+        for (std::uint32_t s = starts[qc], e = starts[qc + 1]; s < e; ++s) {
+          const double d2 = sqdist<D>(c, sorted[s].x);
+          if (d2 < bd || (d2 == bd && s < bi)) {
+            bd = d2;
+            bi = s;
+          }
+        }
+      }
+      warp_argmin<D>(bd, bi);
+      if (bi != 0xFFFFFFFFu) break;
+      bool whole = true;
+#pragma unroll
+      for (int d = 0; d < D; ++d) whole = whole && (cc[d] - r <= 0) && (cc[d] + r >= g.dims[d] - 1);
+      if (whole) break;
+    }
+    // (b) coarse candidates within R = |c - s0| + 2H (+ margins)
+    float r0[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) r0[d] = static_cast<float>(sorted[bi].x[d] - c[d]);
+    const double R = (sqrt(bd) + 2.0 * static_cast<double>(H)) * (1.0 + 1e-6) + sg.margin;
+    const double R2 = R * R;
+    if (lane == 0) s_cnt[warp] = 0;
+    __syncwarp();
+    {
+      int lo_c[D], span[D], count = 1;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const int a = max(static_cast<int>(floor((c[d] - R - g.lo[d]) / g.edge)), 0);
+        const int b = min(static_cast<int>(floor((c[d] + R - g.lo[d]) / g.edge)), static_cast<int>(g.dims[d]) - 1);
+        lo_c[d] = a;
+        span[d] = b - a + 1;
+        count *= span[d];
+      }
+      for (int t0 = 0; t0 < count; t0 += 32) {
+        const int t = t0 + static_cast<int>(lane);
+        std::uint32_t sb = 0, se = 0;
+        if (t < count) {
+          int rem = t, q[D];
+#pragma unroll
+          for (int d = 0; d < D; ++d) {
+            q[d] = lo_c[d] + rem % span[d];
+            rem /= span[d];
+          }
+          long long qc = q[D - 1];
+#pragma unroll
+          for (int d = D - 2; d >= 0; --d) qc = qc * g.dims[d] + q[d];
+          sb = starts[qc];
+          se = starts[qc + 1];
+        }
+        for (std::uint32_t s = sb; s < se; ++s) {
+          const SampleRec rec = sorted[s];
+          const double d2 = sqdist<D>(c, rec.x);
+          if (d2 > R2) continue;
+          float rs[D];
+#pragma unroll
+          for (int d = 0; d < D; ++d) rs[d] = static_cast<float>(rec.x[d] - c[d]);
+          if (s != bi && dominated_f<D>(rs, r0, hw, H)) continue;
+          const int slot = atomicAdd(&s_cnt[warp], 1);
+          if (slot < kVltCap) {
+            s_idx[warp][slot] = s;
+            s_lab[warp][slot] = rec.label;
+#pragma unroll
+            for (int d = 0; d < D; ++d) s_rel[warp][slot][d] = rs[d];
+          }
+        }
+      }
+    }
+    __syncwarp();
+    const int ncand = s_cnt[warp];
+    // (c) fine cells
+    for (int f = 0; f < FC; ++f) {
+      int fi[D];
+      {
+        int rem = f;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          fi[d] = cc[d] * F + rem % F;
+          rem /= F;
+        }
+      }
+      const long long fid = cell * FC + f;
+      std::uint32_t head = kHeadOverflow;
+      if (ncand <= kVltCap) {
+        // fine box centre/half-widths, and the offset of its centre from the coarse centre
+        double fc[D];
+        float fhw[D], off[D];
+        float fH2 = 0.f;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const double lo = g.lo[d] + static_cast<double>(fi[d]) * sg.ef;
+          const double hi = g.lo[d] + static_cast<double>(fi[d] + 1) * sg.ef;
+          fc[d] = 0.5 * (lo + hi);
+          fhw[d] = __double2float_ru(0.5 * (hi - lo) + sg.delta_f);
+          fH2 = __fadd_ru(fH2, __fmul_ru(fhw[d], fhw[d]));
+          off[d] = static_cast<float>(fc[d] - c[d]);
+        }
+        const float fH = __fsqrt_ru(fH2);
+        // Relative coordinates w.r.t. the fine centre are recomputed in binary64
+        // for the stored entries; the dominance test uses (coarse-rel - off),
+        // whose extra rounding is covered by the 1e-5 margin.
+        float bdist = INFINITY;
+        int bj = 0x7fffffff;
+        for (int j = lane; j < ncand; j += 32) {
+          float dd = 0.f;
+#pragma unroll
+          for (int d = 0; d < D; ++d) {
+            const float t = s_rel[warp][j][d] - off[d];
+            dd += t * t;
+          }
+          if (dd < bdist || (dd == bdist && j < bj)) {
+            bdist = dd;
+            bj = j;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const float od = __shfl_xor_sync(0xffffffffu, bdist, o);
+          const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+          if (od < bdist || (od == bdist && oj < bj)) {
+            bdist = od;
+            bj = oj;
+          }
+        }
+        float rt[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) rt[d] = s_rel[warp][bj][d] - off[d];
+        const std::uint32_t lab0 = s_lab[warp][bj];
+        int count = 0;
+        bool uniform = true;
+        for (int j0 = 0; j0 < ncand; j0 += 32) {
+          const int j = j0 + static_cast<int>(lane);
+          bool keep = false;
+          if (j < ncand) {
+            if (j == bj) {
+              keep = true;
+            } else {
+              float rs[D];
+#pragma unroll
+              for (int d = 0; d < D; ++d) rs[d] = s_rel[warp][j][d] - off[d];
+              keep = !dominated_f<D>(rs, rt, fhw, fH);
+            }
+          }
+          const unsigned ballot = __ballot_sync(0xffffffffu, keep);
+          if (__ballot_sync(0xffffffffu, keep && s_lab[warp][j] != lab0)) uniform = false;
+          const int pos = count + __popc(ballot & ((1u << lane) - 1u));
+          if (keep && pos < kSlots) {
+            const std::uint32_t si = s_idx[warp][j];
+            VltEntry e;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) e.r[d] = 0.f;
+#pragma unroll
+            for (int d = 0; d < D; ++d) e.r[d] = static_cast<float>(sorted[si].x[d] - fc[d]);
+            e.idx = si;
+            slab[fid * kSlots + pos] = e;
+          }
+          count += __popc(ballot);
+        }
+        if (uniform) head = lab0 << 8;
+        else if (count <= kSlots) head = static_cast<std::uint32_t>(count);
+        else head = kHeadOverflow;
+      }
+      if (lane == 0) {
+        heads[fid] = head;
+        const std::uint32_t h = head & 15u;
+        if (h == 0) ++st_uniform;
+        else if (h == kHeadOverflow) ++st_over;
+        else ++st_list;
+      }
+    }
+  }
+  if (stats && lane == 0) {
+    atomicAdd(&stats[0], st_uniform);
+    atomicAdd(&stats[1], st_list);
+    atomicAdd(&stats[2], st_over);
+  }
+}
+
+// Exact binary64 argmin over the candidates whose binary32 interval overlaps
+// the winner's (reference squared_distance, lowest pid on ties).
+template <int D>
+__device__ __forceinline__ std::uint32_t exact_among(const double* x, const VltEntry* ents, int cnt, const float* d32,
+                                                     const float* b32, float lim, const SampleRec* __restrict__ sorted) {
+  double best = INFINITY;
+  std::uint32_t best_pid = 0xFFFFFFFFu, label = 0;
+  for (int j = 0; j < cnt; ++j) {
+    if (d32[j] - b32[j] > lim) continue;
+    const SampleRec rec = sorted[ents[j].idx];
+    const double d2 = sqdist<D>(x, rec.x);
+    if (d2 < best || (d2 == best && rec.pid < best_pid)) {
+      best = d2;
+      best_pid = rec.pid;
+      label = rec.label;
+    }
+  }
+  return label;
+}
+
+// K2: table-driven point pass (coordinates streamed once; overflow points
+// are queued for k_assign_overflow so they do not diverge the warp).
+template <int D>
+__global__ void __launch_bounds__(256) k_assign_vlt(const double* __restrict__ xyz, std::uint64_t n,
+                                                    const SampleGrid<D>* __restrict__ sgp,
+                                                    const std::uint32_t* __restrict__ heads,
+                                                    const VltEntry* __restrict__ slab,
+                                                    const SampleRec* __restrict__ sorted,
+                                                    const std::uint32_t* __restrict__ sorted_labels,
+                                                    std::uint32_t* __restrict__ labels, unsigned long long* bbox,
+                                                    std::uint32_t* __restrict__ oq, unsigned* __restrict__ oq_count) {
+  __shared__ SampleGrid<D> s_sg;
+  if (threadIdx.x == 0) s_sg = *sgp;
+  __syncthreads();
+  const SampleGrid<D>& sg = s_sg;
+  constexpr int F = fine_factor<D>();
+  constexpr int FC = fine_per_cell<D>();
+  double blo[D], bhi[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) blo[d] = INFINITY, bhi[d] = -INFINITY;
+  for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += std::uint64_t(gridDim.x) * blockDim.x) {
+    double x[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      x[d] = __ldcs(xyz + i * D + d);
+      blo[d] = fmin(blo[d], x[d]);
+      bhi[d] = fmax(bhi[d], x[d]);
+    }
+    bool inside = true;
+    long long cell = 0, mul = 1;
+    int sub = 0, smul = 1;
+    double fcen[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const double f = floor((x[d] - sg.g.lo[d]) * sg.inv_ef);
+      inside = inside && (f >= 0.0) && (f < static_cast<double>(sg.g.dims[d] * F));
+      const int fi = inside ? static_cast<int>(f) : 0;
+      cell += static_cast<long long>(fi / F) * mul;
+      sub += (fi % F) * smul;
+      mul *= sg.g.dims[d];
+      smul *= F;
+      fcen[d] = 0.5 * ((sg.g.lo[d] + static_cast<double>(fi) * sg.ef) + (sg.g.lo[d] + static_cast<double>(fi + 1) * sg.ef));
+    }
+    std::uint32_t head = kHeadOverflow;
+    const long long fid = cell * FC + sub;
+    if (inside) head = __ldg(heads + fid);
+    const std::uint32_t cnt = head & 15u;
+    if (cnt == 0) {
+      __stcs(labels + i, head >> 8);
+    } else if (cnt == kHeadOverflow) {
+      const unsigned slot = atomicAdd(oq_count, 1u);
+      oq[slot] = static_cast<std::uint32_t>(i);
+    } else {
+      const VltEntry* ents = slab + fid * kSlots;
+      float p[D], pp = 0.f;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        p[d] = static_cast<float>(x[d] - fcen[d]);
+        pp += p[d] * p[d];
+      }
+      float d32[kSlots], b32[kSlots];
+      int best = 0;
+      float bval = INFINITY;
+      for (int j = 0; j < static_cast<int>(cnt); ++j) {
+        const VltEntry e = ents[j];
+        float dd = 0.f, ss = 0.f;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const float t = p[d] - e.r[d];
+          dd += t * t;
+          ss += e.r[d] * e.r[d];
+        }
+        d32[j] = dd;
+        b32[j] = 4e-6f * (pp + ss) + 1e-30f;
+        if (dd < bval) {
+          bval = dd;
+          best = j;
+        }
+      }
+      // decided iff every other candidate is provably farther
+      const float lim = d32[best] + b32[best];
+      bool decided = true;
+      for (int j = 0; j < static_cast<int>(cnt); ++j)
+        if (j != best && d32[j] - b32[j] <= lim) decided = false;
+      const std::uint32_t lab = decided ? __ldg(sorted_labels + ents[best].idx)
+                                        : exact_among<D>(x, ents, static_cast<int>(cnt), d32, b32, lim, sorted);
+      __stcs(labels + i, lab);
+    }
+  }
+  bbox_flush<D>(blo, bhi, bbox);
+}
+
+template <int D>
+__global__ void k_assign_overflow(const double* __restrict__ xyz, const SampleGrid<D>* __restrict__ sgp,
+                                  const std::uint32_t* __restrict__ starts, const SampleRec* __restrict__ sorted,
+                                  std::uint32_t* __restrict__ labels, const std::uint32_t* __restrict__ oq,
+                                  const unsigned* __restrict__ oq_count) {
+  __shared__ SampleGrid<D> sg;
+  if (threadIdx.x == 0) sg = *sgp;
+  __syncthreads();
+  const unsigned cnt = *oq_count;
+  for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < cnt; q += gridDim.x * blockDim.x) {
+    const std::uint32_t i = oq[q];
+    double x[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) x[d] = xyz[std::size_t(i) * D + d];
+    labels[i] = nearest_label_ring<D>(x, sg.g, sg.margin, starts, sorted);
+  }
+}
+
+__global__ void k_sorted_labels(const SampleRec* __restrict__ sorted, std::uint32_t m, std::uint32_t* __restrict__ out) {
+  for (std::uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < m; s += gridDim.x * blockDim.x)
+    out[s] = sorted[s].label;
+}
+
+}  // namespace sbdt_gpu

@@ -83,6 +83,7 @@ def lib():
         L.sbdt_gpu_set_timing.argtypes = [vp, C.c_int]
         L.sbdt_gpu_stage_times.argtypes = [vp, C.c_char_p, C.c_int, C.POINTER(C.c_float), C.c_int]
         L.sbdt_gpu_assign_table_stats.argtypes = [vp, C.POINTER(C.c_uint)]
+        L.sbdt_gpu_border_stats.argtypes = [vp, C.POINTER(C.c_ulonglong)]
         _lib = L
     return _lib
 
@@ -142,6 +143,13 @@ class Context:
         if lib().sbdt_gpu_assign_table_stats(self._h, out) != SBDT_OK:
             return {}
         return {"uniform": int(out[0]), "list": int(out[1]), "overflow": int(out[2])}
+
+    def border_stats(self) -> dict:
+        out = (C.c_ulonglong * 8)()
+        if lib().sbdt_gpu_border_stats(self._h, out) != SBDT_OK:
+            return {}
+        return {"finite_rows": int(out[0]), "exact_stage_rows": int(out[1]), "descent_box_tests": int(out[2]),
+                "descent_expansions": int(out[3]), "start_level_hist": [int(out[4 + i]) for i in range(4)]}
 
     # ---- device-pointer entry points (inputs resident in HBM; async on the stream)
     def assign_points_dev(self, dim, d_xyz, n, d_sample_ids, d_sample_labels, m, k, d_labels, d_part_offsets=None,

@@ -1,0 +1,101 @@
+"""GPU tests beyond the small parity grid: the prefilter path (no sphere
+export), larger instances checked against the oracle on a bounded subset
+(first points / first parts), size-independent properties (policy chain,
+BFS subset, determinism, Partitioning consistency) and error behaviour."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1902_07554_b200 import gpu, host
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("cfg,n,k", [(1, 200_000, 16), (2, 300_000, 16), (3, 300_000, 16), (4, 400_000, 32),
+                                     (5, 600_000, 32)])
+def test_prefilter_path_bit_exact(cfg, n, k, ctx):
+    inst = host.make_instance(cfg, n=n, k=k)
+    lab = gpu.assign_points(inst.points, inst.sample_ids, inst.sample_labels, k, ctx=ctx).labels
+    ref = oracle.assign_kdtree(inst.points, inst.sample_ids, inst.sample_labels)
+    assert np.array_equal(lab, ref)
+    part = host.attach_partials(inst, lab)
+    g = gpu.find_border(inst.points, lab, part, gpu.IntersectionPolicy("grid", 1.0), hull_bfs=True, ctx=ctx)
+    o = oracle.find_border(inst.points, lab, part, "grid")
+    assert np.array_equal(g.positive, o["positive"])
+    assert np.array_equal(g.border, o["border"])
+    assert np.array_equal(g.positive_vertex_ids, o["vertices_positive"])
+    assert np.array_equal(g.border_vertex_ids, o["vertices_border"])
+
+
+def test_large_instance_subset_parity(ctx):
+    """Config 2 at 2M points (k=64): labels of the first 300k points and the
+    flags of the first 6 parts against the oracle (bounded CPU work)."""
+    inst = host.make_instance(2, n=2_000_000, k=64)
+    part_ = gpu.assign_points(inst.points, inst.sample_ids, inst.sample_labels, 64, ctx=ctx)
+    sub = slice(0, 300_000)
+    # oracle on a prefix of the points (the kd-tree still spans the whole sample)
+    full_ref = np.empty(300_000, np.uint32)
+    import ctypes as C
+    pts = np.ascontiguousarray(inst.points)
+    oracle.lib().oracle_assign_kdtree_range(3, oracle._p(pts, C.c_double), 0, 300_000,
+                                            oracle._p(inst.sample_ids, C.c_uint32), len(inst.sample_ids),
+                                            oracle._p(inst.sample_labels, C.c_uint32), oracle._p(full_ref, C.c_uint32),
+                                            8)
+    assert np.array_equal(part_.labels[sub], full_ref)
+    lab = part_.labels
+    part = host.attach_partials(inst, lab)
+    g = gpu.find_border(inst.points, lab, part, gpu.IntersectionPolicy("grid", 1.0), hull_bfs=True, ctx=ctx)
+    o = oracle.find_border(inst.points, lab, part, "grid", parts=(0, 6))
+    hi = int(part.offsets[6])
+    assert np.array_equal(g.positive[:hi], o["positive"][:hi])
+    assert np.array_equal(g.border[:hi], o["border"][:hi])
+
+
+def test_policy_chain_and_subsets(ctx):
+    inst = host.make_instance(4, n=300_000, k=16)
+    lab = gpu.assign_points(inst.points, inst.sample_ids, inst.sample_labels, 16, ctx=ctx).labels
+    part = host.attach_partials(inst, lab)
+    grid = gpu.find_border(inst.points, lab, part, gpu.IntersectionPolicy("grid"), ctx=ctx)
+    bbox = gpu.find_border(inst.points, lab, part, gpu.IntersectionPolicy("bbox"), ctx=ctx)
+    assert set(grid.border_vertex_ids.tolist()) <= set(bbox.border_vertex_ids.tolist())
+    assert np.all(grid.positive <= bbox.positive)
+    assert np.all(grid.border <= grid.positive)  # BFS subset of the full scan
+    assert set(grid.border_vertex_ids.tolist()) <= set(grid.positive_vertex_ids.tolist())
+    again = gpu.find_border(inst.points, lab, part, gpu.IntersectionPolicy("grid"), ctx=ctx)
+    assert np.array_equal(again.positive, grid.positive) and np.array_equal(again.border_vertex_ids,
+                                                                             grid.border_vertex_ids)
+
+
+def test_partitioning_consistency_and_determinism(ctx):
+    inst = host.make_instance(5, n=500_000, k=64)
+    a = gpu.assign_points(inst.points, inst.sample_ids, inst.sample_labels, 64, ctx=ctx)
+    b = gpu.assign_points(inst.points, inst.sample_ids, inst.sample_labels, 64, ctx=ctx)
+    assert np.array_equal(a.labels, b.labels) and np.array_equal(a.parts_ids, b.parts_ids)
+    assert a.parts_offsets[-1] == inst.n
+    for p in range(64):
+        ids = a.part(p)
+        assert np.all(np.diff(ids.astype(np.int64)) > 0)
+        assert np.all(a.labels[ids] == p)
+
+
+def test_sample_points_label_themselves(ctx):
+    inst = host.make_instance(1, n=50_000, k=8)
+    lab = gpu.assign_points(inst.points, inst.sample_ids, inst.sample_labels, 8, ctx=ctx).labels
+    assert np.array_equal(lab[inst.sample_ids], inst.sample_labels)
+
+
+def test_invalid_arguments_raise(ctx):
+    pts = np.random.default_rng(0).random((100, 2))
+    with pytest.raises(ValueError):
+        gpu.assign_points(pts, np.array([], np.uint32), np.array([], np.uint32), 4, ctx=ctx)
+    with pytest.raises(ValueError):
+        gpu.assign_points(np.random.default_rng(0).random((100, 4)), np.array([0], np.uint32),
+                          np.array([0], np.uint32), 1, ctx=ctx)
+
+
+def test_k1_no_border(ctx):
+    inst = host.make_instance(1, n=20_000, k=1)
+    lab = np.zeros(inst.n, np.uint32)
+    part = host.attach_partials(inst, lab)
+    g = gpu.find_border(inst.points, lab, part, ctx=ctx)
+    assert g.positive.sum() == 0 and len(g.border_vertex_ids) == 0
