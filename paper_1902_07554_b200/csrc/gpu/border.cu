@@ -126,7 +126,8 @@ __device__ __forceinline__ void circumsphere_inflated(const double (*p)[D], doub
 // contains the inflated binary64 sphere of circumsphere_inflated(); false
 // when ill-conditioned (the caller then runs the exact path).
 template <int D>
-__device__ __forceinline__ bool enclosing_sphere_f32(const double (*p)[D], double* c, double* R) {
+__device__ __forceinline__ bool enclosing_sphere_f32(const double (*p)[D], double* c, double* R,
+                                                     double* Rin = nullptr) {
   constexpr float g = 2e-6f;
   float rel[D], err[D];
   if constexpr (D == 2) {
@@ -192,6 +193,9 @@ __device__ __forceinline__ bool enclosing_sphere_f32(const double (*p)[D], doubl
 #pragma unroll
   for (int d = 0; d < D; ++d) mag = fmax(mag, fabs(p[0][d]));
   *R = r32 * (1.0 + 1e-6) + 2.01 * e32 + 1e-15 * mag;
+  // INNER radius: the ball (c, Rin) lies inside the binary64 sphere, whose
+  // radius is >= |rel32| - e and whose centre is within e of c.
+  if (Rin) *Rin = r32 * (1.0 - 1e-6) - 2.01 * e32 - 1e-15 * mag;
   return true;
 }
 
@@ -251,8 +255,10 @@ __device__ __forceinline__ int leaf_range(const OwnerGrid<D>& og, const double* 
     lo[d] = fa < 0.0 ? 0 : static_cast<int>(fa);
     const int hi = fb > top ? og.ldims[0][d] - 1 : static_cast<int>(fb);
     span[d] = hi - lo[d] + 1;
-    if (span[d] > 5) mode = 2;
+    if (span[d] > 5) mode = max(mode, 2);
+    if (span[d] > 16) mode = 3;
   }
+  if (mode == 2 && og.levels < 3) mode = 3;
   return mode;
 }
 
@@ -386,14 +392,14 @@ __global__ void __launch_bounds__(kBThreads) k_border_tiles(BorderArgs a, const 
   __shared__ OwnerGrid<D> og;
   __shared__ std::uint32_t qb[kTile];
   __shared__ std::uint32_t qb_self[kTile];
-  __shared__ int nb;
+  __shared__ int nb, next;
   extern __shared__ std::uint64_t s_off[];
   if (threadIdx.x == 0) og = *ogp;
   for (std::uint32_t j = threadIdx.x; j <= a.k; j += blockDim.x) s_off[j] = a.offsets[j];
   __syncthreads();
   const std::uint64_t tiles = (a.S + kTile - 1) / kTile;
   for (std::uint64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    if (threadIdx.x == 0) nb = 0;
+    if (threadIdx.x == 0) nb = next = 0;
     __syncthreads();
     const std::uint64_t base = tile * kTile;
     // ---- stage A
@@ -415,11 +421,37 @@ __global__ void __launch_bounds__(kBThreads) k_border_tiles(BorderArgs a, const 
       for (int j = 0; j <= D; ++j)
 #pragma unroll
         for (int d = 0; d < D; ++d) p[j][d] = a.xyz[std::size_t(v[j]) * D + d];
-      double cc[D], R;
-      if (enclosing_sphere_f32<D>(p, cc, &R)) {
+      double cc[D], R, Rin;
+      if (enclosing_sphere_f32<D>(p, cc, &R, &Rin)) {
         if (window_clear<D>(og, a.owner, a.nbr3, a.nbr5, cc, R, self)) {
           __stcs(a.positive + s, static_cast<std::uint8_t>(0));
           continue;
+        }
+        // positive proof: the inner ball (inside the binary64 sphere) reaches
+        // the cell of its centre, and that cell is occupied by another part
+        const double ri = Rin * (1.0 - 1e-9) - og.margin;
+        if (ri > 0.0) {
+          int c0[D];
+          bool inside = true;
+#pragma unroll
+          for (int d = 0; d < D; ++d) {
+            const double f = floor((cc[d] - og.g.lo[d]) * og.inv_edge);
+            inside = inside && f >= 0.0 && f <= static_cast<double>(og.ldims[0][d] - 1);
+            c0[d] = inside ? static_cast<int>(f) : 0;
+          }
+          if (inside) {
+            const std::uint16_t code = a.owner[og_index<D>(og, 0, c0)];
+            if (code != kOwnerEmpty && code != self) {
+              double blo[D], bhi[D];
+              og_block_box<D>(og, 0, c0, blo, bhi);
+              if (box_sphere<D>(blo, bhi, cc, ri * ri)) {
+                __stcs(a.positive + s, static_cast<std::uint8_t>(1));
+#pragma unroll
+                for (int j = 0; j <= D; ++j) a.vflags[v[j]] = 1;
+                continue;
+              }
+            }
+          }
         }
       }
       {
@@ -434,11 +466,16 @@ __global__ void __launch_bounds__(kBThreads) k_border_tiles(BorderArgs a, const 
       const std::uint64_t rows = (a.S - base) < std::uint64_t(kTile) ? (a.S - base) : std::uint64_t(kTile);
       atomicAdd(&a.counters[0], static_cast<unsigned long long>(rows));
     }
-    // ---- stage C: lane-parallel binary64 spheres, then one warp-cooperative
-    // leaf scan per candidate (lane = cell of the candidate's cell range).
+    // ---- stage C: lane-parallel binary64 spheres, then warp-cooperative scans
+    // (lane = cell, or lane = level-1 block then its 64 cells); warps grab
+    // batches of 32 candidates dynamically so the CTA stays balanced.
     const int nqb = nb;
-    const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    for (int base = warp * 32; base < nqb; base += blockDim.x) {
+    const unsigned lane = threadIdx.x & 31u;
+    for (;;) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&next, 32);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (base >= nqb) break;
       const int t = base + static_cast<int>(lane);
       const bool has = t < nqb;
       std::uint64_t s = 0;
@@ -460,18 +497,93 @@ __global__ void __launch_bounds__(kBThreads) k_border_tiles(BorderArgs a, const 
         mode = leaf_range<D>(og, c, r2, lo, span);
       }
       bool pos = false;
-      if (has && mode == 2) pos = og_sphere_hits_foreign<D>(og, a.owner, c, r2, self);
+      if (has && mode == 3) pos = og_sphere_hits_foreign<D>(og, a.owner, c, r2, self);
+      // mode 2: level-1 blocks cooperatively, then the cells of partial blocks
+      unsigned todo2 = __ballot_sync(0xffffffffu, mode == 2);
+      while (todo2) {
+        const int l = __ffs(todo2) - 1;
+        todo2 &= todo2 - 1;
+        double cl[D];
+        int lol[D], spl[D], blo1[D], bsp[D];
+        unsigned binv[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          cl[d] = __shfl_sync(0xffffffffu, c[d], l);
+          lol[d] = __shfl_sync(0xffffffffu, lo[d], l);
+          spl[d] = __shfl_sync(0xffffffffu, span[d], l);
+          blo1[d] = lol[d] >> og.shift;
+          bsp[d] = ((lol[d] + spl[d] - 1) >> og.shift) - blo1[d] + 1;
+          binv[d] = (65536u + static_cast<unsigned>(bsp[d]) - 1u) / static_cast<unsigned>(bsp[d]);
+        }
+        const double rl = __shfl_sync(0xffffffffu, r2, l);
+        const std::uint32_t sl = __shfl_sync(0xffffffffu, self, l);
+        const int nblk = D == 3 ? bsp[0] * bsp[1] * bsp[2] : bsp[0] * bsp[1];
+        bool hit = false;
+        for (int i0 = 0; i0 < nblk && !hit; i0 += 32) {
+          const int i = i0 + static_cast<int>(lane);
+          bool h = false, partial = false;
+          int bc[D];
+          if (i < nblk) {
+            unsigned rem = static_cast<unsigned>(i);
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+              const unsigned q = (rem * binv[d]) >> 16;  // rem / bsp[d] (rem * bsp < 2^16)
+              bc[d] = blo1[d] + static_cast<int>(rem - q * static_cast<unsigned>(bsp[d]));
+              rem = q;
+            }
+            const std::uint16_t code = a.owner[og_index<D>(og, 1, bc)];
+            if (code != kOwnerEmpty && code != sl) {
+              double blo[D], bhi[D];
+              og_block_box<D>(og, 1, bc, blo, bhi);
+              if (box_sphere<D>(blo, bhi, cl, rl)) {
+                if (box_inside_sphere<D>(blo, bhi, cl, rl)) h = true;
+                else partial = true;
+              }
+            }
+          }
+          hit = __any_sync(0xffffffffu, h);
+          unsigned pm = __ballot_sync(0xffffffffu, partial);
+          while (pm && !hit) {
+            const int pl = __ffs(pm) - 1;
+            pm &= pm - 1;
+            int pb[D];
+#pragma unroll
+            for (int d = 0; d < D; ++d) pb[d] = __shfl_sync(0xffffffffu, bc[d], pl);
+            bool h2 = false;
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+              int cc[D];
+              og_child<D>(pb, half * 32 + static_cast<int>(lane), cc);
+              bool in = true;
+#pragma unroll
+              for (int d = 0; d < D; ++d) in = in && cc[d] >= lol[d] && cc[d] < lol[d] + spl[d];
+              if (in) {
+                const std::uint16_t code = a.owner[og_index<D>(og, 0, cc)];
+                if (code != kOwnerEmpty && code != sl) {
+                  double blo[D], bhi[D];
+                  og_block_box<D>(og, 0, cc, blo, bhi);
+                  h2 = h2 || box_sphere<D>(blo, bhi, cl, rl);
+                }
+              }
+            }
+            hit = __any_sync(0xffffffffu, h2);
+          }
+        }
+        if (static_cast<int>(lane) == l) pos = hit;
+      }
       unsigned todo = __ballot_sync(0xffffffffu, mode == 1);
       while (todo) {
         const int l = __ffs(todo) - 1;
         todo &= todo - 1;
         double cl[D];
         int lol[D], spl[D];
+        unsigned sinv[D];
 #pragma unroll
         for (int d = 0; d < D; ++d) {
           cl[d] = __shfl_sync(0xffffffffu, c[d], l);
           lol[d] = __shfl_sync(0xffffffffu, lo[d], l);
           spl[d] = __shfl_sync(0xffffffffu, span[d], l);
+          sinv[d] = (65536u + static_cast<unsigned>(spl[d]) - 1u) / static_cast<unsigned>(spl[d]);
         }
         const double rl = __shfl_sync(0xffffffffu, r2, l);
         const std::uint32_t sl = __shfl_sync(0xffffffffu, self, l);
@@ -481,11 +593,13 @@ __global__ void __launch_bounds__(kBThreads) k_border_tiles(BorderArgs a, const 
           const int i = i0 + static_cast<int>(lane);
           bool h = false;
           if (i < cells) {
-            int cc[D], rem = i;
+            int cc[D];
+            unsigned rem = static_cast<unsigned>(i);
 #pragma unroll
             for (int d = 0; d < D; ++d) {
-              cc[d] = lol[d] + rem % spl[d];
-              rem /= spl[d];
+              const unsigned q = (rem * sinv[d]) >> 16;  // rem / spl[d] (rem * spl < 2^16)
+              cc[d] = lol[d] + static_cast<int>(rem - q * static_cast<unsigned>(spl[d]));
+              rem = q;
             }
             const std::uint16_t code = a.owner[og_index<D>(og, 0, cc)];
             if (code != kOwnerEmpty && code != sl) {
