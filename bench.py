@@ -323,9 +323,15 @@ def main():
 
     t_assign = sum(v for kk, v in stages.items() if kk.startswith("assign."))
     t_border = sum(v for kk, v in stages.items() if kk.startswith("border."))
+    n_cand = int(border_stats.get("exact_stage_rows", 0))
     kernel_bytes = {
         "assign.points": n * (8 * dim + 4),
-        "border.finite": S * (4 * (dim + 1) + 1) + n * (8 * dim + 1) + cells * 2,
+        "border.finite": S * (4 * (dim + 1) + 1) + n * (8 * dim + 4 + 1) + cells * 2,
+        "border.localize": n * (2 * 8 * dim + 4 + 4),
+        # prefilter: vertex ids + parity + flag per row, localised coords once, 3 code arrays
+        "border.prefilter": S * (4 * (dim + 1) + 2) + n * (8 * dim + 4) + cells * 2 * 3,
+        # exact stage: queue entry + ids per candidate + result, coords once
+        "border.exact": n_cand * (4 + 4 * (dim + 1) + 1) + n * (8 * dim + 4) + cells * 2,
         "border.grid": n * (8 * dim + 4) + cells * 2,
         "assign.bucket": n * 12,
         "border.compact": n + n_vb * 4,

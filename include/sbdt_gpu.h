@@ -75,7 +75,8 @@ int sbdt_gpu_stage_times(sbdt_gpu_ctx* ctx, char* names, int names_len, float* m
  * out3 = {uniform records, candidate-list records, overflow records}. */
 int sbdt_gpu_assign_table_stats(sbdt_gpu_ctx* ctx, unsigned* out3);
 /* Border pipeline census of the last find_border with timing enabled:
- * out4 = {finite rows, rows that reached the exact stage, 0, 0}. */
+ * out4 = {rows scanned by the prefilter, rows that reached the exact stage,
+ * 0, 0} (grid policy; zeros otherwise). */
 int sbdt_gpu_border_stats(sbdt_gpu_ctx* ctx, unsigned long long* out4);
 
 /* ---- assign_points -------------------------------------

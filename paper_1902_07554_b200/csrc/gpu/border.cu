@@ -274,6 +274,8 @@ __device__ __forceinline__ std::uint32_t part_of(const std::uint64_t* offs, std:
 
 struct BorderArgs {
   const double* xyz;
+  const double* xyz_loc;      // coordinates in partition-bucket order (k_loc_scatter)
+  const std::uint32_t* inv;   // PointId -> row of xyz_loc
   std::uint64_t n;
   std::uint32_t k;
   const std::uint64_t* offsets;
@@ -373,253 +375,311 @@ __global__ void __launch_bounds__(kBThreads) k_border_finite(BorderArgs a, const
   }
 }
 
-// Grid policy, two-stage CTA pipeline over tiles of kTile simplices. The
-// simplices that survive stage A are compacted into a shared-memory queue, so
-// both stages run with all lanes busy (no divergence between cheap negatives
-// and exact candidates):
-//   A  all rows: binary32 enclosing sphere + the owner/3^D/5^D neighbourhood
-//      code of the window covering its cell range -> most simplices are proven
-//      negative with one 2-byte lookup and no binary64 arithmetic;
-//   C  candidates: the reference's binary64 circumsphere (exact operation
-//      order) and the exact pyramid descent (og_sphere_hits_foreign).
-// A only concludes "negative" for a sphere that contains the exact binary64
-// sphere, so the flags equal the exact test's.
-constexpr int kTile = 2048;
-
+// Grid policy, two kernels joined by a global candidate queue:
+//   A  k_border_prefilter, one thread per row: binary32 enclosing sphere with
+//      an a-posteriori error bound, then
+//        - negative if its cell range sits in one window (cell, 3^D or 5^D
+//          neighbourhood) whose combined code is EMPTY or self;
+//        - positive if the conservative INNER ball reaches the cell of its
+//          centre and that cell holds another part;
+//        - otherwise the row is appended to the candidate queue.
+//      Rows that reference kInfiniteVertex go to the halfspace queue.
+//   C  k_border_exact, warps pull 32 candidates at a time: the reference's
+//      binary64 circumsphere (exact operation order), then the cells of its
+//      range are tested as one flattened (candidate, cell) stream over the
+//      32 lanes (no per-candidate serial loop, no CTA barriers); wide ranges
+//      use the two-level cooperative scan, huge ones the pyramid descent.
+// A only concludes for spheres that contain / are contained in the exact
+// binary64 sphere, so the flags equal the exact test's.
+constexpr int kExactWarps = 8;
 
 template <int D>
-__global__ void __launch_bounds__(kBThreads) k_border_tiles(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp) {
+__device__ __forceinline__ void load_simplex(const BorderArgs& a, const std::uint32_t* v, double (*p)[D]) {
+  std::uint32_t w[D + 1];
+#pragma unroll
+  for (int j = 0; j <= D; ++j) w[j] = __ldg(a.inv + v[j]);
+#pragma unroll
+  for (int j = 0; j <= D; ++j)
+#pragma unroll
+    for (int d = 0; d < D; ++d) p[j][d] = __ldg(a.xyz_loc + std::size_t(w[j]) * D + d);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
+                                                                std::uint32_t* __restrict__ cand,
+                                                                unsigned* __restrict__ ncand) {
   __shared__ OwnerGrid<D> og;
-  __shared__ std::uint32_t qb[kTile];
-  __shared__ std::uint32_t qb_self[kTile];
-  __shared__ int nb, next;
   extern __shared__ std::uint64_t s_off[];
   if (threadIdx.x == 0) og = *ogp;
   for (std::uint32_t j = threadIdx.x; j <= a.k; j += blockDim.x) s_off[j] = a.offsets[j];
   __syncthreads();
-  const std::uint64_t tiles = (a.S + kTile - 1) / kTile;
-  for (std::uint64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    if (threadIdx.x == 0) nb = next = 0;
-    __syncthreads();
-    const std::uint64_t base = tile * kTile;
-    // ---- stage A
-    for (int t = threadIdx.x; t < kTile; t += blockDim.x) {
-      const std::uint64_t s = base + t;
-      if (s >= a.S) break;
-      std::uint32_t v[D + 1];
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned lt = (1u << lane) - 1u;
+  const std::uint64_t stride = std::uint64_t(gridDim.x) * blockDim.x;
+  const std::uint64_t S_up = (a.S + 31) & ~std::uint64_t(31);  // whole warps iterate together
+  for (std::uint64_t s = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; s < S_up; s += stride) {
+    const bool valid = s < a.S;
+    std::uint32_t v[D + 1];
 #pragma unroll
-      for (int j = 0; j <= D; ++j) v[j] = __ldcs(a.verts + std::uint64_t(j) * a.S + s);
-      if (v[D] == kInfVertex) {
-        const unsigned slot = atomicAdd(a.inf_count, 1u);
-        a.inf_queue[slot] = static_cast<std::uint32_t>(s);
-        continue;
-      }
+    for (int j = 0; j <= D; ++j) v[j] = valid ? __ldcs(a.verts + std::uint64_t(j) * a.S + s) : kInfVertex;
+    const bool inf = valid && v[D] == kInfVertex;
+    bool is_cand = false;
+    if (valid && !inf) {
       if (a.parity[s] == 0) atomicOr(a.status, kStDegenerate);
       const std::uint32_t self = part_of(s_off, a.k, s);
       double p[D + 1][D];
-#pragma unroll
-      for (int j = 0; j <= D; ++j)
-#pragma unroll
-        for (int d = 0; d < D; ++d) p[j][d] = a.xyz[std::size_t(v[j]) * D + d];
+      load_simplex<D>(a, v, p);
+      int res = 2;  // 0 negative, 1 positive, 2 candidate
       double cc[D], R, Rin;
       if (enclosing_sphere_f32<D>(p, cc, &R, &Rin)) {
         if (window_clear<D>(og, a.owner, a.nbr3, a.nbr5, cc, R, self)) {
-          __stcs(a.positive + s, static_cast<std::uint8_t>(0));
-          continue;
-        }
-        // positive proof: the inner ball (inside the binary64 sphere) reaches
-        // the cell of its centre, and that cell is occupied by another part
-        const double ri = Rin * (1.0 - 1e-9) - og.margin;
-        if (ri > 0.0) {
-          int c0[D];
-          bool inside = true;
-#pragma unroll
-          for (int d = 0; d < D; ++d) {
-            const double f = floor((cc[d] - og.g.lo[d]) * og.inv_edge);
-            inside = inside && f >= 0.0 && f <= static_cast<double>(og.ldims[0][d] - 1);
-            c0[d] = inside ? static_cast<int>(f) : 0;
-          }
-          if (inside) {
-            const std::uint16_t code = a.owner[og_index<D>(og, 0, c0)];
-            if (code != kOwnerEmpty && code != self) {
-              double blo[D], bhi[D];
-              og_block_box<D>(og, 0, c0, blo, bhi);
-              if (box_sphere<D>(blo, bhi, cc, ri * ri)) {
-                __stcs(a.positive + s, static_cast<std::uint8_t>(1));
-#pragma unroll
-                for (int j = 0; j <= D; ++j) a.vflags[v[j]] = 1;
-                continue;
-              }
-            }
-          }
-        }
-      }
-      {
-        const int q = atomicAdd(&nb, 1);
-        qb[q] = static_cast<std::uint32_t>(s);
-        qb_self[q] = self;
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0 && a.counters) {
-      atomicAdd(&a.counters[1], static_cast<unsigned long long>(nb));
-      const std::uint64_t rows = (a.S - base) < std::uint64_t(kTile) ? (a.S - base) : std::uint64_t(kTile);
-      atomicAdd(&a.counters[0], static_cast<unsigned long long>(rows));
-    }
-    // ---- stage C: lane-parallel binary64 spheres, then warp-cooperative scans
-    // (lane = cell, or lane = level-1 block then its 64 cells); warps grab
-    // batches of 32 candidates dynamically so the CTA stays balanced.
-    const int nqb = nb;
-    const unsigned lane = threadIdx.x & 31u;
-    for (;;) {
-      int base = 0;
-      if (lane == 0) base = atomicAdd(&next, 32);
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (base >= nqb) break;
-      const int t = base + static_cast<int>(lane);
-      const bool has = t < nqb;
-      std::uint64_t s = 0;
-      std::uint32_t self = 0, v[D + 1];
-      double c[D], r2 = 0.0;
-      int lo[D], span[D];
-      int mode = 0;  // 0 none/negative, 1 cooperative scan, 2 solo descent
-      if (has) {
-        s = qb[t];
-        self = qb_self[t];
-#pragma unroll
-        for (int j = 0; j <= D; ++j) v[j] = a.verts[std::uint64_t(j) * a.S + s];
-        double p[D + 1][D];
-#pragma unroll
-        for (int j = 0; j <= D; ++j)
-#pragma unroll
-          for (int d = 0; d < D; ++d) p[j][d] = a.xyz[std::size_t(v[j]) * D + d];
-        circumsphere_inflated<D>(p, c, &r2);
-        mode = leaf_range<D>(og, c, r2, lo, span);
-      }
-      bool pos = false;
-      if (has && mode == 3) pos = og_sphere_hits_foreign<D>(og, a.owner, c, r2, self);
-      // mode 2: level-1 blocks cooperatively, then the cells of partial blocks
-      unsigned todo2 = __ballot_sync(0xffffffffu, mode == 2);
-      while (todo2) {
-        const int l = __ffs(todo2) - 1;
-        todo2 &= todo2 - 1;
-        double cl[D];
-        int lol[D], spl[D], blo1[D], bsp[D];
-        unsigned binv[D];
-#pragma unroll
-        for (int d = 0; d < D; ++d) {
-          cl[d] = __shfl_sync(0xffffffffu, c[d], l);
-          lol[d] = __shfl_sync(0xffffffffu, lo[d], l);
-          spl[d] = __shfl_sync(0xffffffffu, span[d], l);
-          blo1[d] = lol[d] >> og.shift;
-          bsp[d] = ((lol[d] + spl[d] - 1) >> og.shift) - blo1[d] + 1;
-          binv[d] = (65536u + static_cast<unsigned>(bsp[d]) - 1u) / static_cast<unsigned>(bsp[d]);
-        }
-        const double rl = __shfl_sync(0xffffffffu, r2, l);
-        const std::uint32_t sl = __shfl_sync(0xffffffffu, self, l);
-        const int nblk = D == 3 ? bsp[0] * bsp[1] * bsp[2] : bsp[0] * bsp[1];
-        bool hit = false;
-        for (int i0 = 0; i0 < nblk && !hit; i0 += 32) {
-          const int i = i0 + static_cast<int>(lane);
-          bool h = false, partial = false;
-          int bc[D];
-          if (i < nblk) {
-            unsigned rem = static_cast<unsigned>(i);
+          res = 0;
+        } else {
+          // the inner ball lies inside the binary64 sphere: if it reaches the
+          // cell of its centre and that cell holds another part, s is positive
+          const double ri = Rin * (1.0 - 1e-9) - og.margin;
+          if (ri > 0.0) {
+            int c0[D];
+            bool inside = true;
 #pragma unroll
             for (int d = 0; d < D; ++d) {
-              const unsigned q = (rem * binv[d]) >> 16;  // rem / bsp[d] (rem * bsp < 2^16)
-              bc[d] = blo1[d] + static_cast<int>(rem - q * static_cast<unsigned>(bsp[d]));
-              rem = q;
+              const double f = floor((cc[d] - og.g.lo[d]) * og.inv_edge);
+              inside = inside && f >= 0.0 && f <= static_cast<double>(og.ldims[0][d] - 1);
+              c0[d] = inside ? static_cast<int>(f) : 0;
             }
-            const std::uint16_t code = a.owner[og_index<D>(og, 1, bc)];
-            if (code != kOwnerEmpty && code != sl) {
-              double blo[D], bhi[D];
-              og_block_box<D>(og, 1, bc, blo, bhi);
-              if (box_sphere<D>(blo, bhi, cl, rl)) {
-                if (box_inside_sphere<D>(blo, bhi, cl, rl)) h = true;
-                else partial = true;
+            if (inside) {
+              const std::uint16_t code = a.owner[og_index<D>(og, 0, c0)];
+              if (code != kOwnerEmpty && code != self) {
+                double blo[D], bhi[D];
+                og_block_box<D>(og, 0, c0, blo, bhi);
+                if (box_sphere<D>(blo, bhi, cc, ri * ri)) res = 1;
               }
             }
           }
-          hit = __any_sync(0xffffffffu, h);
-          unsigned pm = __ballot_sync(0xffffffffu, partial);
-          while (pm && !hit) {
-            const int pl = __ffs(pm) - 1;
-            pm &= pm - 1;
-            int pb[D];
-#pragma unroll
-            for (int d = 0; d < D; ++d) pb[d] = __shfl_sync(0xffffffffu, bc[d], pl);
-            bool h2 = false;
-#pragma unroll
-            for (int half = 0; half < 2; ++half) {
-              int cc[D];
-              og_child<D>(pb, half * 32 + static_cast<int>(lane), cc);
-              bool in = true;
-#pragma unroll
-              for (int d = 0; d < D; ++d) in = in && cc[d] >= lol[d] && cc[d] < lol[d] + spl[d];
-              if (in) {
-                const std::uint16_t code = a.owner[og_index<D>(og, 0, cc)];
-                if (code != kOwnerEmpty && code != sl) {
-                  double blo[D], bhi[D];
-                  og_block_box<D>(og, 0, cc, blo, bhi);
-                  h2 = h2 || box_sphere<D>(blo, bhi, cl, rl);
-                }
-              }
-            }
-            hit = __any_sync(0xffffffffu, h2);
-          }
         }
-        if (static_cast<int>(lane) == l) pos = hit;
       }
-      unsigned todo = __ballot_sync(0xffffffffu, mode == 1);
-      while (todo) {
-        const int l = __ffs(todo) - 1;
-        todo &= todo - 1;
-        double cl[D];
-        int lol[D], spl[D];
-        unsigned sinv[D];
-#pragma unroll
-        for (int d = 0; d < D; ++d) {
-          cl[d] = __shfl_sync(0xffffffffu, c[d], l);
-          lol[d] = __shfl_sync(0xffffffffu, lo[d], l);
-          spl[d] = __shfl_sync(0xffffffffu, span[d], l);
-          sinv[d] = (65536u + static_cast<unsigned>(spl[d]) - 1u) / static_cast<unsigned>(spl[d]);
-        }
-        const double rl = __shfl_sync(0xffffffffu, r2, l);
-        const std::uint32_t sl = __shfl_sync(0xffffffffu, self, l);
-        const int cells = D == 3 ? spl[0] * spl[1] * spl[2] : spl[0] * spl[1];
-        bool hit = false;
-        for (int i0 = 0; i0 < cells && !hit; i0 += 32) {
-          const int i = i0 + static_cast<int>(lane);
-          bool h = false;
-          if (i < cells) {
-            int cc[D];
-            unsigned rem = static_cast<unsigned>(i);
-#pragma unroll
-            for (int d = 0; d < D; ++d) {
-              const unsigned q = (rem * sinv[d]) >> 16;  // rem / spl[d] (rem * spl < 2^16)
-              cc[d] = lol[d] + static_cast<int>(rem - q * static_cast<unsigned>(spl[d]));
-              rem = q;
-            }
-            const std::uint16_t code = a.owner[og_index<D>(og, 0, cc)];
-            if (code != kOwnerEmpty && code != sl) {
-              double blo[D], bhi[D];
-              og_block_box<D>(og, 0, cc, blo, bhi);
-              h = box_sphere<D>(blo, bhi, cl, rl);
-            }
-          }
-          hit = __any_sync(0xffffffffu, h);
-        }
-        if (static_cast<int>(lane) == l) pos = hit;
-      }
-      if (has) {
-        __stcs(a.positive + s, static_cast<std::uint8_t>(pos ? 1 : 0));
-        if (pos)
+      if (res == 2) {
+        is_cand = true;
+      } else {
+        __stcs(a.positive + s, static_cast<std::uint8_t>(res));
+        if (res == 1)
 #pragma unroll
           for (int j = 0; j <= D; ++j) a.vflags[v[j]] = 1;
       }
     }
-    __syncthreads();
+    // warp-aggregated queue appends
+    const unsigned mc = __ballot_sync(0xffffffffu, is_cand);
+    const unsigned mi = __ballot_sync(0xffffffffu, inf);
+    unsigned bc = 0, bi = 0;
+    if (lane == 0) {
+      if (mc) bc = atomicAdd(ncand, static_cast<unsigned>(__popc(mc)));
+      if (mi) bi = atomicAdd(a.inf_count, static_cast<unsigned>(__popc(mi)));
+    }
+    bc = __shfl_sync(0xffffffffu, bc, 0);
+    bi = __shfl_sync(0xffffffffu, bi, 0);
+    if (is_cand) cand[bc + __popc(mc & lt)] = static_cast<std::uint32_t>(s);
+    if (inf) a.inf_queue[bi + __popc(mi & lt)] = static_cast<std::uint32_t>(s);
+  }
+}
+
+// per-lane candidate record for the flattened scan (shared memory, per warp)
+template <int D>
+struct CandSlot {
+  double c[D];
+  double r2;
+  int lo[D];
+  int span[D];
+  unsigned inv[D];  // ceil(2^16 / span)
+  unsigned self;
+  unsigned excl;    // first position of this candidate in the flattened stream
+};
+
+template <int D>
+__global__ void __launch_bounds__(kExactWarps * 32) k_border_exact(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
+                                                                   const std::uint32_t* __restrict__ cand,
+                                                                   const unsigned* __restrict__ ncand_p,
+                                                                   unsigned* __restrict__ next) {
+  __shared__ OwnerGrid<D> og;
+  __shared__ CandSlot<D> slots[kExactWarps][32];
+  __shared__ unsigned char nzl[kExactWarps][32];
+  extern __shared__ std::uint64_t s_off[];
+  if (threadIdx.x == 0) og = *ogp;
+  for (std::uint32_t j = threadIdx.x; j <= a.k; j += blockDim.x) s_off[j] = a.offsets[j];
+  __syncthreads();
+  const unsigned ncand = *ncand_p;
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned wid = threadIdx.x >> 5;
+  CandSlot<D>* sl = slots[wid];
+  unsigned char* nz = nzl[wid];
+  const unsigned full = 0xffffffffu;
+  for (;;) {
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(next, 32u);
+    base = __shfl_sync(full, base, 0);
+    if (base >= ncand) break;
+    const unsigned t = base + lane;
+    const bool has = t < ncand;
+    std::uint64_t s = 0;
+    std::uint32_t self = 0, v[D + 1];
+    double c[D], r2 = 0.0;
+    int lo[D], span[D];
+    int mode = 0;  // 0 negative, 1 flattened scan, 2 two-level scan, 3 pyramid descent
+    if (has) {
+      s = cand[t];
+      self = part_of(s_off, a.k, s);
+#pragma unroll
+      for (int j = 0; j <= D; ++j) v[j] = a.verts[std::uint64_t(j) * a.S + s];
+      double p[D + 1][D];
+      load_simplex<D>(a, v, p);
+      circumsphere_inflated<D>(p, c, &r2);
+      mode = leaf_range<D>(og, c, r2, lo, span);
+    }
+    bool pos = false;
+    if (has && mode == 3) pos = og_sphere_hits_foreign<D>(og, a.owner, c, r2, self);
+
+    // ---- mode 1: flattened (candidate, cell) stream
+    unsigned cnt = 0;
+    if (mode == 1) {
+      cnt = D == 3 ? unsigned(span[0] * span[1] * span[2]) : unsigned(span[0] * span[1]);
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        sl[lane].c[d] = c[d];
+        sl[lane].lo[d] = lo[d];
+        sl[lane].span[d] = span[d];
+        sl[lane].inv[d] = (65536u + static_cast<unsigned>(span[d]) - 1u) / static_cast<unsigned>(span[d]);
+      }
+      sl[lane].r2 = r2;
+      sl[lane].self = self;
+    }
+    unsigned incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(full, incl, o);
+      if (lane >= static_cast<unsigned>(o)) incl += y;
+    }
+    const unsigned total = __shfl_sync(full, incl, 31);
+    const unsigned excl = incl - cnt;
+    const unsigned nzmask = __ballot_sync(full, cnt > 0);
+    if (cnt) {
+      sl[lane].excl = excl;
+      nz[__popc(nzmask & ((1u << lane) - 1u))] = static_cast<unsigned char>(lane);
+    }
+    __syncwarp();
+    unsigned done = 0;
+    int cur = -1;
+    for (unsigned b0 = 0; b0 < total; b0 += 32) {
+      const bool st = cnt && excl >= b0 && excl < b0 + 32;
+      const unsigned smask = __reduce_or_sync(full, st ? 1u << (excl - b0) : 0u);
+      const unsigned q = b0 + lane;
+      bool h = false;
+      unsigned cl = 0;
+      if (q < total) {
+        cl = nz[cur + __popc(smask & ((2u << lane) - 1u))];
+        if (!((done >> cl) & 1u)) {
+          const CandSlot<D>& r = sl[cl];
+          unsigned rem = q - r.excl;
+          int cc[D];
+#pragma unroll
+          for (int d = 0; d < D; ++d) {
+            const unsigned qq = (rem * r.inv[d]) >> 16;  // rem / span (rem * span < 2^16)
+            cc[d] = r.lo[d] + static_cast<int>(rem - qq * static_cast<unsigned>(r.span[d]));
+            rem = qq;
+          }
+          const std::uint16_t code = a.owner[og_index<D>(og, 0, cc)];
+          if (code != kOwnerEmpty && code != r.self) {
+            double blo[D], bhi[D], cr[D];
+            og_block_box<D>(og, 0, cc, blo, bhi);
+#pragma unroll
+            for (int d = 0; d < D; ++d) cr[d] = r.c[d];
+            h = box_sphere<D>(blo, bhi, cr, r.r2);
+          }
+        }
+      }
+      done |= __reduce_or_sync(full, h ? 1u << cl : 0u);
+      cur += __popc(smask);
+    }
+    if (mode == 1) pos = (done >> lane) & 1u;
+    __syncwarp();
+
+    // ---- mode 2: level-1 blocks cooperatively, then the cells of partial blocks
+    unsigned todo2 = __ballot_sync(full, mode == 2);
+    while (todo2) {
+      const int l = __ffs(todo2) - 1;
+      todo2 &= todo2 - 1;
+      double cl[D];
+      int lol[D], spl[D], blo1[D], bsp[D];
+      unsigned binv[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        cl[d] = __shfl_sync(full, c[d], l);
+        lol[d] = __shfl_sync(full, lo[d], l);
+        spl[d] = __shfl_sync(full, span[d], l);
+        blo1[d] = lol[d] >> og.shift;
+        bsp[d] = ((lol[d] + spl[d] - 1) >> og.shift) - blo1[d] + 1;
+        binv[d] = (65536u + static_cast<unsigned>(bsp[d]) - 1u) / static_cast<unsigned>(bsp[d]);
+      }
+      const double rl = __shfl_sync(full, r2, l);
+      const std::uint32_t slf = __shfl_sync(full, self, l);
+      const int nblk = D == 3 ? bsp[0] * bsp[1] * bsp[2] : bsp[0] * bsp[1];
+      bool hit = false;
+      for (int i0 = 0; i0 < nblk && !hit; i0 += 32) {
+        const int i = i0 + static_cast<int>(lane);
+        bool h = false, partial = false;
+        int bc[D];
+        if (i < nblk) {
+          unsigned rem = static_cast<unsigned>(i);
+#pragma unroll
+          for (int d = 0; d < D; ++d) {
+            const unsigned qq = (rem * binv[d]) >> 16;
+            bc[d] = blo1[d] + static_cast<int>(rem - qq * static_cast<unsigned>(bsp[d]));
+            rem = qq;
+          }
+          const std::uint16_t code = a.owner[og_index<D>(og, 1, bc)];
+          if (code != kOwnerEmpty && code != slf) {
+            double blo[D], bhi[D];
+            og_block_box<D>(og, 1, bc, blo, bhi);
+            if (box_sphere<D>(blo, bhi, cl, rl)) {
+              if (box_inside_sphere<D>(blo, bhi, cl, rl)) h = true;
+              else partial = true;
+            }
+          }
+        }
+        hit = __any_sync(full, h);
+        unsigned pm = __ballot_sync(full, partial);
+        while (pm && !hit) {
+          const int pl = __ffs(pm) - 1;
+          pm &= pm - 1;
+          int pb[D];
+#pragma unroll
+          for (int d = 0; d < D; ++d) pb[d] = __shfl_sync(full, bc[d], pl);
+          bool h2 = false;
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            int cc[D];
+            og_child<D>(pb, half * 32 + static_cast<int>(lane), cc);
+            bool in = true;
+#pragma unroll
+            for (int d = 0; d < D; ++d) in = in && cc[d] >= lol[d] && cc[d] < lol[d] + spl[d];
+            if (in) {
+              const std::uint16_t code = a.owner[og_index<D>(og, 0, cc)];
+              if (code != kOwnerEmpty && code != slf) {
+                double blo[D], bhi[D];
+                og_block_box<D>(og, 0, cc, blo, bhi);
+                h2 = h2 || box_sphere<D>(blo, bhi, cl, rl);
+              }
+            }
+          }
+          hit = __any_sync(full, h2);
+        }
+      }
+      if (static_cast<int>(lane) == l) pos = hit;
+    }
+    if (has) {
+      __stcs(a.positive + s, static_cast<std::uint8_t>(pos ? 1 : 0));
+      if (pos)
+#pragma unroll
+        for (int j = 0; j <= D; ++j) a.vflags[v[j]] = 1;
+    }
   }
 }
 
@@ -724,6 +784,75 @@ __global__ void k_compact_write(const std::uint8_t* __restrict__ flags, std::uin
       if ((w[i] >> (8 * b)) & 0xFFu) out[pos++] = static_cast<std::uint32_t>(first + 4 * i + b);
 }
 
+// ---------------------------------------------------------------------------
+// Coordinate localisation for the tiled border pass. Simplex rows of part p
+// reference the points of part p, whose PointIds are scattered over the whole
+// coordinate array (ids follow input order, not space): gathering them
+// directly re-reads ~32 B sectors from HBM for every vertex (~9 GB per 10M
+// points in 3D). Bucketing the coordinates by partition once (one read, one
+// write of the array) turns those gathers into L2 hits: the rows a CTA wave
+// works on touch one or two partitions' coordinates. Row order inside a bucket
+// is irrelevant to the results (only the coordinates are read through it).
+constexpr int kLocThreads = 256;
+constexpr int kLocPerThread = 16;
+constexpr int kLocChunk = kLocThreads * kLocPerThread;
+constexpr std::uint32_t kLocMaxBuckets = 4096;
+
+__global__ void __launch_bounds__(kLocThreads) k_loc_count(const std::uint32_t* __restrict__ labels, std::uint64_t n,
+                                                           std::uint32_t div, std::uint32_t nbk,
+                                                           unsigned* __restrict__ hist) {
+  __shared__ unsigned h[kLocMaxBuckets];
+  for (std::uint32_t b = threadIdx.x; b < nbk; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += std::uint64_t(gridDim.x) * blockDim.x)
+    atomicAdd(&h[min(__ldcs(labels + i) / div, nbk - 1)], 1u);
+  __syncthreads();
+  for (std::uint32_t b = threadIdx.x; b < nbk; b += blockDim.x)
+    if (h[b]) atomicAdd(&hist[b], h[b]);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kLocThreads) k_loc_scatter(const double* __restrict__ xyz,
+                                                             const std::uint32_t* __restrict__ labels, std::uint64_t n,
+                                                             std::uint32_t div, std::uint32_t nbk,
+                                                             unsigned* __restrict__ cursor,
+                                                             double* __restrict__ xyz_loc,
+                                                             std::uint32_t* __restrict__ inv) {
+  __shared__ unsigned h[kLocMaxBuckets];
+  for (std::uint32_t b = threadIdx.x; b < nbk; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  const std::uint64_t first = std::uint64_t(blockIdx.x) * kLocChunk;
+  std::uint32_t bk[kLocPerThread];
+  unsigned rk[kLocPerThread];
+#pragma unroll
+  for (int j = 0; j < kLocPerThread; ++j) {
+    const std::uint64_t i = first + std::uint64_t(j) * kLocThreads + threadIdx.x;
+    bk[j] = i < n ? min(__ldcs(labels + i) / div, nbk - 1) : 0u;
+    rk[j] = i < n ? atomicAdd(&h[bk[j]], 1u) : 0u;
+  }
+  __syncthreads();
+  // reserve one range per bucket of this chunk
+  for (std::uint32_t b = threadIdx.x; b < nbk; b += blockDim.x)
+    if (h[b]) h[b] = atomicAdd(&cursor[b], h[b]);
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kLocPerThread; ++j) {
+    const std::uint64_t i = first + std::uint64_t(j) * kLocThreads + threadIdx.x;
+    if (i < n) {
+      const std::uint32_t pos = h[bk[j]] + rk[j];
+      inv[i] = pos;
+#pragma unroll
+      for (int d = 0; d < D; ++d) xyz_loc[std::size_t(pos) * D + d] = __ldcs(xyz + i * D + d);
+    }
+  }
+}
+
+__global__ void k_cand_count(const unsigned* ncand, std::uint64_t S, unsigned long long* counters) {
+  counters[0] = S;  // rows scanned by the prefilter (finite + infinite)
+  counters[1] = *ncand;
+}
+
 __global__ void k_u32_to_u64(const std::uint32_t* in, std::uint64_t* out) { *out = *in; }
 
 // ---------------------------------------------------------------------------
@@ -821,8 +950,34 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   SBDT_CUDA_TRY(cudaMemsetAsync(in->d_vertex_flags, 0, in->n, st));
   SBDT_CUDA_TRY(cudaMemsetAsync(infc, 0, sizeof(unsigned), st));
   tgrid.end();
+  const bool tiled = in->policy == SBDT_POLICY_GRID && !in->d_spheres && nbr3;
+  double* xyz_loc = nullptr;
+  std::uint32_t* inv = nullptr;
+  if (tiled && in->n > 0) {
+    StageTimer tl(ctx, "border.localize");
+    const std::uint32_t div = (in->k + kLocMaxBuckets - 1) / kLocMaxBuckets;
+    const std::uint32_t nbk = (in->k + div - 1) / div;
+    SBDT_WS(xl, double, "border.xyz_loc", in->n * D);
+    SBDT_WS(iv, std::uint32_t, "border.inv", in->n);
+    SBDT_WS(hist, unsigned, "border.loc_hist", nbk + 1);
+    SBDT_WS(cur, unsigned, "border.loc_cursor", nbk + 1);
+    SBDT_WS(tot, unsigned, "border.loc_total", 1);
+    xyz_loc = xl;
+    inv = iv;
+    SBDT_CUDA_TRY(cudaMemsetAsync(hist, 0, sizeof(unsigned) * (nbk + 1), st));
+    const std::uint64_t want = (in->n + kLocThreads - 1) / kLocThreads;
+    const unsigned cb = static_cast<unsigned>(want < std::uint64_t(sms) * 4 ? want : std::uint64_t(sms) * 4);
+    k_loc_count<<<cb, kLocThreads, 0, st>>>(in->d_labels, in->n, div, nbk, hist);
+    k_scan_single<<<1, kScanThreads, 0, st>>>(hist, nbk, tot);
+    SBDT_CUDA_TRY(cudaMemcpyAsync(cur, hist, sizeof(unsigned) * nbk, cudaMemcpyDeviceToDevice, st));
+    const unsigned chunks = static_cast<unsigned>((in->n + kLocChunk - 1) / kLocChunk);
+    k_loc_scatter<D><<<chunks, kLocThreads, 0, st>>>(in->d_xyz, in->d_labels, in->n, div, nbk, cur, xl, iv);
+    ctx->launches += 3;
+  }
   BorderArgs a;
   a.xyz = in->d_xyz;
+  a.xyz_loc = xyz_loc;
+  a.inv = inv;
   a.n = in->n;
   a.k = in->k;
   a.offsets = in->d_offsets;
@@ -852,12 +1007,25 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
     const std::uint64_t want = (in->S + kBThreads - 1) / kBThreads;
     const unsigned blocks = static_cast<unsigned>(want < std::uint64_t(sms) * 32 ? want : std::uint64_t(sms) * 32);
     {
-      StageTimer t(ctx, "border.finite");
-      if (in->policy == SBDT_POLICY_GRID && !in->d_spheres && nbr3) {
-        const std::uint64_t tiles = (in->S + kTile - 1) / kTile;
-        const unsigned tb = static_cast<unsigned>(tiles < std::uint64_t(sms) * 4 ? tiles : std::uint64_t(sms) * 4);
-        if (tb > 0) k_border_tiles<D><<<tb, kBThreads, offs_sh, st>>>(a, og);
+      if (tiled && in->S > 0) {
+        StageTimer ta(ctx, "border.prefilter");
+        SBDT_WS(cq, std::uint32_t, "border.cand", in->S + 32);
+        SBDT_WS(cn, unsigned, "border.cand_n", 2);
+        SBDT_CUDA_TRY(cudaMemsetAsync(cn, 0, 2 * sizeof(unsigned), st));
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_prefilter<D>, kBThreads, offs_sh);
+        std::uint64_t res = std::uint64_t(sms) * std::uint64_t(per_sm > 0 ? per_sm : 1);
+        const std::uint64_t wantA = (in->S + kBThreads - 1) / kBThreads;
+        k_border_prefilter<D><<<static_cast<unsigned>(wantA < res ? wantA : res), kBThreads, offs_sh, st>>>(a, og, cq, cn);
+        ta.end();
+        StageTimer tx(ctx, "border.exact");
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_exact<D>, kExactWarps * 32, offs_sh);
+        res = std::uint64_t(sms) * std::uint64_t(per_sm > 0 ? per_sm : 1);
+        k_border_exact<D><<<static_cast<unsigned>(res), kExactWarps * 32, offs_sh, st>>>(a, og, cq, cn, cn + 1);
+        if (a.counters) k_cand_count<<<1, 1, 0, st>>>(cn, in->S, a.counters);
+        ctx->launches += a.counters ? 3 : 2;
       } else if (blocks > 0) {
+        StageTimer t(ctx, "border.finite");
         k_border_finite<D><<<blocks, kBThreads, offs_sh, st>>>(a, og);
       }
     }
@@ -865,7 +1033,7 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
       StageTimer t(ctx, "border.infinite");
       k_border_infinite<D><<<sms * 2, 128, offs_sh, st>>>(a, og);
     }
-    ctx->launches += 2;
+    ctx->launches += (tiled && in->S > 0) ? 1 : 2;
   }
   StageTimer tc(ctx, "border.compact");
   int rc = compact_flags(ctx, in->d_vertex_flags, in->n, in->d_vertex_ids, in->d_vertex_count);

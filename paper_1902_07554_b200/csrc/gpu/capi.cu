@@ -143,7 +143,7 @@ int sbdt_gpu_border_stats(sbdt_gpu_ctx* ctx, unsigned long long* out4) {
   auto it = ctx->bufs.find("border.counters");
   if (it == ctx->bufs.end()) return SBDT_ERR_INVALID;
   cudaStreamSynchronize(ctx->stream);
-  cudaMemcpy(out4, it->second.ptr, sizeof(unsigned long long) * 8, cudaMemcpyDeviceToHost);
+  cudaMemcpy(out4, it->second.ptr, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost);
   return SBDT_OK;
 }
 

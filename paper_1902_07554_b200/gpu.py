@@ -148,8 +148,7 @@ class Context:
         out = (C.c_ulonglong * 8)()
         if lib().sbdt_gpu_border_stats(self._h, out) != SBDT_OK:
             return {}
-        return {"finite_rows": int(out[0]), "exact_stage_rows": int(out[1]), "descent_box_tests": int(out[2]),
-                "descent_expansions": int(out[3]), "start_level_hist": [int(out[4 + i]) for i in range(4)]}
+        return {"rows": int(out[0]), "exact_stage_rows": int(out[1])}
 
     # ---- device-pointer entry points (inputs resident in HBM; async on the stream)
     def assign_points_dev(self, dim, d_xyz, n, d_sample_ids, d_sample_labels, m, k, d_labels, d_part_offsets=None,
