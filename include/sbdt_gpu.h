@@ -74,10 +74,11 @@ int sbdt_gpu_stage_times(sbdt_gpu_ctx* ctx, char* names, int names_len, float* m
 /* Voronoi-label-table census of the last assign with timing enabled:
  * out3 = {uniform records, candidate-list records, overflow records}. */
 int sbdt_gpu_assign_table_stats(sbdt_gpu_ctx* ctx, unsigned* out3);
-/* Border pipeline census of the last find_border with timing enabled:
- * out4 = {rows scanned by the prefilter, rows that reached the exact stage,
- * 0, 0} (grid policy; zeros otherwise). */
-int sbdt_gpu_border_stats(sbdt_gpu_ctx* ctx, unsigned long long* out4);
+/* Border pipeline census of the last find_border with timing enabled (grid
+ * policy; zeros otherwise): out8 = {rows scanned by the prefilter, rows that
+ * reached the exact stage, exact rows by scan kind: flattened cell scan,
+ * two-level block scan, pyramid descent, 0, 0, 0}. */
+int sbdt_gpu_border_stats(sbdt_gpu_ctx* ctx, unsigned long long* out8);
 
 /* ---- assign_points -------------------------------------
  * coords: n points, AoS binary64 (PointSet::raw(), geometry.hpp:94-95).

@@ -235,15 +235,16 @@ __device__ __forceinline__ bool window_clear(const OwnerGrid<D>& og, const std::
 }
 
 // Leaf-cell range of the (inflated binary64) sphere, as og_sphere_hits_foreign
-// computes it: 0 = no cell reachable (negative), 1 = small range (spans <= 5,
-// cooperative scan), 2 = large / non-finite (pyramid descent).
+// computes it: 0 = no cell reachable (negative), 1 = spans <= 5 (flattened
+// cell scan), 2 = spans <= 16, 3 = wider or non-finite (2 and 3: pyramid
+// descent in k_border_wide).
 template <int D>
 __device__ __forceinline__ int leaf_range(const OwnerGrid<D>& og, const double* c, double r2, int* lo, int* span) {
   if (isnan(r2)) return 0;
   bool fin = isfinite(r2);
 #pragma unroll
   for (int d = 0; d < D; ++d) fin = fin && isfinite(c[d]);
-  if (!fin) return 2;
+  if (!fin) return 3;
   const double r = sqrt(r2) * (1.0 + 1e-9) + og.margin;
   int mode = 1;
 #pragma unroll
@@ -270,6 +271,17 @@ __device__ __forceinline__ std::uint32_t part_of(const std::uint64_t* offs, std:
     else hi = mid;
   }
   return lo;
+}
+
+// part_of for a warp of consecutive rows: one binary search by lane 0, the
+// lanes outside that part (warps straddling a part boundary) search alone.
+// Must be called by the full warp.
+__device__ __forceinline__ std::uint32_t part_of_warp(const std::uint64_t* offs, std::uint32_t k, std::uint64_t s) {
+  std::uint32_t p0 = 0;
+  if ((threadIdx.x & 31u) == 0) p0 = part_of(offs, k, s);
+  p0 = __shfl_sync(0xffffffffu, p0, 0);
+  if (s >= offs[p0] && s < offs[p0 + 1]) return p0;
+  return part_of(offs, k, s);
 }
 
 struct BorderArgs {
@@ -406,7 +418,7 @@ __device__ __forceinline__ void load_simplex(const BorderArgs& a, const std::uin
 
 template <int D>
 __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
-                                                                std::uint32_t* __restrict__ cand,
+                                                                std::uint32_t* __restrict__ cand, std::uint64_t cap,
                                                                 unsigned* __restrict__ ncand) {
   __shared__ OwnerGrid<D> og;
   extern __shared__ std::uint64_t s_off[];
@@ -424,9 +436,9 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
     for (int j = 0; j <= D; ++j) v[j] = valid ? __ldcs(a.verts + std::uint64_t(j) * a.S + s) : kInfVertex;
     const bool inf = valid && v[D] == kInfVertex;
     bool is_cand = false;
+    const std::uint32_t self = part_of_warp(s_off, a.k, valid ? s : a.S - 1);
     if (valid && !inf) {
       if (a.parity[s] == 0) atomicOr(a.status, kStDegenerate);
-      const std::uint32_t self = part_of(s_off, a.k, s);
       double p[D + 1][D];
       load_simplex<D>(a, v, p);
       int res = 2;  // 0 negative, 1 positive, 2 candidate
@@ -477,7 +489,12 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
     }
     bc = __shfl_sync(0xffffffffu, bc, 0);
     bi = __shfl_sync(0xffffffffu, bi, 0);
-    if (is_cand) cand[bc + __popc(mc & lt)] = static_cast<std::uint32_t>(s);
+    if (is_cand) {
+      const unsigned q = bc + __popc(mc & lt);
+      cand[q] = static_cast<std::uint32_t>(s);
+#pragma unroll
+      for (int j = 0; j <= D; ++j) cand[std::uint64_t(j + 1) * cap + q] = v[j];
+    }
     if (inf) a.inf_queue[bi + __popc(mi & lt)] = static_cast<std::uint32_t>(s);
   }
 }
@@ -494,11 +511,16 @@ struct CandSlot {
   unsigned excl;    // first position of this candidate in the flattened stream
 };
 
+// Candidates from the prefilter; rows with wide cell ranges (modes 2, 3) are
+// forwarded to the wide queue (k_border_wide).
 template <int D>
-__global__ void __launch_bounds__(kExactWarps * 32) k_border_exact(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
+__global__ void __launch_bounds__(kExactWarps * 32, 3) k_border_exact(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
                                                                    const std::uint32_t* __restrict__ cand,
+                                                                   std::uint64_t cap,
                                                                    const unsigned* __restrict__ ncand_p,
-                                                                   unsigned* __restrict__ next) {
+                                                                   unsigned* __restrict__ next,
+                                                                   std::uint32_t* __restrict__ wide,
+                                                                   unsigned* __restrict__ nwide) {
   __shared__ OwnerGrid<D> og;
   __shared__ CandSlot<D> slots[kExactWarps][32];
   __shared__ unsigned char nzl[kExactWarps][32];
@@ -528,16 +550,40 @@ __global__ void __launch_bounds__(kExactWarps * 32) k_border_exact(BorderArgs a,
       s = cand[t];
       self = part_of(s_off, a.k, s);
 #pragma unroll
-      for (int j = 0; j <= D; ++j) v[j] = a.verts[std::uint64_t(j) * a.S + s];
+      for (int j = 0; j <= D; ++j) v[j] = cand[std::uint64_t(j + 1) * cap + t];
       double p[D + 1][D];
       load_simplex<D>(a, v, p);
       circumsphere_inflated<D>(p, c, &r2);
       mode = leaf_range<D>(og, c, r2, lo, span);
     }
     bool pos = false;
-    if (has && mode == 3) pos = og_sphere_hits_foreign<D>(og, a.owner, c, r2, self);
+    if (a.counters) {
+      const unsigned m1 = __ballot_sync(full, mode == 1), m2 = __ballot_sync(full, mode == 2),
+                     m3 = __ballot_sync(full, mode == 3);
+      if (lane == 0) {
+        if (m1) atomicAdd(&a.counters[2], static_cast<unsigned long long>(__popc(m1)));
+        if (m2) atomicAdd(&a.counters[3], static_cast<unsigned long long>(__popc(m2)));
+        if (m3) atomicAdd(&a.counters[4], static_cast<unsigned long long>(__popc(m3)));
+      }
+    }
+    {
+      // forward wide ranges
+      const unsigned mw = __ballot_sync(full, mode >= 2);
+      if (mw) {
+        unsigned wb = 0;
+        if (lane == 0) wb = atomicAdd(nwide, static_cast<unsigned>(__popc(mw)));
+        wb = __shfl_sync(full, wb, 0);
+        if (mode >= 2) {
+          const unsigned q = wb + __popc(mw & ((1u << lane) - 1u));
+          wide[q] = static_cast<std::uint32_t>(s);
+#pragma unroll
+          for (int j = 0; j <= D; ++j) wide[std::uint64_t(j + 1) * cap + q] = v[j];
+        }
+      }
+    }
 
     // ---- mode 1: flattened (candidate, cell) stream
+    {
     unsigned cnt = 0;
     if (mode == 1) {
       cnt = D == 3 ? unsigned(span[0] * span[1] * span[2]) : unsigned(span[0] * span[1]);
@@ -600,79 +646,195 @@ __global__ void __launch_bounds__(kExactWarps * 32) k_border_exact(BorderArgs a,
     }
     if (mode == 1) pos = (done >> lane) & 1u;
     __syncwarp();
+    }
 
-    // ---- mode 2: level-1 blocks cooperatively, then the cells of partial blocks
-    unsigned todo2 = __ballot_sync(full, mode == 2);
-    while (todo2) {
-      const int l = __ffs(todo2) - 1;
-      todo2 &= todo2 - 1;
-      double cl[D];
-      int lol[D], spl[D], blo1[D], bsp[D];
-      unsigned binv[D];
+    if (has && mode < 2) {
+      __stcs(a.positive + s, static_cast<std::uint8_t>(pos ? 1 : 0));
+      if (pos)
+#pragma unroll
+        for (int j = 0; j <= D; ++j) a.vflags[v[j]] = 1;
+    }
+  }
+}
+
+// Wide candidates (cell range wider than 5 per axis, or non-finite spheres):
+// one warp descends the owner pyramid for one candidate at a time. A block
+// expansion reads its 64 contiguous child codes (two coalesced 64-byte loads)
+// and tests them on 32 lanes; children that are foreign, overlap the sphere
+// and are neither leaves nor contained in it go on a per-warp LIFO stack in
+// shared memory. Same decisions as og_sphere_hits_foreign (exact pruning),
+// without serialising a whole descent on one lane.
+constexpr int kWideWarps = 4;
+constexpr int kWideStack = 512;  // >= 63 * (levels - 1) + 8 for every admissible grid
+
+template <int D>
+struct WideEntry {
+  int c[D];
+  int level;
+};
+
+template <int D>
+__device__ bool warp_sphere_descent(const OwnerGrid<D>& og, const std::uint16_t* __restrict__ owner, const double* c,
+                                    double r2, std::uint32_t self, WideEntry<D>* stk) {
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned full = 0xffffffffu;
+  if (isnan(r2)) return false;
+  bool fin = isfinite(r2);
+#pragma unroll
+  for (int d = 0; d < D; ++d) fin = fin && isfinite(c[d]);
+  int a[D], b[D];
+  if (fin) {
+    const double r = sqrt(r2) * (1.0 + 1e-9) + og.margin;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const double fa = floor((c[d] - r - og.g.lo[d]) * og.inv_edge);
+      const double fb = floor((c[d] + r - og.g.lo[d]) * og.inv_edge);
+      const double top = static_cast<double>(og.ldims[0][d] - 1);
+      if (fb < 0.0 || fa > top) return false;
+      a[d] = fa < 0.0 ? 0 : static_cast<int>(fa);
+      b[d] = fb > top ? og.ldims[0][d] - 1 : static_cast<int>(fb);
+    }
+  } else {
+#pragma unroll
+    for (int d = 0; d < D; ++d) a[d] = 0, b[d] = og.ldims[0][d] - 1;
+  }
+  int L0 = 0;
+  for (; L0 < og.levels - 1; ++L0) {
+    bool ok = true;
+#pragma unroll
+    for (int d = 0; d < D; ++d) ok = ok && ((b[d] >> (L0 * og.shift)) - (a[d] >> (L0 * og.shift)) <= 1);
+    if (ok) break;
+  }
+  // returns 0 reject, 1 descend, 2 hit
+  auto test = [&](int L, const int* cc) -> int {
+    double blo[D], bhi[D];
+    og_block_box<D>(og, L, cc, blo, bhi);
+    if (!box_sphere<D>(blo, bhi, c, r2)) return 0;
+    if (L == 0 || box_inside_sphere<D>(blo, bhi, c, r2)) return 2;
+    return 1;
+  };
+  int top = 0;
+  // start blocks (<= 2 per axis)
+  {
+    int s0[D], n0[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      s0[d] = a[d] >> (L0 * og.shift);
+      n0[d] = (b[d] >> (L0 * og.shift)) - s0[d] + 1;
+    }
+    const int total = D == 3 ? n0[0] * n0[1] * n0[2] : n0[0] * n0[1];
+    int r = 0;
+    int cc[D];
+    if (static_cast<int>(lane) < total) {
+      int rem = static_cast<int>(lane);
 #pragma unroll
       for (int d = 0; d < D; ++d) {
-        cl[d] = __shfl_sync(full, c[d], l);
-        lol[d] = __shfl_sync(full, lo[d], l);
-        spl[d] = __shfl_sync(full, span[d], l);
-        blo1[d] = lol[d] >> og.shift;
-        bsp[d] = ((lol[d] + spl[d] - 1) >> og.shift) - blo1[d] + 1;
-        binv[d] = (65536u + static_cast<unsigned>(bsp[d]) - 1u) / static_cast<unsigned>(bsp[d]);
+        cc[d] = s0[d] + rem % n0[d];
+        rem /= n0[d];
       }
+      const std::uint16_t code = owner[og_index<D>(og, L0, cc)];
+      if (code != kOwnerEmpty && code != self) r = test(L0, cc);
+    }
+    if (__any_sync(full, r == 2)) return true;
+    const unsigned pm = __ballot_sync(full, r == 1);
+    if (r == 1) {
+      WideEntry<D>& e = stk[__popc(pm & ((1u << lane) - 1u))];
+#pragma unroll
+      for (int d = 0; d < D; ++d) e.c[d] = cc[d];
+      e.level = L0;
+    }
+    top = __popc(pm);
+    __syncwarp();
+  }
+  while (top > 0) {
+    const WideEntry<D> e = stk[top - 1];
+    --top;
+    __syncwarp();
+    const int lv = e.level - 1;
+    const int csh = lv * og.shift;
+    const std::uint16_t* ch = owner + og.loff[lv] + lin_i<D>(og.ldims[e.level], e.c) * 64;
+    int res[2];
+    int cc[2][D];
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int j = half * 32 + static_cast<int>(lane);
+      og_child<D>(e.c, j, cc[half]);
+      bool in = true;
+#pragma unroll
+      for (int d = 0; d < D; ++d) in = in && cc[half][d] >= (a[d] >> csh) && cc[half][d] <= (b[d] >> csh);
+      res[half] = 0;
+      if (in) {
+        const std::uint16_t code = ch[j];
+        if (code != kOwnerEmpty && code != self) res[half] = test(lv, cc[half]);
+      }
+    }
+    if (__any_sync(full, res[0] == 2 || res[1] == 2)) return true;
+    const unsigned p0 = __ballot_sync(full, res[0] == 1), p1 = __ballot_sync(full, res[1] == 1);
+    const int np = __popc(p0) + __popc(p1);
+    if (top + np > kWideStack) return og_sphere_hits_foreign<D>(og, owner, c, r2, self);  // uniform fallback
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const unsigned pm = half ? p1 : p0;
+      if (res[half] == 1) {
+        WideEntry<D>& w = stk[top + (half ? __popc(p0) : 0) + __popc(pm & ((1u << lane) - 1u))];
+#pragma unroll
+        for (int d = 0; d < D; ++d) w.c[d] = cc[half][d];
+        w.level = lv;
+      }
+    }
+    top += np;
+    __syncwarp();
+  }
+  return false;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kWideWarps * 32) k_border_wide(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
+                                                                 const std::uint32_t* __restrict__ wide,
+                                                                 std::uint64_t cap,
+                                                                 const unsigned* __restrict__ nwide_p,
+                                                                 unsigned* __restrict__ next) {
+  __shared__ OwnerGrid<D> og;
+  __shared__ WideEntry<D> stacks[kWideWarps][kWideStack];
+  extern __shared__ std::uint64_t s_off[];
+  if (threadIdx.x == 0) og = *ogp;
+  for (std::uint32_t j = threadIdx.x; j <= a.k; j += blockDim.x) s_off[j] = a.offsets[j];
+  __syncthreads();
+  const unsigned nwide = *nwide_p;
+  const unsigned lane = threadIdx.x & 31u;
+  WideEntry<D>* stk = stacks[threadIdx.x >> 5];
+  const unsigned full = 0xffffffffu;
+  for (;;) {
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(next, 32u);
+    base = __shfl_sync(full, base, 0);
+    if (base >= nwide) break;
+    const unsigned t = base + lane;
+    const bool has = t < nwide;
+    std::uint64_t s = 0;
+    std::uint32_t self = 0, v[D + 1];
+    double c[D], r2 = 0.0;
+    if (has) {
+      s = wide[t];
+      self = part_of(s_off, a.k, s);
+#pragma unroll
+      for (int j = 0; j <= D; ++j) v[j] = wide[std::uint64_t(j + 1) * cap + t];
+      double p[D + 1][D];
+      load_simplex<D>(a, v, p);
+      circumsphere_inflated<D>(p, c, &r2);
+    }
+    bool pos = false;
+    const unsigned todo0 = __ballot_sync(full, has);
+    for (unsigned todo = todo0; todo; todo &= todo - 1) {
+      const int l = __ffs(todo) - 1;
+      double cl[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) cl[d] = __shfl_sync(full, c[d], l);
       const double rl = __shfl_sync(full, r2, l);
-      const std::uint32_t slf = __shfl_sync(full, self, l);
-      const int nblk = D == 3 ? bsp[0] * bsp[1] * bsp[2] : bsp[0] * bsp[1];
-      bool hit = false;
-      for (int i0 = 0; i0 < nblk && !hit; i0 += 32) {
-        const int i = i0 + static_cast<int>(lane);
-        bool h = false, partial = false;
-        int bc[D];
-        if (i < nblk) {
-          unsigned rem = static_cast<unsigned>(i);
-#pragma unroll
-          for (int d = 0; d < D; ++d) {
-            const unsigned qq = (rem * binv[d]) >> 16;
-            bc[d] = blo1[d] + static_cast<int>(rem - qq * static_cast<unsigned>(bsp[d]));
-            rem = qq;
-          }
-          const std::uint16_t code = a.owner[og_index<D>(og, 1, bc)];
-          if (code != kOwnerEmpty && code != slf) {
-            double blo[D], bhi[D];
-            og_block_box<D>(og, 1, bc, blo, bhi);
-            if (box_sphere<D>(blo, bhi, cl, rl)) {
-              if (box_inside_sphere<D>(blo, bhi, cl, rl)) h = true;
-              else partial = true;
-            }
-          }
-        }
-        hit = __any_sync(full, h);
-        unsigned pm = __ballot_sync(full, partial);
-        while (pm && !hit) {
-          const int pl = __ffs(pm) - 1;
-          pm &= pm - 1;
-          int pb[D];
-#pragma unroll
-          for (int d = 0; d < D; ++d) pb[d] = __shfl_sync(full, bc[d], pl);
-          bool h2 = false;
-#pragma unroll
-          for (int half = 0; half < 2; ++half) {
-            int cc[D];
-            og_child<D>(pb, half * 32 + static_cast<int>(lane), cc);
-            bool in = true;
-#pragma unroll
-            for (int d = 0; d < D; ++d) in = in && cc[d] >= lol[d] && cc[d] < lol[d] + spl[d];
-            if (in) {
-              const std::uint16_t code = a.owner[og_index<D>(og, 0, cc)];
-              if (code != kOwnerEmpty && code != slf) {
-                double blo[D], bhi[D];
-                og_block_box<D>(og, 0, cc, blo, bhi);
-                h2 = h2 || box_sphere<D>(blo, bhi, cl, rl);
-              }
-            }
-          }
-          hit = __any_sync(full, h2);
-        }
-      }
+      const std::uint32_t sl = __shfl_sync(full, self, l);
+      const bool hit = warp_sphere_descent<D>(og, a.owner, cl, rl, sl, stk);
       if (static_cast<int>(lane) == l) pos = hit;
+      __syncwarp();
     }
     if (has) {
       __stcs(a.positive + s, static_cast<std::uint8_t>(pos ? 1 : 0));
@@ -1009,21 +1171,30 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
     {
       if (tiled && in->S > 0) {
         StageTimer ta(ctx, "border.prefilter");
-        SBDT_WS(cq, std::uint32_t, "border.cand", in->S + 32);
-        SBDT_WS(cn, unsigned, "border.cand_n", 2);
-        SBDT_CUDA_TRY(cudaMemsetAsync(cn, 0, 2 * sizeof(unsigned), st));
+        const std::uint64_t qcap = in->S + 32;
+        SBDT_WS(cq, std::uint32_t, "border.cand", qcap * (D + 2));
+        SBDT_WS(cn, unsigned, "border.cand_n", 4);  // {candidates, next, wide, next wide}
+        SBDT_CUDA_TRY(cudaMemsetAsync(cn, 0, 4 * sizeof(unsigned), st));
+        const std::uint64_t wcap = qcap;  // wide rows <= candidates
+        SBDT_WS(wq, std::uint32_t, "border.wide", wcap * (D + 2));
         int per_sm = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_prefilter<D>, kBThreads, offs_sh);
         std::uint64_t res = std::uint64_t(sms) * std::uint64_t(per_sm > 0 ? per_sm : 1);
         const std::uint64_t wantA = (in->S + kBThreads - 1) / kBThreads;
-        k_border_prefilter<D><<<static_cast<unsigned>(wantA < res ? wantA : res), kBThreads, offs_sh, st>>>(a, og, cq, cn);
+        k_border_prefilter<D><<<static_cast<unsigned>(wantA < res ? wantA : res), kBThreads, offs_sh, st>>>(a, og, cq, qcap, cn);
         ta.end();
         StageTimer tx(ctx, "border.exact");
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_exact<D>, kExactWarps * 32, offs_sh);
         res = std::uint64_t(sms) * std::uint64_t(per_sm > 0 ? per_sm : 1);
-        k_border_exact<D><<<static_cast<unsigned>(res), kExactWarps * 32, offs_sh, st>>>(a, og, cq, cn, cn + 1);
+        k_border_exact<D><<<static_cast<unsigned>(res), kExactWarps * 32, offs_sh, st>>>(
+            a, og, cq, qcap, cn, cn + 1, wq, cn + 2);
+        tx.end();
+        StageTimer tw(ctx, "border.exact_wide");
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_wide<D>, kWideWarps * 32, offs_sh);
+        res = std::uint64_t(sms) * std::uint64_t(per_sm > 0 ? per_sm : 1);
+        k_border_wide<D><<<static_cast<unsigned>(res), kWideWarps * 32, offs_sh, st>>>(a, og, wq, wcap, cn + 2, cn + 3);
         if (a.counters) k_cand_count<<<1, 1, 0, st>>>(cn, in->S, a.counters);
-        ctx->launches += a.counters ? 3 : 2;
+        ctx->launches += a.counters ? 4 : 3;
       } else if (blocks > 0) {
         StageTimer t(ctx, "border.finite");
         k_border_finite<D><<<blocks, kBThreads, offs_sh, st>>>(a, og);

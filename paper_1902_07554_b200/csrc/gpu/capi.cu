@@ -138,12 +138,12 @@ int sbdt_gpu_assign_table_stats(sbdt_gpu_ctx* ctx, unsigned* out3) {
   return assign_stats(ctx, out3) == kOk ? SBDT_OK : SBDT_ERR_INVALID;
 }
 
-int sbdt_gpu_border_stats(sbdt_gpu_ctx* ctx, unsigned long long* out4) {
-  if (!ctx || !out4) return SBDT_ERR_INVALID;
+int sbdt_gpu_border_stats(sbdt_gpu_ctx* ctx, unsigned long long* out8) {
+  if (!ctx || !out8) return SBDT_ERR_INVALID;
   auto it = ctx->bufs.find("border.counters");
   if (it == ctx->bufs.end()) return SBDT_ERR_INVALID;
   cudaStreamSynchronize(ctx->stream);
-  cudaMemcpy(out4, it->second.ptr, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost);
+  cudaMemcpy(out8, it->second.ptr, sizeof(unsigned long long) * 8, cudaMemcpyDeviceToHost);
   return SBDT_OK;
 }
 
