@@ -348,8 +348,7 @@ def main():
     e2e = None
     if not args.no_e2e and not args.profile:
         def pinned(a):
-            t = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True).numpy()
-            v = t.view(a.dtype).reshape(a.shape)
+            v = gpu.pinned_empty(a.shape, a.dtype)
             v[...] = a
             return v
         h_pts, h_sid, h_slab = pinned(np.ascontiguousarray(inst.points)), pinned(inst.sample_ids), pinned(inst.sample_labels)
@@ -357,17 +356,22 @@ def main():
         h_part = Partials(pinned(part.offsets), pinned(part.verts), pinned(part.nbrs), pinned(part.parity))
         ectx = gpu.Context(local)
         pol = gpu.IntersectionPolicy(args.policy, 1.0)
-        res = gpu.assign_points(h_pts, h_sid, h_slab, k, ctx=ectx)  # warm-up (allocations)
-        gpu.find_border(h_pts, res.labels, h_part, pol, hull_bfs=False, ctx=ectx)
+        # page-locked output buffers, allocated once (a serving loop reuses them)
+        out_a = gpu.Partitioning(gpu.pinned_empty(n, np.uint32), gpu.pinned_empty(k + 1, np.uint64),
+                                 gpu.pinned_empty(n, np.uint32), h_sid, h_slab, gpu.pinned_empty(2 * dim, np.float64))
+        out_b = gpu.BorderSet(gpu.pinned_empty(S, np.uint8), None, None, gpu.pinned_empty(n, np.uint32))
+        res = gpu.assign_points(h_pts, h_sid, h_slab, k, ctx=ectx, out=out_a)  # warm-up (allocations)
+        gpu.find_border(h_pts, res.labels, h_part, pol, hull_bfs=False, ctx=ectx, out=out_b)
         e2e_steps = max(1, min(args.steps, 3))
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            res = gpu.assign_points(h_pts, h_sid, h_slab, k, ctx=ectx)
-            bs = gpu.find_border(h_pts, res.labels, h_part, pol, hull_bfs=False, ctx=ectx)
+            res = gpu.assign_points(h_pts, h_sid, h_slab, k, ctx=ectx, out=out_a)
+            bs = gpu.find_border(h_pts, res.labels, h_part, pol, hull_bfs=False, ctx=ectx, out=out_b)
         t_e2e = (time.perf_counter() - t0) / e2e_steps
         assert np.array_equal(res.labels, labels)
+        # find_border without the BFS reads only the last neighbour row (hull rows)
         h2d = (inst.points.nbytes + 8 * m) + (inst.points.nbytes + 4 * n + part.offsets.nbytes + part.verts.nbytes
-                                               + part.nbrs.nbytes + part.parity.nbytes)
+                                               + 4 * S + part.parity.nbytes)
         d2h = (4 * n + 8 * (k + 1) + 4 * n + 8 * dim) + (S + 8 + 4 * len(bs.positive_vertex_ids))
         e2e = {"value": world * n / t_e2e, "unit": "points/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": round(1e3 * t_e2e, 3),

@@ -80,6 +80,12 @@ int sbdt_gpu_assign_table_stats(sbdt_gpu_ctx* ctx, unsigned* out3);
  * two-level block scan, pyramid descent, 0, 0, 0}. */
 int sbdt_gpu_border_stats(sbdt_gpu_ctx* ctx, unsigned long long* out8);
 
+/* Page-locked host memory for the host-buffer entry points' inputs and
+ * outputs (transfers from/to pageable memory are staged by the driver and
+ * fault in fresh pages). */
+int sbdt_gpu_host_alloc(uint64_t bytes, void** out);
+void sbdt_gpu_host_free(void* p);
+
 /* ---- assign_points -------------------------------------
  * coords: n points, AoS binary64 (PointSet::raw(), geometry.hpp:94-95).
  * sample_ids: m global PointIds; sample_labels: m labels < k.

@@ -50,6 +50,21 @@ int finish(sbdt_gpu_ctx* ctx) {
 
 extern "C" {
 
+int sbdt_gpu_host_alloc(uint64_t bytes, void** out) {
+  if (!out) return SBDT_ERR_INVALID;
+  *out = nullptr;
+  const cudaError_t e = cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    *out = nullptr;
+    return e == cudaErrorMemoryAllocation ? SBDT_ERR_OOM : SBDT_ERR_CUDA;
+  }
+  return SBDT_OK;
+}
+
+void sbdt_gpu_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 int sbdt_gpu_create(int device, sbdt_gpu_ctx** out) {
   if (!out) return SBDT_ERR_INVALID;
   *out = nullptr;
@@ -260,13 +275,13 @@ int sbdt_gpu_find_border(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint6
   TRY(dalloc(ctx, "h.lab", n, &d_lab));
   TRY(dalloc(ctx, "h.off", k + 1, &d_off));
   TRY(dalloc(ctx, "h.verts", S * (dim + 1), &d_verts));
+  const bool bfs = (flags & SBDT_BORDER_HULL_BFS) && border_out;
   TRY(dalloc(ctx, "h.nbrs", S * (dim + 1), &d_nbrs));
   TRY(dalloc(ctx, "h.par", S, &d_par));
   TRY(dalloc(ctx, "h.pos", S, &d_pos));
   TRY(dalloc(ctx, "h.vf", n + 64, &d_vf));
   TRY(dalloc(ctx, "h.vids", n, &d_vids));
   TRY(dalloc(ctx, "h.cnt", 1, &d_cnt));
-  const bool bfs = (flags & SBDT_BORDER_HULL_BFS) && border_out;
   if (bfs) {
     TRY(dalloc(ctx, "h.bor", S, &d_bor));
     TRY(dalloc(ctx, "h.bvf", n + 64, &d_bvf));
@@ -278,7 +293,11 @@ int sbdt_gpu_find_border(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint6
   SBDT_CUDA_TRY(cudaMemcpyAsync(d_lab, labels, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, st));
   SBDT_CUDA_TRY(cudaMemcpyAsync(d_off, offsets, sizeof(uint64_t) * (k + 1), cudaMemcpyHostToDevice, st));
   SBDT_CUDA_TRY(cudaMemcpyAsync(d_verts, verts, sizeof(uint32_t) * S * (dim + 1), cudaMemcpyHostToDevice, st));
-  SBDT_CUDA_TRY(cudaMemcpyAsync(d_nbrs, nbrs, sizeof(uint32_t) * S * (dim + 1), cudaMemcpyHostToDevice, st));
+  // Without the BFS only the hull rows' last neighbour (the finite simplex
+  // across the hull facet, row dim of the SoA) is read.
+  if (bfs) SBDT_CUDA_TRY(cudaMemcpyAsync(d_nbrs, nbrs, sizeof(uint32_t) * S * (dim + 1), cudaMemcpyHostToDevice, st));
+  else
+    SBDT_CUDA_TRY(cudaMemcpyAsync(d_nbrs + S * dim, nbrs + S * dim, sizeof(uint32_t) * S, cudaMemcpyHostToDevice, st));
   SBDT_CUDA_TRY(cudaMemcpyAsync(d_par, parity, S, cudaMemcpyHostToDevice, st));
   a.d_xyz = d_xyz;
   a.d_labels = d_lab;

@@ -45,7 +45,7 @@ class BorderArgs(C.Structure):
 
 
 EXPORTS = [
-    "sbdt_gpu_create", "sbdt_gpu_destroy", "sbdt_gpu_last_error", "sbdt_gpu_set_stream", "sbdt_gpu_synchronize",
+    "sbdt_gpu_host_alloc", "sbdt_gpu_host_free", "sbdt_gpu_create", "sbdt_gpu_destroy", "sbdt_gpu_last_error", "sbdt_gpu_set_stream", "sbdt_gpu_synchronize",
     "sbdt_gpu_launch_count", "sbdt_gpu_check_status", "sbdt_gpu_assign_points", "sbdt_gpu_assign_points_dev",
     "sbdt_gpu_find_border", "sbdt_gpu_find_border_dev",
 ]
@@ -65,6 +65,9 @@ def lib():
         vp, u64, u32, u32p, u64p, dp, i8p, u8p = (C.c_void_p, C.c_uint64, C.c_uint32, C.POINTER(C.c_uint32),
                                                   C.POINTER(C.c_uint64), C.POINTER(C.c_double), C.POINTER(C.c_int8),
                                                   C.POINTER(C.c_uint8))
+        L.sbdt_gpu_host_alloc.argtypes = [C.c_uint64, C.POINTER(vp)]
+        L.sbdt_gpu_host_free.argtypes = [vp]
+        L.sbdt_gpu_host_free.restype = None
         L.sbdt_gpu_create.argtypes = [C.c_int, C.POINTER(vp)]
         L.sbdt_gpu_destroy.argtypes = [vp]
         L.sbdt_gpu_destroy.restype = None
@@ -176,6 +179,33 @@ class Context:
 _default_ctx: Context | None = None
 
 
+class _PinnedBlock:
+    """Owner of one sbdt_gpu_host_alloc block (freed with the last view)."""
+
+    def __init__(self, nbytes: int):
+        self.ptr = C.c_void_p()
+        rc = lib().sbdt_gpu_host_alloc(max(int(nbytes), 1), C.byref(self.ptr))
+        if rc != SBDT_OK:
+            raise MemoryError(f"sbdt_gpu_host_alloc({nbytes}) failed with status {rc}")
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and self.ptr.value:
+            lib().sbdt_gpu_host_free(self.ptr)
+            self.ptr = C.c_void_p()
+
+
+def pinned_empty(shape, dtype) -> np.ndarray:
+    """Page-locked numpy array for the host-buffer entry points' inputs and
+    outputs (pageable buffers are staged by the driver and fault in fresh pages)."""
+    dtype = np.dtype(dtype)
+    shape = (shape,) if np.isscalar(shape) else tuple(shape)
+    nbytes = int(np.prod(shape, dtype=np.int64)) * dtype.itemsize
+    blk = _PinnedBlock(nbytes)
+    buf = (C.c_char * max(nbytes, 1)).from_address(blk.ptr.value)
+    buf._owner = blk  # keep the block alive as long as any view
+    return np.frombuffer(buf, dtype=dtype, count=nbytes // dtype.itemsize).reshape(shape)
+
+
 def default_context() -> Context:
     global _default_ctx
     if _default_ctx is None:
@@ -197,18 +227,29 @@ class Partitioning:
         return self.parts_ids[self.parts_offsets[i]:self.parts_offsets[i + 1]]
 
 
+def _out(buf, shape, dtype):
+    if buf is None:
+        return np.empty(shape, dtype)
+    if buf.dtype != np.dtype(dtype) or buf.shape != ((shape,) if np.isscalar(shape) else tuple(shape)) \
+            or not buf.flags.c_contiguous:
+        raise ValueError(f"output buffer must be a contiguous {np.dtype(dtype)} array of shape {shape}")
+    return buf
+
+
 def assign_points(points: np.ndarray, sample_ids: np.ndarray, sample_labels: np.ndarray, k: int,
-                  ctx: Context | None = None) -> Partitioning:
-    """assign_points through the host-buffer C ABI entry point."""
+                  ctx: Context | None = None, out: Partitioning | None = None) -> Partitioning:
+    """assign_points through the host-buffer C ABI entry point.
+    `out` (optional): a Partitioning whose labels / parts_offsets / parts_ids /
+    bbox arrays are reused as output buffers (e.g. pinned_empty arrays)."""
     ctx = ctx or default_context()
     pts = np.ascontiguousarray(points, np.float64)
     n, dim = pts.shape
     sid = np.ascontiguousarray(sample_ids, np.uint32)
     slab = np.ascontiguousarray(sample_labels, np.uint32)
-    labels = np.empty(n, np.uint32)
-    poff = np.empty(k + 1, np.uint64)
-    pids = np.empty(n, np.uint32)
-    bbox = np.empty(2 * dim, np.float64)
+    labels = _out(out.labels if out else None, n, np.uint32)
+    poff = _out(out.parts_offsets if out else None, k + 1, np.uint64)
+    pids = _out(out.parts_ids if out else None, n, np.uint32)
+    bbox = _out(out.bbox if out else None, 2 * dim, np.float64)
     rc = lib().sbdt_gpu_assign_points(ctx.handle, dim, _p(pts, C.c_double), n, _p(sid, C.c_uint32),
                                       _p(slab, C.c_uint32), len(sid), k, _p(labels, C.c_uint32),
                                       _p(poff, C.c_uint64), _p(pids, C.c_uint32), _p(bbox, C.c_double))
@@ -239,18 +280,22 @@ class BorderSet:
 
 
 def find_border(points: np.ndarray, labels: np.ndarray, partials, policy: IntersectionPolicy | None = None,
-                hull_bfs: bool = True, spheres: bool = False, ctx: Context | None = None) -> BorderSet:
-    """find_border through the host-buffer C ABI entry point."""
+                hull_bfs: bool = True, spheres: bool = False, ctx: Context | None = None,
+                out: BorderSet | None = None) -> BorderSet:
+    """find_border through the host-buffer C ABI entry point.
+    `out` (optional): a BorderSet whose positive / border arrays (length S) and
+    border_vertex_ids / positive_vertex_ids arrays (length n) are reused as
+    output buffers; the result then holds views into them."""
     ctx = ctx or default_context()
     policy = policy or IntersectionPolicy()
     pts = np.ascontiguousarray(points, np.float64)
     n, dim = pts.shape
     lab = np.ascontiguousarray(labels, np.uint32)
     S, k = partials.S, partials.k
-    pos = np.empty(S, np.uint8)
-    bor = np.empty(S, np.uint8) if hull_bfs else None
-    vids = np.empty(n, np.uint32)
-    bvids = np.empty(n, np.uint32) if hull_bfs else None
+    pos = _out(out.positive if out else None, S, np.uint8)
+    bor = _out(out.border if out else None, S, np.uint8) if hull_bfs else None
+    vids = _out(out.positive_vertex_ids if out else None, n, np.uint32)
+    bvids = _out(out.border_vertex_ids if out else None, n, np.uint32) if hull_bfs else None
     nv, nb = C.c_uint64(0), C.c_uint64(0)
     sph = np.empty((S, dim + 1), np.float64) if spheres else None
     rc = lib().sbdt_gpu_find_border(
@@ -261,5 +306,7 @@ def find_border(points: np.ndarray, labels: np.ndarray, partials, policy: Inters
         _p(bvids, C.c_uint32) if hull_bfs else None, C.byref(nb) if hull_bfs else None,
         _p(sph, C.c_double) if spheres else None)
     ctx.check(rc, "find_border")
+    if out is not None:  # views into the caller's buffers
+        return BorderSet(pos, bor, bvids[:nb.value] if hull_bfs else vids[:nv.value], vids[:nv.value], sph)
     return BorderSet(pos, bor, bvids[:nb.value].copy() if hull_bfs else vids[:nv.value].copy(),
                      vids[:nv.value].copy(), sph)

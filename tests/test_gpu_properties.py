@@ -99,3 +99,31 @@ def test_k1_no_border(ctx):
     part = host.attach_partials(inst, lab)
     g = gpu.find_border(inst.points, lab, part, ctx=ctx)
     assert g.positive.sum() == 0 and len(g.border_vertex_ids) == 0
+
+
+def test_pinned_output_buffers_match(ctx):
+    """out= buffers (page-locked) give the same results as fresh arrays, with
+    and without the BFS (the no-BFS host path uploads only the last neighbour row)."""
+    inst = host.make_instance(2, n=100_000, k=16)
+    a = gpu.assign_points(inst.points, inst.sample_ids, inst.sample_labels, 16, ctx=ctx)
+    out_a = gpu.Partitioning(gpu.pinned_empty(inst.n, np.uint32), gpu.pinned_empty(17, np.uint64),
+                             gpu.pinned_empty(inst.n, np.uint32), inst.sample_ids, inst.sample_labels,
+                             gpu.pinned_empty(6, np.float64))
+    b = gpu.assign_points(inst.points, inst.sample_ids, inst.sample_labels, 16, ctx=ctx, out=out_a)
+    assert b.labels is out_a.labels
+    assert np.array_equal(a.labels, b.labels) and np.array_equal(a.parts_ids, b.parts_ids)
+    part = host.attach_partials(inst, a.labels)
+    ref = gpu.find_border(inst.points, a.labels, part, gpu.IntersectionPolicy("grid"), ctx=ctx)
+    S = part.S
+    out_b = gpu.BorderSet(gpu.pinned_empty(S, np.uint8), gpu.pinned_empty(S, np.uint8),
+                          gpu.pinned_empty(inst.n, np.uint32), gpu.pinned_empty(inst.n, np.uint32))
+    got = gpu.find_border(inst.points, a.labels, part, gpu.IntersectionPolicy("grid"), ctx=ctx, out=out_b)
+    assert np.array_equal(got.positive, ref.positive) and np.array_equal(got.border, ref.border)
+    assert np.array_equal(got.border_vertex_ids, ref.border_vertex_ids)
+    assert np.array_equal(got.positive_vertex_ids, ref.positive_vertex_ids)
+    nob = gpu.find_border(inst.points, a.labels, part, gpu.IntersectionPolicy("grid"), hull_bfs=False, ctx=ctx)
+    assert np.array_equal(nob.positive, ref.positive)
+    assert np.array_equal(nob.positive_vertex_ids, ref.positive_vertex_ids)
+    with pytest.raises(ValueError):
+        gpu.find_border(inst.points, a.labels, part, ctx=ctx,
+                        out=gpu.BorderSet(np.empty(S + 1, np.uint8), None, None, np.empty(inst.n, np.uint32)))
