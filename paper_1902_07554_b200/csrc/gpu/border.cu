@@ -114,88 +114,121 @@ __device__ __forceinline__ void circumsphere_inflated(const double (*p)[D], doub
   }
 }
 
-// Binary32 circumsphere with an a-posteriori error bound (Cramer's rule as
-// geometry.cpp:279-327, relative to p0). Inputs p_i - p0 are formed in
-// binary64 and rounded (relative error <= 2^-24); every 2x2/3x3 determinant is
-// accompanied by its permanent P (sum of |products|); its rounding error is
-// <= 8.4e-7 P (inputs + products + sums), bounded here by g = 2e-6 P. When the
-// system is well conditioned (|det| > 4 g P_det) the centre error per axis is
-//   e_i <= g (P_Ni + |rel_i| P_det) / (|det| - g P_det) + 2^-23 |rel_i|,
-// which also dominates the binary64 evaluation's own error (~2^-29 of it).
-// Returns a centre (binary64) and a radius R such that the sphere (c, R)
-// contains the inflated binary64 sphere of circumsphere_inflated(); false
-// when ill-conditioned (the caller then runs the exact path).
+// Binary32 circumsphere with a rigorous error bound, for the prefilter only.
+// Inputs are the binary32 offsets P_j = fl(x_j - lo) of the vertices from the
+// grid origin (k_loc_scatter), so |P_j - (x_j - lo)| <= u |P_j| (u = 2^-24).
+// With a = P1 - P0, b = P2 - P0, c = P3 - P0 the circumcentre relative to P0 is
+//   rel = (|a|^2 (b x c) + |b|^2 (c x a) + |c|^2 (a x b)) / (2 a.(b x c)).
+// Error budget:
+//  - arithmetic (each term a product of at most 12 rounded factors): the
+//    numerators are within g NB and det within g DB of their values at the
+//    rounded inputs, g = 2e-6 > gamma_12, with the absolute-value sums bounded
+//    by Cauchy-Schwarz: NB = |a||b||c| (|a|+|b|+|c|), DB = sqrt(3) |a||b||c|;
+//  - input rounding: each difference is off by at most eta = 2u max|P| per
+//    axis (eta2 = sqrt(3) eta in norm); with M >= every edge length,
+//    |dn| <= 6 M^2 (2 M eta2 + eta2^2) and |ddet| <= 3 M^2 eta2 + M eta2^2.
+// With EN, ED the two totals and |det'| > 4 ED,
+//   |rel_i' - rel_i| <= (EN / 2 + |rel_i'| ED) / (|det'| - ED) + 2u |rel_i'|,
+// plus u |P0_i| for the centre's own offset. The binary64 Cramer evaluation
+// of circumsphere_inflated() is ~1e-9 of that bound from the exact centre
+// (unit roundoff 2^-53), absorbed by the 1e-6 slacks. The 2-D form is the
+// same with a x b (|dn| <= 2 (3 M^2 eta2 + M eta2^2), |ddet| <= 2 M eta2 + eta2^2).
+// Returns the centre c = lo + P0 + rel (binary64), a radius R such that the
+// ball (c, R) contains the inflated binary64 circumsphere and an inner radius
+// Rin such that (c, Rin) lies inside it; false when the bound cannot be
+// established (ill-conditioned, non-finite, binary32 under/overflow range).
+// MUFU approximations used only inside bounds that carry >= 1e-5 relative
+// slack (PTX: rcp.approx.f32 within 1 ulp, sqrt.approx.f32 within ~2^-22.)
+__device__ __forceinline__ float sqrt_apx(float x) {
+  float y;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_apx(float x) {
+  float y;
+  asm("rcp.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// floor(x) for |x| < 2^22: x + 1.5 * 2^23 rounded toward -inf lands in
+// [2^23, 2^24) where the float's bits are 0x4B400000 + floor(x).
+__device__ __forceinline__ int floor_small(float x) { return __float_as_int(__fadd_rd(x, 12582912.f)) - 0x4B400000; }
+
 template <int D>
-__device__ __forceinline__ bool enclosing_sphere_f32(const double (*p)[D], double* c, double* R,
-                                                     double* Rin = nullptr) {
+struct Sphere32 {
+  float rel[D];  // centre - P0
+  float r;       // >= |rel| (1 - 4e-6)^-1 ... see enclosing_sphere_f32
+  float e;       // centre error bound (norm), incl. P0's rounding
+};
+
+template <int D>
+__device__ __forceinline__ bool enclosing_sphere_f32(const float (*P)[D], Sphere32<D>& sp) {
   constexpr float g = 2e-6f;
-  float rel[D], err[D];
+  constexpr float u = 5.9604645e-8f;
+  float pm = 0.f;
+#pragma unroll
+  for (int j = 0; j <= D; ++j)
+#pragma unroll
+    for (int d = 0; d < D; ++d) pm = fmaxf(pm, fabsf(P[j][d]));
+  const float eta2 = 3.4642f * u * pm * 1.0001f;  // sqrt(3) * 2u * max|P|
+  float err[D];
+  float* rel = sp.rel;
   if constexpr (D == 2) {
-    const float ux = static_cast<float>(p[1][0] - p[0][0]), uy = static_cast<float>(p[1][1] - p[0][1]);
-    const float vx = static_cast<float>(p[2][0] - p[0][0]), vy = static_cast<float>(p[2][1] - p[0][1]);
-    const float bu = 0.5f * (ux * ux + uy * uy), bv = 0.5f * (vx * vx + vy * vy);
-    const float det = ux * vy - uy * vx;
-    const float pd = fabsf(ux * vy) + fabsf(uy * vx);
-    if (!(fabsf(det) > 4.f * g * pd)) return false;
-    const float n0 = bu * vy - bv * uy, p0 = fabsf(bu * vy) + fabsf(bv * uy);
-    const float n1 = ux * bv - vx * bu, p1 = fabsf(ux * bv) + fabsf(vx * bu);
-    const float den = fabsf(det) - g * pd;
-    rel[0] = n0 / det;
-    rel[1] = n1 / det;
-    err[0] = g * (p0 + fabsf(rel[0]) * pd) / den + 1.2e-7f * fabsf(rel[0]);
-    err[1] = g * (p1 + fabsf(rel[1]) * pd) / den + 1.2e-7f * fabsf(rel[1]);
+    const float ax = P[1][0] - P[0][0], ay = P[1][1] - P[0][1];
+    const float bx = P[2][0] - P[0][0], by = P[2][1] - P[0][1];
+    const float aa = ax * ax + ay * ay, bb = bx * bx + by * by;
+    const float det = ax * by - ay * bx;
+    const float la = sqrt_apx(aa) * 1.00001f, lb = sqrt_apx(bb) * 1.00001f;
+    const float L = la * lb;
+    const float M = fmaxf(la, lb) * 1.0001f + eta2;
+    const float EN = g * L * (la + lb) * 1.0001f + 2.f * (3.f * M * M * eta2 + M * eta2 * eta2);
+    const float ED = g * L * 1.0001f + 2.f * M * eta2 + eta2 * eta2;
+    if (!(L > 1e-18f) || !(L < 1e18f) || !(fabsf(det) > 4.f * ED)) return false;
+    const float inv2d = 0.5f * rcp_apx(det);
+    rel[0] = (aa * by - bb * ay) * inv2d;
+    rel[1] = (bb * ax - aa * bx) * inv2d;
+    const float rden = 1.0002f * rcp_apx(fabsf(det) - ED);
+#pragma unroll
+    for (int d = 0; d < 2; ++d)
+      err[d] = (0.5f * EN + fabsf(rel[d]) * ED) * rden + 1.5e-6f * fabsf(rel[d]) + 1.0001f * u * fabsf(P[0][d]);
   } else {
-    float m[3][3], r[3];
+    float a[3], b[3], q[3];
 #pragma unroll
-    for (int i = 0; i < 3; ++i) {
-#pragma unroll
-      for (int d = 0; d < 3; ++d) m[i][d] = static_cast<float>(p[i + 1][d] - p[0][d]);
-      r[i] = 0.5f * (m[i][0] * m[i][0] + m[i][1] * m[i][1] + m[i][2] * m[i][2]);
+    for (int d = 0; d < 3; ++d) {
+      a[d] = P[1][d] - P[0][d];
+      b[d] = P[2][d] - P[0][d];
+      q[d] = P[3][d] - P[0][d];
     }
-    // minors of the last two rows
-    const float c0 = m[1][1] * m[2][2] - m[1][2] * m[2][1], q0 = fabsf(m[1][1] * m[2][2]) + fabsf(m[1][2] * m[2][1]);
-    const float c1 = m[1][0] * m[2][2] - m[1][2] * m[2][0], q1 = fabsf(m[1][0] * m[2][2]) + fabsf(m[1][2] * m[2][0]);
-    const float c2 = m[1][0] * m[2][1] - m[1][1] * m[2][0], q2 = fabsf(m[1][0] * m[2][1]) + fabsf(m[1][1] * m[2][0]);
-    const float det = m[0][0] * c0 - m[0][1] * c1 + m[0][2] * c2;
-    const float pd = fabsf(m[0][0]) * q0 + fabsf(m[0][1]) * q1 + fabsf(m[0][2]) * q2;
-    if (!(fabsf(det) > 4.f * g * pd)) return false;
-    const float den = fabsf(det) - g * pd;
+    const float aa = a[0] * a[0] + a[1] * a[1] + a[2] * a[2];
+    const float bb = b[0] * b[0] + b[1] * b[1] + b[2] * b[2];
+    const float qq = q[0] * q[0] + q[1] * q[1] + q[2] * q[2];
+    const float x0 = b[1] * q[2] - b[2] * q[1], x1 = b[2] * q[0] - b[0] * q[2], x2 = b[0] * q[1] - b[1] * q[0];
+    const float y0 = q[1] * a[2] - q[2] * a[1], y1 = q[2] * a[0] - q[0] * a[2], y2 = q[0] * a[1] - q[1] * a[0];
+    const float z0 = a[1] * b[2] - a[2] * b[1], z1 = a[2] * b[0] - a[0] * b[2], z2 = a[0] * b[1] - a[1] * b[0];
+    const float det = a[0] * x0 + a[1] * x1 + a[2] * x2;
+    const float la = sqrt_apx(aa) * 1.00001f, lb = sqrt_apx(bb) * 1.00001f, lq = sqrt_apx(qq) * 1.00001f;
+    const float L = la * lb * lq;
+    const float M = fmaxf(la, fmaxf(lb, lq)) * 1.0001f + eta2;
+    const float EN = g * L * (la + lb + lq) * 1.0001f + 6.f * M * M * (2.f * M * eta2 + eta2 * eta2);
+    const float ED = g * 1.7321f * L * 1.0001f + 3.f * M * M * eta2 + M * eta2 * eta2;
+    if (!(L > 1e-24f) || !(L < 1e24f) || !(fabsf(det) > 4.f * ED)) return false;
+    const float inv2d = 0.5f * rcp_apx(det);
+    rel[0] = (aa * x0 + bb * y0 + qq * z0) * inv2d;
+    rel[1] = (aa * x1 + bb * y1 + qq * z1) * inv2d;
+    rel[2] = (aa * x2 + bb * y2 + qq * z2) * inv2d;
+    const float rden = 1.0002f * rcp_apx(fabsf(det) - ED);
 #pragma unroll
-    for (int col = 0; col < 3; ++col) {
-      float a[3][3];
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) a[i][j] = (j == col) ? r[i] : m[i][j];
-      const float e0 = a[1][1] * a[2][2] - a[1][2] * a[2][1], f0 = fabsf(a[1][1] * a[2][2]) + fabsf(a[1][2] * a[2][1]);
-      const float e1 = a[1][0] * a[2][2] - a[1][2] * a[2][0], f1 = fabsf(a[1][0] * a[2][2]) + fabsf(a[1][2] * a[2][0]);
-      const float e2 = a[1][0] * a[2][1] - a[1][1] * a[2][0], f2 = fabsf(a[1][0] * a[2][1]) + fabsf(a[1][1] * a[2][0]);
-      const float num = a[0][0] * e0 - a[0][1] * e1 + a[0][2] * e2;
-      const float pn = fabsf(a[0][0]) * f0 + fabsf(a[0][1]) * f1 + fabsf(a[0][2]) * f2;
-      rel[col] = num / det;
-      err[col] = g * (pn + fabsf(rel[col]) * pd) / den + 1.2e-7f * fabsf(rel[col]);
-    }
+    for (int d = 0; d < 3; ++d)
+      err[d] = (0.5f * EN + fabsf(rel[d]) * ED) * rden + 1.5e-6f * fabsf(rel[d]) + 1.0001f * u * fabsf(P[0][d]);
   }
   float rr = 0.f, ee = 0.f;
-  bool fin = true;
 #pragma unroll
   for (int d = 0; d < D; ++d) {
-    c[d] = p[0][d] + static_cast<double>(rel[d]);
     rr += rel[d] * rel[d];
     ee += err[d] * err[d];
-    fin = fin && isfinite(rel[d]) && isfinite(err[d]);
   }
-  if (!fin) return false;
-  // radius of the binary64 sphere <= |rel32| + e (+ its inflation 1e-10);
-  // the centres differ by <= e: R = |rel32| (1 + 1e-6) + 2.01 e (+ abs slack)
-  const double r32 = sqrt(static_cast<double>(rr)), e32 = sqrt(static_cast<double>(ee));
-  double mag = 0.0;
-#pragma unroll
-  for (int d = 0; d < D; ++d) mag = fmax(mag, fabs(p[0][d]));
-  *R = r32 * (1.0 + 1e-6) + 2.01 * e32 + 1e-15 * mag;
-  // INNER radius: the ball (c, Rin) lies inside the binary64 sphere, whose
-  // radius is >= |rel32| - e and whose centre is within e of c.
-  if (Rin) *Rin = r32 * (1.0 - 1e-6) - 2.01 * e32 - 1e-15 * mag;
+  if (!isfinite(rr) || !isfinite(ee)) return false;  // also catches non-finite rel / err
+  sp.r = sqrt_apx(rr);
+  sp.e = sqrt_apx(ee) * 1.0001f;
   return true;
 }
 
@@ -286,8 +319,9 @@ __device__ __forceinline__ std::uint32_t part_of_warp(const std::uint64_t* offs,
 
 struct BorderArgs {
   const double* xyz;
-  const double* xyz_loc;      // coordinates in partition-bucket order (k_loc_scatter)
-  const std::uint32_t* inv;   // PointId -> row of xyz_loc
+  const double* xyz_loc;      // coordinates in partition-bucket order, kLocStride doubles per row
+  const float* xyz_f;         // same rows: binary32 offsets from the grid origin, kLocStride floats per row
+  const std::uint32_t* inv;   // PointId -> row of xyz_loc / xyz_f
   std::uint64_t n;
   std::uint32_t k;
   const std::uint64_t* offsets;
@@ -361,16 +395,6 @@ __global__ void __launch_bounds__(kBThreads) k_border_finite(BorderArgs a, const
     for (int j = 0; j <= D; ++j)
 #pragma unroll
       for (int d = 0; d < D; ++d) p[j][d] = a.xyz[std::size_t(v[j]) * D + d];
-    if (!a.spheres && a.policy == SBDT_POLICY_GRID && a.nbr3) {
-      // Prefilter: a binary32 sphere that provably encloses the binary64 one;
-      // if its cell range sits in a 5^D window free of foreign cells, s is
-      // negative exactly.
-      double cc[D], R;
-      if (enclosing_sphere_f32<D>(p, cc, &R) && window_clear<D>(og, a.owner, a.nbr3, a.nbr5, cc, R, self)) {
-        __stcs(a.positive + s, static_cast<std::uint8_t>(0));
-        continue;
-      }
-    }
     double c[D], r2;
     circumsphere_inflated<D>(p, c, &r2);
     if (a.spheres) {
@@ -406,14 +430,103 @@ __global__ void __launch_bounds__(kBThreads) k_border_finite(BorderArgs a, const
 constexpr int kExactWarps = 8;
 
 template <int D>
+constexpr int loc_stride() {
+  return D == 3 ? 4 : 2;  // rows padded to 32 / 16 bytes (binary64) and 16 / 8 bytes (binary32)
+}
+
+template <int D>
 __device__ __forceinline__ void load_simplex(const BorderArgs& a, const std::uint32_t* v, double (*p)[D]) {
   std::uint32_t w[D + 1];
 #pragma unroll
   for (int j = 0; j <= D; ++j) w[j] = __ldg(a.inv + v[j]);
 #pragma unroll
-  for (int j = 0; j <= D; ++j)
+  for (int j = 0; j <= D; ++j) {
+    const double2* r = reinterpret_cast<const double2*>(a.xyz_loc + std::size_t(w[j]) * loc_stride<D>());
+    const double2 xy = __ldg(r);
+    p[j][0] = xy.x;
+    p[j][1] = xy.y;
+    if constexpr (D == 3) p[j][2] = __ldg(r + 1).x;
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void load_simplex_f(const BorderArgs& a, const std::uint32_t* v, float (*P)[D]) {
+  std::uint32_t w[D + 1];
 #pragma unroll
-    for (int d = 0; d < D; ++d) p[j][d] = __ldg(a.xyz_loc + std::size_t(w[j]) * D + d);
+  for (int j = 0; j <= D; ++j) w[j] = __ldg(a.inv + v[j]);
+#pragma unroll
+  for (int j = 0; j <= D; ++j) {
+    if constexpr (D == 3) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(a.xyz_f) + w[j]);
+      P[j][0] = q.x;
+      P[j][1] = q.y;
+      P[j][2] = q.z;
+    } else {
+      const float2 q = __ldg(reinterpret_cast<const float2*>(a.xyz_f) + w[j]);
+      P[j][0] = q.x;
+      P[j][1] = q.y;
+    }
+  }
+}
+
+// Prefilter decision for one finite row from its binary32 sphere:
+// 0 negative, 1 positive, 2 exact stage. Negative: the conservative cell range
+// of the enclosing ball (computed in binary32 cell units with explicit slack,
+// a superset of the exact stage's leaf range) sits in one window (the cell,
+// its 3^D or its 5^D neighbourhood) whose combined code is EMPTY or self.
+// Positive: the INNER ball (inside the binary64 sphere, checked in binary64)
+// reaches the cell of its centre and that cell holds another part.
+template <int D>
+__device__ __forceinline__ int prefilter_decide(const OwnerGrid<D>& og, const BorderArgs& a, const float (*P)[D],
+                                                const Sphere32<D>& sp, std::uint32_t self, float inv_e, float margin_c,
+                                                float lo_mag) {
+  // R >= radius of the inflated binary64 sphere + distance between centres
+  float slack = 0.f;
+#pragma unroll
+  for (int d = 0; d < D; ++d) slack = fmaxf(slack, fabsf(P[0][d]) + fabsf(sp.rel[d]));
+  slack = (slack + lo_mag) * 1e-15f;
+  const float R = (sp.r * 1.000004f + 2.01f * sp.e) * 1.000001f + slack;
+  const float Rc = R * inv_e * 1.000001f + margin_c;
+  int lo[D], w = 0;
+  int c0[D];
+  bool outside = false, inside = true;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const float Uc = (P[0][d] + sp.rel[d]) * inv_e;
+    const float sl = 4e-7f * (fabsf(Uc) + Rc) + 1e-6f;
+    const float top = static_cast<float>(og.ldims[0][d] - 1);
+    const float fl = fminf(fmaxf(Uc - Rc - sl, -2.f), top + 2.f);
+    const float fh = fminf(fmaxf(Uc + Rc + sl, -2.f), top + 2.f);
+    const int ia = floor_small(fl), ib = floor_small(fh);
+    outside = outside || ib < 0 || ia > og.ldims[0][d] - 1;
+    lo[d] = max(ia, 0);
+    w = max(w, min(ib, og.ldims[0][d] - 1) - lo[d]);
+    const int ic = floor_small(fminf(fmaxf(Uc, -2.f), top + 2.f));
+    inside = inside && ic >= 0 && ic <= og.ldims[0][d] - 1;
+    c0[d] = ic;
+  }
+  if (outside) return 0;  // the range misses the grid on some axis: no cell is reachable
+  if (w <= 4) {
+    const int h = w == 0 ? 0 : (w <= 2 ? 1 : 2);
+    int cm[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) cm[d] = min(lo[d] + h, og.ldims[0][d] - 1);
+    const std::uint16_t* src = h == 0 ? a.owner : (h == 1 ? a.nbr3 : a.nbr5);
+    const std::uint16_t code = __ldg(src + og_index<D>(og, 0, cm));
+    if (code == kOwnerEmpty || code == self) return 0;
+  }
+  // positive proof in binary64
+  if (!inside) return 2;
+  const float rin = (sp.r * 0.999996f - 2.01f * sp.e * 1.000001f) * 0.999999f - slack;
+  const double ri = static_cast<double>(rin) * (1.0 - 1e-9) - og.margin;
+  if (!(ri > 0.0)) return 2;
+  const std::uint16_t code = a.owner[og_index<D>(og, 0, c0)];
+  if (code == kOwnerEmpty || code == self) return 2;
+  double cc[D], blo[D], bhi[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) cc[d] = og.g.lo[d] + (static_cast<double>(P[0][d]) + static_cast<double>(sp.rel[d]));
+  og_block_box<D>(og, 0, c0, blo, bhi);
+  return box_sphere<D>(blo, bhi, cc, ri * ri) ? 1 : 2;
 }
 
 template <int D>
@@ -429,47 +542,41 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
   const unsigned lt = (1u << lane) - 1u;
   const std::uint64_t stride = std::uint64_t(gridDim.x) * blockDim.x;
   const std::uint64_t S_up = (a.S + 31) & ~std::uint64_t(31);  // whole warps iterate together
-  for (std::uint64_t s = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; s < S_up; s += stride) {
+  // binary32 cell-unit scale and margin (rounded up; the slacks cover the rest)
+  const float inv_e = static_cast<float>(og.inv_edge);
+  const float margin_c = static_cast<float>(og.margin * og.inv_edge) * 1.0001f + 1e-30f;
+  float lo_mag = 0.f;
+#pragma unroll
+  for (int d = 0; d < D; ++d) lo_mag = fmaxf(lo_mag, static_cast<float>(fabs(og.g.lo[d])) * 1.0001f);
+  // software pipeline: the vertex ids (and parity) of the next row are in
+  // flight while this row's coordinates are gathered and tested
+  std::uint64_t s = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  std::uint32_t vn[D + 1];
+  std::int8_t parn = 1;
+#pragma unroll
+  for (int j = 0; j <= D; ++j) vn[j] = s < a.S ? __ldcs(a.verts + std::uint64_t(j) * a.S + s) : kInfVertex;
+  if (s < a.S) parn = __ldcs(a.parity + s);
+  for (; s < S_up; s += stride) {
     const bool valid = s < a.S;
     std::uint32_t v[D + 1];
 #pragma unroll
-    for (int j = 0; j <= D; ++j) v[j] = valid ? __ldcs(a.verts + std::uint64_t(j) * a.S + s) : kInfVertex;
+    for (int j = 0; j <= D; ++j) v[j] = vn[j];
+    const std::int8_t par = parn;
+    {
+      const std::uint64_t sn = s + stride;
+#pragma unroll
+      for (int j = 0; j <= D; ++j) vn[j] = sn < a.S ? __ldcs(a.verts + std::uint64_t(j) * a.S + sn) : kInfVertex;
+      if (sn < a.S) parn = __ldcs(a.parity + sn);
+    }
     const bool inf = valid && v[D] == kInfVertex;
     bool is_cand = false;
     const std::uint32_t self = part_of_warp(s_off, a.k, valid ? s : a.S - 1);
     if (valid && !inf) {
-      if (a.parity[s] == 0) atomicOr(a.status, kStDegenerate);
-      double p[D + 1][D];
-      load_simplex<D>(a, v, p);
-      int res = 2;  // 0 negative, 1 positive, 2 candidate
-      double cc[D], R, Rin;
-      if (enclosing_sphere_f32<D>(p, cc, &R, &Rin)) {
-        if (window_clear<D>(og, a.owner, a.nbr3, a.nbr5, cc, R, self)) {
-          res = 0;
-        } else {
-          // the inner ball lies inside the binary64 sphere: if it reaches the
-          // cell of its centre and that cell holds another part, s is positive
-          const double ri = Rin * (1.0 - 1e-9) - og.margin;
-          if (ri > 0.0) {
-            int c0[D];
-            bool inside = true;
-#pragma unroll
-            for (int d = 0; d < D; ++d) {
-              const double f = floor((cc[d] - og.g.lo[d]) * og.inv_edge);
-              inside = inside && f >= 0.0 && f <= static_cast<double>(og.ldims[0][d] - 1);
-              c0[d] = inside ? static_cast<int>(f) : 0;
-            }
-            if (inside) {
-              const std::uint16_t code = a.owner[og_index<D>(og, 0, c0)];
-              if (code != kOwnerEmpty && code != self) {
-                double blo[D], bhi[D];
-                og_block_box<D>(og, 0, c0, blo, bhi);
-                if (box_sphere<D>(blo, bhi, cc, ri * ri)) res = 1;
-              }
-            }
-          }
-        }
-      }
+      if (par == 0) atomicOr(a.status, kStDegenerate);
+      float P[D + 1][D];
+      load_simplex_f<D>(a, v, P);
+      Sphere32<D> sp;
+      const int res = enclosing_sphere_f32<D>(P, sp) ? prefilter_decide<D>(og, a, P, sp, self, inv_e, margin_c, lo_mag) : 2;
       if (res == 2) {
         is_cand = true;
       } else {
@@ -979,9 +1086,13 @@ __global__ void __launch_bounds__(kLocThreads) k_loc_scatter(const double* __res
                                                              const std::uint32_t* __restrict__ labels, std::uint64_t n,
                                                              std::uint32_t div, std::uint32_t nbk,
                                                              unsigned* __restrict__ cursor,
-                                                             double* __restrict__ xyz_loc,
+                                                             const OwnerGrid<D>* __restrict__ og,
+                                                             double* __restrict__ xyz_loc, float* __restrict__ xyz_f,
                                                              std::uint32_t* __restrict__ inv) {
   __shared__ unsigned h[kLocMaxBuckets];
+  double lo[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) lo[d] = og->g.lo[d];
   for (std::uint32_t b = threadIdx.x; b < nbk; b += blockDim.x) h[b] = 0;
   __syncthreads();
   const std::uint64_t first = std::uint64_t(blockIdx.x) * kLocChunk;
@@ -1004,8 +1115,21 @@ __global__ void __launch_bounds__(kLocThreads) k_loc_scatter(const double* __res
     if (i < n) {
       const std::uint32_t pos = h[bk[j]] + rk[j];
       inv[i] = pos;
+      double x[D];
 #pragma unroll
-      for (int d = 0; d < D; ++d) xyz_loc[std::size_t(pos) * D + d] = __ldcs(xyz + i * D + d);
+      for (int d = 0; d < D; ++d) x[d] = __ldcs(xyz + i * D + d);
+      if constexpr (D == 3) {
+        double2* r = reinterpret_cast<double2*>(xyz_loc + std::size_t(pos) * 4);
+        r[0] = make_double2(x[0], x[1]);
+        r[1] = make_double2(x[2], 0.0);
+        reinterpret_cast<float4*>(xyz_f)[pos] =
+            make_float4(static_cast<float>(x[0] - lo[0]), static_cast<float>(x[1] - lo[1]),
+                        static_cast<float>(x[2] - lo[2]), 0.f);
+      } else {
+        reinterpret_cast<double2*>(xyz_loc)[pos] = make_double2(x[0], x[1]);
+        reinterpret_cast<float2*>(xyz_f)[pos] =
+            make_float2(static_cast<float>(x[0] - lo[0]), static_cast<float>(x[1] - lo[1]));
+      }
     }
   }
 }
@@ -1114,17 +1238,20 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   tgrid.end();
   const bool tiled = in->policy == SBDT_POLICY_GRID && !in->d_spheres && nbr3;
   double* xyz_loc = nullptr;
+  float* xyz_f = nullptr;
   std::uint32_t* inv = nullptr;
   if (tiled && in->n > 0) {
     StageTimer tl(ctx, "border.localize");
     const std::uint32_t div = (in->k + kLocMaxBuckets - 1) / kLocMaxBuckets;
     const std::uint32_t nbk = (in->k + div - 1) / div;
-    SBDT_WS(xl, double, "border.xyz_loc", in->n * D);
+    SBDT_WS(xl, double, "border.xyz_loc", in->n * loc_stride<D>());
+    SBDT_WS(xf, float, "border.xyz_f", in->n * loc_stride<D>());
     SBDT_WS(iv, std::uint32_t, "border.inv", in->n);
     SBDT_WS(hist, unsigned, "border.loc_hist", nbk + 1);
     SBDT_WS(cur, unsigned, "border.loc_cursor", nbk + 1);
     SBDT_WS(tot, unsigned, "border.loc_total", 1);
     xyz_loc = xl;
+    xyz_f = xf;
     inv = iv;
     SBDT_CUDA_TRY(cudaMemsetAsync(hist, 0, sizeof(unsigned) * (nbk + 1), st));
     const std::uint64_t want = (in->n + kLocThreads - 1) / kLocThreads;
@@ -1133,12 +1260,14 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
     k_scan_single<<<1, kScanThreads, 0, st>>>(hist, nbk, tot);
     SBDT_CUDA_TRY(cudaMemcpyAsync(cur, hist, sizeof(unsigned) * nbk, cudaMemcpyDeviceToDevice, st));
     const unsigned chunks = static_cast<unsigned>((in->n + kLocChunk - 1) / kLocChunk);
-    k_loc_scatter<D><<<chunks, kLocThreads, 0, st>>>(in->d_xyz, in->d_labels, in->n, div, nbk, cur, xl, iv);
+    k_loc_scatter<D><<<chunks, kLocThreads, 0, st>>>(in->d_xyz, in->d_labels, in->n, div, nbk, cur, og, xl, xf,
+                                                                 iv);
     ctx->launches += 3;
   }
   BorderArgs a;
   a.xyz = in->d_xyz;
   a.xyz_loc = xyz_loc;
+  a.xyz_f = xyz_f;
   a.inv = inv;
   a.n = in->n;
   a.k = in->k;
