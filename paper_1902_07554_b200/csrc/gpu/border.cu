@@ -155,26 +155,44 @@ __device__ __forceinline__ int floor_small(float x) { return __float_as_int(__fa
 
 template <int D>
 struct Sphere32 {
+  float P0[D];   // offset of vertex 0 from the grid origin
   float rel[D];  // centre - P0
-  float r;       // >= |rel| (1 - 4e-6)^-1 ... see enclosing_sphere_f32
-  float e;       // centre error bound (norm), incl. P0's rounding
+  float r;       // |rel| (binary32, sqrt.approx)
+  float e;       // bound on |centre - binary64 centre| (norm)
 };
 
+// Binary32 circumcentre with a rigorous error bound, for the prefilter only.
+// Inputs: the edge vectors A[j] = P_{j+1} - P0 rounded to binary32 (at most
+// two relative roundings per component), a bound eta on each component's
+// absolute error from the coordinate encoding, P0 and per-axis bounds P0e on
+// |P0 - (x0 - lo)|. With a, b, c the edges the centre relative to P0 is
+//   rel = (|a|^2 (b x c) + |b|^2 (c x a) + |c|^2 (a x b)) / (2 a.(b x c)).
+// Error budget:
+//  - arithmetic incl. the input roundings (each term a product of at most 16
+//    rounded factors): numerators within g NB and det within g DB of their
+//    values at the encoded inputs, g = 2e-6 > gamma_16, with the absolute-value
+//    sums bounded by Cauchy-Schwarz: NB = |a||b||c| (|a|+|b|+|c|),
+//    DB = sqrt(3) |a||b||c|;
+//  - encoding: with eta2 = sqrt(3) eta and M >= every edge length,
+//    |dn| <= 6 M^2 (2 M eta2 + eta2^2) and |ddet| <= 3 M^2 eta2 + M eta2^2.
+// With EN, ED the two totals and |det'| > 4 ED,
+//   |rel_i' - rel_i| <= (EN / 2 + |rel_i'| ED) / (|det'| - ED) + 1.5e-6 |rel_i'|
+// (the last term: rcp.approx and the product), plus P0e_i for the centre's
+// offset. The binary64 Cramer evaluation of circumsphere_inflated() is ~1e-9
+// of that bound from the exact centre (unit roundoff 2^-53), absorbed by the
+// 1e-6 slacks. The 2-D form is the same with a x b
+// (|dn| <= 2 (3 M^2 eta2 + M eta2^2), |ddet| <= 2 M eta2 + eta2^2).
+// false when the bound cannot be established (ill-conditioned, non-finite,
+// binary32 under/overflow range).
 template <int D>
-__device__ __forceinline__ bool enclosing_sphere_f32(const float (*P)[D], Sphere32<D>& sp) {
+__device__ __forceinline__ bool enclosing_sphere_f32(const float (*A)[D], float eta, const float* P0e,
+                                                     Sphere32<D>& sp) {
   constexpr float g = 2e-6f;
-  constexpr float u = 5.9604645e-8f;
-  float pm = 0.f;
-#pragma unroll
-  for (int j = 0; j <= D; ++j)
-#pragma unroll
-    for (int d = 0; d < D; ++d) pm = fmaxf(pm, fabsf(P[j][d]));
-  const float eta2 = 3.4642f * u * pm * 1.0001f;  // sqrt(3) * 2u * max|P|
+  const float eta2 = 1.7321f * eta * 1.0001f;
   float err[D];
   float* rel = sp.rel;
   if constexpr (D == 2) {
-    const float ax = P[1][0] - P[0][0], ay = P[1][1] - P[0][1];
-    const float bx = P[2][0] - P[0][0], by = P[2][1] - P[0][1];
+    const float ax = A[0][0], ay = A[0][1], bx = A[1][0], by = A[1][1];
     const float aa = ax * ax + ay * ay, bb = bx * bx + by * by;
     const float det = ax * by - ay * bx;
     const float la = sqrt_apx(aa) * 1.00001f, lb = sqrt_apx(bb) * 1.00001f;
@@ -188,16 +206,11 @@ __device__ __forceinline__ bool enclosing_sphere_f32(const float (*P)[D], Sphere
     rel[1] = (bb * ax - aa * bx) * inv2d;
     const float rden = 1.0002f * rcp_apx(fabsf(det) - ED);
 #pragma unroll
-    for (int d = 0; d < 2; ++d)
-      err[d] = (0.5f * EN + fabsf(rel[d]) * ED) * rden + 1.5e-6f * fabsf(rel[d]) + 1.0001f * u * fabsf(P[0][d]);
+    for (int d = 0; d < 2; ++d) err[d] = (0.5f * EN + fabsf(rel[d]) * ED) * rden + 1.5e-6f * fabsf(rel[d]) + P0e[d];
   } else {
-    float a[3], b[3], q[3];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      a[d] = P[1][d] - P[0][d];
-      b[d] = P[2][d] - P[0][d];
-      q[d] = P[3][d] - P[0][d];
-    }
+    const float* a = A[0];
+    const float* b = A[1];
+    const float* q = A[2];
     const float aa = a[0] * a[0] + a[1] * a[1] + a[2] * a[2];
     const float bb = b[0] * b[0] + b[1] * b[1] + b[2] * b[2];
     const float qq = q[0] * q[0] + q[1] * q[1] + q[2] * q[2];
@@ -217,8 +230,7 @@ __device__ __forceinline__ bool enclosing_sphere_f32(const float (*P)[D], Sphere
     rel[2] = (aa * x2 + bb * y2 + qq * z2) * inv2d;
     const float rden = 1.0002f * rcp_apx(fabsf(det) - ED);
 #pragma unroll
-    for (int d = 0; d < 3; ++d)
-      err[d] = (0.5f * EN + fabsf(rel[d]) * ED) * rden + 1.5e-6f * fabsf(rel[d]) + 1.0001f * u * fabsf(P[0][d]);
+    for (int d = 0; d < 3; ++d) err[d] = (0.5f * EN + fabsf(rel[d]) * ED) * rden + 1.5e-6f * fabsf(rel[d]) + P0e[d];
   }
   float rr = 0.f, ee = 0.f;
 #pragma unroll
@@ -230,6 +242,62 @@ __device__ __forceinline__ bool enclosing_sphere_f32(const float (*P)[D], Sphere
   sp.r = sqrt_apx(rr);
   sp.e = sqrt_apx(ee) * 1.0001f;
   return true;
+}
+
+// Decodes the packed prefilter coordinates (k_owner_mark) of one row into the
+// edge vectors, P0 and the encoding error bounds of enclosing_sphere_f32.
+//   3-D: 21-bit fixed point q with |q qh - (x - lo)| <= 0.5001 qh: edges are
+//        exact integer differences times qh (two roundings), eta = 1.0002 qh;
+//        P0 = q0 qh (two roundings): P0e = 0.5001 qh + 2.0001 u |P0|.
+//   2-D: binary32 offsets with |P - (x - lo)| <= u |P|: edges one rounding,
+//        eta = 2u max|P|, P0e = u |P0|.
+template <int D>
+__device__ __forceinline__ void decode_row(const std::uint64_t* __restrict__ xq, const std::uint32_t* v, float qh_f,
+                                           float qh_err, float (*A)[D], float* P0, float* P0e, float* eta) {
+  constexpr float u = 5.9604645e-8f;
+  std::uint64_t w[D + 1];
+#pragma unroll
+  for (int j = 0; j <= D; ++j) w[j] = __ldg(xq + v[j]);
+  if constexpr (D == 3) {
+    int q[4][3];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) q[j][d] = static_cast<int>((w[j] >> (21 * d)) & 0x1FFFFFu);
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        // |dq| < 2^21: exact in binary32 via the 1.5 * 2^23 bias
+        const float dq = __int_as_float(0x4B400000 + (q[j + 1][d] - q[0][d])) - 12582912.f;
+        A[j][d] = dq * qh_f;
+      }
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      P0[d] = (__int_as_float(0x4B000000 | q[0][d]) - 8388608.f) * qh_f;
+      P0e[d] = qh_err + 1.2e-7f * fabsf(P0[d]);
+    }
+    *eta = 2.0004f * qh_err;
+  } else {
+    float P[3][2];
+    float pm = 0.f;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      P[j][0] = __uint_as_float(static_cast<unsigned>(w[j]));
+      P[j][1] = __uint_as_float(static_cast<unsigned>(w[j] >> 32));
+      pm = fmaxf(pm, fmaxf(fabsf(P[j][0]), fabsf(P[j][1])));
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int d = 0; d < 2; ++d) A[j][d] = P[j + 1][d] - P[0][d];
+#pragma unroll
+    for (int d = 0; d < 2; ++d) {
+      P0[d] = P[0][d];
+      P0e[d] = 6e-8f * fabsf(P0[d]);
+    }
+    *eta = 2.0001f * u * pm;
+  }
 }
 
 // true iff every cell the sphere (c, R) can reach lies in one window (the
@@ -319,9 +387,7 @@ __device__ __forceinline__ std::uint32_t part_of_warp(const std::uint64_t* offs,
 
 struct BorderArgs {
   const double* xyz;
-  const double* xyz_loc;      // coordinates in partition-bucket order, kLocStride doubles per row
-  const float* xyz_f;         // same rows: binary32 offsets from the grid origin, kLocStride floats per row
-  const std::uint32_t* inv;   // PointId -> row of xyz_loc / xyz_f
+  const std::uint64_t* xq;    // packed prefilter coordinates by PointId (k_owner_mark)
   std::uint64_t n;
   std::uint32_t k;
   const std::uint64_t* offsets;
@@ -430,43 +496,11 @@ __global__ void __launch_bounds__(kBThreads) k_border_finite(BorderArgs a, const
 constexpr int kExactWarps = 8;
 
 template <int D>
-constexpr int loc_stride() {
-  return D == 3 ? 4 : 2;  // rows padded to 32 / 16 bytes (binary64) and 16 / 8 bytes (binary32)
-}
-
-template <int D>
 __device__ __forceinline__ void load_simplex(const BorderArgs& a, const std::uint32_t* v, double (*p)[D]) {
-  std::uint32_t w[D + 1];
 #pragma unroll
-  for (int j = 0; j <= D; ++j) w[j] = __ldg(a.inv + v[j]);
+  for (int j = 0; j <= D; ++j)
 #pragma unroll
-  for (int j = 0; j <= D; ++j) {
-    const double2* r = reinterpret_cast<const double2*>(a.xyz_loc + std::size_t(w[j]) * loc_stride<D>());
-    const double2 xy = __ldg(r);
-    p[j][0] = xy.x;
-    p[j][1] = xy.y;
-    if constexpr (D == 3) p[j][2] = __ldg(r + 1).x;
-  }
-}
-
-template <int D>
-__device__ __forceinline__ void load_simplex_f(const BorderArgs& a, const std::uint32_t* v, float (*P)[D]) {
-  std::uint32_t w[D + 1];
-#pragma unroll
-  for (int j = 0; j <= D; ++j) w[j] = __ldg(a.inv + v[j]);
-#pragma unroll
-  for (int j = 0; j <= D; ++j) {
-    if constexpr (D == 3) {
-      const float4 q = __ldg(reinterpret_cast<const float4*>(a.xyz_f) + w[j]);
-      P[j][0] = q.x;
-      P[j][1] = q.y;
-      P[j][2] = q.z;
-    } else {
-      const float2 q = __ldg(reinterpret_cast<const float2*>(a.xyz_f) + w[j]);
-      P[j][0] = q.x;
-      P[j][1] = q.y;
-    }
-  }
+    for (int d = 0; d < D; ++d) p[j][d] = __ldg(a.xyz + std::size_t(v[j]) * D + d);
 }
 
 // Prefilter decision for one finite row from its binary32 sphere:
@@ -477,13 +511,12 @@ __device__ __forceinline__ void load_simplex_f(const BorderArgs& a, const std::u
 // Positive: the INNER ball (inside the binary64 sphere, checked in binary64)
 // reaches the cell of its centre and that cell holds another part.
 template <int D>
-__device__ __forceinline__ int prefilter_decide(const OwnerGrid<D>& og, const BorderArgs& a, const float (*P)[D],
-                                                const Sphere32<D>& sp, std::uint32_t self, float inv_e, float margin_c,
+__device__ __forceinline__ int prefilter_decide(const OwnerGrid<D>& og, const BorderArgs& a, const Sphere32<D>& sp, std::uint32_t self, float inv_e, float margin_c,
                                                 float lo_mag) {
   // R >= radius of the inflated binary64 sphere + distance between centres
   float slack = 0.f;
 #pragma unroll
-  for (int d = 0; d < D; ++d) slack = fmaxf(slack, fabsf(P[0][d]) + fabsf(sp.rel[d]));
+  for (int d = 0; d < D; ++d) slack = fmaxf(slack, fabsf(sp.P0[d]) + fabsf(sp.rel[d]));
   slack = (slack + lo_mag) * 1e-15f;
   const float R = (sp.r * 1.000004f + 2.01f * sp.e) * 1.000001f + slack;
   const float Rc = R * inv_e * 1.000001f + margin_c;
@@ -492,7 +525,7 @@ __device__ __forceinline__ int prefilter_decide(const OwnerGrid<D>& og, const Bo
   bool outside = false, inside = true;
 #pragma unroll
   for (int d = 0; d < D; ++d) {
-    const float Uc = (P[0][d] + sp.rel[d]) * inv_e;
+    const float Uc = (sp.P0[d] + sp.rel[d]) * inv_e;
     const float sl = 4e-7f * (fabsf(Uc) + Rc) + 1e-6f;
     const float top = static_cast<float>(og.ldims[0][d] - 1);
     const float fl = fminf(fmaxf(Uc - Rc - sl, -2.f), top + 2.f);
@@ -524,7 +557,7 @@ __device__ __forceinline__ int prefilter_decide(const OwnerGrid<D>& og, const Bo
   if (code == kOwnerEmpty || code == self) return 2;
   double cc[D], blo[D], bhi[D];
 #pragma unroll
-  for (int d = 0; d < D; ++d) cc[d] = og.g.lo[d] + (static_cast<double>(P[0][d]) + static_cast<double>(sp.rel[d]));
+  for (int d = 0; d < D; ++d) cc[d] = og.g.lo[d] + (static_cast<double>(sp.P0[d]) + static_cast<double>(sp.rel[d]));
   og_block_box<D>(og, 0, c0, blo, bhi);
   return box_sphere<D>(blo, bhi, cc, ri * ri) ? 1 : 2;
 }
@@ -548,6 +581,8 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
   float lo_mag = 0.f;
 #pragma unroll
   for (int d = 0; d < D; ++d) lo_mag = fmaxf(lo_mag, static_cast<float>(fabs(og.g.lo[d])) * 1.0001f);
+  const float qh_f = static_cast<float>(og.qh);
+  const float qh_err = static_cast<float>(og.qh) * 0.50011f;
   // software pipeline: the vertex ids (and parity) of the next row are in
   // flight while this row's coordinates are gathered and tested
   std::uint64_t s = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -573,10 +608,11 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
     const std::uint32_t self = part_of_warp(s_off, a.k, valid ? s : a.S - 1);
     if (valid && !inf) {
       if (par == 0) atomicOr(a.status, kStDegenerate);
-      float P[D + 1][D];
-      load_simplex_f<D>(a, v, P);
+      float A[D][D], P0e[D], eta;
       Sphere32<D> sp;
-      const int res = enclosing_sphere_f32<D>(P, sp) ? prefilter_decide<D>(og, a, P, sp, self, inv_e, margin_c, lo_mag) : 2;
+      decode_row<D>(a.xq, v, qh_f, qh_err, A, sp.P0, P0e, &eta);
+      const int res = enclosing_sphere_f32<D>(A, eta, P0e, sp)
+                          ? prefilter_decide<D>(og, a, sp, self, inv_e, margin_c, lo_mag) : 2;
       if (res == 2) {
         is_cand = true;
       } else {
@@ -1053,87 +1089,6 @@ __global__ void k_compact_write(const std::uint8_t* __restrict__ flags, std::uin
       if ((w[i] >> (8 * b)) & 0xFFu) out[pos++] = static_cast<std::uint32_t>(first + 4 * i + b);
 }
 
-// ---------------------------------------------------------------------------
-// Coordinate localisation for the tiled border pass. Simplex rows of part p
-// reference the points of part p, whose PointIds are scattered over the whole
-// coordinate array (ids follow input order, not space): gathering them
-// directly re-reads ~32 B sectors from HBM for every vertex (~9 GB per 10M
-// points in 3D). Bucketing the coordinates by partition once (one read, one
-// write of the array) turns those gathers into L2 hits: the rows a CTA wave
-// works on touch one or two partitions' coordinates. Row order inside a bucket
-// is irrelevant to the results (only the coordinates are read through it).
-constexpr int kLocThreads = 256;
-constexpr int kLocPerThread = 16;
-constexpr int kLocChunk = kLocThreads * kLocPerThread;
-constexpr std::uint32_t kLocMaxBuckets = 4096;
-
-__global__ void __launch_bounds__(kLocThreads) k_loc_count(const std::uint32_t* __restrict__ labels, std::uint64_t n,
-                                                           std::uint32_t div, std::uint32_t nbk,
-                                                           unsigned* __restrict__ hist) {
-  __shared__ unsigned h[kLocMaxBuckets];
-  for (std::uint32_t b = threadIdx.x; b < nbk; b += blockDim.x) h[b] = 0;
-  __syncthreads();
-  for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += std::uint64_t(gridDim.x) * blockDim.x)
-    atomicAdd(&h[min(__ldcs(labels + i) / div, nbk - 1)], 1u);
-  __syncthreads();
-  for (std::uint32_t b = threadIdx.x; b < nbk; b += blockDim.x)
-    if (h[b]) atomicAdd(&hist[b], h[b]);
-}
-
-template <int D>
-__global__ void __launch_bounds__(kLocThreads) k_loc_scatter(const double* __restrict__ xyz,
-                                                             const std::uint32_t* __restrict__ labels, std::uint64_t n,
-                                                             std::uint32_t div, std::uint32_t nbk,
-                                                             unsigned* __restrict__ cursor,
-                                                             const OwnerGrid<D>* __restrict__ og,
-                                                             double* __restrict__ xyz_loc, float* __restrict__ xyz_f,
-                                                             std::uint32_t* __restrict__ inv) {
-  __shared__ unsigned h[kLocMaxBuckets];
-  double lo[D];
-#pragma unroll
-  for (int d = 0; d < D; ++d) lo[d] = og->g.lo[d];
-  for (std::uint32_t b = threadIdx.x; b < nbk; b += blockDim.x) h[b] = 0;
-  __syncthreads();
-  const std::uint64_t first = std::uint64_t(blockIdx.x) * kLocChunk;
-  std::uint32_t bk[kLocPerThread];
-  unsigned rk[kLocPerThread];
-#pragma unroll
-  for (int j = 0; j < kLocPerThread; ++j) {
-    const std::uint64_t i = first + std::uint64_t(j) * kLocThreads + threadIdx.x;
-    bk[j] = i < n ? min(__ldcs(labels + i) / div, nbk - 1) : 0u;
-    rk[j] = i < n ? atomicAdd(&h[bk[j]], 1u) : 0u;
-  }
-  __syncthreads();
-  // reserve one range per bucket of this chunk
-  for (std::uint32_t b = threadIdx.x; b < nbk; b += blockDim.x)
-    if (h[b]) h[b] = atomicAdd(&cursor[b], h[b]);
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < kLocPerThread; ++j) {
-    const std::uint64_t i = first + std::uint64_t(j) * kLocThreads + threadIdx.x;
-    if (i < n) {
-      const std::uint32_t pos = h[bk[j]] + rk[j];
-      inv[i] = pos;
-      double x[D];
-#pragma unroll
-      for (int d = 0; d < D; ++d) x[d] = __ldcs(xyz + i * D + d);
-      if constexpr (D == 3) {
-        double2* r = reinterpret_cast<double2*>(xyz_loc + std::size_t(pos) * 4);
-        r[0] = make_double2(x[0], x[1]);
-        r[1] = make_double2(x[2], 0.0);
-        reinterpret_cast<float4*>(xyz_f)[pos] =
-            make_float4(static_cast<float>(x[0] - lo[0]), static_cast<float>(x[1] - lo[1]),
-                        static_cast<float>(x[2] - lo[2]), 0.f);
-      } else {
-        reinterpret_cast<double2*>(xyz_loc)[pos] = make_double2(x[0], x[1]);
-        reinterpret_cast<float2*>(xyz_f)[pos] =
-            make_float2(static_cast<float>(x[0] - lo[0]), static_cast<float>(x[1] - lo[1]));
-      }
-    }
-  }
-}
-
 __global__ void k_cand_count(const unsigned* ncand, std::uint64_t S, unsigned long long* counters) {
   counters[0] = S;  // rows scanned by the prefilter (finite + infinite)
   counters[1] = *ncand;
@@ -1181,6 +1136,12 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
     pbbox = pb;
   }
 
+  const bool tiled = in->policy == SBDT_POLICY_GRID && !in->d_spheres;
+  std::uint64_t* xq = nullptr;
+  if (tiled) {
+    SBDT_WS(q, std::uint64_t, "border.xq", in->n + 1);
+    xq = q;
+  }
   StageTimer tgrid(ctx, "border.grid");
   const unsigned long long* bb = reinterpret_cast<const unsigned long long*>(in->d_bbox_ordered);
   if (!bb) {
@@ -1201,7 +1162,8 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
     const std::uint64_t want = (in->n + 255) / 256;
     const unsigned blocks = static_cast<unsigned>(want < std::uint64_t(sms) * 16 ? want : std::uint64_t(sms) * 16);
     const std::size_t sh = pbbox ? sizeof(unsigned long long) * in->k * 2 * D : 0;
-    k_owner_mark<D><<<blocks > 0 ? blocks : 1, 256, sh, st>>>(in->d_xyz, in->d_labels, in->n, og, owner, pbbox, in->k);
+    k_owner_mark<D><<<blocks > 0 ? blocks : 1, 256, sh, st>>>(in->d_xyz, in->d_labels, in->n, og, owner, pbbox, in->k,
+                                                               xq);
   }
   k_owner_level<D><<<sms * 8, 256, 0, st>>>(og, owner, 1);
   k_owner_level<D><<<sms * 2, 256, 0, st>>>(og, owner, 2);
@@ -1236,39 +1198,9 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   SBDT_CUDA_TRY(cudaMemsetAsync(in->d_vertex_flags, 0, in->n, st));
   SBDT_CUDA_TRY(cudaMemsetAsync(infc, 0, sizeof(unsigned), st));
   tgrid.end();
-  const bool tiled = in->policy == SBDT_POLICY_GRID && !in->d_spheres && nbr3;
-  double* xyz_loc = nullptr;
-  float* xyz_f = nullptr;
-  std::uint32_t* inv = nullptr;
-  if (tiled && in->n > 0) {
-    StageTimer tl(ctx, "border.localize");
-    const std::uint32_t div = (in->k + kLocMaxBuckets - 1) / kLocMaxBuckets;
-    const std::uint32_t nbk = (in->k + div - 1) / div;
-    SBDT_WS(xl, double, "border.xyz_loc", in->n * loc_stride<D>());
-    SBDT_WS(xf, float, "border.xyz_f", in->n * loc_stride<D>());
-    SBDT_WS(iv, std::uint32_t, "border.inv", in->n);
-    SBDT_WS(hist, unsigned, "border.loc_hist", nbk + 1);
-    SBDT_WS(cur, unsigned, "border.loc_cursor", nbk + 1);
-    SBDT_WS(tot, unsigned, "border.loc_total", 1);
-    xyz_loc = xl;
-    xyz_f = xf;
-    inv = iv;
-    SBDT_CUDA_TRY(cudaMemsetAsync(hist, 0, sizeof(unsigned) * (nbk + 1), st));
-    const std::uint64_t want = (in->n + kLocThreads - 1) / kLocThreads;
-    const unsigned cb = static_cast<unsigned>(want < std::uint64_t(sms) * 4 ? want : std::uint64_t(sms) * 4);
-    k_loc_count<<<cb, kLocThreads, 0, st>>>(in->d_labels, in->n, div, nbk, hist);
-    k_scan_single<<<1, kScanThreads, 0, st>>>(hist, nbk, tot);
-    SBDT_CUDA_TRY(cudaMemcpyAsync(cur, hist, sizeof(unsigned) * nbk, cudaMemcpyDeviceToDevice, st));
-    const unsigned chunks = static_cast<unsigned>((in->n + kLocChunk - 1) / kLocChunk);
-    k_loc_scatter<D><<<chunks, kLocThreads, 0, st>>>(in->d_xyz, in->d_labels, in->n, div, nbk, cur, og, xl, xf,
-                                                                 iv);
-    ctx->launches += 3;
-  }
   BorderArgs a;
   a.xyz = in->d_xyz;
-  a.xyz_loc = xyz_loc;
-  a.xyz_f = xyz_f;
-  a.inv = inv;
+  a.xq = xq;
   a.n = in->n;
   a.k = in->k;
   a.offsets = in->d_offsets;

@@ -31,6 +31,7 @@ struct OwnerGrid {
   Grid<D> g;
   double inv_edge;
   double margin;
+  double qh;   // 3-D fixed-point step of the prefilter's packed coordinates (k_owner_mark)
   int levels;  // levels incl. leaf level 0; the top level has exactly one block
   int shift;   // log2 per-axis fanout
   int ldims[kMaxLevels][D];
@@ -111,6 +112,11 @@ __global__ void k_owner_params(const unsigned long long* bbox, std::uint64_t n, 
   }
   og->g.edge = bad ? 1.0 : e;
   og->inv_edge = 1.0 / og->g.edge;
+  {
+    double span = 0.0;  // the grid covers the bbox: dims * edge >= extent
+    for (int d = 0; d < D; ++d) span = fmax(span, static_cast<double>(og->g.dims[d]) * og->g.edge);
+    og->qh = span / 2097151.0;  // 21 bits per axis
+  }
   og->margin = 1e-9 * (mag + ext_max + og->g.edge);
   constexpr int sh = og_shift<D>();
   og->shift = sh;
@@ -146,7 +152,8 @@ __global__ void k_owner_params(const unsigned long long* bbox, std::uint64_t n, 
 template <int D>
 __global__ void k_owner_mark(const double* __restrict__ xyz, const std::uint32_t* __restrict__ labels, std::uint64_t n,
                              const OwnerGrid<D>* __restrict__ ogp, std::uint16_t* __restrict__ owner,
-                             unsigned long long* __restrict__ pbbox, std::uint32_t k) {
+                             unsigned long long* __restrict__ pbbox, std::uint32_t k,
+                             std::uint64_t* __restrict__ xq = nullptr) {
   __shared__ OwnerGrid<D> og;
   extern __shared__ unsigned long long s_pb[];  // [k][2D] when pbbox != nullptr
   if (threadIdx.x == 0) og = *ogp;
@@ -162,6 +169,24 @@ __global__ void k_owner_mark(const double* __restrict__ xyz, const std::uint32_t
     for (int d = 0; d < D; ++d) {
       x[d] = xyz[i * D + d];
       c[d] = static_cast<int>(cell_coord<D>(og.g, x[d], d));
+    }
+    if (xq) {
+      // packed prefilter coordinates, indexed by PointId: 3-D 21-bit fixed
+      // point of (x - lo) / qh (|error| <= qh / 2), 2-D the binary32 offsets
+      // fl(x - lo) (|error| <= u |offset|)
+      if constexpr (D == 3) {
+        std::uint64_t w = 0;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const double t = rint((x[d] - og.g.lo[d]) / og.qh);
+          const std::uint64_t q = t <= 0.0 ? 0ull : (t >= 2097151.0 ? 2097151ull : static_cast<std::uint64_t>(t));
+          w |= q << (21 * d);
+        }
+        xq[i] = w;
+      } else {
+        const float fx = static_cast<float>(x[0] - og.g.lo[0]), fy = static_cast<float>(x[1] - og.g.lo[1]);
+        xq[i] = static_cast<std::uint64_t>(__float_as_uint(fx)) | (static_cast<std::uint64_t>(__float_as_uint(fy)) << 32);
+      }
     }
     const std::uint32_t lab = labels[i];
     std::uint16_t* slot = owner + og_index<D>(og, 0, c);
