@@ -512,7 +512,7 @@ __device__ __forceinline__ void load_simplex(const BorderArgs& a, const std::uin
 // reaches the cell of its centre and that cell holds another part.
 template <int D>
 __device__ __forceinline__ int prefilter_decide(const OwnerGrid<D>& og, const BorderArgs& a, const Sphere32<D>& sp, std::uint32_t self, float inv_e, float margin_c,
-                                                float lo_mag) {
+                                                float lo_mag, bool pos_ok) {
   // R >= radius of the inflated binary64 sphere + distance between centres
   float slack = 0.f;
 #pragma unroll
@@ -523,10 +523,12 @@ __device__ __forceinline__ int prefilter_decide(const OwnerGrid<D>& og, const Bo
   int lo[D], w = 0;
   int c0[D];
   bool outside = false, inside = true;
+  float sl_max = 0.f;
 #pragma unroll
   for (int d = 0; d < D; ++d) {
     const float Uc = (sp.P0[d] + sp.rel[d]) * inv_e;
     const float sl = 4e-7f * (fabsf(Uc) + Rc) + 1e-6f;
+    sl_max = fmaxf(sl_max, sl);
     const float top = static_cast<float>(og.ldims[0][d] - 1);
     const float fl = fminf(fmaxf(Uc - Rc - sl, -2.f), top + 2.f);
     const float fh = fminf(fmaxf(Uc + Rc + sl, -2.f), top + 2.f);
@@ -548,18 +550,17 @@ __device__ __forceinline__ int prefilter_decide(const OwnerGrid<D>& og, const Bo
     const std::uint16_t code = __ldg(src + og_index<D>(og, 0, cm));
     if (code == kOwnerEmpty || code == self) return 0;
   }
-  // positive proof in binary64
-  if (!inside) return 2;
-  const float rin = (sp.r * 0.999996f - 2.01f * sp.e * 1.000001f) * 0.999999f - slack;
-  const double ri = static_cast<double>(rin) * (1.0 - 1e-9) - og.margin;
-  if (!(ri > 0.0)) return 2;
+  // Positive proof, in binary32 cell units: c0 = floor(Uc) holds Uc, the real
+  // centre lies within sqrt(D) sl of Uc, and the cell box in cell units is
+  // [c0, c0 + 1] up to the binary64 rounding of cell_lo (< 1e-7 cells while
+  // (|lo| / edge + dims) < 2^26, checked by the caller through pos_ok). If the
+  // inner ball, shrunk by the exact stage's margin, still reaches that box,
+  // the binary64 box test on the binary64 sphere accepts it.
+  if (!inside || !pos_ok) return 2;
+  const float rin_c = ((sp.r * 0.999996f - 2.01f * sp.e * 1.000001f) * 0.999999f - slack) * inv_e * 0.999998f;
+  if (!(rin_c - margin_c > 1.7321f * sl_max + 1e-7f)) return 2;
   const std::uint16_t code = a.owner[og_index<D>(og, 0, c0)];
-  if (code == kOwnerEmpty || code == self) return 2;
-  double cc[D], blo[D], bhi[D];
-#pragma unroll
-  for (int d = 0; d < D; ++d) cc[d] = og.g.lo[d] + (static_cast<double>(sp.P0[d]) + static_cast<double>(sp.rel[d]));
-  og_block_box<D>(og, 0, c0, blo, bhi);
-  return box_sphere<D>(blo, bhi, cc, ri * ri) ? 1 : 2;
+  return (code == kOwnerEmpty || code == self) ? 2 : 1;
 }
 
 template <int D>
@@ -581,11 +582,16 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
   float lo_mag = 0.f;
 #pragma unroll
   for (int d = 0; d < D; ++d) lo_mag = fmaxf(lo_mag, static_cast<float>(fabs(og.g.lo[d])) * 1.0001f);
+  bool pos_ok = true;
+#pragma unroll
+  for (int d = 0; d < D; ++d)
+    pos_ok = pos_ok && fabs(og.g.lo[d]) * og.inv_edge + static_cast<double>(og.ldims[0][d]) < 67108864.0;
   const float qh_f = static_cast<float>(og.qh);
   const float qh_err = static_cast<float>(og.qh) * 0.50011f;
   // software pipeline: the vertex ids (and parity) of the next row are in
   // flight while this row's coordinates are gathered and tested
   std::uint64_t s = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  std::uint32_t self = part_of(s_off, a.k, s < a.S ? s : (a.S ? a.S - 1 : 0));
   std::uint32_t vn[D + 1];
   std::int8_t parn = 1;
 #pragma unroll
@@ -605,14 +611,18 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
     }
     const bool inf = valid && v[D] == kInfVertex;
     bool is_cand = false;
-    const std::uint32_t self = part_of_warp(s_off, a.k, valid ? s : a.S - 1);
+    // rows only grow along the grid-stride loop: advance the part cursor
+    {
+      const std::uint64_t sc = valid ? s : a.S - 1;
+      while (self + 1 < a.k && s_off[self + 1] <= sc) ++self;
+    }
     if (valid && !inf) {
       if (par == 0) atomicOr(a.status, kStDegenerate);
       float A[D][D], P0e[D], eta;
       Sphere32<D> sp;
       decode_row<D>(a.xq, v, qh_f, qh_err, A, sp.P0, P0e, &eta);
       const int res = enclosing_sphere_f32<D>(A, eta, P0e, sp)
-                          ? prefilter_decide<D>(og, a, sp, self, inv_e, margin_c, lo_mag) : 2;
+                          ? prefilter_decide<D>(og, a, sp, self, inv_e, margin_c, lo_mag, pos_ok) : 2;
       if (res == 2) {
         is_cand = true;
       } else {
