@@ -1182,26 +1182,10 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   if (in->policy == SBDT_POLICY_GRID) {
     SBDT_WS(n3, std::uint16_t, "border.nbr3", owner_len);
     SBDT_WS(n5, std::uint16_t, "border.nbr5", owner_len);
-    SBDT_WS(tmp, std::uint16_t, "border.nbrtmp", owner_len);
     nbr3 = n3;
     nbr5 = n5;
-    const unsigned nbk = static_cast<unsigned>(sms) * 8;
-    // separable W=1 passes: owner -> nbr3 -> nbr5 (ping-pong through tmp)
-    std::uint16_t* src = owner;
-    for (int rep = 0; rep < 2; ++rep) {
-      std::uint16_t* out = rep == 0 ? nbr3 : nbr5;
-      if constexpr (D == 3) {
-        k_nbr_pass<D><<<nbk, 256, 0, st>>>(og, src, tmp, 0);
-        k_nbr_pass<D><<<nbk, 256, 0, st>>>(og, tmp, out, 1);
-        k_nbr_pass<D><<<nbk, 256, 0, st>>>(og, out, tmp, 2);
-        SBDT_CUDA_TRY(cudaMemcpyAsync(out, tmp, sizeof(std::uint16_t) * owner_len, cudaMemcpyDeviceToDevice, st));
-      } else {
-        k_nbr_pass<D><<<nbk, 256, 0, st>>>(og, src, tmp, 0);
-        k_nbr_pass<D><<<nbk, 256, 0, st>>>(og, tmp, out, 1);
-      }
-      src = out;
-    }
-    ctx->launches += 2 * D;
+    k_nbr_tiles<D><<<sms * 8, 256, 0, st>>>(og, owner, nbr3, nbr5);
+    ctx->launches += 1;
   }
   ctx->launches += 6;
 

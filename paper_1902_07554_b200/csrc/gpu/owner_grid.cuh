@@ -279,34 +279,99 @@ __global__ void k_owner_levels_tail(const OwnerGrid<D>* __restrict__ ogp, std::u
 // around c, clipped to the grid. The combine is a semilattice (EMPTY
 // identity, MULTI absorbing), so the box filter is separable (one 1-D pass of
 // half-width 1 per axis), and a 3-window of 3-windows is the 5-window.
-constexpr int kNbrW = 1;
+// Both neighbourhood code arrays in one pass: each CTA loads a tile of
+// kNbrTile^D leaf cells plus a 2-cell halo into shared memory (EMPTY outside
+// the grid), runs the separable 3-window three times (-> 3^D codes, valid one
+// cell into the halo) and three more times (-> 5^D codes), and writes both
+// for its tile.
+template <int D>
+constexpr int nbr_tile() {
+  return D == 3 ? 8 : 32;
+}
 
 template <int D>
-__global__ void k_nbr_pass(const OwnerGrid<D>* __restrict__ ogp, const std::uint16_t* __restrict__ src,
-                           std::uint16_t* __restrict__ dst, int axis) {
+__global__ void __launch_bounds__(256) k_nbr_tiles(const OwnerGrid<D>* __restrict__ ogp,
+                                                   const std::uint16_t* __restrict__ owner,
+                                                   std::uint16_t* __restrict__ nbr3, std::uint16_t* __restrict__ nbr5) {
+  constexpr int T = nbr_tile<D>();
+  constexpr int RS = T + 4;
+  constexpr int RN = D == 3 ? RS * RS * RS : RS * RS;
+  constexpr int ON = D == 3 ? T * T * T : T * T;
   __shared__ OwnerGrid<D> og;
+  __shared__ std::uint16_t bufA[RN], bufB[RN];
   if (threadIdx.x == 0) og = *ogp;
   __syncthreads();
-  unsigned long long cnt = 1;
+  int nt[D];
+  unsigned long long ntiles = 1;
 #pragma unroll
-  for (int d = 0; d < D; ++d) cnt *= static_cast<unsigned>(og.ldims[0][d]);
-  for (unsigned long long id = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; id < cnt;
-       id += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
-    int c[D];
-    unsigned long long rem = id;
+  for (int d = 0; d < D; ++d) {
+    nt[d] = (og.ldims[0][d] + T - 1) / T;
+    ntiles *= static_cast<unsigned long long>(nt[d]);
+  }
+  for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  int tc[D];
+  unsigned long long rem = tile;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    tc[d] = static_cast<int>(rem % static_cast<unsigned>(nt[d]));
+    rem /= static_cast<unsigned>(nt[d]);
+  }
+  auto coords = [](int r, int* c) {
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      c[d] = static_cast<int>(rem % static_cast<unsigned>(og.ldims[0][d]));
-      rem /= static_cast<unsigned>(og.ldims[0][d]);
+      c[d] = r % RS;
+      r /= RS;
     }
-    const int c0 = c[axis];
-    std::uint16_t code = kOwnerEmpty;
-    for (int t = max(c0 - kNbrW, 0); t <= min(c0 + kNbrW, og.ldims[0][axis] - 1); ++t) {
-      c[axis] = t;
-      code = og_combine(code, src[og_index<D>(og, 0, c)]);
+  };
+  for (int r = threadIdx.x; r < RN; r += blockDim.x) {
+    int c[D];
+    coords(r, c);
+    bool in = true;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      c[d] += tc[d] * T - 2;
+      in = in && c[d] >= 0 && c[d] < og.ldims[0][d];
     }
-    c[axis] = c0;
-    dst[og_index<D>(og, 0, c)] = code;
+    bufA[r] = in ? owner[og_index<D>(og, 0, c)] : kOwnerEmpty;
+  }
+  __syncthreads();
+  std::uint16_t* src = bufA;
+  std::uint16_t* dst = bufB;
+  for (int rep = 0; rep < 2; ++rep) {
+#pragma unroll
+    for (int ax = 0; ax < D; ++ax) {
+      const int st = ax == 0 ? 1 : (ax == 1 ? RS : RS * RS);
+      for (int r = threadIdx.x; r < RN; r += blockDim.x) {
+        int c[D];
+        coords(r, c);
+        std::uint16_t v = src[r];
+        if (c[ax] >= 1 && c[ax] <= RS - 2) v = og_combine(og_combine(src[r - st], v), src[r + st]);
+        dst[r] = v;
+      }
+      __syncthreads();
+      std::uint16_t* t = src;
+      src = dst;
+      dst = t;
+    }
+    std::uint16_t* out = rep == 0 ? nbr3 : nbr5;
+    for (int o = threadIdx.x; o < ON; o += blockDim.x) {
+      int c[D];
+      int oo = o, r = 0, mul = 1;
+      bool in = true;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const int t = oo % T;
+        oo /= T;
+        c[d] = tc[d] * T + t;
+        in = in && c[d] < og.ldims[0][d];
+        r += (t + 2) * mul;
+        mul *= RS;
+      }
+      if (in) out[og_index<D>(og, 0, c)] = src[r];
+    }
+    // src holds the 3^D codes; the second round combines them again
+  }
+  __syncthreads();  // the buffers are reloaded for the next tile
   }
 }
 
