@@ -279,99 +279,104 @@ __global__ void k_owner_levels_tail(const OwnerGrid<D>* __restrict__ ogp, std::u
 // around c, clipped to the grid. The combine is a semilattice (EMPTY
 // identity, MULTI absorbing), so the box filter is separable (one 1-D pass of
 // half-width 1 per axis), and a 3-window of 3-windows is the 5-window.
-// Both neighbourhood code arrays in one pass: each CTA loads a tile of
-// kNbrTile^D leaf cells plus a 2-cell halo into shared memory (EMPTY outside
-// the grid), runs the separable 3-window three times (-> 3^D codes, valid one
-// cell into the halo) and three more times (-> 5^D codes), and writes both
-// for its tile.
-template <int D>
-constexpr int nbr_tile() {
-  return D == 3 ? 8 : 32;
-}
-
+// Both neighbourhood code arrays in one pass. A CTA owns a tile of 2^D
+// pyramid blocks (8^3 cells in 3-D, 16^2 in 2-D) and stages it with a 2-cell
+// halo in shared memory (EMPTY outside the grid); three separable 3-window
+// passes give the 3^D codes (valid one cell into the halo), three more the
+// 5^D codes. Tiles are block-aligned, so every global index is a 32-bit
+// block offset plus the sub-cell bits, and the stores are whole 64-code blocks.
 template <int D>
 __global__ void __launch_bounds__(256) k_nbr_tiles(const OwnerGrid<D>* __restrict__ ogp,
                                                    const std::uint16_t* __restrict__ owner,
                                                    std::uint16_t* __restrict__ nbr3, std::uint16_t* __restrict__ nbr5) {
-  constexpr int T = nbr_tile<D>();
-  constexpr int RS = T + 4;
+  constexpr int F = og_fan<D>();
+  constexpr int SH = og_shift<D>();
+  constexpr int T = 2 * F;      // tile cells per axis
+  constexpr int RS = T + 4;     // staged cells per axis
   constexpr int RN = D == 3 ? RS * RS * RS : RS * RS;
   constexpr int ON = D == 3 ? T * T * T : T * T;
   __shared__ OwnerGrid<D> og;
   __shared__ std::uint16_t bufA[RN], bufB[RN];
   if (threadIdx.x == 0) og = *ogp;
   __syncthreads();
-  int nt[D];
+  if (og.levels < 2) {  // a single cell
+    if (blockIdx.x == 0 && threadIdx.x == 0) nbr3[og.loff[0]] = nbr5[og.loff[0]] = owner[og.loff[0]];
+    return;
+  }
+  int nt[D], bd1[D], cd0[D];
   unsigned long long ntiles = 1;
 #pragma unroll
   for (int d = 0; d < D; ++d) {
-    nt[d] = (og.ldims[0][d] + T - 1) / T;
+    bd1[d] = og.ldims[1][d];
+    cd0[d] = og.ldims[0][d];
+    nt[d] = (bd1[d] + 1) / 2;
     ntiles *= static_cast<unsigned long long>(nt[d]);
   }
-  for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-  int tc[D];
-  unsigned long long rem = tile;
+  const std::uint16_t* own0 = owner + og.loff[0];
+  auto gindex = [&](const int* c) -> unsigned long long {  // level-0 tiled index
+    unsigned b = static_cast<unsigned>(c[D - 1] >> SH), sub = 0;
 #pragma unroll
-  for (int d = 0; d < D; ++d) {
-    tc[d] = static_cast<int>(rem % static_cast<unsigned>(nt[d]));
-    rem /= static_cast<unsigned>(nt[d]);
-  }
-  auto coords = [](int r, int* c) {
+    for (int d = D - 2; d >= 0; --d) b = b * static_cast<unsigned>(bd1[d]) + static_cast<unsigned>(c[d] >> SH);
 #pragma unroll
-    for (int d = 0; d < D; ++d) {
-      c[d] = r % RS;
-      r /= RS;
-    }
+    for (int d = 0; d < D; ++d) sub |= static_cast<unsigned>(c[d] & (F - 1)) << (SH * d);
+    return static_cast<unsigned long long>(b) * 64u + sub;
   };
-  for (int r = threadIdx.x; r < RN; r += blockDim.x) {
-    int c[D];
-    coords(r, c);
-    bool in = true;
+  for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    int org[D];
+    unsigned long long rem = tile;
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      c[d] += tc[d] * T - 2;
-      in = in && c[d] >= 0 && c[d] < og.ldims[0][d];
+      org[d] = static_cast<int>(rem % static_cast<unsigned>(nt[d])) * T;
+      rem /= static_cast<unsigned>(nt[d]);
     }
-    bufA[r] = in ? owner[og_index<D>(og, 0, c)] : kOwnerEmpty;
-  }
-  __syncthreads();
-  std::uint16_t* src = bufA;
-  std::uint16_t* dst = bufB;
-  for (int rep = 0; rep < 2; ++rep) {
-#pragma unroll
-    for (int ax = 0; ax < D; ++ax) {
-      const int st = ax == 0 ? 1 : (ax == 1 ? RS : RS * RS);
-      for (int r = threadIdx.x; r < RN; r += blockDim.x) {
-        int c[D];
-        coords(r, c);
-        std::uint16_t v = src[r];
-        if (c[ax] >= 1 && c[ax] <= RS - 2) v = og_combine(og_combine(src[r - st], v), src[r + st]);
-        dst[r] = v;
-      }
-      __syncthreads();
-      std::uint16_t* t = src;
-      src = dst;
-      dst = t;
-    }
-    std::uint16_t* out = rep == 0 ? nbr3 : nbr5;
-    for (int o = threadIdx.x; o < ON; o += blockDim.x) {
-      int c[D];
-      int oo = o, r = 0, mul = 1;
+    for (int r = threadIdx.x; r < RN; r += blockDim.x) {
+      int c[D], rr = r;
       bool in = true;
 #pragma unroll
       for (int d = 0; d < D; ++d) {
-        const int t = oo % T;
-        oo /= T;
-        c[d] = tc[d] * T + t;
-        in = in && c[d] < og.ldims[0][d];
-        r += (t + 2) * mul;
-        mul *= RS;
+        c[d] = org[d] - 2 + rr % RS;
+        rr /= RS;
+        in = in && c[d] >= 0 && c[d] < cd0[d];
       }
-      if (in) out[og_index<D>(og, 0, c)] = src[r];
+      bufA[r] = in ? own0[gindex(c)] : kOwnerEmpty;
     }
-    // src holds the 3^D codes; the second round combines them again
-  }
-  __syncthreads();  // the buffers are reloaded for the next tile
+    __syncthreads();
+    std::uint16_t* src = bufA;
+    std::uint16_t* dst = bufB;
+    for (int rep = 0; rep < 2; ++rep) {
+#pragma unroll
+      for (int ax = 0; ax < D; ++ax) {
+        constexpr int st0 = 1;
+        const int st = ax == 0 ? st0 : (ax == 1 ? RS : RS * RS);
+        for (int r = threadIdx.x; r < RN; r += blockDim.x) {
+          const int ca = (ax == 0 ? r : (ax == 1 ? r / RS : r / (RS * RS))) % RS;
+          std::uint16_t v = src[r];
+          if (ca >= 1 && ca <= RS - 2) v = og_combine(og_combine(src[r - st], v), src[r + st]);
+          dst[r] = v;
+        }
+        __syncthreads();
+        std::uint16_t* t = src;
+        src = dst;
+        dst = t;
+      }
+      // store the tile in tiled order: output o = block-major, sub-cell minor
+      std::uint16_t* out = (rep == 0 ? nbr3 : nbr5) + og.loff[0];
+      for (int o = threadIdx.x; o < ON; o += blockDim.x) {
+        const int b = o >> 6, sub = o & 63;
+        int c[D], r = 0, mul = 1;
+        bool in = true;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const int t = ((b >> d) & 1) * F + ((sub >> (SH * d)) & (F - 1));
+          c[d] = org[d] + t;
+          in = in && c[d] < cd0[d];
+          r += (t + 2) * mul;
+          mul *= RS;
+        }
+        if (in) out[gindex(c)] = src[r];
+      }
+    }
+    __syncthreads();  // the buffers are reloaded for the next tile
   }
 }
 
