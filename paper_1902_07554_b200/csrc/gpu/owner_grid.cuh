@@ -279,21 +279,27 @@ __global__ void k_owner_levels_tail(const OwnerGrid<D>* __restrict__ ogp, std::u
 // around c, clipped to the grid. The combine is a semilattice (EMPTY
 // identity, MULTI absorbing), so the box filter is separable (one 1-D pass of
 // half-width 1 per axis), and a 3-window of 3-windows is the 5-window.
-// Both neighbourhood code arrays in one pass. A CTA owns a tile of 2^D
-// pyramid blocks (8^3 cells in 3-D, 16^2 in 2-D) and stages it with a 2-cell
-// halo in shared memory (EMPTY outside the grid); three separable 3-window
-// passes give the 3^D codes (valid one cell into the halo), three more the
-// 5^D codes. Tiles are block-aligned, so every global index is a 32-bit
-// block offset plus the sub-cell bits, and the stores are whole 64-code blocks.
+// Both neighbourhood code arrays in one pass. A CTA owns a block-aligned
+// tile (16^3 cells in 3-D, 64^2 in 2-D) and stages it with a 2-cell halo in
+// shared memory (EMPTY outside the grid). Three separable 3-window passes
+// give the 3^D codes (valid one cell into the halo), three more the 5^D
+// codes; each pass runs one thread per grid line with a sliding window.
+template <int D>
+constexpr int nbr_tile() {
+  return D == 3 ? 16 : 64;
+}
+
 template <int D>
 __global__ void __launch_bounds__(256) k_nbr_tiles(const OwnerGrid<D>* __restrict__ ogp,
                                                    const std::uint16_t* __restrict__ owner,
                                                    std::uint16_t* __restrict__ nbr3, std::uint16_t* __restrict__ nbr5) {
   constexpr int F = og_fan<D>();
   constexpr int SH = og_shift<D>();
-  constexpr int T = 2 * F;      // tile cells per axis
+  constexpr int T = nbr_tile<D>();
+  constexpr int TB = T / F;     // tile blocks per axis
   constexpr int RS = T + 4;     // staged cells per axis
   constexpr int RN = D == 3 ? RS * RS * RS : RS * RS;
+  constexpr int LN = D == 3 ? RS * RS : RS;   // lines per pass
   constexpr int ON = D == 3 ? T * T * T : T * T;
   __shared__ OwnerGrid<D> og;
   __shared__ std::uint16_t bufA[RN], bufB[RN];
@@ -309,7 +315,7 @@ __global__ void __launch_bounds__(256) k_nbr_tiles(const OwnerGrid<D>* __restric
   for (int d = 0; d < D; ++d) {
     bd1[d] = og.ldims[1][d];
     cd0[d] = og.ldims[0][d];
-    nt[d] = (bd1[d] + 1) / 2;
+    nt[d] = (bd1[d] + TB - 1) / TB;
     ntiles *= static_cast<unsigned long long>(nt[d]);
   }
   const std::uint16_t* own0 = owner + og.loff[0];
@@ -346,13 +352,26 @@ __global__ void __launch_bounds__(256) k_nbr_tiles(const OwnerGrid<D>* __restric
     for (int rep = 0; rep < 2; ++rep) {
 #pragma unroll
       for (int ax = 0; ax < D; ++ax) {
-        constexpr int st0 = 1;
-        const int st = ax == 0 ? st0 : (ax == 1 ? RS : RS * RS);
-        for (int r = threadIdx.x; r < RN; r += blockDim.x) {
-          const int ca = (ax == 0 ? r : (ax == 1 ? r / RS : r / (RS * RS))) % RS;
-          std::uint16_t v = src[r];
-          if (ca >= 1 && ca <= RS - 2) v = og_combine(og_combine(src[r - st], v), src[r + st]);
-          dst[r] = v;
+        const int st = ax == 0 ? 1 : (ax == 1 ? RS : RS * RS);
+        for (int l = threadIdx.x; l < LN; l += blockDim.x) {
+          // line l: the other coordinates, in increasing axis order
+          int base;
+          if constexpr (D == 3) {
+            const int u = l % RS, w = l / RS;
+            base = ax == 0 ? (u * RS + w * RS * RS) : (ax == 1 ? (u + w * RS * RS) : (u + w * RS));
+          } else {
+            base = ax == 0 ? l * RS : l;
+          }
+          std::uint16_t prev = src[base], cur = src[base + st];
+          dst[base] = prev;
+#pragma unroll 6
+          for (int i = 1; i < RS - 1; ++i) {
+            const std::uint16_t next = src[base + (i + 1) * st];
+            dst[base + i * st] = og_combine(og_combine(prev, cur), next);
+            prev = cur;
+            cur = next;
+          }
+          dst[base + (RS - 1) * st] = cur;
         }
         __syncthreads();
         std::uint16_t* t = src;
@@ -363,11 +382,12 @@ __global__ void __launch_bounds__(256) k_nbr_tiles(const OwnerGrid<D>* __restric
       std::uint16_t* out = (rep == 0 ? nbr3 : nbr5) + og.loff[0];
       for (int o = threadIdx.x; o < ON; o += blockDim.x) {
         const int b = o >> 6, sub = o & 63;
-        int c[D], r = 0, mul = 1;
+        int c[D], r = 0, mul = 1, bb = b;
         bool in = true;
 #pragma unroll
         for (int d = 0; d < D; ++d) {
-          const int t = ((b >> d) & 1) * F + ((sub >> (SH * d)) & (F - 1));
+          const int t = (bb % TB) * F + ((sub >> (SH * d)) & (F - 1));
+          bb /= TB;
           c[d] = org[d] + t;
           in = in && c[d] < cd0[d];
           r += (t + 2) * mul;
