@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(kBThreads) k_border_finite(BorderArgs a, const
 //      use the two-level cooperative scan, huge ones the pyramid descent.
 // A only concludes for spheres that contain / are contained in the exact
 // binary64 sphere, so the flags equal the exact test's.
-constexpr int kExactWarps = 8;
+constexpr int kExactWarps = 4;
 
 template <int D>
 __device__ __forceinline__ void load_simplex(const BorderArgs& a, const std::uint32_t* v, double (*p)[D]) {
@@ -655,10 +655,16 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
 // per-lane candidate record for the flattened scan (shared memory, per warp)
 template <int D>
 struct CandSlot {
-  double c[D];
+  // per axis and cell of the range: the cell's term of the level-0 tiled
+  // index and its squared gap to the centre, so a cell's index is a sum and
+  // box_sphere's d2 is ((g0^2 + g1^2) + g2^2) exactly as box_sphere forms it
+  struct Ent {
+    unsigned long long off;
+    double g2;
+  };
+  Ent ent[D][5];
   double r2;
-  int lo[D];
-  int span[D];
+  unsigned span[D];
   unsigned inv[D];  // ceil(2^16 / span)
   unsigned self;
   unsigned excl;    // first position of this candidate in the flattened stream
@@ -667,7 +673,7 @@ struct CandSlot {
 // Candidates from the prefilter; rows with wide cell ranges (modes 2, 3) are
 // forwarded to the wide queue (k_border_wide).
 template <int D>
-__global__ void __launch_bounds__(kExactWarps * 32, 3) k_border_exact(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
+__global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
                                                                    const std::uint32_t* __restrict__ cand,
                                                                    std::uint64_t cap,
                                                                    const unsigned* __restrict__ ncand_p,
@@ -685,6 +691,11 @@ __global__ void __launch_bounds__(kExactWarps * 32, 3) k_border_exact(BorderArgs
   const unsigned lane = threadIdx.x & 31u;
   const unsigned wid = threadIdx.x >> 5;
   CandSlot<D>* sl = slots[wid];
+  const bool multi_level = og.levels > 1;
+  unsigned long long bst[D];  // level-1 block strides of the tiled level-0 index
+  bst[0] = 1;
+#pragma unroll
+  for (int d = 1; d < D; ++d) bst[d] = bst[d - 1] * static_cast<unsigned long long>(multi_level ? og.ldims[1][d - 1] : 1);
   unsigned char* nz = nzl[wid];
   const unsigned full = 0xffffffffu;
   for (;;) {
@@ -740,12 +751,26 @@ __global__ void __launch_bounds__(kExactWarps * 32, 3) k_border_exact(BorderArgs
     unsigned cnt = 0;
     if (mode == 1) {
       cnt = D == 3 ? unsigned(span[0] * span[1] * span[2]) : unsigned(span[0] * span[1]);
+      constexpr int SH = og_shift<D>();
+      constexpr int F = og_fan<D>();
 #pragma unroll
       for (int d = 0; d < D; ++d) {
-        sl[lane].c[d] = c[d];
-        sl[lane].lo[d] = lo[d];
-        sl[lane].span[d] = span[d];
+        sl[lane].span[d] = static_cast<unsigned>(span[d]);
         sl[lane].inv[d] = (65536u + static_cast<unsigned>(span[d]) - 1u) / static_cast<unsigned>(span[d]);
+        for (int i = 0; i < span[d]; ++i) {
+          const int cell = lo[d] + i;
+          const unsigned long long off =
+              multi_level ? (static_cast<unsigned long long>(cell >> SH) * bst[d]) * 64ull +
+                                (static_cast<unsigned long long>(cell & (F - 1)) << (SH * d))
+                          : 0ull;
+          const long long last1 = (static_cast<long long>(cell) + 1) > og.g.dims[d] ? og.g.dims[d] : cell + 1;
+          const double blo = cell_lo<D>(og.g, cell, d), bhi = cell_lo<D>(og.g, last1, d);
+          double g = 0.0;
+          if (c[d] < blo) g = blo - c[d];
+          else if (c[d] > bhi) g = c[d] - bhi;
+          sl[lane].ent[d][i].off = off;
+          sl[lane].ent[d][i].g2 = g * g;
+        }
       }
       sl[lane].r2 = r2;
       sl[lane].self = self;
@@ -764,38 +789,50 @@ __global__ void __launch_bounds__(kExactWarps * 32, 3) k_border_exact(BorderArgs
       nz[__popc(nzmask & ((1u << lane) - 1u))] = static_cast<unsigned char>(lane);
     }
     __syncwarp();
+    // Chunks of 32 (candidate, cell) pairs, kChunkUnroll at a time: the owner
+    // code loads of a group are independent (no early exit between chunks),
+    // so their L2 latencies overlap.
     unsigned done = 0;
     int cur = -1;
-    for (unsigned b0 = 0; b0 < total; b0 += 32) {
-      const bool st = cnt && excl >= b0 && excl < b0 + 32;
-      const unsigned smask = __reduce_or_sync(full, st ? 1u << (excl - b0) : 0u);
-      const unsigned q = b0 + lane;
-      bool h = false;
-      unsigned cl = 0;
-      if (q < total) {
-        cl = nz[cur + __popc(smask & ((2u << lane) - 1u))];
-        if (!((done >> cl) & 1u)) {
+    constexpr int kChunkUnroll = 4;
+    for (unsigned g0 = 0; g0 < total; g0 += 32 * kChunkUnroll) {
+      std::uint16_t code[kChunkUnroll];
+      unsigned clv[kChunkUnroll];
+      bool geo[kChunkUnroll];
+#pragma unroll
+      for (int u = 0; u < kChunkUnroll; ++u) {
+        const unsigned b0 = g0 + 32u * u;
+        const bool st = cnt && excl >= b0 && excl < b0 + 32;
+        const unsigned smask = __reduce_or_sync(full, st ? 1u << (excl - b0) : 0u);
+        const unsigned q = b0 + lane;
+        code[u] = kOwnerEmpty;
+        clv[u] = 0;
+        geo[u] = false;
+        if (q < total) {
+          const unsigned cl = nz[cur + __popc(smask & ((2u << lane) - 1u))];
           const CandSlot<D>& r = sl[cl];
           unsigned rem = q - r.excl;
-          int cc[D];
+          unsigned long long idx = og.loff[0];
+          double d2 = 0.0;
 #pragma unroll
           for (int d = 0; d < D; ++d) {
             const unsigned qq = (rem * r.inv[d]) >> 16;  // rem / span (rem * span < 2^16)
-            cc[d] = r.lo[d] + static_cast<int>(rem - qq * static_cast<unsigned>(r.span[d]));
+            const typename CandSlot<D>::Ent& e = r.ent[d][rem - qq * r.span[d]];
+            idx += e.off;
+            d2 += e.g2;
             rem = qq;
           }
-          const std::uint16_t code = a.owner[og_index<D>(og, 0, cc)];
-          if (code != kOwnerEmpty && code != r.self) {
-            double blo[D], bhi[D], cr[D];
-            og_block_box<D>(og, 0, cc, blo, bhi);
-#pragma unroll
-            for (int d = 0; d < D; ++d) cr[d] = r.c[d];
-            h = box_sphere<D>(blo, bhi, cr, r.r2);
-          }
+          clv[u] = cl;
+          geo[u] = d2 <= r.r2;
+          if (geo[u]) code[u] = __ldg(a.owner + idx);
         }
+        cur += __popc(smask);
       }
-      done |= __reduce_or_sync(full, h ? 1u << cl : 0u);
-      cur += __popc(smask);
+#pragma unroll
+      for (int u = 0; u < kChunkUnroll; ++u) {
+        const bool h = geo[u] && code[u] != kOwnerEmpty && code[u] != sl[clv[u]].self;
+        done |= __reduce_or_sync(full, h ? 1u << clv[u] : 0u);
+      }
     }
     if (mode == 1) pos = (done >> lane) & 1u;
     __syncwarp();
