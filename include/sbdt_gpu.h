@@ -72,8 +72,9 @@ int sbdt_gpu_check_status(sbdt_gpu_ctx* ctx);
 int sbdt_gpu_set_timing(sbdt_gpu_ctx* ctx, int enable);
 int sbdt_gpu_stage_times(sbdt_gpu_ctx* ctx, char* names, int names_len, float* ms, int max_stages);
 /* Voronoi-label-table census of the last assign with timing enabled:
- * out3 = {uniform records, candidate-list records, overflow records}. */
-int sbdt_gpu_assign_table_stats(sbdt_gpu_ctx* ctx, unsigned* out3);
+ * out4 = {uniform records, short-list records, ring-search records,
+ * long-list records}. */
+int sbdt_gpu_assign_table_stats(sbdt_gpu_ctx* ctx, unsigned* out4);
 /* Border pipeline census of the last find_border with timing enabled (grid
  * policy; zeros otherwise): out8 = {rows scanned by the prefilter, rows that
  * reached the exact stage, exact rows by scan kind: flattened cell scan,

@@ -367,6 +367,10 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
   const unsigned long long fine = cap * fine_per_cell<D>();
   SBDT_WS(heads, std::uint32_t, "assign.heads", fine);
   SBDT_WS(slab, VltEntry, "assign.slab", fine * kSlots);
+  const unsigned long long lcap_ll = fine * 4 + 4096;  // long lists; full -> ring search
+  const unsigned lcap = lcap_ll < (1ull << 28) ? static_cast<unsigned>(lcap_ll) : (1u << 28);
+  SBDT_WS(lslab, VltEntry, "assign.lslab", lcap);
+  SBDT_WS(lcount, unsigned, "assign.lcount", 1);
   SBDT_WS(slabels, std::uint32_t, "assign.slabels", m);
   SBDT_WS(stats, unsigned, "assign.stats", 4);
   SBDT_WS(oq, std::uint32_t, "assign.oq", n + 1);
@@ -391,7 +395,9 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
   {
     StageTimer t1(ctx, "assign.table");
     if (ctx->timing) SBDT_CUDA_TRY(cudaMemsetAsync(stats, 0, sizeof(unsigned) * 4, st));
-    k_vlt_build<D><<<sms * 16, 32 * kVltWarps, 0, st>>>(sg, starts, sorted, heads, slab, ctx->timing ? stats : nullptr);
+    SBDT_CUDA_TRY(cudaMemsetAsync(lcount, 0, sizeof(unsigned), st));
+    k_vlt_build<D><<<sms * 16, 32 * kVltWarps, 0, st>>>(sg, starts, sorted, heads, slab, lslab, lcount, lcap,
+                                                           ctx->timing ? stats : nullptr);
     ctx->launches += 1;
   }
   const std::uint64_t want = (n + kBlock - 1) / kBlock;
@@ -400,7 +406,8 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
     StageTimer t2(ctx, "assign.points");
     SBDT_CUDA_TRY(cudaMemsetAsync(oqc, 0, sizeof(unsigned), st));
     k_assign_vlt<D><<<blocks, kBlock, 0, st>>>(d_xyz, n, sg, heads, slab, sorted, slabels, d_labels, d_bbox, oq, oqc);
-    k_assign_overflow<D><<<sms * 4, 128, 0, st>>>(d_xyz, sg, starts, sorted, d_labels, oq, oqc);
+    k_assign_overflow<D><<<sms * 8, 128, 0, st>>>(d_xyz, sg, starts, sorted, slabels, heads, lslab, d_labels, oq,
+                                                   oqc);
     ctx->launches += 2;
   }
   SBDT_CUDA_TRY(cudaGetLastError());
@@ -430,11 +437,11 @@ int bucket_impl(sbdt_gpu_ctx* ctx, const std::uint32_t* d_labels, std::uint64_t 
 }
 
 // Table statistics of the last timed assign (uniform, list, overflow records).
-int assign_stats(sbdt_gpu_ctx* ctx, unsigned* out3) {
+int assign_stats(sbdt_gpu_ctx* ctx, unsigned* out4) {
   auto it = ctx->bufs.find("assign.stats");
   if (it == ctx->bufs.end()) return kErrInvalid;
   cudaStreamSynchronize(ctx->stream);
-  cudaMemcpy(out3, it->second.ptr, sizeof(unsigned) * 3, cudaMemcpyDeviceToHost);
+  cudaMemcpy(out4, it->second.ptr, sizeof(unsigned) * 4, cudaMemcpyDeviceToHost);
   return kOk;
 }
 

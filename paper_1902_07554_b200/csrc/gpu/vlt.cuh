@@ -16,7 +16,10 @@
 // Record per fine cell (u32 head): count 0 -> UNIFORM (label << 8), all
 // candidates share one label; 1..kSlots -> candidate list in the cell's slab
 // slot (16-byte entries: binary32 coordinates relative to the fine-cell centre
-// + sample index); kOverflow -> the point is queued for the exact ring search.
+// + sample index); kHeadLong -> a longer list in the long slab (header entry
+// holds the count), evaluated warp-cooperatively; kHeadOverflow -> the point
+// is queued for the exact ring search (coarse candidate overflow, or the long
+// slab is full).
 // Point decision: binary32 distances with a rigorous per-candidate error bound
 // pick the winner when the gap exceeds both bounds; otherwise the tied
 // candidates are compared exactly in binary64 (reference formula + pid).
@@ -25,7 +28,8 @@
 namespace sbdt_gpu {
 
 constexpr int kSlots = 12;
-constexpr std::uint32_t kHeadOverflow = 15u;
+constexpr std::uint32_t kHeadLong = 14u;      // list in the long slab: head = (offset << 4) | kHeadLong
+constexpr std::uint32_t kHeadOverflow = 15u;  // exact ring search
 constexpr int kVltWarps = 4;
 constexpr int kVltCap = 192;
 
@@ -65,7 +69,9 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
                                                               const std::uint32_t* __restrict__ starts,
                                                               const SampleRec* __restrict__ sorted,
                                                               std::uint32_t* __restrict__ heads,
-                                                              VltEntry* __restrict__ slab, unsigned* __restrict__ stats) {
+                                                              VltEntry* __restrict__ slab, VltEntry* __restrict__ lslab,
+                                                              unsigned* __restrict__ lcount, unsigned lcap,
+                                                              unsigned* __restrict__ stats) {
   __shared__ SampleGrid<D> sg;
   __shared__ std::uint32_t s_idx[kVltWarps][kVltCap];
   __shared__ float s_rel[kVltWarps][kVltCap][D];  // relative to the coarse centre
@@ -77,7 +83,7 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
   const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   constexpr int F = fine_factor<D>();
   constexpr int FC = fine_per_cell<D>();
-  unsigned st_uniform = 0, st_list = 0, st_over = 0;
+  unsigned st_uniform = 0, st_list = 0, st_over = 0, st_long = 0;
   const long long cells = static_cast<long long>(sg.cells);
   for (long long cell = static_cast<long long>(blockIdx.x) * kVltWarps + warp; cell < cells;
        cell += static_cast<long long>(gridDim.x) * kVltWarps) {
@@ -250,10 +256,14 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
 #pragma unroll
         for (int d = 0; d < D; ++d) rt[d] = s_rel[warp][bj][d] - off[d];
         const std::uint32_t lab0 = s_lab[warp][bj];
+        // pass 1: keep flags (one ballot word per 32 coarse candidates)
+        constexpr int kW = kVltCap / 32;
+        unsigned kw[kW];
         int count = 0;
         bool uniform = true;
-        for (int j0 = 0; j0 < ncand; j0 += 32) {
-          const int j = j0 + static_cast<int>(lane);
+#pragma unroll
+        for (int w = 0; w < kW; ++w) {
+          const int j = w * 32 + static_cast<int>(lane);
           bool keep = false;
           if (j < ncand) {
             if (j == bj) {
@@ -265,30 +275,59 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
               keep = !dominated_f<D>(rs, rt, fhw, fH);
             }
           }
-          const unsigned ballot = __ballot_sync(0xffffffffu, keep);
-          if (__ballot_sync(0xffffffffu, keep && s_lab[warp][j] != lab0)) uniform = false;
-          const int pos = count + __popc(ballot & ((1u << lane) - 1u));
-          if (keep && pos < kSlots) {
-            const std::uint32_t si = s_idx[warp][j];
-            VltEntry e;
-#pragma unroll
-            for (int d = 0; d < 3; ++d) e.r[d] = 0.f;
-#pragma unroll
-            for (int d = 0; d < D; ++d) e.r[d] = static_cast<float>(sorted[si].x[d] - fc[d]);
-            e.idx = si;
-            slab[fid * kSlots + pos] = e;
-          }
-          count += __popc(ballot);
+          kw[w] = __ballot_sync(0xffffffffu, keep);
+          if (__ballot_sync(0xffffffffu, keep && s_lab[warp][j < ncand ? j : 0] != lab0)) uniform = false;
+          count += __popc(kw[w]);
         }
-        if (uniform) head = lab0 << 8;
-        else if (count <= kSlots) head = static_cast<std::uint32_t>(count);
-        else head = kHeadOverflow;
+        VltEntry* out = nullptr;
+        if (uniform) {
+          head = lab0 << 8;
+        } else if (count <= kSlots) {
+          head = static_cast<std::uint32_t>(count);
+          out = slab + fid * kSlots;
+        } else {
+          unsigned o = 0;
+          if (lane == 0) o = atomicAdd(lcount, static_cast<unsigned>(count + 1));
+          o = __shfl_sync(0xffffffffu, o, 0);
+          if (static_cast<unsigned long long>(o) + count + 1 <= lcap && o < (1u << 28)) {
+            head = (o << 4) | kHeadLong;
+            if (lane == 0) {
+              VltEntry h;
+              h.r[0] = h.r[1] = h.r[2] = 0.f;
+              h.idx = static_cast<std::uint32_t>(count);
+              lslab[o] = h;
+            }
+            out = lslab + o + 1;
+          } else {
+            head = kHeadOverflow;
+          }
+        }
+        if (out) {
+          int before = 0;
+#pragma unroll
+          for (int w = 0; w < kW; ++w) {
+            const int j = w * 32 + static_cast<int>(lane);
+            if ((kw[w] >> lane) & 1u) {
+              const int pos = before + __popc(kw[w] & ((1u << lane) - 1u));
+              const std::uint32_t si = s_idx[warp][j];
+              VltEntry e;
+#pragma unroll
+              for (int d = 0; d < 3; ++d) e.r[d] = 0.f;
+#pragma unroll
+              for (int d = 0; d < D; ++d) e.r[d] = static_cast<float>(sorted[si].x[d] - fc[d]);
+              e.idx = si;
+              out[pos] = e;
+            }
+            before += __popc(kw[w]);
+          }
+        }
       }
       if (lane == 0) {
         heads[fid] = head;
         const std::uint32_t h = head & 15u;
         if (h == 0) ++st_uniform;
         else if (h == kHeadOverflow) ++st_over;
+        else if (h == kHeadLong) ++st_long;
         else ++st_list;
       }
     }
@@ -297,6 +336,7 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
     atomicAdd(&stats[0], st_uniform);
     atomicAdd(&stats[1], st_list);
     atomicAdd(&stats[2], st_over);
+    atomicAdd(&stats[3], st_long);
   }
 }
 
@@ -370,7 +410,7 @@ __global__ void __launch_bounds__(256) k_assign_vlt(const double* __restrict__ x
     const std::uint32_t cnt = head & 15u;
     if (cnt == 0) {
       __stcs(labels + i, head >> 8);
-    } else if (cnt == kHeadOverflow) {
+    } else if (cnt >= kHeadLong) {
       const unsigned slot = atomicAdd(oq_count, 1u);
       oq[slot] = static_cast<std::uint32_t>(i);
     } else {
@@ -413,21 +453,153 @@ __global__ void __launch_bounds__(256) k_assign_vlt(const double* __restrict__ x
   bbox_flush<D>(blo, bhi, bbox);
 }
 
+// Queued points: long lists are evaluated by the whole warp (lanes take the
+// entries, binary32 distances with the same error bounds as the list path,
+// exact binary64 argmin over the undecided ones); ring-search points run solo.
 template <int D>
-__global__ void k_assign_overflow(const double* __restrict__ xyz, const SampleGrid<D>* __restrict__ sgp,
-                                  const std::uint32_t* __restrict__ starts, const SampleRec* __restrict__ sorted,
-                                  std::uint32_t* __restrict__ labels, const std::uint32_t* __restrict__ oq,
-                                  const unsigned* __restrict__ oq_count) {
+__global__ void __launch_bounds__(128) k_assign_overflow(const double* __restrict__ xyz,
+                                                         const SampleGrid<D>* __restrict__ sgp,
+                                                         const std::uint32_t* __restrict__ starts,
+                                                         const SampleRec* __restrict__ sorted,
+                                                         const std::uint32_t* __restrict__ sorted_labels,
+                                                         const std::uint32_t* __restrict__ heads,
+                                                         const VltEntry* __restrict__ lslab,
+                                                         std::uint32_t* __restrict__ labels,
+                                                         const std::uint32_t* __restrict__ oq,
+                                                         const unsigned* __restrict__ oq_count) {
   __shared__ SampleGrid<D> sg;
   if (threadIdx.x == 0) sg = *sgp;
   __syncthreads();
+  constexpr int F = fine_factor<D>();
+  constexpr int FC = fine_per_cell<D>();
+  const unsigned full = 0xffffffffu;
+  const unsigned lane = threadIdx.x & 31u;
   const unsigned cnt = *oq_count;
-  for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < cnt; q += gridDim.x * blockDim.x) {
-    const std::uint32_t i = oq[q];
-    double x[D];
+  const unsigned warps = gridDim.x * (blockDim.x >> 5);
+  for (unsigned q0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32u; q0 < cnt; q0 += warps * 32u) {
+    const unsigned q = q0 + lane;
+    const bool has = q < cnt;
+    std::uint32_t i = 0, head = kHeadOverflow;
+    double x[D], fcen[D];
+    if (has) {
+      i = oq[q];
+      bool inside = true;
+      long long cell = 0, mul = 1;
+      int sub = 0, smul = 1;
 #pragma unroll
-    for (int d = 0; d < D; ++d) x[d] = xyz[std::size_t(i) * D + d];
-    labels[i] = nearest_label_ring<D>(x, sg.g, sg.margin, starts, sorted);
+      for (int d = 0; d < D; ++d) {
+        x[d] = xyz[std::size_t(i) * D + d];
+        const double f = floor((x[d] - sg.g.lo[d]) * sg.inv_ef);
+        inside = inside && (f >= 0.0) && (f < static_cast<double>(sg.g.dims[d] * F));
+        const int fi = inside ? static_cast<int>(f) : 0;
+        cell += static_cast<long long>(fi / F) * mul;
+        sub += (fi % F) * smul;
+        mul *= sg.g.dims[d];
+        smul *= F;
+        fcen[d] = 0.5 * ((sg.g.lo[d] + static_cast<double>(fi) * sg.ef) + (sg.g.lo[d] + static_cast<double>(fi + 1) * sg.ef));
+      }
+      if (inside) head = heads[cell * FC + sub];
+      if ((head & 15u) != kHeadLong) labels[i] = nearest_label_ring<D>(x, sg.g, sg.margin, starts, sorted);
+    }
+    for (unsigned todo = __ballot_sync(full, has && (head & 15u) == kHeadLong); todo; todo &= todo - 1) {
+      const int l = __ffs(todo) - 1;
+      double xl[D];
+      float p[D], pp = 0.f;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        xl[d] = __shfl_sync(full, x[d], l);
+        p[d] = static_cast<float>(xl[d] - __shfl_sync(full, fcen[d], l));
+        pp += p[d] * p[d];
+      }
+      const std::uint32_t hl = __shfl_sync(full, head, l);
+      const VltEntry* ents = lslab + (hl >> 4);
+      const int ne = static_cast<int>(ents[0].idx);
+      ++ents;
+      // binary32 distances and bounds; lane-local minimum, then the warp's
+      float bv = INFINITY;
+      int bj = 0x7fffffff;
+      for (int j = lane; j < ne; j += 32) {
+        const VltEntry e = ents[j];
+        float dd = 0.f;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const float t = p[d] - e.r[d];
+          dd += t * t;
+        }
+        if (dd < bv || (dd == bv && j < bj)) {
+          bv = dd;
+          bj = j;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(full, bv, o);
+        const int oj = __shfl_xor_sync(full, bj, o);
+        if (ov < bv || (ov == bv && oj < bj)) {
+          bv = ov;
+          bj = oj;
+        }
+      }
+      auto bound = [&](const VltEntry& e) {
+        float ss = 0.f;
+#pragma unroll
+        for (int d = 0; d < D; ++d) ss += e.r[d] * e.r[d];
+        return 4e-6f * (pp + ss) + 1e-30f;
+      };
+      const VltEntry eb = ents[bj];
+      const float lim = bv + bound(eb);
+      bool amb = false;
+      for (int j = lane; j < ne; j += 32) {
+        if (j == bj) continue;
+        const VltEntry e = ents[j];
+        float dd = 0.f;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const float t = p[d] - e.r[d];
+          dd += t * t;
+        }
+        amb = amb || (dd - bound(e) <= lim);
+      }
+      std::uint32_t lab;
+      if (!__any_sync(full, amb)) {
+        lab = __ldg(sorted_labels + eb.idx);
+      } else {
+        // exact binary64 argmin (reference squared_distance, lowest pid on
+        // ties) over the candidates whose binary32 interval reaches lim
+        double best = INFINITY;
+        std::uint32_t bpid = 0xFFFFFFFFu, blab = 0;
+        for (int j = lane; j < ne; j += 32) {
+          const VltEntry e = ents[j];
+          float dd = 0.f;
+#pragma unroll
+          for (int d = 0; d < D; ++d) {
+            const float t = p[d] - e.r[d];
+            dd += t * t;
+          }
+          if (j != bj && dd - bound(e) > lim) continue;
+          const SampleRec rec = sorted[e.idx];
+          const double d2 = sqdist<D>(xl, rec.x);
+          if (d2 < best || (d2 == best && rec.pid < bpid)) {
+            best = d2;
+            bpid = rec.pid;
+            blab = rec.label;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(full, best, o);
+          const std::uint32_t op = __shfl_xor_sync(full, bpid, o);
+          const std::uint32_t ol = __shfl_xor_sync(full, blab, o);
+          if (ob < best || (ob == best && op < bpid)) {
+            best = ob;
+            bpid = op;
+            blab = ol;
+          }
+        }
+        lab = blab;
+      }
+      if (static_cast<int>(lane) == l) labels[i] = lab;
+    }
   }
 }
 
