@@ -863,31 +863,15 @@ struct WideEntry {
   int level;
 };
 
-template <int D>
-__device__ bool warp_sphere_descent(const OwnerGrid<D>& og, const std::uint16_t* __restrict__ owner, const double* c,
-                                    double r2, std::uint32_t self, WideEntry<D>* stk) {
+// Warp-cooperative exact descent of the owner pyramid over the leaf range
+// [a, b]: test(L, block) returns 0 reject, 1 descend, 2 accept (leaf or every
+// sub-box passes); fallback() answers alone when the stack would overflow.
+template <int D, class Test, class Fallback>
+__device__ bool warp_descent(const OwnerGrid<D>& og, const std::uint16_t* __restrict__ owner, const int* a,
+                             const int* b, std::uint32_t self, const Test& test, const Fallback& fallback,
+                             WideEntry<D>* stk) {
   const unsigned lane = threadIdx.x & 31u;
   const unsigned full = 0xffffffffu;
-  if (isnan(r2)) return false;
-  bool fin = isfinite(r2);
-#pragma unroll
-  for (int d = 0; d < D; ++d) fin = fin && isfinite(c[d]);
-  int a[D], b[D];
-  if (fin) {
-    const double r = sqrt(r2) * (1.0 + 1e-9) + og.margin;
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      const double fa = floor((c[d] - r - og.g.lo[d]) * og.inv_edge);
-      const double fb = floor((c[d] + r - og.g.lo[d]) * og.inv_edge);
-      const double top = static_cast<double>(og.ldims[0][d] - 1);
-      if (fb < 0.0 || fa > top) return false;
-      a[d] = fa < 0.0 ? 0 : static_cast<int>(fa);
-      b[d] = fb > top ? og.ldims[0][d] - 1 : static_cast<int>(fb);
-    }
-  } else {
-#pragma unroll
-    for (int d = 0; d < D; ++d) a[d] = 0, b[d] = og.ldims[0][d] - 1;
-  }
   int L0 = 0;
   for (; L0 < og.levels - 1; ++L0) {
     bool ok = true;
@@ -895,14 +879,6 @@ __device__ bool warp_sphere_descent(const OwnerGrid<D>& og, const std::uint16_t*
     for (int d = 0; d < D; ++d) ok = ok && ((b[d] >> (L0 * og.shift)) - (a[d] >> (L0 * og.shift)) <= 1);
     if (ok) break;
   }
-  // returns 0 reject, 1 descend, 2 hit
-  auto test = [&](int L, const int* cc) -> int {
-    double blo[D], bhi[D];
-    og_block_box<D>(og, L, cc, blo, bhi);
-    if (!box_sphere<D>(blo, bhi, c, r2)) return 0;
-    if (L == 0 || box_inside_sphere<D>(blo, bhi, c, r2)) return 2;
-    return 1;
-  };
   int top = 0;
   // start blocks (<= 2 per axis)
   {
@@ -961,7 +937,7 @@ __device__ bool warp_sphere_descent(const OwnerGrid<D>& og, const std::uint16_t*
     if (__any_sync(full, res[0] == 2 || res[1] == 2)) return true;
     const unsigned p0 = __ballot_sync(full, res[0] == 1), p1 = __ballot_sync(full, res[1] == 1);
     const int np = __popc(p0) + __popc(p1);
-    if (top + np > kWideStack) return og_sphere_hits_foreign<D>(og, owner, c, r2, self);  // uniform fallback
+    if (top + np > kWideStack) return fallback();  // uniform fallback
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
       const unsigned pm = half ? p1 : p0;
@@ -976,6 +952,40 @@ __device__ bool warp_sphere_descent(const OwnerGrid<D>& og, const std::uint16_t*
     __syncwarp();
   }
   return false;
+}
+
+template <int D>
+__device__ bool warp_sphere_descent(const OwnerGrid<D>& og, const std::uint16_t* __restrict__ owner, const double* c,
+                                    double r2, std::uint32_t self, WideEntry<D>* stk) {
+  if (isnan(r2)) return false;
+  bool fin = isfinite(r2);
+#pragma unroll
+  for (int d = 0; d < D; ++d) fin = fin && isfinite(c[d]);
+  int a[D], b[D];
+  if (fin) {
+    const double r = sqrt(r2) * (1.0 + 1e-9) + og.margin;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const double fa = floor((c[d] - r - og.g.lo[d]) * og.inv_edge);
+      const double fb = floor((c[d] + r - og.g.lo[d]) * og.inv_edge);
+      const double top = static_cast<double>(og.ldims[0][d] - 1);
+      if (fb < 0.0 || fa > top) return false;
+      a[d] = fa < 0.0 ? 0 : static_cast<int>(fa);
+      b[d] = fb > top ? og.ldims[0][d] - 1 : static_cast<int>(fb);
+    }
+  } else {
+#pragma unroll
+    for (int d = 0; d < D; ++d) a[d] = 0, b[d] = og.ldims[0][d] - 1;
+  }
+  auto test = [&](int L, const int* cc) -> int {
+    double blo[D], bhi[D];
+    og_block_box<D>(og, L, cc, blo, bhi);
+    if (!box_sphere<D>(blo, bhi, c, r2)) return 0;
+    if (L == 0 || box_inside_sphere<D>(blo, bhi, c, r2)) return 2;
+    return 1;
+  };
+  auto fallback = [&]() { return og_sphere_hits_foreign<D>(og, owner, c, r2, self); };
+  return warp_descent<D>(og, owner, a, b, self, test, fallback, stk);
 }
 
 template <int D>
@@ -1035,58 +1045,108 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_border_wide(BorderArgs a, c
   }
 }
 
+// K6: rows with the infinite vertex (hull facets). Lanes set up 32 rows
+// (facet ids, the finite neighbour's inner vertex, its exact orientation);
+// under the grid policy each row's halfspace descent then runs on the whole
+// warp (warp_descent), the bbox policy tests the k-1 root boxes per lane.
 template <int D>
-__global__ void __launch_bounds__(128) k_border_infinite(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp) {
+__global__ void __launch_bounds__(kWideWarps * 32) k_border_infinite(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp) {
   __shared__ OwnerGrid<D> og;
+  __shared__ WideEntry<D> stacks[kWideWarps][kWideStack];
   extern __shared__ std::uint64_t s_off[];
   if (threadIdx.x == 0) og = *ogp;
   for (std::uint32_t j = threadIdx.x; j <= a.k; j += blockDim.x) s_off[j] = a.offsets[j];
   __syncthreads();
+  const unsigned full = 0xffffffffu;
+  const unsigned lane = threadIdx.x & 31u;
+  WideEntry<D>* stk = stacks[threadIdx.x >> 5];
   const unsigned count = *a.inf_count;
-  for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < count; q += gridDim.x * blockDim.x) {
-    const std::uint64_t s = a.inf_queue[q];
-    const std::uint32_t self = part_of(s_off, a.k, s);
-    std::uint32_t fv[D];
+  const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
+  for (unsigned q0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32u; q0 < count; q0 += nwarps * 32u) {
+    const unsigned q = q0 + lane;
+    const bool has = q < count;
+    std::uint64_t s = 0;
+    std::uint32_t self = 0, fv[D];
+    int inner_sign = 0;
+    double fx[D][D];  // facet vertex coordinates
+    if (has) {
+      s = a.inf_queue[q];
+      self = part_of(s_off, a.k, s);
 #pragma unroll
-    for (int j = 0; j < D; ++j) fv[j] = a.verts[std::uint64_t(j) * a.S + s];
-    const std::uint64_t owner_row = s_off[self] + a.nbrs[std::uint64_t(D) * a.S + s];
-    std::uint32_t inner = kInfVertex;
-    for (int j = 0; j <= D; ++j) {
-      const std::uint32_t w = a.verts[std::uint64_t(j) * a.S + owner_row];
-      bool on = false;
+      for (int j = 0; j < D; ++j) fv[j] = a.verts[std::uint64_t(j) * a.S + s];
+      const std::uint64_t owner_row = s_off[self] + a.nbrs[std::uint64_t(D) * a.S + s];
+      std::uint32_t inner = kInfVertex;
+      for (int j = 0; j <= D; ++j) {
+        const std::uint32_t w = a.verts[std::uint64_t(j) * a.S + owner_row];
+        bool on = false;
 #pragma unroll
-      for (int f = 0; f < D; ++f) on = on || (fv[f] == w);
-      if (!on) {
-        inner = w;
-        break;
+        for (int f = 0; f < D; ++f) on = on || (fv[f] == w);
+        if (!on) {
+          inner = w;
+          break;
+        }
       }
+#pragma unroll
+      for (int j = 0; j < D; ++j)
+#pragma unroll
+        for (int d = 0; d < D; ++d) fx[j][d] = a.xyz[std::size_t(fv[j]) * D + d];
+      const double* pts[D + 1];
+#pragma unroll
+      for (int j = 0; j < D; ++j) pts[j] = fx[j];
+      pts[D] = a.xyz + std::size_t(inner) * D;
+      inner_sign = orient_dev<D>(pts);
     }
-    const double* facet[D];
-#pragma unroll
-    for (int j = 0; j < D; ++j) facet[j] = a.xyz + std::size_t(fv[j]) * D;
-    const double* pts[D + 1];
-#pragma unroll
-    for (int j = 0; j < D; ++j) pts[j] = facet[j];
-    pts[D] = a.xyz + std::size_t(inner) * D;
-    const int inner_sign = orient_dev<D>(pts);
     bool pos = false;
     if (a.policy == SBDT_POLICY_BBOX) {
-      for (std::uint32_t j = 0; j < a.k && !pos; ++j) {
-        if (j == self) continue;
-        double blo[D], bhi[D];
-        if (bbox_policy_box<D>(og, a.pbbox, j, blo, bhi) && corners_outside<D>(facet, inner_sign, blo, bhi) > 0)
-          pos = true;
+      if (has) {
+        const double* facet[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) facet[j] = fx[j];
+        for (std::uint32_t j = 0; j < a.k && !pos; ++j) {
+          if (j == self) continue;
+          double blo[D], bhi[D];
+          if (bbox_policy_box<D>(og, a.pbbox, j, blo, bhi) && corners_outside<D>(facet, inner_sign, blo, bhi) > 0)
+            pos = true;
+        }
       }
     } else {
-      pos = og_halfspace_hits_foreign<D>(og, a.owner, facet, inner_sign, self);
+      for (unsigned todo = __ballot_sync(full, has); todo; todo &= todo - 1) {
+        const int l = __ffs(todo) - 1;
+        double fl[D][D];
+#pragma unroll
+        for (int j = 0; j < D; ++j)
+#pragma unroll
+          for (int d = 0; d < D; ++d) fl[j][d] = __shfl_sync(full, fx[j][d], l);
+        const int sl_sign = __shfl_sync(full, inner_sign, l);
+        const std::uint32_t sl_self = __shfl_sync(full, self, l);
+        const double* facet[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) facet[j] = fl[j];
+        int lo[D], hi[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) lo[d] = 0, hi[d] = og.ldims[0][d] - 1;
+        auto test = [&](int L, const int* cc) -> int {
+          double blo[D], bhi[D];
+          og_block_box<D>(og, L, cc, blo, bhi);
+          const int out = corners_outside<D>(facet, sl_sign, blo, bhi);
+          if (out == 0) return 0;
+          return (L == 0 || out == (1 << D)) ? 2 : 1;
+        };
+        auto fallback = [&]() { return og_halfspace_hits_foreign<D>(og, a.owner, facet, sl_sign, sl_self); };
+        const bool hit = warp_descent<D>(og, a.owner, lo, hi, sl_self, test, fallback, stk);
+        if (static_cast<int>(lane) == l) pos = hit;
+        __syncwarp();
+      }
     }
-    a.positive[s] = pos ? 1 : 0;
-    if (a.spheres)
+    if (has) {
+      a.positive[s] = pos ? 1 : 0;
+      if (a.spheres)
 #pragma unroll
-      for (int d = 0; d <= D; ++d) a.spheres[s * (D + 1) + d] = 0.0;
-    if (pos)
+        for (int d = 0; d <= D; ++d) a.spheres[s * (D + 1) + d] = 0.0;
+      if (pos)
 #pragma unroll
-      for (int j = 0; j < D; ++j) a.vflags[fv[j]] = 1;
+        for (int j = 0; j < D; ++j) a.vflags[fv[j]] = 1;
+    }
   }
 }
 
@@ -1294,7 +1354,7 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
     }
     {
       StageTimer t(ctx, "border.infinite");
-      k_border_infinite<D><<<sms * 2, 128, offs_sh, st>>>(a, og);
+      k_border_infinite<D><<<sms * 4, kWideWarps * 32, offs_sh, st>>>(a, og);
     }
     ctx->launches += (tiled && in->S > 0) ? 1 : 2;
   }
