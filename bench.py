@@ -327,7 +327,6 @@ def main():
     kernel_bytes = {
         "assign.points": n * (8 * dim + 4),
         "border.finite": S * (4 * (dim + 1) + 1) + n * (8 * dim + 4 + 1) + cells * 2,
-        "border.localize": n * (2 * 8 * dim + 4 + 4),
         # prefilter: vertex ids + parity + flag per row, localised coords once, 3 code arrays
         "border.prefilter": S * (4 * (dim + 1) + 2) + n * (8 * dim + 4) + cells * 2 * 3,
         # exact stage: queue entry + ids per candidate + result, coords once
