@@ -78,7 +78,8 @@ int sbdt_gpu_assign_table_stats(sbdt_gpu_ctx* ctx, unsigned* out4);
 /* Border pipeline census of the last find_border with timing enabled (grid
  * policy; zeros otherwise): out8 = {rows scanned by the prefilter, rows that
  * reached the exact stage, exact rows by scan kind: flattened cell scan,
- * two-level block scan, pyramid descent, 0, 0, 0}. */
+ * two-level block scan, pyramid descent, (candidate, cell row) pairs of the
+ * flattened scan, 0, positives of the flattened scan}. */
 int sbdt_gpu_border_stats(sbdt_gpu_ctx* ctx, unsigned long long* out8);
 
 /* Page-locked host memory for the host-buffer entry points' inputs and

@@ -746,17 +746,15 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
       }
     }
 
-    // ---- mode 1: flattened (candidate, cell) stream
-    {
+    // ---- mode 1: flattened stream of (candidate, row) pairs, a row being the
+    // cells along axis 0 for fixed (i1, i2); a lane tests its row's <= 5 cells
+    // with independent owner-code loads.
     unsigned cnt = 0;
     if (mode == 1) {
-      cnt = D == 3 ? unsigned(span[0] * span[1] * span[2]) : unsigned(span[0] * span[1]);
       constexpr int SH = og_shift<D>();
       constexpr int F = og_fan<D>();
 #pragma unroll
       for (int d = 0; d < D; ++d) {
-        sl[lane].span[d] = static_cast<unsigned>(span[d]);
-        sl[lane].inv[d] = (65536u + static_cast<unsigned>(span[d]) - 1u) / static_cast<unsigned>(span[d]);
         for (int i = 0; i < span[d]; ++i) {
           const int cell = lo[d] + i;
           const unsigned long long off =
@@ -771,9 +769,12 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
           sl[lane].ent[d][i].off = off;
           sl[lane].ent[d][i].g2 = g * g;
         }
+        sl[lane].span[d] = static_cast<unsigned>(span[d]);
+        sl[lane].inv[d] = (65536u + static_cast<unsigned>(span[d]) - 1u) / static_cast<unsigned>(span[d]);
       }
       sl[lane].r2 = r2;
       sl[lane].self = self;
+      cnt = D == 3 ? unsigned(span[1] * span[2]) : unsigned(span[1]);
     }
     unsigned incl = cnt;
 #pragma unroll
@@ -784,59 +785,62 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
     const unsigned total = __shfl_sync(full, incl, 31);
     const unsigned excl = incl - cnt;
     const unsigned nzmask = __ballot_sync(full, cnt > 0);
+    if (a.counters && lane == 0) atomicAdd(&a.counters[5], static_cast<unsigned long long>(total));
     if (cnt) {
       sl[lane].excl = excl;
       nz[__popc(nzmask & ((1u << lane) - 1u))] = static_cast<unsigned char>(lane);
     }
     __syncwarp();
-    // Chunks of 32 (candidate, cell) pairs, kChunkUnroll at a time: the owner
-    // code loads of a group are independent (no early exit between chunks),
-    // so their L2 latencies overlap.
     unsigned done = 0;
     int cur = -1;
-    constexpr int kChunkUnroll = 4;
-    for (unsigned g0 = 0; g0 < total; g0 += 32 * kChunkUnroll) {
-      std::uint16_t code[kChunkUnroll];
-      unsigned clv[kChunkUnroll];
-      bool geo[kChunkUnroll];
-#pragma unroll
-      for (int u = 0; u < kChunkUnroll; ++u) {
-        const unsigned b0 = g0 + 32u * u;
-        const bool st = cnt && excl >= b0 && excl < b0 + 32;
-        const unsigned smask = __reduce_or_sync(full, st ? 1u << (excl - b0) : 0u);
-        const unsigned q = b0 + lane;
-        code[u] = kOwnerEmpty;
-        clv[u] = 0;
-        geo[u] = false;
-        if (q < total) {
-          const unsigned cl = nz[cur + __popc(smask & ((2u << lane) - 1u))];
-          const CandSlot<D>& r = sl[cl];
-          unsigned rem = q - r.excl;
-          unsigned long long idx = og.loff[0];
-          double d2 = 0.0;
-#pragma unroll
-          for (int d = 0; d < D; ++d) {
-            const unsigned qq = (rem * r.inv[d]) >> 16;  // rem / span (rem * span < 2^16)
-            const typename CandSlot<D>::Ent& e = r.ent[d][rem - qq * r.span[d]];
-            idx += e.off;
-            d2 += e.g2;
-            rem = qq;
-          }
-          clv[u] = cl;
-          geo[u] = d2 <= r.r2;
-          if (geo[u]) code[u] = __ldg(a.owner + idx);
+    for (unsigned b0 = 0; b0 < total; b0 += 32) {
+      const bool st = cnt && excl >= b0 && excl < b0 + 32;
+      const unsigned smask = __reduce_or_sync(full, st ? 1u << (excl - b0) : 0u);
+      const unsigned q = b0 + lane;
+      bool h = false;
+      unsigned cl = 0;
+      if (q < total) {
+        cl = nz[cur + __popc(smask & ((2u << lane) - 1u))];
+        const CandSlot<D>& r = sl[cl];
+        const unsigned rem = q - r.excl;
+        unsigned long long base = og.loff[0];
+        double g12;  // g1^2 (+ g2^2 added after g0^2, box_sphere's order)
+        double g2z = 0.0;
+        if constexpr (D == 3) {
+          const unsigned i2 = (rem * r.inv[1]) >> 16;  // rem / span1 (rem * span1 < 2^16)
+          const unsigned i1 = rem - i2 * r.span[1];
+          base += r.ent[1][i1].off + r.ent[2][i2].off;
+          g12 = r.ent[1][i1].g2;
+          g2z = r.ent[2][i2].g2;
+        } else {
+          base += r.ent[1][rem].off;
+          g12 = r.ent[1][rem].g2;
         }
-        cur += __popc(smask);
-      }
+        const double rr = r.r2;
+        std::uint16_t code[5];
+        bool geo[5];
 #pragma unroll
-      for (int u = 0; u < kChunkUnroll; ++u) {
-        const bool h = geo[u] && code[u] != kOwnerEmpty && code[u] != sl[clv[u]].self;
-        done |= __reduce_or_sync(full, h ? 1u << clv[u] : 0u);
+        for (int i0 = 0; i0 < 5; ++i0) {
+          geo[i0] = false;
+          code[i0] = kOwnerEmpty;
+          if (i0 < static_cast<int>(r.span[0])) {
+            const typename CandSlot<D>::Ent& e = r.ent[0][i0];
+            double d2 = e.g2 + g12;
+            if constexpr (D == 3) d2 += g2z;
+            geo[i0] = d2 <= rr;
+            if (geo[i0]) code[i0] = __ldg(a.owner + base + e.off);
+          }
+        }
+        const std::uint32_t sf = r.self;
+#pragma unroll
+        for (int i0 = 0; i0 < 5; ++i0) h = h || (geo[i0] && code[i0] != kOwnerEmpty && code[i0] != sf);
       }
+      done |= __reduce_or_sync(full, h ? 1u << cl : 0u);
+      cur += __popc(smask);
     }
     if (mode == 1) pos = (done >> lane) & 1u;
+    if (a.counters && lane == 0) atomicAdd(&a.counters[7], static_cast<unsigned long long>(__popc(done)));
     __syncwarp();
-    }
 
     if (has && mode < 2) {
       __stcs(a.positive + s, static_cast<std::uint8_t>(pos ? 1 : 0));

@@ -152,7 +152,8 @@ class Context:
         if lib().sbdt_gpu_border_stats(self._h, out) != SBDT_OK:
             return {}
         return {"rows": int(out[0]), "exact_stage_rows": int(out[1]), "exact_flat_scan": int(out[2]),
-                "exact_block_scan": int(out[3]), "exact_descent": int(out[4])}
+                "exact_block_scan": int(out[3]), "exact_descent": int(out[4]), "row_pairs": int(out[5]),
+                "exact_flat_positive": int(out[7])}
 
     # ---- device-pointer entry points (inputs resident in HBM; async on the stream)
     def assign_points_dev(self, dim, d_xyz, n, d_sample_ids, d_sample_labels, m, k, d_labels, d_part_offsets=None,
