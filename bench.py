@@ -299,10 +299,15 @@ def main():
         t_wall = time.perf_counter() - t_wall0
     if dist:
         dist.barrier()
-    table_stats = ctx.table_stats()
-    border_stats = ctx.border_stats()
     total_ms = sdist.max_over_ranks(sum(ms), device=dev)  # device time, max over ranks
     ctx.synchronize()
+    # pipeline census: one extra, untimed step with the counters on
+    ctx.set_timing(False, census=True)
+    step()
+    ctx.synchronize()
+    table_stats = ctx.table_stats()
+    border_stats = ctx.border_stats()
+    ctx.set_timing(False)
 
     n_vb = int(d_cnt.item())
     # SPEC find_border (hull-seeded BFS) variant, timed separately (K8 included)

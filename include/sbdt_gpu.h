@@ -66,21 +66,25 @@ int sbdt_gpu_synchronize(sbdt_gpu_ctx* ctx);
 unsigned long long sbdt_gpu_launch_count(const sbdt_gpu_ctx* ctx);
 /* Reads and clears the device status word; returns the mapped status. */
 int sbdt_gpu_check_status(sbdt_gpu_ctx* ctx);
-/* Per-stage CUDA-event timing on the context stream (off by default).
- * sbdt_gpu_stage_times synchronizes, writes up to max_stages durations (ms)
- * and '\n'-separated stage names, clears the record and returns the count. */
+/* enable bit 0: per-stage CUDA-event timing on the context stream; bit 1:
+ * pipeline census counters (extra atomics: not for timed runs). Off by
+ * default. sbdt_gpu_stage_times synchronizes, writes up to max_stages
+ * durations (ms) and '\n'-separated stage names, clears the record and
+ * returns the count. */
 int sbdt_gpu_set_timing(sbdt_gpu_ctx* ctx, int enable);
 int sbdt_gpu_stage_times(sbdt_gpu_ctx* ctx, char* names, int names_len, float* ms, int max_stages);
-/* Voronoi-label-table census of the last assign with timing enabled:
+/* Voronoi-label-table census of the last assign with the census enabled:
  * out4 = {uniform records, short-list records, ring-search records,
  * long-list records}. */
 int sbdt_gpu_assign_table_stats(sbdt_gpu_ctx* ctx, unsigned* out4);
-/* Border pipeline census of the last find_border with timing enabled (grid
- * policy; zeros otherwise): out8 = {rows scanned by the prefilter, rows that
+/* Border pipeline census of the last find_border with the census enabled (grid
+ * policy; zeros otherwise): out12 = {rows scanned by the prefilter, rows that
  * reached the exact stage, exact rows by scan kind: flattened cell scan,
- * two-level block scan, pyramid descent, (candidate, cell row) pairs of the
- * flattened scan, 0, positives of the flattened scan}. */
-int sbdt_gpu_border_stats(sbdt_gpu_ctx* ctx, unsigned long long* out8);
+ * two-level range (wide), pyramid range (wide), (candidate, cell row) pairs
+ * of the flattened scan, wide-stage block expansions, positives of the
+ * flattened scan, positives proven by the prefilter, positives of the wide
+ * stage, 0, 0}. */
+int sbdt_gpu_border_stats(sbdt_gpu_ctx* ctx, unsigned long long* out12);
 
 /* Page-locked host memory for the host-buffer entry points' inputs and
  * outputs (transfers from/to pageable memory are staged by the driver and

@@ -394,10 +394,10 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
   }
   {
     StageTimer t1(ctx, "assign.table");
-    if (ctx->timing) SBDT_CUDA_TRY(cudaMemsetAsync(stats, 0, sizeof(unsigned) * 4, st));
+    if (ctx->census) SBDT_CUDA_TRY(cudaMemsetAsync(stats, 0, sizeof(unsigned) * 4, st));
     SBDT_CUDA_TRY(cudaMemsetAsync(lcount, 0, sizeof(unsigned), st));
     k_vlt_build<D><<<sms * 16, 32 * kVltWarps, 0, st>>>(sg, starts, sorted, heads, slab, lslab, lcount, lcap,
-                                                           ctx->timing ? stats : nullptr);
+                                                           ctx->census ? stats : nullptr);
     ctx->launches += 1;
   }
   const std::uint64_t want = (n + kBlock - 1) / kBlock;

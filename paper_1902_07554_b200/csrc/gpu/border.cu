@@ -623,6 +623,7 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
       decode_row<D>(a.xq, v, qh_f, qh_err, A, sp.P0, P0e, &eta);
       const int res = enclosing_sphere_f32<D>(A, eta, P0e, sp)
                           ? prefilter_decide<D>(og, a, sp, self, inv_e, margin_c, lo_mag, pos_ok) : 2;
+      if (a.counters && res == 1) atomicAdd(&a.counters[8], 1ull);
       if (res == 2) {
         is_cand = true;
       } else {
@@ -859,7 +860,7 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
 // shared memory. Same decisions as og_sphere_hits_foreign (exact pruning),
 // without serialising a whole descent on one lane.
 constexpr int kWideWarps = 4;
-constexpr int kWideStack = 512;  // >= 63 * (levels - 1) + 8 for every admissible grid
+constexpr int kWideStack = 256;  // deeper stacks (> 4 levels of dense partial blocks) take the serial fallback
 
 template <int D>
 struct WideEntry {
@@ -873,7 +874,7 @@ struct WideEntry {
 template <int D, class Test, class Fallback>
 __device__ bool warp_descent(const OwnerGrid<D>& og, const std::uint16_t* __restrict__ owner, const int* a,
                              const int* b, std::uint32_t self, const Test& test, const Fallback& fallback,
-                             WideEntry<D>* stk) {
+                             WideEntry<D>* stk, unsigned long long* counters = nullptr) {
   const unsigned lane = threadIdx.x & 31u;
   const unsigned full = 0xffffffffu;
   int L0 = 0;
@@ -920,6 +921,7 @@ __device__ bool warp_descent(const OwnerGrid<D>& og, const std::uint16_t* __rest
     const WideEntry<D> e = stk[top - 1];
     --top;
     __syncwarp();
+    if (counters && lane == 0) atomicAdd(&counters[6], 1ull);
     const int lv = e.level - 1;
     const int csh = lv * og.shift;
     const std::uint16_t* ch = owner + og.loff[lv] + lin_i<D>(og.ldims[e.level], e.c) * 64;
@@ -960,7 +962,8 @@ __device__ bool warp_descent(const OwnerGrid<D>& og, const std::uint16_t* __rest
 
 template <int D>
 __device__ bool warp_sphere_descent(const OwnerGrid<D>& og, const std::uint16_t* __restrict__ owner, const double* c,
-                                    double r2, std::uint32_t self, WideEntry<D>* stk) {
+                                    double r2, std::uint32_t self, WideEntry<D>* stk,
+                                    unsigned long long* counters = nullptr) {
   if (isnan(r2)) return false;
   bool fin = isfinite(r2);
 #pragma unroll
@@ -989,11 +992,11 @@ __device__ bool warp_sphere_descent(const OwnerGrid<D>& og, const std::uint16_t*
     return 1;
   };
   auto fallback = [&]() { return og_sphere_hits_foreign<D>(og, owner, c, r2, self); };
-  return warp_descent<D>(og, owner, a, b, self, test, fallback, stk);
+  return warp_descent<D>(og, owner, a, b, self, test, fallback, stk, counters);
 }
 
 template <int D>
-__global__ void __launch_bounds__(kWideWarps * 32) k_border_wide(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
+__global__ void __launch_bounds__(kWideWarps * 32, 6) k_border_wide(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
                                                                  const std::uint32_t* __restrict__ wide,
                                                                  std::uint64_t cap,
                                                                  const unsigned* __restrict__ nwide_p,
@@ -1036,8 +1039,9 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_border_wide(BorderArgs a, c
       for (int d = 0; d < D; ++d) cl[d] = __shfl_sync(full, c[d], l);
       const double rl = __shfl_sync(full, r2, l);
       const std::uint32_t sl = __shfl_sync(full, self, l);
-      const bool hit = warp_sphere_descent<D>(og, a.owner, cl, rl, sl, stk);
+      const bool hit = warp_sphere_descent<D>(og, a.owner, cl, rl, sl, stk, a.counters);
       if (static_cast<int>(lane) == l) pos = hit;
+      if (a.counters && hit && lane == 0) atomicAdd(&a.counters[9], 1ull);
       __syncwarp();
     }
     if (has) {
@@ -1315,9 +1319,9 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   a.inf_count = infc;
   a.status = ctx->d_status;
   a.counters = nullptr;
-  if (ctx->timing) {
-    SBDT_WS(cnt, unsigned long long, "border.counters", 8);
-    SBDT_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 8, st));
+  if (ctx->census) {
+    SBDT_WS(cnt, unsigned long long, "border.counters", 12);
+    SBDT_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 12, st));
     a.counters = cnt;
   }
   const std::size_t offs_sh = sizeof(std::uint64_t) * (in->k + 1);

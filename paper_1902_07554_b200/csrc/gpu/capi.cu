@@ -118,7 +118,8 @@ unsigned long long sbdt_gpu_launch_count(const sbdt_gpu_ctx* ctx) { return ctx ?
 
 int sbdt_gpu_set_timing(sbdt_gpu_ctx* ctx, int enable) {
   if (!ctx) return SBDT_ERR_INVALID;
-  ctx->timing = enable != 0;
+  ctx->timing = (enable & 1) != 0;
+  ctx->census = (enable & 2) != 0;
   ctx->stages.clear();
   ctx->events_used = 0;
   return SBDT_OK;
@@ -153,12 +154,12 @@ int sbdt_gpu_assign_table_stats(sbdt_gpu_ctx* ctx, unsigned* out4) {
   return assign_stats(ctx, out4) == kOk ? SBDT_OK : SBDT_ERR_INVALID;
 }
 
-int sbdt_gpu_border_stats(sbdt_gpu_ctx* ctx, unsigned long long* out8) {
-  if (!ctx || !out8) return SBDT_ERR_INVALID;
+int sbdt_gpu_border_stats(sbdt_gpu_ctx* ctx, unsigned long long* out12) {
+  if (!ctx || !out12) return SBDT_ERR_INVALID;
   auto it = ctx->bufs.find("border.counters");
   if (it == ctx->bufs.end()) return SBDT_ERR_INVALID;
   cudaStreamSynchronize(ctx->stream);
-  cudaMemcpy(out8, it->second.ptr, sizeof(unsigned long long) * 8, cudaMemcpyDeviceToHost);
+  cudaMemcpy(out12, it->second.ptr, sizeof(unsigned long long) * 12, cudaMemcpyDeviceToHost);
   return SBDT_OK;
 }
 

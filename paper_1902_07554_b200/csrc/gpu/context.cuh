@@ -29,6 +29,8 @@ struct sbdt_gpu_ctx {
   unsigned long long stats[8] = {0};
   // optional per-stage CUDA-event timing (bench.py: live per-kernel durations)
   bool timing = false;
+  // optional pipeline census (counters; adds atomics, so never in a timed run)
+  bool census = false;
   struct Stage {
     std::string name;
     cudaEvent_t start = nullptr, stop = nullptr;

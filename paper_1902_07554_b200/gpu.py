@@ -128,8 +128,10 @@ class Context:
     def launches(self) -> int:
         return int(lib().sbdt_gpu_launch_count(self._h))
 
-    def set_timing(self, enable: bool):
-        self.check(lib().sbdt_gpu_set_timing(self._h, 1 if enable else 0), "set_timing")
+    def set_timing(self, enable: bool, census: bool = False):
+        """Per-stage CUDA-event timing; census=True also fills the pipeline
+        counters (table_stats / border_stats) at the cost of extra atomics."""
+        self.check(lib().sbdt_gpu_set_timing(self._h, (1 if enable else 0) | (2 if census else 0)), "set_timing")
 
     def stage_times(self) -> list[tuple[str, float]]:
         """(stage, ms) pairs recorded since the last call (CUDA events on the context stream)."""
@@ -148,12 +150,12 @@ class Context:
         return {"uniform": int(out[0]), "list": int(out[1]), "ring_search": int(out[2]), "long_list": int(out[3])}
 
     def border_stats(self) -> dict:
-        out = (C.c_ulonglong * 8)()
+        out = (C.c_ulonglong * 12)()
         if lib().sbdt_gpu_border_stats(self._h, out) != SBDT_OK:
             return {}
-        return {"rows": int(out[0]), "exact_stage_rows": int(out[1]), "exact_flat_scan": int(out[2]),
-                "exact_block_scan": int(out[3]), "exact_descent": int(out[4]), "row_pairs": int(out[5]),
-                "exact_flat_positive": int(out[7])}
+        keys = ["rows", "exact_stage_rows", "exact_flat_scan", "wide_two_level", "wide_pyramid", "row_pairs",
+                "wide_expansions", "exact_flat_positive", "prefilter_positive", "wide_positive"]
+        return {kk: int(out[i]) for i, kk in enumerate(keys)}
 
     # ---- device-pointer entry points (inputs resident in HBM; async on the stream)
     def assign_points_dev(self, dim, d_xyz, n, d_sample_ids, d_sample_labels, m, k, d_labels, d_part_offsets=None,
