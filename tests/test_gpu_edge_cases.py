@@ -1,0 +1,109 @@
+"""GPU parity on the edge cases the reference's contract names (SPEC.md
+acceptance criteria): exact ties and cospherical / collinear
+configurations (integer lattices), tiny inputs, a part without points, and a
+far-from-origin translate (binning and prefilter bounds under large |x|).
+Every case is compared bit for bit with the CPU oracle through the C ABI."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1902_07554_b200 import gpu, host
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(points, sample_ids, sample_labels, k, ctx, seed=7, policies=("grid", "bbox")):
+    part = gpu.assign_points(points, sample_ids, sample_labels, k, ctx=ctx)
+    ref = oracle.assign_brute(points, sample_ids, sample_labels)
+    assert np.array_equal(part.labels, ref)
+    partials = host.build_partials(points, ref, k, seed)
+    for policy in policies:
+        g = gpu.find_border(points, ref, partials, gpu.IntersectionPolicy(policy, 1.0), hull_bfs=True, ctx=ctx)
+        o = oracle.find_border(points, ref, partials, policy)
+        assert np.array_equal(g.positive, o["positive"]), policy
+        assert np.array_equal(g.border, o["border"]), policy
+        assert np.array_equal(g.positive_vertex_ids, o["vertices_positive"]), policy
+        assert np.array_equal(g.border_vertex_ids, o["vertices_border"]), policy
+    return part, partials
+
+
+def _lattice(dim, side, jitter=0.0, seed=0):
+    axes = [np.arange(side, dtype=np.float64)] * dim
+    pts = np.stack(np.meshgrid(*axes, indexing="ij"), axis=-1).reshape(-1, dim)
+    if jitter:
+        pts = pts + np.random.default_rng(seed).uniform(-jitter, jitter, pts.shape)
+    return np.ascontiguousarray(pts)
+
+
+@pytest.mark.parametrize("dim,side", [(2, 300), (3, 40)])
+def test_integer_lattice_assignment_ties(dim, side, ctx):
+    """Exact lattice: equidistant samples everywhere; the lowest sample
+    PointId must win (assign_points only: the reference's DT rejects exact
+    lattices as affinely degenerate beyond its tie-break)."""
+    pts = _lattice(dim, side)
+    rng = np.random.default_rng(1)
+    sid = np.sort(rng.choice(len(pts), size=len(pts) // 20, replace=False)).astype(np.uint32)
+    slab = (np.arange(len(sid)) % 7).astype(np.uint32)
+    part = gpu.assign_points(pts, sid, slab, 7, ctx=ctx)
+    assert np.array_equal(part.labels, oracle.assign_brute(pts, sid, slab))
+
+
+@pytest.mark.parametrize("dim,side", [(2, 60), (3, 16)])
+def test_jittered_lattice(dim, side, ctx):
+    """Lattice + 1e-7 jitter: near-cospherical simplices everywhere."""
+    pts = _lattice(dim, side, jitter=1e-7, seed=dim)
+    rng = np.random.default_rng(1)
+    sid = np.sort(rng.choice(len(pts), size=len(pts) // 20, replace=False)).astype(np.uint32)
+    slab = np.minimum((pts[sid, 0] * 4 // side).astype(np.uint32), 3)
+    _check(pts, sid, slab, 4, ctx)
+
+
+def test_tiny_inputs(ctx):
+    rng = np.random.default_rng(3)
+    pts = np.ascontiguousarray(rng.random((40, 2)))
+    sid = np.array([0, 5, 11, 17, 23, 31], np.uint32)
+    slab = np.array([0, 0, 1, 1, 0, 1], np.uint32)
+    _check(pts, sid, slab, 2, ctx)
+    pts3 = np.ascontiguousarray(rng.random((60, 3)))
+    sid3 = np.array([1, 7, 13, 29, 41, 50, 55], np.uint32)
+    slab3 = np.array([0, 1, 2, 0, 1, 2, 0], np.uint32)
+    _check(pts3, sid3, slab3, 3, ctx)
+
+
+def test_part_without_points(ctx):
+    """k = 5 but no sample carries label 4: part 4 is empty (no points, no
+    simplex rows; the DT builder needs >= D+1 points, so its empty row range
+    is appended) and must be handled by the part offsets and the grid."""
+    inst = host.make_instance(1, n=30_000, k=4)
+    part = gpu.assign_points(inst.points, inst.sample_ids, inst.sample_labels, 5, ctx=ctx)
+    ref = oracle.assign_brute(inst.points, inst.sample_ids, inst.sample_labels)
+    assert np.array_equal(part.labels, ref)
+    assert part.parts_offsets[4] == part.parts_offsets[5] == len(ref)
+    p4 = host.build_partials(inst.points, ref, 4, 7)
+    p5 = host.Partials(np.append(p4.offsets, p4.offsets[-1]).astype(np.uint64), p4.verts, p4.nbrs, p4.parity)
+    for policy in ("grid", "bbox"):
+        g = gpu.find_border(inst.points, ref, p5, gpu.IntersectionPolicy(policy, 1.0), hull_bfs=True, ctx=ctx)
+        g4 = gpu.find_border(inst.points, ref, p4, gpu.IntersectionPolicy(policy, 1.0), hull_bfs=True, ctx=ctx)
+        o = oracle.find_border(inst.points, ref, p4, policy)
+        assert np.array_equal(g.positive, o["positive"]) and np.array_equal(g4.positive, o["positive"])
+        assert np.array_equal(g.border, o["border"])
+        assert np.array_equal(g.positive_vertex_ids, o["vertices_positive"])
+
+
+@pytest.mark.parametrize("shift", [1e3, -2.5e5])
+def test_far_from_origin(shift, ctx):
+    """A translated instance: the grid origin, the packed prefilter offsets and
+    every margin are relative to large |x|."""
+    inst = host.make_instance(2, n=40_000, k=8)
+    pts = np.ascontiguousarray(inst.points + shift)
+    _check(pts, inst.sample_ids, inst.sample_labels, 8, ctx, policies=("grid",))
+
+
+def test_jittered_lattice_near_degenerate(ctx):
+    """Lattice plus 1e-9 jitter: binary32 bounds cannot decide most simplices
+    (the prefilter must defer them to binary64)."""
+    pts = _lattice(3, 14, jitter=1e-9, seed=5)
+    rng = np.random.default_rng(2)
+    sid = np.sort(rng.choice(len(pts), size=len(pts) // 16, replace=False)).astype(np.uint32)
+    slab = np.minimum((pts[sid, 1] * 3 // 14).astype(np.uint32), 2)
+    _check(pts, sid, slab, 3, ctx)
