@@ -97,7 +97,8 @@ __global__ void k_bbox_init(unsigned long long* bbox, int dim) {
 template <int D>
 __global__ void k_sample_gather(const double* __restrict__ xyz, const std::uint32_t* __restrict__ sample_ids,
                                 const std::uint32_t* __restrict__ sample_labels, std::uint32_t m,
-                                SampleRec* __restrict__ recs, unsigned long long* bbox) {
+                                SampleRec* __restrict__ recs, unsigned long long* bbox,
+                                const double* __restrict__ sxyz) {
   double lo[D], hi[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) lo[d] = INFINITY, hi[d] = -INFINITY;
@@ -108,7 +109,7 @@ __global__ void k_sample_gather(const double* __restrict__ xyz, const std::uint3
     for (int d = 0; d < 3; ++d) r.x[d] = 0.0;
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      r.x[d] = xyz[std::size_t(pid) * D + d];
+      r.x[d] = sxyz ? sxyz[std::size_t(s) * D + d] : xyz[std::size_t(pid) * D + d];
       lo[d] = fmin(lo[d], r.x[d]);
       hi[d] = fmax(hi[d], r.x[d]);
     }
@@ -382,7 +383,8 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
     StageTimer t0(ctx, "assign.sample_grid");
     k_bbox_init<<<1, 32, 0, st>>>(sbbox, D);
     k_bbox_init<<<1, 32, 0, st>>>(d_bbox, D);
-    k_sample_gather<D><<<sblocks, kBlock, 0, st>>>(d_xyz, d_sample_ids, d_sample_labels, m, recs, sbbox);
+    k_sample_gather<D><<<sblocks, kBlock, 0, st>>>(d_xyz, d_sample_ids, d_sample_labels, m, recs, sbbox,
+                                                   ctx->sample_xyz);
     k_sample_grid_params<D><<<1, 1, 0, st>>>(sbbox, m, cap, sg);
     SBDT_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(std::uint32_t) * (cap + 1), st));
     k_sample_count<D><<<sblocks, kBlock, 0, st>>>(recs, m, sg, counts, cell_of);
@@ -405,7 +407,26 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
   if (blocks > 0) {
     StageTimer t2(ctx, "assign.points");
     SBDT_CUDA_TRY(cudaMemsetAsync(oqc, 0, sizeof(unsigned), st));
-    k_assign_vlt<D><<<blocks, kBlock, 0, st>>>(d_xyz, n, sg, heads, slab, sorted, slabels, d_labels, d_bbox, oq, oqc);
+    if (ctx->chunks.empty()) {
+      k_assign_vlt<D><<<blocks, kBlock, 0, st>>>(d_xyz, 0, n, sg, heads, slab, sorted, slabels, d_labels, d_bbox, oq,
+                                                 oqc);
+    } else {
+      // host path: each chunk of points as soon as its upload has landed
+      std::uint64_t i0 = 0;
+      for (const auto& c : ctx->chunks) {
+        const std::uint64_t i1 = c.first < n ? c.first : n;
+        SBDT_CUDA_TRY(cudaStreamWaitEvent(st, c.second, 0));
+        if (i1 > i0) {
+          const std::uint64_t w = (i1 - i0 + kBlock - 1) / kBlock;
+          const unsigned b = static_cast<unsigned>(w < std::uint64_t(sms) * 16 ? w : std::uint64_t(sms) * 16);
+          k_assign_vlt<D><<<b, kBlock, 0, st>>>(d_xyz, i0, i1, sg, heads, slab, sorted, slabels, d_labels, d_bbox, oq,
+                                                oqc);
+          ++ctx->launches;
+        }
+        i0 = i1;
+      }
+      --ctx->launches;
+    }
     k_assign_overflow<D><<<sms * 8, 128, 0, st>>>(d_xyz, sg, starts, sorted, slabels, heads, lslab, d_labels, oq,
                                                    oqc);
     ctx->launches += 2;

@@ -566,7 +566,8 @@ __device__ __forceinline__ int prefilter_decide(const OwnerGrid<D>& og, const Bo
 template <int D>
 __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
                                                                 std::uint32_t* __restrict__ cand, std::uint64_t cap,
-                                                                unsigned* __restrict__ ncand) {
+                                                                unsigned* __restrict__ ncand, std::uint64_t row_begin,
+                                                                std::uint64_t row_end) {
   __shared__ OwnerGrid<D> og;
   extern __shared__ std::uint64_t s_off[];
   if (threadIdx.x == 0) og = *ogp;
@@ -575,7 +576,8 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
   const unsigned lane = threadIdx.x & 31u;
   const unsigned lt = (1u << lane) - 1u;
   const std::uint64_t stride = std::uint64_t(gridDim.x) * blockDim.x;
-  const std::uint64_t S_up = (a.S + 31) & ~std::uint64_t(31);  // whole warps iterate together
+  // rows [row_begin, row_end); whole warps iterate together
+  const std::uint64_t S_up = row_begin + ((row_end - row_begin + 31) & ~std::uint64_t(31));
   // binary32 cell-unit scale and margin (rounded up; the slacks cover the rest)
   const float inv_e = static_cast<float>(og.inv_edge);
   const float margin_c = static_cast<float>(og.margin * og.inv_edge) * 1.0001f + 1e-30f;
@@ -590,15 +592,15 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
   const float qh_err = static_cast<float>(og.qh) * 0.50011f;
   // software pipeline: the vertex ids (and parity) of the next row are in
   // flight while this row's coordinates are gathered and tested
-  std::uint64_t s = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  std::uint32_t self = part_of(s_off, a.k, s < a.S ? s : (a.S ? a.S - 1 : 0));
+  std::uint64_t s = row_begin + std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  std::uint32_t self = part_of(s_off, a.k, s < row_end ? s : row_end - 1);
   std::uint32_t vn[D + 1];
   std::int8_t parn = 1;
 #pragma unroll
-  for (int j = 0; j <= D; ++j) vn[j] = s < a.S ? __ldcs(a.verts + std::uint64_t(j) * a.S + s) : kInfVertex;
-  if (s < a.S) parn = __ldcs(a.parity + s);
+  for (int j = 0; j <= D; ++j) vn[j] = s < row_end ? __ldcs(a.verts + std::uint64_t(j) * a.S + s) : kInfVertex;
+  if (s < row_end) parn = __ldcs(a.parity + s);
   for (; s < S_up; s += stride) {
-    const bool valid = s < a.S;
+    const bool valid = s < row_end;
     std::uint32_t v[D + 1];
 #pragma unroll
     for (int j = 0; j <= D; ++j) v[j] = vn[j];
@@ -606,14 +608,14 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
     {
       const std::uint64_t sn = s + stride;
 #pragma unroll
-      for (int j = 0; j <= D; ++j) vn[j] = sn < a.S ? __ldcs(a.verts + std::uint64_t(j) * a.S + sn) : kInfVertex;
-      if (sn < a.S) parn = __ldcs(a.parity + sn);
+      for (int j = 0; j <= D; ++j) vn[j] = sn < row_end ? __ldcs(a.verts + std::uint64_t(j) * a.S + sn) : kInfVertex;
+      if (sn < row_end) parn = __ldcs(a.parity + sn);
     }
     const bool inf = valid && v[D] == kInfVertex;
     bool is_cand = false;
     // rows only grow along the grid-stride loop: advance the part cursor
     {
-      const std::uint64_t sc = valid ? s : a.S - 1;
+      const std::uint64_t sc = valid ? s : row_end - 1;
       while (self + 1 < a.k && s_off[self + 1] <= sc) ++self;
     }
     if (valid && !inf) {
@@ -653,6 +655,28 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
   }
 }
 
+// Queue cursors: warps claim batches of 32 with atomicAdd, so a drained
+// cursor overshoots the queue length; the last CTA of a launch rewinds it to
+// the length the launch worked on, so a later launch over a grown queue
+// (host-path chunks) resumes exactly there.
+__device__ __forceinline__ unsigned claim_batch(unsigned* next) {
+  unsigned base = 0;
+  if ((threadIdx.x & 31u) == 0) base = atomicAdd(next, 32u);
+  return __shfl_sync(0xffffffffu, base, 0);
+}
+
+__device__ __forceinline__ void rewind_cursor(unsigned* next, unsigned* fin, unsigned limit) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(fin, 1u) == gridDim.x - 1) {
+      *next = limit;
+      *fin = 0u;
+      __threadfence();
+    }
+  }
+}
+
 // per-lane candidate record for the flattened scan (shared memory, per warp)
 template <int D>
 struct CandSlot {
@@ -680,7 +704,8 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
                                                                    const unsigned* __restrict__ ncand_p,
                                                                    unsigned* __restrict__ next,
                                                                    std::uint32_t* __restrict__ wide,
-                                                                   unsigned* __restrict__ nwide) {
+                                                                   unsigned* __restrict__ nwide,
+                                                                   unsigned* __restrict__ fin) {
   __shared__ OwnerGrid<D> og;
   __shared__ CandSlot<D> slots[kExactWarps][32];
   __shared__ unsigned char nzl[kExactWarps][32];
@@ -700,9 +725,7 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
   unsigned char* nz = nzl[wid];
   const unsigned full = 0xffffffffu;
   for (;;) {
-    unsigned base = 0;
-    if (lane == 0) base = atomicAdd(next, 32u);
-    base = __shfl_sync(full, base, 0);
+    const unsigned base = claim_batch(next);
     if (base >= ncand) break;
     const unsigned t = base + lane;
     const bool has = t < ncand;
@@ -850,6 +873,7 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
         for (int j = 0; j <= D; ++j) a.vflags[v[j]] = 1;
     }
   }
+  rewind_cursor(next, fin, ncand);
 }
 
 // Wide candidates (cell range wider than 5 per axis, or non-finite spheres):
@@ -1000,7 +1024,8 @@ __global__ void __launch_bounds__(kWideWarps * 32, 6) k_border_wide(BorderArgs a
                                                                  const std::uint32_t* __restrict__ wide,
                                                                  std::uint64_t cap,
                                                                  const unsigned* __restrict__ nwide_p,
-                                                                 unsigned* __restrict__ next) {
+                                                                 unsigned* __restrict__ next,
+                                                                 unsigned* __restrict__ fin) {
   __shared__ OwnerGrid<D> og;
   __shared__ WideEntry<D> stacks[kWideWarps][kWideStack];
   extern __shared__ std::uint64_t s_off[];
@@ -1012,9 +1037,7 @@ __global__ void __launch_bounds__(kWideWarps * 32, 6) k_border_wide(BorderArgs a
   WideEntry<D>* stk = stacks[threadIdx.x >> 5];
   const unsigned full = 0xffffffffu;
   for (;;) {
-    unsigned base = 0;
-    if (lane == 0) base = atomicAdd(next, 32u);
-    base = __shfl_sync(full, base, 0);
+    const unsigned base = claim_batch(next);
     if (base >= nwide) break;
     const unsigned t = base + lane;
     const bool has = t < nwide;
@@ -1051,6 +1074,7 @@ __global__ void __launch_bounds__(kWideWarps * 32, 6) k_border_wide(BorderArgs a
         for (int j = 0; j <= D; ++j) a.vflags[v[j]] = 1;
     }
   }
+  rewind_cursor(next, fin, nwide);
 }
 
 // K6: rows with the infinite vertex (hull facets). Lanes set up 32 rows
@@ -1330,36 +1354,69 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
     const unsigned blocks = static_cast<unsigned>(want < std::uint64_t(sms) * 32 ? want : std::uint64_t(sms) * 32);
     {
       if (tiled && in->S > 0) {
-        StageTimer ta(ctx, "border.prefilter");
         const std::uint64_t qcap = in->S + 32;
         SBDT_WS(cq, std::uint32_t, "border.cand", qcap * (D + 2));
-        SBDT_WS(cn, unsigned, "border.cand_n", 4);  // {candidates, next, wide, next wide}
-        SBDT_CUDA_TRY(cudaMemsetAsync(cn, 0, 4 * sizeof(unsigned), st));
+        // {candidates, cursor, wide rows, wide cursor, CTAs done (exact), CTAs done (wide)}
+        SBDT_WS(cn, unsigned, "border.cand_n", 6);
+        SBDT_CUDA_TRY(cudaMemsetAsync(cn, 0, 6 * sizeof(unsigned), st));
         const std::uint64_t wcap = qcap;  // wide rows <= candidates
         SBDT_WS(wq, std::uint32_t, "border.wide", wcap * (D + 2));
         int per_sm = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_prefilter<D>, kBThreads, offs_sh);
-        std::uint64_t res = std::uint64_t(sms) * std::uint64_t(per_sm > 0 ? per_sm : 1);
-        const std::uint64_t wantA = (in->S + kBThreads - 1) / kBThreads;
-        k_border_prefilter<D><<<static_cast<unsigned>(wantA < res ? wantA : res), kBThreads, offs_sh, st>>>(a, og, cq, qcap, cn);
-        ta.end();
-        StageTimer tx(ctx, "border.exact");
+        const std::uint64_t resA = std::uint64_t(sms) * std::uint64_t(per_sm > 0 ? per_sm : 1);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_exact<D>, kExactWarps * 32, offs_sh);
-        res = std::uint64_t(sms) * std::uint64_t(per_sm > 0 ? per_sm : 1);
-        k_border_exact<D><<<static_cast<unsigned>(res), kExactWarps * 32, offs_sh, st>>>(
-            a, og, cq, qcap, cn, cn + 1, wq, cn + 2);
-        tx.end();
-        StageTimer tw(ctx, "border.exact_wide");
+        const unsigned resX = static_cast<unsigned>(sms * (per_sm > 0 ? per_sm : 1));
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_wide<D>, kWideWarps * 32, offs_sh);
-        res = std::uint64_t(sms) * std::uint64_t(per_sm > 0 ? per_sm : 1);
-        k_border_wide<D><<<static_cast<unsigned>(res), kWideWarps * 32, offs_sh, st>>>(a, og, wq, wcap, cn + 2, cn + 3);
-        if (a.counters) k_cand_count<<<1, 1, 0, st>>>(cn, in->S, a.counters);
-        ctx->launches += a.counters ? 4 : 3;
+        const unsigned resW = static_cast<unsigned>(sms * (per_sm > 0 ? per_sm : 1));
+        auto prefilter = [&](std::uint64_t r0, std::uint64_t r1) {
+          const std::uint64_t want = (r1 - r0 + kBThreads - 1) / kBThreads;
+          k_border_prefilter<D><<<static_cast<unsigned>(want < resA ? want : resA), kBThreads, offs_sh, st>>>(
+              a, og, cq, qcap, cn, r0, r1);
+        };
+        auto exact = [&]() {
+          k_border_exact<D><<<resX, kExactWarps * 32, offs_sh, st>>>(a, og, cq, qcap, cn, cn + 1, wq, cn + 2, cn + 4);
+        };
+        auto wide = [&]() { k_border_wide<D><<<resW, kWideWarps * 32, offs_sh, st>>>(a, og, wq, wcap, cn + 2, cn + 3, cn + 5); };
+        if (ctx->chunks.empty()) {
+          {
+            StageTimer ta(ctx, "border.prefilter");
+            prefilter(0, in->S);
+          }
+          {
+            StageTimer tx(ctx, "border.exact");
+            exact();
+          }
+          StageTimer tw(ctx, "border.exact_wide");
+          wide();
+          ctx->launches += 3;
+        } else {
+          // host path: every chunk of rows as soon as its upload has landed;
+          // the exact and wide kernels drain the queues grown so far (their
+          // cursors persist), so all three overlap the remaining uploads
+          std::uint64_t r0 = 0;
+          for (const auto& c : ctx->chunks) {
+            const std::uint64_t r1 = c.first < in->S ? c.first : in->S;
+            SBDT_CUDA_TRY(cudaStreamWaitEvent(st, c.second, 0));
+            if (r1 > r0) {
+              prefilter(r0, r1);
+              exact();
+              wide();
+              ctx->launches += 3;
+            }
+            r0 = r1;
+          }
+        }
+        if (a.counters) {
+          k_cand_count<<<1, 1, 0, st>>>(cn, in->S, a.counters);
+          ctx->launches += 1;
+        }
       } else if (blocks > 0) {
+        for (const auto& c : ctx->chunks) SBDT_CUDA_TRY(cudaStreamWaitEvent(st, c.second, 0));
         StageTimer t(ctx, "border.finite");
         k_border_finite<D><<<blocks, kBThreads, offs_sh, st>>>(a, og);
       }
     }
+    for (const auto& c : ctx->chunks) SBDT_CUDA_TRY(cudaStreamWaitEvent(st, c.second, 0));
     {
       StageTimer t(ctx, "border.infinite");
       k_border_infinite<D><<<sms * 4, kWideWarps * 32, offs_sh, st>>>(a, og);

@@ -91,6 +91,9 @@ void sbdt_gpu_destroy(sbdt_gpu_ctx* ctx) {
   for (auto& kv : ctx->bufs)
     if (kv.second.ptr) cudaFree(kv.second.ptr);
   if (ctx->d_status) cudaFree(ctx->d_status);
+  for (cudaEvent_t e : ctx->chunk_events) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -196,6 +199,32 @@ int sbdt_gpu_assign_points_dev(sbdt_gpu_ctx* ctx, int dim, const double* d_coord
   return kOk;
 }
 
+// Chunked uploads for the host-buffer entry points: copies go to the
+// context's copy stream in kUploadChunks pieces, each closed by an event the
+// kernels wait for, so the kernels on chunk i overlap the upload of chunk
+// i+1 (and the compute stream never waits for the whole input).
+static constexpr int kUploadChunks = 8;
+
+static int prepare_chunks(sbdt_gpu_ctx* ctx) {
+  if (!ctx->copy_stream) SBDT_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  while (ctx->chunk_events.size() < kUploadChunks + 1) {
+    cudaEvent_t e;
+    SBDT_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->chunk_events.push_back(e);
+  }
+  ctx->chunks.clear();
+  return SBDT_OK;
+}
+
+// Clears the chunk state on every exit path of a host-buffer call.
+struct ChunkScope {
+  sbdt_gpu_ctx* ctx;
+  ~ChunkScope() {
+    ctx->chunks.clear();
+    ctx->sample_xyz = nullptr;
+  }
+};
+
 int sbdt_gpu_assign_points(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint64_t n,
                            const uint32_t* sample_ids, const uint32_t* sample_labels, uint32_t m, uint32_t k,
                            uint32_t* labels_out, uint64_t* part_offsets_out, uint32_t* part_ids_out,
@@ -215,9 +244,29 @@ int sbdt_gpu_assign_points(sbdt_gpu_ctx* ctx, int dim, const double* coords, uin
     TRY(dalloc(ctx, "h.poff", k + 1, &d_poff));
     TRY(dalloc(ctx, "h.pids", n, &d_pids));
   }
-  SBDT_CUDA_TRY(cudaMemcpyAsync(d_xyz, coords, sizeof(double) * n * dim, cudaMemcpyHostToDevice, st));
+  TRY(prepare_chunks(ctx));
+  ChunkScope scope{ctx};
+  // samples first (compact coordinates gathered here: the table build needs
+  // only them), then the points in chunks on the copy stream
+  double* d_sxyz;
+  TRY(dalloc(ctx, "h.sxyz", std::uint64_t(m) * dim, &d_sxyz));
+  std::vector<double> sxyz(std::size_t(m) * dim);
+  for (uint32_t i = 0; i < m; ++i) {
+    if (sample_ids[i] >= n) return fail(ctx, SBDT_ERR_INVALID, "sample id out of range");
+    for (int d = 0; d < dim; ++d) sxyz[std::size_t(i) * dim + d] = coords[std::size_t(sample_ids[i]) * dim + d];
+  }
+  SBDT_CUDA_TRY(cudaMemcpyAsync(d_sxyz, sxyz.data(), sizeof(double) * sxyz.size(), cudaMemcpyHostToDevice, st));
   SBDT_CUDA_TRY(cudaMemcpyAsync(d_sid, sample_ids, sizeof(uint32_t) * m, cudaMemcpyHostToDevice, st));
   SBDT_CUDA_TRY(cudaMemcpyAsync(d_slab, sample_labels, sizeof(uint32_t) * m, cudaMemcpyHostToDevice, st));
+  ctx->sample_xyz = d_sxyz;
+  for (int c = 0; c < kUploadChunks; ++c) {
+    const uint64_t i0 = n * c / kUploadChunks, i1 = n * (c + 1) / kUploadChunks;
+    if (i1 > i0)
+      SBDT_CUDA_TRY(cudaMemcpyAsync(d_xyz + i0 * dim, coords + i0 * dim, sizeof(double) * (i1 - i0) * dim,
+                                    cudaMemcpyHostToDevice, ctx->copy_stream));
+    SBDT_CUDA_TRY(cudaEventRecord(ctx->chunk_events[c], ctx->copy_stream));
+    ctx->chunks.emplace_back(i1, ctx->chunk_events[c]);
+  }
   TRY(sbdt_gpu_assign_points_dev(ctx, dim, d_xyz, n, d_sid, d_slab, m, k, d_lab, d_poff, d_pids, d_bbox));
   SBDT_CUDA_TRY(cudaMemcpyAsync(labels_out, d_lab, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, st));
   if (parts) {
@@ -290,16 +339,33 @@ int sbdt_gpu_find_border(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint6
     TRY(dalloc(ctx, "h.bcnt", 1, &d_bcnt));
   }
   if (spheres_out) TRY(dalloc(ctx, "h.sph", S * (dim + 1), &d_sph));
-  SBDT_CUDA_TRY(cudaMemcpyAsync(d_xyz, coords, sizeof(double) * n * dim, cudaMemcpyHostToDevice, st));
-  SBDT_CUDA_TRY(cudaMemcpyAsync(d_lab, labels, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, st));
-  SBDT_CUDA_TRY(cudaMemcpyAsync(d_off, offsets, sizeof(uint64_t) * (k + 1), cudaMemcpyHostToDevice, st));
-  SBDT_CUDA_TRY(cudaMemcpyAsync(d_verts, verts, sizeof(uint32_t) * S * (dim + 1), cudaMemcpyHostToDevice, st));
-  // Without the BFS only the hull rows' last neighbour (the finite simplex
-  // across the hull facet, row dim of the SoA) is read.
-  if (bfs) SBDT_CUDA_TRY(cudaMemcpyAsync(d_nbrs, nbrs, sizeof(uint32_t) * S * (dim + 1), cudaMemcpyHostToDevice, st));
-  else
-    SBDT_CUDA_TRY(cudaMemcpyAsync(d_nbrs + S * dim, nbrs + S * dim, sizeof(uint32_t) * S, cudaMemcpyHostToDevice, st));
-  SBDT_CUDA_TRY(cudaMemcpyAsync(d_par, parity, S, cudaMemcpyHostToDevice, st));
+  TRY(prepare_chunks(ctx));
+  ChunkScope scope{ctx};
+  cudaStream_t cs = ctx->copy_stream;
+  // points, labels and part offsets first (the owner grid needs them), then
+  // the simplex rows in chunks; everything on the copy stream, in order
+  SBDT_CUDA_TRY(cudaMemcpyAsync(d_xyz, coords, sizeof(double) * n * dim, cudaMemcpyHostToDevice, cs));
+  SBDT_CUDA_TRY(cudaMemcpyAsync(d_lab, labels, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, cs));
+  SBDT_CUDA_TRY(cudaMemcpyAsync(d_off, offsets, sizeof(uint64_t) * (k + 1), cudaMemcpyHostToDevice, cs));
+  SBDT_CUDA_TRY(cudaEventRecord(ctx->chunk_events[kUploadChunks], cs));
+  SBDT_CUDA_TRY(cudaStreamWaitEvent(st, ctx->chunk_events[kUploadChunks], 0));
+  for (int c = 0; c < kUploadChunks; ++c) {
+    const uint64_t r0 = S * c / kUploadChunks, r1 = S * (c + 1) / kUploadChunks;
+    if (r1 > r0) {
+      for (int j = 0; j <= dim; ++j)
+        SBDT_CUDA_TRY(cudaMemcpyAsync(d_verts + j * S + r0, verts + j * S + r0, sizeof(uint32_t) * (r1 - r0),
+                                      cudaMemcpyHostToDevice, cs));
+      SBDT_CUDA_TRY(cudaMemcpyAsync(d_par + r0, parity + r0, r1 - r0, cudaMemcpyHostToDevice, cs));
+      // without the BFS only the hull rows' last neighbour (the finite
+      // simplex across the hull facet, row dim of the SoA) is read
+      for (int j = bfs ? 0 : dim; j <= dim; ++j)
+        SBDT_CUDA_TRY(cudaMemcpyAsync(d_nbrs + j * S + r0, nbrs + j * S + r0, sizeof(uint32_t) * (r1 - r0),
+                                      cudaMemcpyHostToDevice, cs));
+    }
+    SBDT_CUDA_TRY(cudaEventRecord(ctx->chunk_events[c], cs));
+    ctx->chunks.emplace_back(r1, ctx->chunk_events[c]);
+  }
+
   a.d_xyz = d_xyz;
   a.d_labels = d_lab;
   a.d_offsets = d_off;

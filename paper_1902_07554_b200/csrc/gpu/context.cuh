@@ -38,6 +38,13 @@ struct sbdt_gpu_ctx {
   std::vector<Stage> stages;
   std::vector<cudaEvent_t> event_pool;
   std::size_t events_used = 0;
+  // host-buffer entry points: uploads run on copy_stream in chunks; chunk i
+  // (points / simplex rows below chunks[i].first) is resident once
+  // chunks[i].second has completed. Empty for the *_dev entry points.
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> chunk_events;
+  std::vector<std::pair<std::uint64_t, cudaEvent_t>> chunks;
+  const double* sample_xyz = nullptr;  // compact sample coordinates (host path), else gathered from the points
 };
 
 namespace sbdt_gpu {

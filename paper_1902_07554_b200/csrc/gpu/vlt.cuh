@@ -363,7 +363,8 @@ __device__ __forceinline__ std::uint32_t exact_among(const double* x, const VltE
 // K2: table-driven point pass (coordinates streamed once; overflow points
 // are queued for k_assign_overflow so they do not diverge the warp).
 template <int D>
-__global__ void __launch_bounds__(256) k_assign_vlt(const double* __restrict__ xyz, std::uint64_t n,
+__global__ void __launch_bounds__(256) k_assign_vlt(const double* __restrict__ xyz, std::uint64_t i_begin,
+                                                    std::uint64_t n,
                                                     const SampleGrid<D>* __restrict__ sgp,
                                                     const std::uint32_t* __restrict__ heads,
                                                     const VltEntry* __restrict__ slab,
@@ -380,7 +381,7 @@ __global__ void __launch_bounds__(256) k_assign_vlt(const double* __restrict__ x
   double blo[D], bhi[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) blo[d] = INFINITY, bhi[d] = -INFINITY;
-  for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+  for (std::uint64_t i = i_begin + std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += std::uint64_t(gridDim.x) * blockDim.x) {
     double x[D];
 #pragma unroll
