@@ -127,3 +127,49 @@ def test_pinned_output_buffers_match(ctx):
     with pytest.raises(ValueError):
         gpu.find_border(inst.points, a.labels, part, ctx=ctx,
                         out=gpu.BorderSet(np.empty(S + 1, np.uint8), None, None, np.empty(inst.n, np.uint32)))
+
+
+def test_host_path_equals_device_path(ctx):
+    """The host-buffer entry points (chunked uploads overlapping the kernels,
+    queue cursors resumed across chunk launches) give the same results as the
+    device-pointer entry points on one instance."""
+    import torch
+    inst = host.make_instance(2, n=300_000, k=16)
+    part = gpu.assign_points(inst.points, inst.sample_ids, inst.sample_labels, 16, ctx=ctx)
+    pt = host.attach_partials(inst, part.labels)
+    hb = gpu.find_border(inst.points, part.labels, pt, gpu.IntersectionPolicy("grid"), hull_bfs=False, ctx=ctx)
+    dev = torch.device("cuda", 0)
+    t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a).view(dt)).to(dev)  # noqa: E731
+    d_xyz = torch.from_numpy(np.ascontiguousarray(inst.points)).to(dev)
+    d_sid, d_slab = t(inst.sample_ids, np.int32), t(inst.sample_labels, np.int32)
+    d_lab = torch.empty(inst.n, dtype=torch.int32, device=dev)
+    d_bbox = torch.empty(6, dtype=torch.int64, device=dev)
+    dctx = gpu.Context(0)  # device-pointer path on torch's stream
+    dctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    dctx.assign_points_dev(inst.dim, d_xyz.data_ptr(), inst.n, d_sid.data_ptr(), d_slab.data_ptr(),
+                          len(inst.sample_ids), 16, d_lab.data_ptr(), None, None, d_bbox.data_ptr())
+    torch.cuda.synchronize()
+    assert np.array_equal(d_lab.cpu().numpy().view(np.uint32), part.labels)
+    S = pt.S
+    a = gpu.BorderArgs()
+    keep = [d_xyz, d_lab, d_bbox]
+    d_off, d_v, d_n, d_p = t(pt.offsets, np.int64), t(pt.verts, np.int32), t(pt.nbrs, np.int32), t(pt.parity, np.int8)
+    d_pos = torch.empty(S, dtype=torch.uint8, device=dev)
+    d_vf = torch.empty(inst.n + 64, dtype=torch.uint8, device=dev)
+    d_vids = torch.empty(inst.n, dtype=torch.int32, device=dev)
+    d_cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    keep += [d_off, d_v, d_n, d_p, d_pos, d_vf, d_vids, d_cnt]
+    a.dim, a.d_xyz, a.n, a.d_labels, a.k = inst.dim, d_xyz.data_ptr(), inst.n, d_lab.data_ptr(), 16
+    a.d_offsets, a.d_verts, a.d_nbrs, a.d_parity, a.S = d_off.data_ptr(), d_v.data_ptr(), d_n.data_ptr(), \
+        d_p.data_ptr(), S
+    a.policy, a.c_G, a.flags = gpu.POLICY["grid"], 1.0, 0
+    a.d_bbox_ordered = d_bbox.data_ptr()
+    a.d_positive, a.d_vertex_flags, a.d_vertex_ids, a.d_vertex_count = d_pos.data_ptr(), d_vf.data_ptr(), \
+        d_vids.data_ptr(), d_cnt.data_ptr()
+    dctx.find_border_dev(a)
+    torch.cuda.synchronize()
+    dctx.synchronize()
+    assert np.array_equal(d_pos.cpu().numpy(), hb.positive)
+    nv = int(d_cnt.item())
+    assert np.array_equal(d_vids[:nv].cpu().numpy().view(np.uint32), hb.positive_vertex_ids)
+    dctx.close()
