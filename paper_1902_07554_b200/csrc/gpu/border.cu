@@ -406,8 +406,64 @@ struct BorderArgs {
   std::uint32_t* inf_queue;
   unsigned* inf_count;
   unsigned* status;
-  unsigned long long* counters;  // [0] finite rows, [1] exact-stage rows, [2] positive (optional)
+  unsigned long long* counters;  // census (optional), see sbdt_gpu_border_stats
+  // exact policy
+  int exact;
+  const std::uint32_t* cell_start;  // per level-0 cell: first slot in cell_pts (k_cell_*)
+  const void* cell_pts;             // CellPt<D>[n]
+  std::uint32_t* esc;               // undecided filtered in_sphere tests: (row, cell-point slot)
+  unsigned* esc_count;
+  unsigned esc_cap;
 };
+
+// Exact policy, one leaf cell: is some point of another part strictly inside
+// the circumsphere of p (in_sphere_oriented, geometry.hpp:144-151)? The
+// filtered predicate decides almost always; undecided pairs are queued for
+// k_border_escalate (expansion arithmetic) and count as "not inside" here.
+template <int D>
+__device__ bool cell_points_inside(const BorderArgs& a, unsigned long long idx, const double (*p)[D], int parity,
+                                   std::uint32_t self, std::uint64_t s) {
+  const CellPt<D>* pts = static_cast<const CellPt<D>*>(a.cell_pts);
+  const double* A = parity != 1 ? p[1] : p[0];
+  const double* B = parity != 1 ? p[0] : p[1];
+  for (std::uint32_t t = a.cell_start[idx], e = a.cell_start[idx + 1]; t < e; ++t) {
+    const CellPt<D> q = pts[t];
+    if (q.label == self) continue;
+    int r;
+    if constexpr (D == 3) r = sbdt_pred::in_sphere3_filtered(A, B, p[2], p[3], q.x);
+    else r = sbdt_pred::in_sphere2_filtered(A, B, p[2], q.x);
+    if (r == 1) return true;
+    if (r == 2) {
+      const unsigned slot = atomicAdd(a.esc_count, 1u);
+      if (slot < a.esc_cap) {
+        a.esc[2ull * slot] = static_cast<std::uint32_t>(s);
+        a.esc[2ull * slot + 1] = t;
+      } else {
+        atomicOr(a.status, kStQueueOverflow);
+      }
+    }
+  }
+  return false;
+}
+
+// Exact policy, hull row: is some point of another part of this leaf cell
+// strictly on the outer side of the facet (orient != 0, != inner side)?
+template <int D>
+__device__ bool cell_points_outside(const BorderArgs& a, unsigned long long idx, const double* const* facet,
+                                    int inner_sign, std::uint32_t self) {
+  const CellPt<D>* pts = static_cast<const CellPt<D>*>(a.cell_pts);
+  const double* q4[D + 1];
+#pragma unroll
+  for (int j = 0; j < D; ++j) q4[j] = facet[j];
+  for (std::uint32_t t = a.cell_start[idx], e = a.cell_start[idx + 1]; t < e; ++t) {
+    const CellPt<D> q = pts[t];
+    if (q.label == self) continue;
+    q4[D] = q.x;
+    const int o = orient_dev<D>(q4);
+    if (o != 0 && o != inner_sign) return true;
+  }
+  return false;
+}
 
 // bbox-policy root box of partition j: its point bbox snapped to the occupied
 // cells (= the AABB-tree root, oracle GridIndex::bbox_policy_box). Cell
@@ -556,7 +612,7 @@ __device__ __forceinline__ int prefilter_decide(const OwnerGrid<D>& og, const Bo
   // (|lo| / edge + dims) < 2^26, checked by the caller through pos_ok). If the
   // inner ball, shrunk by the exact stage's margin, still reaches that box,
   // the binary64 box test on the binary64 sphere accepts it.
-  if (!inside || !pos_ok) return 2;
+  if (!inside || !pos_ok || a.exact) return 2;  // exact policy: a foreign cell is not a foreign point
   const float rin_c = ((sp.r * 0.999996f - 2.01f * sp.e * 1.000001f) * 0.999999f - slack) * inv_e * 0.999998f;
   if (!(rin_c - margin_c > 1.7321f * sl_max + 1e-7f)) return 2;
   const std::uint16_t code = a.owner[og_index<D>(og, 0, c0)];
@@ -693,11 +749,13 @@ struct CandSlot {
   unsigned inv[D];  // ceil(2^16 / span)
   unsigned self;
   unsigned excl;    // first position of this candidate in the flattened stream
+  unsigned row;     // simplex row (exact policy: reload its vertices for the point tests)
+  unsigned qi;      // its queue position
 };
 
 // Candidates from the prefilter; rows with wide cell ranges (modes 2, 3) are
 // forwarded to the wide queue (k_border_wide).
-template <int D>
+template <int D, bool Ex>
 __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
                                                                    const std::uint32_t* __restrict__ cand,
                                                                    std::uint64_t cap,
@@ -798,6 +856,8 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
       }
       sl[lane].r2 = r2;
       sl[lane].self = self;
+      sl[lane].row = static_cast<unsigned>(s);
+      sl[lane].qi = t;
       cnt = D == 3 ? unsigned(span[1] * span[2]) : unsigned(span[1]);
     }
     unsigned incl = cnt;
@@ -856,8 +916,27 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
           }
         }
         const std::uint32_t sf = r.self;
+        if constexpr (!Ex) {
 #pragma unroll
-        for (int i0 = 0; i0 < 5; ++i0) h = h || (geo[i0] && code[i0] != kOwnerEmpty && code[i0] != sf);
+          for (int i0 = 0; i0 < 5; ++i0) h = h || (geo[i0] && code[i0] != kOwnerEmpty && code[i0] != sf);
+        } else {
+          // exact policy: the points of the foreign overlapping cells
+          bool loaded = false;
+          double pv[D + 1][D];
+          int par = 1;
+          for (int i0 = 0; i0 < static_cast<int>(r.span[0]) && !h; ++i0) {
+            if (!(geo[i0] && code[i0] != kOwnerEmpty && code[i0] != sf)) continue;
+            if (!loaded) {
+              std::uint32_t vv[D + 1];
+#pragma unroll
+              for (int j = 0; j <= D; ++j) vv[j] = cand[std::uint64_t(j + 1) * cap + r.qi];
+              load_simplex<D>(a, vv, pv);
+              par = a.parity[r.row];
+              loaded = true;
+            }
+            h = cell_points_inside<D>(a, base + r.ent[0][i0].off, pv, par, sf, r.row);
+          }
+        }
       }
       done |= __reduce_or_sync(full, h ? 1u << cl : 0u);
       cur += __popc(smask);
@@ -984,9 +1063,9 @@ __device__ bool warp_descent(const OwnerGrid<D>& og, const std::uint16_t* __rest
   return false;
 }
 
-template <int D>
+template <int D, bool Ex, class Leaf>
 __device__ bool warp_sphere_descent(const OwnerGrid<D>& og, const std::uint16_t* __restrict__ owner, const double* c,
-                                    double r2, std::uint32_t self, WideEntry<D>* stk,
+                                    double r2, std::uint32_t self, WideEntry<D>* stk, const Leaf& leaf,
                                     unsigned long long* counters = nullptr) {
   if (isnan(r2)) return false;
   bool fin = isfinite(r2);
@@ -1012,14 +1091,21 @@ __device__ bool warp_sphere_descent(const OwnerGrid<D>& og, const std::uint16_t*
     double blo[D], bhi[D];
     og_block_box<D>(og, L, cc, blo, bhi);
     if (!box_sphere<D>(blo, bhi, c, r2)) return 0;
-    if (L == 0 || box_inside_sphere<D>(blo, bhi, c, r2)) return 2;
-    return 1;
+    if constexpr (Ex) {
+      return L > 0 ? 1 : (leaf(cc) ? 2 : 0);
+    } else {
+      if (L == 0 || box_inside_sphere<D>(blo, bhi, c, r2)) return 2;
+      return 1;
+    }
   };
-  auto fallback = [&]() { return og_sphere_hits_foreign<D>(og, owner, c, r2, self); };
+  auto fallback = [&]() {
+    if constexpr (Ex) return og_sphere_exact_serial<D>(og, owner, c, r2, self, leaf);
+    else return og_sphere_hits_foreign<D>(og, owner, c, r2, self);
+  };
   return warp_descent<D>(og, owner, a, b, self, test, fallback, stk, counters);
 }
 
-template <int D>
+template <int D, bool Ex>
 __global__ void __launch_bounds__(kWideWarps * 32, 6) k_border_wide(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
                                                                  const std::uint32_t* __restrict__ wide,
                                                                  std::uint64_t cap,
@@ -1062,7 +1148,24 @@ __global__ void __launch_bounds__(kWideWarps * 32, 6) k_border_wide(BorderArgs a
       for (int d = 0; d < D; ++d) cl[d] = __shfl_sync(full, c[d], l);
       const double rl = __shfl_sync(full, r2, l);
       const std::uint32_t sl = __shfl_sync(full, self, l);
-      const bool hit = warp_sphere_descent<D>(og, a.owner, cl, rl, sl, stk, a.counters);
+      // exact policy: lanes test their leaf cells' points against the
+      // candidate's circumsphere (vertices broadcast, coordinates reloaded)
+      std::uint32_t vl[D + 1];
+#pragma unroll
+      for (int j = 0; j <= D; ++j) vl[j] = __shfl_sync(full, v[j], l);
+      const std::uint64_t srow = __shfl_sync(full, s, l);
+      double pv[D + 1][D];
+      int par = 1;
+      bool loaded = false;
+      auto leaf = [&](const int* cell) -> bool {
+        if (!loaded) {
+          load_simplex<D>(a, vl, pv);
+          par = a.parity[srow];
+          loaded = true;
+        }
+        return cell_points_inside<D>(a, og_index<D>(og, 0, cell), pv, par, sl, srow);
+      };
+      const bool hit = warp_sphere_descent<D, Ex>(og, a.owner, cl, rl, sl, stk, leaf, a.counters);
       if (static_cast<int>(lane) == l) pos = hit;
       if (a.counters && hit && lane == 0) atomicAdd(&a.counters[9], 1ull);
       __syncwarp();
@@ -1081,7 +1184,7 @@ __global__ void __launch_bounds__(kWideWarps * 32, 6) k_border_wide(BorderArgs a
 // (facet ids, the finite neighbour's inner vertex, its exact orientation);
 // under the grid policy each row's halfspace descent then runs on the whole
 // warp (warp_descent), the bbox policy tests the k-1 root boxes per lane.
-template <int D>
+template <int D, bool Ex>
 __global__ void __launch_bounds__(kWideWarps * 32) k_border_infinite(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp) {
   __shared__ OwnerGrid<D> og;
   __shared__ WideEntry<D> stacks[kWideWarps][kWideStack];
@@ -1157,14 +1260,23 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_border_infinite(BorderArgs 
         int lo[D], hi[D];
 #pragma unroll
         for (int d = 0; d < D; ++d) lo[d] = 0, hi[d] = og.ldims[0][d] - 1;
+        auto leaf = [&](const int* cell) -> bool {
+          return cell_points_outside<D>(a, og_index<D>(og, 0, cell), facet, sl_sign, sl_self);
+        };
         auto test = [&](int L, const int* cc) -> int {
           double blo[D], bhi[D];
           og_block_box<D>(og, L, cc, blo, bhi);
           const int out = corners_outside<D>(facet, sl_sign, blo, bhi);
           if (out == 0) return 0;
-          return (L == 0 || out == (1 << D)) ? 2 : 1;
+          if (out == (1 << D)) return 2;  // the whole box is strictly outside
+          if (L > 0) return 1;
+          if constexpr (Ex) return leaf(cc) ? 2 : 0;
+          else return 2;
         };
-        auto fallback = [&]() { return og_halfspace_hits_foreign<D>(og, a.owner, facet, sl_sign, sl_self); };
+        auto fallback = [&]() {
+          if constexpr (Ex) return og_halfspace_exact_serial<D>(og, a.owner, facet, sl_sign, sl_self, leaf);
+          else return og_halfspace_hits_foreign<D>(og, a.owner, facet, sl_sign, sl_self);
+        };
         const bool hit = warp_descent<D>(og, a.owner, lo, hi, sl_self, test, fallback, stk);
         if (static_cast<int>(lane) == l) pos = hit;
         __syncwarp();
@@ -1228,6 +1340,102 @@ __global__ void k_compact_write(const std::uint8_t* __restrict__ flags, std::uin
       if ((w[i] >> (8 * b)) & 0xFFu) out[pos++] = static_cast<std::uint32_t>(first + 4 * i + b);
 }
 
+// ---- exact policy: per-cell point lists and the escalation pass --------------
+template <int D>
+__global__ void k_cell_count(const double* __restrict__ xyz, std::uint64_t n, const OwnerGrid<D>* __restrict__ ogp,
+                             std::uint32_t* __restrict__ cnt) {
+  __shared__ OwnerGrid<D> og;
+  if (threadIdx.x == 0) og = *ogp;
+  __syncthreads();
+  for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += std::uint64_t(gridDim.x) * blockDim.x) {
+    int c[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) c[d] = static_cast<int>(cell_coord<D>(og.g, xyz[i * D + d], d));
+    atomicAdd(&cnt[og_index<D>(og, 0, c)], 1u);
+  }
+}
+
+template <int D>
+__global__ void k_cell_scatter(const double* __restrict__ xyz, const std::uint32_t* __restrict__ labels,
+                               std::uint64_t n, const OwnerGrid<D>* __restrict__ ogp,
+                               const std::uint32_t* __restrict__ start, std::uint32_t* __restrict__ fill,
+                               CellPt<D>* __restrict__ pts) {
+  __shared__ OwnerGrid<D> og;
+  if (threadIdx.x == 0) og = *ogp;
+  __syncthreads();
+  for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += std::uint64_t(gridDim.x) * blockDim.x) {
+    CellPt<D> q;
+    int c[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      q.x[d] = xyz[i * D + d];
+      c[d] = static_cast<int>(cell_coord<D>(og.g, q.x[d], d));
+    }
+    q.label = labels[i];
+    q.pid = static_cast<std::uint32_t>(i);
+    const unsigned long long idx = og_index<D>(og, 0, c);
+    pts[start[idx] + atomicAdd(&fill[idx], 1u)] = q;
+  }
+}
+
+// Undecided filtered in_sphere tests, decided with expansion arithmetic
+// (predicates.hpp; an independent exact method from the reference's
+// scaled-integer fallback, geometry.cpp:32-146). One scratch area per thread.
+constexpr int kEscThreads = 256;
+
+template <int D>
+__global__ void __launch_bounds__(128) k_border_escalate(BorderArgs a, double* __restrict__ scratch) {
+  const unsigned count = min(*a.esc_count, a.esc_cap);
+  const unsigned tid = blockIdx.x * blockDim.x + threadIdx.x;
+  double* buf = scratch + std::size_t(tid) * (D == 3 ? sbdt_pred::kInSphere3Scratch : sbdt_pred::kInSphere2Scratch);
+  const CellPt<D>* pts = static_cast<const CellPt<D>*>(a.cell_pts);
+  for (unsigned e = tid; e < count; e += gridDim.x * blockDim.x) {
+    const std::uint64_t s = a.esc[2ull * e];
+    if (a.positive[s]) continue;  // decided by another point
+    const std::uint32_t t = a.esc[2ull * e + 1];
+    std::uint32_t v[D + 1];
+#pragma unroll
+    for (int j = 0; j <= D; ++j) v[j] = a.verts[std::uint64_t(j) * a.S + s];
+    const double* p[D + 1];
+#pragma unroll
+    for (int j = 0; j <= D; ++j) p[j] = a.xyz + std::size_t(v[j]) * D;
+    if (a.parity[s] != 1) {
+      const double* tmp = p[0];
+      p[0] = p[1];
+      p[1] = tmp;
+    }
+    const double* q = pts[t].x;
+    int r;
+    if constexpr (D == 3) r = sbdt_pred::in_sphere3_exact_buf(p[0], p[1], p[2], p[3], q, buf);
+    else r = sbdt_pred::in_sphere2_exact_buf(p[0], p[1], p[2], q, buf);
+    if (r > 0) {
+      a.positive[s] = 1;
+#pragma unroll
+      for (int j = 0; j <= D; ++j) a.vflags[v[j]] = 1;
+    }
+  }
+}
+
+// Circumspheres only (spheres_out with the grid / exact policies).
+template <int D>
+__global__ void k_border_spheres(BorderArgs a) {
+  for (std::uint64_t s = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; s < a.S;
+       s += std::uint64_t(gridDim.x) * blockDim.x) {
+    std::uint32_t v[D + 1];
+#pragma unroll
+    for (int j = 0; j <= D; ++j) v[j] = a.verts[std::uint64_t(j) * a.S + s];
+    if (v[D] == kInfVertex) continue;  // written by k_border_infinite
+    double p[D + 1][D], c[D], r2;
+    load_simplex<D>(a, v, p);
+    circumsphere_inflated<D>(p, c, &r2);
+#pragma unroll
+    for (int d = 0; d < D; ++d) a.spheres[s * (D + 1) + d] = c[d];
+    a.spheres[s * (D + 1) + D] = r2;
+  }
+}
+
 __global__ void k_cand_count(const unsigned* ncand, std::uint64_t S, unsigned long long* counters) {
   counters[0] = S;  // rows scanned by the prefilter (finite + infinite)
   counters[1] = *ncand;
@@ -1275,7 +1483,10 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
     pbbox = pb;
   }
 
-  const bool tiled = in->policy == SBDT_POLICY_GRID && !in->d_spheres;
+  // grid and exact policies: prefilter + exact + wide pipeline (spheres, when
+  // requested, by a separate pass); bbox: one lane per row (k_border_finite)
+  const bool tiled = in->policy != SBDT_POLICY_BBOX;
+  const bool exact_policy = in->policy == SBDT_POLICY_EXACT;
   std::uint64_t* xq = nullptr;
   if (tiled) {
     SBDT_WS(q, std::uint64_t, "border.xq", in->n + 1);
@@ -1307,8 +1518,27 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   k_owner_level<D><<<sms * 8, 256, 0, st>>>(og, owner, 1);
   k_owner_level<D><<<sms * 2, 256, 0, st>>>(og, owner, 2);
   k_owner_levels_tail<D><<<1, 1024, 0, st>>>(og, owner, 3);
+  // exact policy: per-cell point lists over the level-0 tiled index
+  std::uint32_t* cell_start = nullptr;
+  void* cell_pts = nullptr;
+  if (exact_policy) {
+    SBDT_WS(ccnt, std::uint32_t, "border.cell_cnt", owner_len + 1);
+    SBDT_WS(cstart, std::uint32_t, "border.cell_start", owner_len + 1);
+    SBDT_WS(cbs, std::uint32_t, "border.cell_bs", (owner_len + 1) / kScanTile + 2);
+    SBDT_WS(cpts, CellPt<D>, "border.cell_pts", in->n + 1);
+    SBDT_CUDA_TRY(cudaMemsetAsync(ccnt, 0, sizeof(std::uint32_t) * (owner_len + 1), st));
+    const std::uint64_t want = (in->n + 255) / 256;
+    const unsigned blocks = static_cast<unsigned>(want < std::uint64_t(sms) * 16 ? want : std::uint64_t(sms) * 16);
+    k_cell_count<D><<<blocks > 0 ? blocks : 1, 256, 0, st>>>(in->d_xyz, in->n, og, ccnt);
+    exclusive_scan(ccnt, cstart, owner_len + 1, cbs, nullptr, st, &ctx->launches);
+    SBDT_CUDA_TRY(cudaMemsetAsync(ccnt, 0, sizeof(std::uint32_t) * (owner_len + 1), st));
+    k_cell_scatter<D><<<blocks > 0 ? blocks : 1, 256, 0, st>>>(in->d_xyz, in->d_labels, in->n, og, cstart, ccnt, cpts);
+    ctx->launches += 2;
+    cell_start = cstart;
+    cell_pts = cpts;
+  }
   std::uint16_t *nbr3 = nullptr, *nbr5 = nullptr;
-  if (in->policy == SBDT_POLICY_GRID) {
+  if (tiled) {
     SBDT_WS(n3, std::uint16_t, "border.nbr3", owner_len);
     SBDT_WS(n5, std::uint16_t, "border.nbr5", owner_len);
     nbr3 = n3;
@@ -1342,6 +1572,21 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   a.inf_queue = infq;
   a.inf_count = infc;
   a.status = ctx->d_status;
+  a.exact = exact_policy ? 1 : 0;
+  a.cell_start = cell_start;
+  a.cell_pts = cell_pts;
+  a.esc = nullptr;
+  a.esc_count = nullptr;
+  a.esc_cap = 0;
+  if (exact_policy) {
+    const unsigned long long want = 2ull * in->S + 2ull * in->n + (1ull << 20);
+    a.esc_cap = static_cast<unsigned>(want < 0x7FFFFFFFull ? want : 0x7FFFFFFFull);
+    SBDT_WS(esc, std::uint32_t, "border.esc", 2ull * a.esc_cap);
+    SBDT_WS(escn, unsigned, "border.esc_n", 1);
+    SBDT_CUDA_TRY(cudaMemsetAsync(escn, 0, sizeof(unsigned), st));
+    a.esc = esc;
+    a.esc_count = escn;
+  }
   a.counters = nullptr;
   if (ctx->census) {
     SBDT_WS(cnt, unsigned long long, "border.counters", 12);
@@ -1364,9 +1609,15 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
         int per_sm = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_prefilter<D>, kBThreads, offs_sh);
         const std::uint64_t resA = std::uint64_t(sms) * std::uint64_t(per_sm > 0 ? per_sm : 1);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_exact<D>, kExactWarps * 32, offs_sh);
+        if (exact_policy)
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_exact<D, true>, kExactWarps * 32, offs_sh);
+        else
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_exact<D, false>, kExactWarps * 32, offs_sh);
         const unsigned resX = static_cast<unsigned>(sms * (per_sm > 0 ? per_sm : 1));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_wide<D>, kWideWarps * 32, offs_sh);
+        if (exact_policy)
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_wide<D, true>, kWideWarps * 32, offs_sh);
+        else
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_wide<D, false>, kWideWarps * 32, offs_sh);
         const unsigned resW = static_cast<unsigned>(sms * (per_sm > 0 ? per_sm : 1));
         auto prefilter = [&](std::uint64_t r0, std::uint64_t r1) {
           const std::uint64_t want = (r1 - r0 + kBThreads - 1) / kBThreads;
@@ -1374,9 +1625,19 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
               a, og, cq, qcap, cn, r0, r1);
         };
         auto exact = [&]() {
-          k_border_exact<D><<<resX, kExactWarps * 32, offs_sh, st>>>(a, og, cq, qcap, cn, cn + 1, wq, cn + 2, cn + 4);
+          if (exact_policy)
+            k_border_exact<D, true><<<resX, kExactWarps * 32, offs_sh, st>>>(a, og, cq, qcap, cn, cn + 1, wq, cn + 2,
+                                                                            cn + 4);
+          else
+            k_border_exact<D, false><<<resX, kExactWarps * 32, offs_sh, st>>>(a, og, cq, qcap, cn, cn + 1, wq, cn + 2,
+                                                                             cn + 4);
         };
-        auto wide = [&]() { k_border_wide<D><<<resW, kWideWarps * 32, offs_sh, st>>>(a, og, wq, wcap, cn + 2, cn + 3, cn + 5); };
+        auto wide = [&]() {
+          if (exact_policy)
+            k_border_wide<D, true><<<resW, kWideWarps * 32, offs_sh, st>>>(a, og, wq, wcap, cn + 2, cn + 3, cn + 5);
+          else
+            k_border_wide<D, false><<<resW, kWideWarps * 32, offs_sh, st>>>(a, og, wq, wcap, cn + 2, cn + 3, cn + 5);
+        };
         if (ctx->chunks.empty()) {
           {
             StageTimer ta(ctx, "border.prefilter");
@@ -1419,7 +1680,21 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
     for (const auto& c : ctx->chunks) SBDT_CUDA_TRY(cudaStreamWaitEvent(st, c.second, 0));
     {
       StageTimer t(ctx, "border.infinite");
-      k_border_infinite<D><<<sms * 4, kWideWarps * 32, offs_sh, st>>>(a, og);
+      if (exact_policy) k_border_infinite<D, true><<<sms * 4, kWideWarps * 32, offs_sh, st>>>(a, og);
+      else k_border_infinite<D, false><<<sms * 4, kWideWarps * 32, offs_sh, st>>>(a, og);
+    }
+    if (exact_policy) {
+      StageTimer t(ctx, "border.escalate");
+      constexpr std::size_t per = D == 3 ? sbdt_pred::kInSphere3Scratch : sbdt_pred::kInSphere2Scratch;
+      SBDT_WS(scr, double, "border.esc_scratch", per * kEscThreads);
+      k_border_escalate<D><<<kEscThreads / 128, 128, 0, st>>>(a, scr);
+      ctx->launches += 1;
+    }
+    if (tiled && in->d_spheres) {
+      const std::uint64_t want = (in->S + 255) / 256;
+      k_border_spheres<D><<<static_cast<unsigned>(want < std::uint64_t(sms) * 16 ? want : std::uint64_t(sms) * 16),
+                            256, 0, st>>>(a);
+      ctx->launches += 1;
     }
     ctx->launches += (tiled && in->S > 0) ? 1 : 2;
   }

@@ -285,8 +285,8 @@ int sbdt_gpu_find_border_dev(sbdt_gpu_ctx* ctx, const sbdt_border_args* a) {
   if (!ctx || !a) return SBDT_ERR_INVALID;
   if (a->dim != 2 && a->dim != 3) return fail(ctx, SBDT_ERR_INVALID, "dim must be 2 or 3");
   if (a->k == 0 || a->k >= 0xFFFE) return fail(ctx, SBDT_ERR_INVALID, "need 1 <= k < 65534");
-  if (a->policy != SBDT_POLICY_BBOX && a->policy != SBDT_POLICY_GRID)
-    return fail(ctx, SBDT_ERR_INVALID, "policy not supported by this build (bbox, grid)");
+  if (a->policy != SBDT_POLICY_BBOX && a->policy != SBDT_POLICY_GRID && a->policy != SBDT_POLICY_EXACT)
+    return fail(ctx, SBDT_ERR_INVALID, "unknown intersection policy");
   if (!a->d_positive || !a->d_vertex_flags || !a->d_vertex_ids || !a->d_vertex_count)
     return fail(ctx, SBDT_ERR_INVALID, "missing output buffers");
   if (a->S > 0xFFFFFFFFull) return fail(ctx, SBDT_ERR_INVALID, "S exceeds the 32-bit SimplexId range");

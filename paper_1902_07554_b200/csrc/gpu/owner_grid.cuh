@@ -457,8 +457,9 @@ __device__ __forceinline__ unsigned long long og_child_mask(const OwnerGrid<D>& 
 }
 
 // Depth-first descent. Start blocks: the blocks of level L0 covering the leaf
-// range [a, b] (at most two per axis). test(blo, bhi) returns 0 reject,
-// 1 descend, 2 accept (every sub-box passes). A passing leaf is a hit.
+// range [a, b] (at most two per axis). test(blo, bhi, level, block) returns
+// 0 reject, 1 descend, 2 accept (every sub-box passes). A passing leaf is a
+// hit.
 template <int D, class Test>
 __device__ bool og_descend(const OwnerGrid<D>& og, const std::uint16_t* __restrict__ owner, std::uint32_t self, int L0,
                            const int* a, const int* b, const Test& test, unsigned long long* stats = nullptr) {
@@ -501,7 +502,7 @@ __device__ bool og_descend(const OwnerGrid<D>& og, const std::uint16_t* __restri
     double blo[D], bhi[D];
     og_block_box<D>(og, L0, cc, blo, bhi);
     ++n_tests;
-    const int r = test(blo, bhi);
+    const int r = test(blo, bhi, L0, cc);
     if (r == 0) continue;
     if (L0 == 0 || r == 2) return true;
     // explore this start block
@@ -532,7 +533,7 @@ __device__ bool og_descend(const OwnerGrid<D>& og, const std::uint16_t* __restri
       double blo[D], bhi[D];
       og_block_box<D>(og, lv, ch, blo, bhi);
       ++n_tests;
-      const int r2 = test(blo, bhi);
+      const int r2 = test(blo, bhi, lv, ch);
       if (r2 == 0) continue;
       if (lv == 0 || r2 == 2) return true;
       const int cl = lv - 1, csh = cl * og.shift;
@@ -586,7 +587,7 @@ __device__ __forceinline__ bool og_sphere_hits_foreign(const OwnerGrid<D>& og, c
     for (int d = 0; d < D; ++d) ok = ok && ((b[d] >> (L * og.shift)) - (a[d] >> (L * og.shift)) <= 1);
     if (ok) break;
   }
-  return og_descend<D>(og, owner, self, L, a, b, [&](const double* blo, const double* bhi) {
+  return og_descend<D>(og, owner, self, L, a, b, [&](const double* blo, const double* bhi, int, const int*) {
     if (!box_sphere<D>(blo, bhi, c, r2)) return 0;
     return box_inside_sphere<D>(blo, bhi, c, r2) ? 2 : 1;
   }, stats);
@@ -618,11 +619,86 @@ __device__ bool og_halfspace_hits_foreign(const OwnerGrid<D>& og, const std::uin
   int a[D], b[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) a[d] = 0, b[d] = og.ldims[0][d] - 1;
-  return og_descend<D>(og, owner, self, og.levels - 1, a, b, [&](const double* blo, const double* bhi) {
+  return og_descend<D>(og, owner, self, og.levels - 1, a, b, [&](const double* blo, const double* bhi, int, const int*) {
     const int out = corners_outside<D>(facet, inner_sign, blo, bhi);
     if (out == 0) return 0;
     return out == (1 << D) ? 2 : 1;
   });
+}
+
+// ---- exact policy: the points of the candidate cells ------
+// Per-cell point lists over the level-0 tiled index (built by k_cell_count /
+// k_cell_scatter): start[idx] .. start[idx+1] in pts.
+template <int D>
+struct CellPt {
+  double x[D];
+  std::uint32_t label;
+  std::uint32_t pid;
+};
+
+template <int D>
+struct CellPoints {
+  const std::uint32_t* start;
+  const CellPt<D>* pts;
+};
+
+// Serial exact-policy descents (fallbacks of the warp-cooperative ones): a
+// leaf passes only if leaf(cell) finds a qualifying point; no block is
+// accepted wholesale for spheres (the points must be strictly inside the
+// exact circumsphere, not the inflated one), whereas a block entirely in the
+// open outer halfspace of a hull facet holds only strictly-outside points.
+template <int D, class Leaf>
+__device__ bool og_sphere_exact_serial(const OwnerGrid<D>& og, const std::uint16_t* __restrict__ owner, const double* c,
+                                       double r2, std::uint32_t self, const Leaf& leaf) {
+  if (isnan(r2)) return false;
+  bool fin = isfinite(r2);
+#pragma unroll
+  for (int d = 0; d < D; ++d) fin = fin && isfinite(c[d]);
+  int a[D], b[D];
+  if (fin) {
+    const double r = sqrt(r2) * (1.0 + 1e-9) + og.margin;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const double fa = floor((c[d] - r - og.g.lo[d]) * og.inv_edge);
+      const double fb = floor((c[d] + r - og.g.lo[d]) * og.inv_edge);
+      const double top = static_cast<double>(og.ldims[0][d] - 1);
+      if (fb < 0.0 || fa > top) return false;
+      a[d] = fa < 0.0 ? 0 : static_cast<int>(fa);
+      b[d] = fb > top ? og.ldims[0][d] - 1 : static_cast<int>(fb);
+    }
+  } else {
+#pragma unroll
+    for (int d = 0; d < D; ++d) a[d] = 0, b[d] = og.ldims[0][d] - 1;
+  }
+  int L = 0;
+  for (; L < og.levels - 1; ++L) {
+    bool ok = true;
+#pragma unroll
+    for (int d = 0; d < D; ++d) ok = ok && ((b[d] >> (L * og.shift)) - (a[d] >> (L * og.shift)) <= 1);
+    if (ok) break;
+  }
+  return og_descend<D>(og, owner, self, L, a, b, [&](const double* blo, const double* bhi, int lv, const int* cell) {
+    if (!box_sphere<D>(blo, bhi, c, r2)) return 0;
+    if (lv > 0) return 1;
+    return leaf(cell) ? 2 : 0;
+  });
+}
+
+template <int D, class Leaf>
+__device__ bool og_halfspace_exact_serial(const OwnerGrid<D>& og, const std::uint16_t* __restrict__ owner,
+                                          const double* const* facet, int inner_sign, std::uint32_t self,
+                                          const Leaf& leaf) {
+  int a[D], b[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) a[d] = 0, b[d] = og.ldims[0][d] - 1;
+  return og_descend<D>(og, owner, self, og.levels - 1, a, b,
+                       [&](const double* blo, const double* bhi, int lv, const int* cell) {
+                         const int out = corners_outside<D>(facet, inner_sign, blo, bhi);
+                         if (out == 0) return 0;
+                         if (out == (1 << D)) return 2;
+                         if (lv > 0) return 1;
+                         return leaf(cell) ? 2 : 0;
+                       });
 }
 
 }  // namespace sbdt_gpu

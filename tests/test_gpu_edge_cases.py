@@ -12,7 +12,7 @@ from paper_1902_07554_b200 import gpu, host
 pytestmark = pytest.mark.gpu
 
 
-def _check(points, sample_ids, sample_labels, k, ctx, seed=7, policies=("grid", "bbox")):
+def _check(points, sample_ids, sample_labels, k, ctx, seed=7, policies=("grid", "bbox", "exact")):
     part = gpu.assign_points(points, sample_ids, sample_labels, k, ctx=ctx)
     ref = oracle.assign_brute(points, sample_ids, sample_labels)
     assert np.array_equal(part.labels, ref)
@@ -81,7 +81,7 @@ def test_part_without_points(ctx):
     assert part.parts_offsets[4] == part.parts_offsets[5] == len(ref)
     p4 = host.build_partials(inst.points, ref, 4, 7)
     p5 = host.Partials(np.append(p4.offsets, p4.offsets[-1]).astype(np.uint64), p4.verts, p4.nbrs, p4.parity)
-    for policy in ("grid", "bbox"):
+    for policy in ("grid", "bbox", "exact"):
         g = gpu.find_border(inst.points, ref, p5, gpu.IntersectionPolicy(policy, 1.0), hull_bfs=True, ctx=ctx)
         g4 = gpu.find_border(inst.points, ref, p4, gpu.IntersectionPolicy(policy, 1.0), hull_bfs=True, ctx=ctx)
         o = oracle.find_border(inst.points, ref, p4, policy)
@@ -96,7 +96,7 @@ def test_far_from_origin(shift, ctx):
     every margin are relative to large |x|."""
     inst = host.make_instance(2, n=40_000, k=8)
     pts = np.ascontiguousarray(inst.points + shift)
-    _check(pts, inst.sample_ids, inst.sample_labels, 8, ctx, policies=("grid",))
+    _check(pts, inst.sample_ids, inst.sample_labels, 8, ctx, policies=("grid", "exact"))
 
 
 def test_jittered_lattice_near_degenerate(ctx):

@@ -40,7 +40,7 @@ def test_assign_points_bit_exact(cfg, ctx):
 
 
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
-@pytest.mark.parametrize("policy", ["grid", "bbox"])
+@pytest.mark.parametrize("policy", ["grid", "bbox", "exact"])
 def test_find_border_bit_exact(cfg, policy, ctx):
     inst = instance(cfg)
     g = gpu.find_border(inst.points, inst.labels, inst.partials, gpu.IntersectionPolicy(policy, 1.0), hull_bfs=True,

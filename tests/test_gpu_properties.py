@@ -57,8 +57,14 @@ def test_policy_chain_and_subsets(ctx):
     part = host.attach_partials(inst, lab)
     grid = gpu.find_border(inst.points, lab, part, gpu.IntersectionPolicy("grid"), ctx=ctx)
     bbox = gpu.find_border(inst.points, lab, part, gpu.IntersectionPolicy("bbox"), ctx=ctx)
+    exact = gpu.find_border(inst.points, lab, part, gpu.IntersectionPolicy("exact"), ctx=ctx)
     assert set(grid.border_vertex_ids.tolist()) <= set(bbox.border_vertex_ids.tolist())
     assert np.all(grid.positive <= bbox.positive)
+    # exact <= grid <= bbox
+    assert np.all(exact.positive <= grid.positive)
+    assert set(exact.border_vertex_ids.tolist()) <= set(grid.border_vertex_ids.tolist())
+    o = oracle.find_border(inst.points, lab, part, "exact")
+    assert np.array_equal(exact.positive, o["positive"]) and np.array_equal(exact.border, o["border"])
     assert np.all(grid.border <= grid.positive)  # BFS subset of the full scan
     assert set(grid.border_vertex_ids.tolist()) <= set(grid.positive_vertex_ids.tolist())
     again = gpu.find_border(inst.points, lab, part, gpu.IntersectionPolicy("grid"), ctx=ctx)
