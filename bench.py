@@ -321,10 +321,20 @@ def main():
     b_assign, b_border = algorithmic_bytes(dim, n, S, cells, n_vb)
     peak, peak_kind = peaks()
 
-    def roof(bytes_, ms_):
+    # DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) from
+    # the committed ncu --set full capture of the same command (config 2)
+    traffic_by_stage = {}
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath) and args.config == 2 and args.n is None and args.policy == "grid":
+        with open(tpath) as f:
+            traffic_by_stage = json.load(f).get("stages", {})
+
+    def roof(bytes_, ms_, stage=None):
         a = bytes_ / (ms_ * 1e-3) / 1e9
+        t = traffic_by_stage.get(stage)
         return {"bound": "hbm", "achieved": round(a, 1), "peak": peak, "unit": "GB/s", "frac": round(a / peak, 4),
-                "traffic": None, "algorithmic_bytes": int(bytes_), "ms": round(ms_, 4), "peak_kind": peak_kind}
+                "traffic": int(t) if t else None, "algorithmic_bytes": int(bytes_), "ms": round(ms_, 4),
+                "peak_kind": peak_kind}
 
     t_assign = sum(v for kk, v in stages.items() if kk.startswith("assign."))
     t_border = sum(v for kk, v in stages.items() if kk.startswith("border."))
@@ -341,7 +351,7 @@ def main():
         "border.compact": n + n_vb * 4,
     }
     dominant = max(stages.items(), key=lambda kv: kv[1])[0]
-    per_kernel = {kk: roof(kernel_bytes[kk], v) for kk, v in stages.items() if kk in kernel_bytes}
+    per_kernel = {kk: roof(kernel_bytes[kk], v, kk) for kk, v in stages.items() if kk in kernel_bytes}
     roofline = per_kernel.get(dominant) or roof(b_border, t_border)
     roofline = dict(roofline, kernel=dominant)
 

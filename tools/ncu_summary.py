@@ -2,6 +2,8 @@
 
   python tools/ncu_summary.py launches <launch-list.csv>      per-kernel time shares
   python tools/ncu_summary.py full <report.ncu-rep> [...]      key --set full metrics
+  python tools/ncu_summary.py traffic <report.ncu-rep> [...]   DRAM bytes per launch -> JSON
+                                                               (profiles/ncu_traffic.json, read by bench.py)
 
 The launch list comes from
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file F \
@@ -77,8 +79,46 @@ def full(paths):
             print("\nwarp-stall samples: " + ", ".join(f"{k} {100 * x / tot:.1f}%" for k, x in st[:6]) + "\n")
 
 
+# bench.py stage -> kernels whose DRAM traffic makes up the stage
+STAGE_KERNELS = {
+    "border.prefilter": ["k_border_prefilter"],
+    "border.exact": ["k_border_exact"],
+    "border.exact_wide": ["k_border_wide"],
+    "border.infinite": ["k_border_infinite"],
+    "border.grid": ["k_owner_mark", "k_nbr_tiles"],
+    "assign.table": ["k_vlt_build"],
+    "assign.points": ["k_assign_vlt", "k_assign_overflow"],
+}
+
+
+def traffic(paths):
+    import json
+    per = {}
+    for path in paths:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rd = csv.reader(io.StringIO(out))
+        hdr = next(rd)
+        units = next(rd)
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+        for vals in rd:
+            d = dict(zip(hdr, vals))
+            u = dict(zip(hdr, units))
+            name = d.get("Kernel Name", "?").split("(")[0].replace("void ", "").split("::")[-1].split("<")[0]
+            b = 0.0
+            for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                b += float(d[k].replace(",", "")) * scale.get(u.get(k, "byte"), 1)
+            per.setdefault(name, []).append(b)
+    res = {"source": [str(p) for p in paths], "kernels": {k: sum(v) / len(v) for k, v in per.items()}, "stages": {}}
+    for st, ks in STAGE_KERNELS.items():
+        if all(k in res["kernels"] for k in ks):
+            res["stages"][st] = sum(res["kernels"][k] for k in ks)
+    print(json.dumps(res, indent=1))
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2])
+    elif sys.argv[1] == "traffic":
+        traffic(sys.argv[2:])
     else:
         full(sys.argv[2:])
