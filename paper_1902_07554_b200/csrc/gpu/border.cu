@@ -335,10 +335,12 @@ __device__ __forceinline__ bool window_clear(const OwnerGrid<D>& og, const std::
   return code == kOwnerEmpty || code == self;
 }
 
+constexpr int kFlatSpan = 7;  // widest per-axis cell range of the flattened exact scan
+
 // Leaf-cell range of the (inflated binary64) sphere, as og_sphere_hits_foreign
-// computes it: 0 = no cell reachable (negative), 1 = spans <= 5 (flattened
-// cell scan), 2 = spans <= 16, 3 = wider or non-finite (2 and 3: pyramid
-// descent in k_border_wide).
+// computes it: 0 = no cell reachable (negative), 1 = spans <= kFlatSpan
+// (flattened cell scan), 2 = spans <= 16, 3 = wider or non-finite (2 and 3:
+// pyramid descent in k_border_wide).
 template <int D>
 __device__ __forceinline__ int leaf_range(const OwnerGrid<D>& og, const double* c, double r2, int* lo, int* span) {
   if (isnan(r2)) return 0;
@@ -357,7 +359,7 @@ __device__ __forceinline__ int leaf_range(const OwnerGrid<D>& og, const double* 
     lo[d] = fa < 0.0 ? 0 : static_cast<int>(fa);
     const int hi = fb > top ? og.ldims[0][d] - 1 : static_cast<int>(fb);
     span[d] = hi - lo[d] + 1;
-    if (span[d] > 5) mode = max(mode, 2);
+    if (span[d] > kFlatSpan) mode = max(mode, 2);
     if (span[d] > 16) mode = 3;
   }
   if (mode == 2 && og.levels < 3) mode = 3;
@@ -734,17 +736,25 @@ __device__ __forceinline__ void rewind_cursor(unsigned* next, unsigned* fin, uns
 }
 
 // per-lane candidate record for the flattened scan (shared memory, per warp)
+// Term of axis d's cell coordinate in the level-0 tiled index (og_index is
+// the sum over the axes plus loff[0]).
+template <int D>
+__device__ __forceinline__ unsigned long long cell_off(int cell, int d, const unsigned long long* bst, bool multi) {
+  constexpr int SH = og_shift<D>();
+  constexpr int F = og_fan<D>();
+  return multi ? (static_cast<unsigned long long>(cell >> SH) * bst[d]) * 64ull +
+                     (static_cast<unsigned long long>(cell & (F - 1)) << (SH * d))
+               : 0ull;
+}
+
 template <int D>
 struct CandSlot {
-  // per axis and cell of the range: the cell's term of the level-0 tiled
-  // index and its squared gap to the centre, so a cell's index is a sum and
-  // box_sphere's d2 is ((g0^2 + g1^2) + g2^2) exactly as box_sphere forms it
-  struct Ent {
-    unsigned long long off;
-    double g2;
-  };
-  Ent ent[D][5];
+  // per axis and cell of the range: the squared gap to the centre, so
+  // box_sphere's d2 is ((g0^2 + g1^2) + g2^2) exactly as box_sphere forms it;
+  // the cell's term of the level-0 tiled index is recomputed from lo
+  double g2[D][kFlatSpan];
   double r2;
+  int lo[D];
   unsigned span[D];
   unsigned inv[D];  // ceil(2^16 / span)
   unsigned self;
@@ -833,24 +843,18 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
     // with independent owner-code loads.
     unsigned cnt = 0;
     if (mode == 1) {
-      constexpr int SH = og_shift<D>();
-      constexpr int F = og_fan<D>();
 #pragma unroll
       for (int d = 0; d < D; ++d) {
         for (int i = 0; i < span[d]; ++i) {
           const int cell = lo[d] + i;
-          const unsigned long long off =
-              multi_level ? (static_cast<unsigned long long>(cell >> SH) * bst[d]) * 64ull +
-                                (static_cast<unsigned long long>(cell & (F - 1)) << (SH * d))
-                          : 0ull;
           const long long last1 = (static_cast<long long>(cell) + 1) > og.g.dims[d] ? og.g.dims[d] : cell + 1;
           const double blo = cell_lo<D>(og.g, cell, d), bhi = cell_lo<D>(og.g, last1, d);
           double g = 0.0;
           if (c[d] < blo) g = blo - c[d];
           else if (c[d] > bhi) g = c[d] - bhi;
-          sl[lane].ent[d][i].off = off;
-          sl[lane].ent[d][i].g2 = g * g;
+          sl[lane].g2[d][i] = g * g;
         }
+        sl[lane].lo[d] = lo[d];
         sl[lane].span[d] = static_cast<unsigned>(span[d]);
         sl[lane].inv[d] = (65536u + static_cast<unsigned>(span[d]) - 1u) / static_cast<unsigned>(span[d]);
       }
@@ -893,32 +897,35 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
         if constexpr (D == 3) {
           const unsigned i2 = (rem * r.inv[1]) >> 16;  // rem / span1 (rem * span1 < 2^16)
           const unsigned i1 = rem - i2 * r.span[1];
-          base += r.ent[1][i1].off + r.ent[2][i2].off;
-          g12 = r.ent[1][i1].g2;
-          g2z = r.ent[2][i2].g2;
+          base += cell_off<D>(r.lo[1] + static_cast<int>(i1), 1, bst, multi_level) +
+                  cell_off<D>(r.lo[2] + static_cast<int>(i2), 2, bst, multi_level);
+          g12 = r.g2[1][i1];
+          g2z = r.g2[2][i2];
         } else {
-          base += r.ent[1][rem].off;
-          g12 = r.ent[1][rem].g2;
+          base += cell_off<D>(r.lo[1] + static_cast<int>(rem), 1, bst, multi_level);
+          g12 = r.g2[1][rem];
         }
         const double rr = r.r2;
-        std::uint16_t code[5];
-        bool geo[5];
+        std::uint16_t code[kFlatSpan];
+        bool geo[kFlatSpan];
+        unsigned long long cidx[kFlatSpan];
 #pragma unroll
-        for (int i0 = 0; i0 < 5; ++i0) {
+        for (int i0 = 0; i0 < kFlatSpan; ++i0) {
           geo[i0] = false;
           code[i0] = kOwnerEmpty;
+          cidx[i0] = 0;
           if (i0 < static_cast<int>(r.span[0])) {
-            const typename CandSlot<D>::Ent& e = r.ent[0][i0];
-            double d2 = e.g2 + g12;
+            double d2 = r.g2[0][i0] + g12;
             if constexpr (D == 3) d2 += g2z;
             geo[i0] = d2 <= rr;
-            if (geo[i0]) code[i0] = __ldg(a.owner + base + e.off);
+            cidx[i0] = base + cell_off<D>(r.lo[0] + i0, 0, bst, multi_level);
+            if (geo[i0]) code[i0] = __ldg(a.owner + cidx[i0]);
           }
         }
         const std::uint32_t sf = r.self;
         if constexpr (!Ex) {
 #pragma unroll
-          for (int i0 = 0; i0 < 5; ++i0) h = h || (geo[i0] && code[i0] != kOwnerEmpty && code[i0] != sf);
+          for (int i0 = 0; i0 < kFlatSpan; ++i0) h = h || (geo[i0] && code[i0] != kOwnerEmpty && code[i0] != sf);
         } else {
           // exact policy: the points of the foreign overlapping cells
           bool loaded = false;
@@ -934,7 +941,7 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
               par = a.parity[r.row];
               loaded = true;
             }
-            h = cell_points_inside<D>(a, base + r.ent[0][i0].off, pv, par, sf, r.row);
+            h = cell_points_inside<D>(a, cidx[i0], pv, par, sf, r.row);
           }
         }
       }
