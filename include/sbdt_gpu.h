@@ -51,7 +51,12 @@ enum sbdt_policy { SBDT_POLICY_BBOX = 0, SBDT_POLICY_GRID = 1, SBDT_POLICY_EXACT
 
 /* find_border flags */
 enum sbdt_border_flags {
-  SBDT_BORDER_HULL_BFS = 1u /* also compute the SPEC find_border BFS subset (border_out) */
+  SBDT_BORDER_HULL_BFS = 1u, /* also compute the SPEC find_border BFS subset (border_out) */
+  /* host-buffer call only: coords and labels are the buffers of the last
+   * sbdt_gpu_assign_points call on this context (coords as passed, labels as
+   * written to labels_out) and are unchanged since; their device copies are
+   * reused instead of uploaded again (checked: same pointers, n and dim). */
+  SBDT_BORDER_RESIDENT_POINTS = 2u
 };
 
 int sbdt_gpu_create(int device, sbdt_gpu_ctx** out);

@@ -230,6 +230,7 @@ int sbdt_gpu_assign_points(sbdt_gpu_ctx* ctx, int dim, const double* coords, uin
                            uint32_t* labels_out, uint64_t* part_offsets_out, uint32_t* part_ids_out,
                            double* bbox_out) {
   if (!ctx || !coords || !sample_ids || !sample_labels || !labels_out) return SBDT_ERR_INVALID;
+  ctx->res_coords = ctx->res_labels = nullptr;  // re-established on success
   cudaStream_t st = ctx->stream;
   double* d_xyz;
   uint32_t *d_sid, *d_slab, *d_lab, *d_pids = nullptr;
@@ -278,6 +279,11 @@ int sbdt_gpu_assign_points(sbdt_gpu_ctx* ctx, int dim, const double* coords, uin
   TRY(finish(ctx));
   if (bbox_out)
     for (int i = 0; i < 2 * dim; ++i) bbox_out[i] = ordered_to_dbl(hb[i]);
+  ctx->res_coords = coords;
+  ctx->res_labels = labels_out;
+  ctx->res_n = n;
+  ctx->res_dim = dim;
+  ctx->res_bbox = true;
   return SBDT_OK;
 }
 
@@ -344,8 +350,24 @@ int sbdt_gpu_find_border(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint6
   cudaStream_t cs = ctx->copy_stream;
   // points, labels and part offsets first (the owner grid needs them), then
   // the simplex rows in chunks; everything on the copy stream, in order
-  SBDT_CUDA_TRY(cudaMemcpyAsync(d_xyz, coords, sizeof(double) * n * dim, cudaMemcpyHostToDevice, cs));
-  SBDT_CUDA_TRY(cudaMemcpyAsync(d_lab, labels, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, cs));
+  const bool resident = (flags & SBDT_BORDER_RESIDENT_POINTS) != 0;
+  if (resident) {
+    if (ctx->res_coords != coords || ctx->res_labels != labels || ctx->res_n != n || ctx->res_dim != dim)
+      return fail(ctx, SBDT_ERR_INVALID, "RESIDENT_POINTS: coords/labels are not those of the last assign_points call");
+    if (ctx->res_bbox) {
+      uint64_t* d_bb;
+      TRY(dalloc(ctx, "h.bbox", 6, &d_bb));
+      a.d_bbox_ordered = d_bb;  // written by that assign_points call
+    }
+  } else {
+    SBDT_CUDA_TRY(cudaMemcpyAsync(d_xyz, coords, sizeof(double) * n * dim, cudaMemcpyHostToDevice, cs));
+    SBDT_CUDA_TRY(cudaMemcpyAsync(d_lab, labels, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, cs));
+    ctx->res_coords = coords;
+    ctx->res_labels = labels;
+    ctx->res_n = n;
+    ctx->res_dim = dim;
+    ctx->res_bbox = false;
+  }
   SBDT_CUDA_TRY(cudaMemcpyAsync(d_off, offsets, sizeof(uint64_t) * (k + 1), cudaMemcpyHostToDevice, cs));
   SBDT_CUDA_TRY(cudaEventRecord(ctx->chunk_events[kUploadChunks], cs));
   SBDT_CUDA_TRY(cudaStreamWaitEvent(st, ctx->chunk_events[kUploadChunks], 0));

@@ -45,6 +45,13 @@ struct sbdt_gpu_ctx {
   std::vector<cudaEvent_t> chunk_events;
   std::vector<std::pair<std::uint64_t, cudaEvent_t>> chunks;
   const double* sample_xyz = nullptr;  // compact sample coordinates (host path), else gathered from the points
+  // host buffers whose device copies ("h.xyz", "h.lab", "h.bbox") are current
+  // (SBDT_BORDER_RESIDENT_POINTS)
+  const void* res_coords = nullptr;
+  const void* res_labels = nullptr;
+  std::uint64_t res_n = 0;
+  int res_dim = 0;
+  bool res_bbox = false;
 };
 
 namespace sbdt_gpu {

@@ -21,6 +21,7 @@ _lib = None
 
 SBDT_OK, SBDT_ERR_INVALID, SBDT_ERR_DEGENERATE, SBDT_ERR_CUDA, SBDT_ERR_OOM, SBDT_ERR_RANGE = range(6)
 POLICY = {"bbox": 0, "grid": 1, "exact": 2}
+RESIDENT_POINTS = 2
 HULL_BFS = 1
 
 
@@ -284,11 +285,14 @@ class BorderSet:
 
 def find_border(points: np.ndarray, labels: np.ndarray, partials, policy: IntersectionPolicy | None = None,
                 hull_bfs: bool = True, spheres: bool = False, ctx: Context | None = None,
-                out: BorderSet | None = None) -> BorderSet:
+                out: BorderSet | None = None, resident: bool = False) -> BorderSet:
     """find_border through the host-buffer C ABI entry point.
     `out` (optional): a BorderSet whose positive / border arrays (length S) and
     border_vertex_ids / positive_vertex_ids arrays (length n) are reused as
-    output buffers; the result then holds views into them."""
+    output buffers; the result then holds views into them. resident=True:
+    `points` and `labels` are the arrays of the last assign_points call on
+    `ctx` (labels = its Partitioning.labels), unchanged: their device copies
+    are reused instead of uploaded (SBDT_BORDER_RESIDENT_POINTS)."""
     ctx = ctx or default_context()
     policy = policy or IntersectionPolicy()
     pts = np.ascontiguousarray(points, np.float64)
@@ -304,7 +308,8 @@ def find_border(points: np.ndarray, labels: np.ndarray, partials, policy: Inters
     rc = lib().sbdt_gpu_find_border(
         ctx.handle, dim, _p(pts, C.c_double), n, _p(lab, C.c_uint32), k, _p(partials.offsets, C.c_uint64),
         _p(partials.verts, C.c_uint32), _p(partials.nbrs, C.c_uint32), _p(partials.parity, C.c_int8),
-        POLICY[policy.kind], policy.c_G, HULL_BFS if hull_bfs else 0, _p(pos, C.c_uint8),
+        POLICY[policy.kind], policy.c_G, (HULL_BFS if hull_bfs else 0) | (RESIDENT_POINTS if resident else 0),
+        _p(pos, C.c_uint8),
         _p(bor, C.c_uint8) if hull_bfs else None, _p(vids, C.c_uint32), C.byref(nv),
         _p(bvids, C.c_uint32) if hull_bfs else None, C.byref(nb) if hull_bfs else None,
         _p(sph, C.c_double) if spheres else None)

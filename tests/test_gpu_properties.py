@@ -179,3 +179,18 @@ def test_host_path_equals_device_path(ctx):
     nv = int(d_cnt.item())
     assert np.array_equal(d_vids[:nv].cpu().numpy().view(np.uint32), hb.positive_vertex_ids)
     dctx.close()
+
+
+def test_resident_points_flag(ctx):
+    """SBDT_BORDER_RESIDENT_POINTS: find_border reuses the device copies of the
+    last assign_points call's points and labels; same results, and a call with
+    other buffers is rejected."""
+    inst = host.make_instance(1, n=80_000, k=8)
+    part = gpu.assign_points(inst.points, inst.sample_ids, inst.sample_labels, 8, ctx=ctx)
+    pt = host.attach_partials(inst, part.labels)
+    res = gpu.find_border(inst.points, part.labels, pt, gpu.IntersectionPolicy("grid"), ctx=ctx, resident=True)
+    ref = gpu.find_border(inst.points, part.labels, pt, gpu.IntersectionPolicy("grid"), ctx=ctx)
+    assert np.array_equal(res.positive, ref.positive) and np.array_equal(res.border, ref.border)
+    assert np.array_equal(res.positive_vertex_ids, ref.positive_vertex_ids)
+    with pytest.raises(ValueError):
+        gpu.find_border(inst.points.copy(), part.labels, pt, ctx=ctx, resident=True)
