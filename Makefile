@@ -3,6 +3,9 @@
 #   libsbdt_host.so  : host setup (generators, DT builder, partitioner)        [setup]
 #   oracle/liboracle.so : CPU restatement of the path (tests / cpu baseline)   [checker]
 #   oracle/_ref/*    : reference sources compiled by path (only where /root/reference exists)
+#   $(PKG)/dropin_example : the C++ drop-in headers (include/sbdt/*.hpp) compiled against the
+#                      reference's own headers (only where /root/reference exists; header-only
+#                      use of the reference types, linked against libsbdt_gpu.so)
 PKG      := paper_1902_07554_b200
 CSRC     := $(PKG)/csrc
 NVCC     ?= nvcc
@@ -17,7 +20,15 @@ GPU_HDR  := $(wildcard $(CSRC)/gpu/*.cuh) $(wildcard $(CSRC)/common/*.hpp) inclu
 HOST_SRC := $(CSRC)/host/delaunay.cpp $(CSRC)/host/setup.cpp $(CSRC)/host/host_capi.cpp
 HOST_HDR := $(wildcard $(CSRC)/host/*.hpp) $(CSRC)/common/predicates.hpp
 
-all: $(PKG)/libsbdt_gpu.so $(PKG)/libsbdt_host.so oracle
+REF_INC  := /root/reference/proj/include
+DROPIN   := $(if $(wildcard $(REF_INC)/sbdt/geometry.hpp),$(PKG)/dropin_example,)
+
+all: $(PKG)/libsbdt_gpu.so $(PKG)/libsbdt_host.so oracle $(DROPIN)
+
+$(PKG)/dropin_example: tests/cpp/dropin_example.cpp include/sbdt/border.hpp include/sbdt/sample_partition.hpp \
+                       include/sbdt_gpu.h $(PKG)/libsbdt_gpu.so
+	$(CXX) -O2 -std=c++20 -ffp-contract=off -Iinclude -I$(REF_INC) -o $@ tests/cpp/dropin_example.cpp \
+	    -L$(PKG) -lsbdt_gpu -Wl,-rpath,'$$ORIGIN' -lpthread
 
 $(PKG)/libsbdt_host.so: $(HOST_SRC) $(HOST_HDR)
 	$(CXX) $(CXXFLAGS) -shared -o $@ $(HOST_SRC) -lpthread
@@ -29,7 +40,7 @@ oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -f $(PKG)/*.so $(PKG)/ptxas.log
+	rm -f $(PKG)/*.so $(PKG)/ptxas.log $(PKG)/dropin_example
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean
