@@ -454,9 +454,8 @@ __global__ void __launch_bounds__(256) k_assign_vlt(const double* __restrict__ x
   bbox_flush<D>(blo, bhi, bbox);
 }
 
-// Queued points: long lists are evaluated by the whole warp (lanes take the
-// entries, binary32 distances with the same error bounds as the list path,
-// exact binary64 argmin over the undecided ones); ring-search points run solo.
+// Queued points (long candidate lists and ring searches), one lane per point:
+// the queue holds only these, so the lanes of a warp do the same kind of work.
 template <int D>
 __global__ void __launch_bounds__(128) k_assign_overflow(const double* __restrict__ xyz,
                                                          const SampleGrid<D>* __restrict__ sgp,
@@ -502,104 +501,70 @@ __global__ void __launch_bounds__(128) k_assign_overflow(const double* __restric
       if (inside) head = heads[cell * FC + sub];
       if ((head & 15u) != kHeadLong) labels[i] = nearest_label_ring<D>(x, sg.g, sg.margin, starts, sorted);
     }
-    for (unsigned todo = __ballot_sync(full, has && (head & 15u) == kHeadLong); todo; todo &= todo - 1) {
-      const int l = __ffs(todo) - 1;
-      double xl[D];
+    if (has && (head & 15u) == kHeadLong) {
+      // one lane per point, its whole list: the list path's decision
+      // (binary32 distances with the rigorous bound, exact binary64 argmin
+      // over the undecided entries) in three passes over the entries
+      const VltEntry* ents = lslab + (head >> 4);
+      const int ne = static_cast<int>(ents[0].idx);
+      ++ents;
       float p[D], pp = 0.f;
 #pragma unroll
       for (int d = 0; d < D; ++d) {
-        xl[d] = __shfl_sync(full, x[d], l);
-        p[d] = static_cast<float>(xl[d] - __shfl_sync(full, fcen[d], l));
+        p[d] = static_cast<float>(x[d] - fcen[d]);
         pp += p[d] * p[d];
       }
-      const std::uint32_t hl = __shfl_sync(full, head, l);
-      const VltEntry* ents = lslab + (hl >> 4);
-      const int ne = static_cast<int>(ents[0].idx);
-      ++ents;
-      // binary32 distances and bounds; lane-local minimum, then the warp's
-      float bv = INFINITY;
-      int bj = 0x7fffffff;
-      for (int j = lane; j < ne; j += 32) {
-        const VltEntry e = ents[j];
-        float dd = 0.f;
+      auto dist = [&](const VltEntry& e, float* bnd) {
+        float dd = 0.f, ss = 0.f;
 #pragma unroll
         for (int d = 0; d < D; ++d) {
           const float t = p[d] - e.r[d];
           dd += t * t;
+          ss += e.r[d] * e.r[d];
         }
-        if (dd < bv || (dd == bv && j < bj)) {
+        *bnd = 4e-6f * (pp + ss) + 1e-30f;
+        return dd;
+      };
+      float bv = INFINITY, bb = 0.f;
+      int bj = 0;
+      for (int j = 0; j < ne; ++j) {
+        float bnd;
+        const float dd = dist(ents[j], &bnd);
+        if (dd < bv) {
           bv = dd;
+          bb = bnd;
           bj = j;
         }
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float ov = __shfl_xor_sync(full, bv, o);
-        const int oj = __shfl_xor_sync(full, bj, o);
-        if (ov < bv || (ov == bv && oj < bj)) {
-          bv = ov;
-          bj = oj;
-        }
-      }
-      auto bound = [&](const VltEntry& e) {
-        float ss = 0.f;
-#pragma unroll
-        for (int d = 0; d < D; ++d) ss += e.r[d] * e.r[d];
-        return 4e-6f * (pp + ss) + 1e-30f;
-      };
-      const VltEntry eb = ents[bj];
-      const float lim = bv + bound(eb);
-      bool amb = false;
-      for (int j = lane; j < ne; j += 32) {
+      const float lim = bv + bb;
+      bool decided = true;
+      for (int j = 0; j < ne && decided; ++j) {
         if (j == bj) continue;
-        const VltEntry e = ents[j];
-        float dd = 0.f;
-#pragma unroll
-        for (int d = 0; d < D; ++d) {
-          const float t = p[d] - e.r[d];
-          dd += t * t;
-        }
-        amb = amb || (dd - bound(e) <= lim);
+        float bnd;
+        const float dd = dist(ents[j], &bnd);
+        if (dd - bnd <= lim) decided = false;
       }
       std::uint32_t lab;
-      if (!__any_sync(full, amb)) {
-        lab = __ldg(sorted_labels + eb.idx);
+      if (decided) {
+        lab = __ldg(sorted_labels + ents[bj].idx);
       } else {
-        // exact binary64 argmin (reference squared_distance, lowest pid on
-        // ties) over the candidates whose binary32 interval reaches lim
         double best = INFINITY;
-        std::uint32_t bpid = 0xFFFFFFFFu, blab = 0;
-        for (int j = lane; j < ne; j += 32) {
-          const VltEntry e = ents[j];
-          float dd = 0.f;
-#pragma unroll
-          for (int d = 0; d < D; ++d) {
-            const float t = p[d] - e.r[d];
-            dd += t * t;
-          }
-          if (j != bj && dd - bound(e) > lim) continue;
-          const SampleRec rec = sorted[e.idx];
-          const double d2 = sqdist<D>(xl, rec.x);
+        std::uint32_t bpid = 0xFFFFFFFFu;
+        lab = 0;
+        for (int j = 0; j < ne; ++j) {
+          float bnd;
+          const float dd = dist(ents[j], &bnd);
+          if (j != bj && dd - bnd > lim) continue;
+          const SampleRec rec = sorted[ents[j].idx];
+          const double d2 = sqdist<D>(x, rec.x);
           if (d2 < best || (d2 == best && rec.pid < bpid)) {
             best = d2;
             bpid = rec.pid;
-            blab = rec.label;
+            lab = rec.label;
           }
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ob = __shfl_xor_sync(full, best, o);
-          const std::uint32_t op = __shfl_xor_sync(full, bpid, o);
-          const std::uint32_t ol = __shfl_xor_sync(full, blab, o);
-          if (ob < best || (ob == best && op < bpid)) {
-            best = ob;
-            bpid = op;
-            blab = ol;
-          }
-        }
-        lab = blab;
       }
-      if (static_cast<int>(lane) == l) labels[i] = lab;
+      labels[i] = lab;
     }
   }
 }
