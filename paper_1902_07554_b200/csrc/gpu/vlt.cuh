@@ -198,6 +198,18 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
     }
     __syncwarp();
     const int ncand = s_cnt[warp];
+    // Coarse candidates (a superset of every fine cell's) of one label: every
+    // fine cell is UNIFORM with that label (partition interiors).
+    if (ncand >= 1 && ncand <= kVltCap) {
+      const std::uint32_t lab0 = s_lab[warp][0];
+      bool mixed = false;
+      for (int j = lane; j < ncand; j += 32) mixed = mixed || s_lab[warp][j] != lab0;
+      if (!__any_sync(0xffffffffu, mixed)) {
+        for (int f = lane; f < FC; f += 32) heads[cell * FC + f] = lab0 << 8;
+        if (lane == 0) st_uniform += FC;
+        continue;
+      }
+    }
     // (c) fine cells
     for (int f = 0; f < FC; ++f) {
       int fi[D];
