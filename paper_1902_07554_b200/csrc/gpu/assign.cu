@@ -368,10 +368,14 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
   const unsigned long long fine = cap * fine_per_cell<D>();
   SBDT_WS(heads, std::uint32_t, "assign.heads", fine);
   SBDT_WS(slab, VltEntry, "assign.slab", fine * kSlots);
-  const unsigned long long lcap_ll = fine * 4 + 4096;  // long lists; full -> ring search
+  const unsigned long long lcap_ll = fine * 24 + 4096;  // long lists (dense cells: ~100 per fine cell); full -> ring search
   const unsigned lcap = lcap_ll < (1ull << 28) ? static_cast<unsigned>(lcap_ll) : (1u << 28);
   SBDT_WS(lslab, VltEntry, "assign.lslab", lcap);
   SBDT_WS(lcount, unsigned, "assign.lcount", 1);
+  SBDT_WS(dq, std::uint32_t, "assign.dense_q", cap + 1);
+  SBDT_WS(dqn, unsigned, "assign.dense_n", 1);
+  constexpr unsigned kDenseBlocks = 148 * 2;
+  SBDT_WS(dscr, char, "assign.dense_scratch", vlt_dense_bytes_per_warp<D>() * kDenseBlocks * kVltWarps);
   SBDT_WS(slabels, std::uint32_t, "assign.slabels", m);
   SBDT_WS(stats, unsigned, "assign.stats", 4);
   SBDT_WS(oq, std::uint32_t, "assign.oq", n + 1);
@@ -398,8 +402,13 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
     StageTimer t1(ctx, "assign.table");
     if (ctx->census) SBDT_CUDA_TRY(cudaMemsetAsync(stats, 0, sizeof(unsigned) * 4, st));
     SBDT_CUDA_TRY(cudaMemsetAsync(lcount, 0, sizeof(unsigned), st));
-    k_vlt_build<D><<<sms * 16, 32 * kVltWarps, 0, st>>>(sg, starts, sorted, heads, slab, lslab, lcount, lcap,
-                                                           ctx->census ? stats : nullptr);
+    SBDT_CUDA_TRY(cudaMemsetAsync(dqn, 0, sizeof(unsigned), st));
+    k_vlt_build<D, false><<<sms * 16, 32 * kVltWarps, 0, st>>>(sg, starts, sorted, heads, slab, lslab, lcount, lcap,
+                                                                  ctx->census ? stats : nullptr, dq, dqn, nullptr);
+    // coarse cells with more than kVltCap candidates (clustered samples)
+    k_vlt_build<D, true><<<kDenseBlocks, 32 * kVltWarps, 0, st>>>(sg, starts, sorted, heads, slab, lslab, lcount, lcap,
+                                                                   ctx->census ? stats : nullptr, dq, dqn, dscr);
+    ctx->launches += 1;
     ctx->launches += 1;
   }
   const std::uint64_t want = (n + kBlock - 1) / kBlock;

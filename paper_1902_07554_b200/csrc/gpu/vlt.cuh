@@ -63,30 +63,70 @@ __device__ __forceinline__ bool dominated_f(const float* rs, const float* rt, co
 
 // One warp per grid cell: coarse candidates (radius + dominance against the
 // sample nearest to the cell centre), then per fine cell the nearest coarse
-// candidate as dominator.
+// candidate as dominator. Two instantiations:
+//   DENSE = false: all cells, candidate arrays in shared memory (kVltCap);
+//                  a cell with more coarse candidates is queued (dq) for
+//   DENSE = true : the queued cells, candidate arrays in a global per-warp
+//                  scratch (kVltDenseCap; beyond that: ring search). Sample-
+//                  clustered inputs (BASELINE config 4) have such cells.
+constexpr int kVltDenseCap = 4096;
+constexpr int kVltDenseWarps = 4;
+
 template <int D>
+constexpr std::size_t vlt_dense_bytes_per_warp() {
+  return ((std::size_t(kVltDenseCap) * (8 + 4 * D) + kVltDenseCap / 8) + 255) / 256 * 256;
+}
+
+template <int D>
+struct VltScratch {
+  std::uint32_t* idx;
+  std::uint32_t* lab;
+  float* rel;      // [cap][D], relative to the coarse centre
+  unsigned* kw;    // [cap / 32] keep words
+};
+
+template <int D, bool DENSE>
 __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D>* __restrict__ sgp,
                                                               const std::uint32_t* __restrict__ starts,
                                                               const SampleRec* __restrict__ sorted,
                                                               std::uint32_t* __restrict__ heads,
                                                               VltEntry* __restrict__ slab, VltEntry* __restrict__ lslab,
                                                               unsigned* __restrict__ lcount, unsigned lcap,
-                                                              unsigned* __restrict__ stats) {
+                                                              unsigned* __restrict__ stats,
+                                                              std::uint32_t* __restrict__ dq, unsigned* __restrict__ dqn,
+                                                              void* __restrict__ dense_scratch) {
+  constexpr int CAP = DENSE ? kVltDenseCap : kVltCap;
   __shared__ SampleGrid<D> sg;
-  __shared__ std::uint32_t s_idx[kVltWarps][kVltCap];
-  __shared__ float s_rel[kVltWarps][kVltCap][D];  // relative to the coarse centre
-  __shared__ std::uint32_t s_lab[kVltWarps][kVltCap];
+  __shared__ std::uint32_t s_idx[DENSE ? 1 : kVltWarps][DENSE ? 1 : kVltCap];
+  __shared__ float s_rel[DENSE ? 1 : kVltWarps][DENSE ? 1 : kVltCap][D];
+  __shared__ std::uint32_t s_lab[DENSE ? 1 : kVltWarps][DENSE ? 1 : kVltCap];
+  __shared__ unsigned s_kw[kVltWarps][DENSE ? 1 : kVltCap / 32];
   __shared__ int s_cnt[kVltWarps];
   if (threadIdx.x == 0) sg = *sgp;
   __syncthreads();
   const Grid<D>& g = sg.g;
   const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  VltScratch<D> A;
+  if constexpr (DENSE) {
+    const std::size_t gw = std::size_t(blockIdx.x) * kVltWarps + warp;
+    char* base = static_cast<char*>(dense_scratch) + gw * vlt_dense_bytes_per_warp<D>();
+    A.idx = reinterpret_cast<std::uint32_t*>(base);
+    A.lab = A.idx + CAP;
+    A.rel = reinterpret_cast<float*>(A.lab + CAP);
+    A.kw = reinterpret_cast<unsigned*>(A.rel + std::size_t(CAP) * D);
+  } else {
+    A.idx = s_idx[warp];
+    A.lab = s_lab[warp];
+    A.rel = &s_rel[warp][0][0];
+    A.kw = s_kw[warp];
+  }
   constexpr int F = fine_factor<D>();
   constexpr int FC = fine_per_cell<D>();
   unsigned st_uniform = 0, st_list = 0, st_over = 0, st_long = 0;
-  const long long cells = static_cast<long long>(sg.cells);
-  for (long long cell = static_cast<long long>(blockIdx.x) * kVltWarps + warp; cell < cells;
-       cell += static_cast<long long>(gridDim.x) * kVltWarps) {
+  const long long cells = DENSE ? static_cast<long long>(*dqn) : static_cast<long long>(sg.cells);
+  for (long long item = static_cast<long long>(blockIdx.x) * kVltWarps + warp; item < cells;
+       item += static_cast<long long>(gridDim.x) * kVltWarps) {
+    const long long cell = DENSE ? static_cast<long long>(dq[item]) : item;
     int cc[D];
     {
       long long rem = cell;
@@ -187,23 +227,32 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
           for (int d = 0; d < D; ++d) rs[d] = static_cast<float>(rec.x[d] - c[d]);
           if (s != bi && dominated_f<D>(rs, r0, hw, H)) continue;
           const int slot = atomicAdd(&s_cnt[warp], 1);
-          if (slot < kVltCap) {
-            s_idx[warp][slot] = s;
-            s_lab[warp][slot] = rec.label;
+          if (slot < CAP) {
+            A.idx[slot] = s;
+            A.lab[slot] = rec.label;
 #pragma unroll
-            for (int d = 0; d < D; ++d) s_rel[warp][slot][d] = rs[d];
+            for (int d = 0; d < D; ++d) A.rel[std::size_t(slot) * D + d] = rs[d];
           }
         }
       }
     }
     __syncwarp();
     const int ncand = s_cnt[warp];
+    if (ncand > CAP) {
+      if constexpr (!DENSE) {
+        if (lane == 0) dq[atomicAdd(dqn, 1u)] = static_cast<std::uint32_t>(cell);  // heads by the dense pass
+      } else {
+        for (int f = lane; f < FC; f += 32) heads[cell * FC + f] = kHeadOverflow;
+        if (lane == 0) st_over += FC;
+      }
+      continue;
+    }
     // Coarse candidates (a superset of every fine cell's) of one label: every
     // fine cell is UNIFORM with that label (partition interiors).
-    if (ncand >= 1 && ncand <= kVltCap) {
-      const std::uint32_t lab0 = s_lab[warp][0];
+    if (ncand >= 1) {
+      const std::uint32_t lab0 = A.lab[0];
       bool mixed = false;
-      for (int j = lane; j < ncand; j += 32) mixed = mixed || s_lab[warp][j] != lab0;
+      for (int j = lane; j < ncand; j += 32) mixed = mixed || A.lab[j] != lab0;
       if (!__any_sync(0xffffffffu, mixed)) {
         for (int f = lane; f < FC; f += 32) heads[cell * FC + f] = lab0 << 8;
         if (lane == 0) st_uniform += FC;
@@ -211,6 +260,7 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
       }
     }
     // (c) fine cells
+    const int nw = (ncand + 31) / 32;
     for (int f = 0; f < FC; ++f) {
       int fi[D];
       {
@@ -223,7 +273,7 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
       }
       const long long fid = cell * FC + f;
       std::uint32_t head = kHeadOverflow;
-      if (ncand <= kVltCap) {
+      {
         // fine box centre/half-widths, and the offset of its centre from the coarse centre
         double fc[D];
         float fhw[D], off[D];
@@ -247,7 +297,7 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
           float dd = 0.f;
 #pragma unroll
           for (int d = 0; d < D; ++d) {
-            const float t = s_rel[warp][j][d] - off[d];
+            const float t = A.rel[std::size_t(j) * D + d] - off[d];
             dd += t * t;
           }
           if (dd < bdist || (dd == bdist && j < bj)) {
@@ -266,15 +316,12 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
         }
         float rt[D];
 #pragma unroll
-        for (int d = 0; d < D; ++d) rt[d] = s_rel[warp][bj][d] - off[d];
-        const std::uint32_t lab0 = s_lab[warp][bj];
+        for (int d = 0; d < D; ++d) rt[d] = A.rel[std::size_t(bj) * D + d] - off[d];
+        const std::uint32_t lab0 = A.lab[bj];
         // pass 1: keep flags (one ballot word per 32 coarse candidates)
-        constexpr int kW = kVltCap / 32;
-        unsigned kw[kW];
         int count = 0;
         bool uniform = true;
-#pragma unroll
-        for (int w = 0; w < kW; ++w) {
+        for (int w = 0; w < nw; ++w) {
           const int j = w * 32 + static_cast<int>(lane);
           bool keep = false;
           if (j < ncand) {
@@ -283,14 +330,16 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
             } else {
               float rs[D];
 #pragma unroll
-              for (int d = 0; d < D; ++d) rs[d] = s_rel[warp][j][d] - off[d];
+              for (int d = 0; d < D; ++d) rs[d] = A.rel[std::size_t(j) * D + d] - off[d];
               keep = !dominated_f<D>(rs, rt, fhw, fH);
             }
           }
-          kw[w] = __ballot_sync(0xffffffffu, keep);
-          if (__ballot_sync(0xffffffffu, keep && s_lab[warp][j < ncand ? j : 0] != lab0)) uniform = false;
-          count += __popc(kw[w]);
+          const unsigned word = __ballot_sync(0xffffffffu, keep);
+          if (lane == 0) A.kw[w] = word;
+          if (__ballot_sync(0xffffffffu, keep && A.lab[j < ncand ? j : 0] != lab0)) uniform = false;
+          count += __popc(word);
         }
+        __syncwarp();
         VltEntry* out = nullptr;
         if (uniform) {
           head = lab0 << 8;
@@ -316,12 +365,12 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
         }
         if (out) {
           int before = 0;
-#pragma unroll
-          for (int w = 0; w < kW; ++w) {
+          for (int w = 0; w < nw; ++w) {
+            const unsigned word = A.kw[w];
             const int j = w * 32 + static_cast<int>(lane);
-            if ((kw[w] >> lane) & 1u) {
-              const int pos = before + __popc(kw[w] & ((1u << lane) - 1u));
-              const std::uint32_t si = s_idx[warp][j];
+            if ((word >> lane) & 1u) {
+              const int pos = before + __popc(word & ((1u << lane) - 1u));
+              const std::uint32_t si = A.idx[j];
               VltEntry e;
 #pragma unroll
               for (int d = 0; d < 3; ++d) e.r[d] = 0.f;
@@ -330,9 +379,10 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
               e.idx = si;
               out[pos] = e;
             }
-            before += __popc(kw[w]);
+            before += __popc(word);
           }
         }
+        __syncwarp();
       }
       if (lane == 0) {
         heads[fid] = head;
