@@ -372,6 +372,10 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
   const unsigned lcap = lcap_ll < (1ull << 28) ? static_cast<unsigned>(lcap_ll) : (1u << 28);
   SBDT_WS(lslab, VltEntry, "assign.lslab", lcap);
   SBDT_WS(lcount, unsigned, "assign.lcount", 1);
+  const unsigned long long subcap_ll = fine * 8 + 4096;  // sub-box heads; full -> long lists
+  const unsigned subcap = subcap_ll < (1ull << 28) ? static_cast<unsigned>(subcap_ll) : (1u << 28);
+  SBDT_WS(subheads, std::uint32_t, "assign.subheads", subcap);
+  SBDT_WS(subcount, unsigned, "assign.subcount", 1);
   SBDT_WS(dq, std::uint32_t, "assign.dense_q", cap + 1);
   SBDT_WS(dqn, unsigned, "assign.dense_n", 1);
   constexpr unsigned kDenseBlocks = 148 * 2;
@@ -403,11 +407,14 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
     if (ctx->census) SBDT_CUDA_TRY(cudaMemsetAsync(stats, 0, sizeof(unsigned) * 4, st));
     SBDT_CUDA_TRY(cudaMemsetAsync(lcount, 0, sizeof(unsigned), st));
     SBDT_CUDA_TRY(cudaMemsetAsync(dqn, 0, sizeof(unsigned), st));
+    SBDT_CUDA_TRY(cudaMemsetAsync(subcount, 0, sizeof(unsigned), st));
     k_vlt_build<D, false><<<sms * 16, 32 * kVltWarps, 0, st>>>(sg, starts, sorted, heads, slab, lslab, lcount, lcap,
-                                                                  ctx->census ? stats : nullptr, dq, dqn, nullptr);
+                                                                  ctx->census ? stats : nullptr, dq, dqn, nullptr,
+                                                                  subheads, subcount, subcap);
     // coarse cells with more than kVltCap candidates (clustered samples)
     k_vlt_build<D, true><<<kDenseBlocks, 32 * kVltWarps, 0, st>>>(sg, starts, sorted, heads, slab, lslab, lcount, lcap,
-                                                                   ctx->census ? stats : nullptr, dq, dqn, dscr);
+                                                                   ctx->census ? stats : nullptr, dq, dqn, dscr,
+                                                                   subheads, subcount, subcap);
     ctx->launches += 1;
     ctx->launches += 1;
   }
@@ -417,7 +424,8 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
     StageTimer t2(ctx, "assign.points");
     SBDT_CUDA_TRY(cudaMemsetAsync(oqc, 0, sizeof(unsigned), st));
     if (ctx->chunks.empty()) {
-      k_assign_vlt<D><<<blocks, kBlock, 0, st>>>(d_xyz, 0, n, sg, heads, slab, sorted, slabels, d_labels, d_bbox, oq,
+      k_assign_vlt<D><<<blocks, kBlock, 0, st>>>(d_xyz, 0, n, sg, heads, subheads, slab, lslab, sorted, slabels, d_labels,
+                                                 d_bbox, oq,
                                                  oqc);
     } else {
       // host path: each chunk of points as soon as its upload has landed
@@ -428,7 +436,8 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
         if (i1 > i0) {
           const std::uint64_t w = (i1 - i0 + kBlock - 1) / kBlock;
           const unsigned b = static_cast<unsigned>(w < std::uint64_t(sms) * 16 ? w : std::uint64_t(sms) * 16);
-          k_assign_vlt<D><<<b, kBlock, 0, st>>>(d_xyz, i0, i1, sg, heads, slab, sorted, slabels, d_labels, d_bbox, oq,
+          k_assign_vlt<D><<<b, kBlock, 0, st>>>(d_xyz, i0, i1, sg, heads, subheads, slab, lslab, sorted, slabels,
+                                                d_labels, d_bbox, oq,
                                                 oqc);
           ++ctx->launches;
         }
@@ -436,7 +445,7 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
       }
       --ctx->launches;
     }
-    k_assign_overflow<D><<<sms * 8, 128, 0, st>>>(d_xyz, sg, starts, sorted, slabels, heads, lslab, d_labels, oq,
+    k_assign_overflow<D><<<sms * 8, 128, 0, st>>>(d_xyz, sg, starts, sorted, slabels, heads, subheads, lslab, d_labels, oq,
                                                    oqc);
     ctx->launches += 2;
   }

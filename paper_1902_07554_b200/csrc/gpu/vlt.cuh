@@ -15,11 +15,12 @@
 //
 // Record per fine cell (u32 head): count 0 -> UNIFORM (label << 8), all
 // candidates share one label; 1..kSlots -> candidate list in the cell's slab
-// slot (16-byte entries: binary32 coordinates relative to the fine-cell centre
-// + sample index); kHeadLong -> a longer list in the long slab (header entry
-// holds the count), evaluated warp-cooperatively; kHeadOverflow -> the point
-// is queued for the exact ring search (coarse candidate overflow, or the long
-// slab is full).
+// slot (16-byte entries: binary32 coordinates relative to the cell centre +
+// sample index); SUB (kHeadSubBit) -> the cell is split at its centre into 2^D
+// sub-boxes with their own heads (density-adaptive: a list longer than
+// kSlots is refined up to kVltDepth times; sub-box lists live in the long
+// slab as kHeadPool); kHeadLong -> a long list (header entry holds the
+// count), evaluated by the queue kernel; kHeadOverflow -> exact ring search.
 // Point decision: binary32 distances with a rigorous per-candidate error bound
 // pick the winner when the gap exceeds both bounds; otherwise the tied
 // candidates are compared exactly in binary64 (reference formula + pid).
@@ -27,9 +28,16 @@
 
 namespace sbdt_gpu {
 
-constexpr int kSlots = 12;
-constexpr std::uint32_t kHeadLong = 14u;      // list in the long slab: head = (offset << 4) | kHeadLong
+constexpr int kSlots = 12;                    // head 1..12: list of that length in the cell's slab slot
+// head & 15 == 0: UNIFORM (label << 8) or, with bit 4 set, SUB: 2^D sub-box
+// heads at subheads[head >> 8]
+constexpr std::uint32_t kHeadSubBit = 0x10u;
+constexpr std::uint32_t kHeadPool = 13u;      // short list (<= kSlots) in the long slab: header + entries
+constexpr std::uint32_t kHeadLong = 14u;      // long list in the long slab (header + entries), queued points
 constexpr std::uint32_t kHeadOverflow = 15u;  // exact ring search
+constexpr int kVltDepth = 3;                  // sub-box levels below a fine cell (cell size / 2^3)
+constexpr int kVltSplitMin = 32;              // lists longer than this are refined
+constexpr int kVltLevels = kVltDepth + 2;     // kept-set levels: coarse, fine, sub-boxes
 constexpr int kVltWarps = 4;
 constexpr int kVltCap = 192;
 
@@ -74,7 +82,68 @@ constexpr int kVltDenseWarps = 4;
 
 template <int D>
 constexpr std::size_t vlt_dense_bytes_per_warp() {
-  return ((std::size_t(kVltDenseCap) * (8 + 4 * D) + kVltDenseCap / 8) + 255) / 256 * 256;
+  return ((std::size_t(kVltDenseCap) * (8 + 4 * D) + std::size_t(kVltDenseCap) * 2 * kVltLevels) + 255) / 256 * 256;
+}
+
+// DFS node of the fine-cell refinement: a box and where its head goes.
+template <int D>
+struct VltNode {
+  double lo[D], hi[D];
+  unsigned long long target;  // index into heads (fine cells) or subheads (sub-boxes)
+  int level;                  // 1 = fine cell, 2.. = sub-boxes
+  int sub;                    // target is in subheads
+};
+constexpr int kVltStack = 8 + (1 << 3) * kVltDepth;
+
+// Locates the table record of point x: its fine cell, then the sub-boxes
+// (split at the centre, x >= centre -> upper half, the same binary64
+// expressions as the build). Returns the head; fid = fine cell, centre of
+// the final box in fcen; false if x lies outside the table.
+template <int D>
+__device__ __forceinline__ bool vlt_locate(const double* x, const SampleGrid<D>& sg,
+                                           const std::uint32_t* __restrict__ heads,
+                                           const std::uint32_t* __restrict__ subheads, std::uint32_t* head_out,
+                                           long long* fid_out, double* fcen) {
+  constexpr int F = fine_factor<D>();
+  constexpr int FC = fine_per_cell<D>();
+  bool inside = true;
+  long long cell = 0, mul = 1;
+  int sub = 0, smul = 1;
+  double lo[D], hi[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const double f = floor((x[d] - sg.g.lo[d]) * sg.inv_ef);
+    inside = inside && (f >= 0.0) && (f < static_cast<double>(sg.g.dims[d] * F));
+    const int fi = inside ? static_cast<int>(f) : 0;
+    cell += static_cast<long long>(fi / F) * mul;
+    sub += (fi % F) * smul;
+    mul *= sg.g.dims[d];
+    smul *= F;
+    lo[d] = sg.g.lo[d] + static_cast<double>(fi) * sg.ef;
+    hi[d] = sg.g.lo[d] + static_cast<double>(fi + 1) * sg.ef;
+  }
+  if (!inside) return false;
+  const long long fid = cell * FC + sub;
+  std::uint32_t head = __ldg(heads + fid);
+  while ((head & 0xFFu) == kHeadSubBit) {
+    unsigned idx = 0;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const double mid = 0.5 * (lo[d] + hi[d]);
+      if (x[d] >= mid) {
+        idx |= 1u << d;
+        lo[d] = mid;
+      } else {
+        hi[d] = mid;
+      }
+    }
+    head = __ldg(subheads + (head >> 8) + idx);
+  }
+#pragma unroll
+  for (int d = 0; d < D; ++d) fcen[d] = 0.5 * (lo[d] + hi[d]);
+  *head_out = head;
+  *fid_out = fid;
+  return true;
 }
 
 template <int D>
@@ -82,7 +151,7 @@ struct VltScratch {
   std::uint32_t* idx;
   std::uint32_t* lab;
   float* rel;      // [cap][D], relative to the coarse centre
-  unsigned* kw;    // [cap / 32] keep words
+  std::uint16_t* kl;  // [kVltLevels][cap] kept-set index lists per level (level 0 implicit: 0..ncand-1)
 };
 
 template <int D, bool DENSE>
@@ -94,13 +163,17 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
                                                               unsigned* __restrict__ lcount, unsigned lcap,
                                                               unsigned* __restrict__ stats,
                                                               std::uint32_t* __restrict__ dq, unsigned* __restrict__ dqn,
-                                                              void* __restrict__ dense_scratch) {
+                                                              void* __restrict__ dense_scratch,
+                                                              std::uint32_t* __restrict__ subheads,
+                                                              unsigned* __restrict__ subcount, unsigned subcap) {
   constexpr int CAP = DENSE ? kVltDenseCap : kVltCap;
   __shared__ SampleGrid<D> sg;
   __shared__ std::uint32_t s_idx[DENSE ? 1 : kVltWarps][DENSE ? 1 : kVltCap];
   __shared__ float s_rel[DENSE ? 1 : kVltWarps][DENSE ? 1 : kVltCap][D];
   __shared__ std::uint32_t s_lab[DENSE ? 1 : kVltWarps][DENSE ? 1 : kVltCap];
-  __shared__ unsigned s_kw[kVltWarps][DENSE ? 1 : kVltCap / 32];
+  __shared__ std::uint16_t s_kl[kVltWarps][DENSE ? 1 : kVltLevels * kVltCap];
+  __shared__ int s_kn[kVltWarps][kVltLevels];
+  __shared__ VltNode<D> s_stk[kVltWarps][kVltStack];
   __shared__ int s_cnt[kVltWarps];
   if (threadIdx.x == 0) sg = *sgp;
   __syncthreads();
@@ -113,12 +186,12 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
     A.idx = reinterpret_cast<std::uint32_t*>(base);
     A.lab = A.idx + CAP;
     A.rel = reinterpret_cast<float*>(A.lab + CAP);
-    A.kw = reinterpret_cast<unsigned*>(A.rel + std::size_t(CAP) * D);
+    A.kl = reinterpret_cast<std::uint16_t*>(A.rel + std::size_t(CAP) * D);
   } else {
     A.idx = s_idx[warp];
     A.lab = s_lab[warp];
     A.rel = &s_rel[warp][0][0];
-    A.kw = s_kw[warp];
+    A.kl = s_kl[warp];
   }
   constexpr int F = fine_factor<D>();
   constexpr int FC = fine_per_cell<D>();
@@ -259,99 +332,154 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
         continue;
       }
     }
-    // (c) fine cells
-    const int nw = (ncand + 31) / 32;
-    for (int f = 0; f < FC; ++f) {
-      int fi[D];
-      {
+    // (c) fine cells, refined into 2^D sub-boxes (depth <= kVltDepth) while a
+    //     box's candidate list is longer than kSlots. Kept candidates per
+    //     level as index lists in A.kl (level 0 = all coarse candidates).
+    VltNode<D>* stk = s_stk[warp];
+    int top = 0;
+    if (lane == 0) {
+      for (int f = FC - 1; f >= 0; --f) {
+        int fi[D];
         int rem = f;
 #pragma unroll
         for (int d = 0; d < D; ++d) {
           fi[d] = cc[d] * F + rem % F;
           rem /= F;
         }
-      }
-      const long long fid = cell * FC + f;
-      std::uint32_t head = kHeadOverflow;
-      {
-        // fine box centre/half-widths, and the offset of its centre from the coarse centre
-        double fc[D];
-        float fhw[D], off[D];
-        float fH2 = 0.f;
+        VltNode<D> nd;
 #pragma unroll
         for (int d = 0; d < D; ++d) {
-          const double lo = g.lo[d] + static_cast<double>(fi[d]) * sg.ef;
-          const double hi = g.lo[d] + static_cast<double>(fi[d] + 1) * sg.ef;
-          fc[d] = 0.5 * (lo + hi);
-          fhw[d] = __double2float_ru(0.5 * (hi - lo) + sg.delta_f);
-          fH2 = __fadd_ru(fH2, __fmul_ru(fhw[d], fhw[d]));
-          off[d] = static_cast<float>(fc[d] - c[d]);
+          nd.lo[d] = g.lo[d] + static_cast<double>(fi[d]) * sg.ef;
+          nd.hi[d] = g.lo[d] + static_cast<double>(fi[d] + 1) * sg.ef;
         }
-        const float fH = __fsqrt_ru(fH2);
-        // Relative coordinates w.r.t. the fine centre are recomputed in binary64
-        // for the stored entries; the dominance test uses (coarse-rel - off),
-        // whose extra rounding is covered by the 1e-5 margin.
-        float bdist = INFINITY;
-        int bj = 0x7fffffff;
-        for (int j = lane; j < ncand; j += 32) {
-          float dd = 0.f;
+        nd.target = static_cast<unsigned long long>(cell * FC + f);
+        nd.level = 1;
+        nd.sub = 0;
+        stk[top++] = nd;
+      }
+      s_kn[warp][0] = ncand;
+    }
+    top = __shfl_sync(0xffffffffu, top, 0);
+    __syncwarp();
+    while (top > 0) {
+      const VltNode<D> nd = stk[top - 1];
+      --top;
+      __syncwarp();
+      const int pl = nd.level - 1;
+      const std::uint16_t* plist = A.kl + std::size_t(pl) * CAP;  // unused for level 0 (identity)
+      const int np = s_kn[warp][pl];
+      std::uint16_t* klist = A.kl + std::size_t(nd.level) * CAP;
+      auto cand = [&](int t) -> int { return pl == 0 ? t : static_cast<int>(plist[t]); };
+      // box centre/half-widths, and the offset of its centre from the coarse centre
+      double fc[D];
+      float fhw[D], off[D];
+      float fH2 = 0.f;
 #pragma unroll
-          for (int d = 0; d < D; ++d) {
-            const float t = A.rel[std::size_t(j) * D + d] - off[d];
-            dd += t * t;
-          }
-          if (dd < bdist || (dd == bdist && j < bj)) {
-            bdist = dd;
-            bj = j;
+      for (int d = 0; d < D; ++d) {
+        fc[d] = 0.5 * (nd.lo[d] + nd.hi[d]);
+        fhw[d] = __double2float_ru(0.5 * (nd.hi[d] - nd.lo[d]) + sg.delta_f);
+        fH2 = __fadd_ru(fH2, __fmul_ru(fhw[d], fhw[d]));
+        off[d] = static_cast<float>(fc[d] - c[d]);
+      }
+      const float fH = __fsqrt_ru(fH2);
+      // Relative coordinates w.r.t. the box centre are recomputed in binary64
+      // for the stored entries; the dominance test uses (coarse-rel - off),
+      // whose extra rounding is covered by the 1e-5 margin.
+      float bdist = INFINITY;
+      int bj = 0x7fffffff;
+      for (int t = lane; t < np; t += 32) {
+        const int j = cand(t);
+        float dd = 0.f;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const float u = A.rel[std::size_t(j) * D + d] - off[d];
+          dd += u * u;
+        }
+        if (dd < bdist || (dd == bdist && j < bj)) {
+          bdist = dd;
+          bj = j;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float od = __shfl_xor_sync(0xffffffffu, bdist, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+        if (od < bdist || (od == bdist && oj < bj)) {
+          bdist = od;
+          bj = oj;
+        }
+      }
+      float rt[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) rt[d] = A.rel[std::size_t(bj) * D + d] - off[d];
+      const std::uint32_t lab0 = A.lab[bj];
+      // kept list of this box (dominance against the nearest parent candidate)
+      int count = 0;
+      bool uniform = true;
+      for (int t0 = 0; t0 < np; t0 += 32) {
+        const int t = t0 + static_cast<int>(lane);
+        bool keep = false;
+        int j = 0;
+        if (t < np) {
+          j = cand(t);
+          if (j == bj) {
+            keep = true;
+          } else {
+            float rs[D];
+#pragma unroll
+            for (int d = 0; d < D; ++d) rs[d] = A.rel[std::size_t(j) * D + d] - off[d];
+            keep = !dominated_f<D>(rs, rt, fhw, fH);
           }
         }
+        const unsigned word = __ballot_sync(0xffffffffu, keep);
+        if (keep) klist[count + __popc(word & ((1u << lane) - 1u))] = static_cast<std::uint16_t>(j);
+        if (__ballot_sync(0xffffffffu, keep && A.lab[j] != lab0)) uniform = false;
+        count += __popc(word);
+      }
+      if (lane == 0) s_kn[warp][nd.level] = count;
+      __syncwarp();
+      std::uint32_t head = kHeadOverflow;
+      VltEntry* out = nullptr;
+      bool split = false;
+      if (uniform) {
+        head = lab0 << 8;
+      } else if (count <= kSlots && !nd.sub) {
+        head = static_cast<std::uint32_t>(count);
+        out = slab + nd.target * kSlots;
+      } else {
+        // split long lists while the depth allows and the sub-head pool has
+        // room (moderately long lists stay long: one pass in the queue kernel
+        // is cheaper than 2^D sub-boxes)
+        if (count > kVltSplitMin && nd.level <= kVltDepth) {
+          unsigned so = 0;
+          if (lane == 0) so = atomicAdd(subcount, 1u << D);
+          so = __shfl_sync(0xffffffffu, so, 0);
+          if (static_cast<unsigned long long>(so) + (1u << D) <= subcap && so < (1u << 24)) {
+            head = (so << 8) | kHeadSubBit;
+            split = true;
+            if (lane == 0) {
+              for (int i = (1 << D) - 1; i >= 0; --i) {
+                VltNode<D> ch;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const float od = __shfl_xor_sync(0xffffffffu, bdist, o);
-          const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
-          if (od < bdist || (od == bdist && oj < bj)) {
-            bdist = od;
-            bj = oj;
-          }
-        }
-        float rt[D];
-#pragma unroll
-        for (int d = 0; d < D; ++d) rt[d] = A.rel[std::size_t(bj) * D + d] - off[d];
-        const std::uint32_t lab0 = A.lab[bj];
-        // pass 1: keep flags (one ballot word per 32 coarse candidates)
-        int count = 0;
-        bool uniform = true;
-        for (int w = 0; w < nw; ++w) {
-          const int j = w * 32 + static_cast<int>(lane);
-          bool keep = false;
-          if (j < ncand) {
-            if (j == bj) {
-              keep = true;
-            } else {
-              float rs[D];
-#pragma unroll
-              for (int d = 0; d < D; ++d) rs[d] = A.rel[std::size_t(j) * D + d] - off[d];
-              keep = !dominated_f<D>(rs, rt, fhw, fH);
+                for (int d = 0; d < D; ++d) {
+                  const bool up = (i >> d) & 1;
+                  ch.lo[d] = up ? fc[d] : nd.lo[d];
+                  ch.hi[d] = up ? nd.hi[d] : fc[d];
+                }
+                ch.target = so + static_cast<unsigned>(i);
+                ch.level = nd.level + 1;
+                ch.sub = 1;
+                stk[top + ((1 << D) - 1 - i)] = ch;
+              }
             }
           }
-          const unsigned word = __ballot_sync(0xffffffffu, keep);
-          if (lane == 0) A.kw[w] = word;
-          if (__ballot_sync(0xffffffffu, keep && A.lab[j < ncand ? j : 0] != lab0)) uniform = false;
-          count += __popc(word);
         }
-        __syncwarp();
-        VltEntry* out = nullptr;
-        if (uniform) {
-          head = lab0 << 8;
-        } else if (count <= kSlots) {
-          head = static_cast<std::uint32_t>(count);
-          out = slab + fid * kSlots;
-        } else {
+        if (!split) {
           unsigned o = 0;
           if (lane == 0) o = atomicAdd(lcount, static_cast<unsigned>(count + 1));
           o = __shfl_sync(0xffffffffu, o, 0);
           if (static_cast<unsigned long long>(o) + count + 1 <= lcap && o < (1u << 28)) {
-            head = (o << 4) | kHeadLong;
+            head = (o << 4) | (count <= kSlots ? kHeadPool : kHeadLong);
             if (lane == 0) {
               VltEntry h;
               h.r[0] = h.r[1] = h.r[2] = 0.f;
@@ -359,39 +487,37 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
               lslab[o] = h;
             }
             out = lslab + o + 1;
-          } else {
-            head = kHeadOverflow;
           }
         }
-        if (out) {
-          int before = 0;
-          for (int w = 0; w < nw; ++w) {
-            const unsigned word = A.kw[w];
-            const int j = w * 32 + static_cast<int>(lane);
-            if ((word >> lane) & 1u) {
-              const int pos = before + __popc(word & ((1u << lane) - 1u));
-              const std::uint32_t si = A.idx[j];
-              VltEntry e;
+      }
+      if (out) {
+        for (int t = lane; t < count; t += 32) {
+          const std::uint32_t si = A.idx[klist[t]];
+          VltEntry e;
 #pragma unroll
-              for (int d = 0; d < 3; ++d) e.r[d] = 0.f;
+          for (int d = 0; d < 3; ++d) e.r[d] = 0.f;
 #pragma unroll
-              for (int d = 0; d < D; ++d) e.r[d] = static_cast<float>(sorted[si].x[d] - fc[d]);
-              e.idx = si;
-              out[pos] = e;
-            }
-            before += __popc(word);
-          }
+          for (int d = 0; d < D; ++d) e.r[d] = static_cast<float>(sorted[si].x[d] - fc[d]);
+          e.idx = si;
+          out[t] = e;
         }
-        __syncwarp();
       }
       if (lane == 0) {
-        heads[fid] = head;
+        if (nd.sub) subheads[nd.target] = head;
+        else heads[nd.target] = head;
         const std::uint32_t h = head & 15u;
-        if (h == 0) ++st_uniform;
-        else if (h == kHeadOverflow) ++st_over;
-        else if (h == kHeadLong) ++st_long;
-        else ++st_list;
+        if (h == 0) {
+          if (!(head & kHeadSubBit)) ++st_uniform;
+        } else if (h == kHeadOverflow) {
+          ++st_over;
+        } else if (h == kHeadLong) {
+          ++st_long;
+        } else {
+          ++st_list;
+        }
       }
+      if (split) top += 1 << D;
+      __syncwarp();
     }
   }
   if (stats && lane == 0) {
@@ -429,7 +555,9 @@ __global__ void __launch_bounds__(256) k_assign_vlt(const double* __restrict__ x
                                                     std::uint64_t n,
                                                     const SampleGrid<D>* __restrict__ sgp,
                                                     const std::uint32_t* __restrict__ heads,
+                                                    const std::uint32_t* __restrict__ subheads,
                                                     const VltEntry* __restrict__ slab,
+                                                    const VltEntry* __restrict__ lslab,
                                                     const SampleRec* __restrict__ sorted,
                                                     const std::uint32_t* __restrict__ sorted_labels,
                                                     std::uint32_t* __restrict__ labels, unsigned long long* bbox,
@@ -452,25 +580,11 @@ __global__ void __launch_bounds__(256) k_assign_vlt(const double* __restrict__ x
       blo[d] = fmin(blo[d], x[d]);
       bhi[d] = fmax(bhi[d], x[d]);
     }
-    bool inside = true;
-    long long cell = 0, mul = 1;
-    int sub = 0, smul = 1;
     double fcen[D];
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      const double f = floor((x[d] - sg.g.lo[d]) * sg.inv_ef);
-      inside = inside && (f >= 0.0) && (f < static_cast<double>(sg.g.dims[d] * F));
-      const int fi = inside ? static_cast<int>(f) : 0;
-      cell += static_cast<long long>(fi / F) * mul;
-      sub += (fi % F) * smul;
-      mul *= sg.g.dims[d];
-      smul *= F;
-      fcen[d] = 0.5 * ((sg.g.lo[d] + static_cast<double>(fi) * sg.ef) + (sg.g.lo[d] + static_cast<double>(fi + 1) * sg.ef));
-    }
     std::uint32_t head = kHeadOverflow;
-    const long long fid = cell * FC + sub;
-    if (inside) head = __ldg(heads + fid);
-    const std::uint32_t cnt = head & 15u;
+    long long fid = 0;
+    vlt_locate<D>(x, sg, heads, subheads, &head, &fid, fcen);
+    std::uint32_t cnt = head & 15u;
     if (cnt == 0) {
       __stcs(labels + i, head >> 8);
     } else if (cnt >= kHeadLong) {
@@ -478,6 +592,11 @@ __global__ void __launch_bounds__(256) k_assign_vlt(const double* __restrict__ x
       oq[slot] = static_cast<std::uint32_t>(i);
     } else {
       const VltEntry* ents = slab + fid * kSlots;
+      if (cnt == kHeadPool) {  // sub-box list in the long slab
+        ents = lslab + (head >> 4);
+        cnt = ents[0].idx;
+        ++ents;
+      }
       float p[D], pp = 0.f;
 #pragma unroll
       for (int d = 0; d < D; ++d) {
@@ -525,6 +644,7 @@ __global__ void __launch_bounds__(128) k_assign_overflow(const double* __restric
                                                          const SampleRec* __restrict__ sorted,
                                                          const std::uint32_t* __restrict__ sorted_labels,
                                                          const std::uint32_t* __restrict__ heads,
+                                                         const std::uint32_t* __restrict__ subheads,
                                                          const VltEntry* __restrict__ lslab,
                                                          std::uint32_t* __restrict__ labels,
                                                          const std::uint32_t* __restrict__ oq,
@@ -545,22 +665,10 @@ __global__ void __launch_bounds__(128) k_assign_overflow(const double* __restric
     double x[D], fcen[D];
     if (has) {
       i = oq[q];
-      bool inside = true;
-      long long cell = 0, mul = 1;
-      int sub = 0, smul = 1;
 #pragma unroll
-      for (int d = 0; d < D; ++d) {
-        x[d] = xyz[std::size_t(i) * D + d];
-        const double f = floor((x[d] - sg.g.lo[d]) * sg.inv_ef);
-        inside = inside && (f >= 0.0) && (f < static_cast<double>(sg.g.dims[d] * F));
-        const int fi = inside ? static_cast<int>(f) : 0;
-        cell += static_cast<long long>(fi / F) * mul;
-        sub += (fi % F) * smul;
-        mul *= sg.g.dims[d];
-        smul *= F;
-        fcen[d] = 0.5 * ((sg.g.lo[d] + static_cast<double>(fi) * sg.ef) + (sg.g.lo[d] + static_cast<double>(fi + 1) * sg.ef));
-      }
-      if (inside) head = heads[cell * FC + sub];
+      for (int d = 0; d < D; ++d) x[d] = xyz[std::size_t(i) * D + d];
+      long long fid = 0;
+      vlt_locate<D>(x, sg, heads, subheads, &head, &fid, fcen);
       if ((head & 15u) != kHeadLong) labels[i] = nearest_label_ring<D>(x, sg.g, sg.margin, starts, sorted);
     }
     if (has && (head & 15u) == kHeadLong) {
