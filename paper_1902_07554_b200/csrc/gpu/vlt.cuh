@@ -414,23 +414,24 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
       for (int d = 0; d < D; ++d) rt[d] = A.rel[std::size_t(bj) * D + d] - off[d];
       const std::uint32_t lab0 = A.lab[bj];
       // kept list of this box (dominance against the nearest parent candidate)
-      int count = 0;
+      int count = 0, inbox = 0;  // kept candidates; samples inside the box (~ points to expect)
       bool uniform = true;
       for (int t0 = 0; t0 < np; t0 += 32) {
         const int t = t0 + static_cast<int>(lane);
-        bool keep = false;
+        bool keep = false, ins = false;
         int j = 0;
         if (t < np) {
           j = cand(t);
-          if (j == bj) {
-            keep = true;
-          } else {
-            float rs[D];
+          float rs[D];
+          ins = true;
 #pragma unroll
-            for (int d = 0; d < D; ++d) rs[d] = A.rel[std::size_t(j) * D + d] - off[d];
-            keep = !dominated_f<D>(rs, rt, fhw, fH);
+          for (int d = 0; d < D; ++d) {
+            rs[d] = A.rel[std::size_t(j) * D + d] - off[d];
+            ins = ins && fabsf(rs[d]) <= fhw[d];
           }
+          keep = (j == bj) || !dominated_f<D>(rs, rt, fhw, fH);
         }
+        inbox += __popc(__ballot_sync(0xffffffffu, ins));
         const unsigned word = __ballot_sync(0xffffffffu, keep);
         if (keep) klist[count + __popc(word & ((1u << lane) - 1u))] = static_cast<std::uint16_t>(j);
         if (__ballot_sync(0xffffffffu, keep && A.lab[j] != lab0)) uniform = false;
@@ -450,7 +451,7 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
         // split long lists while the depth allows and the sub-head pool has
         // room (moderately long lists stay long: one pass in the queue kernel
         // is cheaper than 2^D sub-boxes)
-        if (count > kVltSplitMin && nd.level <= kVltDepth) {
+        if ((count > kVltSplitMin || inbox >= 2) && nd.level <= kVltDepth) {
           unsigned so = 0;
           if (lane == 0) so = atomicAdd(subcount, 1u << D);
           so = __shfl_sync(0xffffffffu, so, 0);
