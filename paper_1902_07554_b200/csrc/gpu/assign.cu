@@ -381,7 +381,7 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
   constexpr unsigned kDenseBlocks = 148 * 2;
   SBDT_WS(dscr, char, "assign.dense_scratch", vlt_dense_bytes_per_warp<D>() * kDenseBlocks * kVltWarps);
   SBDT_WS(slabels, std::uint32_t, "assign.slabels", m);
-  SBDT_WS(stats, unsigned, "assign.stats", 4);
+  SBDT_WS(stats, unsigned, "assign.stats", 6);
   SBDT_WS(oq, std::uint32_t, "assign.oq", n + 1);
   SBDT_WS(oqc, unsigned, "assign.oqc", 1);
   int sms = 148;
@@ -404,7 +404,7 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
   }
   {
     StageTimer t1(ctx, "assign.table");
-    if (ctx->census) SBDT_CUDA_TRY(cudaMemsetAsync(stats, 0, sizeof(unsigned) * 4, st));
+    if (ctx->census) SBDT_CUDA_TRY(cudaMemsetAsync(stats, 0, sizeof(unsigned) * 6, st));
     SBDT_CUDA_TRY(cudaMemsetAsync(lcount, 0, sizeof(unsigned), st));
     SBDT_CUDA_TRY(cudaMemsetAsync(dqn, 0, sizeof(unsigned), st));
     SBDT_CUDA_TRY(cudaMemsetAsync(subcount, 0, sizeof(unsigned), st));
@@ -448,6 +448,9 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
     k_assign_overflow<D><<<sms * 8, 128, 0, st>>>(d_xyz, sg, starts, sorted, slabels, heads, subheads, lslab, d_labels, oq,
                                                    oqc);
     ctx->launches += 2;
+    if (ctx->census) {  // queued points (long lists + ring searches)
+      SBDT_CUDA_TRY(cudaMemcpyAsync(stats + 4, oqc, sizeof(unsigned), cudaMemcpyDeviceToDevice, st));
+    }
   }
   SBDT_CUDA_TRY(cudaGetLastError());
   return kOk;
@@ -480,7 +483,7 @@ int assign_stats(sbdt_gpu_ctx* ctx, unsigned* out4) {
   auto it = ctx->bufs.find("assign.stats");
   if (it == ctx->bufs.end()) return kErrInvalid;
   cudaStreamSynchronize(ctx->stream);
-  cudaMemcpy(out4, it->second.ptr, sizeof(unsigned) * 4, cudaMemcpyDeviceToHost);
+  cudaMemcpy(out4, it->second.ptr, sizeof(unsigned) * 5, cudaMemcpyDeviceToHost);
   return kOk;
 }
 

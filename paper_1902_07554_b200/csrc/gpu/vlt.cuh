@@ -653,9 +653,6 @@ __global__ void __launch_bounds__(128) k_assign_overflow(const double* __restric
   __shared__ SampleGrid<D> sg;
   if (threadIdx.x == 0) sg = *sgp;
   __syncthreads();
-  constexpr int F = fine_factor<D>();
-  constexpr int FC = fine_per_cell<D>();
-  const unsigned full = 0xffffffffu;
   const unsigned lane = threadIdx.x & 31u;
   const unsigned cnt = *oq_count;
   const unsigned warps = gridDim.x * (blockDim.x >> 5);
