@@ -198,7 +198,7 @@ __global__ void k_sample_scatter(const SampleRec* __restrict__ recs, std::uint32
 // is the last one visited only when a rigorous lower bound (binning error +
 // rounding margin) proves every unvisited sample strictly farther in binary64.
 template <int D>
-__device__ std::uint32_t nearest_label_ring(const double* x, const Grid<D>& g, double margin,
+__device__ __noinline__ std::uint32_t nearest_label_ring(const double* x, const Grid<D>& g, double margin,
                                             const std::uint32_t* __restrict__ starts,
                                             const SampleRec* __restrict__ sorted) {
   long long ci[D];
@@ -213,30 +213,49 @@ __device__ std::uint32_t nearest_label_ring(const double* x, const Grid<D>& g, d
       lo_c[d] = ci[d] - r < 0 ? 0 : ci[d] - r;
       hi_c[d] = ci[d] + r > g.dims[d] - 1 ? g.dims[d] - 1 : ci[d] + r;
     }
-    long long c[D];
-    long long count = 1;
+    // the shell of Chebyshev radius r only: rows along axis 0 over the
+    // (D-1)-dimensional cross-section; a row on the shell's side faces is
+    // scanned whole, an interior row contributes its two end cells
+    long long rows = 1;
 #pragma unroll
-    for (int d = 0; d < D; ++d) count *= (hi_c[d] - lo_c[d] + 1);
-    for (long long t = 0; t < count; ++t) {
-      long long rem = t, cheb = 0;
+    for (int d = 1; d < D; ++d) rows *= (hi_c[d] - lo_c[d] + 1);
+    for (long long t = 0; t < rows; ++t) {
+      long long c[D], rem = t, cheb = 0;
 #pragma unroll
-      for (int d = 0; d < D; ++d) {
+      for (int d = 1; d < D; ++d) {
         const long long span = hi_c[d] - lo_c[d] + 1;
         c[d] = lo_c[d] + rem % span;
         rem /= span;
         const long long dd = c[d] > ci[d] ? c[d] - ci[d] : ci[d] - c[d];
         cheb = dd > cheb ? dd : cheb;
       }
-      if (cheb != r) continue;
-      const long long cell = linear<D>(g, c);
-      for (std::uint32_t s = starts[cell], e = starts[cell + 1]; s < e; ++s) {
-        const SampleRec rec = sorted[s];
-        const double d2 = sqdist<D>(x, rec.x);
-        if (d2 < best || (d2 == best && rec.pid < best_pid)) {
-          best = d2;
-          best_pid = rec.pid;
-          best_label = rec.label;
+      long long xs[2];
+      int nx = 0;
+      if (cheb == r) {
+        xs[0] = lo_c[0];
+        xs[1] = hi_c[0];
+        nx = -1;  // the whole row
+      } else {
+        if (ci[0] - r >= 0) xs[nx++] = ci[0] - r;
+        if (r > 0 && ci[0] + r <= g.dims[0] - 1) xs[nx++] = ci[0] + r;
+      }
+      auto scan_cell = [&](long long x0) {
+        c[0] = x0;
+        const long long cell = linear<D>(g, c);
+        for (std::uint32_t s = starts[cell], e = starts[cell + 1]; s < e; ++s) {
+          const SampleRec rec = sorted[s];
+          const double d2 = sqdist<D>(x, rec.x);
+          if (d2 < best || (d2 == best && rec.pid < best_pid)) {
+            best = d2;
+            best_pid = rec.pid;
+            best_label = rec.label;
+          }
         }
+      };
+      if (nx < 0) {
+        for (long long x0 = xs[0]; x0 <= xs[1]; ++x0) scan_cell(x0);
+      } else {
+        for (int k = 0; k < nx; ++k) scan_cell(xs[k]);
       }
     }
     double lb = INFINITY;

@@ -413,7 +413,45 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
 #pragma unroll
       for (int d = 0; d < D; ++d) rt[d] = A.rel[std::size_t(bj) * D + d] - off[d];
       const std::uint32_t lab0 = A.lab[bj];
-      // kept list of this box (dominance against the nearest parent candidate)
+      // two more dominators: the next nearest candidates to the box centre
+      // (a sample survives only if none of the three beats it over the box)
+      int dj[2] = {bj, bj};
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        float kd = INFINITY;
+        int kj = 0x7fffffff;
+        for (int t = lane; t < np; t += 32) {
+          const int j = cand(t);
+          if (j == bj || (k == 1 && j == dj[0])) continue;
+          float dd = 0.f;
+#pragma unroll
+          for (int d = 0; d < D; ++d) {
+            const float u = A.rel[std::size_t(j) * D + d] - off[d];
+            dd += u * u;
+          }
+          if (dd < kd || (dd == kd && j < kj)) {
+            kd = dd;
+            kj = j;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const float od = __shfl_xor_sync(0xffffffffu, kd, o);
+          const int oj = __shfl_xor_sync(0xffffffffu, kj, o);
+          if (od < kd || (od == kd && oj < kj)) {
+            kd = od;
+            kj = oj;
+          }
+        }
+        dj[k] = kj == 0x7fffffff ? bj : kj;
+      }
+      float rt1[D], rt2[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        rt1[d] = A.rel[std::size_t(dj[0]) * D + d] - off[d];
+        rt2[d] = A.rel[std::size_t(dj[1]) * D + d] - off[d];
+      }
+      // kept list of this box (dominance against the nearest parent candidates)
       int count = 0, inbox = 0;  // kept candidates; samples inside the box (~ points to expect)
       bool uniform = true;
       for (int t0 = 0; t0 < np; t0 += 32) {
@@ -429,7 +467,8 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
             rs[d] = A.rel[std::size_t(j) * D + d] - off[d];
             ins = ins && fabsf(rs[d]) <= fhw[d];
           }
-          keep = (j == bj) || !dominated_f<D>(rs, rt, fhw, fH);
+          keep = (j == bj) || !(dominated_f<D>(rs, rt, fhw, fH) || dominated_f<D>(rs, rt1, fhw, fH) ||
+                                dominated_f<D>(rs, rt2, fhw, fH));
         }
         inbox += __popc(__ballot_sync(0xffffffffu, ins));
         const unsigned word = __ballot_sync(0xffffffffu, keep);
@@ -639,7 +678,7 @@ __global__ void __launch_bounds__(256) k_assign_vlt(const double* __restrict__ x
 // Queued points (long candidate lists and ring searches), one lane per point:
 // the queue holds only these, so the lanes of a warp do the same kind of work.
 template <int D>
-__global__ void __launch_bounds__(128) k_assign_overflow(const double* __restrict__ xyz,
+__global__ void __launch_bounds__(128, 8) k_assign_overflow(const double* __restrict__ xyz,
                                                          const SampleGrid<D>* __restrict__ sgp,
                                                          const std::uint32_t* __restrict__ starts,
                                                          const SampleRec* __restrict__ sorted,
@@ -671,8 +710,8 @@ __global__ void __launch_bounds__(128) k_assign_overflow(const double* __restric
     }
     if (has && (head & 15u) == kHeadLong) {
       // one lane per point, its whole list: the list path's decision
-      // (binary32 distances with the rigorous bound, exact binary64 argmin
-      // over the undecided entries) in three passes over the entries
+      // (binary32 distances with the rigorous bound; exact binary64 argmin
+      // over the undecided entries only when the bounds overlap)
       const VltEntry* ents = lslab + (head >> 4);
       const int ne = static_cast<int>(ents[0].idx);
       ++ents;
@@ -693,25 +732,34 @@ __global__ void __launch_bounds__(128) k_assign_overflow(const double* __restric
         *bnd = 4e-6f * (pp + ss) + 1e-30f;
         return dd;
       };
-      float bv = INFINITY, bb = 0.f;
-      int bj = 0;
+      // one pass: the winner (min dd) and the two smallest lower ends dd - bnd
+      // (the smallest one not belonging to the winner decides)
+      float bv = INFINITY, bb = 0.f, m1 = INFINITY, m2 = INFINITY;
+      int bj = 0, j1 = -1;
       for (int j = 0; j < ne; ++j) {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(ents + j));
+        VltEntry e;
+        e.r[0] = q.x;
+        e.r[1] = q.y;
+        e.r[2] = q.z;
         float bnd;
-        const float dd = dist(ents[j], &bnd);
+        const float dd = dist(e, &bnd);
         if (dd < bv) {
           bv = dd;
           bb = bnd;
           bj = j;
         }
+        const float lo_end = dd - bnd;
+        if (lo_end < m1) {
+          m2 = m1;
+          m1 = lo_end;
+          j1 = j;
+        } else if (lo_end < m2) {
+          m2 = lo_end;
+        }
       }
       const float lim = bv + bb;
-      bool decided = true;
-      for (int j = 0; j < ne && decided; ++j) {
-        if (j == bj) continue;
-        float bnd;
-        const float dd = dist(ents[j], &bnd);
-        if (dd - bnd <= lim) decided = false;
-      }
+      const bool decided = (j1 == bj ? m2 : m1) > lim;
       std::uint32_t lab;
       if (decided) {
         lab = __ldg(sorted_labels + ents[bj].idx);
