@@ -385,8 +385,10 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
       // Relative coordinates w.r.t. the box centre are recomputed in binary64
       // for the stored entries; the dominance test uses (coarse-rel - off),
       // whose extra rounding is covered by the 1e-5 margin.
-      float bdist = INFINITY;
-      int bj = 0x7fffffff;
+      // the three candidates nearest to the box centre (dominators): per-lane
+      // top 3 in one pass, then three warp argmin rounds
+      float ld[3] = {INFINITY, INFINITY, INFINITY};
+      int lj[3] = {0x7fffffff, 0x7fffffff, 0x7fffffff};
       for (int t = lane; t < np; t += 32) {
         const int j = cand(t);
         float dd = 0.f;
@@ -395,61 +397,62 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
           const float u = A.rel[std::size_t(j) * D + d] - off[d];
           dd += u * u;
         }
-        if (dd < bdist || (dd == bdist && j < bj)) {
-          bdist = dd;
-          bj = j;
+        // insert (dd, j) into the lane's sorted top 3 (ties: lower j first)
+        if (dd < ld[2] || (dd == ld[2] && j < lj[2])) {
+          if (dd < ld[1] || (dd == ld[1] && j < lj[1])) {
+            ld[2] = ld[1];
+            lj[2] = lj[1];
+            if (dd < ld[0] || (dd == ld[0] && j < lj[0])) {
+              ld[1] = ld[0];
+              lj[1] = lj[0];
+              ld[0] = dd;
+              lj[0] = j;
+            } else {
+              ld[1] = dd;
+              lj[1] = j;
+            }
+          } else {
+            ld[2] = dd;
+            lj[2] = j;
+          }
         }
       }
+      int dom[3];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float od = __shfl_xor_sync(0xffffffffu, bdist, o);
-        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
-        if (od < bdist || (od == bdist && oj < bj)) {
-          bdist = od;
-          bj = oj;
+      for (int k = 0; k < 3; ++k) {
+        float bdv = ld[0];
+        int bjv = lj[0];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const float od = __shfl_xor_sync(0xffffffffu, bdv, o);
+          const int oj = __shfl_xor_sync(0xffffffffu, bjv, o);
+          if (od < bdv || (od == bdv && oj < bjv)) {
+            bdv = od;
+            bjv = oj;
+          }
+        }
+        dom[k] = bjv;
+        if (lj[0] == bjv && bjv != 0x7fffffff) {  // the winning lane pops its head
+          ld[0] = ld[1];
+          lj[0] = lj[1];
+          ld[1] = ld[2];
+          lj[1] = lj[2];
+          ld[2] = INFINITY;
+          lj[2] = 0x7fffffff;
         }
       }
+      const int bj = dom[0];
       float rt[D];
 #pragma unroll
       for (int d = 0; d < D; ++d) rt[d] = A.rel[std::size_t(bj) * D + d] - off[d];
       const std::uint32_t lab0 = A.lab[bj];
-      // two more dominators: the next nearest candidates to the box centre
-      // (a sample survives only if none of the three beats it over the box)
-      int dj[2] = {bj, bj};
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        float kd = INFINITY;
-        int kj = 0x7fffffff;
-        for (int t = lane; t < np; t += 32) {
-          const int j = cand(t);
-          if (j == bj || (k == 1 && j == dj[0])) continue;
-          float dd = 0.f;
-#pragma unroll
-          for (int d = 0; d < D; ++d) {
-            const float u = A.rel[std::size_t(j) * D + d] - off[d];
-            dd += u * u;
-          }
-          if (dd < kd || (dd == kd && j < kj)) {
-            kd = dd;
-            kj = j;
-          }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const float od = __shfl_xor_sync(0xffffffffu, kd, o);
-          const int oj = __shfl_xor_sync(0xffffffffu, kj, o);
-          if (od < kd || (od == kd && oj < kj)) {
-            kd = od;
-            kj = oj;
-          }
-        }
-        dj[k] = kj == 0x7fffffff ? bj : kj;
-      }
+      const int dj0 = dom[1] == 0x7fffffff ? bj : dom[1];
+      const int dj1 = dom[2] == 0x7fffffff ? bj : dom[2];
       float rt1[D], rt2[D];
 #pragma unroll
       for (int d = 0; d < D; ++d) {
-        rt1[d] = A.rel[std::size_t(dj[0]) * D + d] - off[d];
-        rt2[d] = A.rel[std::size_t(dj[1]) * D + d] - off[d];
+        rt1[d] = A.rel[std::size_t(dj0) * D + d] - off[d];
+        rt2[d] = A.rel[std::size_t(dj1) * D + d] - off[d];
       }
       // kept list of this box (dominance against the nearest parent candidates)
       int count = 0, inbox = 0;  // kept candidates; samples inside the box (~ points to expect)
