@@ -79,9 +79,10 @@ int sbdt_gpu_check_status(sbdt_gpu_ctx* ctx);
 int sbdt_gpu_set_timing(sbdt_gpu_ctx* ctx, int enable);
 int sbdt_gpu_stage_times(sbdt_gpu_ctx* ctx, char* names, int names_len, float* ms, int max_stages);
 /* Voronoi-label-table census of the last assign with the census enabled:
- * out5 = {uniform records, short-list records, ring-search records,
- * long-list records, queued points (long lists + ring searches)}. */
-int sbdt_gpu_assign_table_stats(sbdt_gpu_ctx* ctx, unsigned* out5);
+ * out6 = {uniform records, short-list records, ring-search records,
+ * long-list records, queued points (long lists + ring searches), coarse cells
+ * built by the dense pass}. */
+int sbdt_gpu_assign_table_stats(sbdt_gpu_ctx* ctx, unsigned* out6);
 /* Border pipeline census of the last find_border with the census enabled (grid
  * policy; zeros otherwise): out12 = {rows scanned by the prefilter, rows that
  * reached the exact stage, exact rows by scan kind: flattened cell scan,

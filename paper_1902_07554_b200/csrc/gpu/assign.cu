@@ -467,8 +467,9 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
     k_assign_overflow<D><<<sms * 8, 128, 0, st>>>(d_xyz, sg, starts, sorted, slabels, heads, subheads, lslab, d_labels, oq,
                                                    oqc);
     ctx->launches += 2;
-    if (ctx->census) {  // queued points (long lists + ring searches)
+    if (ctx->census) {  // queued points (long lists + ring searches), dense coarse cells
       SBDT_CUDA_TRY(cudaMemcpyAsync(stats + 4, oqc, sizeof(unsigned), cudaMemcpyDeviceToDevice, st));
+      SBDT_CUDA_TRY(cudaMemcpyAsync(stats + 5, dqn, sizeof(unsigned), cudaMemcpyDeviceToDevice, st));
     }
   }
   SBDT_CUDA_TRY(cudaGetLastError());
@@ -502,7 +503,7 @@ int assign_stats(sbdt_gpu_ctx* ctx, unsigned* out4) {
   auto it = ctx->bufs.find("assign.stats");
   if (it == ctx->bufs.end()) return kErrInvalid;
   cudaStreamSynchronize(ctx->stream);
-  cudaMemcpy(out4, it->second.ptr, sizeof(unsigned) * 5, cudaMemcpyDeviceToHost);
+  cudaMemcpy(out4, it->second.ptr, sizeof(unsigned) * 6, cudaMemcpyDeviceToHost);
   return kOk;
 }
 

@@ -152,9 +152,9 @@ int sbdt_gpu_stage_times(sbdt_gpu_ctx* ctx, char* names, int names_len, float* m
   return count;
 }
 
-int sbdt_gpu_assign_table_stats(sbdt_gpu_ctx* ctx, unsigned* out5) {
-  if (!ctx || !out5) return SBDT_ERR_INVALID;
-  return assign_stats(ctx, out5) == kOk ? SBDT_OK : SBDT_ERR_INVALID;
+int sbdt_gpu_assign_table_stats(sbdt_gpu_ctx* ctx, unsigned* out6) {
+  if (!ctx || !out6) return SBDT_ERR_INVALID;
+  return assign_stats(ctx, out6) == kOk ? SBDT_OK : SBDT_ERR_INVALID;
 }
 
 int sbdt_gpu_border_stats(sbdt_gpu_ctx* ctx, unsigned long long* out12) {

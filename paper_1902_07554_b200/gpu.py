@@ -145,11 +145,11 @@ class Context:
         return [(labels[i], float(ms[i])) for i in range(cnt)]
 
     def table_stats(self) -> dict:
-        out = (C.c_uint * 5)()
+        out = (C.c_uint * 6)()
         if lib().sbdt_gpu_assign_table_stats(self._h, out) != SBDT_OK:
             return {}
         return {"uniform": int(out[0]), "list": int(out[1]), "ring_search": int(out[2]), "long_list": int(out[3]),
-                "queued_points": int(out[4])}
+                "queued_points": int(out[4]), "dense_cells": int(out[5])}
 
     def border_stats(self) -> dict:
         out = (C.c_ulonglong * 12)()
