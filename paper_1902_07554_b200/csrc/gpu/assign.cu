@@ -397,7 +397,7 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
   SBDT_WS(subcount, unsigned, "assign.subcount", 1);
   SBDT_WS(dq, std::uint32_t, "assign.dense_q", cap + 1);
   SBDT_WS(dqn, unsigned, "assign.dense_n", 1);
-  constexpr unsigned kDenseBlocks = 148 * 2;
+  constexpr unsigned kDenseBlocks = 148 * 8;
   SBDT_WS(dscr, char, "assign.dense_scratch", vlt_dense_bytes_per_warp<D>() * kDenseBlocks * kVltWarps);
   SBDT_WS(slabels, std::uint32_t, "assign.slabels", m);
   SBDT_WS(stats, unsigned, "assign.stats", 6);
