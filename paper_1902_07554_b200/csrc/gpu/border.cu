@@ -568,9 +568,13 @@ __device__ __forceinline__ void load_simplex(const BorderArgs& a, const std::uin
 // its 3^D or its 5^D neighbourhood) whose combined code is EMPTY or self.
 // Positive: the INNER ball (inside the binary64 sphere, checked in binary64)
 // reaches the cell of its centre and that cell holds another part.
-template <int D>
-__device__ __forceinline__ int prefilter_decide(const OwnerGrid<D>& og, const BorderArgs& a, const Sphere32<D>& sp, std::uint32_t self, float inv_e, float margin_c,
-                                                float lo_mag, bool pos_ok) {
+// kWindow: run the negative (window) test; kNbrs: also try the neighbours of
+// the centre cell for the positive proof (the exact stage, where every lane
+// holds an undecided row, so the extra lookups do not diverge the warp).
+template <int D, bool kWindow, bool kNbrs>
+__device__ __forceinline__ int prefilter_decide(const OwnerGrid<D>& og, const BorderArgs& a, const Sphere32<D>& sp,
+                                                std::uint32_t self, float inv_e, float margin_c, float lo_mag,
+                                                bool pos_ok) {
   // R >= radius of the inflated binary64 sphere + distance between centres
   float slack = 0.f;
 #pragma unroll
@@ -580,6 +584,7 @@ __device__ __forceinline__ int prefilter_decide(const OwnerGrid<D>& og, const Bo
   const float Rc = R * inv_e * 1.000001f + margin_c;
   int lo[D], w = 0;
   int c0[D];
+  float Ucs[D];
   bool outside = false, inside = true;
   float sl_max = 0.f;
 #pragma unroll
@@ -594,12 +599,13 @@ __device__ __forceinline__ int prefilter_decide(const OwnerGrid<D>& og, const Bo
     outside = outside || ib < 0 || ia > og.ldims[0][d] - 1;
     lo[d] = max(ia, 0);
     w = max(w, min(ib, og.ldims[0][d] - 1) - lo[d]);
+    Ucs[d] = Uc;
     const int ic = floor_small(fminf(fmaxf(Uc, -2.f), top + 2.f));
     inside = inside && ic >= 0 && ic <= og.ldims[0][d] - 1;
     c0[d] = ic;
   }
-  if (outside) return 0;  // the range misses the grid on some axis: no cell is reachable
-  if (w <= 4) {
+  if (outside) return kWindow ? 0 : 2;  // the range misses the grid on some axis: no cell is reachable
+  if (kWindow && w <= 4) {
     const int h = w == 0 ? 0 : (w <= 2 ? 1 : 2);
     int cm[D];
 #pragma unroll
@@ -614,11 +620,69 @@ __device__ __forceinline__ int prefilter_decide(const OwnerGrid<D>& og, const Bo
   // (|lo| / edge + dims) < 2^26, checked by the caller through pos_ok). If the
   // inner ball, shrunk by the exact stage's margin, still reaches that box,
   // the binary64 box test on the binary64 sphere accepts it.
+  // The same holds for a neighbour of c0 whose box (in cell units) is within
+  // the remaining reach of Uc.
   if (!inside || !pos_ok || a.exact) return 2;  // exact policy: a foreign cell is not a foreign point
   const float rin_c = ((sp.r * 0.999996f - 2.01f * sp.e * 1.000001f) * 0.999999f - slack) * inv_e * 0.999998f;
-  if (!(rin_c - margin_c > 1.7321f * sl_max + 1e-7f)) return 2;
-  const std::uint16_t code = a.owner[og_index<D>(og, 0, c0)];
-  return (code == kOwnerEmpty || code == self) ? 2 : 1;
+  const float reach = rin_c - margin_c - 1.7321f * sl_max - 2e-7f;
+  if (!(reach > 0.f)) return 2;
+  {
+    const std::uint16_t code = a.owner[og_index<D>(og, 0, c0)];
+    if (code != kOwnerEmpty && code != self) return 1;
+  }
+  if constexpr (!kNbrs) return 2;
+  // the neighbours on the near side of Uc in each axis (the 2^D - 1 cells of
+  // the octant Uc lies in; the far ones are at least half a cell further)
+  const float reach2 = reach * reach;
+  int side[D];
+  float gap[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const float f = Ucs[d] - static_cast<float>(c0[d]);
+    side[d] = f < 0.5f ? -1 : 1;
+    gap[d] = f < 0.5f ? f : 1.f - f;
+  }
+#pragma unroll
+  for (int k = 1; k < (1 << D); ++k) {
+    int cn[D];
+    float d2 = 0.f;
+    bool ok = true;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const bool move = (k >> d) & 1;
+      cn[d] = c0[d] + (move ? side[d] : 0);
+      ok = ok && cn[d] >= 0 && cn[d] < og.ldims[0][d];
+      d2 += move ? gap[d] * gap[d] : 0.f;
+    }
+    if (!ok || !(d2 * 1.000002f + 1e-12f < reach2)) continue;
+    const std::uint16_t code = a.owner[og_index<D>(og, 0, cn)];
+    if (code != kOwnerEmpty && code != self) return 1;
+  }
+  return 2;
+}
+
+// Per-launch constants of the binary32 decisions (cell-unit scale, margins,
+// fixed-point step), rounded up where they bound an error.
+struct PfConsts {
+  float inv_e, margin_c, lo_mag, qh_f, qh_err;
+  bool pos_ok;
+};
+
+template <int D>
+__device__ __forceinline__ PfConsts pf_consts(const OwnerGrid<D>& og) {
+  PfConsts k;
+  k.inv_e = static_cast<float>(og.inv_edge);
+  k.margin_c = static_cast<float>(og.margin * og.inv_edge) * 1.0001f + 1e-30f;
+  k.lo_mag = 0.f;
+  k.pos_ok = true;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    k.lo_mag = fmaxf(k.lo_mag, static_cast<float>(fabs(og.g.lo[d])) * 1.0001f);
+    k.pos_ok = k.pos_ok && fabs(og.g.lo[d]) * og.inv_edge + static_cast<double>(og.ldims[0][d]) < 67108864.0;
+  }
+  k.qh_f = static_cast<float>(og.qh);
+  k.qh_err = static_cast<float>(og.qh) * 0.50011f;
+  return k;
 }
 
 template <int D>
@@ -682,7 +746,8 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
       Sphere32<D> sp;
       decode_row<D>(a.xq, v, qh_f, qh_err, A, sp.P0, P0e, &eta);
       const int res = enclosing_sphere_f32<D>(A, eta, P0e, sp)
-                          ? prefilter_decide<D>(og, a, sp, self, inv_e, margin_c, lo_mag, pos_ok) : 2;
+                          ? prefilter_decide<D, true, false>(og, a, sp, self, inv_e, margin_c, lo_mag, pos_ok)
+                          : 2;
       if (a.counters && res == 1) atomicAdd(&a.counters[8], 1ull);
       if (res == 2) {
         is_cand = true;
@@ -785,6 +850,7 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
   const unsigned lane = threadIdx.x & 31u;
   const unsigned wid = threadIdx.x >> 5;
   CandSlot<D>* sl = slots[wid];
+  const PfConsts pf = pf_consts<D>(og);
   const bool multi_level = og.levels > 1;
   unsigned long long bst[D];  // level-1 block strides of the tiled level-0 index
   bst[0] = 1;
@@ -801,18 +867,34 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
     std::uint32_t self = 0, v[D + 1];
     double c[D], r2 = 0.0;
     int lo[D], span[D];
-    int mode = 0;  // 0 negative, 1 flattened scan, 2 two-level scan, 3 pyramid descent
+    int mode = 0;  // 0 decided, 1 flattened scan, 2 two-level scan, 3 pyramid descent
+    bool pre_pos = false;
     if (has) {
       s = cand[t];
       self = part_of(s_off, a.k, s);
 #pragma unroll
       for (int j = 0; j <= D; ++j) v[j] = cand[std::uint64_t(j + 1) * cap + t];
-      double p[D + 1][D];
-      load_simplex<D>(a, v, p);
-      circumsphere_inflated<D>(p, c, &r2);
-      mode = leaf_range<D>(og, c, r2, lo, span);
+      bool proven = false;
+      if constexpr (!Ex) {
+        // binary32 positive proof over the centre cell's neighbourhood (the
+        // prefilter tried the centre cell only)
+        float A32[D][D], P0e[D], eta;
+        Sphere32<D> sp;
+        decode_row<D>(a.xq, v, pf.qh_f, pf.qh_err, A32, sp.P0, P0e, &eta);
+        proven = enclosing_sphere_f32<D>(A32, eta, P0e, sp) &&
+                 prefilter_decide<D, false, true>(og, a, sp, self, pf.inv_e, pf.margin_c, pf.lo_mag, pf.pos_ok) == 1;
+      }
+      if (proven) {
+        mode = 0;
+        pre_pos = true;
+      } else {
+        double p[D + 1][D];
+        load_simplex<D>(a, v, p);
+        circumsphere_inflated<D>(p, c, &r2);
+        mode = leaf_range<D>(og, c, r2, lo, span);
+      }
     }
-    bool pos = false;
+    bool pos = pre_pos;
     if (a.counters) {
       const unsigned m1 = __ballot_sync(full, mode == 1), m2 = __ballot_sync(full, mode == 2),
                      m3 = __ballot_sync(full, mode == 3);
