@@ -385,8 +385,11 @@ def main():
         t_e2e = (time.perf_counter() - t0) / e2e_steps
         assert np.array_equal(res.labels, labels)
         # find_border without the BFS reads only the last neighbour row (hull rows)
+        # (the hull rows' neighbour is read in place from the page-locked
+        # nbrs buffer: ~1% of S entries cross PCIe, counted as 4 B each)
+        n_hull = int(np.count_nonzero(part.verts[dim] == 0xFFFFFFFF))
         h2d = (inst.points.nbytes + 8 * m + 8 * m * dim) + (part.offsets.nbytes + part.verts.nbytes
-                                                            + 4 * S + part.parity.nbytes)
+                                                            + 4 * n_hull + part.parity.nbytes)
         d2h = (4 * n + 8 * (k + 1) + 4 * n + 8 * dim) + (S + 8 + 4 * len(bs.positive_vertex_ids))
         e2e = {"value": world * n / t_e2e, "unit": "points/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": round(1e3 * t_e2e, 3),

@@ -371,6 +371,17 @@ int sbdt_gpu_find_border(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint6
   SBDT_CUDA_TRY(cudaMemcpyAsync(d_off, offsets, sizeof(uint64_t) * (k + 1), cudaMemcpyHostToDevice, cs));
   SBDT_CUDA_TRY(cudaEventRecord(ctx->chunk_events[kUploadChunks], cs));
   SBDT_CUDA_TRY(cudaStreamWaitEvent(st, ctx->chunk_events[kUploadChunks], 0));
+  // Without the BFS the ~1% hull rows read one neighbour each: a page-locked
+  // caller buffer is mapped into the device address space and read in place
+  // instead of uploading a whole SoA row.
+  const uint32_t* nbrs_mapped = nullptr;
+  if (!bfs) {
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, nbrs) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
+      nbrs_mapped = static_cast<const uint32_t*>(pa.devicePointer);
+    else
+      cudaGetLastError();  // pageable: clear the error, upload the row
+  }
   for (int c = 0; c < kUploadChunks; ++c) {
     const uint64_t r0 = S * c / kUploadChunks, r1 = S * (c + 1) / kUploadChunks;
     if (r1 > r0) {
@@ -379,10 +390,12 @@ int sbdt_gpu_find_border(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint6
                                       cudaMemcpyHostToDevice, cs));
       SBDT_CUDA_TRY(cudaMemcpyAsync(d_par + r0, parity + r0, r1 - r0, cudaMemcpyHostToDevice, cs));
       // without the BFS only the hull rows' last neighbour (the finite
-      // simplex across the hull facet, row dim of the SoA) is read
-      for (int j = bfs ? 0 : dim; j <= dim; ++j)
-        SBDT_CUDA_TRY(cudaMemcpyAsync(d_nbrs + j * S + r0, nbrs + j * S + r0, sizeof(uint32_t) * (r1 - r0),
-                                      cudaMemcpyHostToDevice, cs));
+      // simplex across the hull facet, row dim of the SoA) is read, and from
+      // a page-locked caller buffer it is read in place (zero-copy)
+      if (!nbrs_mapped)
+        for (int j = bfs ? 0 : dim; j <= dim; ++j)
+          SBDT_CUDA_TRY(cudaMemcpyAsync(d_nbrs + j * S + r0, nbrs + j * S + r0, sizeof(uint32_t) * (r1 - r0),
+                                        cudaMemcpyHostToDevice, cs));
     }
     SBDT_CUDA_TRY(cudaEventRecord(ctx->chunk_events[c], cs));
     ctx->chunks.emplace_back(r1, ctx->chunk_events[c]);
@@ -392,7 +405,7 @@ int sbdt_gpu_find_border(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint6
   a.d_labels = d_lab;
   a.d_offsets = d_off;
   a.d_verts = d_verts;
-  a.d_nbrs = d_nbrs;
+  a.d_nbrs = nbrs_mapped ? nbrs_mapped : d_nbrs;
   a.d_parity = d_par;
   a.d_positive = d_pos;
   a.d_border = d_bor;

@@ -194,3 +194,25 @@ def test_resident_points_flag(ctx):
     assert np.array_equal(res.positive_vertex_ids, ref.positive_vertex_ids)
     with pytest.raises(ValueError):
         gpu.find_border(inst.points.copy(), part.labels, pt, ctx=ctx, resident=True)
+
+
+def test_zero_copy_hull_neighbours(ctx):
+    """No-BFS host call with page-locked partials: the hull rows' neighbours
+    are read in place from host memory (zero-copy); same results as the
+    pageable (uploaded) path."""
+    inst = host.make_instance(2, n=120_000, k=16)
+    part = gpu.assign_points(inst.points, inst.sample_ids, inst.sample_labels, 16, ctx=ctx)
+    pt = host.attach_partials(inst, part.labels)
+
+    def pinned(a):
+        v = gpu.pinned_empty(a.shape, a.dtype)
+        v[...] = a
+        return v
+
+    pp = host.Partials(pinned(pt.offsets), pinned(pt.verts), pinned(pt.nbrs), pinned(pt.parity))
+    zc = gpu.find_border(inst.points, part.labels, pp, gpu.IntersectionPolicy("grid"), hull_bfs=False, ctx=ctx)
+    ref = gpu.find_border(inst.points, part.labels, pt, gpu.IntersectionPolicy("grid"), hull_bfs=False, ctx=ctx)
+    assert np.array_equal(zc.positive, ref.positive)
+    assert np.array_equal(zc.positive_vertex_ids, ref.positive_vertex_ids)
+    o = oracle.find_border(inst.points, part.labels, pt, "grid")
+    assert np.array_equal(zc.positive, o["positive"])
