@@ -1274,7 +1274,9 @@ __global__ void __launch_bounds__(kWideWarps * 32, 6) k_border_wide(BorderArgs a
 // under the grid policy each row's halfspace descent then runs on the whole
 // warp (warp_descent), the bbox policy tests the k-1 root boxes per lane.
 template <int D, bool Ex>
-__global__ void __launch_bounds__(kWideWarps * 32) k_border_infinite(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp) {
+__global__ void __launch_bounds__(kWideWarps * 32) k_border_infinite(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
+                                                                     unsigned* __restrict__ next,
+                                                                     unsigned* __restrict__ fin) {
   __shared__ OwnerGrid<D> og;
   __shared__ WideEntry<D> stacks[kWideWarps][kWideStack];
   extern __shared__ std::uint64_t s_off[];
@@ -1285,8 +1287,9 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_border_infinite(BorderArgs 
   const unsigned lane = threadIdx.x & 31u;
   WideEntry<D>* stk = stacks[threadIdx.x >> 5];
   const unsigned count = *a.inf_count;
-  const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
-  for (unsigned q0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32u; q0 < count; q0 += nwarps * 32u) {
+  for (;;) {
+    const unsigned q0 = claim_batch(next);
+    if (q0 >= count) break;
     const unsigned q = q0 + lane;
     const bool has = q < count;
     std::uint64_t s = 0;
@@ -1381,6 +1384,7 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_border_infinite(BorderArgs 
         for (int j = 0; j < D; ++j) a.vflags[fv[j]] = 1;
     }
   }
+  rewind_cursor(next, fin, count);
 }
 
 // ---- K9: flag compaction (two passes, ballot + block prefix sums) -------------
@@ -1683,6 +1687,15 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
     a.counters = cnt;
   }
   const std::size_t offs_sh = sizeof(std::uint64_t) * (in->k + 1);
+  SBDT_WS(icur, unsigned, "border.inf_cursor", 2);  // {cursor, CTAs done}
+  SBDT_CUDA_TRY(cudaMemsetAsync(icur, 0, 2 * sizeof(unsigned), st));
+  auto infinite = [&]() {
+    if (exact_policy) k_border_infinite<D, true><<<sms * 4, kWideWarps * 32, offs_sh, st>>>(a, og, icur, icur + 1);
+    else k_border_infinite<D, false><<<sms * 4, kWideWarps * 32, offs_sh, st>>>(a, og, icur, icur + 1);
+  };
+  // host path, grid policy: a chunk's positive flags are final once its rows
+  // went through all stages; they are downloaded while later chunks run
+  const bool stream_out = ctx->positive_host && !exact_policy;
   {
     const std::uint64_t want = (in->S + kBThreads - 1) / kBThreads;
     const unsigned blocks = static_cast<unsigned>(want < std::uint64_t(sms) * 32 ? want : std::uint64_t(sms) * 32);
@@ -1752,6 +1765,15 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
               exact();
               wide();
               ctx->launches += 3;
+              if (stream_out) {
+                infinite();
+                ++ctx->launches;
+                cudaEvent_t ev = ctx->chunk_done[&c - &ctx->chunks[0]];
+                SBDT_CUDA_TRY(cudaEventRecord(ev, st));
+                SBDT_CUDA_TRY(cudaStreamWaitEvent(ctx->d2h_stream, ev, 0));
+                SBDT_CUDA_TRY(cudaMemcpyAsync(ctx->positive_host + r0, in->d_positive + r0, r1 - r0,
+                                              cudaMemcpyDeviceToHost, ctx->d2h_stream));
+              }
             }
             r0 = r1;
           }
@@ -1769,8 +1791,7 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
     for (const auto& c : ctx->chunks) SBDT_CUDA_TRY(cudaStreamWaitEvent(st, c.second, 0));
     {
       StageTimer t(ctx, "border.infinite");
-      if (exact_policy) k_border_infinite<D, true><<<sms * 4, kWideWarps * 32, offs_sh, st>>>(a, og);
-      else k_border_infinite<D, false><<<sms * 4, kWideWarps * 32, offs_sh, st>>>(a, og);
+      infinite();  // the rows not yet drained (all of them unless the chunked path ran it)
     }
     if (exact_policy) {
       StageTimer t(ctx, "border.escalate");

@@ -92,6 +92,8 @@ void sbdt_gpu_destroy(sbdt_gpu_ctx* ctx) {
     if (kv.second.ptr) cudaFree(kv.second.ptr);
   if (ctx->d_status) cudaFree(ctx->d_status);
   for (cudaEvent_t e : ctx->chunk_events) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->chunk_done) cudaEventDestroy(e);
+  if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
   for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -207,10 +209,16 @@ static constexpr int kUploadChunks = 8;
 
 static int prepare_chunks(sbdt_gpu_ctx* ctx) {
   if (!ctx->copy_stream) SBDT_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  if (!ctx->d2h_stream) SBDT_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
   while (ctx->chunk_events.size() < kUploadChunks + 1) {
     cudaEvent_t e;
     SBDT_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     ctx->chunk_events.push_back(e);
+  }
+  while (ctx->chunk_done.size() < kUploadChunks) {
+    cudaEvent_t e;
+    SBDT_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->chunk_done.push_back(e);
   }
   ctx->chunks.clear();
   return SBDT_OK;
@@ -222,6 +230,7 @@ struct ChunkScope {
   ~ChunkScope() {
     ctx->chunks.clear();
     ctx->sample_xyz = nullptr;
+    ctx->positive_host = nullptr;
   }
 };
 
@@ -416,9 +425,11 @@ int sbdt_gpu_find_border(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint6
   a.d_bfs_vertex_ids = d_bvids;
   a.d_bfs_vertex_count = d_bcnt;
   a.d_spheres = d_sph;
+  const bool streamed = policy == SBDT_POLICY_GRID;  // border_impl streams the flags per chunk
+  ctx->positive_host = streamed ? positive_out : nullptr;
   TRY(sbdt_gpu_find_border_dev(ctx, &a));
   uint64_t nv = 0, nb = 0;
-  SBDT_CUDA_TRY(cudaMemcpyAsync(positive_out, d_pos, S, cudaMemcpyDeviceToHost, st));
+  if (!streamed) SBDT_CUDA_TRY(cudaMemcpyAsync(positive_out, d_pos, S, cudaMemcpyDeviceToHost, st));
   SBDT_CUDA_TRY(cudaMemcpyAsync(&nv, d_cnt, 8, cudaMemcpyDeviceToHost, st));
   if (bfs) {
     SBDT_CUDA_TRY(cudaMemcpyAsync(border_out, d_bor, S, cudaMemcpyDeviceToHost, st));
@@ -427,6 +438,7 @@ int sbdt_gpu_find_border(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint6
   if (spheres_out)
     SBDT_CUDA_TRY(cudaMemcpyAsync(spheres_out, d_sph, sizeof(double) * S * (dim + 1), cudaMemcpyDeviceToHost, st));
   TRY(finish(ctx));
+  if (streamed) SBDT_CUDA_TRY(cudaStreamSynchronize(ctx->d2h_stream));
   SBDT_CUDA_TRY(cudaMemcpy(vertex_ids_out, d_vids, sizeof(uint32_t) * nv, cudaMemcpyDeviceToHost));
   *n_vertices_out = nv;
   if (bfs) {

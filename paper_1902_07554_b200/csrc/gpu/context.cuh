@@ -45,6 +45,10 @@ struct sbdt_gpu_ctx {
   std::vector<cudaEvent_t> chunk_events;
   std::vector<std::pair<std::uint64_t, cudaEvent_t>> chunks;
   const double* sample_xyz = nullptr;  // compact sample coordinates (host path), else gathered from the points
+  // host path: positive flags streamed back per chunk on d2h_stream
+  std::uint8_t* positive_host = nullptr;
+  cudaStream_t d2h_stream = nullptr;
+  std::vector<cudaEvent_t> chunk_done;
   // host buffers whose device copies ("h.xyz", "h.lab", "h.bbox") are current
   // (SBDT_BORDER_RESIDENT_POINTS)
   const void* res_coords = nullptr;
