@@ -403,6 +403,7 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
   SBDT_WS(stats, unsigned, "assign.stats", 6);
   SBDT_WS(oq, std::uint32_t, "assign.oq", n + 1);
   SBDT_WS(oqc, unsigned, "assign.oqc", 1);
+  SBDT_WS(oqcur, unsigned, "assign.oq_cursor", 2);  // {cursor, CTAs done}
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
   const unsigned sblocks = static_cast<unsigned>((m + kBlock - 1) / kBlock);
@@ -442,6 +443,11 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
   if (blocks > 0) {
     StageTimer t2(ctx, "assign.points");
     SBDT_CUDA_TRY(cudaMemsetAsync(oqc, 0, sizeof(unsigned), st));
+    SBDT_CUDA_TRY(cudaMemsetAsync(oqcur, 0, 2 * sizeof(unsigned), st));
+    auto overflow = [&]() {
+      k_assign_overflow<D><<<sms * 8, 128, 0, st>>>(d_xyz, sg, starts, sorted, slabels, heads, subheads, lslab,
+                                                     d_labels, oq, oqc, oqcur, oqcur + 1);
+    };
     if (ctx->chunks.empty()) {
       k_assign_vlt<D><<<blocks, kBlock, 0, st>>>(d_xyz, 0, n, sg, heads, subheads, slab, lslab, sorted, slabels, d_labels,
                                                  d_bbox, oq,
@@ -459,13 +465,23 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
                                                 d_labels, d_bbox, oq,
                                                 oqc);
           ++ctx->launches;
+          if (ctx->labels_host) {
+            // the chunk's labels are final once its queued points are done:
+            // download them while later chunks run
+            overflow();
+            ++ctx->launches;
+            cudaEvent_t ev = ctx->chunk_done[&c - &ctx->chunks[0]];
+            SBDT_CUDA_TRY(cudaEventRecord(ev, st));
+            SBDT_CUDA_TRY(cudaStreamWaitEvent(ctx->d2h_stream, ev, 0));
+            SBDT_CUDA_TRY(cudaMemcpyAsync(ctx->labels_host + i0, d_labels + i0, sizeof(std::uint32_t) * (i1 - i0),
+                                          cudaMemcpyDeviceToHost, ctx->d2h_stream));
+          }
         }
         i0 = i1;
       }
       --ctx->launches;
     }
-    k_assign_overflow<D><<<sms * 8, 128, 0, st>>>(d_xyz, sg, starts, sorted, slabels, heads, subheads, lslab, d_labels, oq,
-                                                   oqc);
+    overflow();  // the queued points not yet done (all of them outside the streamed host path)
     ctx->launches += 2;
     if (ctx->census) {  // queued points (long lists + ring searches), dense coarse cells
       SBDT_CUDA_TRY(cudaMemcpyAsync(stats + 4, oqc, sizeof(unsigned), cudaMemcpyDeviceToDevice, st));

@@ -778,28 +778,6 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
   }
 }
 
-// Queue cursors: warps claim batches of 32 with atomicAdd, so a drained
-// cursor overshoots the queue length; the last CTA of a launch rewinds it to
-// the length the launch worked on, so a later launch over a grown queue
-// (host-path chunks) resumes exactly there.
-__device__ __forceinline__ unsigned claim_batch(unsigned* next) {
-  unsigned base = 0;
-  if ((threadIdx.x & 31u) == 0) base = atomicAdd(next, 32u);
-  return __shfl_sync(0xffffffffu, base, 0);
-}
-
-__device__ __forceinline__ void rewind_cursor(unsigned* next, unsigned* fin, unsigned limit) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(fin, 1u) == gridDim.x - 1) {
-      *next = limit;
-      *fin = 0u;
-      __threadfence();
-    }
-  }
-}
-
 // per-lane candidate record for the flattened scan (shared memory, per warp)
 // Term of axis d's cell coordinate in the level-0 tiled index (og_index is
 // the sum over the axes plus loff[0]).

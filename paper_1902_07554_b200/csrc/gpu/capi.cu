@@ -231,6 +231,7 @@ struct ChunkScope {
     ctx->chunks.clear();
     ctx->sample_xyz = nullptr;
     ctx->positive_host = nullptr;
+    ctx->labels_host = nullptr;
   }
 };
 
@@ -277,8 +278,8 @@ int sbdt_gpu_assign_points(sbdt_gpu_ctx* ctx, int dim, const double* coords, uin
     SBDT_CUDA_TRY(cudaEventRecord(ctx->chunk_events[c], ctx->copy_stream));
     ctx->chunks.emplace_back(i1, ctx->chunk_events[c]);
   }
+  ctx->labels_host = labels_out;  // streamed per chunk by assign_impl
   TRY(sbdt_gpu_assign_points_dev(ctx, dim, d_xyz, n, d_sid, d_slab, m, k, d_lab, d_poff, d_pids, d_bbox));
-  SBDT_CUDA_TRY(cudaMemcpyAsync(labels_out, d_lab, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, st));
   if (parts) {
     SBDT_CUDA_TRY(cudaMemcpyAsync(part_offsets_out, d_poff, sizeof(uint64_t) * (k + 1), cudaMemcpyDeviceToHost, st));
     SBDT_CUDA_TRY(cudaMemcpyAsync(part_ids_out, d_pids, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, st));
@@ -286,6 +287,7 @@ int sbdt_gpu_assign_points(sbdt_gpu_ctx* ctx, int dim, const double* coords, uin
   unsigned long long hb[6] = {0, 0, 0, 0, 0, 0};
   if (bbox_out) SBDT_CUDA_TRY(cudaMemcpyAsync(hb, d_bbox, sizeof(uint64_t) * 2 * dim, cudaMemcpyDeviceToHost, st));
   TRY(finish(ctx));
+  SBDT_CUDA_TRY(cudaStreamSynchronize(ctx->d2h_stream));
   if (bbox_out)
     for (int i = 0; i < 2 * dim; ++i) bbox_out[i] = ordered_to_dbl(hb[i]);
   ctx->res_coords = coords;

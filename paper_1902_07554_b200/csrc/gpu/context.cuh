@@ -47,6 +47,7 @@ struct sbdt_gpu_ctx {
   const double* sample_xyz = nullptr;  // compact sample coordinates (host path), else gathered from the points
   // host path: positive flags streamed back per chunk on d2h_stream
   std::uint8_t* positive_host = nullptr;
+  std::uint32_t* labels_host = nullptr;  // assign_points: labels streamed back per chunk
   cudaStream_t d2h_stream = nullptr;
   std::vector<cudaEvent_t> chunk_done;
   // host buffers whose device copies ("h.xyz", "h.lab", "h.bbox") are current

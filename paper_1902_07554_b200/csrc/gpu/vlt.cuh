@@ -691,14 +691,16 @@ __global__ void __launch_bounds__(128, 8) k_assign_overflow(const double* __rest
                                                          const VltEntry* __restrict__ lslab,
                                                          std::uint32_t* __restrict__ labels,
                                                          const std::uint32_t* __restrict__ oq,
-                                                         const unsigned* __restrict__ oq_count) {
+                                                         const unsigned* __restrict__ oq_count,
+                                                         unsigned* __restrict__ next, unsigned* __restrict__ fin) {
   __shared__ SampleGrid<D> sg;
   if (threadIdx.x == 0) sg = *sgp;
   __syncthreads();
   const unsigned lane = threadIdx.x & 31u;
   const unsigned cnt = *oq_count;
-  const unsigned warps = gridDim.x * (blockDim.x >> 5);
-  for (unsigned q0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32u; q0 < cnt; q0 += warps * 32u) {
+  for (;;) {
+    const unsigned q0 = claim_batch(next);
+    if (q0 >= cnt) break;
     const unsigned q = q0 + lane;
     const bool has = q < cnt;
     std::uint32_t i = 0, head = kHeadOverflow;
@@ -786,6 +788,7 @@ __global__ void __launch_bounds__(128, 8) k_assign_overflow(const double* __rest
       labels[i] = lab;
     }
   }
+  rewind_cursor(next, fin, cnt);
 }
 
 __global__ void k_sorted_labels(const SampleRec* __restrict__ sorted, std::uint32_t m, std::uint32_t* __restrict__ out) {
