@@ -568,13 +568,15 @@ __device__ __forceinline__ void load_simplex(const BorderArgs& a, const std::uin
 // its 3^D or its 5^D neighbourhood) whose combined code is EMPTY or self.
 // Positive: the INNER ball (inside the binary64 sphere, checked in binary64)
 // reaches the cell of its centre and that cell holds another part.
-// kWindow: run the negative (window) test; kNbrs: also try the neighbours of
-// the centre cell for the positive proof (the exact stage, where every lane
-// holds an undecided row, so the extra lookups do not diverge the warp).
-template <int D, bool kWindow, bool kNbrs>
+// For an undecided row (2) the cell-unit centre U and the inner ball's reach
+// are stored in out_U / out_reach (reach < 0: no positive proof possible) for
+// the exact stage's neighbour test (octant_proof), where every lane holds an
+// undecided row, so the extra lookups do not diverge the warp.
+template <int D>
 __device__ __forceinline__ int prefilter_decide(const OwnerGrid<D>& og, const BorderArgs& a, const Sphere32<D>& sp,
                                                 std::uint32_t self, float inv_e, float margin_c, float lo_mag,
-                                                bool pos_ok) {
+                                                bool pos_ok, float* out_U, float* out_reach) {
+  if (out_reach) *out_reach = -1.f;
   // R >= radius of the inflated binary64 sphere + distance between centres
   float slack = 0.f;
 #pragma unroll
@@ -604,8 +606,8 @@ __device__ __forceinline__ int prefilter_decide(const OwnerGrid<D>& og, const Bo
     inside = inside && ic >= 0 && ic <= og.ldims[0][d] - 1;
     c0[d] = ic;
   }
-  if (outside) return kWindow ? 0 : 2;  // the range misses the grid on some axis: no cell is reachable
-  if (kWindow && w <= 4) {
+  if (outside) return 0;  // the range misses the grid on some axis: no cell is reachable
+  if (w <= 4) {
     const int h = w == 0 ? 0 : (w <= 2 ? 1 : 2);
     int cm[D];
 #pragma unroll
@@ -630,15 +632,30 @@ __device__ __forceinline__ int prefilter_decide(const OwnerGrid<D>& og, const Bo
     const std::uint16_t code = a.owner[og_index<D>(og, 0, c0)];
     if (code != kOwnerEmpty && code != self) return 1;
   }
-  if constexpr (!kNbrs) return 2;
-  // the neighbours on the near side of Uc in each axis (the 2^D - 1 cells of
-  // the octant Uc lies in; the far ones are at least half a cell further)
+  if (out_reach) {
+    *out_reach = reach;
+#pragma unroll
+    for (int d = 0; d < D; ++d) out_U[d] = Ucs[d];
+  }
+  return 2;
+}
+
+// The neighbours of the centre cell c0 = floor(U) on the near side of U in
+// each axis (the 2^D - 1 cells of the octant U lies in; the far ones are at
+// least half a cell further): positive if one holds another part and its box
+// is within `reach` (cell units, all error slack already subtracted, see
+// prefilter_decide) of U.
+template <int D>
+__device__ __forceinline__ bool octant_proof(const OwnerGrid<D>& og, const BorderArgs& a, const float* U, float reach,
+                                             std::uint32_t self) {
+  if (!(reach > 0.f)) return false;
   const float reach2 = reach * reach;
-  int side[D];
+  int c0[D], side[D];
   float gap[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) {
-    const float f = Ucs[d] - static_cast<float>(c0[d]);
+    c0[d] = floor_small(U[d]);  // U lies in the grid (checked when reach was recorded)
+    const float f = U[d] - static_cast<float>(c0[d]);
     side[d] = f < 0.5f ? -1 : 1;
     gap[d] = f < 0.5f ? f : 1.f - f;
   }
@@ -656,33 +673,9 @@ __device__ __forceinline__ int prefilter_decide(const OwnerGrid<D>& og, const Bo
     }
     if (!ok || !(d2 * 1.000002f + 1e-12f < reach2)) continue;
     const std::uint16_t code = a.owner[og_index<D>(og, 0, cn)];
-    if (code != kOwnerEmpty && code != self) return 1;
+    if (code != kOwnerEmpty && code != self) return true;
   }
-  return 2;
-}
-
-// Per-launch constants of the binary32 decisions (cell-unit scale, margins,
-// fixed-point step), rounded up where they bound an error.
-struct PfConsts {
-  float inv_e, margin_c, lo_mag, qh_f, qh_err;
-  bool pos_ok;
-};
-
-template <int D>
-__device__ __forceinline__ PfConsts pf_consts(const OwnerGrid<D>& og) {
-  PfConsts k;
-  k.inv_e = static_cast<float>(og.inv_edge);
-  k.margin_c = static_cast<float>(og.margin * og.inv_edge) * 1.0001f + 1e-30f;
-  k.lo_mag = 0.f;
-  k.pos_ok = true;
-#pragma unroll
-  for (int d = 0; d < D; ++d) {
-    k.lo_mag = fmaxf(k.lo_mag, static_cast<float>(fabs(og.g.lo[d])) * 1.0001f);
-    k.pos_ok = k.pos_ok && fabs(og.g.lo[d]) * og.inv_edge + static_cast<double>(og.ldims[0][d]) < 67108864.0;
-  }
-  k.qh_f = static_cast<float>(og.qh);
-  k.qh_err = static_cast<float>(og.qh) * 0.50011f;
-  return k;
+  return false;
 }
 
 template <int D>
@@ -735,6 +728,7 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
     }
     const bool inf = valid && v[D] == kInfVertex;
     bool is_cand = false;
+    float cU[D], creach = -1.f;  // recorded for the exact stage's neighbour test
     // rows only grow along the grid-stride loop: advance the part cursor
     {
       const std::uint64_t sc = valid ? s : row_end - 1;
@@ -746,7 +740,7 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
       Sphere32<D> sp;
       decode_row<D>(a.xq, v, qh_f, qh_err, A, sp.P0, P0e, &eta);
       const int res = enclosing_sphere_f32<D>(A, eta, P0e, sp)
-                          ? prefilter_decide<D, true, false>(og, a, sp, self, inv_e, margin_c, lo_mag, pos_ok)
+                          ? prefilter_decide<D>(og, a, sp, self, inv_e, margin_c, lo_mag, pos_ok, cU, &creach)
                           : 2;
       if (a.counters && res == 1) atomicAdd(&a.counters[8], 1ull);
       if (res == 2) {
@@ -773,6 +767,9 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
       cand[q] = static_cast<std::uint32_t>(s);
 #pragma unroll
       for (int j = 0; j <= D; ++j) cand[std::uint64_t(j + 1) * cap + q] = v[j];
+#pragma unroll
+      for (int d = 0; d < D; ++d) cand[std::uint64_t(D + 2 + d) * cap + q] = __float_as_uint(creach > 0.f ? cU[d] : 0.f);
+      cand[std::uint64_t(2 * D + 2) * cap + q] = __float_as_uint(creach);
     }
     if (inf) a.inf_queue[bi + __popc(mi & lt)] = static_cast<std::uint32_t>(s);
   }
@@ -828,7 +825,6 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
   const unsigned lane = threadIdx.x & 31u;
   const unsigned wid = threadIdx.x >> 5;
   CandSlot<D>* sl = slots[wid];
-  const PfConsts pf = pf_consts<D>(og);
   const bool multi_level = og.levels > 1;
   unsigned long long bst[D];  // level-1 block strides of the tiled level-0 index
   bst[0] = 1;
@@ -854,13 +850,14 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
       for (int j = 0; j <= D; ++j) v[j] = cand[std::uint64_t(j + 1) * cap + t];
       bool proven = false;
       if constexpr (!Ex) {
-        // binary32 positive proof over the centre cell's neighbourhood (the
-        // prefilter tried the centre cell only)
-        float A32[D][D], P0e[D], eta;
-        Sphere32<D> sp;
-        decode_row<D>(a.xq, v, pf.qh_f, pf.qh_err, A32, sp.P0, P0e, &eta);
-        proven = enclosing_sphere_f32<D>(A32, eta, P0e, sp) &&
-                 prefilter_decide<D, false, true>(og, a, sp, self, pf.inv_e, pf.margin_c, pf.lo_mag, pf.pos_ok) == 1;
+        // binary32 positive proof over the centre cell's near-octant
+        // neighbours (the prefilter tried the centre cell and recorded the
+        // cell-unit centre and the inner ball's reach)
+        float U[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) U[d] = __uint_as_float(cand[std::uint64_t(D + 2 + d) * cap + t]);
+        const float reach = __uint_as_float(cand[std::uint64_t(2 * D + 2) * cap + t]);
+        proven = octant_proof<D>(og, a, U, reach, self);
       }
       if (proven) {
         mode = 0;
@@ -1680,7 +1677,7 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
     {
       if (tiled && in->S > 0) {
         const std::uint64_t qcap = in->S + 32;
-        SBDT_WS(cq, std::uint32_t, "border.cand", qcap * (D + 2));
+        SBDT_WS(cq, std::uint32_t, "border.cand", qcap * (2 * D + 3));  // {row, vertices, U, reach}
         // {candidates, cursor, wide rows, wide cursor, CTAs done (exact), CTAs done (wide)}
         SBDT_WS(cn, unsigned, "border.cand_n", 6);
         SBDT_CUDA_TRY(cudaMemsetAsync(cn, 0, 6 * sizeof(unsigned), st));
