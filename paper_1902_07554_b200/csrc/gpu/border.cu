@@ -767,9 +767,10 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
       cand[q] = static_cast<std::uint32_t>(s);
 #pragma unroll
       for (int j = 0; j <= D; ++j) cand[std::uint64_t(j + 1) * cap + q] = v[j];
-#pragma unroll
-      for (int d = 0; d < D; ++d) cand[std::uint64_t(D + 2 + d) * cap + q] = __float_as_uint(creach > 0.f ? cU[d] : 0.f);
       cand[std::uint64_t(2 * D + 2) * cap + q] = __float_as_uint(creach);
+      if (creach > 0.f)
+#pragma unroll
+        for (int d = 0; d < D; ++d) cand[std::uint64_t(D + 2 + d) * cap + q] = __float_as_uint(cU[d]);
     }
     if (inf) a.inf_queue[bi + __popc(mi & lt)] = static_cast<std::uint32_t>(s);
   }
@@ -853,11 +854,13 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
         // binary32 positive proof over the centre cell's near-octant
         // neighbours (the prefilter tried the centre cell and recorded the
         // cell-unit centre and the inner ball's reach)
-        float U[D];
-#pragma unroll
-        for (int d = 0; d < D; ++d) U[d] = __uint_as_float(cand[std::uint64_t(D + 2 + d) * cap + t]);
         const float reach = __uint_as_float(cand[std::uint64_t(2 * D + 2) * cap + t]);
-        proven = octant_proof<D>(og, a, U, reach, self);
+        if (reach > 0.f) {
+          float U[D];
+#pragma unroll
+          for (int d = 0; d < D; ++d) U[d] = __uint_as_float(cand[std::uint64_t(D + 2 + d) * cap + t]);
+          proven = octant_proof<D>(og, a, U, reach, self);
+        }
       }
       if (proven) {
         mode = 0;
