@@ -6,6 +6,9 @@
  *       (Alg. 2 lines "find nearest
  *       sample point" / "assign p to v_n's partition") and the
  *       Partitioning.parts bucketing.
+ *   sbdt_gpu_merge*          replaces  dc-engine `merge` + `update_neighbors`
+ *       (Alg. 1 merging / neighbourhood blocks), the
+ *       step after the border triangulation.
  *   sbdt_gpu_find_border*    replaces  dc-engine `find_border` with the
  *       border-geom `GridIndex` / `intersects_{bbox,grid}` queries
  *       (Alg. 1 border block) on the
@@ -43,7 +46,10 @@ enum sbdt_status {
   SBDT_ERR_DEGENERATE = 2, /* sbdt::DegenerateSimplex (geometry.cpp:281) */
   SBDT_ERR_CUDA = 3,       /* std::runtime_error                        */
   SBDT_ERR_OOM = 4,        /* std::bad_alloc                            */
-  SBDT_ERR_RANGE = 5       /* grid larger than 4 n / c_G^D cells         */
+  SBDT_ERR_RANGE = 5,      /* grid larger than 4 n / c_G^D cells; output
+                              capacity too small (merge)                 */
+  SBDT_ERR_MERGE = 6       /* sbdt InconsistentMerge / DanglingFacet
+                                                      */
 };
 
 /* IntersectionPolicy::Kind */
@@ -176,6 +182,61 @@ typedef struct sbdt_border_args {
 } sbdt_border_args;
 
 int sbdt_gpu_find_border_dev(sbdt_gpu_ctx* ctx, const sbdt_border_args* args);
+
+/* ---- merge + update_neighbors --------------------------
+ * Inputs: the k partial triangulations (layout of sbdt_gpu_find_border), the
+ * border flags B (border[s] != 0: row s is a border simplex — find_border's
+ * border_out or positive_out), the border triangulation T_B over B's vertices
+ * (tb_verts / tb_nbrs (dim+1) x S_B vertex-major, T_B-local neighbour ids,
+ * tb_parity) and labels[i], the partition of point i.
+ * Result (SPEC merge): the finite partial rows not in B, then the finite T_B
+ * rows whose vertices span >= 2 partitions or whose vertex tuple is a finite
+ * row of B, each group in row order; neighbour links rebuilt over the merged
+ * set (update_neighbors); facets with a single finite owner are hull facets:
+ * kNone (0xFFFFFFFF) links, or, with SBDT_MERGE_HULL, one infinite row per
+ * hull facet appended in (owner row, facet) order ({facet ids, 0xFFFFFFFF},
+ * parity 0, neighbours[dim] = owner), linked among themselves through their
+ * ridges — the reference's Triangulation layout.
+ * out_offsets (k+3): rows of part p are [out_offsets[p], out_offsets[p+1]),
+ * the inserted T_B rows [out_offsets[k], out_offsets[k+1]), the hull rows
+ * [out_offsets[k+1], out_offsets[k+2]).
+ * Errors: SBDT_ERR_MERGE (a facet with three owners = InconsistentMerge; a
+ * hull ridge without two hull facets = DanglingFacet); SBDT_ERR_RANGE when the
+ * result exceeds `capacity` rows (*rows_out then holds the rows needed, or a
+ * lower bound of them). Synchronizes the context stream (table sizing). */
+enum sbdt_merge_flags { SBDT_MERGE_HULL = 1u };
+
+typedef struct sbdt_merge_args {
+  int dim;
+  uint32_t k;
+  const uint32_t* d_labels;   /* n */
+  uint64_t n;
+  const uint64_t* d_offsets;  /* k+1 */
+  const uint32_t* d_verts;    /* (dim+1) x S */
+  const uint32_t* d_nbrs;     /* (dim+1) x S, part-local */
+  const int8_t* d_parity;     /* S */
+  uint64_t S;
+  const uint8_t* d_border;    /* S */
+  const uint32_t* d_tb_verts; /* (dim+1) x S_B */
+  const uint32_t* d_tb_nbrs;  /* (dim+1) x S_B */
+  const int8_t* d_tb_parity;  /* S_B */
+  uint64_t S_B;
+  uint32_t flags;             /* sbdt_merge_flags */
+} sbdt_merge_args;
+
+/* Device outputs, vertex-major with row stride `capacity`. */
+int sbdt_gpu_merge_dev(sbdt_gpu_ctx* ctx, const sbdt_merge_args* args, uint64_t capacity, uint32_t* d_out_verts,
+                       uint32_t* d_out_nbrs, int8_t* d_out_parity, uint64_t* d_out_offsets, uint64_t* rows_out);
+
+/* Host buffers; outputs vertex-major with row stride *rows_out (compact):
+ * out_verts[j * rows + s]. Each out array holds (dim+1) * capacity entries
+ * (out_parity: capacity). */
+int sbdt_gpu_merge(sbdt_gpu_ctx* ctx, int dim, const uint32_t* labels, uint64_t n, uint32_t k,
+                   const uint64_t* offsets, const uint32_t* verts, const uint32_t* nbrs, const int8_t* parity,
+                   const uint8_t* border, const uint32_t* tb_verts, const uint32_t* tb_nbrs,
+                   const int8_t* tb_parity, uint64_t S_B, uint32_t flags, uint64_t capacity,
+                   uint32_t* out_verts, uint32_t* out_nbrs, int8_t* out_parity, uint64_t* out_offsets,
+                   uint64_t* rows_out);
 
 #ifdef __cplusplus
 }

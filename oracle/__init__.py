@@ -6,7 +6,8 @@ path: the product (paper_1902_07554_b200, libsbdt_gpu.so) does not load it.
 
 liboracle.so  : restatement of SPEC.md assign_points (kd-tree + brute force),
                 GridIndex / intersects_* and find_border (oracle/path.hpp) on
-                restated primitives (oracle/prims.hpp).
+                restated primitives (oracle/prims.hpp); merge +
+                update_neighbors (oracle/merge.hpp).
 _ref/libsbdt_ref.so : the same path templates instantiated on the reference's
                 own geometry.cpp / triangulation.cpp / sequential_dt.cpp
                 (compiled by path in this container; pins the restatement).
@@ -47,6 +48,13 @@ def lib():
         L.oracle_time_border.argtypes = [C.c_int, dp, u64, u32p, C.c_uint32, C.POINTER(C.c_uint64), u32p, u32p, i8p,
                                          C.c_int, C.c_double, C.c_int, C.c_uint32, C.c_uint32, C.c_int, dp, dp,
                                          C.POINTER(C.c_uint64)]
+        L.oracle_merge.restype = C.c_void_p
+        L.oracle_merge.argtypes = [C.c_int, C.c_uint32, C.POINTER(C.c_uint64), u32p, u32p, i8p, u8p, u32p, u32p, i8p,
+                                   u64, u32p, C.c_int, C.c_char_p, C.c_int]
+        L.oracle_merge_rows.restype = u64
+        L.oracle_merge_rows.argtypes = [C.c_void_p]
+        L.oracle_merge_export.argtypes = [C.c_void_p, u32p, u32p, i8p, C.POINTER(C.c_uint64)]
+        L.oracle_merge_free.argtypes = [C.c_void_p]
         L.oracle_orient.argtypes = [C.c_int, dp]
         L.oracle_in_sphere.argtypes = [C.c_int, dp, dp]
         L.oracle_circumsphere.argtypes = [C.c_int, dp, dp]
@@ -156,3 +164,32 @@ def time_border(points, labels, partials, policy="grid", c_G=1.0, threads=8, par
                              _p(partials.nbrs, C.c_uint32), _p(partials.parity, C.c_int8), POLICY[policy], c_G,
                              threads, parts[0], parts[1] or partials.k, reps, C.byref(tb), C.byref(tr), C.byref(nv))
     return tb.value, tr.value, nv.value
+
+
+def merge(partials, border, tb, labels, hull=True):
+    """SPEC.md:497-514 merge + update_neighbors (oracle/merge.hpp). `border`:
+    per partial row, nonzero = border simplex; `tb`: the border triangulation
+    (verts/nbrs (D+1, S_B), parity). Returns (verts, nbrs, parity, offsets)."""
+    dim = partials.verts.shape[0] - 1
+    bor = np.ascontiguousarray(border, np.uint8)
+    lab = np.ascontiguousarray(labels, np.uint32)
+    tv = np.ascontiguousarray(tb.verts, np.uint32)
+    tn = np.ascontiguousarray(tb.nbrs, np.uint32)
+    tp = np.ascontiguousarray(tb.parity, np.int8)
+    err = C.create_string_buffer(256)
+    h = lib().oracle_merge(dim, partials.k, _p(partials.offsets, C.c_uint64), _p(partials.verts, C.c_uint32),
+                           _p(partials.nbrs, C.c_uint32), _p(partials.parity, C.c_int8), _p(bor, C.c_uint8),
+                           _p(tv, C.c_uint32), _p(tn, C.c_uint32), _p(tp, C.c_int8), tv.shape[1],
+                           _p(lab, C.c_uint32), int(hull), err, 256)
+    if not h:
+        raise RuntimeError("oracle_merge: " + err.value.decode())
+    try:
+        R = lib().oracle_merge_rows(h)
+        v = np.empty((dim + 1, R), np.uint32)
+        nb = np.empty((dim + 1, R), np.uint32)
+        par = np.empty(R, np.int8)
+        off = np.empty(partials.k + 3, np.uint64)
+        lib().oracle_merge_export(h, _p(v, C.c_uint32), _p(nb, C.c_uint32), _p(par, C.c_int8), _p(off, C.c_uint64))
+    finally:
+        lib().oracle_merge_free(h)
+    return v, nb, par, off

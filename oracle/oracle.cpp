@@ -7,6 +7,7 @@
 #include <cstring>
 #include <exception>
 
+#include "merge.hpp"
 #include "path.hpp"
 
 using namespace sbdt_oracle;
@@ -194,5 +195,37 @@ int oracle_halfspace_box(int dim, const double* facet, const double* inner, cons
   const double* f[3] = {facet, facet + 3, facet + 6};
   return halfspace_box_overlap<3>(f, inner, Box<3>{{lo[0], lo[1], lo[2]}, {hi[0], hi[1], hi[2]}});
 }
+
+// merge + update_neighbors (oracle/merge.hpp). Returns a handle (nullptr on
+// error, message in err); rows / export / free below.
+void* oracle_merge(int dim, std::uint32_t k, const std::uint64_t* offsets, const std::uint32_t* verts,
+                   const std::uint32_t* nbrs, const std::int8_t* parity, const std::uint8_t* border,
+                   const std::uint32_t* tb_verts, const std::uint32_t* tb_nbrs, const std::int8_t* tb_parity,
+                   std::uint64_t SB, const std::uint32_t* labels, int hull, char* err, int errlen) {
+  try {
+    MergeOut r = dim == 2 ? merge_oracle<2>(k, offsets, verts, nbrs, parity, border, tb_verts, tb_nbrs, tb_parity,
+                                            SB, labels, hull != 0)
+                          : merge_oracle<3>(k, offsets, verts, nbrs, parity, border, tb_verts, tb_nbrs, tb_parity,
+                                            SB, labels, hull != 0);
+    if (!r.error.empty()) {
+      if (err && errlen > 0) std::snprintf(err, errlen, "%s", r.error.c_str());
+      return nullptr;
+    }
+    return new MergeOut(std::move(r));
+  } catch (const std::exception& e) {
+    if (err && errlen > 0) std::snprintf(err, errlen, "%s", e.what());
+    return nullptr;
+  }
+}
+std::uint64_t oracle_merge_rows(void* h) { return static_cast<MergeOut*>(h)->rows; }
+void oracle_merge_export(void* h, std::uint32_t* verts, std::uint32_t* nbrs, std::int8_t* parity,
+                         std::uint64_t* offsets) {
+  const MergeOut* r = static_cast<MergeOut*>(h);
+  std::memcpy(verts, r->verts.data(), r->verts.size() * 4);
+  std::memcpy(nbrs, r->nbrs.data(), r->nbrs.size() * 4);
+  std::memcpy(parity, r->parity.data(), r->parity.size());
+  std::memcpy(offsets, r->offsets.data(), r->offsets.size() * 8);
+}
+void oracle_merge_free(void* h) { delete static_cast<MergeOut*>(h); }
 
 }  // extern "C"

@@ -20,6 +20,9 @@ template <int D>
 int border_impl(sbdt_gpu_ctx*, const sbdt_border_args*);
 int reach_impl(sbdt_gpu_ctx*, const sbdt_border_args*);
 int assign_stats(sbdt_gpu_ctx*, unsigned*);
+template <int D>
+int merge_impl(sbdt_gpu_ctx*, const sbdt_merge_args*, std::uint64_t, std::uint32_t*, std::uint32_t*, std::int8_t*,
+               std::uint64_t*, std::uint64_t*);
 }  // namespace sbdt_gpu
 
 using namespace sbdt_gpu;
@@ -177,6 +180,8 @@ int sbdt_gpu_check_status(sbdt_gpu_ctx* ctx) {
   if (st & kStDegenerate) return fail(ctx, SBDT_ERR_DEGENERATE, "degenerate simplex (parity 0) in a partial triangulation");
   if (st & kStGridCap) return fail(ctx, SBDT_ERR_RANGE, "grid index would exceed 4 n / c_G^D cells (degenerate bbox?)");
   if (st & kStQueueOverflow) return fail(ctx, SBDT_ERR_RANGE, "escalation queue overflow");
+  if (st & 8u) return fail(ctx, SBDT_ERR_MERGE, "InconsistentMerge: a facet with more than two finite owners");
+  if (st & 16u) return fail(ctx, SBDT_ERR_MERGE, "DanglingFacet: a hull ridge without exactly two hull facets");
   return SBDT_OK;
 }
 
@@ -448,6 +453,118 @@ int sbdt_gpu_find_border(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint6
     if (n_bfs_vertices_out) *n_bfs_vertices_out = nb;
   }
   return SBDT_OK;
+}
+
+namespace {
+int merge_checks(sbdt_gpu_ctx* ctx, const sbdt_merge_args* a, uint64_t capacity, const void* ov, const void* on,
+                 const void* op, const void* oo, uint64_t* rows_out) {
+  if (!a || !ov || !on || !op || !oo || !rows_out) return fail(ctx, SBDT_ERR_INVALID, "merge: null argument");
+  if (a->dim != 2 && a->dim != 3) return fail(ctx, SBDT_ERR_INVALID, "dim must be 2 or 3");
+  if (a->k == 0) return fail(ctx, SBDT_ERR_INVALID, "merge: k must be >= 1");
+  if ((a->S && (!a->d_verts || !a->d_nbrs || !a->d_parity || !a->d_border)) ||
+      (a->S_B && (!a->d_tb_verts || !a->d_tb_nbrs || !a->d_tb_parity || !a->d_labels)) || !a->d_offsets)
+    return fail(ctx, SBDT_ERR_INVALID, "merge: null input array");
+  if (a->S > 0xFFFFFFFFull || a->S_B > 0xFFFFFFFFull || capacity > 0xFFFFFFFFull)
+    return fail(ctx, SBDT_ERR_INVALID, "merge: more than 2^32 rows");
+  return kOk;
+}
+}  // namespace
+
+int sbdt_gpu_merge_dev(sbdt_gpu_ctx* ctx, const sbdt_merge_args* args, uint64_t capacity, uint32_t* d_out_verts,
+                       uint32_t* d_out_nbrs, int8_t* d_out_parity, uint64_t* d_out_offsets, uint64_t* rows_out) {
+  if (!ctx) return SBDT_ERR_INVALID;
+  TRY(merge_checks(ctx, args, capacity, d_out_verts, d_out_nbrs, d_out_parity, d_out_offsets, rows_out));
+  *rows_out = 0;
+  const int rc = args->dim == 2 ? merge_impl<2>(ctx, args, capacity, d_out_verts, d_out_nbrs, d_out_parity,
+                                                d_out_offsets, rows_out)
+                                : merge_impl<3>(ctx, args, capacity, d_out_verts, d_out_nbrs, d_out_parity,
+                                                d_out_offsets, rows_out);
+  if (rc != kOk) return rc;
+  return finish(ctx);
+}
+
+int sbdt_gpu_merge(sbdt_gpu_ctx* ctx, int dim, const uint32_t* labels, uint64_t n, uint32_t k,
+                   const uint64_t* offsets, const uint32_t* verts, const uint32_t* nbrs, const int8_t* parity,
+                   const uint8_t* border, const uint32_t* tb_verts, const uint32_t* tb_nbrs,
+                   const int8_t* tb_parity, uint64_t S_B, uint32_t flags, uint64_t capacity,
+                   uint32_t* out_verts, uint32_t* out_nbrs, int8_t* out_parity, uint64_t* out_offsets,
+                   uint64_t* rows_out) {
+  if (!ctx) return SBDT_ERR_INVALID;
+  if (!offsets || k == 0) return fail(ctx, SBDT_ERR_INVALID, "merge: offsets / k");
+  sbdt_merge_args a{};
+  a.dim = dim;
+  a.k = k;
+  a.n = n;
+  a.S = offsets[k];
+  a.S_B = S_B;
+  a.flags = flags;
+  // host pointers stand in for the checks; replaced by device copies below
+  a.d_labels = labels;
+  a.d_offsets = offsets;
+  a.d_verts = verts;
+  a.d_nbrs = nbrs;
+  a.d_parity = parity;
+  a.d_border = border;
+  a.d_tb_verts = tb_verts;
+  a.d_tb_nbrs = tb_nbrs;
+  a.d_tb_parity = tb_parity;
+  TRY(merge_checks(ctx, &a, capacity, out_verts, out_nbrs, out_parity, out_offsets, rows_out));
+  *rows_out = 0;
+  const uint64_t S = a.S, D1 = dim + 1;
+  uint32_t *d_lab, *d_verts, *d_nbrs, *d_tbv, *d_tbn, *d_ov, *d_on;
+  uint64_t *d_off, *d_oo;
+  int8_t *d_par, *d_tbp, *d_op;
+  uint8_t* d_bor;
+  TRY(dalloc(ctx, "m.lab", n, &d_lab));
+  TRY(dalloc(ctx, "m.off", k + 1, &d_off));
+  TRY(dalloc(ctx, "m.verts", S * D1, &d_verts));
+  TRY(dalloc(ctx, "m.nbrs", S * D1, &d_nbrs));
+  TRY(dalloc(ctx, "m.par", S, &d_par));
+  TRY(dalloc(ctx, "m.bor", S, &d_bor));
+  TRY(dalloc(ctx, "m.tbv", S_B * D1, &d_tbv));
+  TRY(dalloc(ctx, "m.tbn", S_B * D1, &d_tbn));
+  TRY(dalloc(ctx, "m.tbp", S_B, &d_tbp));
+  TRY(dalloc(ctx, "m.ov", capacity * D1, &d_ov));
+  TRY(dalloc(ctx, "m.on", capacity * D1, &d_on));
+  TRY(dalloc(ctx, "m.op", capacity, &d_op));
+  TRY(dalloc(ctx, "m.oo", k + 3, &d_oo));
+  cudaStream_t st = ctx->stream;
+  auto up = [&](void* d, const void* h, std::size_t bytes) {
+    return bytes ? cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st) : cudaSuccess;
+  };
+  SBDT_CUDA_TRY(up(d_off, offsets, 8 * (k + 1)));
+  SBDT_CUDA_TRY(up(d_verts, verts, 4 * S * D1));
+  SBDT_CUDA_TRY(up(d_nbrs, nbrs, 4 * S * D1));
+  SBDT_CUDA_TRY(up(d_par, parity, S));
+  SBDT_CUDA_TRY(up(d_bor, border, S));
+  if (S_B) {
+    SBDT_CUDA_TRY(up(d_lab, labels, 4 * n));
+    SBDT_CUDA_TRY(up(d_tbv, tb_verts, 4 * S_B * D1));
+    SBDT_CUDA_TRY(up(d_tbn, tb_nbrs, 4 * S_B * D1));
+    SBDT_CUDA_TRY(up(d_tbp, tb_parity, S_B));
+  }
+  a.d_labels = d_lab;
+  a.d_offsets = d_off;
+  a.d_verts = d_verts;
+  a.d_nbrs = d_nbrs;
+  a.d_parity = d_par;
+  a.d_border = d_bor;
+  a.d_tb_verts = d_tbv;
+  a.d_tb_nbrs = d_tbn;
+  a.d_tb_parity = d_tbp;
+  uint64_t rows = 0;
+  const int rc = dim == 2 ? merge_impl<2>(ctx, &a, capacity, d_ov, d_on, d_op, d_oo, &rows)
+                          : merge_impl<3>(ctx, &a, capacity, d_ov, d_on, d_op, d_oo, &rows);
+  *rows_out = rows;
+  if (rc != kOk) return rc;
+  TRY(sbdt_gpu_check_status(ctx));
+  for (uint64_t j = 0; j < D1 && rows; ++j) {
+    SBDT_CUDA_TRY(cudaMemcpyAsync(out_verts + j * rows, d_ov + j * capacity, 4 * rows, cudaMemcpyDeviceToHost, st));
+    SBDT_CUDA_TRY(cudaMemcpyAsync(out_nbrs + j * rows, d_on + j * capacity, 4 * rows, cudaMemcpyDeviceToHost, st));
+  }
+  if (rows) SBDT_CUDA_TRY(cudaMemcpyAsync(out_parity, d_op, rows, cudaMemcpyDeviceToHost, st));
+  SBDT_CUDA_TRY(cudaMemcpyAsync(out_offsets, d_oo, 8 * (k + 3), cudaMemcpyDeviceToHost, st));
+  return finish(ctx);
 }
 
 }  // extern "C"

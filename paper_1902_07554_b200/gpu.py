@@ -5,6 +5,7 @@ Names and argument meaning follow SPEC.md's operations:
   assign_points(P, sample_ids, sample_labels, k) -> Partitioning
   find_border(P, labels, partials, policy)        -> BorderSet
   IntersectionPolicy(kind, c_G)                                     SPEC.md:403-406
+  merge(partials, border, T_B, labels)            -> Triangulation  SPEC.md:497-514 (+ update_neighbors)
 Errors map like the reference's exceptions (common.hpp:22-65). There is no
 CPU fallback: a missing library or device raises.
 """
@@ -19,7 +20,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _lib = None
 
-SBDT_OK, SBDT_ERR_INVALID, SBDT_ERR_DEGENERATE, SBDT_ERR_CUDA, SBDT_ERR_OOM, SBDT_ERR_RANGE = range(6)
+SBDT_OK, SBDT_ERR_INVALID, SBDT_ERR_DEGENERATE, SBDT_ERR_CUDA, SBDT_ERR_OOM, SBDT_ERR_RANGE, SBDT_ERR_MERGE = range(7)
+MERGE_HULL = 1
 POLICY = {"bbox": 0, "grid": 1, "exact": 2}
 RESIDENT_POINTS = 2
 HULL_BFS = 1
@@ -31,6 +33,10 @@ class DegenerateSimplex(RuntimeError):
 
 class SbdtGpuError(RuntimeError):
     pass
+
+
+class InconsistentMerge(SbdtGpuError):
+    """dc-engine InconsistentMerge / DanglingFacet."""
 
 
 class BorderArgs(C.Structure):
@@ -84,6 +90,9 @@ def lib():
         L.sbdt_gpu_find_border.argtypes = [vp, C.c_int, dp, u64, u32p, u32, u64p, u32p, u32p, i8p, C.c_int, C.c_double,
                                            u32, u8p, u8p, u32p, u64p, u32p, u64p, dp]
         L.sbdt_gpu_find_border_dev.argtypes = [vp, C.POINTER(BorderArgs)]
+        L.sbdt_gpu_merge.argtypes = [vp, C.c_int, u32p, u64, u32, u64p, u32p, u32p, i8p, u8p, u32p, u32p, i8p, u64,
+                                     u32, u64, u32p, u32p, i8p, u64p, u64p]
+        L.sbdt_gpu_merge_dev.argtypes = [vp, vp, u64, vp, vp, vp, vp, u64p]
         L.sbdt_gpu_set_timing.argtypes = [vp, C.c_int]
         L.sbdt_gpu_stage_times.argtypes = [vp, C.c_char_p, C.c_int, C.POINTER(C.c_float), C.c_int]
         L.sbdt_gpu_assign_table_stats.argtypes = [vp, C.POINTER(C.c_uint)]
@@ -117,6 +126,8 @@ class Context:
             raise DegenerateSimplex(msg)
         if rc == SBDT_ERR_INVALID:
             raise ValueError(f"{what}: {msg}")
+        if rc == SBDT_ERR_MERGE:
+            raise InconsistentMerge(f"{what}: {msg}")
         raise SbdtGpuError(f"{what}: status {rc}: {msg}")
 
     def set_stream(self, stream_handle: int | None):
@@ -319,3 +330,55 @@ def find_border(points: np.ndarray, labels: np.ndarray, partials, policy: Inters
         return BorderSet(pos, bor, bvids[:nb.value] if hull_bfs else vids[:nv.value], vids[:nv.value], sph)
     return BorderSet(pos, bor, bvids[:nb.value].copy() if hull_bfs else vids[:nv.value].copy(),
                      vids[:nv.value].copy(), sph)
+
+
+@dataclass
+class Merged:
+    """The merged triangulation, vertex-major SoA like host.Tri.
+    offsets (k+3): rows of part p are [offsets[p], offsets[p+1]); the inserted
+    T_B rows [offsets[k], offsets[k+1]); the hull rows [offsets[k+1], offsets[k+2])."""
+    verts: np.ndarray   # (D+1, R) uint32
+    nbrs: np.ndarray    # (D+1, R) uint32
+    parity: np.ndarray  # (R,) int8
+    offsets: np.ndarray  # (k+3,) uint64
+
+
+def merge(partials, border: np.ndarray, tb, labels: np.ndarray, hull: bool = True,
+          ctx: Context | None = None) -> Merged:
+    """merge + update_neighbors through the host-buffer C ABI.
+    `border`: per partial row, nonzero = border simplex (BorderSet.border or
+    .positive); `tb`: the triangulation of the border vertices (host.Tri:
+    verts / nbrs (D+1, S_B), parity); `labels`: the partition of every point.
+    hull=True appends the re-derived infinite simplices (reference layout);
+    False leaves kNone links on the hull facets."""
+    ctx = ctx or default_context()
+    dim = partials.verts.shape[0] - 1
+    k, S = partials.k, partials.S
+    bor = np.ascontiguousarray(border, np.uint8)
+    if bor.shape != (S,):
+        raise ValueError("merge: border must hold one flag per partial row")
+    lab = np.ascontiguousarray(labels, np.uint32)
+    tv = np.ascontiguousarray(tb.verts, np.uint32)
+    tn = np.ascontiguousarray(tb.nbrs, np.uint32)
+    tp = np.ascontiguousarray(tb.parity, np.int8)
+    SB = tv.shape[1]
+    cap = S + SB + 64
+    for _ in range(3):
+        ov = np.empty((dim + 1) * cap, np.uint32)
+        on = np.empty((dim + 1) * cap, np.uint32)
+        op = np.empty(cap, np.int8)
+        oo = np.empty(k + 3, np.uint64)
+        rows = C.c_uint64(0)
+        rc = lib().sbdt_gpu_merge(ctx.handle, dim, _p(lab, C.c_uint32), len(lab), k, _p(partials.offsets, C.c_uint64),
+                                  _p(partials.verts, C.c_uint32), _p(partials.nbrs, C.c_uint32),
+                                  _p(partials.parity, C.c_int8), _p(bor, C.c_uint8), _p(tv, C.c_uint32),
+                                  _p(tn, C.c_uint32), _p(tp, C.c_int8), SB, MERGE_HULL if hull else 0, cap,
+                                  _p(ov, C.c_uint32), _p(on, C.c_uint32), _p(op, C.c_int8), _p(oo, C.c_uint64),
+                                  C.byref(rows))
+        if rc == SBDT_ERR_RANGE and rows.value > cap:
+            cap = int(rows.value) * 2 + 64
+            continue
+        ctx.check(rc, "merge")
+        R = int(rows.value)
+        return Merged(ov[:(dim + 1) * R].reshape(dim + 1, R), on[:(dim + 1) * R].reshape(dim + 1, R), op[:R], oo)
+    raise SbdtGpuError("merge: output capacity retry failed")
