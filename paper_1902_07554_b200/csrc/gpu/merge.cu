@@ -229,20 +229,21 @@ __device__ __forceinline__ void emit_row(const MergeDev& a, std::uint32_t o, con
   a.out_parity[o] = par;
 }
 
-// Join the facet opposite v[d] of output row o.
+// Join the facet opposite verts[d] of output row o (rows are published: the
+// join runs in a later launch than the emission).
 template <int D>
-__device__ __forceinline__ void join_facet(const MergeDev& a, std::uint32_t o, const std::uint32_t* v, int d) {
+__device__ __forceinline__ void join_facet(const MergeDev& a, std::uint32_t o, int d) {
   std::uint32_t f[D];
 #pragma unroll
   for (int j = 0, q = 0; j <= D; ++j)
-    if (j != d) f[q++] = v[j];
+    if (j != d) f[q++] = __ldg(a.out_verts + std::uint64_t(j) * a.ostride + o);
   const std::uint32_t partner = join_insert(
       a.join, a.join_mask, key_of<D>(f), o * (D + 1) + d, a.status, [&](std::uint32_t ov) {
         const std::uint32_t po = ov / (D + 1), pd = ov % (D + 1);
         bool eq = true;
 #pragma unroll
         for (int j = 0, q = 0; j <= D; ++j)
-          if (j != static_cast<int>(pd)) eq &= __ldcg(a.out_verts + std::uint64_t(j) * a.ostride + po) == f[q++];
+          if (j != static_cast<int>(pd)) eq &= __ldg(a.out_verts + std::uint64_t(j) * a.ostride + po) == f[q++];
         return eq;
       });
   if (partner != kNoneId) {
@@ -252,61 +253,158 @@ __device__ __forceinline__ void join_facet(const MergeDev& a, std::uint32_t o, c
   }
 }
 
-// K12 ------------------------------------------------------------------------
+// Warp-aggregated append of the facet handles in `bits` (row o) to a queue.
+// Every lane of the warp must call it.
 template <int D>
-__global__ void __launch_bounds__(kMergeThreads) k_merge_emit_partial(MergeDev a) {
-  const std::uint64_t s = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (s >= a.S || !bit_set(a, s >> 5, unsigned(s & 31))) return;
-  const std::uint32_t o = out_index(a, s >> 5, unsigned(s & 31));
-  std::uint32_t v[D + 1];
+__device__ __forceinline__ void queue_facets(unsigned* count, std::uint32_t* q, std::uint64_t cap, unsigned* status,
+                                             std::uint32_t o, unsigned bits) {
+  const unsigned lane = lane_id();
+  const unsigned c = __popc(bits);
+  unsigned incl = c;
 #pragma unroll
-  for (int j = 0; j <= D; ++j) v[j] = a.verts[std::uint64_t(j) * a.S + s];
-  emit_row<D>(a, o, v, a.parity[s]);
-  __threadfence();
-  // part of row s: upper bound in offsets
-  std::uint32_t lo = 0, hi = a.k;
-  while (hi - lo > 1) {
-    const std::uint32_t mid = (lo + hi) >> 1;
-    if (__ldg(a.offsets + mid) <= s) lo = mid;
-    else hi = mid;
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= static_cast<unsigned>(off)) incl += y;
   }
-  const std::uint64_t first = __ldg(a.offsets + lo);
-#pragma unroll
-  for (int d = 0; d <= D; ++d) {
-    const std::uint32_t nb = a.nbrs[std::uint64_t(d) * a.S + s];
-    if (nb != kNoneId) {
-      const std::uint64_t g = first + nb;
-      if (g < a.S && bit_set(a, g >> 5, unsigned(g & 31))) {
-        a.out_nbrs[std::uint64_t(d) * a.ostride + o] = out_index(a, g >> 5, unsigned(g & 31));
-        continue;
-      }
-    }
-    join_facet<D>(a, o, v, d);
+  const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+  if (!total) return;
+  unsigned base = 0;
+  if (lane == 31) base = atomicAdd(count, total);
+  base = __shfl_sync(0xffffffffu, base, 31);
+  std::uint64_t pos = std::uint64_t(base) + incl - c;
+  while (bits) {
+    const int d = __ffs(bits) - 1;
+    bits &= bits - 1;
+    if (pos < cap) q[pos] = o * (D + 1) + d;
+    else atomicOr(status, kStQueueOverflow);
+    ++pos;
   }
 }
 
+// K12 ------------------------------------------------------------------------
+// Emission: the row, its surviving links (relinked through the bitmaps) and
+// kNone + a queue entry for every other facet. Whole warps stay resident for
+// the queue append.
 template <int D>
-__global__ void __launch_bounds__(kMergeThreads) k_merge_emit_tb(MergeDev a) {
-  const std::uint64_t t = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= a.SB || !bit_set(a, a.WS + (t >> 5), unsigned(t & 31))) return;
-  const std::uint32_t o = out_index(a, a.WS + (t >> 5), unsigned(t & 31));
-  std::uint32_t v[D + 1];
+__global__ void __launch_bounds__(kMergeThreads) k_merge_emit_partial(MergeDev a, unsigned* qcount,
+                                                                      std::uint32_t* queue, std::uint64_t qcap) {
+  const std::uint64_t s = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool live = s < a.S && bit_set(a, s >> 5, unsigned(s & 31));
+  std::uint32_t o = 0;
+  unsigned jb = 0;
+  if (live) {
+    o = out_index(a, s >> 5, unsigned(s & 31));
+    std::uint32_t v[D + 1];
 #pragma unroll
-  for (int j = 0; j <= D; ++j) v[j] = a.tb_verts[std::uint64_t(j) * a.SB + t];
-  emit_row<D>(a, o, v, a.tb_parity[t]);
-  __threadfence();
-#pragma unroll
-  for (int d = 0; d <= D; ++d) {
-    const std::uint32_t nb = a.tb_nbrs[std::uint64_t(d) * a.SB + t];
-    if (nb != kNoneId && nb < a.SB && bit_set(a, a.WS + (nb >> 5), nb & 31u)) {
-      a.out_nbrs[std::uint64_t(d) * a.ostride + o] = out_index(a, a.WS + (nb >> 5), nb & 31u);
-      continue;
+    for (int j = 0; j <= D; ++j) v[j] = a.verts[std::uint64_t(j) * a.S + s];
+    emit_row<D>(a, o, v, a.parity[s]);
+    // part of row s: the last p with offsets[p] <= s
+    std::uint32_t lo = 0, hi = a.k;
+    while (hi - lo > 1) {
+      const std::uint32_t mid = (lo + hi) >> 1;
+      if (__ldg(a.offsets + mid) <= s) lo = mid;
+      else hi = mid;
     }
-    join_facet<D>(a, o, v, d);
+    const std::uint64_t first = __ldg(a.offsets + lo);
+#pragma unroll
+    for (int d = 0; d <= D; ++d) {
+      const std::uint32_t nb = a.nbrs[std::uint64_t(d) * a.S + s];
+      std::uint32_t link = kNoneId;
+      if (nb != kNoneId) {
+        const std::uint64_t g = first + nb;
+        if (g < a.S && bit_set(a, g >> 5, unsigned(g & 31))) link = out_index(a, g >> 5, unsigned(g & 31));
+      }
+      a.out_nbrs[std::uint64_t(d) * a.ostride + o] = link;
+      if (link == kNoneId) jb |= 1u << d;
+    }
   }
+  queue_facets<D>(qcount, queue, qcap, a.status, o, jb);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kMergeThreads) k_merge_emit_tb(MergeDev a, unsigned* qcount, std::uint32_t* queue,
+                                                                 std::uint64_t qcap) {
+  const std::uint64_t t = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool live = t < a.SB && bit_set(a, a.WS + (t >> 5), unsigned(t & 31));
+  std::uint32_t o = 0;
+  unsigned jb = 0;
+  if (live) {
+    o = out_index(a, a.WS + (t >> 5), unsigned(t & 31));
+    std::uint32_t v[D + 1];
+#pragma unroll
+    for (int j = 0; j <= D; ++j) v[j] = a.tb_verts[std::uint64_t(j) * a.SB + t];
+    emit_row<D>(a, o, v, a.tb_parity[t]);
+#pragma unroll
+    for (int d = 0; d <= D; ++d) {
+      const std::uint32_t nb = a.tb_nbrs[std::uint64_t(d) * a.SB + t];
+      std::uint32_t link = kNoneId;
+      if (nb != kNoneId && nb < a.SB && bit_set(a, a.WS + (nb >> 5), nb & 31u))
+        link = out_index(a, a.WS + (nb >> 5), nb & 31u);
+      a.out_nbrs[std::uint64_t(d) * a.ostride + o] = link;
+      if (link == kNoneId) jb |= 1u << d;
+    }
+  }
+  queue_facets<D>(qcount, queue, qcap, a.status, o, jb);
+}
+
+// The facet join over the queued facets (update_neighbors).
+template <int D>
+__global__ void __launch_bounds__(kMergeThreads) k_merge_join(MergeDev a, const std::uint32_t* queue,
+                                                              std::uint32_t J) {
+  const std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= J) return;
+  const std::uint32_t h = queue[i];
+  join_facet<D>(a, h / (D + 1), static_cast<int>(h % (D + 1)));
 }
 
 // K13 ------------------------------------------------------------------------
+// Hull facets = queued facets left without a partner.
+template <int D>
+__global__ void __launch_bounds__(kMergeThreads) k_merge_hull_collect(MergeDev a, const std::uint32_t* queue,
+                                                                      std::uint32_t J, unsigned* hcount,
+                                                                      std::uint32_t* hull, std::uint64_t hcap) {
+  const std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned bit = 0;
+  std::uint32_t h = 0;
+  if (i < J) {
+    h = queue[i];
+    bit = a.out_nbrs[std::uint64_t(h % (D + 1)) * a.ostride + h / (D + 1)] == kNoneId;
+  }
+  // one handle per lane: reuse the facet-queue append with row = h / (D+1)
+  queue_facets<D>(hcount, hull, hcap, a.status, h / (D + 1), bit << (h % (D + 1)));
+}
+
+// Single-CTA bitonic sort of up to kHullSortMax handles (ascending = (owner
+// row, facet) order).
+constexpr int kHullSortMax = 16384;
+constexpr int kSortThreads = 1024;
+__global__ void __launch_bounds__(kSortThreads) k_sort_small(std::uint32_t* data, std::uint32_t n) {
+  extern __shared__ std::uint32_t sm[];
+  std::uint32_t len = 2;
+  while (len < n) len <<= 1;
+  for (std::uint32_t i = threadIdx.x; i < len; i += kSortThreads) sm[i] = i < n ? data[i] : 0xFFFFFFFFu;
+  __syncthreads();
+  for (std::uint32_t k2 = 2; k2 <= len; k2 <<= 1) {
+    for (std::uint32_t j = k2 >> 1; j > 0; j >>= 1) {
+      for (std::uint32_t i = threadIdx.x; i < len; i += kSortThreads) {
+        const std::uint32_t l = i ^ j;
+        if (l > i) {
+          const bool up = (i & k2) == 0;
+          const std::uint32_t x = sm[i], y = sm[l];
+          if ((x > y) == up) {
+            sm[i] = y;
+            sm[l] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (std::uint32_t i = threadIdx.x; i < n; i += kSortThreads) data[i] = sm[i];
+}
+
+// Ordered hull list without the sort (many hull facets): per output row the
+// count of its kNone facets, scanned, then the handles written in order.
 template <int D>
 __global__ void __launch_bounds__(kMergeThreads) k_merge_hull_count(MergeDev a, std::uint32_t M,
                                                                     std::uint32_t* cnt) {
@@ -317,71 +415,63 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_hull_count(MergeDev a, 
   for (int d = 0; d <= D; ++d) c += a.out_nbrs[std::uint64_t(d) * a.ostride + o] == kNoneId;
   cnt[o] = c;
 }
-
 template <int D>
-__global__ void __launch_bounds__(kMergeThreads) k_merge_hull_emit(MergeDev a, std::uint32_t M,
-                                                                   const std::uint32_t* hbase) {
+__global__ void __launch_bounds__(kMergeThreads) k_merge_hull_list(MergeDev a, std::uint32_t M,
+                                                                   const std::uint32_t* base, std::uint32_t* hull) {
   const std::uint32_t o = blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= M) return;
-  std::uint32_t nb[D + 1];
-  int c = 0;
+  std::uint32_t pos = base[o];
 #pragma unroll
-  for (int d = 0; d <= D; ++d) {
-    nb[d] = a.out_nbrs[std::uint64_t(d) * a.ostride + o];
-    c += nb[d] == kNoneId;
-  }
-  if (!c) return;
-  std::uint32_t v[D + 1];
+  for (int d = 0; d <= D; ++d)
+    if (a.out_nbrs[std::uint64_t(d) * a.ostride + o] == kNoneId) hull[pos++] = o * (D + 1) + d;
+}
+
+// Hull row M + i for the i-th hull facet: {facet ids, kInf}, parity 0,
+// neighbours[D] = owner; the owner's facet is linked back.
+template <int D>
+__global__ void __launch_bounds__(kMergeThreads) k_merge_hull_emit(MergeDev a, std::uint32_t M,
+                                                                   const std::uint32_t* hull, std::uint32_t H) {
+  const std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= H) return;
+  const std::uint32_t hd = hull[i], o = hd / (D + 1), d = hd % (D + 1), h = M + i;
+  std::uint32_t hv[D + 1];
 #pragma unroll
-  for (int j = 0; j <= D; ++j) v[j] = a.out_verts[std::uint64_t(j) * a.ostride + o];
-  std::uint32_t h = M + hbase[o];
-  const std::uint32_t h0 = h;
+  for (int j = 0, q = 0; j <= D; ++j)
+    if (j != static_cast<int>(d)) hv[q++] = a.out_verts[std::uint64_t(j) * a.ostride + o];
+  hv[D] = kInfVertex;
+  emit_row<D>(a, h, hv, 0);
 #pragma unroll
-  for (int d = 0; d <= D; ++d) {
-    if (nb[d] != kNoneId) continue;
-    std::uint32_t hv[D + 1];
+  for (int j = 0; j < D; ++j) a.out_nbrs[std::uint64_t(j) * a.ostride + h] = kNoneId;
+  a.out_nbrs[std::uint64_t(D) * a.ostride + h] = o;
+  a.out_nbrs[std::uint64_t(d) * a.ostride + o] = h;
+}
+
+// Ridge join: the ridge opposite hv[i] (i < D) of hull row h is {the other
+// D-1 facet ids, kInf}; its two hull rows are linked.
+template <int D>
+__global__ void __launch_bounds__(kMergeThreads) k_merge_ridge_join(MergeDev a, std::uint32_t M, std::uint32_t H) {
+  const std::uint64_t t = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= std::uint64_t(H) * D) return;
+  const std::uint32_t h = M + static_cast<std::uint32_t>(t / D);
+  const int i = static_cast<int>(t % D);
+  std::uint32_t r[D];
 #pragma unroll
-    for (int j = 0, q = 0; j <= D; ++j)
-      if (j != d) hv[q++] = v[j];
-    hv[D] = kInfVertex;
-    emit_row<D>(a, h, hv, 0);
-    a.out_nbrs[std::uint64_t(D) * a.ostride + h] = o;
-    a.out_nbrs[std::uint64_t(d) * a.ostride + o] = h;
-    ++h;
-  }
-  __threadfence();
-  h = h0;
+  for (int j = 0, q = 0; j < D; ++j)
+    if (j != i) r[q++] = __ldg(a.out_verts + std::uint64_t(j) * a.ostride + h);
+  r[D - 1] = kInfVertex;
+  const std::uint32_t partner = join_insert(
+      a.join, a.join_mask, key_of<D>(r), h * (D + 1) + i, a.status, [&](std::uint32_t ov) {
+        const std::uint32_t ph = ov / (D + 1), pi = ov % (D + 1);
+        bool eq = true;
 #pragma unroll
-  for (int d = 0; d <= D; ++d) {
-    if (nb[d] != kNoneId) continue;
-    std::uint32_t f[D];
-#pragma unroll
-    for (int j = 0, q = 0; j <= D; ++j)
-      if (j != d) f[q++] = v[j];
-    // ridge opposite f[i] of hull row h: the other D-1 facet ids plus the infinite vertex
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-      std::uint32_t r[D];
-#pragma unroll
-      for (int j = 0, q = 0; j < D; ++j)
-        if (j != i) r[q++] = f[j];
-      r[D - 1] = kInfVertex;
-      const std::uint32_t partner = join_insert(
-          a.join, a.join_mask, key_of<D>(r), h * (D + 1) + i, a.status, [&](std::uint32_t ov) {
-            const std::uint32_t ph = ov / (D + 1), pi = ov % (D + 1);
-            bool eq = true;
-#pragma unroll
-            for (int j = 0, q = 0; j < D; ++j)
-              if (j != static_cast<int>(pi)) eq &= __ldcg(a.out_verts + std::uint64_t(j) * a.ostride + ph) == r[q++];
-            return eq;
-          });
-      if (partner != kNoneId) {
-        const std::uint32_t ph = partner / (D + 1), pi = partner % (D + 1);
-        a.out_nbrs[std::uint64_t(i) * a.ostride + h] = ph;
-        a.out_nbrs[std::uint64_t(pi) * a.ostride + ph] = h;
-      }
-    }
-    ++h;
+        for (int j = 0, q = 0; j < D; ++j)
+          if (j != static_cast<int>(pi)) eq &= __ldg(a.out_verts + std::uint64_t(j) * a.ostride + ph) == r[q++];
+        return eq;
+      });
+  if (partner != kNoneId) {
+    const std::uint32_t ph = partner / (D + 1), pi = partner % (D + 1);
+    a.out_nbrs[std::uint64_t(i) * a.ostride + h] = ph;
+    a.out_nbrs[std::uint64_t(pi) * a.ostride + ph] = h;
   }
 }
 
@@ -483,55 +573,76 @@ int merge_impl(sbdt_gpu_ctx* ctx, const sbdt_merge_args* args, std::uint64_t ost
   if ((M + 1) * (D + 1) >= kPairedBit) return fail(ctx, kErrRange, "merge: row count exceeds the 31-bit join handle");
 
   StageTimer t_emit(ctx, "merge.emit");
-  for (int j = 0; j <= D; ++j)
-    if (M) SBDT_CUDA_TRY(cudaMemsetAsync(out_nbrs + std::uint64_t(j) * ostride, 0xFF, 4 * M, st));
-  const unsigned long long jbound = (D + 1) * ((S - kept) + (M - kept));
-  const unsigned long long jcap = pow2_at_least(2 * jbound);
-  SBDT_WS(join, unsigned long long, "merge.join", jcap);
-  SBDT_CUDA_TRY(cudaMemsetAsync(join, 0xFF, sizeof(unsigned long long) * jcap, st));
-  a.join = join;
-  a.join_mask = jcap - 1;
+  // join facets: at most D+1 per dropped partial row (each facet of a dropped
+  // row has one kept neighbour) and D+1 per inserted T_B row
+  const std::uint64_t qcap = (D + 1) * ((S - kept) + (M - kept)) + 64;
+  SBDT_WS(queue, std::uint32_t, "merge.queue", qcap);
+  unsigned* qcount = reinterpret_cast<unsigned*>(counters + 1);  // [0] = J, [1] = H
+  SBDT_CUDA_TRY(cudaMemsetAsync(qcount, 0, 8, st));
   if (S) {
-    k_merge_emit_partial<D><<<blocks_for(S), kMergeThreads, 0, st>>>(a);
+    k_merge_emit_partial<D><<<blocks_for(S), kMergeThreads, 0, st>>>(a, qcount, queue, qcap);
     ++ctx->launches;
   }
   if (SB) {
-    k_merge_emit_tb<D><<<blocks_for(SB), kMergeThreads, 0, st>>>(a);
+    k_merge_emit_tb<D><<<blocks_for(SB), kMergeThreads, 0, st>>>(a, qcount, queue, qcap);
+    ++ctx->launches;
+  }
+  unsigned J = 0;
+  SBDT_CUDA_TRY(cudaMemcpyAsync(&J, qcount, 4, cudaMemcpyDeviceToHost, st));
+  SBDT_CUDA_TRY(cudaStreamSynchronize(st));
+  if (J > qcap) return fail(ctx, kErrRange, "merge: join queue overflow");
+  const unsigned long long jcap = pow2_at_least(2ull * J);
+  SBDT_WS(join, unsigned long long, "merge.join", jcap);
+  a.join = join;
+  a.join_mask = jcap - 1;
+  if (J) {
+    SBDT_CUDA_TRY(cudaMemsetAsync(join, 0xFF, sizeof(unsigned long long) * jcap, st));
+    k_merge_join<D><<<blocks_for(J), kMergeThreads, 0, st>>>(a, queue, J);
     ++ctx->launches;
   }
   t_emit.end();
 
   std::uint64_t H = 0;
-  if (args->flags & SBDT_MERGE_HULL) {
+  if ((args->flags & SBDT_MERGE_HULL) && J) {
     StageTimer t_hull(ctx, "merge.hull");
-    SBDT_WS(hcnt, std::uint32_t, "merge.hcnt", M + 1);
-    SBDT_WS(hsums, std::uint32_t, "merge.hsums", M / kScanTile + 2);
-    if (M) {
-      k_merge_hull_count<D><<<blocks_for(M), kMergeThreads, 0, st>>>(a, static_cast<std::uint32_t>(M), hcnt);
-      ++ctx->launches;
-    }
-    exclusive_scan(hcnt, hcnt, M, hsums, hdr + 2, st, &ctx->launches);
-    std::uint32_t h32 = 0;
-    SBDT_CUDA_TRY(cudaMemcpyAsync(&h32, hdr + 2, 4, cudaMemcpyDeviceToHost, st));
+    SBDT_WS(hull, std::uint32_t, "merge.hull", J + 64);
+    k_merge_hull_collect<D><<<blocks_for(J), kMergeThreads, 0, st>>>(a, queue, J, qcount + 1, hull, J + 64);
+    ++ctx->launches;
+    unsigned h32 = 0;
+    SBDT_CUDA_TRY(cudaMemcpyAsync(&h32, qcount + 1, 4, cudaMemcpyDeviceToHost, st));
     SBDT_CUDA_TRY(cudaStreamSynchronize(st));
     H = h32;
     *rows_out = M + H;
     if (M + H > ostride) return fail(ctx, kErrRange, "merge: output capacity below the merged row count");
     if ((M + H + 1) * (D + 1) >= kPairedBit) return fail(ctx, kErrRange, "merge: row count exceeds the 31-bit join handle");
     if (H) {
-      for (int j = 0; j <= D; ++j)
-        SBDT_CUDA_TRY(cudaMemsetAsync(out_nbrs + std::uint64_t(j) * ostride + M, 0xFF, 4 * H, st));
-      const unsigned long long rcap = pow2_at_least(2 * D * H);
+      if (H <= static_cast<std::uint64_t>(kHullSortMax)) {
+        std::uint32_t len = 2;
+        while (len < H) len <<= 1;
+        k_sort_small<<<1, kSortThreads, len * sizeof(std::uint32_t), st>>>(hull, static_cast<std::uint32_t>(H));
+        ++ctx->launches;
+      } else {
+        SBDT_WS(hcnt, std::uint32_t, "merge.hcnt", M + 1);
+        SBDT_WS(hsums, std::uint32_t, "merge.hsums", M / kScanTile + 2);
+        k_merge_hull_count<D><<<blocks_for(M), kMergeThreads, 0, st>>>(a, static_cast<std::uint32_t>(M), hcnt);
+        exclusive_scan(hcnt, hcnt, M, hsums, hdr + 2, st, &ctx->launches);
+        k_merge_hull_list<D><<<blocks_for(M), kMergeThreads, 0, st>>>(a, static_cast<std::uint32_t>(M), hcnt, hull);
+        ctx->launches += 2;
+      }
+      k_merge_hull_emit<D><<<blocks_for(H), kMergeThreads, 0, st>>>(a, static_cast<std::uint32_t>(M), hull,
+                                                                       static_cast<std::uint32_t>(H));
+      const unsigned long long rcap = pow2_at_least(2ull * D * H);
       if (rcap > jcap) {
         SBDT_WS(join2, unsigned long long, "merge.join2", rcap);
         a.join = join2;
       }
       a.join_mask = rcap - 1;
       SBDT_CUDA_TRY(cudaMemsetAsync(a.join, 0xFF, sizeof(unsigned long long) * rcap, st));
-      k_merge_hull_emit<D><<<blocks_for(M), kMergeThreads, 0, st>>>(a, static_cast<std::uint32_t>(M), hcnt);
+      k_merge_ridge_join<D><<<blocks_for(H * D), kMergeThreads, 0, st>>>(a, static_cast<std::uint32_t>(M),
+                                                                           static_cast<std::uint32_t>(H));
       k_merge_hull_check<D><<<blocks_for(H), kMergeThreads, 0, st>>>(a, static_cast<std::uint32_t>(M),
                                                                        static_cast<std::uint32_t>(H));
-      ctx->launches += 2;
+      ctx->launches += 3;
     }
   }
   // offsets[k+1] = M, offsets[k+2] = M + H

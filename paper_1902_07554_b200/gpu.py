@@ -51,10 +51,20 @@ class BorderArgs(C.Structure):
     ]
 
 
+class MergeArgs(C.Structure):
+    """sbdt_merge_args (include/sbdt_gpu.h)."""
+    _fields_ = [
+        ("dim", C.c_int), ("k", C.c_uint32), ("d_labels", C.c_void_p), ("n", C.c_uint64), ("d_offsets", C.c_void_p),
+        ("d_verts", C.c_void_p), ("d_nbrs", C.c_void_p), ("d_parity", C.c_void_p), ("S", C.c_uint64),
+        ("d_border", C.c_void_p), ("d_tb_verts", C.c_void_p), ("d_tb_nbrs", C.c_void_p),
+        ("d_tb_parity", C.c_void_p), ("S_B", C.c_uint64), ("flags", C.c_uint32),
+    ]
+
+
 EXPORTS = [
     "sbdt_gpu_host_alloc", "sbdt_gpu_host_free", "sbdt_gpu_create", "sbdt_gpu_destroy", "sbdt_gpu_last_error", "sbdt_gpu_set_stream", "sbdt_gpu_synchronize",
     "sbdt_gpu_launch_count", "sbdt_gpu_check_status", "sbdt_gpu_assign_points", "sbdt_gpu_assign_points_dev",
-    "sbdt_gpu_find_border", "sbdt_gpu_find_border_dev",
+    "sbdt_gpu_find_border", "sbdt_gpu_find_border_dev", "sbdt_gpu_merge", "sbdt_gpu_merge_dev",
 ]
 
 
@@ -92,7 +102,7 @@ def lib():
         L.sbdt_gpu_find_border_dev.argtypes = [vp, C.POINTER(BorderArgs)]
         L.sbdt_gpu_merge.argtypes = [vp, C.c_int, u32p, u64, u32, u64p, u32p, u32p, i8p, u8p, u32p, u32p, i8p, u64,
                                      u32, u64, u32p, u32p, i8p, u64p, u64p]
-        L.sbdt_gpu_merge_dev.argtypes = [vp, vp, u64, vp, vp, vp, vp, u64p]
+        L.sbdt_gpu_merge_dev.argtypes = [vp, C.POINTER(MergeArgs), u64, vp, vp, vp, vp, u64p]
         L.sbdt_gpu_set_timing.argtypes = [vp, C.c_int]
         L.sbdt_gpu_stage_times.argtypes = [vp, C.c_char_p, C.c_int, C.POINTER(C.c_float), C.c_int]
         L.sbdt_gpu_assign_table_stats.argtypes = [vp, C.POINTER(C.c_uint)]
@@ -179,6 +189,13 @@ class Context:
 
     def find_border_dev(self, args: "BorderArgs"):
         self.check(lib().sbdt_gpu_find_border_dev(self._h, C.byref(args)), "find_border_dev")
+
+    def merge_dev(self, args: "MergeArgs", capacity: int, d_out_verts, d_out_nbrs, d_out_parity, d_out_offsets) -> int:
+        """Device-pointer merge (outputs with row stride `capacity`); returns the row count."""
+        rows = C.c_uint64(0)
+        self.check(lib().sbdt_gpu_merge_dev(self._h, C.byref(args), capacity, d_out_verts, d_out_nbrs, d_out_parity,
+                                            d_out_offsets, C.byref(rows)), "merge_dev")
+        return int(rows.value)
 
     def close(self):
         if self._h:

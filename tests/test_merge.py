@@ -278,3 +278,39 @@ def test_gpu_pipeline_equals_sequential_dt(ctx, dim, dist, n, k, which):
     sv, snb = seq_dt(pts)
     assert np.array_equal(canon(r.merged.verts), canon(sv))
     assert adjacency(r.merged.verts, r.merged.nbrs) == adjacency(sv, snb)
+
+
+def ring_instance():
+    """2-D points near a circle: nearly every point is a hull vertex, so the
+    merged hull has more facets than the GPU's single-CTA sort takes (16384)."""
+    if "ring" not in _inst:
+        rng = np.random.default_rng(12)
+        n = 20_000
+        th = np.sort(rng.random(n)) * 2 * np.pi
+        r = 1.0 - 1e-11 * rng.random(n)
+        pts = np.stack([r * np.cos(th), r * np.sin(th)], axis=1)
+        lab = (np.arange(n) * 4 // n).astype(np.uint32)  # 4 arcs
+        P = host.build_partials(pts, lab, 4, 1)
+        fb = oracle.find_border(pts, lab, P)
+        _inst["ring"] = (pts, lab, P, fb)
+    return _inst["ring"]
+
+
+def test_oracle_merge_many_hull_facets():
+    pts, lab, P, fb = ring_instance()
+    tb = border_tri(pts, fb["vertices_border"])
+    v, nb, par, off = oracle.merge(P, fb["border"], tb, lab)
+    sv, snb = seq_dt(pts)
+    assert np.array_equal(canon(v), canon(sv))
+    assert v.shape[1] - off[P.k + 1] > 16384
+
+
+@pytest.mark.gpu
+def test_gpu_merge_many_hull_facets(ctx):
+    from paper_1902_07554_b200 import gpu
+    pts, lab, P, fb = ring_instance()
+    tb = border_tri(pts, fb["vertices_border"])
+    g = gpu.merge(P, fb["border"], tb, lab, ctx=ctx)
+    v, nb, par, off = oracle.merge(P, fb["border"], tb, lab)
+    assert np.array_equal(g.offsets, off)
+    assert np.array_equal(g.verts, v) and np.array_equal(g.nbrs, nb) and np.array_equal(g.parity, par)
