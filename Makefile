@@ -33,14 +33,21 @@ $(PKG)/dropin_example: tests/cpp/dropin_example.cpp include/sbdt/border.hpp incl
 $(PKG)/libsbdt_host.so: $(HOST_SRC) $(HOST_HDR)
 	$(CXX) $(CXXFLAGS) -shared -o $@ $(HOST_SRC) -lpthread
 
-$(PKG)/libsbdt_gpu.so: $(GPU_SRC) $(GPU_HDR)
-	$(NVCC) $(NVFLAGS) -Iinclude -shared -o $@ $(GPU_SRC) 2> $(PKG)/ptxas.log || (cat $(PKG)/ptxas.log; exit 1)
+GPU_OBJ  := $(patsubst $(CSRC)/gpu/%.cu,build/gpu/%.o,$(GPU_SRC))
+
+build/gpu/%.o: $(CSRC)/gpu/%.cu $(GPU_HDR)
+	@mkdir -p build/gpu
+	$(NVCC) $(NVFLAGS) -Iinclude -c -o $@ $< 2> build/gpu/$*.ptxas.log || (cat build/gpu/$*.ptxas.log; exit 1)
+
+$(PKG)/libsbdt_gpu.so: $(GPU_OBJ)
+	$(NVCC) -shared -gencode arch=compute_100a,code=sm_100a -o $@ $(GPU_OBJ)
+	cat build/gpu/*.ptxas.log > $(PKG)/ptxas.log
 
 oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -f $(PKG)/*.so $(PKG)/ptxas.log $(PKG)/dropin_example
+	rm -rf $(PKG)/*.so $(PKG)/ptxas.log $(PKG)/dropin_example build/gpu
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean

@@ -19,6 +19,7 @@
 // K9  border vertices: positive simplices flag their finite vertices; a
 //     two-pass ballot/prefix-sum compaction emits the sorted, deduplicated
 //     border-vertex ids.
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -114,29 +115,6 @@ __device__ __forceinline__ void circumsphere_inflated(const double (*p)[D], doub
   }
 }
 
-// Binary32 circumsphere with a rigorous error bound, for the prefilter only.
-// Inputs are the binary32 offsets P_j = fl(x_j - lo) of the vertices from the
-// grid origin (k_loc_scatter), so |P_j - (x_j - lo)| <= u |P_j| (u = 2^-24).
-// With a = P1 - P0, b = P2 - P0, c = P3 - P0 the circumcentre relative to P0 is
-//   rel = (|a|^2 (b x c) + |b|^2 (c x a) + |c|^2 (a x b)) / (2 a.(b x c)).
-// Error budget:
-//  - arithmetic (each term a product of at most 12 rounded factors): the
-//    numerators are within g NB and det within g DB of their values at the
-//    rounded inputs, g = 2e-6 > gamma_12, with the absolute-value sums bounded
-//    by Cauchy-Schwarz: NB = |a||b||c| (|a|+|b|+|c|), DB = sqrt(3) |a||b||c|;
-//  - input rounding: each difference is off by at most eta = 2u max|P| per
-//    axis (eta2 = sqrt(3) eta in norm); with M >= every edge length,
-//    |dn| <= 6 M^2 (2 M eta2 + eta2^2) and |ddet| <= 3 M^2 eta2 + M eta2^2.
-// With EN, ED the two totals and |det'| > 4 ED,
-//   |rel_i' - rel_i| <= (EN / 2 + |rel_i'| ED) / (|det'| - ED) + 2u |rel_i'|,
-// plus u |P0_i| for the centre's own offset. The binary64 Cramer evaluation
-// of circumsphere_inflated() is ~1e-9 of that bound from the exact centre
-// (unit roundoff 2^-53), absorbed by the 1e-6 slacks. The 2-D form is the
-// same with a x b (|dn| <= 2 (3 M^2 eta2 + M eta2^2), |ddet| <= 2 M eta2 + eta2^2).
-// Returns the centre c = lo + P0 + rel (binary64), a radius R such that the
-// ball (c, R) contains the inflated binary64 circumsphere and an inner radius
-// Rin such that (c, Rin) lies inside it; false when the bound cannot be
-// established (ill-conditioned, non-finite, binary32 under/overflow range).
 // MUFU approximations used only inside bounds that carry >= 1e-5 relative
 // slack (PTX: rcp.approx.f32 within 1 ulp, sqrt.approx.f32 within ~2^-22.)
 __device__ __forceinline__ float sqrt_apx(float x) {
@@ -187,56 +165,68 @@ struct Sphere32 {
 template <int D>
 __device__ __forceinline__ bool enclosing_sphere_f32(const float (*A)[D], float eta, const float* P0e,
                                                      Sphere32<D>& sp) {
+  // Fused multiply-adds (explicit: the file is built with -fmad=false for the
+  // binary64 reference expressions) round once where a separate product and
+  // sum round twice, so every term carries at most as many roundings as the
+  // gamma_16 budget above counts, with the same absolute-value sums.
   constexpr float g = 2e-6f;
   const float eta2 = 1.7321f * eta * 1.0001f;
   float err[D];
   float* rel = sp.rel;
   if constexpr (D == 2) {
     const float ax = A[0][0], ay = A[0][1], bx = A[1][0], by = A[1][1];
-    const float aa = ax * ax + ay * ay, bb = bx * bx + by * by;
-    const float det = ax * by - ay * bx;
+    const float aa = fmaf(ax, ax, ay * ay), bb = fmaf(bx, bx, by * by);
+    const float det = fmaf(ax, by, -(ay * bx));
     const float la = sqrt_apx(aa) * 1.00001f, lb = sqrt_apx(bb) * 1.00001f;
     const float L = la * lb;
-    const float M = fmaxf(la, lb) * 1.0001f + eta2;
-    const float EN = g * L * (la + lb) * 1.0001f + 2.f * (3.f * M * M * eta2 + M * eta2 * eta2);
-    const float ED = g * L * 1.0001f + 2.f * M * eta2 + eta2 * eta2;
+    const float M = fmaf(fmaxf(la, lb), 1.0001f, eta2);
+    const float EN = fmaf(g * L * 1.0001f, la + lb, 2.f * M * eta2 * fmaf(3.f, M, eta2));
+    const float ED = fmaf(g * 1.0001f, L, eta2 * fmaf(2.f, M, eta2));
     if (!(L > 1e-18f) || !(L < 1e18f) || !(fabsf(det) > 4.f * ED)) return false;
     const float inv2d = 0.5f * rcp_apx(det);
-    rel[0] = (aa * by - bb * ay) * inv2d;
-    rel[1] = (bb * ax - aa * bx) * inv2d;
+    rel[0] = fmaf(aa, by, -(bb * ay)) * inv2d;
+    rel[1] = fmaf(bb, ax, -(aa * bx)) * inv2d;
     const float rden = 1.0002f * rcp_apx(fabsf(det) - ED);
+    const float hEN = 0.5f * EN;
 #pragma unroll
-    for (int d = 0; d < 2; ++d) err[d] = (0.5f * EN + fabsf(rel[d]) * ED) * rden + 1.5e-6f * fabsf(rel[d]) + P0e[d];
+    for (int d = 0; d < 2; ++d)
+      err[d] = fmaf(fmaf(fabsf(rel[d]), ED, hEN), rden, fmaf(1.5e-6f, fabsf(rel[d]), P0e[d]));
   } else {
     const float* a = A[0];
     const float* b = A[1];
     const float* q = A[2];
-    const float aa = a[0] * a[0] + a[1] * a[1] + a[2] * a[2];
-    const float bb = b[0] * b[0] + b[1] * b[1] + b[2] * b[2];
-    const float qq = q[0] * q[0] + q[1] * q[1] + q[2] * q[2];
-    const float x0 = b[1] * q[2] - b[2] * q[1], x1 = b[2] * q[0] - b[0] * q[2], x2 = b[0] * q[1] - b[1] * q[0];
-    const float y0 = q[1] * a[2] - q[2] * a[1], y1 = q[2] * a[0] - q[0] * a[2], y2 = q[0] * a[1] - q[1] * a[0];
-    const float z0 = a[1] * b[2] - a[2] * b[1], z1 = a[2] * b[0] - a[0] * b[2], z2 = a[0] * b[1] - a[1] * b[0];
-    const float det = a[0] * x0 + a[1] * x1 + a[2] * x2;
+    const float aa = fmaf(a[0], a[0], fmaf(a[1], a[1], a[2] * a[2]));
+    const float bb = fmaf(b[0], b[0], fmaf(b[1], b[1], b[2] * b[2]));
+    const float qq = fmaf(q[0], q[0], fmaf(q[1], q[1], q[2] * q[2]));
+    const float x0 = fmaf(b[1], q[2], -(b[2] * q[1])), x1 = fmaf(b[2], q[0], -(b[0] * q[2])),
+                x2 = fmaf(b[0], q[1], -(b[1] * q[0]));
+    const float y0 = fmaf(q[1], a[2], -(q[2] * a[1])), y1 = fmaf(q[2], a[0], -(q[0] * a[2])),
+                y2 = fmaf(q[0], a[1], -(q[1] * a[0]));
+    const float z0 = fmaf(a[1], b[2], -(a[2] * b[1])), z1 = fmaf(a[2], b[0], -(a[0] * b[2])),
+                z2 = fmaf(a[0], b[1], -(a[1] * b[0]));
+    const float det = fmaf(a[0], x0, fmaf(a[1], x1, a[2] * x2));
     const float la = sqrt_apx(aa) * 1.00001f, lb = sqrt_apx(bb) * 1.00001f, lq = sqrt_apx(qq) * 1.00001f;
     const float L = la * lb * lq;
-    const float M = fmaxf(la, fmaxf(lb, lq)) * 1.0001f + eta2;
-    const float EN = g * L * (la + lb + lq) * 1.0001f + 6.f * M * M * (2.f * M * eta2 + eta2 * eta2);
-    const float ED = g * 1.7321f * L * 1.0001f + 3.f * M * M * eta2 + M * eta2 * eta2;
+    const float M = fmaf(fmaxf(la, fmaxf(lb, lq)), 1.0001f, eta2);
+    const float M2 = M * M;
+    const float EN = fmaf(g * L * 1.0001f, la + lb + lq, 6.f * M2 * eta2 * fmaf(2.f, M, eta2));
+    const float ED = fmaf(g * 1.7321f * 1.0001f, L, M * eta2 * fmaf(3.f, M, eta2));
     if (!(L > 1e-24f) || !(L < 1e24f) || !(fabsf(det) > 4.f * ED)) return false;
     const float inv2d = 0.5f * rcp_apx(det);
-    rel[0] = (aa * x0 + bb * y0 + qq * z0) * inv2d;
-    rel[1] = (aa * x1 + bb * y1 + qq * z1) * inv2d;
-    rel[2] = (aa * x2 + bb * y2 + qq * z2) * inv2d;
+    rel[0] = fmaf(aa, x0, fmaf(bb, y0, qq * z0)) * inv2d;
+    rel[1] = fmaf(aa, x1, fmaf(bb, y1, qq * z1)) * inv2d;
+    rel[2] = fmaf(aa, x2, fmaf(bb, y2, qq * z2)) * inv2d;
     const float rden = 1.0002f * rcp_apx(fabsf(det) - ED);
+    const float hEN = 0.5f * EN;
 #pragma unroll
-    for (int d = 0; d < 3; ++d) err[d] = (0.5f * EN + fabsf(rel[d]) * ED) * rden + 1.5e-6f * fabsf(rel[d]) + P0e[d];
+    for (int d = 0; d < 3; ++d)
+      err[d] = fmaf(fmaf(fabsf(rel[d]), ED, hEN), rden, fmaf(1.5e-6f, fabsf(rel[d]), P0e[d]));
   }
-  float rr = 0.f, ee = 0.f;
+  float rr = rel[0] * rel[0], ee = err[0] * err[0];
 #pragma unroll
-  for (int d = 0; d < D; ++d) {
-    rr += rel[d] * rel[d];
-    ee += err[d] * err[d];
+  for (int d = 1; d < D; ++d) {
+    rr = fmaf(rel[d], rel[d], rr);
+    ee = fmaf(err[d], err[d], ee);
   }
   if (!isfinite(rr) || !isfinite(ee)) return false;  // also catches non-finite rel / err
   sp.r = sqrt_apx(rr);
@@ -245,19 +235,23 @@ __device__ __forceinline__ bool enclosing_sphere_f32(const float (*A)[D], float 
 }
 
 // Decodes the packed prefilter coordinates (k_owner_mark) of one row into the
-// edge vectors, P0 and the encoding error bounds of enclosing_sphere_f32.
-//   3-D: 21-bit fixed point q with |q qh - (x - lo)| <= 0.5001 qh: edges are
-//        exact integer differences times qh (two roundings), eta = 1.0002 qh;
-//        P0 = q0 qh (two roundings): P0e = 0.5001 qh + 2.0001 u |P0|.
-//   2-D: binary32 offsets with |P - (x - lo)| <= u |P|: edges one rounding,
-//        eta = 2u max|P|, P0e = u |P0|.
+// edge vectors, P0 and the encoding error bounds of enclosing_sphere_f32, in
+// the row's coordinate UNIT (prefilter_decide scales by it):
+//   3-D: unit = qh, 21-bit fixed point q with |q - (x - lo) / qh| <= 0.5001:
+//        edges are exact integer differences, eta = 1.0003 (two encodings);
+//        P0 = q0 exactly: P0e = 0.50011;
+//   2-D: unit = 1, binary32 offsets with |P - (x - lo)| <= u |P|: edges one
+//        rounding, eta = 2u max|P|, P0e = u |P0|.
 template <int D>
-__device__ __forceinline__ void decode_row(const std::uint64_t* __restrict__ xq, const std::uint32_t* v, float qh_f,
-                                           float qh_err, float (*A)[D], float* P0, float* P0e, float* eta) {
-  constexpr float u = 5.9604645e-8f;
-  std::uint64_t w[D + 1];
+__device__ __forceinline__ void gather_row(const std::uint64_t* __restrict__ xq, const std::uint32_t* v, std::uint64_t n,
+                                           std::uint64_t* w) {
 #pragma unroll
-  for (int j = 0; j <= D; ++j) w[j] = __ldg(xq + v[j]);
+  for (int j = 0; j <= D; ++j) w[j] = __ldg(xq + (v[j] < n ? v[j] : n));  // xq[n] exists (infinite / padding rows)
+}
+
+template <int D>
+__device__ __forceinline__ void decode_row(const std::uint64_t* w, float (*A)[D], float* P0, float* P0e, float* eta) {
+  constexpr float u = 5.9604645e-8f;
   if constexpr (D == 3) {
     int q[4][3];
 #pragma unroll
@@ -267,17 +261,15 @@ __device__ __forceinline__ void decode_row(const std::uint64_t* __restrict__ xq,
 #pragma unroll
     for (int j = 0; j < 3; ++j)
 #pragma unroll
-      for (int d = 0; d < 3; ++d) {
+      for (int d = 0; d < 3; ++d)
         // |dq| < 2^21: exact in binary32 via the 1.5 * 2^23 bias
-        const float dq = __int_as_float(0x4B400000 + (q[j + 1][d] - q[0][d])) - 12582912.f;
-        A[j][d] = dq * qh_f;
-      }
+        A[j][d] = __int_as_float(0x4B400000 + (q[j + 1][d] - q[0][d])) - 12582912.f;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      P0[d] = (__int_as_float(0x4B000000 | q[0][d]) - 8388608.f) * qh_f;
-      P0e[d] = qh_err + 1.2e-7f * fabsf(P0[d]);
+      P0[d] = __int_as_float(0x4B000000 | q[0][d]) - 8388608.f;  // exact
+      P0e[d] = 0.50011f;
     }
-    *eta = 2.0004f * qh_err;
+    *eta = 1.0003f;
   } else {
     float P[3][2];
     float pm = 0.f;
@@ -552,6 +544,8 @@ __global__ void __launch_bounds__(kBThreads) k_border_finite(BorderArgs a, const
 // A only concludes for spheres that contain / are contained in the exact
 // binary64 sphere, so the flags equal the exact test's.
 constexpr int kExactWarps = 4;
+constexpr unsigned kQChunk = 64;              // candidate-queue slots claimed per warp at a time
+constexpr std::uint32_t kNoRow = 0xFFFFFFFFu;  // unused (hole) candidate-queue slot
 
 template <int D>
 __device__ __forceinline__ void load_simplex(const BorderArgs& a, const std::uint32_t* v, double (*p)[D]) {
@@ -582,8 +576,8 @@ __device__ __forceinline__ int prefilter_decide(const OwnerGrid<D>& og, const Bo
 #pragma unroll
   for (int d = 0; d < D; ++d) slack = fmaxf(slack, fabsf(sp.P0[d]) + fabsf(sp.rel[d]));
   slack = (slack + lo_mag) * 1e-15f;
-  const float R = (sp.r * 1.000004f + 2.01f * sp.e) * 1.000001f + slack;
-  const float Rc = R * inv_e * 1.000001f + margin_c;
+  const float R = fmaf(fmaf(sp.r, 1.000004f, 2.01f * sp.e), 1.000001f, slack);
+  const float Rc = fmaf(R * inv_e, 1.000001f, margin_c);
   int lo[D], w = 0;
   int c0[D];
   float Ucs[D];
@@ -592,7 +586,7 @@ __device__ __forceinline__ int prefilter_decide(const OwnerGrid<D>& og, const Bo
 #pragma unroll
   for (int d = 0; d < D; ++d) {
     const float Uc = (sp.P0[d] + sp.rel[d]) * inv_e;
-    const float sl = 4e-7f * (fabsf(Uc) + Rc) + 1e-6f;
+    const float sl = fmaf(4e-7f, fabsf(Uc) + Rc, 1e-6f);
     sl_max = fmaxf(sl_max, sl);
     const float top = static_cast<float>(og.ldims[0][d] - 1);
     const float fl = fminf(fmaxf(Uc - Rc - sl, -2.f), top + 2.f);
@@ -694,38 +688,41 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
   // rows [row_begin, row_end); whole warps iterate together
   const std::uint64_t S_up = row_begin + ((row_end - row_begin + 31) & ~std::uint64_t(31));
   // binary32 cell-unit scale and margin (rounded up; the slacks cover the rest)
-  const float inv_e = static_cast<float>(og.inv_edge);
+  // decode_row's coordinate unit: the fixed-point step in 3-D, 1 in 2-D
+  const double unit = D == 3 ? og.qh : 1.0;
+  const float inv_e = static_cast<float>(og.inv_edge * unit);
   const float margin_c = static_cast<float>(og.margin * og.inv_edge) * 1.0001f + 1e-30f;
   float lo_mag = 0.f;
 #pragma unroll
-  for (int d = 0; d < D; ++d) lo_mag = fmaxf(lo_mag, static_cast<float>(fabs(og.g.lo[d])) * 1.0001f);
+  for (int d = 0; d < D; ++d) lo_mag = fmaxf(lo_mag, static_cast<float>(fabs(og.g.lo[d]) / unit) * 1.0001f);
   bool pos_ok = true;
 #pragma unroll
   for (int d = 0; d < D; ++d)
     pos_ok = pos_ok && fabs(og.g.lo[d]) * og.inv_edge + static_cast<double>(og.ldims[0][d]) < 67108864.0;
-  const float qh_f = static_cast<float>(og.qh);
-  const float qh_err = static_cast<float>(og.qh) * 0.50011f;
   // software pipeline: the vertex ids (and parity) of the next row are in
   // flight while this row's coordinates are gathered and tested
   std::uint64_t s = row_begin + std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   std::uint32_t self = part_of(s_off, a.k, s < row_end ? s : row_end - 1);
   std::uint32_t vn[D + 1];
   std::int8_t parn = 1;
+  auto load_ids = [&](std::uint64_t r, std::uint32_t* ids, std::int8_t& pr) {
 #pragma unroll
-  for (int j = 0; j <= D; ++j) vn[j] = s < row_end ? __ldcs(a.verts + std::uint64_t(j) * a.S + s) : kInfVertex;
-  if (s < row_end) parn = __ldcs(a.parity + s);
+    for (int j = 0; j <= D; ++j) ids[j] = r < row_end ? __ldcs(a.verts + std::uint64_t(j) * a.S + r) : kInfVertex;
+    if (r < row_end) pr = __ldcs(a.parity + r);
+  };
+  load_ids(s, vn, parn);
+  // candidate-queue slots are claimed per warp in chunks of kQChunk (one
+  // atomic per chunk instead of one per iteration on the single counter);
+  // the slots a warp leaves unused at exit are written as kNoRow holes
+  unsigned qbase = 0, qleft = 0;
   for (; s < S_up; s += stride) {
     const bool valid = s < row_end;
     std::uint32_t v[D + 1];
+    std::uint64_t w[D + 1];
 #pragma unroll
     for (int j = 0; j <= D; ++j) v[j] = vn[j];
     const std::int8_t par = parn;
-    {
-      const std::uint64_t sn = s + stride;
-#pragma unroll
-      for (int j = 0; j <= D; ++j) vn[j] = sn < row_end ? __ldcs(a.verts + std::uint64_t(j) * a.S + sn) : kInfVertex;
-      if (sn < row_end) parn = __ldcs(a.parity + sn);
-    }
+    load_ids(s + stride, vn, parn);
     const bool inf = valid && v[D] == kInfVertex;
     bool is_cand = false;
     float cU[D], creach = -1.f;  // recorded for the exact stage's neighbour test
@@ -738,7 +735,8 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
       if (par == 0) atomicOr(a.status, kStDegenerate);
       float A[D][D], P0e[D], eta;
       Sphere32<D> sp;
-      decode_row<D>(a.xq, v, qh_f, qh_err, A, sp.P0, P0e, &eta);
+      gather_row<D>(a.xq, v, a.n, w);
+      decode_row<D>(w, A, sp.P0, P0e, &eta);
       const int res = enclosing_sphere_f32<D>(A, eta, P0e, sp)
                           ? prefilter_decide<D>(og, a, sp, self, inv_e, margin_c, lo_mag, pos_ok, cU, &creach)
                           : 2;
@@ -755,15 +753,24 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
     // warp-aggregated queue appends
     const unsigned mc = __ballot_sync(0xffffffffu, is_cand);
     const unsigned mi = __ballot_sync(0xffffffffu, inf);
-    unsigned bc = 0, bi = 0;
+    const unsigned nc = __popc(mc);
+    unsigned nbase = 0, bi = 0;
     if (lane == 0) {
-      if (mc) bc = atomicAdd(ncand, static_cast<unsigned>(__popc(mc)));
+      if (nc > qleft) nbase = atomicAdd(ncand, kQChunk);
       if (mi) bi = atomicAdd(a.inf_count, static_cast<unsigned>(__popc(mi)));
     }
-    bc = __shfl_sync(0xffffffffu, bc, 0);
+    nbase = __shfl_sync(0xffffffffu, nbase, 0);
     bi = __shfl_sync(0xffffffffu, bi, 0);
+    const unsigned rank = __popc(mc & lt);
+    const unsigned q = rank < qleft ? qbase + rank : nbase + (rank - qleft);
+    if (nc > qleft) {  // the current chunk is used up, the rest goes to the new one
+      qbase = nbase + (nc - qleft);
+      qleft = kQChunk - (nc - qleft);
+    } else {
+      qbase += nc;
+      qleft -= nc;
+    }
     if (is_cand) {
-      const unsigned q = bc + __popc(mc & lt);
       cand[q] = static_cast<std::uint32_t>(s);
 #pragma unroll
       for (int j = 0; j <= D; ++j) cand[std::uint64_t(j + 1) * cap + q] = v[j];
@@ -774,6 +781,8 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
     }
     if (inf) a.inf_queue[bi + __popc(mi & lt)] = static_cast<std::uint32_t>(s);
   }
+  for (unsigned i = lane; i < qleft; i += 32) cand[qbase + i] = kNoRow;
+  if (a.counters && lane == 0 && qleft) atomicAdd(&a.counters[11], static_cast<unsigned long long>(qleft));
 }
 
 // per-lane candidate record for the flattened scan (shared memory, per warp)
@@ -837,7 +846,8 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
     const unsigned base = claim_batch(next);
     if (base >= ncand) break;
     const unsigned t = base + lane;
-    const bool has = t < ncand;
+    const std::uint32_t crow = t < ncand ? cand[t] : kNoRow;
+    const bool has = crow != kNoRow;
     std::uint64_t s = 0;
     std::uint32_t self = 0, v[D + 1];
     double c[D], r2 = 0.0;
@@ -845,7 +855,7 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
     int mode = 0;  // 0 decided, 1 flattened scan, 2 two-level scan, 3 pyramid descent
     bool pre_pos = false;
     if (has) {
-      s = cand[t];
+      s = crow;
       self = part_of(s_off, a.k, s);
 #pragma unroll
       for (int j = 0; j <= D; ++j) v[j] = cand[std::uint64_t(j + 1) * cap + t];
@@ -1509,7 +1519,7 @@ __global__ void k_border_spheres(BorderArgs a) {
 
 __global__ void k_cand_count(const unsigned* ncand, std::uint64_t S, unsigned long long* counters) {
   counters[0] = S;  // rows scanned by the prefilter (finite + infinite)
-  counters[1] = *ncand;
+  counters[1] = *ncand - counters[11];  // queue slots minus the holes
 }
 
 __global__ void k_u32_to_u64(const std::uint32_t* in, std::uint64_t* out) { *out = *in; }
@@ -1667,10 +1677,11 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   const std::size_t offs_sh = sizeof(std::uint64_t) * (in->k + 1);
   SBDT_WS(icur, unsigned, "border.inf_cursor", 2);  // {cursor, CTAs done}
   SBDT_CUDA_TRY(cudaMemsetAsync(icur, 0, 2 * sizeof(unsigned), st));
-  auto infinite = [&]() {
-    if (exact_policy) k_border_infinite<D, true><<<sms * 4, kWideWarps * 32, offs_sh, st>>>(a, og, icur, icur + 1);
-    else k_border_infinite<D, false><<<sms * 4, kWideWarps * 32, offs_sh, st>>>(a, og, icur, icur + 1);
+  auto infinite = [&](cudaStream_t on) {
+    if (exact_policy) k_border_infinite<D, true><<<sms * 4, kWideWarps * 32, offs_sh, on>>>(a, og, icur, icur + 1);
+    else k_border_infinite<D, false><<<sms * 4, kWideWarps * 32, offs_sh, on>>>(a, og, icur, icur + 1);
   };
+  bool inf_forked = false;  // device path: the hull rows ran on the side stream
   // host path, grid policy: a chunk's positive flags are final once its rows
   // went through all stages; they are downloaded while later chunks run
   const bool stream_out = ctx->positive_host && !exact_policy;
@@ -1679,16 +1690,18 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
     const unsigned blocks = static_cast<unsigned>(want < std::uint64_t(sms) * 32 ? want : std::uint64_t(sms) * 32);
     {
       if (tiled && in->S > 0) {
-        const std::uint64_t qcap = in->S + 32;
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_prefilter<D>, kBThreads, offs_sh);
+        const std::uint64_t resA = std::uint64_t(sms) * std::uint64_t(per_sm > 0 ? per_sm : 1);
+        // candidates <= rows, plus < kQChunk holes per prefilter warp and launch
+        const std::uint64_t launches_A = ctx->chunks.empty() ? 1 : ctx->chunks.size();
+        const std::uint64_t qcap = in->S + 32 + launches_A * resA * (kBThreads / 32) * kQChunk;
         SBDT_WS(cq, std::uint32_t, "border.cand", qcap * (2 * D + 3));  // {row, vertices, U, reach}
         // {candidates, cursor, wide rows, wide cursor, CTAs done (exact), CTAs done (wide)}
         SBDT_WS(cn, unsigned, "border.cand_n", 6);
         SBDT_CUDA_TRY(cudaMemsetAsync(cn, 0, 6 * sizeof(unsigned), st));
         const std::uint64_t wcap = qcap;  // wide rows <= candidates
         SBDT_WS(wq, std::uint32_t, "border.wide", wcap * (D + 2));
-        int per_sm = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_prefilter<D>, kBThreads, offs_sh);
-        const std::uint64_t resA = std::uint64_t(sms) * std::uint64_t(per_sm > 0 ? per_sm : 1);
         if (exact_policy)
           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_exact<D, true>, kExactWarps * 32, offs_sh);
         else
@@ -1723,13 +1736,30 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
             StageTimer ta(ctx, "border.prefilter");
             prefilter(0, in->S);
           }
+          // the hull queue is complete once the prefilter ran: its halfspace
+          // kernel (few rows, latency-bound) overlaps exact + wide on the side
+          // stream and joins before the escalation / compaction
+          if (!ctx->side_stream) SBDT_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
+          if (!ctx->fork_ev) SBDT_CUDA_TRY(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+          if (!ctx->join_ev) SBDT_CUDA_TRY(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
+          SBDT_CUDA_TRY(cudaEventRecord(ctx->fork_ev, st));
+          SBDT_CUDA_TRY(cudaStreamWaitEvent(ctx->side_stream, ctx->fork_ev, 0));
+          {
+            StageTimer ti(ctx, "border.infinite", ctx->side_stream);
+            infinite(ctx->side_stream);
+          }
+          SBDT_CUDA_TRY(cudaEventRecord(ctx->join_ev, ctx->side_stream));
+          inf_forked = true;
           {
             StageTimer tx(ctx, "border.exact");
             exact();
           }
-          StageTimer tw(ctx, "border.exact_wide");
-          wide();
-          ctx->launches += 3;
+          {
+            StageTimer tw(ctx, "border.exact_wide");
+            wide();
+          }
+          SBDT_CUDA_TRY(cudaStreamWaitEvent(st, ctx->join_ev, 0));
+          ctx->launches += 4;
         } else {
           // host path: every chunk of rows as soon as its upload has landed;
           // the exact and wide kernels drain the queues grown so far (their
@@ -1744,7 +1774,7 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
               wide();
               ctx->launches += 3;
               if (stream_out) {
-                infinite();
+                infinite(st);
                 ++ctx->launches;
                 cudaEvent_t ev = ctx->chunk_done[&c - &ctx->chunks[0]];
                 SBDT_CUDA_TRY(cudaEventRecord(ev, st));
@@ -1767,9 +1797,9 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
       }
     }
     for (const auto& c : ctx->chunks) SBDT_CUDA_TRY(cudaStreamWaitEvent(st, c.second, 0));
-    {
+    if (!inf_forked) {
       StageTimer t(ctx, "border.infinite");
-      infinite();  // the rows not yet drained (all of them unless the chunked path ran it)
+      infinite(st);  // the rows not yet drained (all of them unless the chunked path ran it)
     }
     if (exact_policy) {
       StageTimer t(ctx, "border.escalate");
@@ -1784,7 +1814,7 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
                             256, 0, st>>>(a);
       ctx->launches += 1;
     }
-    ctx->launches += (tiled && in->S > 0) ? 1 : 2;
+    ctx->launches += inf_forked ? 0 : ((tiled && in->S > 0) ? 1 : 2);
   }
   StageTimer tc(ctx, "border.compact");
   int rc = compact_flags(ctx, in->d_vertex_flags, in->n, in->d_vertex_ids, in->d_vertex_count);

@@ -97,6 +97,9 @@ void sbdt_gpu_destroy(sbdt_gpu_ctx* ctx) {
   for (cudaEvent_t e : ctx->chunk_events) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->chunk_done) cudaEventDestroy(e);
   if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
+  if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
+  if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+  if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
   for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);

@@ -49,6 +49,10 @@ struct sbdt_gpu_ctx {
   std::uint8_t* positive_host = nullptr;
   std::uint32_t* labels_host = nullptr;  // assign_points: labels streamed back per chunk
   cudaStream_t d2h_stream = nullptr;
+  // device path: work off the critical path (the hull rows' halfspace kernel)
+  // runs on side_stream between fork/join events
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   std::vector<cudaEvent_t> chunk_done;
   // host buffers whose device copies ("h.xyz", "h.lab", "h.bbox") are current
   // (SBDT_BORDER_RESIDENT_POINTS)
@@ -116,18 +120,19 @@ inline cudaEvent_t pooled_event(sbdt_gpu_ctx* ctx) {
 struct StageTimer {
   sbdt_gpu_ctx* ctx;
   std::size_t idx = static_cast<std::size_t>(-1);
-  StageTimer(sbdt_gpu_ctx* c, const char* name) : ctx(c) {
+  cudaStream_t stream;
+  StageTimer(sbdt_gpu_ctx* c, const char* name, cudaStream_t on = nullptr) : ctx(c), stream(on ? on : c->stream) {
     if (!ctx->timing) return;
     sbdt_gpu_ctx::Stage s;
     s.name = name;
     s.start = pooled_event(ctx);
     s.stop = pooled_event(ctx);
-    cudaEventRecord(s.start, ctx->stream);
+    cudaEventRecord(s.start, stream);
     idx = ctx->stages.size();
     ctx->stages.push_back(s);
   }
   void end() {
-    if (idx != static_cast<std::size_t>(-1)) cudaEventRecord(ctx->stages[idx].stop, ctx->stream);
+    if (idx != static_cast<std::size_t>(-1)) cudaEventRecord(ctx->stages[idx].stop, stream);
     idx = static_cast<std::size_t>(-1);
   }
   ~StageTimer() { end(); }
