@@ -95,7 +95,7 @@ int sbdt_gpu_assign_table_stats(sbdt_gpu_ctx* ctx, unsigned* out6);
  * two-level range (wide), pyramid range (wide), (candidate, cell row) pairs
  * of the flattened scan, wide-stage block expansions, positives of the
  * flattened scan, positives proven by the prefilter, positives of the wide
- * stage, 0, 0}. */
+ * stage, 0, candidate-queue slots left unused (holes of the per-warp chunks)}. */
 int sbdt_gpu_border_stats(sbdt_gpu_ctx* ctx, unsigned long long* out12);
 
 /* Page-locked host memory for the host-buffer entry points' inputs and
