@@ -146,6 +146,56 @@ __device__ __forceinline__ bool vlt_locate(const double* x, const SampleGrid<D>&
   return true;
 }
 
+// Visits every sample of the cell block [lo_c, lo_c + span) with the whole
+// warp. The cells of a row along axis 0 are consecutive in the cell-sorted
+// sample array, so a row is one contiguous run; 32 rows at a time, their runs
+// are flattened over the lanes (balanced however the samples cluster, no
+// per-cell divisions). f(s) runs on the lane that owns sample s; it must not
+// contain warp collectives. Must be called by the full warp.
+template <int D, class Fn>
+__device__ __forceinline__ void warp_visit_samples(const Grid<D>& g, const std::uint32_t* __restrict__ starts,
+                                                   const int* lo_c, const int* span, Fn&& f) {
+  const unsigned lane = threadIdx.x & 31u;
+  const int rows = D == 3 ? span[1] * span[2] : span[1];
+  for (int r0 = 0; r0 < rows; r0 += 32) {
+    const int r = r0 + static_cast<int>(lane);
+    std::uint32_t sb = 0, len = 0;
+    if (r < rows) {
+      long long c0;
+      if constexpr (D == 3) {
+        const int q2 = r / span[1], q1 = r - q2 * span[1];
+        c0 = (static_cast<long long>(lo_c[2] + q2) * g.dims[1] + (lo_c[1] + q1)) * g.dims[0] + lo_c[0];
+      } else {
+        c0 = static_cast<long long>(lo_c[1] + r) * g.dims[0] + lo_c[0];
+      }
+      sb = starts[c0];
+      len = starts[c0 + span[0]] - sb;
+    }
+    std::uint32_t incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const std::uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= static_cast<unsigned>(o)) incl += y;
+    }
+    const std::uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const std::uint32_t excl = incl - len;
+    for (std::uint32_t b0 = 0; b0 < total; b0 += 32) {
+      const std::uint32_t q = b0 + lane;
+      // the row holding item q: the last lane j with excl_j <= q (excl is
+      // non-decreasing over the lanes)
+      int j = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const std::uint32_t e = __shfl_sync(0xffffffffu, excl, j + step);
+        if (e <= q) j += step;
+      }
+      const std::uint32_t ej = __shfl_sync(0xffffffffu, excl, j);
+      const std::uint32_t sj = __shfl_sync(0xffffffffu, sb, j);
+      if (q < total) f(sj + (q - ej));
+    }
+  }
+}
+
 template <int D>
 struct VltScratch {
   std::uint32_t* idx;
@@ -225,31 +275,19 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
     double bd = INFINITY;
     std::uint32_t bi = 0xFFFFFFFFu;
     for (int r = 1;; ++r) {
-      int lo_c[D], span[D], count = 1;
+      int lo_c[D], span[D];
 #pragma unroll
       for (int d = 0; d < D; ++d) {
         lo_c[d] = max(cc[d] - r, 0);
         span[d] = min(cc[d] + r, static_cast<int>(g.dims[d]) - 1) - lo_c[d] + 1;
-        count *= span[d];
       }
-      for (int t = lane; t < count; t += 32) {
-        int rem = t, q[D];
-#pragma unroll
-        for (int d = 0; d < D; ++d) {
-          q[d] = lo_c[d] + rem % span[d];
-          rem /= span[d];
+      warp_visit_samples<D>(g, starts, lo_c, span, [&](std::uint32_t s) {
+        const double d2 = sqdist<D>(c, sorted[s].x);
+        if (d2 < bd || (d2 == bd && s < bi)) {
+          bd = d2;
+          bi = s;
         }
-        long long qc = q[D - 1];
-#pragma unroll
-        for (int d = D - 2; d >= 0; --d) qc = qc * g.dims[d] + q[d];
-        for (std::uint32_t s = starts[qc], e = starts[qc + 1]; s < e; ++s) {
-          const double d2 = sqdist<D>(c, sorted[s].x);
-          if (d2 < bd || (d2 == bd && s < bi)) {
-            bd = d2;
-            bi = s;
-          }
-        }
-      }
+      });
       warp_argmin<D>(bd, bi);
       if (bi != 0xFFFFFFFFu) break;
       bool whole = true;
@@ -266,48 +304,30 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
     if (lane == 0) s_cnt[warp] = 0;
     __syncwarp();
     {
-      int lo_c[D], span[D], count = 1;
+      int lo_c[D], span[D];
 #pragma unroll
       for (int d = 0; d < D; ++d) {
         const int a = max(static_cast<int>(floor((c[d] - R - g.lo[d]) / g.edge)), 0);
         const int b = min(static_cast<int>(floor((c[d] + R - g.lo[d]) / g.edge)), static_cast<int>(g.dims[d]) - 1);
         lo_c[d] = a;
         span[d] = b - a + 1;
-        count *= span[d];
       }
-      for (int t0 = 0; t0 < count; t0 += 32) {
-        const int t = t0 + static_cast<int>(lane);
-        std::uint32_t sb = 0, se = 0;
-        if (t < count) {
-          int rem = t, q[D];
+      warp_visit_samples<D>(g, starts, lo_c, span, [&](std::uint32_t s) {
+        const SampleRec rec = sorted[s];
+        const double d2 = sqdist<D>(c, rec.x);
+        if (d2 > R2) return;
+        float rs[D];
 #pragma unroll
-          for (int d = 0; d < D; ++d) {
-            q[d] = lo_c[d] + rem % span[d];
-            rem /= span[d];
-          }
-          long long qc = q[D - 1];
+        for (int d = 0; d < D; ++d) rs[d] = static_cast<float>(rec.x[d] - c[d]);
+        if (s != bi && dominated_f<D>(rs, r0, hw, H)) return;
+        const int slot = atomicAdd(&s_cnt[warp], 1);
+        if (slot < CAP) {
+          A.idx[slot] = s;
+          A.lab[slot] = rec.label;
 #pragma unroll
-          for (int d = D - 2; d >= 0; --d) qc = qc * g.dims[d] + q[d];
-          sb = starts[qc];
-          se = starts[qc + 1];
+          for (int d = 0; d < D; ++d) A.rel[std::size_t(slot) * D + d] = rs[d];
         }
-        for (std::uint32_t s = sb; s < se; ++s) {
-          const SampleRec rec = sorted[s];
-          const double d2 = sqdist<D>(c, rec.x);
-          if (d2 > R2) continue;
-          float rs[D];
-#pragma unroll
-          for (int d = 0; d < D; ++d) rs[d] = static_cast<float>(rec.x[d] - c[d]);
-          if (s != bi && dominated_f<D>(rs, r0, hw, H)) continue;
-          const int slot = atomicAdd(&s_cnt[warp], 1);
-          if (slot < CAP) {
-            A.idx[slot] = s;
-            A.lab[slot] = rec.label;
-#pragma unroll
-            for (int d = 0; d < D; ++d) A.rel[std::size_t(slot) * D + d] = rs[d];
-          }
-        }
-      }
+      });
     }
     __syncwarp();
     const int ncand = s_cnt[warp];
