@@ -25,7 +25,7 @@ DROPIN   := $(if $(wildcard $(REF_INC)/sbdt/geometry.hpp),$(PKG)/dropin_example,
 
 all: $(PKG)/libsbdt_gpu.so $(PKG)/libsbdt_host.so oracle $(DROPIN)
 
-$(PKG)/dropin_example: tests/cpp/dropin_example.cpp include/sbdt/border.hpp include/sbdt/sample_partition.hpp \
+$(PKG)/dropin_example: tests/cpp/dropin_example.cpp include/sbdt/border.hpp include/sbdt/sample_partition.hpp include/sbdt/dc_engine.hpp \
                        include/sbdt_gpu.h $(PKG)/libsbdt_gpu.so
 	$(CXX) -O2 -std=c++20 -ffp-contract=off -Iinclude -I$(REF_INC) -o $@ tests/cpp/dropin_example.cpp \
 	    -L$(PKG) -lsbdt_gpu -Wl,-rpath,'$$ORIGIN' -lpthread

@@ -1,20 +1,24 @@
 // Drop-in check of the C++ layer (include/sbdt/*.hpp) on the reference's own
-// types: reads an instance (points, sample, labels, partial triangulations),
-// calls sbdt::assign_points and sbdt::find_border exactly as delaunay_dc would
-// (SPEC.md:479-496), and writes the results for tests/test_cpp_dropin.py.
+// types: reads an instance (points, sample, labels, partial triangulations,
+// optionally the border triangulation T_B), calls sbdt::assign_points,
+// sbdt::find_border and sbdt::merge exactly as delaunay_dc would
+// (SPEC.md:479-505), and writes the results for tests/test_cpp_dropin.py.
 //
 // Input file (little-endian): u32 dim, u64 n, u32 m, u32 k, u64 S; f64 points
 // [n*dim]; u32 sample_ids[m]; u32 sample_labels[m]; u64 offsets[k+1];
-// u32 verts[(dim+1)*S]; u32 nbrs[(dim+1)*S]; i8 parity[S].
+// u32 verts[(dim+1)*S]; u32 nbrs[(dim+1)*S]; i8 parity[S]; optionally
+// u64 S_B; u32 tb_verts[(dim+1)*S_B]; u32 tb_nbrs[(dim+1)*S_B]; i8 tb_parity[S_B].
 // Output file: u32 labels[n]; u8 positive[S]; u8 border[S]; u64 nv;
-// u32 positive_vertex_ids[nv]; u64 nb; u32 border_vertex_ids[nb].
+// u32 positive_vertex_ids[nv]; u64 nb; u32 border_vertex_ids[nb]; with T_B:
+// u64 rows; u32 verts[(dim+1)*rows]; u32 nbrs[(dim+1)*rows]; i8 parity[rows]
+// (the merged triangulation, slot order, vertex-major).
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
 #include <iostream>
 #include <vector>
 
-#include "sbdt/border.hpp"
+#include "sbdt/dc_engine.hpp"
 
 using namespace sbdt;
 
@@ -89,6 +93,43 @@ static int run(std::ifstream& in, std::uint64_t n, std::uint32_t m, std::uint32_
   wr(out, B.positive_vertex_ids.data(), nv);
   wr(out, &nb, 1);
   wr(out, B.border_vertex_ids.data(), nb);
+  // merge the partials with T_B (the DT of B's vertices)
+  std::uint64_t SB = 0;
+  in.read(reinterpret_cast<char*>(&SB), sizeof(SB));
+  if (in) {
+    std::vector<std::uint32_t> tv((D + 1) * SB), tn((D + 1) * SB);
+    std::vector<std::int8_t> tp(SB);
+    rd(in, tv.data(), tv.size());
+    rd(in, tn.data(), tn.size());
+    rd(in, tp.data(), SB);
+    Triangulation<D> TB(&P);
+    for (std::uint64_t r = 0; r < SB; ++r) {
+      Simplex<D> s;
+      for (int j = 0; j <= D; ++j) {
+        s.vertices[j] = tv[std::uint64_t(j) * SB + r];
+        s.neighbors[j] = tn[std::uint64_t(j) * SB + r];
+      }
+      s.parity = tp[r];
+      TB.append_slot(s);
+    }
+    const Triangulation<D> T = merge<D>(std::span<const Triangulation<D>>(partials), B, TB,
+                                        std::span<const PartitionId>(part.labels));
+    const std::uint64_t rows = T.slot_count();
+    std::vector<std::uint32_t> ov((D + 1) * rows), on((D + 1) * rows);
+    std::vector<std::int8_t> op(rows);
+    for (std::uint64_t r = 0; r < rows; ++r) {
+      const Simplex<D>& s = T.at(static_cast<SimplexId>(r));
+      for (int j = 0; j <= D; ++j) {
+        ov[std::uint64_t(j) * rows + r] = s.vertices[j];
+        on[std::uint64_t(j) * rows + r] = s.neighbors[j];
+      }
+      op[r] = s.parity;
+    }
+    wr(out, &rows, 1);
+    wr(out, ov.data(), ov.size());
+    wr(out, on.data(), on.size());
+    wr(out, op.data(), rows);
+  }
   return out ? 0 : 1;
 }
 
