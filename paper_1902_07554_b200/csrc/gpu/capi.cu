@@ -1,6 +1,8 @@
 // C ABI (include/sbdt_gpu.h): context management, host-buffer entry points
 // (H2D -> kernels -> D2H, synchronous) and device-pointer entry points
 // (asynchronous on the context stream). No exception crosses this boundary.
+#include <algorithm>
+#include <thread>
 #include <cuda_runtime.h>
 
 #include <cstring>
@@ -97,6 +99,7 @@ void sbdt_gpu_destroy(sbdt_gpu_ctx* ctx) {
   for (cudaEvent_t e : ctx->chunk_events) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->chunk_done) cudaEventDestroy(e);
   if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
+  if (ctx->sample_stage) cudaFreeHost(ctx->sample_stage);
   if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
   if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
   if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
@@ -215,6 +218,14 @@ int sbdt_gpu_assign_points_dev(sbdt_gpu_ctx* ctx, int dim, const double* d_coord
 // i+1 (and the compute stream never waits for the whole input).
 static constexpr int kUploadChunks = 8;
 
+// Simplex-row chunk boundaries: the last chunks are smaller, so the kernels
+// still to run after the final upload (the tail of the call) are short.
+static_assert(kUploadChunks == 8, "row_chunk_end's table has 8 entries");
+static uint64_t row_chunk_end(uint64_t S, int c) {
+  static constexpr unsigned kCum[kUploadChunks] = {11, 22, 33, 43, 51, 57, 61, 64};  // of 64
+  return c < 0 ? 0 : S * kCum[c] / 64;
+}
+
 static int prepare_chunks(sbdt_gpu_ctx* ctx) {
   if (!ctx->copy_stream) SBDT_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
   if (!ctx->d2h_stream) SBDT_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
@@ -269,12 +280,35 @@ int sbdt_gpu_assign_points(sbdt_gpu_ctx* ctx, int dim, const double* coords, uin
   // only them), then the points in chunks on the copy stream
   double* d_sxyz;
   TRY(dalloc(ctx, "h.sxyz", std::uint64_t(m) * dim, &d_sxyz));
-  std::vector<double> sxyz(std::size_t(m) * dim);
-  for (uint32_t i = 0; i < m; ++i) {
+  for (uint32_t i = 0; i < m; ++i)
     if (sample_ids[i] >= n) return fail(ctx, SBDT_ERR_INVALID, "sample id out of range");
-    for (int d = 0; d < dim; ++d) sxyz[std::size_t(i) * dim + d] = coords[std::size_t(sample_ids[i]) * dim + d];
+  // the gather is m cache misses into the caller's point array: split over
+  // host threads, into a page-locked staging buffer (an async copy)
+  const std::size_t sbytes = sizeof(double) * std::size_t(m) * dim;
+  if (ctx->sample_stage_bytes < sbytes) {
+    if (ctx->sample_stage) cudaFreeHost(ctx->sample_stage);
+    ctx->sample_stage = nullptr;
+    ctx->sample_stage_bytes = 0;
+    SBDT_CUDA_TRY(cudaMallocHost(&ctx->sample_stage, sbytes));
+    ctx->sample_stage_bytes = sbytes;
   }
-  SBDT_CUDA_TRY(cudaMemcpyAsync(d_sxyz, sxyz.data(), sizeof(double) * sxyz.size(), cudaMemcpyHostToDevice, st));
+  SBDT_CUDA_TRY(cudaStreamSynchronize(st));  // the previous call's copy out of the staging buffer is done
+  double* sxyz = static_cast<double*>(ctx->sample_stage);
+  {
+    const unsigned hw = std::thread::hardware_concurrency();
+    const unsigned nt = m < 16384 ? 1u : std::min(16u, hw ? hw : 1u);
+    auto work = [&](unsigned t) {
+      const uint32_t a = static_cast<uint32_t>(std::uint64_t(m) * t / nt),
+                     b = static_cast<uint32_t>(std::uint64_t(m) * (t + 1) / nt);
+      for (uint32_t i = a; i < b; ++i)
+        for (int d = 0; d < dim; ++d) sxyz[std::size_t(i) * dim + d] = coords[std::size_t(sample_ids[i]) * dim + d];
+    };
+    std::vector<std::thread> pool;
+    for (unsigned t = 1; t < nt; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th : pool) th.join();
+  }
+  SBDT_CUDA_TRY(cudaMemcpyAsync(d_sxyz, sxyz, sbytes, cudaMemcpyHostToDevice, st));
   SBDT_CUDA_TRY(cudaMemcpyAsync(d_sid, sample_ids, sizeof(uint32_t) * m, cudaMemcpyHostToDevice, st));
   SBDT_CUDA_TRY(cudaMemcpyAsync(d_slab, sample_labels, sizeof(uint32_t) * m, cudaMemcpyHostToDevice, st));
   ctx->sample_xyz = d_sxyz;
@@ -402,7 +436,7 @@ int sbdt_gpu_find_border(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint6
       cudaGetLastError();  // pageable: clear the error, upload the row
   }
   for (int c = 0; c < kUploadChunks; ++c) {
-    const uint64_t r0 = S * c / kUploadChunks, r1 = S * (c + 1) / kUploadChunks;
+    const uint64_t r0 = row_chunk_end(S, c - 1), r1 = row_chunk_end(S, c);
     if (r1 > r0) {
       for (int j = 0; j <= dim; ++j)
         SBDT_CUDA_TRY(cudaMemcpyAsync(d_verts + j * S + r0, verts + j * S + r0, sizeof(uint32_t) * (r1 - r0),

@@ -45,6 +45,8 @@ struct sbdt_gpu_ctx {
   std::vector<cudaEvent_t> chunk_events;
   std::vector<std::pair<std::uint64_t, cudaEvent_t>> chunks;
   const double* sample_xyz = nullptr;  // compact sample coordinates (host path), else gathered from the points
+  void* sample_stage = nullptr;        // page-locked host staging of those (grow-only)
+  std::size_t sample_stage_bytes = 0;
   // host path: positive flags streamed back per chunk on d2h_stream
   std::uint8_t* positive_host = nullptr;
   std::uint32_t* labels_host = nullptr;  // assign_points: labels streamed back per chunk
