@@ -601,15 +601,21 @@ __device__ __forceinline__ int prefilter_decide(const OwnerGrid<D>& og, const Bo
     c0[d] = ic;
   }
   if (outside) return 0;  // the range misses the grid on some axis: no cell is reachable
+  // Both owner-code loads go out together (one latency instead of two in a
+  // row): the window's code for the negative proof and the centre cell's
+  // code for the positive proof below.
+  const bool cen = inside && pos_ok && !a.exact;  // exact policy: a foreign cell is not a foreign point
+  std::uint16_t wcode = kOwnerMulti, ccode = kOwnerEmpty;
   if (w <= 4) {
     const int h = w == 0 ? 0 : (w <= 2 ? 1 : 2);
     int cm[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) cm[d] = min(lo[d] + h, og.ldims[0][d] - 1);
     const std::uint16_t* src = h == 0 ? a.owner : (h == 1 ? a.nbr3 : a.nbr5);
-    const std::uint16_t code = __ldg(src + og_index<D>(og, 0, cm));
-    if (code == kOwnerEmpty || code == self) return 0;
+    wcode = __ldg(src + og_index<D>(og, 0, cm));
   }
+  if (cen) ccode = __ldg(a.owner + og_index<D>(og, 0, c0));
+  if (wcode == kOwnerEmpty || wcode == self) return 0;
   // Positive proof, in binary32 cell units: c0 = floor(Uc) holds Uc, the real
   // centre lies within sqrt(D) sl of Uc, and the cell box in cell units is
   // [c0, c0 + 1] up to the binary64 rounding of cell_lo (< 1e-7 cells while
@@ -618,14 +624,11 @@ __device__ __forceinline__ int prefilter_decide(const OwnerGrid<D>& og, const Bo
   // the binary64 box test on the binary64 sphere accepts it.
   // The same holds for a neighbour of c0 whose box (in cell units) is within
   // the remaining reach of Uc.
-  if (!inside || !pos_ok || a.exact) return 2;  // exact policy: a foreign cell is not a foreign point
+  if (!cen) return 2;
   const float rin_c = ((sp.r * 0.999996f - 2.01f * sp.e * 1.000001f) * 0.999999f - slack) * inv_e * 0.999998f;
   const float reach = rin_c - margin_c - 1.7321f * sl_max - 2e-7f;
   if (!(reach > 0.f)) return 2;
-  {
-    const std::uint16_t code = a.owner[og_index<D>(og, 0, c0)];
-    if (code != kOwnerEmpty && code != self) return 1;
-  }
+  if (ccode != kOwnerEmpty && ccode != self) return 1;
   if (out_reach) {
     *out_reach = reach;
 #pragma unroll
