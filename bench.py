@@ -415,8 +415,9 @@ def main():
         # (the hull rows' neighbour is read in place from the page-locked
         # nbrs buffer: ~1% of S entries cross PCIe, counted as 4 B each)
         n_hull = int(np.count_nonzero(part.verts[dim] == 0xFFFFFFFF))
-        h2d = (inst.points.nbytes + 8 * m + 8 * m * dim) + (part.offsets.nbytes + part.verts.nbytes
-                                                            + 4 * n_hull + part.parity.nbytes)
+        # (parity crosses only for the exact policy, which orients in_sphere with it)
+        h2d = (inst.points.nbytes + 8 * m + 8 * m * dim) + (part.offsets.nbytes + part.verts.nbytes + 4 * n_hull
+                                                            + (part.parity.nbytes if args.policy == "exact" else 0))
         d2h = (4 * n + 8 * (k + 1) + 4 * n + 8 * dim) + (S + 8 + 4 * len(bs.positive_vertex_ids))
         e2e = {"value": world * n / t_e2e, "unit": "points/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": round(1e3 * t_e2e, 3),

@@ -132,7 +132,11 @@ int sbdt_gpu_assign_points_dev(sbdt_gpu_ctx* ctx, int dim, const double* d_coord
  * Simplex::vertices[j] / neighbors[j] of every simplex):
  *   verts[j*S + s]  global PointId, ascending, kInfiniteVertex (0xFFFFFFFF) last
  *   nbrs[j*S + s]   part-local SimplexId sharing the facet opposite verts[j]
- *   parity[s]       Simplex::parity (orientation sign of the stored order)
+ *   parity[s]       Simplex::parity (orientation sign of the stored order);
+ *                   read by the exact policy only (in_sphere_oriented), may be
+ *                   NULL otherwise: a simplex whose vertices have zero exact
+ *                   orientation fails the call with SBDT_ERR_DEGENERATE, as the
+ *                   reference's circumsphere throws DegenerateSimplex
  * labels[i] is the partition of point i (the GridIndex of part j is built from
  * the points labelled j; cell edge c_G (V/n)^(1/D) over the global bbox).
  * Outputs (caller buffers):

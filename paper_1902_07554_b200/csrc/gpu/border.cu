@@ -72,6 +72,15 @@ __global__ void k_pbbox_init(unsigned long long* pbbox, std::uint32_t count, int
     pbbox[j] = ((j % (2 * dim)) < static_cast<std::uint32_t>(dim)) ? 0xFFFFFFFFFFFFFFFFULL : 0ULL;
 }
 
+// Exact orientation of the simplex (predicates.hpp: filter + expansion
+// arithmetic); 0 = degenerate, which the reference's circumsphere rejects
+// with DegenerateSimplex (geometry.cpp:279-297).
+template <int D>
+__device__ __forceinline__ int orientation_exact(const double (*p)[D]) {
+  if constexpr (D == 3) return sbdt_pred::orient3(p[0], p[1], p[2], p[3]);
+  else return sbdt_pred::orient2(p[0], p[1], p[2]);
+}
+
 // circumsphere (geometry.cpp:279-327) + inflated (geometry.hpp:179-183)
 template <int D>
 __device__ __forceinline__ void circumsphere_inflated(const double (*p)[D], double* center, double* r2) {
@@ -504,13 +513,13 @@ __global__ void __launch_bounds__(kBThreads) k_border_finite(BorderArgs a, const
       a.inf_queue[slot] = static_cast<std::uint32_t>(s);
       continue;
     }
-    if (a.parity[s] == 0) atomicOr(a.status, kStDegenerate);
     const std::uint32_t self = part_of(s_off, a.k, s);
     double p[D + 1][D];
 #pragma unroll
     for (int j = 0; j <= D; ++j)
 #pragma unroll
       for (int d = 0; d < D; ++d) p[j][d] = a.xyz[std::size_t(v[j]) * D + d];
+    if (orientation_exact<D>(p) == 0) atomicOr(a.status, kStDegenerate);
     double c[D], r2;
     circumsphere_inflated<D>(p, c, &r2);
     if (a.spheres) {
@@ -544,6 +553,9 @@ __global__ void __launch_bounds__(kBThreads) k_border_finite(BorderArgs a, const
 // A only concludes for spheres that contain / are contained in the exact
 // binary64 sphere, so the flags equal the exact test's.
 constexpr int kExactWarps = 4;
+// candidate-queue reach value of a row whose binary32 sphere failed: the
+// exact stage checks its exact orientation (DegenerateSimplex, geometry.cpp:281)
+constexpr float kReachCheckOrient = -2.f;
 constexpr unsigned kQChunk = 64;              // candidate-queue slots claimed per warp at a time
 constexpr std::uint32_t kNoRow = 0xFFFFFFFFu;  // unused (hole) candidate-queue slot
 
@@ -702,18 +714,16 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
 #pragma unroll
   for (int d = 0; d < D; ++d)
     pos_ok = pos_ok && fabs(og.g.lo[d]) * og.inv_edge + static_cast<double>(og.ldims[0][d]) < 67108864.0;
-  // software pipeline: the vertex ids (and parity) of the next row are in
-  // flight while this row's coordinates are gathered and tested
+  // software pipeline: the vertex ids of the next row are in flight while
+  // this row's coordinates are gathered and tested
   std::uint64_t s = row_begin + std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   std::uint32_t self = part_of(s_off, a.k, s < row_end ? s : row_end - 1);
   std::uint32_t vn[D + 1];
-  std::int8_t parn = 1;
-  auto load_ids = [&](std::uint64_t r, std::uint32_t* ids, std::int8_t& pr) {
+  auto load_ids = [&](std::uint64_t r, std::uint32_t* ids) {
 #pragma unroll
     for (int j = 0; j <= D; ++j) ids[j] = r < row_end ? __ldcs(a.verts + std::uint64_t(j) * a.S + r) : kInfVertex;
-    if (r < row_end) pr = __ldcs(a.parity + r);
   };
-  load_ids(s, vn, parn);
+  load_ids(s, vn);
   // candidate-queue slots are claimed per warp in chunks of kQChunk (one
   // atomic per chunk instead of one per iteration on the single counter);
   // the slots a warp leaves unused at exit are written as kNoRow holes
@@ -724,8 +734,7 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
     std::uint64_t w[D + 1];
 #pragma unroll
     for (int j = 0; j <= D; ++j) v[j] = vn[j];
-    const std::int8_t par = parn;
-    load_ids(s + stride, vn, parn);
+    load_ids(s + stride, vn);
     const bool inf = valid && v[D] == kInfVertex;
     bool is_cand = false;
     float cU[D], creach = -1.f;  // recorded for the exact stage's neighbour test
@@ -735,14 +744,18 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
       while (self + 1 < a.k && s_off[self + 1] <= sc) ++self;
     }
     if (valid && !inf) {
-      if (par == 0) atomicOr(a.status, kStDegenerate);
       float A[D][D], P0e[D], eta;
       Sphere32<D> sp;
       gather_row<D>(a.xq, v, a.n, w);
       decode_row<D>(w, A, sp.P0, P0e, &eta);
-      const int res = enclosing_sphere_f32<D>(A, eta, P0e, sp)
-                          ? prefilter_decide<D>(og, a, sp, self, inv_e, margin_c, lo_mag, pos_ok, cU, &creach)
-                          : 2;
+      // a binary32 sphere with its bound proves |det| > 0 (the orientation
+      // of the binary64 vertices is nonzero); rows without one are checked
+      // with the exact orientation in the exact stage (kReachCheckOrient)
+      int res = 2;
+      if (enclosing_sphere_f32<D>(A, eta, P0e, sp))
+        res = prefilter_decide<D>(og, a, sp, self, inv_e, margin_c, lo_mag, pos_ok, cU, &creach);
+      else
+        creach = kReachCheckOrient;
       if (a.counters && res == 1) atomicAdd(&a.counters[8], 1ull);
       if (res == 2) {
         is_cand = true;
@@ -864,10 +877,10 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
       for (int j = 0; j <= D; ++j) v[j] = cand[std::uint64_t(j + 1) * cap + t];
       bool proven = false;
       if constexpr (!Ex) {
+        const float reach = __uint_as_float(cand[std::uint64_t(2 * D + 2) * cap + t]);
         // binary32 positive proof over the centre cell's near-octant
         // neighbours (the prefilter tried the centre cell and recorded the
         // cell-unit centre and the inner ball's reach)
-        const float reach = __uint_as_float(cand[std::uint64_t(2 * D + 2) * cap + t]);
         if (reach > 0.f) {
           float U[D];
 #pragma unroll
@@ -1033,6 +1046,25 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
     }
   }
   rewind_cursor(next, fin, ncand);
+}
+
+// Candidates whose binary32 sphere failed (reach == kReachCheckOrient): the
+// exact orientation of their binary64 vertices; zero is DegenerateSimplex
+// (geometry.cpp:279-297). Rare rows, off the critical path (side stream).
+template <int D>
+__global__ void __launch_bounds__(256) k_border_orient(BorderArgs a, const std::uint32_t* __restrict__ cand,
+                                                      std::uint64_t cap, const unsigned* __restrict__ ncand_p) {
+  const unsigned ncand = *ncand_p;
+  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < ncand; t += gridDim.x * blockDim.x) {
+    if (cand[t] == kNoRow) continue;
+    if (__uint_as_float(cand[std::uint64_t(2 * D + 2) * cap + t]) != kReachCheckOrient) continue;
+    std::uint32_t v[D + 1];
+#pragma unroll
+    for (int j = 0; j <= D; ++j) v[j] = cand[std::uint64_t(j + 1) * cap + t];
+    double p[D + 1][D];
+    load_simplex<D>(a, v, p);
+    if (orientation_exact<D>(p) == 0) atomicOr(a.status, kStDegenerate);
+  }
 }
 
 // Wide candidates (cell range wider than 5 per axis, or non-finite spheres):
@@ -1751,6 +1783,8 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
             StageTimer ti(ctx, "border.infinite", ctx->side_stream);
             infinite(ctx->side_stream);
           }
+          k_border_orient<D><<<sms * 4, 256, 0, ctx->side_stream>>>(a, cq, qcap, cn);
+          ++ctx->launches;
           SBDT_CUDA_TRY(cudaEventRecord(ctx->join_ev, ctx->side_stream));
           inf_forked = true;
           {
@@ -1788,6 +1822,8 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
             }
             r0 = r1;
           }
+          k_border_orient<D><<<sms * 4, 256, 0, st>>>(a, cq, qcap, cn);
+          ++ctx->launches;
         }
         if (a.counters) {
           k_cand_count<<<1, 1, 0, st>>>(cn, in->S, a.counters);

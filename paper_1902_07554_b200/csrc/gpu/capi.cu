@@ -183,7 +183,7 @@ int sbdt_gpu_check_status(sbdt_gpu_ctx* ctx) {
   cudaError_t e = cudaMemcpy(&st, ctx->d_status, sizeof(unsigned), cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return fail_cuda(ctx, e, "status readback");
   if (st) cudaMemset(ctx->d_status, 0, sizeof(unsigned));
-  if (st & kStDegenerate) return fail(ctx, SBDT_ERR_DEGENERATE, "degenerate simplex (parity 0) in a partial triangulation");
+  if (st & kStDegenerate) return fail(ctx, SBDT_ERR_DEGENERATE, "degenerate simplex (zero orientation) in a partial triangulation");
   if (st & kStGridCap) return fail(ctx, SBDT_ERR_RANGE, "grid index would exceed 4 n / c_G^D cells (degenerate bbox?)");
   if (st & kStQueueOverflow) return fail(ctx, SBDT_ERR_RANGE, "escalation queue overflow");
   if (st & 8u) return fail(ctx, SBDT_ERR_MERGE, "InconsistentMerge: a facet with more than two finite owners");
@@ -360,8 +360,8 @@ int sbdt_gpu_find_border(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint6
                          const int8_t* parity, int policy, double c_G, uint32_t flags, uint8_t* positive_out,
                          uint8_t* border_out, uint32_t* vertex_ids_out, uint64_t* n_vertices_out,
                          uint32_t* bfs_vertex_ids_out, uint64_t* n_bfs_vertices_out, double* spheres_out) {
-  if (!ctx || !coords || !labels || !offsets || !verts || !nbrs || !parity || !positive_out || !vertex_ids_out ||
-      !n_vertices_out)
+  if (!ctx || !coords || !labels || !offsets || !verts || !nbrs || (!parity && policy == SBDT_POLICY_EXACT) ||
+      !positive_out || !vertex_ids_out || !n_vertices_out)
     return SBDT_ERR_INVALID;
   if (dim != 2 && dim != 3) return fail(ctx, SBDT_ERR_INVALID, "dim must be 2 or 3");
   const uint64_t S = offsets[k];
@@ -441,7 +441,10 @@ int sbdt_gpu_find_border(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint6
       for (int j = 0; j <= dim; ++j)
         SBDT_CUDA_TRY(cudaMemcpyAsync(d_verts + j * S + r0, verts + j * S + r0, sizeof(uint32_t) * (r1 - r0),
                                       cudaMemcpyHostToDevice, cs));
-      SBDT_CUDA_TRY(cudaMemcpyAsync(d_par + r0, parity + r0, r1 - r0, cudaMemcpyHostToDevice, cs));
+      // parity orients in_sphere (exact policy only); the other policies
+      // check degeneracy geometrically and never read it
+      if (policy == SBDT_POLICY_EXACT)
+        SBDT_CUDA_TRY(cudaMemcpyAsync(d_par + r0, parity + r0, r1 - r0, cudaMemcpyHostToDevice, cs));
       // without the BFS only the hull rows' last neighbour (the finite
       // simplex across the hull facet, row dim of the SoA) is read, and from
       // a page-locked caller buffer it is read in place (zero-copy)

@@ -107,3 +107,39 @@ def test_jittered_lattice_near_degenerate(ctx):
     sid = np.sort(rng.choice(len(pts), size=len(pts) // 16, replace=False)).astype(np.uint32)
     slab = np.minimum((pts[sid, 1] * 3 // 14).astype(np.uint32), 2)
     _check(pts, sid, slab, 3, ctx)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_degenerate_simplex_raises(dim, ctx):
+    """A finite simplex whose vertices have zero exact orientation is the
+    reference's DegenerateSimplex (circumsphere, geometry.cpp:279-297): two of
+    its vertices are made to coincide. Every policy raises it, without reading
+    Simplex::parity for grid / bbox (the check is geometric)."""
+    inst = host.make_instance(1 if dim == 2 else 2, n=20_000, k=4)
+    lab = oracle.assign_brute(inst.points, inst.sample_ids, inst.sample_labels)
+    P = host.attach_partials(inst, lab)
+    fin = np.nonzero(P.verts[dim] != 0xFFFFFFFF)[0]
+    row = int(fin[len(fin) // 2])
+    pts = inst.points.copy()
+    pts[P.verts[dim, row]] = pts[P.verts[0, row]]
+    for policy in ("grid", "bbox", "exact"):
+        with pytest.raises(gpu.DegenerateSimplex):
+            gpu.find_border(pts, lab, P, gpu.IntersectionPolicy(policy, 1.0), hull_bfs=False, ctx=ctx)
+    # the context stays usable
+    g = gpu.find_border(inst.points, lab, P, gpu.IntersectionPolicy("grid", 1.0), hull_bfs=False, ctx=ctx)
+    o = oracle.find_border(inst.points, lab, P, "grid")
+    assert np.array_equal(g.positive, o["positive"])
+
+
+def test_grid_policy_does_not_read_parity(ctx):
+    """grid / bbox results are independent of Simplex::parity (zeroed here)."""
+    inst = host.make_instance(2, n=20_000, k=4)
+    lab = oracle.assign_brute(inst.points, inst.sample_ids, inst.sample_labels)
+    P = host.attach_partials(inst, lab)
+    from paper_1902_07554_b200.host import Partials
+    Z = Partials(P.offsets, P.verts, P.nbrs, np.zeros_like(P.parity))
+    for policy in ("grid", "bbox"):
+        g = gpu.find_border(inst.points, lab, Z, gpu.IntersectionPolicy(policy, 1.0), hull_bfs=True, ctx=ctx)
+        o = oracle.find_border(inst.points, lab, P, policy)
+        assert np.array_equal(g.positive, o["positive"]), policy
+        assert np.array_equal(g.border, o["border"]), policy
