@@ -417,6 +417,11 @@ struct BorderArgs {
   std::uint32_t* esc;               // undecided filtered in_sphere tests: (row, cell-point slot)
   unsigned* esc_count;
   unsigned esc_cap;
+  // exact policy, hull rows: the hull vertex set of all partials (sorted ids)
+  const std::uint32_t* labels;
+  const std::uint32_t* hull_ids;
+  const unsigned long long* hull_count;
+  const unsigned* hull_valid;  // 1: every partition with points has simplex rows (the set is complete)
 };
 
 // Exact policy, one leaf cell: is some point of another part strictly inside
@@ -1310,6 +1315,8 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_border_infinite(BorderArgs 
   const unsigned lane = threadIdx.x & 31u;
   WideEntry<D>* stk = stacks[threadIdx.x >> 5];
   const unsigned count = *a.inf_count;
+  const bool use_hull_set = Ex && a.hull_valid && *a.hull_valid;
+  const unsigned long long n_hull = use_hull_set ? *a.hull_count : 0ull;
   for (;;) {
     const unsigned q0 = claim_batch(next);
     if (q0 >= count) break;
@@ -1392,7 +1399,37 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_border_infinite(BorderArgs 
           if constexpr (Ex) return og_halfspace_exact_serial<D>(og, a.owner, facet, sl_sign, sl_self, leaf);
           else return og_halfspace_hits_foreign<D>(og, a.owner, facet, sl_sign, sl_self);
         };
-        const bool hit = warp_descent<D>(og, a.owner, lo, hi, sl_self, test, fallback, stk);
+        bool hit;
+        if (Ex && use_hull_set) {
+          // Exact policy: some foreign point strictly outside the facet's
+          // plane <=> some foreign HULL vertex (a finite vertex of an
+          // infinite row of its partial) is: a partition's points are convex
+          // combinations of its hull vertices, so if all of those lie in the
+          // closed inner halfspace, so do all its points (and a partition's
+          // own points never lie outside its own hull facets). A point
+          // strictly outside lies in a cell with a corner strictly outside,
+          // so the reference's candidate-cell filter changes nothing.
+          const double* q4[D + 1];
+#pragma unroll
+          for (int j = 0; j < D; ++j) q4[j] = fl[j];
+          bool out = false;
+          for (unsigned long long u0 = 0; u0 < n_hull && !out; u0 += 32) {
+            bool o = false;
+            const unsigned long long u = u0 + lane;
+            if (u < n_hull) {
+              const std::uint32_t id = a.hull_ids[u];
+              if (a.labels[id] != sl_self) {
+                q4[D] = a.xyz + std::size_t(id) * D;
+                const int r = orient_dev<D>(q4);
+                o = r != 0 && r != sl_sign;
+              }
+            }
+            out = __any_sync(full, o);
+          }
+          hit = out;
+        } else {
+          hit = warp_descent<D>(og, a.owner, lo, hi, sl_self, test, fallback, stk);
+        }
         if (static_cast<int>(lane) == l) pos = hit;
         __syncwarp();
       }
@@ -1560,6 +1597,39 @@ __global__ void k_cand_count(const unsigned* ncand, std::uint64_t S, unsigned lo
 __global__ void k_u32_to_u64(const std::uint32_t* in, std::uint64_t* out) { *out = *in; }
 
 // ---------------------------------------------------------------------------
+// Exact policy: the hull vertex set of the partials (finite vertices of their
+// infinite rows) for k_border_infinite, and whether it is complete (every
+// partition that holds points has rows, hence hull facets).
+template <int D>
+__global__ void k_hull_mark(BorderArgs a, std::uint8_t* __restrict__ hflags) {
+  const unsigned count = *a.inf_count;
+  for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < count; q += gridDim.x * blockDim.x) {
+    const std::uint64_t s = a.inf_queue[q];
+#pragma unroll
+    for (int j = 0; j < D; ++j) hflags[a.verts[std::uint64_t(j) * a.S + s]] = 1;
+  }
+}
+
+__global__ void k_part_present(const std::uint32_t* __restrict__ labels, std::uint64_t n,
+                               std::uint8_t* __restrict__ present) {
+  for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += std::uint64_t(gridDim.x) * blockDim.x) {
+    const std::uint32_t l = labels[i];
+    if (!present[l]) present[l] = 1;
+  }
+}
+
+__global__ void k_hull_valid(const std::uint64_t* __restrict__ offsets, std::uint32_t k,
+                             const std::uint8_t* __restrict__ present, unsigned* __restrict__ valid) {
+  __shared__ unsigned ok;
+  if (threadIdx.x == 0) ok = 1;
+  __syncthreads();
+  for (std::uint32_t p = threadIdx.x; p < k; p += blockDim.x)
+    if (present[p] && offsets[p + 1] == offsets[p]) ok = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) *valid = ok;
+}
+
 int compact_flags(sbdt_gpu_ctx* ctx, const std::uint8_t* d_flags, std::uint64_t n, std::uint32_t* d_out,
                   std::uint64_t* d_count) {
   cudaStream_t st = ctx->stream;
@@ -1694,6 +1764,37 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   a.esc = nullptr;
   a.esc_count = nullptr;
   a.esc_cap = 0;
+  a.labels = in->d_labels;
+  a.hull_ids = nullptr;
+  a.hull_count = nullptr;
+  a.hull_valid = nullptr;
+  std::uint8_t *hflags = nullptr, *hpresent = nullptr;
+  if (exact_policy) {
+    SBDT_WS(hf, std::uint8_t, "border.hull_flags", in->n + 64);
+    SBDT_WS(hi, std::uint32_t, "border.hull_ids", in->n + 64);
+    SBDT_WS(hc, std::uint64_t, "border.hull_count", 1);
+    SBDT_WS(hp, std::uint8_t, "border.part_present", in->k + 64);
+    SBDT_WS(hv, unsigned, "border.hull_valid", 1);
+    hflags = hf;
+    hpresent = hp;
+    a.hull_ids = hi;
+    a.hull_count = reinterpret_cast<const unsigned long long*>(hc);
+    a.hull_valid = hv;
+  }
+  // exact policy: the hull vertex set, once the hull queue is complete
+  auto build_hull_set = [&]() -> int {
+    if (!exact_policy) return kOk;
+    SBDT_CUDA_TRY(cudaMemsetAsync(hflags, 0, in->n, st));
+    SBDT_CUDA_TRY(cudaMemsetAsync(hpresent, 0, in->k, st));
+    k_hull_mark<D><<<sms * 4, 256, 0, st>>>(a, hflags);
+    const std::uint64_t want = (in->n + 255) / 256;
+    k_part_present<<<static_cast<unsigned>(want < std::uint64_t(sms) * 8 ? (want ? want : 1) : std::uint64_t(sms) * 8),
+                     256, 0, st>>>(in->d_labels, in->n, hpresent);
+    k_hull_valid<<<1, 256, 0, st>>>(in->d_offsets, in->k, hpresent, const_cast<unsigned*>(a.hull_valid));
+    ctx->launches += 3;
+    return compact_flags(ctx, hflags, in->n, const_cast<std::uint32_t*>(a.hull_ids),
+                         reinterpret_cast<std::uint64_t*>(const_cast<unsigned long long*>(a.hull_count)));
+  };
   if (exact_policy) {
     const unsigned long long want = 2ull * in->S + 2ull * in->n + (1ull << 20);
     a.esc_cap = static_cast<unsigned>(want < 0x7FFFFFFFull ? want : 0x7FFFFFFFull);
@@ -1774,6 +1875,10 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
           // the hull queue is complete once the prefilter ran: its halfspace
           // kernel (few rows, latency-bound) overlaps exact + wide on the side
           // stream and joins before the escalation / compaction
+          {
+            const int hrc = build_hull_set();
+            if (hrc != kOk) return hrc;
+          }
           if (!ctx->side_stream) SBDT_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
           if (!ctx->fork_ev) SBDT_CUDA_TRY(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
           if (!ctx->join_ev) SBDT_CUDA_TRY(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
@@ -1837,6 +1942,8 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
     }
     for (const auto& c : ctx->chunks) SBDT_CUDA_TRY(cudaStreamWaitEvent(st, c.second, 0));
     if (!inf_forked) {
+      const int hrc = build_hull_set();
+      if (hrc != kOk) return hrc;
       StageTimer t(ctx, "border.infinite");
       infinite(st);  // the rows not yet drained (all of them unless the chunked path ran it)
     }
