@@ -1080,6 +1080,7 @@ __global__ void __launch_bounds__(256) k_border_orient(BorderArgs a, const std::
 // shared memory. Same decisions as og_sphere_hits_foreign (exact pruning),
 // without serialising a whole descent on one lane.
 constexpr int kWideWarps = 4;
+constexpr unsigned kWideClaim = 4;  // rows a warp claims at a time in the wide / hull kernels
 constexpr int kWideStack = 256;  // deeper stacks (> 4 levels of dense partial blocks) take the serial fallback
 
 template <int D>
@@ -1240,10 +1241,12 @@ __global__ void __launch_bounds__(kWideWarps * 32, 6) k_border_wide(BorderArgs a
   WideEntry<D>* stk = stacks[threadIdx.x >> 5];
   const unsigned full = 0xffffffffu;
   for (;;) {
-    const unsigned base = claim_batch(next);
+    // few rows per claim: a row is a whole-warp descent of very uneven cost,
+    // and warps holding 32 of them leave the others idle at the end
+    const unsigned base = claim_batch(next, kWideClaim);
     if (base >= nwide) break;
     const unsigned t = base + lane;
-    const bool has = t < nwide;
+    const bool has = lane < kWideClaim && t < nwide;
     std::uint64_t s = 0;
     std::uint32_t self = 0, v[D + 1];
     double c[D], r2 = 0.0;
@@ -1318,10 +1321,10 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_border_infinite(BorderArgs 
   const bool use_hull_set = Ex && a.hull_valid && *a.hull_valid;
   const unsigned long long n_hull = use_hull_set ? *a.hull_count : 0ull;
   for (;;) {
-    const unsigned q0 = claim_batch(next);
+    const unsigned q0 = claim_batch(next, kWideClaim);
     if (q0 >= count) break;
     const unsigned q = q0 + lane;
-    const bool has = q < count;
+    const bool has = lane < kWideClaim && q < count;
     std::uint64_t s = 0;
     std::uint32_t self = 0, fv[D];
     int inner_sign = 0;

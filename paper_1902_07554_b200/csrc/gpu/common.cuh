@@ -133,9 +133,9 @@ __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 // cursor overshoots the queue length; the last CTA of a launch rewinds it to
 // the length the launch worked on, so a later launch over a grown queue
 // (host-path chunks) resumes exactly there.
-__device__ __forceinline__ unsigned claim_batch(unsigned* next) {
+__device__ __forceinline__ unsigned claim_batch(unsigned* next, unsigned batch = 32u) {
   unsigned base = 0;
-  if ((threadIdx.x & 31u) == 0) base = atomicAdd(next, 32u);
+  if ((threadIdx.x & 31u) == 0) base = atomicAdd(next, batch);
   return __shfl_sync(0xffffffffu, base, 0);
 }
 
