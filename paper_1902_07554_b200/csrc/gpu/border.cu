@@ -844,7 +844,8 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
                                                                    unsigned* __restrict__ next,
                                                                    std::uint32_t* __restrict__ wide,
                                                                    unsigned* __restrict__ nwide,
-                                                                   unsigned* __restrict__ fin) {
+                                                                   unsigned* __restrict__ fin,
+                                                                   unsigned* __restrict__ nlight) {
   __shared__ OwnerGrid<D> og;
   __shared__ CandSlot<D> slots[kExactWarps][32];
   __shared__ unsigned char nzl[kExactWarps][32];
@@ -914,14 +915,22 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
       }
     }
     {
-      // forward wide ranges
-      const unsigned mw = __ballot_sync(full, mode >= 2);
-      if (mw) {
-        unsigned wb = 0;
-        if (lane == 0) wb = atomicAdd(nwide, static_cast<unsigned>(__popc(mw)));
-        wb = __shfl_sync(full, wb, 0);
-        if (mode >= 2) {
-          const unsigned q = wb + __popc(mw & ((1u << lane) - 1u));
+      // forward wide ranges. With nlight, the pyramid rows (mode 3: the
+      // costliest descents) fill the queue from the front and the two-level
+      // rows from the back, so k_border_wide starts the long ones first.
+      const unsigned lt = (1u << lane) - 1u;
+      const unsigned mh = __ballot_sync(full, nlight ? mode == 3 : mode >= 2);
+      const unsigned ml = nlight ? __ballot_sync(full, mode == 2) : 0u;
+      if (mh | ml) {
+        unsigned hb = 0, lb = 0;
+        if (lane == 0) {
+          if (mh) hb = atomicAdd(nwide, static_cast<unsigned>(__popc(mh)));
+          if (ml) lb = atomicAdd(nlight, static_cast<unsigned>(__popc(ml)));
+        }
+        hb = __shfl_sync(full, hb, 0);
+        lb = __shfl_sync(full, lb, 0);
+        if ((mh >> lane) & 1u || (ml >> lane) & 1u) {
+          const std::uint64_t q = ((mh >> lane) & 1u) ? hb + __popc(mh & lt) : cap - 1 - (lb + __popc(ml & lt));
           wide[q] = static_cast<std::uint32_t>(s);
 #pragma unroll
           for (int j = 0; j <= D; ++j) wide[std::uint64_t(j + 1) * cap + q] = v[j];
@@ -1229,14 +1238,18 @@ __global__ void __launch_bounds__(kWideWarps * 32, 6) k_border_wide(BorderArgs a
                                                                  std::uint64_t cap,
                                                                  const unsigned* __restrict__ nwide_p,
                                                                  unsigned* __restrict__ next,
-                                                                 unsigned* __restrict__ fin) {
+                                                                 unsigned* __restrict__ fin,
+                                                                 const unsigned* __restrict__ nlight_p) {
   __shared__ OwnerGrid<D> og;
   __shared__ WideEntry<D> stacks[kWideWarps][kWideStack];
   extern __shared__ std::uint64_t s_off[];
   if (threadIdx.x == 0) og = *ogp;
   for (std::uint32_t j = threadIdx.x; j <= a.k; j += blockDim.x) s_off[j] = a.offsets[j];
   __syncthreads();
-  const unsigned nwide = *nwide_p;
+  // rows [0, nheavy) from the front of the queue, then the nlight rows
+  // stored from the back (see k_border_exact)
+  const unsigned nheavy = *nwide_p;
+  const unsigned nwide = nheavy + (nlight_p ? *nlight_p : 0u);
   const unsigned lane = threadIdx.x & 31u;
   WideEntry<D>* stk = stacks[threadIdx.x >> 5];
   const unsigned full = 0xffffffffu;
@@ -1251,10 +1264,11 @@ __global__ void __launch_bounds__(kWideWarps * 32, 6) k_border_wide(BorderArgs a
     std::uint32_t self = 0, v[D + 1];
     double c[D], r2 = 0.0;
     if (has) {
-      s = wide[t];
+      const std::uint64_t slot = t < nheavy ? t : cap - 1 - (t - nheavy);
+      s = wide[slot];
       self = part_of(s_off, a.k, s);
 #pragma unroll
-      for (int j = 0; j <= D; ++j) v[j] = wide[std::uint64_t(j + 1) * cap + t];
+      for (int j = 0; j <= D; ++j) v[j] = wide[std::uint64_t(j + 1) * cap + slot];
       double p[D + 1][D];
       load_simplex<D>(a, v, p);
       circumsphere_inflated<D>(p, c, &r2);
@@ -1837,8 +1851,12 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
         const std::uint64_t qcap = in->S + 32 + launches_A * resA * (kBThreads / 32) * kQChunk;
         SBDT_WS(cq, std::uint32_t, "border.cand", qcap * (2 * D + 3));  // {row, vertices, U, reach}
         // {candidates, cursor, wide rows, wide cursor, CTAs done (exact), CTAs done (wide)}
-        SBDT_WS(cn, unsigned, "border.cand_n", 6);
-        SBDT_CUDA_TRY(cudaMemsetAsync(cn, 0, 6 * sizeof(unsigned), st));
+        // {candidates, cursor, wide rows, wide cursor, CTAs done (exact), CTAs done (wide), light wide rows}
+        SBDT_WS(cn, unsigned, "border.cand_n", 8);
+        SBDT_CUDA_TRY(cudaMemsetAsync(cn, 0, 8 * sizeof(unsigned), st));
+        // device path: one exact and one wide launch, the wide queue split
+        // by cost class (host path: the launches per chunk share one cursor)
+        unsigned* nlight = ctx->chunks.empty() ? cn + 6 : nullptr;
         const std::uint64_t wcap = qcap;  // wide rows <= candidates
         SBDT_WS(wq, std::uint32_t, "border.wide", wcap * (D + 2));
         if (exact_policy)
@@ -1859,16 +1877,18 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
         auto exact = [&]() {
           if (exact_policy)
             k_border_exact<D, true><<<resX, kExactWarps * 32, offs_sh, st>>>(a, og, cq, qcap, cn, cn + 1, wq, cn + 2,
-                                                                            cn + 4);
+                                                                            cn + 4, nlight);
           else
             k_border_exact<D, false><<<resX, kExactWarps * 32, offs_sh, st>>>(a, og, cq, qcap, cn, cn + 1, wq, cn + 2,
-                                                                             cn + 4);
+                                                                             cn + 4, nlight);
         };
         auto wide = [&]() {
           if (exact_policy)
-            k_border_wide<D, true><<<resW, kWideWarps * 32, offs_sh, st>>>(a, og, wq, wcap, cn + 2, cn + 3, cn + 5);
+            k_border_wide<D, true><<<resW, kWideWarps * 32, offs_sh, st>>>(a, og, wq, wcap, cn + 2, cn + 3, cn + 5,
+                                                                          nlight);
           else
-            k_border_wide<D, false><<<resW, kWideWarps * 32, offs_sh, st>>>(a, og, wq, wcap, cn + 2, cn + 3, cn + 5);
+            k_border_wide<D, false><<<resW, kWideWarps * 32, offs_sh, st>>>(a, og, wq, wcap, cn + 2, cn + 3, cn + 5,
+                                                                           nlight);
         };
         if (ctx->chunks.empty()) {
           {
