@@ -591,35 +591,16 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
   }
 }
 
-// Binary32 squared distance of the point (p, relative to the box centre, |p|^2
-// = pp) to entry e and its rigorous error bound 4e-6 (|p|^2 + |s|^2) (3x the
-// worst case of these few roundings).
-template <int D>
-__device__ __forceinline__ void dist32(const float* p, float pp, const VltEntry& e, float* dd, float* bb) {
-  float d2 = 0.f, ss = 0.f;
-#pragma unroll
-  for (int d = 0; d < D; ++d) {
-    const float t = p[d] - e.r[d];
-    d2 += t * t;
-    ss += e.r[d] * e.r[d];
-  }
-  *dd = d2;
-  *bb = 4e-6f * (pp + ss) + 1e-30f;
-}
-
 // Exact binary64 argmin over the candidates whose binary32 interval overlaps
 // the winner's (reference squared_distance, lowest pid on ties).
 template <int D>
-__device__ __forceinline__ std::uint32_t exact_among(const double* x, const VltEntry* ents, int cnt, const float* p,
-                                                     float pp, float lim, const SampleRec* __restrict__ sorted) {
+__device__ __forceinline__ std::uint32_t exact_among(const double* x, const VltEntry* ents, int cnt, const float* d32,
+                                                     const float* b32, float lim, const SampleRec* __restrict__ sorted) {
   double best = INFINITY;
   std::uint32_t best_pid = 0xFFFFFFFFu, label = 0;
   for (int j = 0; j < cnt; ++j) {
-    const VltEntry e = ents[j];
-    float dd, bb;
-    dist32<D>(p, pp, e, &dd, &bb);
-    if (dd - bb > lim) continue;
-    const SampleRec rec = sorted[e.idx];
+    if (d32[j] - b32[j] > lim) continue;
+    const SampleRec rec = sorted[ents[j].idx];
     const double d2 = sqdist<D>(x, rec.x);
     if (d2 < best || (d2 == best && rec.pid < best_pid)) {
       best = d2;
@@ -670,14 +651,8 @@ __global__ void __launch_bounds__(256) k_assign_vlt(const double* __restrict__ x
     if (cnt == 0) {
       __stcs(labels + i, head >> 8);
     } else if (cnt >= kHeadLong) {
-      // warp-aggregated append (one atomic per warp and iteration)
-      const unsigned m = __activemask();
-      const unsigned lane = threadIdx.x & 31u;
-      const int leader = __ffs(m) - 1;
-      unsigned base = 0;
-      if (static_cast<int>(lane) == leader) base = atomicAdd(oq_count, static_cast<unsigned>(__popc(m)));
-      base = __shfl_sync(m, base, leader);
-      oq[base + __popc(m & ((1u << lane) - 1u))] = static_cast<std::uint32_t>(i);
+      const unsigned slot = atomicAdd(oq_count, 1u);
+      oq[slot] = static_cast<std::uint32_t>(i);
     } else {
       const VltEntry* ents = slab + fid * kSlots;
       if (cnt == kHeadPool) {  // sub-box list in the long slab
@@ -691,29 +666,32 @@ __global__ void __launch_bounds__(256) k_assign_vlt(const double* __restrict__ x
         p[d] = static_cast<float>(x[d] - fcen[d]);
         pp += p[d] * p[d];
       }
-      // pass 1: the binary32 winner; pass 2 (the entries again, L1-resident;
-      // no per-thread arrays): decided iff every other candidate is
-      // provably farther
+      float d32[kSlots], b32[kSlots];
       int best = 0;
-      float bval = INFINITY, bbnd = 0.f;
+      float bval = INFINITY;
       for (int j = 0; j < static_cast<int>(cnt); ++j) {
-        float dd, bb;
-        dist32<D>(p, pp, ents[j], &dd, &bb);
+        const VltEntry e = ents[j];
+        float dd = 0.f, ss = 0.f;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const float t = p[d] - e.r[d];
+          dd += t * t;
+          ss += e.r[d] * e.r[d];
+        }
+        d32[j] = dd;
+        b32[j] = 4e-6f * (pp + ss) + 1e-30f;
         if (dd < bval) {
           bval = dd;
-          bbnd = bb;
           best = j;
         }
       }
-      const float lim = bval + bbnd;
+      // decided iff every other candidate is provably farther
+      const float lim = d32[best] + b32[best];
       bool decided = true;
-      for (int j = 0; j < static_cast<int>(cnt) && decided; ++j) {
-        float dd, bb;
-        dist32<D>(p, pp, ents[j], &dd, &bb);
-        if (j != best && dd - bb <= lim) decided = false;
-      }
+      for (int j = 0; j < static_cast<int>(cnt); ++j)
+        if (j != best && d32[j] - b32[j] <= lim) decided = false;
       const std::uint32_t lab = decided ? __ldg(sorted_labels + ents[best].idx)
-                                        : exact_among<D>(x, ents, static_cast<int>(cnt), p, pp, lim, sorted);
+                                        : exact_among<D>(x, ents, static_cast<int>(cnt), d32, b32, lim, sorted);
       __stcs(labels + i, lab);
     }
   }
