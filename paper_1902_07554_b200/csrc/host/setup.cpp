@@ -577,7 +577,10 @@ std::vector<std::uint32_t> partition_graph(const SampleGraph& sg, std::uint32_t 
 Partials build_partials(int dim, const double* coords, std::size_t n, const std::uint32_t* labels,
                         std::uint32_t k, std::uint64_t seed, unsigned threads) {
   std::vector<std::vector<std::uint32_t>> parts(k);
-  for (std::size_t i = 0; i < n; ++i) parts[labels[i]].push_back(static_cast<std::uint32_t>(i));
+  for (std::size_t i = 0; i < n; ++i) {
+    if (labels[i] >= k) throw std::invalid_argument("label " + std::to_string(labels[i]) + " >= k");
+    parts[labels[i]].push_back(static_cast<std::uint32_t>(i));
+  }
   std::vector<TriSoA> tris(k);
   std::atomic<std::uint32_t> next{0};
   std::vector<std::string> errors(k);

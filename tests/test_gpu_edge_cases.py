@@ -143,3 +143,27 @@ def test_grid_policy_does_not_read_parity(ctx):
         o = oracle.find_border(inst.points, lab, P, policy)
         assert np.array_equal(g.positive, o["positive"]), policy
         assert np.array_equal(g.border, o["border"]), policy
+
+
+def test_exact_policy_partition_without_rows(ctx):
+    """Exact policy: a partition holding points but too few for a simplex (2
+    points in 3-D: no rows, hence no hull facets) leaves the hull vertex set
+    incomplete; the hull rows must then take the leaf-scan descent, and its
+    points still count as foreign points for every other partition."""
+    inst = host.make_instance(2, n=20_000, k=4)
+    lab = oracle.assign_brute(inst.points, inst.sample_ids, inst.sample_labels).copy()
+    # two points near the domain's lower corner become partition 4
+    far = np.argsort(inst.points.sum(axis=1))[:2]
+    lab[far] = 4
+    # the DTs of parts 0..3; part 4 (2 points) has none: an empty row range
+    tris = [host.triangulate(inst.points, np.nonzero(lab == p)[0].astype(np.uint32), 7) for p in range(4)]
+    offs = np.zeros(6, np.uint64)
+    offs[1:5] = np.cumsum([t.verts.shape[1] for t in tris])
+    offs[5] = offs[4]
+    P5 = host.Partials(offs, np.concatenate([t.verts for t in tris], axis=1),
+                       np.concatenate([t.nbrs for t in tris], axis=1), np.concatenate([t.parity for t in tris]))
+    g = gpu.find_border(inst.points, lab, P5, gpu.IntersectionPolicy("exact", 1.0), hull_bfs=True, ctx=ctx)
+    o = oracle.find_border(inst.points, lab, P5, "exact")
+    assert np.array_equal(g.positive, o["positive"])
+    assert np.array_equal(g.border, o["border"])
+    assert np.array_equal(g.positive_vertex_ids, o["vertices_positive"])
