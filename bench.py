@@ -312,7 +312,7 @@ def main():
     # one step captured as a CUDA graph (every launch, memset and cross-stream
     # fork/join of assign_points_dev + find_border_dev), replayed per step
     graph_ms, gms = None, []
-    if not args.no_graph:
+    if not args.no_graph and not args.profile:
         pos_ref, cnt_ref, lab_ref = d_pos.clone(), d_cnt.clone(), d_lab.clone()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream):
