@@ -391,8 +391,8 @@ def main():
     kernel_bytes = {
         "assign.points": n * (8 * dim + 4),
         "border.finite": S * (4 * (dim + 1) + 1) + n * (8 * dim + 4 + 1) + cells * 2,
-        # prefilter: vertex ids + parity + flag per row, localised coords once, 3 code arrays
-        "border.prefilter": S * (4 * (dim + 1) + 2) + n * (8 * dim + 4) + cells * 2 * 3,
+        # prefilter: vertex ids + flag per row, coords once, 3 code arrays (parity is not read)
+        "border.prefilter": S * (4 * (dim + 1) + 1) + n * (8 * dim + 4) + cells * 2 * 3,
         # exact stage: queue entry + ids per candidate + result, coords once
         "border.exact": n_cand * (4 + 4 * (dim + 1) + 1) + n * (8 * dim + 4) + cells * 2,
         "border.grid": n * (8 * dim + 4) + cells * 2,
