@@ -1521,7 +1521,7 @@ __global__ void k_cell_count(const double* __restrict__ xyz, std::uint64_t n, co
        i += std::uint64_t(gridDim.x) * blockDim.x) {
     int c[D];
 #pragma unroll
-    for (int d = 0; d < D; ++d) c[d] = static_cast<int>(cell_coord<D>(og.g, xyz[i * D + d], d));
+    for (int d = 0; d < D; ++d) c[d] = static_cast<int>(cell_coord_fast<D>(og.g, og.inv_edge, xyz[i * D + d], d));
     atomicAdd(&cnt[og_index<D>(og, 0, c)], 1u);
   }
 }
@@ -1541,7 +1541,7 @@ __global__ void k_cell_scatter(const double* __restrict__ xyz, const std::uint32
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       q.x[d] = xyz[i * D + d];
-      c[d] = static_cast<int>(cell_coord<D>(og.g, q.x[d], d));
+      c[d] = static_cast<int>(cell_coord_fast<D>(og.g, og.inv_edge, q.x[d], d));
     }
     q.label = labels[i];
     q.pid = static_cast<std::uint32_t>(i);

@@ -75,6 +75,24 @@ __device__ __forceinline__ long long cell_coord(const Grid<D>& g, double x, int 
   else c = static_cast<long long>(f);
   return c;
 }
+
+// cell_coord through a product with the rounded reciprocal of the edge, exact:
+// y = (x - lo) * inv_edge is within ~3.3e-16 |y| of the correctly rounded
+// quotient q of cell_coord, so floor(y) == floor(q) unless an integer lies
+// within that distance of y; those (rare) cases take the division.
+template <int D>
+__device__ __forceinline__ long long cell_coord_fast(const Grid<D>& g, double inv_edge, double x, int d) {
+  const double y = (x - g.lo[d]) * inv_edge;
+  const double fy = floor(y);
+  const double fr = y - fy;  // exact
+  const double m = fmax(fabs(y), 1.0) * 4e-15;
+  if (!(fr > m && fr < 1.0 - m)) return cell_coord<D>(g, x, d);
+  long long c;
+  if (!(fy >= 0.0)) c = 0;
+  else if (fy >= static_cast<double>(g.dims[d] - 1)) c = g.dims[d] - 1;
+  else c = static_cast<long long>(fy);
+  return c;
+}
 template <int D>
 __device__ __forceinline__ double cell_lo(const Grid<D>& g, long long i, int d) {
   return g.lo[d] + static_cast<double>(i) * g.edge;

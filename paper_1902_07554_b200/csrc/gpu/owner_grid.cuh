@@ -161,6 +161,10 @@ __global__ void k_owner_mark(const double* __restrict__ xyz, const std::uint32_t
     for (std::uint32_t j = threadIdx.x; j < k * 2 * D; j += blockDim.x)
       s_pb[j] = ((j % (2 * D)) < D) ? 0xFFFFFFFFFFFFFFFFULL : 0ULL;
   __syncthreads();
+  // (x - lo) / qh as a product with the rounded reciprocal: a few ulps of
+  // 2^21 off the quotient, far inside the 0.5001 qh the prefilter's bound
+  // allows for the fixed-point encoding (decode_row)
+  const double inv_qh = 1.0 / og.qh;
   for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += std::uint64_t(gridDim.x) * blockDim.x) {
     double x[D];
@@ -168,7 +172,7 @@ __global__ void k_owner_mark(const double* __restrict__ xyz, const std::uint32_t
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       x[d] = xyz[i * D + d];
-      c[d] = static_cast<int>(cell_coord<D>(og.g, x[d], d));
+      c[d] = static_cast<int>(cell_coord_fast<D>(og.g, og.inv_edge, x[d], d));
     }
     if (xq) {
       // packed prefilter coordinates, indexed by PointId: 3-D 21-bit fixed
@@ -178,7 +182,7 @@ __global__ void k_owner_mark(const double* __restrict__ xyz, const std::uint32_t
         std::uint64_t w = 0;
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-          const double t = rint((x[d] - og.g.lo[d]) / og.qh);
+          const double t = rint((x[d] - og.g.lo[d]) * inv_qh);
           const std::uint64_t q = t <= 0.0 ? 0ull : (t >= 2097151.0 ? 2097151ull : static_cast<std::uint64_t>(t));
           w |= q << (21 * d);
         }
