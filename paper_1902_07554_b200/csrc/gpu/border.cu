@@ -1706,7 +1706,8 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
     bb = bbox;
   }
   k_owner_params<D><<<1, 1, 0, st>>>(bb, in->n, cg, cap, owner_len, og, ctx->d_status);
-  SBDT_CUDA_TRY(cudaMemsetAsync(owner, 0xFF, sizeof(std::uint16_t) * owner_len, st));
+  k_owner_clear<D><<<sms * 8, 256, 0, st>>>(og, owner);
+  ++ctx->launches;
   if (pbbox) {
     k_pbbox_init<<<(in->k * 2 * D + 255) / 256, 256, 0, st>>>(pbbox, in->k * 2 * D, D);
     ctx->launches += 1;

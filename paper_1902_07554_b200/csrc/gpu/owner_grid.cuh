@@ -404,6 +404,22 @@ __global__ void __launch_bounds__(256) k_nbr_tiles(const OwnerGrid<D>* __restric
   }
 }
 
+// EMPTY over the entries the grid actually uses (loff[levels], known only on
+// the device) instead of the worst-case capacity.
+template <int D>
+__global__ void k_owner_clear(const OwnerGrid<D>* __restrict__ ogp, std::uint16_t* __restrict__ owner) {
+  const unsigned long long len = ogp->loff[ogp->levels];
+  unsigned long long i = (static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x) * 8ull;
+  const unsigned long long step = static_cast<unsigned long long>(gridDim.x) * blockDim.x * 8ull;
+  for (; i < len; i += step) {
+    if (i + 8 <= len) {
+      *reinterpret_cast<uint4*>(owner + i) = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+    } else {
+      for (unsigned long long j = i; j < len; ++j) owner[j] = kOwnerEmpty;
+    }
+  }
+}
+
 // ---- queries ----------------------------------------------------------------------
 template <int D>
 __device__ __forceinline__ void og_block_box(const OwnerGrid<D>& og, int L, const int* c, double* blo, double* bhi) {
