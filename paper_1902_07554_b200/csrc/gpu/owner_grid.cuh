@@ -293,6 +293,14 @@ constexpr int nbr_tile() {
   return D == 3 ? 16 : 64;
 }
 
+__device__ __forceinline__ std::uint32_t nbr_pack(std::uint16_t code) {
+  return (static_cast<std::uint32_t>(code) << 16) | (code == kOwnerEmpty ? 0xFFFFu : 0xFFFFu - code);
+}
+__device__ __forceinline__ std::uint16_t nbr_unpack(std::uint32_t w) {
+  const std::uint32_t mn = w >> 16, mx = 0xFFFFu - (w & 0xFFFFu);
+  return mn == kOwnerEmpty ? kOwnerEmpty : static_cast<std::uint16_t>(mn == mx ? mn : kOwnerMulti);
+}
+
 template <int D>
 __global__ void __launch_bounds__(256) k_nbr_tiles(const OwnerGrid<D>* __restrict__ ogp,
                                                    const std::uint16_t* __restrict__ owner,
@@ -306,7 +314,11 @@ __global__ void __launch_bounds__(256) k_nbr_tiles(const OwnerGrid<D>* __restric
   constexpr int LN = D == 3 ? RS * RS : RS;   // lines per pass
   constexpr int ON = D == 3 ? T * T * T : T * T;
   __shared__ OwnerGrid<D> og;
-  __shared__ std::uint16_t bufA[RN], bufB[RN];
+  // one packed word per staged cell: (min code) << 16 | (0xFFFF - max code),
+  // EMPTY counting as +inf for the min and as 0 for the max; then the window
+  // combine (EMPTY identity, MULTI absorbing) is one 16x2 three-way min
+  // (VIMNMX3.U16x2), and the code is recovered from (min, max) at the end
+  __shared__ std::uint32_t buf[RN];
   if (threadIdx.x == 0) og = *ogp;
   __syncthreads();
   if (og.levels < 2) {  // a single cell
@@ -348,11 +360,9 @@ __global__ void __launch_bounds__(256) k_nbr_tiles(const OwnerGrid<D>* __restric
         rr /= RS;
         in = in && c[d] >= 0 && c[d] < cd0[d];
       }
-      bufA[r] = in ? own0[gindex(c)] : kOwnerEmpty;
+      buf[r] = nbr_pack(in ? own0[gindex(c)] : kOwnerEmpty);
     }
     __syncthreads();
-    std::uint16_t* src = bufA;
-    std::uint16_t* dst = bufB;
     for (int rep = 0; rep < 2; ++rep) {
 #pragma unroll
       for (int ax = 0; ax < D; ++ax) {
@@ -366,21 +376,18 @@ __global__ void __launch_bounds__(256) k_nbr_tiles(const OwnerGrid<D>* __restric
           } else {
             base = ax == 0 ? l * RS : l;
           }
-          std::uint16_t prev = src[base], cur = src[base + st];
-          dst[base] = prev;
+          // in place: a line belongs to one thread, and the registers hold
+          // the original values of the cells already overwritten
+          std::uint32_t prev = buf[base], cur = buf[base + st];
 #pragma unroll 6
           for (int i = 1; i < RS - 1; ++i) {
-            const std::uint16_t next = src[base + (i + 1) * st];
-            dst[base + i * st] = og_combine(og_combine(prev, cur), next);
+            const std::uint32_t next = buf[base + (i + 1) * st];
+            buf[base + i * st] = __vminu2(__vminu2(prev, cur), next);
             prev = cur;
             cur = next;
           }
-          dst[base + (RS - 1) * st] = cur;
         }
         __syncthreads();
-        std::uint16_t* t = src;
-        src = dst;
-        dst = t;
       }
       // store the tile in tiled order: output o = block-major, sub-cell minor
       std::uint16_t* out = (rep == 0 ? nbr3 : nbr5) + og.loff[0];
@@ -397,7 +404,7 @@ __global__ void __launch_bounds__(256) k_nbr_tiles(const OwnerGrid<D>* __restric
           r += (t + 2) * mul;
           mul *= RS;
         }
-        if (in) out[gindex(c)] = src[r];
+        if (in) out[gindex(c)] = nbr_unpack(buf[r]);
       }
     }
     __syncthreads();  // the buffers are reloaded for the next tile
