@@ -673,6 +673,9 @@ __device__ __forceinline__ bool octant_proof(const OwnerGrid<D>& og, const Borde
     side[d] = f < 0.5f ? -1 : 1;
     gap[d] = f < 0.5f ? f : 1.f - f;
   }
+  // all the neighbours' codes are loaded before any is tested (one memory
+  // latency instead of up to 2^D - 1 in a row)
+  std::uint16_t code[(1 << D) - 1];
 #pragma unroll
   for (int k = 1; k < (1 << D); ++k) {
     int cn[D];
@@ -685,11 +688,12 @@ __device__ __forceinline__ bool octant_proof(const OwnerGrid<D>& og, const Borde
       ok = ok && cn[d] >= 0 && cn[d] < og.ldims[0][d];
       d2 += move ? gap[d] * gap[d] : 0.f;
     }
-    if (!ok || !(d2 * 1.000002f + 1e-12f < reach2)) continue;
-    const std::uint16_t code = a.owner[og_index<D>(og, 0, cn)];
-    if (code != kOwnerEmpty && code != self) return true;
+    code[k - 1] = (ok && d2 * 1.000002f + 1e-12f < reach2) ? __ldg(a.owner + og_index<D>(og, 0, cn)) : kOwnerEmpty;
   }
-  return false;
+  bool hit = false;
+#pragma unroll
+  for (int k = 0; k < (1 << D) - 1; ++k) hit = hit || (code[k] != kOwnerEmpty && code[k] != self);
+  return hit;
 }
 
 template <int D>
