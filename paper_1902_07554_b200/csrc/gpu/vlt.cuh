@@ -65,7 +65,12 @@ __device__ __forceinline__ bool dominated_f(const float* rs, const float* rt, co
     slope = __fadd_rn(slope, __fmul_rn(fabsf(__fsub_rn(rt[d], rs[d])), hw[d]));
   }
   const float fmin_ = __fsub_rn(__fsub_rn(ds, dt), __fmul_rn(2.f, slope));
-  const float a = __fadd_rn(sqrtf(ds), H), b = __fadd_rn(sqrtf(dt), H);
+  // |c-s| + H and |c-t| + H only scale the safety margin: MUFU square roots
+  // (within 2^-22 relative) rounded up by 1e-6 can only raise it
+  float ra, rb;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(ra) : "f"(ds));
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(rb) : "f"(dt));
+  const float a = __fadd_ru(ra * 1.000001f, H), b = __fadd_ru(rb * 1.000001f, H);
   return fmin_ > 1e-5f * (a * a + b * b);
 }
 
