@@ -445,17 +445,13 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
       int dom[3];
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        float bdv = ld[0];
-        int bjv = lj[0];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const float od = __shfl_xor_sync(0xffffffffu, bdv, o);
-          const int oj = __shfl_xor_sync(0xffffffffu, bjv, o);
-          if (od < bdv || (od == bdv && oj < bjv)) {
-            bdv = od;
-            bjv = oj;
-          }
-        }
+        // argmin of (distance, index) over the lanes' heads: distances are
+        // >= 0 (or +inf), so their bit patterns order like the values; two
+        // warp reductions (min distance, then min index among the ties)
+        const unsigned bits = __float_as_uint(ld[0]);
+        const unsigned mb = __reduce_min_sync(0xffffffffu, bits);
+        const int bjv = static_cast<int>(
+            __reduce_min_sync(0xffffffffu, bits == mb ? static_cast<unsigned>(lj[0]) : 0x7fffffffu));
         dom[k] = bjv;
         if (lj[0] == bjv && bjv != 0x7fffffff) {  // the winning lane pops its head
           ld[0] = ld[1];
