@@ -1133,9 +1133,9 @@ __device__ bool warp_descent(const OwnerGrid<D>& og, const std::uint16_t* __rest
     if (static_cast<int>(lane) < total) {
       int rem = static_cast<int>(lane);
 #pragma unroll
-      for (int d = 0; d < D; ++d) {
-        cc[d] = s0[d] + rem % n0[d];
-        rem /= n0[d];
+      for (int d = 0; d < D; ++d) {  // n0[d] is 1 or 2
+        cc[d] = s0[d] + (n0[d] == 2 ? (rem & 1) : 0);
+        rem = n0[d] == 2 ? rem >> 1 : rem;
       }
       const std::uint16_t code = owner[og_index<D>(og, L0, cc)];
       if (code != kOwnerEmpty && code != self) r = test(L0, cc);
