@@ -868,9 +868,13 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
   for (int d = 1; d < D; ++d) bst[d] = bst[d - 1] * static_cast<unsigned long long>(multi_level ? og.ldims[1][d - 1] : 1);
   unsigned char* nz = nzl[wid];
   const unsigned full = 0xffffffffu;
+  // the next batch is claimed while this one is processed (the atomic's
+  // round trip on the shared cursor overlaps the work)
+  unsigned base = claim_batch(next);
   for (;;) {
-    const unsigned base = claim_batch(next);
     if (base >= ncand) break;
+    unsigned nclaim = 0;
+    if (lane == 0) nclaim = atomicAdd(next, 32u);
     const unsigned t = base + lane;
     const std::uint32_t crow = t < ncand ? cand[t] : kNoRow;
     const bool has = crow != kNoRow;
@@ -1062,6 +1066,7 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
 #pragma unroll
         for (int j = 0; j <= D; ++j) a.vflags[v[j]] = 1;
     }
+    base = __shfl_sync(full, nclaim, 0);
   }
   rewind_cursor(next, fin, ncand);
 }
