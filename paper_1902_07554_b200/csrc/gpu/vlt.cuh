@@ -257,11 +257,14 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
     const long long cell = DENSE ? static_cast<long long>(dq[item]) : item;
     int cc[D];
     {
-      long long rem = cell;
+      // 32-bit: the sample grid has at most 2 m + 1024 cells
+      unsigned rem = static_cast<unsigned>(cell);
 #pragma unroll
       for (int d = 0; d < D; ++d) {
-        cc[d] = static_cast<int>(rem % g.dims[d]);
-        rem /= g.dims[d];
+        const unsigned dd = static_cast<unsigned>(g.dims[d]);
+        const unsigned qd = rem / dd;
+        cc[d] = static_cast<int>(rem - qd * dd);
+        rem = qd;
       }
     }
     double c[D];
