@@ -302,28 +302,38 @@ namespace sbdt_gpu {
 constexpr int kBucketTile = 4096;  // points per CTA tile
 constexpr int kBucketThreads = 256;
 
-__global__ void k_bucket_count(const std::uint32_t* __restrict__ labels, std::uint64_t n, std::uint32_t k,
-                               std::uint32_t* __restrict__ tile_counts /* [k][tiles] */, std::uint32_t tiles) {
+// Both bucketing kernels work on the labels [l0, l0 + kl) (kl <= kBucketLabels,
+// so the shared histograms fit for any k; larger k takes several passes).
+constexpr std::uint32_t kBucketLabels = 1024;
+
+__global__ void k_bucket_count(const std::uint32_t* __restrict__ labels, std::uint64_t n, std::uint32_t l0,
+                               std::uint32_t kl, std::uint32_t* __restrict__ tile_counts /* [k][tiles] */,
+                               std::uint32_t tiles) {
   extern __shared__ std::uint32_t hist[];
-  for (std::uint32_t j = threadIdx.x; j < k; j += blockDim.x) hist[j] = 0;
+  for (std::uint32_t j = threadIdx.x; j < kl; j += blockDim.x) hist[j] = 0;
   __syncthreads();
   const std::uint64_t base = std::uint64_t(blockIdx.x) * kBucketTile;
   for (int t = threadIdx.x; t < kBucketTile; t += blockDim.x) {
     const std::uint64_t i = base + t;
-    if (i < n) atomicAdd(&hist[labels[i]], 1u);
+    if (i < n) {
+      const std::uint32_t l = labels[i] - l0;
+      if (l < kl) atomicAdd(&hist[l], 1u);
+    }
   }
   __syncthreads();
-  for (std::uint32_t j = threadIdx.x; j < k; j += blockDim.x) tile_counts[std::uint64_t(j) * tiles + blockIdx.x] = hist[j];
+  for (std::uint32_t j = threadIdx.x; j < kl; j += blockDim.x)
+    tile_counts[std::uint64_t(l0 + j) * tiles + blockIdx.x] = hist[j];
 }
 
 // Stable scatter: each warp owns a contiguous slice of the tile; per-warp
 // label histograms give exact in-order ranks.
 __global__ void __launch_bounds__(kBucketThreads) k_bucket_scatter(const std::uint32_t* __restrict__ labels,
-                                                                   std::uint64_t n, std::uint32_t k,
+                                                                   std::uint64_t n, std::uint32_t l0,
+                                                                   std::uint32_t k,
                                                                    const std::uint32_t* __restrict__ tile_offsets,
                                                                    std::uint32_t tiles,
                                                                    std::uint32_t* __restrict__ part_ids) {
-  extern __shared__ std::uint32_t sh[];  // [warps][k]
+  extern __shared__ std::uint32_t sh[];  // [warps][k], labels l0 .. l0 + k - 1
   constexpr int kWarps = kBucketThreads / 32;
   constexpr int kSlice = kBucketTile / kWarps;
   const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
@@ -332,12 +342,15 @@ __global__ void __launch_bounds__(kBucketThreads) k_bucket_scatter(const std::ui
   const std::uint64_t base = std::uint64_t(blockIdx.x) * kBucketTile + std::uint64_t(warp) * kSlice;
   for (int t = lane; t < kSlice; t += 32) {
     const std::uint64_t i = base + t;
-    if (i < n) atomicAdd(&sh[warp * k + labels[i]], 1u);
+    if (i < n) {
+      const std::uint32_t l = labels[i] - l0;
+      if (l < k) atomicAdd(&sh[warp * k + l], 1u);
+    }
   }
   __syncthreads();
   // exclusive scan across warps per label, plus the tile's global offset
   for (std::uint32_t j = threadIdx.x; j < k; j += blockDim.x) {
-    std::uint32_t run = tile_offsets[std::uint64_t(j) * tiles + blockIdx.x];
+    std::uint32_t run = tile_offsets[std::uint64_t(l0 + j) * tiles + blockIdx.x];
     for (int w = 0; w < kWarps; ++w) {
       const std::uint32_t c = sh[w * k + j];
       sh[w * k + j] = run;
@@ -347,8 +360,9 @@ __global__ void __launch_bounds__(kBucketThreads) k_bucket_scatter(const std::ui
   __syncthreads();
   for (int t0 = 0; t0 < kSlice; t0 += 32) {
     const std::uint64_t i = base + t0 + lane;
-    const bool valid = i < n;
-    const std::uint32_t lab = valid ? labels[i] : 0xFFFFFFFFu;
+    const std::uint32_t l = i < n ? labels[i] - l0 : 0xFFFFFFFFu;
+    const bool valid = l < k;
+    const std::uint32_t lab = valid ? l : 0xFFFFFFFFu;
     const unsigned peers = __match_any_sync(0xffffffffu, lab);
     const unsigned rank = __popc(peers & ((1u << lane) - 1u));
     const int leader = __ffs(peers) - 1;
@@ -504,12 +518,20 @@ int bucket_impl(sbdt_gpu_ctx* ctx, const std::uint32_t* d_labels, std::uint64_t 
   const std::uint64_t cells = std::uint64_t(k) * tiles;
   SBDT_WS(tc, std::uint32_t, "bucket.tc", cells + 1);
   SBDT_WS(bs, std::uint32_t, "bucket.bs", (cells + 1) / kScanTile + 2);
-  k_bucket_count<<<tiles, kBucketThreads, sizeof(std::uint32_t) * k, st>>>(d_labels, n, k, tc, tiles);
+  for (std::uint32_t l0 = 0; l0 < k; l0 += kBucketLabels) {
+    const std::uint32_t kl = k - l0 < kBucketLabels ? k - l0 : kBucketLabels;
+    k_bucket_count<<<tiles, kBucketThreads, sizeof(std::uint32_t) * kl, st>>>(d_labels, n, l0, kl, tc, tiles);
+    ++ctx->launches;
+  }
   exclusive_scan(tc, tc, cells, bs, nullptr, st, &ctx->launches);
   k_part_offsets<<<1, 256, 0, st>>>(tc, k, tiles, n, d_part_offsets);
-  k_bucket_scatter<<<tiles, kBucketThreads, sizeof(std::uint32_t) * k * (kBucketThreads / 32), st>>>(
-      d_labels, n, k, tc, tiles, d_part_ids);
-  ctx->launches += 3;
+  ++ctx->launches;
+  for (std::uint32_t l0 = 0; l0 < k; l0 += kBucketLabels) {
+    const std::uint32_t kl = k - l0 < kBucketLabels ? k - l0 : kBucketLabels;
+    k_bucket_scatter<<<tiles, kBucketThreads, sizeof(std::uint32_t) * kl * (kBucketThreads / 32), st>>>(
+        d_labels, n, l0, kl, tc, tiles, d_part_ids);
+    ++ctx->launches;
+  }
   SBDT_CUDA_TRY(cudaGetLastError());
   return kOk;
 }

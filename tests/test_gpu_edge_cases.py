@@ -167,3 +167,19 @@ def test_exact_policy_partition_without_rows(ctx):
     assert np.array_equal(g.positive, o["positive"])
     assert np.array_equal(g.border, o["border"])
     assert np.array_equal(g.positive_vertex_ids, o["vertices_positive"])
+
+
+def test_bucketing_many_partitions(ctx):
+    """k = 3000 > the shared-memory label chunk of the bucketing kernels (1024):
+    Partitioning.parts over several label passes, ids ascending per part."""
+    rng = np.random.default_rng(11)
+    pts = np.ascontiguousarray(rng.random((200_000, 3)))
+    sid = np.sort(rng.choice(len(pts), 6000, replace=False)).astype(np.uint32)
+    slab = (np.arange(6000) % 3000).astype(np.uint32)
+    part = gpu.assign_points(pts, sid, slab, 3000, ctx=ctx)
+    ref = oracle.assign_brute(pts, sid, slab)
+    assert np.array_equal(part.labels, ref)
+    order = np.lexsort((np.arange(len(ref)), ref)).astype(np.uint32)
+    counts = np.bincount(ref, minlength=3000)
+    assert np.array_equal(part.parts_offsets, np.concatenate([[0], np.cumsum(counts)]).astype(np.uint64))
+    assert np.array_equal(part.parts_ids, order)
