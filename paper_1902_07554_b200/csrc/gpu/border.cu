@@ -31,6 +31,7 @@
 namespace sbdt_gpu {
 
 constexpr int kBThreads = 256;
+constexpr std::uint32_t kSmemOffsMax = 1024;  // part offsets staged in shared memory up to this many (k + 1)
 
 __global__ void k_bbox_points_init(unsigned long long* bbox, int dim) {
   if (threadIdx.x < static_cast<unsigned>(dim)) {
@@ -377,6 +378,19 @@ __device__ __forceinline__ std::uint32_t part_of(const std::uint64_t* offs, std:
   return lo;
 }
 
+// The part offsets of a kernel: staged in shared memory when k + 1 <=
+// kSmemOffsMax, else read in place (an explicit, warp-uniform branch keeps
+// the common case on shared-memory loads rather than generic ones).
+struct PartOffs {
+  const std::uint64_t* sh;
+  const std::uint64_t* gl;
+  bool small;
+  __device__ __forceinline__ std::uint64_t operator[](std::uint32_t j) const { return small ? sh[j] : __ldg(gl + j); }
+  __device__ __forceinline__ std::uint32_t part(std::uint32_t k, std::uint64_t s) const {
+    return small ? part_of(sh, k, s) : part_of(gl, k, s);
+  }
+};
+
 // part_of for a warp of consecutive rows: one binary search by lane 0, the
 // lanes outside that part (warps straddling a part boundary) search alone.
 // Must be called by the full warp.
@@ -504,10 +518,13 @@ __device__ __forceinline__ bool bbox_policy_sphere(const OwnerGrid<D>& og, const
 template <int D>
 __global__ void __launch_bounds__(kBThreads) k_border_finite(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp) {
   __shared__ OwnerGrid<D> og;
-  extern __shared__ std::uint64_t s_off[];
+  extern __shared__ std::uint64_t s_off_sh[];
   if (threadIdx.x == 0) og = *ogp;
-  for (std::uint32_t j = threadIdx.x; j <= a.k; j += blockDim.x) s_off[j] = a.offsets[j];
+  if (a.k + 1 <= kSmemOffsMax)
+    for (std::uint32_t j = threadIdx.x; j <= a.k; j += blockDim.x) s_off_sh[j] = a.offsets[j];
   __syncthreads();
+  // part offsets in shared memory, or read in place for very large k
+  const PartOffs s_off{s_off_sh, a.offsets, a.k + 1 <= kSmemOffsMax};
   for (std::uint64_t s = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; s < a.S;
        s += std::uint64_t(gridDim.x) * blockDim.x) {
     std::uint32_t v[D + 1];
@@ -518,7 +535,7 @@ __global__ void __launch_bounds__(kBThreads) k_border_finite(BorderArgs a, const
       a.inf_queue[slot] = static_cast<std::uint32_t>(s);
       continue;
     }
-    const std::uint32_t self = part_of(s_off, a.k, s);
+    const std::uint32_t self = s_off.part(a.k, s);
     double p[D + 1][D];
 #pragma unroll
     for (int j = 0; j <= D; ++j)
@@ -696,16 +713,19 @@ __device__ __forceinline__ bool octant_proof(const OwnerGrid<D>& og, const Borde
   return hit;
 }
 
-template <int D>
+template <int D, bool BIGK>
 __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
                                                                 std::uint32_t* __restrict__ cand, std::uint64_t cap,
                                                                 unsigned* __restrict__ ncand, std::uint64_t row_begin,
                                                                 std::uint64_t row_end) {
   __shared__ OwnerGrid<D> og;
-  extern __shared__ std::uint64_t s_off[];
+  extern __shared__ std::uint64_t s_off_sh[];
   if (threadIdx.x == 0) og = *ogp;
-  for (std::uint32_t j = threadIdx.x; j <= a.k; j += blockDim.x) s_off[j] = a.offsets[j];
+  if constexpr (!BIGK)
+    for (std::uint32_t j = threadIdx.x; j <= a.k; j += blockDim.x) s_off_sh[j] = a.offsets[j];
   __syncthreads();
+  // part offsets in shared memory, or read in place for very large k (BIGK)
+  const std::uint64_t* s_off = BIGK ? a.offsets : s_off_sh;
   const unsigned lane = threadIdx.x & 31u;
   const unsigned lt = (1u << lane) - 1u;
   const std::uint64_t stride = std::uint64_t(gridDim.x) * blockDim.x;
@@ -853,10 +873,13 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
   __shared__ OwnerGrid<D> og;
   __shared__ CandSlot<D> slots[kExactWarps][32];
   __shared__ unsigned char nzl[kExactWarps][32];
-  extern __shared__ std::uint64_t s_off[];
+  extern __shared__ std::uint64_t s_off_sh[];
   if (threadIdx.x == 0) og = *ogp;
-  for (std::uint32_t j = threadIdx.x; j <= a.k; j += blockDim.x) s_off[j] = a.offsets[j];
+  if (a.k + 1 <= kSmemOffsMax)
+    for (std::uint32_t j = threadIdx.x; j <= a.k; j += blockDim.x) s_off_sh[j] = a.offsets[j];
   __syncthreads();
+  // part offsets in shared memory, or read in place for very large k
+  const PartOffs s_off{s_off_sh, a.offsets, a.k + 1 <= kSmemOffsMax};
   const unsigned ncand = *ncand_p;
   const unsigned lane = threadIdx.x & 31u;
   const unsigned wid = threadIdx.x >> 5;
@@ -886,7 +909,7 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
     bool pre_pos = false;
     if (has) {
       s = crow;
-      self = part_of(s_off, a.k, s);
+      self = s_off.part(a.k, s);
 #pragma unroll
       for (int j = 0; j <= D; ++j) v[j] = cand[std::uint64_t(j + 1) * cap + t];
       bool proven = false;
@@ -1251,10 +1274,13 @@ __global__ void __launch_bounds__(kWideWarps * 32, 6) k_border_wide(BorderArgs a
                                                                  const unsigned* __restrict__ nlight_p) {
   __shared__ OwnerGrid<D> og;
   __shared__ WideEntry<D> stacks[kWideWarps][kWideStack];
-  extern __shared__ std::uint64_t s_off[];
+  extern __shared__ std::uint64_t s_off_sh[];
   if (threadIdx.x == 0) og = *ogp;
-  for (std::uint32_t j = threadIdx.x; j <= a.k; j += blockDim.x) s_off[j] = a.offsets[j];
+  if (a.k + 1 <= kSmemOffsMax)
+    for (std::uint32_t j = threadIdx.x; j <= a.k; j += blockDim.x) s_off_sh[j] = a.offsets[j];
   __syncthreads();
+  // part offsets in shared memory, or read in place for very large k
+  const PartOffs s_off{s_off_sh, a.offsets, a.k + 1 <= kSmemOffsMax};
   // rows [0, nheavy) from the front of the queue, then the nlight rows
   // stored from the back (see k_border_exact)
   const unsigned nheavy = *nwide_p;
@@ -1275,7 +1301,7 @@ __global__ void __launch_bounds__(kWideWarps * 32, 6) k_border_wide(BorderArgs a
     if (has) {
       const std::uint64_t slot = t < nheavy ? t : cap - 1 - (t - nheavy);
       s = wide[slot];
-      self = part_of(s_off, a.k, s);
+      self = s_off.part(a.k, s);
 #pragma unroll
       for (int j = 0; j <= D; ++j) v[j] = wide[std::uint64_t(j + 1) * cap + slot];
       double p[D + 1][D];
@@ -1333,10 +1359,13 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_border_infinite(BorderArgs 
                                                                      unsigned* __restrict__ fin) {
   __shared__ OwnerGrid<D> og;
   __shared__ WideEntry<D> stacks[kWideWarps][kWideStack];
-  extern __shared__ std::uint64_t s_off[];
+  extern __shared__ std::uint64_t s_off_sh[];
   if (threadIdx.x == 0) og = *ogp;
-  for (std::uint32_t j = threadIdx.x; j <= a.k; j += blockDim.x) s_off[j] = a.offsets[j];
+  if (a.k + 1 <= kSmemOffsMax)
+    for (std::uint32_t j = threadIdx.x; j <= a.k; j += blockDim.x) s_off_sh[j] = a.offsets[j];
   __syncthreads();
+  // part offsets in shared memory, or read in place for very large k
+  const PartOffs s_off{s_off_sh, a.offsets, a.k + 1 <= kSmemOffsMax};
   const unsigned full = 0xffffffffu;
   const unsigned lane = threadIdx.x & 31u;
   WideEntry<D>* stk = stacks[threadIdx.x >> 5];
@@ -1354,7 +1383,7 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_border_infinite(BorderArgs 
     double fx[D][D];  // facet vertex coordinates
     if (has) {
       s = a.inf_queue[q];
-      self = part_of(s_off, a.k, s);
+      self = s_off.part(a.k, s);
 #pragma unroll
       for (int j = 0; j < D; ++j) fv[j] = a.verts[std::uint64_t(j) * a.S + s];
       const std::uint64_t owner_row = s_off[self] + a.nbrs[std::uint64_t(D) * a.S + s];
@@ -1724,9 +1753,14 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   {
     const std::uint64_t want = (in->n + 255) / 256;
     const unsigned blocks = static_cast<unsigned>(want < std::uint64_t(sms) * 16 ? want : std::uint64_t(sms) * 16);
-    const std::size_t sh = pbbox ? sizeof(unsigned long long) * in->k * 2 * D : 0;
-    k_owner_mark<D><<<blocks > 0 ? blocks : 1, 256, sh, st>>>(in->d_xyz, in->d_labels, in->n, og, owner, pbbox, in->k,
-                                                               xq);
+    const bool pb_sh = pbbox && in->k * 2 * D <= kPbboxSmem;
+    const std::size_t sh = pb_sh ? sizeof(unsigned long long) * in->k * 2 * D : 0;
+    k_owner_mark<D><<<blocks > 0 ? blocks : 1, 256, sh, st>>>(in->d_xyz, in->d_labels, in->n, og, owner,
+                                                               pb_sh ? pbbox : nullptr, in->k, xq);
+    if (pbbox && !pb_sh) {
+      k_pbbox_global<D><<<blocks > 0 ? blocks : 1, 256, 0, st>>>(in->d_xyz, in->d_labels, in->n, pbbox);
+      ++ctx->launches;
+    }
   }
   k_owner_level<D><<<sms * 8, 256, 0, st>>>(og, owner, 1);
   k_owner_level<D><<<sms * 2, 256, 0, st>>>(og, owner, 2);
@@ -1837,7 +1871,7 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
     SBDT_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 12, st));
     a.counters = cnt;
   }
-  const std::size_t offs_sh = sizeof(std::uint64_t) * (in->k + 1);
+  const std::size_t offs_sh = in->k + 1 <= kSmemOffsMax ? sizeof(std::uint64_t) * (in->k + 1) : 0;
   SBDT_WS(icur, unsigned, "border.inf_cursor", 2);  // {cursor, CTAs done}
   SBDT_CUDA_TRY(cudaMemsetAsync(icur, 0, 2 * sizeof(unsigned), st));
   auto infinite = [&](cudaStream_t on) {
@@ -1854,7 +1888,9 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
     {
       if (tiled && in->S > 0) {
         int per_sm = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_prefilter<D>, kBThreads, offs_sh);
+        const bool bigk = in->k + 1 > kSmemOffsMax;
+        if (bigk) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_prefilter<D, true>, kBThreads, 0);
+        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_prefilter<D, false>, kBThreads, offs_sh);
         const std::uint64_t resA = std::uint64_t(sms) * std::uint64_t(per_sm > 0 ? per_sm : 1);
         // candidates <= rows, plus < kQChunk holes per prefilter warp and launch
         const std::uint64_t launches_A = ctx->chunks.empty() ? 1 : ctx->chunks.size();
@@ -1881,8 +1917,12 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
         const unsigned resW = static_cast<unsigned>(sms * (per_sm > 0 ? per_sm : 1));
         auto prefilter = [&](std::uint64_t r0, std::uint64_t r1) {
           const std::uint64_t want = (r1 - r0 + kBThreads - 1) / kBThreads;
-          k_border_prefilter<D><<<static_cast<unsigned>(want < resA ? want : resA), kBThreads, offs_sh, st>>>(
-              a, og, cq, qcap, cn, r0, r1);
+          if (bigk)
+            k_border_prefilter<D, true><<<static_cast<unsigned>(want < resA ? want : resA), kBThreads, 0, st>>>(
+                a, og, cq, qcap, cn, r0, r1);
+          else
+            k_border_prefilter<D, false><<<static_cast<unsigned>(want < resA ? want : resA), kBThreads, offs_sh, st>>>(
+                a, og, cq, qcap, cn, r0, r1);
         };
         auto exact = [&]() {
           if (exact_policy)

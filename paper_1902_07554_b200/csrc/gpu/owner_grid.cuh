@@ -411,6 +411,25 @@ __global__ void __launch_bounds__(256) k_nbr_tiles(const OwnerGrid<D>* __restric
   }
 }
 
+// bbox policy with more partitions than k_owner_mark stages in shared
+// memory: the partition bboxes by global atomics (ordered keys).
+constexpr std::uint32_t kPbboxSmem = 3072;  // [k][2D] words k_owner_mark stages in shared memory (24 KB)
+
+template <int D>
+__global__ void k_pbbox_global(const double* __restrict__ xyz, const std::uint32_t* __restrict__ labels,
+                               std::uint64_t n, unsigned long long* __restrict__ pbbox) {
+  for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += std::uint64_t(gridDim.x) * blockDim.x) {
+    const std::uint32_t lab = labels[i];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const unsigned long long o = dbl_to_ordered(xyz[i * D + d]);
+      atomicMin(&pbbox[lab * 2 * D + d], o);
+      atomicMax(&pbbox[lab * 2 * D + D + d], o);
+    }
+  }
+}
+
 // EMPTY over the entries the grid actually uses (loff[levels], known only on
 // the device) instead of the worst-case capacity.
 template <int D>

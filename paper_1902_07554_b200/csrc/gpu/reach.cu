@@ -80,16 +80,20 @@ __global__ void k_reach_init(ReachArgs a) {
   }
 }
 
+constexpr std::uint32_t kReachSmemOffs = 1024;  // part offsets staged in shared memory up to this many (k + 1)
+
 __global__ void k_reach_hook(ReachArgs a) {
-  extern __shared__ std::uint64_t s_off[];
-  for (std::uint32_t j = threadIdx.x; j <= a.k; j += blockDim.x) s_off[j] = a.offsets[j];
+  extern __shared__ std::uint64_t s_off_sh[];
+  if (a.k + 1 <= kReachSmemOffs)
+    for (std::uint32_t j = threadIdx.x; j <= a.k; j += blockDim.x) s_off_sh[j] = a.offsets[j];
   __syncthreads();
+  const bool small = a.k + 1 <= kReachSmemOffs;  // else in place (very large k)
   const std::uint64_t P = *a.pos_count;
   const int D = a.dim;
   for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < P;
        i += std::uint64_t(gridDim.x) * blockDim.x) {
     const std::uint64_t s = a.pos_ids[i];
-    const std::uint64_t off = s_off[part_of_row(s_off, a.k, s)];
+    const std::uint64_t off = small ? s_off_sh[part_of_row(s_off_sh, a.k, s)] : a.offsets[part_of_row(a.offsets, a.k, s)];
     for (int d = 0; d <= D; ++d) {
       const std::uint64_t nb = off + a.nbrs[std::uint64_t(d) * a.S + s];
       if (nb < s && a.positive[nb]) unite(a.parent, static_cast<std::uint32_t>(i), a.cidx[nb]);
@@ -99,9 +103,11 @@ __global__ void k_reach_hook(ReachArgs a) {
 
 // hull seed test (triangulation.cpp:34-53) + root mark
 __global__ void k_reach_mark(ReachArgs a) {
-  extern __shared__ std::uint64_t s_off[];
-  for (std::uint32_t j = threadIdx.x; j <= a.k; j += blockDim.x) s_off[j] = a.offsets[j];
+  extern __shared__ std::uint64_t s_off_sh[];
+  if (a.k + 1 <= kReachSmemOffs)
+    for (std::uint32_t j = threadIdx.x; j <= a.k; j += blockDim.x) s_off_sh[j] = a.offsets[j];
   __syncthreads();
+  const bool small = a.k + 1 <= kReachSmemOffs;  // else in place (very large k)
   const std::uint64_t P = *a.pos_count;
   const int D = a.dim;
   for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < P;
@@ -109,7 +115,7 @@ __global__ void k_reach_mark(ReachArgs a) {
     const std::uint64_t s = a.pos_ids[i];
     bool hull = a.verts[std::uint64_t(D) * a.S + s] == kInfVertex;
     if (!hull) {
-      const std::uint64_t off = s_off[part_of_row(s_off, a.k, s)];
+      const std::uint64_t off = small ? s_off_sh[part_of_row(s_off_sh, a.k, s)] : a.offsets[part_of_row(a.offsets, a.k, s)];
       for (int d = 0; d <= D && !hull; ++d) {
         const std::uint64_t nb = off + a.nbrs[std::uint64_t(d) * a.S + s];
         hull = a.verts[std::uint64_t(D) * a.S + nb] == kInfVertex;
@@ -152,7 +158,7 @@ int reach_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   ReachArgs a{in->dim, in->k, in->d_offsets, in->d_verts, in->d_nbrs, in->S, in->d_positive, pos_ids, pos_count,
               cidx, parent, mark, in->d_border, in->d_bfs_vertex_flags};
   const unsigned blocks = static_cast<unsigned>(sms) * 8;
-  const std::size_t sh = sizeof(std::uint64_t) * (in->k + 1);
+  const std::size_t sh = in->k + 1 <= kReachSmemOffs ? sizeof(std::uint64_t) * (in->k + 1) : 0;
   k_reach_init<<<blocks, 256, 0, st>>>(a);
   k_reach_hook<<<blocks, 256, sh, st>>>(a);
   k_reach_mark<<<blocks, 256, sh, st>>>(a);

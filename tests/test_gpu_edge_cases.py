@@ -183,3 +183,17 @@ def test_bucketing_many_partitions(ctx):
     counts = np.bincount(ref, minlength=3000)
     assert np.array_equal(part.parts_offsets, np.concatenate([[0], np.cumsum(counts)]).astype(np.uint64))
     assert np.array_equal(part.parts_ids, order)
+
+
+def test_find_border_many_partitions(ctx):
+    """k = 1200: the part offsets no longer fit the kernels' shared memory and
+    the bbox policy's per-partition boxes go straight to global memory."""
+    inst = host.make_instance(dict(name="manyk", dist="uniform", dim=3, n=60_000, seed=5, frac=0.05, k=1200))
+    lab = oracle.assign_kdtree(inst.points, inst.sample_ids, inst.sample_labels)
+    P = host.build_partials(inst.points, lab, 1200, 3)
+    for policy in ("grid", "bbox", "exact"):
+        g = gpu.find_border(inst.points, lab, P, gpu.IntersectionPolicy(policy, 1.0), hull_bfs=True, ctx=ctx)
+        o = oracle.find_border(inst.points, lab, P, policy)
+        assert np.array_equal(g.positive, o["positive"]), policy
+        assert np.array_equal(g.border, o["border"]), policy
+        assert np.array_equal(g.positive_vertex_ids, o["vertices_positive"]), policy
