@@ -976,10 +976,12 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
     if (mode == 1) {
 #pragma unroll
       for (int d = 0; d < D; ++d) {
+        // the range lies in the grid (cell + 1 <= dims), so the upper bound of
+        // a cell is the lower bound of the next: one cell_lo per boundary
+        double bhi = cell_lo<D>(og.g, lo[d], d);
         for (int i = 0; i < span[d]; ++i) {
-          const int cell = lo[d] + i;
-          const long long last1 = (static_cast<long long>(cell) + 1) > og.g.dims[d] ? og.g.dims[d] : cell + 1;
-          const double blo = cell_lo<D>(og.g, cell, d), bhi = cell_lo<D>(og.g, last1, d);
+          const double blo = bhi;
+          bhi = cell_lo<D>(og.g, lo[d] + i + 1, d);
           double g = 0.0;
           if (c[d] < blo) g = blo - c[d];
           else if (c[d] > bhi) g = c[d] - bhi;
