@@ -747,6 +747,7 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
   // this row's coordinates are gathered and tested
   std::uint64_t s = row_begin + std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   std::uint32_t self = part_of(s_off, a.k, s < row_end ? s : row_end - 1);
+  std::uint64_t next_off = self + 1 < a.k ? s_off[self + 1] : ~0ull;  // first row of the next part
   std::uint32_t vn[D + 1];
   auto load_ids = [&](std::uint64_t r, std::uint32_t* ids) {
 #pragma unroll
@@ -770,7 +771,10 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
     // rows only grow along the grid-stride loop: advance the part cursor
     {
       const std::uint64_t sc = valid ? s : row_end - 1;
-      while (self + 1 < a.k && s_off[self + 1] <= sc) ++self;
+      while (next_off <= sc) {
+        ++self;
+        next_off = self + 1 < a.k ? s_off[self + 1] : ~0ull;
+      }
     }
     if (valid && !inf) {
       float A[D][D], P0e[D], eta;
@@ -989,7 +993,9 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
         }
         sl[lane].lo[d] = lo[d];
         sl[lane].span[d] = static_cast<unsigned>(span[d]);
-        sl[lane].inv[d] = (65536u + static_cast<unsigned>(span[d]) - 1u) / static_cast<unsigned>(span[d]);
+        // ceil(2^16 / span) for span <= kFlatSpan: the correctly rounded
+        // binary32 quotient is exact or >= 0.1 away from an integer
+        sl[lane].inv[d] = static_cast<unsigned>(ceilf(__fdiv_rn(65536.f, static_cast<float>(span[d]))));
       }
       sl[lane].r2 = r2;
       sl[lane].self = self;
