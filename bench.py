@@ -43,7 +43,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-budget-s", type=float, default=20.0, help="CPU work per baseline step (seconds, approx.)")
+    ap.add_argument("--ref-budget-s", type=float, default=180.0,
+                    help="--impl reference: wall budget for the timed full CPU steps (at least 3 run)")
+    ap.add_argument("--no-parity", action="store_true", help="skip the full-size parity leg (and the CPU baseline)")
     ap.add_argument("--profile", action="store_true", help="single short run for ncu (no baseline/e2e)")
     ap.add_argument("--no-graph", action="store_true",
                     help="time launched steps only (default: the headline times the step replayed as one CUDA graph)")
@@ -141,43 +143,78 @@ def algorithmic_bytes(dim, n, S, cells, n_vb):
     return b_assign, b_border
 
 
-def cpu_baseline(inst, labels, policy, budget_s, threads):
-    """The CPU oracle (restatement of SPEC assign_points / find_border on the
-    reference's algorithm) timed on a bounded sample of the same workload."""
+def config_dict(inst, policy, world, cells):
+    """The `config` of both arms (identical keys and values)."""
+    part = inst.partials
+    return {"workload": inst.config["name"], "n": inst.n, "dim": inst.dim, "k": inst.config["k"],
+            "m": len(inst.sample_ids), "S": part.S, "policy": f"{policy}(c_G=1)", "cells": cells,
+            "l2": "inputs > L2 (coords %d MB, simplices %d MB); the GPU arm also writes a 256 MB buffer (> L2) "
+                  "between steps" % (inst.points.nbytes >> 20, (part.verts.nbytes + part.nbrs.nbytes) >> 20),
+            "parallelism": f"{world} independent instance(s), one per rank"}
+
+
+def single_core(inst, labels, policy, budget_s=8.0):
+    """One host core (TaskPool(1), the reference's determinism baseline,
+    task_pool.hpp:20-21) on a bounded sample: the first points and the first
+    part, on the reference's compiled primitives (oracle/_ref) when built."""
     import oracle
-    n, S, k = inst.n, inst.partials.S, inst.config["k"]
-    # assignment sample sized to ~budget/3 seconds
+    n, k = inst.n, inst.config["k"]
     n_s = min(n, 200_000)
-    t0 = time.perf_counter()
-    oracle.assign_kdtree(inst.points[:n_s], inst.sample_ids, inst.sample_labels, threads)  # warm-up + estimate
-    est = (time.perf_counter() - t0) / n_s
-    n_s = int(min(n, max(200_000, (budget_s / 3) / max(est, 1e-9))))
-    lab = np.empty(n_s, np.uint32)
-    import ctypes as C
-    pts = np.ascontiguousarray(inst.points)
-    t0 = time.perf_counter()
-    oracle.lib().oracle_assign_kdtree_range(inst.dim, oracle._p(pts, C.c_double), 0, n_s,
-                                            oracle._p(inst.sample_ids, C.c_uint32), len(inst.sample_ids),
-                                            oracle._p(inst.sample_labels, C.c_uint32), oracle._p(lab, C.c_uint32),
-                                            threads)
-    t_assign = time.perf_counter() - t0
-    # border sample: `threads` partitions (one BFS task per partition, SPEC.md:529)
-    p_s = max(1, min(k, threads))
-    t_build, t_border, _ = oracle.time_border(inst.points, labels, inst.partials, policy, 1.0, threads, (0, p_s), 1)
-    S_s = int(inst.partials.offsets[p_s])
-    t_est = t_assign * (n / n_s) + t_border * (S / max(S_s, 1))
-    return dict(value=n / t_est, unit="points/s", cores=threads, kind="port",
-                sample=(f"oracle (SPEC restatement, kd-tree assign + per-part GridIndex/AABB find_border) on "
-                        f"{n_s} points assigned ({t_assign:.2f}s) and parts 0..{p_s - 1} = {S_s} simplices "
-                        f"border-tested ({t_border:.2f}s, index build {t_build:.2f}s excluded); "
-                        f"extrapolated to the full step ({t_est:.1f}s)"),
-                assign_points_per_s=n_s / t_assign, border_simplices_per_s=S_s / t_border, est_step_s=t_est)
+    r = oracle.ref_time_step(inst.points, inst.sample_ids, inst.sample_labels, labels, inst.partials, policy,
+                             threads=1, n_assign=n_s, parts=(0, 1))
+    kind = "reference"
+    if r is None:  # no oracle/_ref: the restatement on one thread
+        import time as _t
+        t0 = _t.perf_counter()
+        lab = np.empty(n_s, np.uint32)
+        oracle.assign_kdtree(inst.points[:n_s], inst.sample_ids, inst.sample_labels, 1)
+        ta = _t.perf_counter() - t0
+        o = oracle.find_border(inst.points, labels, inst.partials, policy, threads=1, parts=(0, 1))
+        r, kind = {"times": (ta, o["times"][0], o["times"][1])}, "port"
+    S1 = int(inst.partials.offsets[1])
+    return {"cores": 1, "kind": kind, "assign_points_per_s": n_s / r["times"][0],
+            "border_simplices_per_s": S1 / max(r["times"][2], 1e-9),
+            "sample": f"{n_s} points assigned ({r['times'][0]:.2f}s), part 0 = {S1} simplices border-tested "
+                      f"({r['times'][2]:.2f}s; its index build {r['times'][1]:.2f}s excluded)",
+            "est_step_s": n * r["times"][0] / n_s + inst.partials.S * r["times"][2] / max(S1, 1)}
+
+
+def parity_leg(inst, policy, threads, g):
+    """Full-size parity of this run's GPU outputs against the CPU oracle on
+    all host threads (oracle/parity.py), and the oracle's own measured times:
+    the CPU path over ALL n points and ALL k partials (not a sample)."""
+    from oracle import parity
+    res, _ = parity.check_labels(inst.points, inst.sample_ids, inst.sample_labels, inst.config["k"], g["labels"],
+                                 g["parts_offsets"], g["parts_ids"], threads)
+    res.update(parity.check_border(inst.points, g["labels"], inst.partials, g["positive"], g["border"],
+                                   g["positive_vertex_ids"], g["border_vertex_ids"], policy, threads))
+    res["all_equal"] = parity.all_equal(res)
+    res["checked"] = ("labels (all n), Partitioning.parts, positive + BFS border flags (all S rows), both vertex "
+                      "sets vs the CPU oracle, bit for bit")
+    return res
+
+
+def cpu_baseline_from(par, inst, threads, one_core):
+    import oracle
+    t_step = par["assign_s"] + par["border_s"]
+    return {"value": inst.n / t_step, "unit": "points/s", "cores": threads, "kind": "port",
+            "cpu_model": oracle.cpu_model(),
+            "sample": (f"full step measured, not extrapolated: all {inst.n} points assigned (kd-tree, "
+                       f"{par['assign_s']:.2f}s) + all {inst.partials.S} simplex rows of the {inst.config['k']} "
+                       f"partials border-tested (full scan + BFS, {par['border_s']:.2f}s; per-part GridIndex "
+                       f"build {par['index_build_s']:.2f}s excluded, it is an input of find_border)"),
+            "assign_points_per_s": inst.n / par["assign_s"],
+            "border_simplices_per_s": inst.partials.S / par["border_s"], "step_s": t_step,
+            "single_core": one_core}
 
 
 # ---------------------------------------------------------------------------
 def run_reference(args):
-    """--impl reference: the CPU path (oracle port of the reference algorithm;
-    the reference ships no hot-path code) on all host threads."""
+    """--impl reference: the CPU path on all host threads, full steps (all n
+    points, all k partials), measured. On the reference's own compiled
+    primitives (geometry.cpp) and TaskPool (oracle/_ref, kind "reference")
+    when built, else the restatement (kind "port"); the reference ships no
+    hot-path code of its own."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -186,21 +223,51 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     inst = host.make_instance(args.config, n=args.n, k=args.k)
     labels = oracle.assign_kdtree(inst.points, inst.sample_ids, inst.sample_labels, threads)
-    host.attach_partials(inst, labels)
-    per_step = max(2.0, min(args.cpu_budget_s, 150.0 / max(1, args.steps + args.warmup)))
-    vals, res = [], None
-    for i in range(args.warmup + args.steps):
-        res = cpu_baseline(inst, labels, args.policy, per_step, threads)
-        if i >= args.warmup:
-            vals.append(res["value"])
-    v = statistics.median(vals)
+    host.attach_partials(inst, labels, threads=threads)
+    cells = int(np.prod(oracle.grid_params(inst.points, 1.0)[3]))
+    kind = "reference" if oracle.ref_lib() is not None else "port"
+
+    def step():
+        if kind == "reference":
+            r = oracle.ref_time_step(inst.points, inst.sample_ids, inst.sample_labels, labels, inst.partials,
+                                     args.policy, threads=threads)
+            return r["times"]
+        t0 = time.perf_counter()
+        oracle.assign_kdtree(inst.points, inst.sample_ids, inst.sample_labels, threads)
+        ta = time.perf_counter() - t0
+        o = oracle.find_border(inst.points, labels, inst.partials, args.policy, threads=threads)
+        return (ta, o["times"][0], o["times"][1])
+
+    # full steps within a wall budget: one warm-up, then up to --steps timed
+    # steps (at least 3) while the budget lasts
+    t_begin = time.perf_counter()
+    step()
+    steps, ts = [], []
+    while len(steps) < max(1, args.steps):
+        ts.append(step())
+        steps.append(ts[-1][0] + ts[-1][2])
+        if len(steps) >= 3 and time.perf_counter() - t_begin > args.ref_budget_s:
+            break
+    t = statistics.median(steps)
+    v = inst.n / t
+    ta = statistics.median(x[0] for x in ts)
+    tb = statistics.median(x[2] for x in ts)
+    one = single_core(inst, labels, args.policy)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "points/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * inst.n / v, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json config)",
-            "config": {"workload": inst.config["name"], "n": inst.n, "k": inst.config["k"],
-                       "m": len(inst.sample_ids), "S": inst.partials.S, "policy": args.policy},
-            "cpu_baseline": {"value": v, "unit": "points/s", "cores": threads, "kind": "port",
-                             "sample": res["sample"]},
+            "steps": len(steps), "steps_requested": args.steps, "warmup": 1, "ms_per_step": 1e3 * t,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, BASELINE.json config)",
+            "config": config_dict(inst, args.policy, args.gpus, cells),
+            "cpu_baseline": {"value": v, "unit": "points/s", "cores": threads, "kind": kind,
+                             "cpu_model": oracle.cpu_model(),
+                             "sample": (f"full steps, measured: all {inst.n} points assigned (kd-tree, median "
+                                        f"{ta:.2f}s) + all {inst.partials.S} simplex rows border-tested (median "
+                                        f"{tb:.2f}s; per-part GridIndex build excluded), {len(steps)} timed steps "
+                                        f"after 1 warm-up" + (", on the reference's geometry.cpp + TaskPool("
+                                        f"{threads})" if kind == "reference" else ", oracle restatement")),
+                             "assign_points_per_s": inst.n / ta, "border_simplices_per_s": inst.partials.S / tb,
+                             "single_core": one},
+            "stage_rates": {"assign_points_per_s": inst.n / ta, "border_simplices_per_s": inst.partials.S / tb},
             "e2e": {"value": v, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -359,6 +426,11 @@ def main():
     ms_bfs, stages_bfs, _ = timed(max(1, min(args.steps, 5)), bfs=True)
     n_vb_bfs = int(d_bcnt.item())
     n_pos = int(d_pos.sum().item())
+    # this run's device outputs, for the full-size parity leg
+    u32 = lambda t: t.cpu().numpy().view(np.uint32)  # noqa: E731
+    g_out = {"labels": u32(d_lab), "parts_offsets": d_poff.cpu().numpy().view(np.uint64),
+             "parts_ids": u32(d_pids), "positive": d_pos.cpu().numpy(), "border": d_bor.cpu().numpy(),
+             "positive_vertex_ids": u32(d_vids[:n_vb]), "border_vertex_ids": u32(d_bvids[:n_vb_bfs])}
 
     import oracle  # checker only: grid cell count for the byte model
     lo, hi, edge, dims = oracle.grid_params(inst.points, 1.0)
@@ -454,20 +526,20 @@ def main():
                "path": "sbdt_gpu_assign_points + sbdt_gpu_find_border(RESIDENT_POINTS) (host buffers, pinned)"}
         ectx.close()
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
-        cpu = cpu_baseline(inst, labels, args.policy, args.cpu_budget_s, os.cpu_count() or 1)
+    cpu, par = None, None
+    if rank == 0 and world == 1 and not args.no_parity and not args.profile:
+        cores = os.cpu_count() or 1
+        par = parity_leg(inst, args.policy, cores, g_out)
+        if not args.no_cpu_baseline:
+            cpu = cpu_baseline_from(par, inst, cores, single_core(inst, labels, args.policy))
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json config)",
-            "config": {"workload": inst.config["name"], "n": n, "dim": dim, "k": k, "m": m, "S": S,
-                       "policy": f"{args.policy}(c_G=1)", "cells": cells,
-                       "l2": "inputs > L2 (coords %d MB, simplices %d MB) and 256 MB L2 flush between steps"
-                             % (inst.points.nbytes >> 20, (part.verts.nbytes + part.nbrs.nbytes) >> 20),
-                       "parallelism": f"{world} independent instance(s), one per GPU"},
+            "config": config_dict(inst, args.policy, world, cells),
+            "parity": par,
             "stages_ms": {kk: round(v, 4) for kk, v in stages.items()},
             "overlapped_stages": sorted(overlapped),
             "launched_ms_per_step": round(sum(ms) / len(ms), 4),

@@ -89,14 +89,17 @@ int sbdt_gpu_stage_times(sbdt_gpu_ctx* ctx, char* names, int names_len, float* m
  * long-list records, queued points (long lists + ring searches), coarse cells
  * built by the dense pass}. */
 int sbdt_gpu_assign_table_stats(sbdt_gpu_ctx* ctx, unsigned* out6);
-/* Border pipeline census of the last find_border with the census enabled (grid
- * policy; zeros otherwise): out12 = {rows scanned by the prefilter, rows that
+/* Border pipeline census of the last find_border with the census enabled:
+ * the first `count` (<= 16) of {rows scanned by the prefilter, rows that
  * reached the exact stage, exact rows by scan kind: flattened cell scan,
  * two-level range (wide), pyramid range (wide), (candidate, cell row) pairs
  * of the flattened scan, wide-stage block expansions, positives of the
  * flattened scan, positives proven by the prefilter, positives of the wide
- * stage, 0, candidate-queue slots left unused (holes of the per-warp chunks)}. */
-int sbdt_gpu_border_stats(sbdt_gpu_ctx* ctx, unsigned long long* out12);
+ * stage, 0, candidate-queue slots left unused (holes of the per-warp chunks),
+ * rows whose binary32 sphere failed (exact orientation checked), orientation
+ * predicates escalated to expansion arithmetic, in_sphere predicates
+ * escalated to expansion arithmetic (exact policy), 0}. */
+int sbdt_gpu_border_stats(sbdt_gpu_ctx* ctx, unsigned long long* out, int count);
 
 /* Page-locked host memory for the host-buffer entry points' inputs and
  * outputs (transfers from/to pageable memory are staged by the driver and
@@ -119,7 +122,11 @@ int sbdt_gpu_assign_points(sbdt_gpu_ctx* ctx, int dim, const double* coords, uin
                            uint32_t* part_ids_out, double* bbox_out);
 
 /* Device-pointer variant. d_bbox_ordered_out (optional) receives 2*dim
- * order-preserving uint64 keys of the bbox (input of sbdt_gpu_find_border_dev). */
+ * order-preserving uint64 keys of the bbox (input of sbdt_gpu_find_border_dev).
+ * Precondition (not re-checked on the host: the labels stay on the device):
+ * every sample id < n and every sample label < k. A label >= k is detected
+ * by the bucketing pass when part_offsets / part_ids are requested and then
+ * fails the next synchronizing call with SBDT_ERR_INVALID. */
 int sbdt_gpu_assign_points_dev(sbdt_gpu_ctx* ctx, int dim, const double* d_coords, uint64_t n,
                                const uint32_t* d_sample_ids, const uint32_t* d_sample_labels,
                                uint32_t m, uint32_t k, uint32_t* d_labels_out,
@@ -241,6 +248,25 @@ int sbdt_gpu_merge(sbdt_gpu_ctx* ctx, int dim, const uint32_t* labels, uint64_t 
                    const int8_t* tb_parity, uint64_t S_B, uint32_t flags, uint64_t capacity,
                    uint32_t* out_verts, uint32_t* out_nbrs, int8_t* out_parity, uint64_t* out_offsets,
                    uint64_t* rows_out);
+
+/* ---- diagnostics (tests and bench only; not on the path) ----------------- */
+
+/* The device predicates on host arrays (synchronous): op 0 = orient, `pts`
+ * holds count x (dim+1) points of dim coordinates, out = sign of
+ * orient2/orient3 (geometry.cpp:150-189 / geometry.hpp:112-121 convention);
+ * op 1 = in_sphere, count x (dim+2) points (the simplex, then q), out = sign
+ * of in_sphere2/in_sphere3 (geometry.cpp:191-277). Binary64 filter, then
+ * expansion arithmetic where the filter cannot decide; *n_escalated (may be
+ * NULL) = how many cases took the exact path. Replaces no reference entry
+ * point: it exposes what find_border evaluates internally so tests can pin it
+ * case by case (SPEC.md acceptance criterion 2). */
+int sbdt_gpu_predicates(sbdt_gpu_ctx* ctx, int op, int dim, const double* pts, uint64_t count, int8_t* out,
+                        uint64_t* n_escalated);
+
+/* Binding-ceiling microbenchmarks on the context's device: kind 0 = DFMA
+ * throughput (FLOP/s, 2 per DFMA); kind 1 = random 8-byte gathers from a table
+ * of `bytes` bytes (gathers/s). Best of 4 timed launches (CUDA events). */
+int sbdt_gpu_microbench(sbdt_gpu_ctx* ctx, int kind, uint64_t bytes, double* result);
 
 #ifdef __cplusplus
 }

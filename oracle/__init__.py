@@ -44,7 +44,7 @@ def lib():
         L.oracle_grid_params.argtypes = [C.c_int, dp, u64, C.c_double, dp, dp, dp, C.POINTER(C.c_int64)]
         L.oracle_find_border.argtypes = [C.c_int, dp, u64, u32p, C.c_uint32, C.POINTER(C.c_uint64), u32p, u32p, i8p,
                                          C.c_int, C.c_double, C.c_int, C.c_uint32, C.c_uint32, u8p, u8p, u32p,
-                                         C.POINTER(C.c_uint64), u32p, C.POINTER(C.c_uint64), dp, C.c_char_p, C.c_int]
+                                         C.POINTER(C.c_uint64), u32p, C.POINTER(C.c_uint64), dp, dp, C.c_char_p, C.c_int]
         L.oracle_time_border.argtypes = [C.c_int, dp, u64, u32p, C.c_uint32, C.POINTER(C.c_uint64), u32p, u32p, i8p,
                                          C.c_int, C.c_double, C.c_int, C.c_uint32, C.c_uint32, C.c_int, dp, dp,
                                          C.POINTER(C.c_uint64)]
@@ -58,6 +58,8 @@ def lib():
         L.oracle_orient.argtypes = [C.c_int, dp]
         L.oracle_in_sphere.argtypes = [C.c_int, dp, dp]
         L.oracle_circumsphere.argtypes = [C.c_int, dp, dp]
+        L.oracle_orient_batch.argtypes = [C.c_int, dp, u64, C.POINTER(C.c_int8)]
+        L.oracle_in_sphere_batch.argtypes = [C.c_int, dp, u64, C.POINTER(C.c_int8)]
         L.oracle_box_sphere.argtypes = [C.c_int, dp, dp, dp, C.c_double]
         L.oracle_halfspace_box.argtypes = [C.c_int, dp, dp, dp, dp]
         _oracle = L
@@ -76,6 +78,8 @@ def ref_lib():
         L.ref_orient.argtypes = [C.c_int, dp]
         L.ref_in_sphere.argtypes = [C.c_int, dp, dp]
         L.ref_circumsphere.argtypes = [C.c_int, dp, dp]
+        L.ref_orient_batch.argtypes = [C.c_int, dp, u64, C.POINTER(C.c_int8)]
+        L.ref_in_sphere_batch.argtypes = [C.c_int, dp, u64, C.POINTER(C.c_int8)]
         L.ref_inflate.restype = C.c_double
         L.ref_inflate.argtypes = [C.c_double]
         L.ref_box_sphere.argtypes = [C.c_int, dp, dp, dp, C.c_double]
@@ -90,6 +94,9 @@ def ref_lib():
         L.ref_find_border.argtypes = [C.c_int, dp, u64, u32p, C.c_uint32, C.POINTER(C.c_uint64), u32p, u32p, i8p,
                                       C.c_int, C.c_double, u8p, u8p, u32p, C.POINTER(C.c_uint64), u32p,
                                       C.POINTER(C.c_uint64)]
+        L.ref_time_step.argtypes = [C.c_int, dp, u64, u32p, u64, u32p, u64, u32p, C.c_uint32, C.POINTER(C.c_uint64),
+                                    u32p, u32p, i8p, C.c_int, C.c_double, C.c_uint, C.c_uint32, C.c_uint32, u32p, u8p,
+                                    dp, C.POINTER(C.c_uint64)]
         _ref = L
     return _ref
 
@@ -125,7 +132,8 @@ def grid_params(points, c_G=1.0):
 
 
 def find_border(points, labels, partials, policy="grid", c_G=1.0, threads=8, parts=None, spheres=False):
-    """Returns dict(positive, border, vertices_positive, vertices_border[, spheres])."""
+    """Returns dict(positive, border, vertices_positive, vertices_border, times[, spheres]);
+    times = (index build s, find_border s) measured inside the library."""
     pts = np.ascontiguousarray(points, np.float64)
     lab = np.ascontiguousarray(labels, np.uint32)
     dim = pts.shape[1]
@@ -139,16 +147,17 @@ def find_border(points, labels, partials, policy="grid", c_G=1.0, threads=8, par
     npos, nbfs = C.c_uint64(0), C.c_uint64(0)
     sph = np.empty((S, dim + 1), np.float64) if spheres else None
     err = C.create_string_buffer(256)
+    times = np.zeros(2)
     rc = lib().oracle_find_border(dim, _p(pts, C.c_double), len(pts), _p(lab, C.c_uint32), k,
                                   _p(partials.offsets, C.c_uint64), _p(partials.verts, C.c_uint32),
                                   _p(partials.nbrs, C.c_uint32), _p(partials.parity, C.c_int8), POLICY[policy], c_G,
                                   threads, p0, p1, _p(pos, C.c_uint8), _p(bor, C.c_uint8), _p(vpos, C.c_uint32),
                                   C.byref(npos), _p(vbfs, C.c_uint32), C.byref(nbfs),
-                                  _p(sph, C.c_double) if spheres else None, err, 256)
+                                  _p(sph, C.c_double) if spheres else None, _p(times, C.c_double), err, 256)
     if rc != 0:
         raise RuntimeError("oracle_find_border: " + err.value.decode())
     out = dict(positive=pos, border=bor, vertices_positive=vpos[:npos.value].copy(),
-               vertices_border=vbfs[:nbfs.value].copy())
+               vertices_border=vbfs[:nbfs.value].copy(), times=(float(times[0]), float(times[1])))
     if spheres:
         out["spheres"] = sph
     return out
@@ -193,3 +202,63 @@ def merge(partials, border, tb, labels, hull=True):
     finally:
         lib().oracle_merge_free(h)
     return v, nb, par, off
+
+
+def ref_time_step(points, sample_ids, sample_labels, labels, partials, policy="grid", c_G=1.0, threads=1,
+                  n_assign=None, parts=(0, 0)):
+    """One CPU step of the path on the reference's own compiled primitives and
+    its TaskPool(threads) (oracle/_ref; None if it was not built): kd-tree
+    assign_points over points [0, n_assign), then find_border over parts
+    [p0, p1) with `labels`. Returns dict(labels, positive, times=(assign,
+    index build, border) seconds, border_vertices)."""
+    L = ref_lib()
+    if L is None:
+        return None
+    pts = np.ascontiguousarray(points, np.float64)
+    sid = np.ascontiguousarray(sample_ids, np.uint32)
+    slab = np.ascontiguousarray(sample_labels, np.uint32)
+    lab = np.ascontiguousarray(labels, np.uint32)
+    n = len(pts)
+    na = n if n_assign is None else int(n_assign)
+    out_lab = np.empty(max(na, 1), np.uint32)
+    pos = np.zeros(partials.S, np.uint8)
+    times = np.zeros(3)
+    nvb = C.c_uint64(0)
+    rc = L.ref_time_step(pts.shape[1], _p(pts, C.c_double), n, _p(sid, C.c_uint32), len(sid), _p(slab, C.c_uint32),
+                         na, _p(lab, C.c_uint32), partials.k, _p(partials.offsets, C.c_uint64),
+                         _p(partials.verts, C.c_uint32), _p(partials.nbrs, C.c_uint32), _p(partials.parity, C.c_int8),
+                         POLICY[policy], c_G, threads, parts[0], parts[1], _p(out_lab, C.c_uint32),
+                         _p(pos, C.c_uint8), _p(times, C.c_double), C.byref(nvb))
+    if rc != 0:
+        raise RuntimeError("ref_time_step failed")
+    return dict(labels=out_lab[:na], positive=pos, times=tuple(float(t) for t in times),
+                border_vertices=int(nvb.value))
+
+
+def cpu_model() -> str:
+    """Host CPU model string (/proc/cpuinfo) for the baseline records."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def predicates_batch(op, pts, use_ref=True):
+    """orient / in_sphere signs of the cases in `pts` (layout of
+    gpu.Context.predicates), by the reference's compiled geometry.cpp when
+    oracle/_ref exists (use_ref), else by the restatement. Returns (signs, which)."""
+    pts = np.ascontiguousarray(pts, np.float64)
+    count, _, dim = pts.shape
+    out = np.empty(count, np.int8)
+    L = ref_lib() if use_ref else None
+    if L is not None:
+        fn, which = (L.ref_orient_batch if op == "orient" else L.ref_in_sphere_batch), "reference"
+    else:
+        fn, which = (lib().oracle_orient_batch if op == "orient" else lib().oracle_in_sphere_batch), "oracle"
+    fn(dim, _p(pts, C.c_double), count, _p(out, C.c_int8))
+    return out, which

@@ -103,21 +103,25 @@ int oracle_find_border(int dim, const double* xyz, std::uint64_t n, const std::u
                        const std::int8_t* parity, int policy, double c_G, int threads, std::uint32_t p0,
                        std::uint32_t p1, std::uint8_t* positive_out, std::uint8_t* border_out,
                        std::uint32_t* vpos_out, std::uint64_t* n_vpos, std::uint32_t* vbfs_out,
-                       std::uint64_t* n_vbfs, double* spheres_out, char* err, int errlen) {
+                       std::uint64_t* n_vbfs, double* spheres_out, double* times_out, char* err, int errlen) {
   try {
     PartialsView pv{k, offsets, verts, nbrs, parity, offsets[k]};
     if (p1 == 0) p1 = k;
-    if (dim == 2) {
-      BorderOracle<2, OwnPrims<2>> bo(xyz, n, labels, pv, policy, c_G, threads);
+    auto now = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    auto go = [&](auto tag) {
+      constexpr int D = decltype(tag)::value;
+      const double t0 = now();
+      BorderOracle<D, OwnPrims<D>> bo(xyz, n, labels, pv, policy, c_G, threads);
+      const double t1 = now();
       auto r = bo.run(p0, p1);
-      export_border<2>(bo, r, positive_out, border_out, vpos_out, n_vpos, vbfs_out, n_vbfs, spheres_out, pv.S, verts);
-    } else if (dim == 3) {
-      BorderOracle<3, OwnPrims<3>> bo(xyz, n, labels, pv, policy, c_G, threads);
-      auto r = bo.run(p0, p1);
-      export_border<3>(bo, r, positive_out, border_out, vpos_out, n_vpos, vbfs_out, n_vbfs, spheres_out, pv.S, verts);
-    } else {
-      return 1;
-    }
+      const double t2 = now();
+      // times_out: [index build (per-part GridIndex), full scan + BFS + vertex sets]
+      if (times_out) times_out[0] = t1 - t0, times_out[1] = t2 - t1;
+      export_border<D>(bo, r, positive_out, border_out, vpos_out, n_vpos, vbfs_out, n_vbfs, spheres_out, pv.S, verts);
+    };
+    if (dim == 2) go(std::integral_constant<int, 2>{});
+    else if (dim == 3) go(std::integral_constant<int, 3>{});
+    else return 1;
     return 0;
   } catch (const std::exception& e) {
     if (err && errlen > 0) std::snprintf(err, errlen, "%s", e.what());
@@ -164,6 +168,19 @@ int oracle_in_sphere(int dim, const double* pts, const double* q) {
   if (dim == 2) return in_sphere2(pts, pts + 2, pts + 4, q);
   return in_sphere3(pts, pts + 3, pts + 6, pts + 9, q);
 }
+// Batches in the layout of sbdt_gpu_predicates (see ref_orient_batch).
+void oracle_orient_batch(int dim, const double* pts, std::uint64_t count, std::int8_t* out) {
+  const std::uint64_t per = std::uint64_t(dim + 1) * dim;
+  for (std::uint64_t i = 0; i < count; ++i) out[i] = static_cast<std::int8_t>(oracle_orient(dim, pts + i * per));
+}
+void oracle_in_sphere_batch(int dim, const double* pts, std::uint64_t count, std::int8_t* out) {
+  const std::uint64_t per = std::uint64_t(dim + 2) * dim;
+  for (std::uint64_t i = 0; i < count; ++i) {
+    const double* b = pts + i * per;
+    out[i] = static_cast<std::int8_t>(oracle_in_sphere(dim, b, b + std::uint64_t(dim + 1) * dim));
+  }
+}
+
 int oracle_circumsphere(int dim, const double* pts, double* out) {
   try {
     const double* p[4] = {pts, pts + dim, pts + 2 * dim, pts + 3 * dim};

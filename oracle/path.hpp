@@ -27,8 +27,19 @@ constexpr std::uint32_t kInf = 0xFFFFFFFFu;
 
 enum PolicyKind : int { kBbox = 0, kGrid = 1, kExact = 2 };
 
+// Optional external pool (oracle/ref/ref_glue.cpp installs the reference's own
+// sbdt::TaskPool, task_pool.hpp:63-80, for the timed "reference" CPU arm).
+// Chunking is by `grain` either way, so results are identical.
+using ParallelRunner = void (*)(std::size_t n, std::size_t grain,
+                                const std::function<void(std::size_t, std::size_t)>& fn);
+inline ParallelRunner g_runner = nullptr;
+
 inline void parallel_for(std::size_t n, std::size_t grain, unsigned threads,
                          const std::function<void(std::size_t, std::size_t)>& fn) {
+  if (g_runner && threads > 1) {
+    g_runner(n, grain, fn);
+    return;
+  }
   if (threads <= 1 || n <= grain) {
     for (std::size_t b = 0; b < n; b += grain) fn(b, std::min(n, b + grain));
     return;

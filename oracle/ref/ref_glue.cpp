@@ -4,6 +4,8 @@
 // Used only to pin the oracle's restatement (oracle/prims.hpp, path.hpp) and
 // the host DT builder, and to generate tests/golden/ fixtures.
 #include <algorithm>
+#include <chrono>
+#include <functional>
 #include <array>
 #include <cstring>
 #include <numeric>
@@ -11,6 +13,7 @@
 
 #include "sbdt/geometry.hpp"
 #include "sbdt/sequential_dt.hpp"
+#include "sbdt/task_pool.hpp"
 #include "sbdt/triangulation.hpp"
 #include "../path.hpp"
 
@@ -103,9 +106,76 @@ RefTri run_ref_dt(const double* xyz, std::uint64_t n_points, const std::uint32_t
   return r;
 }
 
+// The reference's own work pool (task_pool.hpp:63-80) behind path.hpp's
+// parallel_for: fixed-grain chunks, so the outputs equal the oracle's.
+sbdt::TaskPool* g_pool = nullptr;
+void pool_runner(std::size_t n, std::size_t grain, const std::function<void(std::size_t, std::size_t)>& fn) {
+  g_pool->parallel_for(n, grain, fn);
+}
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+template <int D>
+void time_step(const double* xyz, std::uint64_t n, const std::uint32_t* sample_ids, std::uint64_t m,
+               const std::uint32_t* sample_labels, std::uint64_t n_assign, const std::uint32_t* labels,
+               const sbdt_oracle::PartialsView& pv, int policy, double c_G, unsigned threads, std::uint32_t p0,
+               std::uint32_t p1, std::uint32_t* labels_out, std::uint8_t* positive_out, double* times,
+               std::uint64_t* n_vb) {
+  const double t0 = now_s();
+  sbdt_oracle::SampleKdTree<D, RefPrims<D>> tree(xyz, sample_ids, m, sample_labels);
+  sbdt_oracle::parallel_for(n_assign, 4096, threads, [&](std::size_t b, std::size_t e) {
+    for (std::size_t i = b; i < e; ++i) labels_out[i] = tree.nearest_label(xyz + i * D);
+  });
+  const double t1 = now_s();
+  sbdt_oracle::BorderOracle<D, RefPrims<D>> bo(xyz, n, labels, pv, policy, c_G, threads);
+  const double t2 = now_s();
+  auto r = bo.run(p0, p1);
+  const double t3 = now_s();
+  times[0] = t1 - t0, times[1] = t2 - t1, times[2] = t3 - t2;
+  *n_vb = r.vertices_border.size();
+  if (positive_out) std::memcpy(positive_out + pv.offsets[p0], r.positive.data() + pv.offsets[p0],
+                                pv.offsets[p1] - pv.offsets[p0]);
+}
+
 }  // namespace
 
 extern "C" {
+
+// One timed CPU step of the path on the REFERENCE's primitives (geometry.cpp,
+// compiled by path) and the reference's TaskPool(threads) (threads <= 1: the
+// inline determinism baseline, task_pool.hpp:20-21): kd-tree assign_points
+// over points [0, n_assign) -> labels_out, then find_border
+// (per-part GridIndex build + full scan + BFS) over
+// parts [p0, p1) with the given labels. times: [assign, index build, border].
+int ref_time_step(int dim, const double* xyz, std::uint64_t n, const std::uint32_t* sample_ids, std::uint64_t m,
+                  const std::uint32_t* sample_labels, std::uint64_t n_assign, const std::uint32_t* labels,
+                  std::uint32_t k, const std::uint64_t* offsets, const std::uint32_t* verts,
+                  const std::uint32_t* nbrs, const std::int8_t* parity, int policy, double c_G, unsigned threads,
+                  std::uint32_t p0, std::uint32_t p1, std::uint32_t* labels_out, std::uint8_t* positive_out,
+                  double* times, std::uint64_t* n_vb) {
+  try {
+    sbdt_oracle::PartialsView pv{k, offsets, verts, nbrs, parity, offsets[k]};
+    if (p1 == 0 || p1 > k) p1 = k;
+    sbdt::TaskPool pool(threads);
+    g_pool = &pool;
+    sbdt_oracle::g_runner = threads > 1 ? pool_runner : nullptr;
+    if (dim == 2)
+      time_step<2>(xyz, n, sample_ids, m, sample_labels, n_assign, labels, pv, policy, c_G, threads, p0, p1,
+                   labels_out, positive_out, times, n_vb);
+    else
+      time_step<3>(xyz, n, sample_ids, m, sample_labels, n_assign, labels, pv, policy, c_G, threads, p0, p1,
+                   labels_out, positive_out, times, n_vb);
+    sbdt_oracle::g_runner = nullptr;
+    g_pool = nullptr;
+    return 0;
+  } catch (...) {
+    sbdt_oracle::g_runner = nullptr;
+    g_pool = nullptr;
+    return 1;
+  }
+}
 
 int ref_orient(int dim, const double* pts) {
   if (dim == 2) return sbdt::orient2({pts[0], pts[1]}, {pts[2], pts[3]}, {pts[4], pts[5]});
@@ -117,6 +187,20 @@ int ref_in_sphere(int dim, const double* p, const double* q) {
   return sbdt::in_sphere3({p[0], p[1], p[2]}, {p[3], p[4], p[5]}, {p[6], p[7], p[8]}, {p[9], p[10], p[11]},
                           {q[0], q[1], q[2]});
 }
+// Batches in the layout of sbdt_gpu_predicates: per case (dim+1) points for
+// orient, (dim+1) simplex points then q for in_sphere.
+void ref_orient_batch(int dim, const double* pts, std::uint64_t count, std::int8_t* out) {
+  const std::uint64_t per = std::uint64_t(dim + 1) * dim;
+  for (std::uint64_t i = 0; i < count; ++i) out[i] = static_cast<std::int8_t>(ref_orient(dim, pts + i * per));
+}
+void ref_in_sphere_batch(int dim, const double* pts, std::uint64_t count, std::int8_t* out) {
+  const std::uint64_t per = std::uint64_t(dim + 2) * dim;
+  for (std::uint64_t i = 0; i < count; ++i) {
+    const double* b = pts + i * per;
+    out[i] = static_cast<std::int8_t>(ref_in_sphere(dim, b, b + std::uint64_t(dim + 1) * dim));
+  }
+}
+
 int ref_circumsphere(int dim, const double* pts, double* out) {
   try {
     if (dim == 2) {

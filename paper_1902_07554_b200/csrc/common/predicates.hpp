@@ -206,9 +206,292 @@ SBDT_HD int minor2(const Diff2& a, const Diff2& b, const Diff2& c, const Diff2& 
   return expansion_sum(lp, p, lq, q, out);
 }
 
+// ---- wide exponent ranges: scaled big integers ------------------------------
+// Expansion arithmetic is exact only while no product underflows or
+// overflows. Every component of a degree-g homogeneous determinant of
+// coordinate differences is a multiple of 2^(g (emin - 52)) (emin: the smallest
+// exponent of a nonzero input) and below 2^(g (emax + 1) + 8), so it is exact
+// when those fit binary64 (after an exact power-of-two prescale of all
+// inputs, which leaves every sign unchanged). Inputs whose exponents span
+// more than that (e.g. 5.0 next to 5e-324) take the reference's own method
+// (ExactScaler, geometry.cpp:28-55): every value becomes the integer
+// mantissa * 2^(e - emin) and the determinant is evaluated in big integers.
+
+// Power-of-two prescale exponent for a degree-g determinant, or kNoScale.
+constexpr int kNoScale = 1 << 30;
+SBDT_HD int prescale_exponent(const double* v, int count, int g) {
+  int emin = 1 << 20, emax = -(1 << 20);
+  for (int i = 0; i < count; ++i) {
+    if (v[i] == 0.0) continue;
+    const int e = ilogb(v[i]);
+    emin = e < emin ? e : emin;
+    emax = e > emax ? e : emax;
+  }
+  if (emax < emin) return 0;  // all zero
+  // need g (emin + s - 52) >= -1074 + 53 (a margin: the lowest product bits
+  // stay above the subnormal range) and g (emax + s + 1) + 8 <= 1000
+  const int lo_need = 52 + (-1021 + g - 1) / g + 1 - emin;  // ceil((-1021) / g), rounded up once more
+  const int hi_allow = (1000 - 8) / g - 1 - emax;
+  if (lo_need > hi_allow) return kNoScale;
+  if (lo_need > 0) return lo_need;
+  if (hi_allow < 0) return hi_allow;
+  return 0;
+}
+
+// Signed-magnitude big integer over 32-bit limbs in caller storage.
+struct Big {
+  std::uint32_t* d;
+  int n;    // limbs in use (no leading zero limb); 0 = zero
+  int neg;  // 1 = negative
+};
+
+SBDT_HD int big_sign(const Big& a) { return a.n == 0 ? 0 : (a.neg ? -1 : 1); }
+
+SBDT_HD int min_exponent(const double* v, int count) {
+  int emin = 1 << 20;
+  for (int i = 0; i < count; ++i)
+    if (v[i] != 0.0) {
+      const int e = ilogb(v[i]);
+      emin = e < emin ? e : emin;
+    }
+  return emin == (1 << 20) ? 0 : emin;
+}
+
+// r = v * 2^(52 - emin) as an integer: mantissa(v) << (ilogb(v) - emin).
+SBDT_HD void big_scaled(Big& r, double v, int emin) {
+  r.n = 0;
+  r.neg = v < 0.0;
+  if (v == 0.0) return;
+  const int e = ilogb(v);
+  const std::uint64_t m = static_cast<std::uint64_t>(fabs(scalbn(v, 52 - e)));
+  const int shift = e - emin;
+  const int w = shift >> 5, b = shift & 31;
+  for (int i = 0; i < w; ++i) r.d[i] = 0u;
+  const std::uint64_t lo = m << b;                     // bits [b, 64)
+  const std::uint64_t hi = b ? (m >> (64 - b)) : 0u;  // the bits shifted out
+  r.d[w] = static_cast<std::uint32_t>(lo);
+  r.d[w + 1] = static_cast<std::uint32_t>(lo >> 32);
+  r.d[w + 2] = static_cast<std::uint32_t>(hi);
+  r.n = w + 3;
+  while (r.n > 0 && r.d[r.n - 1] == 0u) --r.n;
+}
+
+SBDT_HD int big_cmp_mag(const Big& a, const Big& b) {
+  if (a.n != b.n) return a.n < b.n ? -1 : 1;
+  for (int i = a.n - 1; i >= 0; --i)
+    if (a.d[i] != b.d[i]) return a.d[i] < b.d[i] ? -1 : 1;
+  return 0;
+}
+
+// r = a + (negb ? -b : b); r must not alias a or b.
+SBDT_HD void big_add(Big& r, const Big& a, const Big& b, int negb) {
+  const int bneg = b.neg ^ negb;
+  if (b.n == 0) {
+    for (int i = 0; i < a.n; ++i) r.d[i] = a.d[i];
+    r.n = a.n, r.neg = a.neg;
+    return;
+  }
+  if (a.n == 0) {
+    for (int i = 0; i < b.n; ++i) r.d[i] = b.d[i];
+    r.n = b.n, r.neg = bneg;
+    return;
+  }
+  if (a.neg == bneg) {  // magnitudes add
+    const int n = a.n > b.n ? a.n : b.n;
+    std::uint64_t c = 0;
+    for (int i = 0; i < n; ++i) {
+      c += std::uint64_t(i < a.n ? a.d[i] : 0u) + (i < b.n ? b.d[i] : 0u);
+      r.d[i] = static_cast<std::uint32_t>(c);
+      c >>= 32;
+    }
+    r.n = n;
+    if (c) r.d[r.n++] = static_cast<std::uint32_t>(c);
+    r.neg = a.neg;
+    return;
+  }
+  const int cmp = big_cmp_mag(a, b);
+  if (cmp == 0) {
+    r.n = 0, r.neg = 0;
+    return;
+  }
+  const Big& x = cmp > 0 ? a : b;  // larger magnitude
+  const Big& y = cmp > 0 ? b : a;
+  std::int64_t br = 0;
+  for (int i = 0; i < x.n; ++i) {
+    std::int64_t t = std::int64_t(x.d[i]) - (i < y.n ? std::int64_t(y.d[i]) : 0) - br;
+    br = t < 0;
+    r.d[i] = static_cast<std::uint32_t>(t + (br << 32));
+  }
+  r.n = x.n;
+  while (r.n > 0 && r.d[r.n - 1] == 0u) --r.n;
+  r.neg = cmp > 0 ? a.neg : bneg;
+}
+
+// r = a * b (schoolbook); r must not alias a or b.
+SBDT_HD void big_mul(Big& r, const Big& a, const Big& b) {
+  if (a.n == 0 || b.n == 0) {
+    r.n = 0, r.neg = 0;
+    return;
+  }
+  const int n = a.n + b.n;
+  for (int i = 0; i < n; ++i) r.d[i] = 0u;
+  for (int i = 0; i < a.n; ++i) {
+    std::uint64_t c = 0;
+    for (int j = 0; j < b.n; ++j) {
+      c += std::uint64_t(a.d[i]) * b.d[j] + r.d[i + j];
+      r.d[i + j] = static_cast<std::uint32_t>(c);
+      c >>= 32;
+    }
+    r.d[i + b.n] = static_cast<std::uint32_t>(c);
+  }
+  r.n = n;
+  while (r.n > 0 && r.d[r.n - 1] == 0u) --r.n;
+  r.neg = a.neg ^ b.neg;
+}
+
+// Limbs of one scaled input: < 2^(1023 + 1074 + 53) (+1 bit for a difference).
+constexpr int kBigIn = 70;
+
+// Big determinant helpers over scaled differences. Storage `w` must hold the
+// documented number of limbs.
+// det2 of big entries (a d - b c) into r; scratch t1, t2 of na+nd / nb+nc limbs.
+SBDT_HD void big_det2(Big& r, const Big& a, const Big& b, const Big& c, const Big& d, Big& t1, Big& t2) {
+  big_mul(t1, a, d);
+  big_mul(t2, b, c);
+  big_add(r, t1, t2, 1);
+}
+
+// out = det [[m0 m1 m2],[m3 m4 m5],[m6 m7 m8]] (cofactor expansion along row
+// 0, as geometry.cpp:63-66), entries of at most E limbs. out holds 3E + 6
+// limbs, scratch w 12E + 16 (disjoint).
+SBDT_HD void big_det3(Big& out, const Big* m, std::uint32_t* w, int E) {
+  Big t1{w, 0, 0}, t2{w + 2 * E + 2, 0, 0}, mi{w + 4 * E + 4, 0, 0};
+  Big term{w + 6 * E + 8, 0, 0}, acc2{w + 9 * E + 12, 0, 0};
+  out.n = 0, out.neg = 0;
+  for (int j = 0; j < 3; ++j) {
+    const int c1 = j == 0 ? 1 : 0, c2 = j == 2 ? 1 : 2;
+    big_det2(mi, m[3 + c1], m[3 + c2], m[6 + c1], m[6 + c2], t1, t2);
+    big_mul(term, m[j], mi);
+    big_add(acc2, out, term, j == 1);
+    for (int i = 0; i < acc2.n; ++i) out.d[i] = acc2.d[i];
+    out.n = acc2.n, out.neg = acc2.neg;
+  }
+}
+constexpr int big_det3_scratch(int E) { return 15 * E + 22; }  // out + w
+
+// orient2 / orient3 on big integers: rows b-a, c-a(, d-a) (the reference's
+// orient2_exact / orient3_exact, geometry.cpp:90-107).
+SBDT_HDN int orient2_big(const double* a, const double* b, const double* c) {
+  const double v[6] = {a[0], a[1], b[0], b[1], c[0], c[1]};
+  const int emin = min_exponent(v, 6);
+  std::uint32_t w[12 * kBigIn];
+  Big x{w, 0, 0}, y{w + kBigIn, 0, 0}, e[4] = {{w + 2 * kBigIn, 0, 0}, {w + 3 * kBigIn, 0, 0},
+                                              {w + 4 * kBigIn, 0, 0}, {w + 5 * kBigIn, 0, 0}};
+  const double* rows[2] = {b, c};
+  for (int i = 0; i < 2; ++i)
+    for (int k = 0; k < 2; ++k) {
+      big_scaled(x, rows[i][k], emin);
+      big_scaled(y, a[k], emin);
+      big_add(e[2 * i + k], x, y, 1);
+    }
+  Big t1{w + 6 * kBigIn, 0, 0}, t2{w + 8 * kBigIn, 0, 0}, r{w + 10 * kBigIn, 0, 0};
+  big_det2(r, e[0], e[1], e[2], e[3], t1, t2);
+  return big_sign(r);
+}
+
+SBDT_HDN int orient3_big(const double* a, const double* b, const double* c, const double* d) {
+  const double v[12] = {a[0], a[1], a[2], b[0], b[1], b[2], c[0], c[1], c[2], d[0], d[1], d[2]};
+  const int emin = min_exponent(v, 12);
+  std::uint32_t w[11 * kBigIn + big_det3_scratch(kBigIn)];
+  Big x{w, 0, 0}, y{w + kBigIn, 0, 0};
+  Big m[9];
+  for (int i = 0; i < 9; ++i) m[i] = Big{w + (2 + i) * kBigIn, 0, 0};
+  const double* rows[3] = {b, c, d};
+  for (int i = 0; i < 3; ++i)
+    for (int k = 0; k < 3; ++k) {
+      big_scaled(x, rows[i][k], emin);
+      big_scaled(y, a[k], emin);
+      big_add(m[3 * i + k], x, y, 1);
+    }
+  Big out{w + 11 * kBigIn, 0, 0};
+  big_det3(out, m, w + 11 * kBigIn + 3 * kBigIn + 6, kBigIn);
+  return big_sign(out);
+}
+
+// Rows (p_i - q, |p_i - q|^2) of the lifted in_sphere matrix, scaled big
+// integers (geometry.cpp:109-146 layout), into m (row stride D + 1, entries of
+// E = 2 kBigIn + 2 limbs each) using w (2 kBigIn + E limbs) for temporaries.
+template <int D>
+SBDT_HD void big_lifted_rows(const double* const* p, const double* q, Big* m, std::uint32_t* w, int emin) {
+  const int E = 2 * kBigIn + 2;
+  Big x{w, 0, 0}, y{w + kBigIn, 0, 0}, sq{w + 2 * kBigIn, 0, 0}, acc{w + 2 * kBigIn + E, 0, 0};
+  for (int i = 0; i <= D; ++i) {
+    Big& lift = m[i * (D + 1) + D];
+    lift.n = 0, lift.neg = 0;
+    for (int k = 0; k < D; ++k) {
+      big_scaled(x, p[i][k], emin);
+      big_scaled(y, q[k], emin);
+      Big& dk = m[i * (D + 1) + k];
+      big_add(dk, x, y, 1);
+      big_mul(sq, dk, dk);
+      big_add(acc, lift, sq, 0);
+      for (int t = 0; t < acc.n; ++t) lift.d[t] = acc.d[t];
+      lift.n = acc.n, lift.neg = acc.neg;
+    }
+  }
+}
+
+// in_sphere2: sign det [[p_i - q, lift_i]] (3 x 3); in_sphere3: -sign of the
+// 4 x 4 determinant (geometry.cpp:130-146), cofactor expansion along row 0 as
+// the reference's det4. buf: scratch (doubles, reinterpreted as limbs).
+SBDT_HDN int in_sphere2_big(const double* a, const double* b, const double* c, const double* q, double* buf) {
+  const double v[8] = {a[0], a[1], b[0], b[1], c[0], c[1], q[0], q[1]};
+  const int emin = min_exponent(v, 8);
+  std::uint32_t* w = reinterpret_cast<std::uint32_t*>(buf);
+  const int E = 2 * kBigIn + 2;
+  Big m[9];
+  for (int i = 0; i < 9; ++i) m[i] = Big{w + i * E, 0, 0};
+  const double* p[3] = {a, b, c};
+  big_lifted_rows<2>(p, q, m, w + 9 * E, emin);
+  Big out{w + 9 * E, 0, 0};
+  big_det3(out, m, w + 9 * E + 3 * E + 6, E);
+  return big_sign(out);
+}
+
+SBDT_HDN int in_sphere3_big(const double* a, const double* b, const double* c, const double* d, const double* q,
+                            double* buf) {
+  const double v[15] = {a[0], a[1], a[2], b[0], b[1], b[2], c[0], c[1], c[2], d[0], d[1], d[2], q[0], q[1], q[2]};
+  const int emin = min_exponent(v, 15);
+  std::uint32_t* w = reinterpret_cast<std::uint32_t*>(buf);
+  const int E = 2 * kBigIn + 2;
+  Big m[16];
+  for (int i = 0; i < 16; ++i) m[i] = Big{w + i * E, 0, 0};
+  const double* p[4] = {a, b, c, d};
+  std::uint32_t* free0 = w + 16 * E;
+  big_lifted_rows<3>(p, q, m, free0, emin);
+  // det4 = sum_j (-1)^j m[0][j] det3(minor_j)
+  const int E3 = 3 * E + 6;
+  Big minor[9];
+  Big d3{free0, 0, 0}, term{free0 + E3, 0, 0}, acc{free0 + E3 + E3 + E, 0, 0}, acc2{free0 + 3 * E3 + 2 * E + 4, 0, 0};
+  std::uint32_t* wd = free0 + 4 * E3 + 3 * E + 8;
+  acc.n = 0, acc.neg = 0;
+  for (int j = 0; j < 4; ++j) {
+    int idx = 0;
+    for (int row = 1; row < 4; ++row)
+      for (int col = 0; col < 4; ++col)
+        if (col != j) minor[idx++] = m[4 * row + col];
+    big_det3(d3, minor, wd, E);
+    big_mul(term, m[j], d3);
+    big_add(acc2, acc, term, j & 1);
+    for (int t = 0; t < acc2.n; ++t) acc.d[t] = acc2.d[t];
+    acc.n = acc2.n, acc.neg = acc2.neg;
+  }
+  return -big_sign(acc);
+}
+
 // Exact orient2 sign (geometry.cpp:150-170 contract): sign of
 // (a-c)x (b-c)y - (a-c)y (b-c)x.
-SBDT_HDN int orient2_exact(const double* a, const double* b, const double* c) {
+SBDT_HDN int orient2_expansion(const double* a, const double* b, const double* c) {
   const Diff2 acx = exact_diff(a[0], c[0]), acy = exact_diff(a[1], c[1]);
   const Diff2 bcx = exact_diff(b[0], c[0]), bcy = exact_diff(b[1], c[1]);
   double out[16];
@@ -216,7 +499,21 @@ SBDT_HDN int orient2_exact(const double* a, const double* b, const double* c) {
   return expansion_sign(n, out);
 }
 
-SBDT_HD int orient2(const double* a, const double* b, const double* c) {
+// Exact orient2: expansion arithmetic on prescaled inputs, big integers
+// when the inputs' exponent range is too wide for it.
+SBDT_HD int orient2_exact(const double* a, const double* b, const double* c) {
+  const double v[6] = {a[0], a[1], b[0], b[1], c[0], c[1]};
+  const int s = prescale_exponent(v, 6, 2);
+  if (s == kNoScale) return orient2_big(a, b, c);
+  if (s == 0) return orient2_expansion(a, b, c);
+  double w[6];
+  for (int i = 0; i < 6; ++i) w[i] = ldexp(v[i], s);
+  return orient2_expansion(w, w + 2, w + 4);
+}
+
+// Filter stage only: the sign, or 2 when the binary64 evaluation cannot
+// decide it (the caller escalates to orient2_exact).
+SBDT_HD int orient2_filtered(const double* a, const double* b, const double* c) {
   const double detleft = (a[0] - c[0]) * (b[1] - c[1]);
   const double detright = (a[1] - c[1]) * (b[0] - c[0]);
   const double det = detleft - detright;
@@ -233,7 +530,12 @@ SBDT_HD int orient2(const double* a, const double* b, const double* c) {
   const double errbound = kCcwBound * detsum;
   if (det >= errbound) return 1;
   if (-det >= errbound) return -1;
-  return orient2_exact(a, b, c);
+  return 2;
+}
+
+SBDT_HD int orient2(const double* a, const double* b, const double* c) {
+  const int r = orient2_filtered(a, b, c);
+  return r != 2 ? r : orient2_exact(a, b, c);
 }
 
 // Exact 3x3 determinant of rows r0,r1,r2 (2-term entries). out size >= 192.
@@ -262,7 +564,7 @@ SBDT_HD int det3_exact(const Diff2 r[3][3], double* out, double* scratch) {
 }
 
 // orient3 = sign det(b-a, c-a, d-a)  (geometry.hpp:112-121 convention).
-SBDT_HDN int orient3_exact(const double* a, const double* b, const double* c, const double* d) {
+SBDT_HDN int orient3_expansion(const double* a, const double* b, const double* c, const double* d) {
   Diff2 r[3][3];
   for (int k = 0; k < 3; ++k) {
     r[0][k] = exact_diff(b[k], a[k]);
@@ -275,7 +577,17 @@ SBDT_HDN int orient3_exact(const double* a, const double* b, const double* c, co
   return expansion_sign(n, out);
 }
 
-SBDT_HD int orient3(const double* a, const double* b, const double* c, const double* d) {
+SBDT_HD int orient3_exact(const double* a, const double* b, const double* c, const double* d) {
+  const double v[12] = {a[0], a[1], a[2], b[0], b[1], b[2], c[0], c[1], c[2], d[0], d[1], d[2]};
+  const int s = prescale_exponent(v, 12, 3);
+  if (s == kNoScale) return orient3_big(a, b, c, d);
+  if (s == 0) return orient3_expansion(a, b, c, d);
+  double w[12];
+  for (int i = 0; i < 12; ++i) w[i] = ldexp(v[i], s);
+  return orient3_expansion(w, w + 3, w + 6, w + 9);
+}
+
+SBDT_HD int orient3_filtered(const double* a, const double* b, const double* c, const double* d) {
   const double adx = a[0] - d[0], ady = a[1] - d[1], adz = a[2] - d[2];
   const double bdx = b[0] - d[0], bdy = b[1] - d[1], bdz = b[2] - d[2];
   const double cdx = c[0] - d[0], cdy = c[1] - d[1], cdz = c[2] - d[2];
@@ -290,14 +602,19 @@ SBDT_HD int orient3(const double* a, const double* b, const double* c, const dou
   // det(a-d,b-d,c-d) has the opposite sign of det(b-a,c-a,d-a).
   if (det > errbound) return -1;
   if (-det > errbound) return 1;
-  return orient3_exact(a, b, c, d);
+  return 2;  // undecided: orient3_exact
+}
+
+SBDT_HD int orient3(const double* a, const double* b, const double* c, const double* d) {
+  const int r = orient3_filtered(a, b, c, d);
+  return r != 2 ? r : orient3_exact(a, b, c, d);
 }
 
 // ---- in_sphere exact (host + escalation kernels) ---------------------------
 // Scratch requirement for in_sphere2_exact: kInSphere2Scratch doubles.
 constexpr int kInSphere2Scratch = 8192;
 // in_sphere2 = sign det [[p_i - q, |p_i - q|^2]] for the three rows.
-SBDT_HDN int in_sphere2_exact_buf(const double* a, const double* b, const double* c,
+SBDT_HDN int in_sphere2_expansion(const double* a, const double* b, const double* c,
                                   const double* q, double* buf) {
   const double* pts[3] = {a, b, c};
   Diff2 dx[3], dy[3];
@@ -333,6 +650,18 @@ SBDT_HDN int in_sphere2_exact_buf(const double* a, const double* b, const double
   return expansion_sign(rlen, res);
 }
 
+// Exact in_sphere2 (degree 4): expansion arithmetic on prescaled inputs, big
+// integers for too wide an exponent range. buf: kInSphere2Scratch doubles.
+SBDT_HD int in_sphere2_exact_buf(const double* a, const double* b, const double* c, const double* q, double* buf) {
+  const double v[8] = {a[0], a[1], b[0], b[1], c[0], c[1], q[0], q[1]};
+  const int s = prescale_exponent(v, 8, 4);
+  if (s == kNoScale) return in_sphere2_big(a, b, c, q, buf);
+  if (s == 0) return in_sphere2_expansion(a, b, c, q, buf);
+  double w[8];
+  for (int i = 0; i < 8; ++i) w[i] = ldexp(v[i], s);
+  return in_sphere2_expansion(w, w + 2, w + 4, w + 6, buf);
+}
+
 SBDT_HD int in_sphere2_filtered(const double* a, const double* b, const double* c,
                                 const double* q) {
   const double adx = a[0] - q[0], ady = a[1] - q[1];
@@ -357,7 +686,7 @@ SBDT_HD int in_sphere2_filtered(const double* a, const double* b, const double* 
 
 // in_sphere3 exact: -sign det M, M rows (p_i - q | lift_i)  (geometry.cpp:130-146).
 constexpr int kInSphere3Scratch = 131072;
-SBDT_HDN int in_sphere3_exact_buf(const double* a, const double* b, const double* c,
+SBDT_HDN int in_sphere3_expansion(const double* a, const double* b, const double* c,
                                   const double* d, const double* q, double* buf) {
   const double* pts[4] = {a, b, c, d};
   Diff2 df[4][3];
@@ -401,6 +730,18 @@ SBDT_HDN int in_sphere3_exact_buf(const double* a, const double* b, const double
     rlen = n;
   }
   return -expansion_sign(rlen, res);
+}
+
+// Exact in_sphere3 (degree 5), as in_sphere2_exact_buf. buf: kInSphere3Scratch doubles.
+SBDT_HD int in_sphere3_exact_buf(const double* a, const double* b, const double* c, const double* d,
+                                 const double* q, double* buf) {
+  const double v[15] = {a[0], a[1], a[2], b[0], b[1], b[2], c[0], c[1], c[2], d[0], d[1], d[2], q[0], q[1], q[2]};
+  const int s = prescale_exponent(v, 15, 5);
+  if (s == kNoScale) return in_sphere3_big(a, b, c, d, q, buf);
+  if (s == 0) return in_sphere3_expansion(a, b, c, d, q, buf);
+  double w[15];
+  for (int i = 0; i < 15; ++i) w[i] = ldexp(v[i], s);
+  return in_sphere3_expansion(w, w + 3, w + 6, w + 9, w + 12, buf);
 }
 
 SBDT_HD int in_sphere3_filtered(const double* a, const double* b, const double* c,

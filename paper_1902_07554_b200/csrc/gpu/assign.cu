@@ -378,9 +378,12 @@ __global__ void __launch_bounds__(kBucketThreads) k_bucket_scatter(const std::ui
 // tile_offsets[j][t] = part_offset[j] + sum_{t'<t} counts[j][t'] via one flat
 // exclusive scan over the label-major [k][tiles] matrix.
 __global__ void k_part_offsets(const std::uint32_t* __restrict__ tile_offsets, std::uint32_t k, std::uint32_t tiles,
-                               std::uint64_t n, std::uint64_t* __restrict__ part_offsets) {
+                               std::uint64_t n, std::uint64_t* __restrict__ part_offsets, unsigned* status) {
   for (std::uint32_t j = threadIdx.x; j <= k; j += blockDim.x)
     part_offsets[j] = (j == k) ? n : tile_offsets[std::uint64_t(j) * tiles];
+  // every label < k was counted: a total short of n means some label >= k
+  // (a sample label out of range on the device-pointer path)
+  if (threadIdx.x == 0 && tile_offsets[std::uint64_t(k) * tiles] != n) atomicOr(status, kStLabelRange);
 }
 
 // ---------------------------------------------------------------------------
@@ -523,8 +526,8 @@ int bucket_impl(sbdt_gpu_ctx* ctx, const std::uint32_t* d_labels, std::uint64_t 
     k_bucket_count<<<tiles, kBucketThreads, sizeof(std::uint32_t) * kl, st>>>(d_labels, n, l0, kl, tc, tiles);
     ++ctx->launches;
   }
-  exclusive_scan(tc, tc, cells, bs, nullptr, st, &ctx->launches);
-  k_part_offsets<<<1, 256, 0, st>>>(tc, k, tiles, n, d_part_offsets);
+  exclusive_scan(tc, tc, cells, bs, tc + cells, st, &ctx->launches);
+  k_part_offsets<<<1, 256, 0, st>>>(tc, k, tiles, n, d_part_offsets, ctx->d_status);
   ++ctx->launches;
   for (std::uint32_t l0 = 0; l0 < k; l0 += kBucketLabels) {
     const std::uint32_t kl = k - l0 < kBucketLabels ? k - l0 : kBucketLabels;

@@ -77,9 +77,11 @@ __global__ void k_pbbox_init(unsigned long long* pbbox, std::uint32_t count, int
 // arithmetic); 0 = degenerate, which the reference's circumsphere rejects
 // with DegenerateSimplex (geometry.cpp:279-297).
 template <int D>
-__device__ __forceinline__ int orientation_exact(const double (*p)[D]) {
-  if constexpr (D == 3) return sbdt_pred::orient3(p[0], p[1], p[2], p[3]);
-  else return sbdt_pred::orient2(p[0], p[1], p[2]);
+__device__ __forceinline__ int orientation_exact(const double (*p)[D], unsigned long long* escalations = nullptr) {
+  const double* q[D + 1];
+#pragma unroll
+  for (int j = 0; j <= D; ++j) q[j] = p[j];
+  return orient_dev<D>(q, escalations);
 }
 
 // circumsphere (geometry.cpp:279-327) + inflated (geometry.hpp:179-183)
@@ -481,7 +483,7 @@ __device__ bool cell_points_outside(const BorderArgs& a, unsigned long long idx,
     const CellPt<D> q = pts[t];
     if (q.label == self) continue;
     q4[D] = q.x;
-    const int o = orient_dev<D>(q4);
+    const int o = orient_dev<D>(q4, a.counters ? a.counters + kCtrOrientExact : nullptr);
     if (o != 0 && o != inner_sign) return true;
   }
   return false;
@@ -1117,7 +1119,9 @@ __global__ void __launch_bounds__(256) k_border_orient(BorderArgs a, const std::
     for (int j = 0; j <= D; ++j) v[j] = cand[std::uint64_t(j + 1) * cap + t];
     double p[D + 1][D];
     load_simplex<D>(a, v, p);
-    if (orientation_exact<D>(p) == 0) atomicOr(a.status, kStDegenerate);
+    if (a.counters) atomicAdd(a.counters + kCtrOrientRows, 1ull);
+    if (orientation_exact<D>(p, a.counters ? a.counters + kCtrOrientExact : nullptr) == 0)
+      atomicOr(a.status, kStDegenerate);
   }
 }
 
@@ -1377,6 +1381,7 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_border_infinite(BorderArgs 
   const unsigned full = 0xffffffffu;
   const unsigned lane = threadIdx.x & 31u;
   WideEntry<D>* stk = stacks[threadIdx.x >> 5];
+  unsigned long long* const pesc = a.counters ? a.counters + kCtrOrientExact : nullptr;
   const unsigned count = *a.inf_count;
   const bool use_hull_set = Ex && a.hull_valid && *a.hull_valid;
   const unsigned long long n_hull = use_hull_set ? *a.hull_count : 0ull;
@@ -1414,7 +1419,7 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_border_infinite(BorderArgs 
 #pragma unroll
       for (int j = 0; j < D; ++j) pts[j] = fx[j];
       pts[D] = a.xyz + std::size_t(inner) * D;
-      inner_sign = orient_dev<D>(pts);
+      inner_sign = orient_dev<D>(pts, pesc);
     }
     bool pos = false;
     if (a.policy == SBDT_POLICY_BBOX) {
@@ -1425,7 +1430,7 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_border_infinite(BorderArgs 
         for (std::uint32_t j = 0; j < a.k && !pos; ++j) {
           if (j == self) continue;
           double blo[D], bhi[D];
-          if (bbox_policy_box<D>(og, a.pbbox, j, blo, bhi) && corners_outside<D>(facet, inner_sign, blo, bhi) > 0)
+          if (bbox_policy_box<D>(og, a.pbbox, j, blo, bhi) && corners_outside<D>(facet, inner_sign, blo, bhi, pesc) > 0)
             pos = true;
         }
       }
@@ -1451,7 +1456,7 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_border_infinite(BorderArgs 
         auto test = [&](int L, const int* cc) -> int {
           double blo[D], bhi[D];
           og_block_box<D>(og, L, cc, blo, bhi);
-          const int out = corners_outside<D>(facet, sl_sign, blo, bhi);
+          const int out = corners_outside<D>(facet, sl_sign, blo, bhi, pesc);
           if (out == 0) return 0;
           if (out == (1 << D)) return 2;  // the whole box is strictly outside
           if (L > 0) return 1;
@@ -1483,7 +1488,7 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_border_infinite(BorderArgs 
               const std::uint32_t id = a.hull_ids[u];
               if (a.labels[id] != sl_self) {
                 q4[D] = a.xyz + std::size_t(id) * D;
-                const int r = orient_dev<D>(q4);
+                const int r = orient_dev<D>(q4, pesc);
                 o = r != 0 && r != sl_sign;
               }
             }
@@ -1652,9 +1657,12 @@ __global__ void k_border_spheres(BorderArgs a) {
   }
 }
 
-__global__ void k_cand_count(const unsigned* ncand, std::uint64_t S, unsigned long long* counters) {
+__global__ void k_cand_count(const unsigned* ncand, std::uint64_t S, unsigned long long* counters,
+                             const unsigned* esc_count, unsigned esc_cap) {
   counters[0] = S;  // rows scanned by the prefilter (finite + infinite)
   counters[1] = *ncand - counters[11];  // queue slots minus the holes
+  // exact policy: (row, point) in_sphere tests the filter left undecided
+  counters[kCtrInSphereExact] = esc_count ? min(*esc_count, esc_cap) : 0u;
 }
 
 __global__ void k_u32_to_u64(const std::uint32_t* in, std::uint64_t* out) { *out = *in; }
@@ -1724,7 +1732,8 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   SBDT_WS(og, OwnerGrid<D>, "border.og", 1);
   SBDT_WS(owner, std::uint16_t, "border.owner", owner_len);
   SBDT_WS(bbox, unsigned long long, "border.bbox", 2 * D);
-  SBDT_WS(infq, std::uint32_t, "border.infq", in->S / 2 + 1024);
+  // hull rows <= rows (small partitions can be mostly hull: >50% at ~5 points per part)
+  SBDT_WS(infq, std::uint32_t, "border.infq", in->S + 1024);
   SBDT_WS(infc, unsigned, "border.infc", 1);
   unsigned long long* pbbox = nullptr;
   if (in->policy == SBDT_POLICY_BBOX) {
@@ -1875,8 +1884,8 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   }
   a.counters = nullptr;
   if (ctx->census) {
-    SBDT_WS(cnt, unsigned long long, "border.counters", 12);
-    SBDT_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 12, st));
+    SBDT_WS(cnt, unsigned long long, "border.counters", kBorderCounters);
+    SBDT_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * kBorderCounters, st));
     a.counters = cnt;
   }
   const std::size_t offs_sh = in->k + 1 <= kSmemOffsMax ? sizeof(std::uint64_t) * (in->k + 1) : 0;
@@ -2012,7 +2021,7 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
           ++ctx->launches;
         }
         if (a.counters) {
-          k_cand_count<<<1, 1, 0, st>>>(cn, in->S, a.counters);
+          k_cand_count<<<1, 1, 0, st>>>(cn, in->S, a.counters, a.esc_count, a.esc_cap);
           ctx->launches += 1;
         }
       } else if (blocks > 0) {

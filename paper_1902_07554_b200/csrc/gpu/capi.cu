@@ -168,12 +168,13 @@ int sbdt_gpu_assign_table_stats(sbdt_gpu_ctx* ctx, unsigned* out6) {
   return assign_stats(ctx, out6) == kOk ? SBDT_OK : SBDT_ERR_INVALID;
 }
 
-int sbdt_gpu_border_stats(sbdt_gpu_ctx* ctx, unsigned long long* out12) {
-  if (!ctx || !out12) return SBDT_ERR_INVALID;
+int sbdt_gpu_border_stats(sbdt_gpu_ctx* ctx, unsigned long long* out, int count) {
+  if (!ctx || !out || count < 0) return SBDT_ERR_INVALID;
   auto it = ctx->bufs.find("border.counters");
   if (it == ctx->bufs.end()) return SBDT_ERR_INVALID;
+  const int c = count < kBorderCounters ? count : kBorderCounters;
   cudaStreamSynchronize(ctx->stream);
-  cudaMemcpy(out12, it->second.ptr, sizeof(unsigned long long) * 12, cudaMemcpyDeviceToHost);
+  cudaMemcpy(out, it->second.ptr, sizeof(unsigned long long) * c, cudaMemcpyDeviceToHost);
   return SBDT_OK;
 }
 
@@ -188,6 +189,7 @@ int sbdt_gpu_check_status(sbdt_gpu_ctx* ctx) {
   if (st & kStQueueOverflow) return fail(ctx, SBDT_ERR_RANGE, "escalation queue overflow");
   if (st & 8u) return fail(ctx, SBDT_ERR_MERGE, "InconsistentMerge: a facet with more than two finite owners");
   if (st & 16u) return fail(ctx, SBDT_ERR_MERGE, "DanglingFacet: a hull ridge without exactly two hull facets");
+  if (st & kStLabelRange) return fail(ctx, SBDT_ERR_INVALID, "sample label out of range (must be < k)");
   return SBDT_OK;
 }
 
@@ -280,8 +282,10 @@ int sbdt_gpu_assign_points(sbdt_gpu_ctx* ctx, int dim, const double* coords, uin
   // only them), then the points in chunks on the copy stream
   double* d_sxyz;
   TRY(dalloc(ctx, "h.sxyz", std::uint64_t(m) * dim, &d_sxyz));
-  for (uint32_t i = 0; i < m; ++i)
+  for (uint32_t i = 0; i < m; ++i) {
     if (sample_ids[i] >= n) return fail(ctx, SBDT_ERR_INVALID, "sample id out of range");
+    if (sample_labels[i] >= k) return fail(ctx, SBDT_ERR_INVALID, "sample label out of range (must be < k)");
+  }
   // the gather is m cache misses into the caller's point array: split over
   // host threads, into a page-locked staging buffer (an async copy)
   const std::size_t sbytes = sizeof(double) * std::size_t(m) * dim;

@@ -127,10 +127,17 @@ __device__ __forceinline__ bool box_inside_sphere(const double* blo, const doubl
   return d2 <= r2;
 }
 
+// Exact orientation (filter, then expansion arithmetic when it cannot
+// decide); `escalations` (optional census counter) counts the expansion runs.
 template <int D>
-__device__ __forceinline__ int orient_dev(const double* const* p) {
-  if constexpr (D == 2) return sbdt_pred::orient2(p[0], p[1], p[2]);
-  else return sbdt_pred::orient3(p[0], p[1], p[2], p[3]);
+__device__ __forceinline__ int orient_dev(const double* const* p, unsigned long long* escalations = nullptr) {
+  int r;
+  if constexpr (D == 2) r = sbdt_pred::orient2_filtered(p[0], p[1], p[2]);
+  else r = sbdt_pred::orient3_filtered(p[0], p[1], p[2], p[3]);
+  if (r != 2) return r;
+  if (escalations) atomicAdd(escalations, 1ull);
+  if constexpr (D == 2) return sbdt_pred::orient2_exact(p[0], p[1], p[2]);
+  else return sbdt_pred::orient3_exact(p[0], p[1], p[2], p[3]);
 }
 
 // squared_distance (geometry.hpp:102-110): s = 0; s += t*t left to right.

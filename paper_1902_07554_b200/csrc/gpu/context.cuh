@@ -80,6 +80,20 @@ enum DeviceStatusBits : unsigned {
   kStDegenerate = 1u,
   kStGridCap = 2u,
   kStQueueOverflow = 4u,
+  // 8, 16: merge (InconsistentMerge, DanglingFacet)
+  kStLabelRange = 32u,  // a sample label >= k (device-pointer assign path)
+};
+
+// find_border census counters (sbdt_gpu_border_stats, census mode only):
+//  0 rows, 1 exact-stage rows, 2 flat scans, 3 two-level, 4 pyramid,
+//  5 (row, cell row) pairs, 6 pyramid expansions, 7 exact-stage binary32
+//  positives, 8 prefilter positives, 9 wide positives, 10 (unused),
+//  11 queue holes, then the predicate escalations:
+enum BorderCounter : int {
+  kCtrOrientRows = 12,     // rows whose binary32 sphere failed: exact orientation checked
+  kCtrOrientExact = 13,    // orient evaluations escalated to expansion arithmetic
+  kCtrInSphereExact = 14,  // in_sphere tests escalated (exact policy, k_border_escalate)
+  kBorderCounters = 16,
 };
 
 inline int fail(sbdt_gpu_ctx* ctx, int code, const std::string& msg) {

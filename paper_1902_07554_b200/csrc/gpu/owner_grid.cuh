@@ -643,7 +643,8 @@ __device__ __forceinline__ bool og_sphere_hits_foreign(const OwnerGrid<D>& og, c
 // box corner strictly on the outer side of the hull facet plane (exact
 // orient), accept = every corner strictly outside.
 template <int D>
-__device__ int corners_outside(const double* const* facet, int inner_sign, const double* blo, const double* bhi) {
+__device__ int corners_outside(const double* const* facet, int inner_sign, const double* blo, const double* bhi,
+                               unsigned long long* escalations = nullptr) {
   const double* pts[D + 1];
 #pragma unroll
   for (int i = 0; i < D; ++i) pts[i] = facet[i];
@@ -653,7 +654,7 @@ __device__ int corners_outside(const double* const* facet, int inner_sign, const
   for (unsigned cm = 0; cm < (1u << D); ++cm) {
 #pragma unroll
     for (int d = 0; d < D; ++d) corner[d] = (cm & (1u << d)) ? bhi[d] : blo[d];
-    const int s = orient_dev<D>(pts);
+    const int s = orient_dev<D>(pts, escalations);
     if (s != 0 && s != inner_sign) ++outside;
   }
   return outside;

@@ -5,6 +5,9 @@
 #include <cstring>
 #include <exception>
 
+#include <vector>
+
+#include "../common/predicates.hpp"
 #include "rng.hpp"
 #include "setup.hpp"
 
@@ -17,6 +20,34 @@ void set_err(char* err, int errlen, const char* msg) {
 }  // namespace
 
 extern "C" {
+
+// The shared predicates (csrc/common/predicates.hpp: binary64 filter, then
+// expansion arithmetic or scaled big integers), host build, in the layout of
+// sbdt_gpu_predicates: op 0 orient ((dim+1) points per case), op 1 in_sphere
+// ((dim+1) simplex points then q). The same source the kernels compile; the
+// tests pin it against the reference's compiled geometry.cpp on CPU.
+int sbdt_host_predicates(int op, int dim, const double* pts, std::uint64_t count, std::int8_t* out) {
+  if ((op != 0 && op != 1) || (dim != 2 && dim != 3)) return 1;
+  std::vector<double> buf(op == 1 ? (dim == 3 ? sbdt_pred::kInSphere3Scratch : sbdt_pred::kInSphere2Scratch) : 1);
+  for (std::uint64_t i = 0; i < count; ++i) {
+    int r;
+    if (op == 0) {
+      const double* b = pts + i * (dim + 1) * dim;
+      r = dim == 2 ? sbdt_pred::orient2(b, b + 2, b + 4) : sbdt_pred::orient3(b, b + 3, b + 6, b + 9);
+    } else {
+      const double* b = pts + i * (dim + 2) * dim;
+      if (dim == 2) {
+        r = sbdt_pred::in_sphere2_filtered(b, b + 2, b + 4, b + 6);
+        if (r == 2) r = sbdt_pred::in_sphere2_exact_buf(b, b + 2, b + 4, b + 6, buf.data());
+      } else {
+        r = sbdt_pred::in_sphere3_filtered(b, b + 3, b + 6, b + 9, b + 12);
+        if (r == 2) r = sbdt_pred::in_sphere3_exact_buf(b, b + 3, b + 6, b + 9, b + 12, buf.data());
+      }
+    }
+    out[i] = static_cast<std::int8_t>(r);
+  }
+  return 0;
+}
 
 std::uint64_t sbdt_host_generate(int kind, int dim, std::uint64_t n, std::uint64_t seed,
                                  const double* params, int nparams, double* out) {

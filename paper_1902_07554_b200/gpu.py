@@ -65,6 +65,8 @@ EXPORTS = [
     "sbdt_gpu_host_alloc", "sbdt_gpu_host_free", "sbdt_gpu_create", "sbdt_gpu_destroy", "sbdt_gpu_last_error", "sbdt_gpu_set_stream", "sbdt_gpu_synchronize",
     "sbdt_gpu_launch_count", "sbdt_gpu_check_status", "sbdt_gpu_assign_points", "sbdt_gpu_assign_points_dev",
     "sbdt_gpu_find_border", "sbdt_gpu_find_border_dev", "sbdt_gpu_merge", "sbdt_gpu_merge_dev",
+    "sbdt_gpu_set_timing", "sbdt_gpu_stage_times", "sbdt_gpu_assign_table_stats", "sbdt_gpu_border_stats",
+    "sbdt_gpu_predicates", "sbdt_gpu_microbench",
 ]
 
 
@@ -106,7 +108,9 @@ def lib():
         L.sbdt_gpu_set_timing.argtypes = [vp, C.c_int]
         L.sbdt_gpu_stage_times.argtypes = [vp, C.c_char_p, C.c_int, C.POINTER(C.c_float), C.c_int]
         L.sbdt_gpu_assign_table_stats.argtypes = [vp, C.POINTER(C.c_uint)]
-        L.sbdt_gpu_border_stats.argtypes = [vp, C.POINTER(C.c_ulonglong)]
+        L.sbdt_gpu_border_stats.argtypes = [vp, C.POINTER(C.c_ulonglong), C.c_int]
+        L.sbdt_gpu_predicates.argtypes = [vp, C.c_int, C.c_int, dp, u64, i8p, u64p]
+        L.sbdt_gpu_microbench.argtypes = [vp, C.c_int, u64, dp]
         _lib = L
     return _lib
 
@@ -173,12 +177,36 @@ class Context:
                 "queued_points": int(out[4]), "dense_cells": int(out[5])}
 
     def border_stats(self) -> dict:
-        out = (C.c_ulonglong * 12)()
-        if lib().sbdt_gpu_border_stats(self._h, out) != SBDT_OK:
+        out = (C.c_ulonglong * 16)()
+        if lib().sbdt_gpu_border_stats(self._h, out, 16) != SBDT_OK:
             return {}
-        keys = ["rows", "exact_stage_rows", "exact_flat_scan", "wide_two_level", "wide_pyramid", "row_pairs",
-                "wide_expansions", "exact_flat_positive", "prefilter_positive", "wide_positive"]
-        return {kk: int(out[i]) for i, kk in enumerate(keys)}
+        keys = {0: "rows", 1: "exact_stage_rows", 2: "exact_flat_scan", 3: "wide_two_level", 4: "wide_pyramid",
+                5: "row_pairs", 6: "wide_expansions", 7: "exact_flat_positive", 8: "prefilter_positive",
+                9: "wide_positive", 12: "orient_check_rows", 13: "orient_escalations", 14: "in_sphere_escalations"}
+        return {kk: int(out[i]) for i, kk in keys.items()}
+
+    # ---- diagnostics (tests / bench): device predicates, binding ceilings
+    def predicates(self, op: str, pts: np.ndarray):
+        """Device orient / in_sphere (filter + expansion arithmetic) on host
+        cases: pts (count, dim+1, dim) for "orient", (count, dim+2, dim) for
+        "in_sphere" (simplex then q). Returns (signs int8, n_escalated)."""
+        pts = np.ascontiguousarray(pts, np.float64)
+        count, npts, dim = pts.shape
+        opc = {"orient": 0, "in_sphere": 1}[op]
+        if npts != dim + 1 + opc:
+            raise ValueError("predicates: wrong point count per case")
+        out = np.empty(count, np.int8)
+        ne = C.c_uint64(0)
+        self.check(lib().sbdt_gpu_predicates(self._h, opc, dim, _p(pts, C.c_double), count, _p(out, C.c_int8),
+                                             C.byref(ne)), "predicates")
+        return out, int(ne.value)
+
+    def microbench(self, kind: str, nbytes: int = 0) -> float:
+        """"dfma" -> FLOP/s; "gather" -> random 8-byte gathers/s from an nbytes table."""
+        r = C.c_double(0)
+        self.check(lib().sbdt_gpu_microbench(self._h, {"dfma": 0, "gather": 1}[kind], nbytes, C.byref(r)),
+                   "microbench")
+        return float(r.value)
 
     # ---- device-pointer entry points (inputs resident in HBM; async on the stream)
     def assign_points_dev(self, dim, d_xyz, n, d_sample_ids, d_sample_labels, m, k, d_labels, d_part_offsets=None,

@@ -50,6 +50,7 @@ def lib():
         L.sbdt_host_partials_total.argtypes = [C.c_void_p]
         L.sbdt_host_partials_export.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), u32p, u32p, i8p]
         L.sbdt_host_partials_free.argtypes = [C.c_void_p]
+        L.sbdt_host_predicates.argtypes = [C.c_int, C.c_int, dp, u64, C.POINTER(C.c_int8)]
         _lib = L
     return _lib
 
@@ -66,6 +67,19 @@ def generate(dist: str, dim: int, n: int, seed: int, params=()) -> np.ndarray:
     if got != n:
         raise ValueError(f"generate({dist}, dim={dim}) failed")
     return out.reshape(n, dim)
+
+
+def predicates(op: str, pts: np.ndarray) -> np.ndarray:
+    """The shared predicates (predicates.hpp) on the host, same layout as
+    gpu.Context.predicates: (count, dim+1, dim) orient / (count, dim+2, dim)
+    in_sphere cases -> signs."""
+    pts = np.ascontiguousarray(pts, np.float64)
+    count, _, dim = pts.shape
+    out = np.empty(count, np.int8)
+    if lib().sbdt_host_predicates({"orient": 0, "in_sphere": 1}[op], dim, ptr(pts, C.c_double), count,
+                                  ptr(out, C.c_int8)) != 0:
+        raise ValueError("predicates: bad op / dim")
+    return out
 
 
 def deduplicate(points: np.ndarray) -> np.ndarray:

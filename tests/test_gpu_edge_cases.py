@@ -197,3 +197,67 @@ def test_find_border_many_partitions(ctx):
         assert np.array_equal(g.positive, o["positive"]), policy
         assert np.array_equal(g.border, o["border"]), policy
         assert np.array_equal(g.positive_vertex_ids, o["vertices_positive"]), policy
+
+
+def _grid_parts(dim, n, side, seed):
+    """Points labelled by a side^dim grid of parts (a few points per part);
+    parts with fewer than dim + 1 points get an empty row range."""
+    rng = np.random.default_rng(seed)
+    pts = np.ascontiguousarray(rng.random((n, dim)))
+    cell = np.minimum((pts * side).astype(np.int64), side - 1)
+    lab = np.zeros(n, np.int64)
+    for d in range(dim):
+        lab = lab * side + cell[:, d]
+    lab = lab.astype(np.uint32)
+    k = side ** dim
+    tris = [host.triangulate(pts, np.nonzero(lab == p)[0].astype(np.uint32), 7)
+            if np.count_nonzero(lab == p) > dim else None for p in range(k)]
+    offs = np.zeros(k + 1, np.uint64)
+    offs[1:] = np.cumsum([t.verts.shape[1] if t else 0 for t in tris])
+    T = [t for t in tris if t]
+    P = host.Partials(offs, np.concatenate([t.verts for t in T], 1), np.concatenate([t.nbrs for t in T], 1),
+                      np.concatenate([t.parity for t in T]))
+    return pts, lab, P
+
+
+def test_tiny_parts_mostly_hull_rows(ctx):
+    """~3 points per part (k = 4096, 3-D): two thirds of all rows are hull
+    (infinite) rows — more than half, the old hull-queue capacity."""
+    pts, lab, P = _grid_parts(3, 12_000, 16, 21)
+    assert np.count_nonzero(P.verts[3] == 0xFFFFFFFF) > 0.6 * P.S
+    for policy in ("grid", "exact"):
+        g = gpu.find_border(pts, lab, P, gpu.IntersectionPolicy(policy, 1.0), hull_bfs=True, ctx=ctx)
+        o = oracle.find_border(pts, lab, P, policy)
+        assert np.array_equal(g.positive, o["positive"]), policy
+        assert np.array_equal(g.border, o["border"]), policy
+        assert np.array_equal(g.positive_vertex_ids, o["vertices_positive"]), policy
+
+
+def test_sample_label_out_of_range(ctx):
+    """A sample label >= k is rejected (the C++ header's precondition,
+    include/sbdt/sample_partition.hpp): up front by the host-buffer entry
+    point, and by the bucketing pass's count check on the device path."""
+    import torch
+    rng = np.random.default_rng(9)
+    pts = np.ascontiguousarray(rng.random((5000, 3)))
+    sid = np.arange(0, 5000, 50, dtype=np.uint32)
+    slab = (np.arange(len(sid)) % 4).astype(np.uint32)
+    slab[7] = 4  # k = 4
+    with pytest.raises(ValueError):
+        gpu.assign_points(pts, sid, slab, 4, ctx=ctx)
+    dev = torch.device("cuda", 0)
+    d_xyz = torch.from_numpy(pts).to(dev)
+    d_sid = torch.from_numpy(sid.view(np.int32)).to(dev)
+    d_slab = torch.from_numpy(slab.view(np.int32)).to(dev)
+    d_lab = torch.empty(5000, dtype=torch.int32, device=dev)
+    d_off = torch.empty(5, dtype=torch.int64, device=dev)
+    d_ids = torch.empty(5000, dtype=torch.int32, device=dev)
+    torch.cuda.synchronize()
+    ctx.assign_points_dev(3, d_xyz.data_ptr(), 5000, d_sid.data_ptr(), d_slab.data_ptr(), len(sid), 4,
+                          d_lab.data_ptr(), d_off.data_ptr(), d_ids.data_ptr())
+    with pytest.raises(ValueError):
+        ctx.synchronize()
+    ctx.synchronize()  # the status was consumed: the context stays usable
+    slab[7] = 3
+    part = gpu.assign_points(pts, sid, slab, 4, ctx=ctx)
+    assert np.array_equal(part.labels, oracle.assign_brute(pts, sid, slab))
