@@ -143,6 +143,27 @@ def algorithmic_bytes(dim, n, S, cells, n_vb):
     return b_assign, b_border
 
 
+def ceilings(ctx):
+    """Binding ceilings measured on this device (diagnostic C-ABI microbenchmarks):
+    the DFMA issue peak and random 8-byte gathers from an L2-sized table (the
+    prefilter's 80 MB packed coordinates) and from an HBM-sized one (2 GB,
+    the exact stage's binary64 coordinates by PointId, ~L2-missing). The border
+    kernels are gather-, latency- and issue-bound rather than bandwidth-bound;
+    these are the ceilings their per-kernel fractions are read against
+    (profiles/README.md)."""
+    try:
+        dfma = ctx.microbench("dfma")
+        g80 = ctx.microbench("gather", 80 << 20)
+        g2g = ctx.microbench("gather", 2 << 30)
+    except Exception as e:  # diagnostic only
+        return {"error": str(e)}
+    return {"dfma_tflops": round(dfma / 1e12, 2), "gather8_l2_gps": round(g80 / 1e9, 1),
+            "gather8_hbm_gps": round(g2g / 1e9, 1),
+            "issue_peak_warp_inst_per_s": None,
+            "note": "gathers/s of independent random 8-byte loads (4 in flight per thread, 148x16 CTAs of 256); "
+                    "DFMA: 8 independent chains per thread"}
+
+
 def config_dict(inst, policy, world, cells):
     """The `config` of both arms (identical keys and values)."""
     part = inst.partials
@@ -478,6 +499,10 @@ def main():
 
     value = sdist.aggregate_throughput(n, world, total_ms / args.steps * 1e-3)
     clocks = clk.summary()
+    ceil = ceilings(ctx) if rank == 0 and not args.profile else None
+    if ceil and "error" not in ceil:
+        sm = torch.cuda.get_device_properties(dev).multi_processor_count
+        ceil["issue_peak_warp_inst_per_s"] = sm * 4 * (clocks.get("sm_mhz") or 1965.0) * 1e6
 
     # ---- end to end through the host-buffer C ABI (pinned buffers; H2D+D2H inside)
     e2e = None
@@ -548,6 +573,7 @@ def main():
                             "assign_roofline": roof(b_assign, t_assign), "border_roofline": roof(b_border, t_border)},
             "roofline": roofline,
             "kernel_rooflines": per_kernel,
+            "ceilings": ceil,
             "hull_bfs": {"ms_per_step": round(sum(ms_bfs) / len(ms_bfs), 4),
                          "stages_ms": {kk: round(v, 4) for kk, v in stages_bfs.items()},
                          "border_vertices": n_vb_bfs},

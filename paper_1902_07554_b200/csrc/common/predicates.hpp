@@ -501,7 +501,7 @@ SBDT_HDN int orient2_expansion(const double* a, const double* b, const double* c
 
 // Exact orient2: expansion arithmetic on prescaled inputs, big integers
 // when the inputs' exponent range is too wide for it.
-SBDT_HD int orient2_exact(const double* a, const double* b, const double* c) {
+SBDT_HDN int orient2_exact(const double* a, const double* b, const double* c) {
   const double v[6] = {a[0], a[1], b[0], b[1], c[0], c[1]};
   const int s = prescale_exponent(v, 6, 2);
   if (s == kNoScale) return orient2_big(a, b, c);
@@ -577,7 +577,7 @@ SBDT_HDN int orient3_expansion(const double* a, const double* b, const double* c
   return expansion_sign(n, out);
 }
 
-SBDT_HD int orient3_exact(const double* a, const double* b, const double* c, const double* d) {
+SBDT_HDN int orient3_exact(const double* a, const double* b, const double* c, const double* d) {
   const double v[12] = {a[0], a[1], a[2], b[0], b[1], b[2], c[0], c[1], c[2], d[0], d[1], d[2]};
   const int s = prescale_exponent(v, 12, 3);
   if (s == kNoScale) return orient3_big(a, b, c, d);
@@ -652,7 +652,7 @@ SBDT_HDN int in_sphere2_expansion(const double* a, const double* b, const double
 
 // Exact in_sphere2 (degree 4): expansion arithmetic on prescaled inputs, big
 // integers for too wide an exponent range. buf: kInSphere2Scratch doubles.
-SBDT_HD int in_sphere2_exact_buf(const double* a, const double* b, const double* c, const double* q, double* buf) {
+SBDT_HDN int in_sphere2_exact_buf(const double* a, const double* b, const double* c, const double* q, double* buf) {
   const double v[8] = {a[0], a[1], b[0], b[1], c[0], c[1], q[0], q[1]};
   const int s = prescale_exponent(v, 8, 4);
   if (s == kNoScale) return in_sphere2_big(a, b, c, q, buf);
@@ -733,7 +733,7 @@ SBDT_HDN int in_sphere3_expansion(const double* a, const double* b, const double
 }
 
 // Exact in_sphere3 (degree 5), as in_sphere2_exact_buf. buf: kInSphere3Scratch doubles.
-SBDT_HD int in_sphere3_exact_buf(const double* a, const double* b, const double* c, const double* d,
+SBDT_HDN int in_sphere3_exact_buf(const double* a, const double* b, const double* c, const double* d,
                                  const double* q, double* buf) {
   const double v[15] = {a[0], a[1], a[2], b[0], b[1], b[2], c[0], c[1], c[2], d[0], d[1], d[2], q[0], q[1], q[2]};
   const int s = prescale_exponent(v, 15, 5);

@@ -715,11 +715,21 @@ __device__ __forceinline__ bool octant_proof(const OwnerGrid<D>& og, const Borde
   return hit;
 }
 
+// Rows are claimed by CTAs in chunks of kPfChunk from a launch-wide cursor
+// (instead of a static grid-stride split): every CTA works on the same
+// sliding window of rows, so the packed-coordinate lines and owner codes of
+// the 1-2 partitions in flight stay in L2 instead of spreading over the rows
+// of CTAs that drifted apart, and the CTA's warps take consecutive 32-row
+// slices of its chunk (vertices shared by neighbouring rows hit in L1).
+constexpr unsigned kPfIters = 16;
+constexpr unsigned kPfChunk = kBThreads * kPfIters;
+
 template <int D, bool BIGK>
 __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
                                                                 std::uint32_t* __restrict__ cand, std::uint64_t cap,
                                                                 unsigned* __restrict__ ncand, std::uint64_t row_begin,
-                                                                std::uint64_t row_end) {
+                                                                std::uint64_t row_end,
+                                                                unsigned long long* __restrict__ cursor) {
   __shared__ OwnerGrid<D> og;
   extern __shared__ std::uint64_t s_off_sh[];
   if (threadIdx.x == 0) og = *ogp;
@@ -730,9 +740,15 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
   const std::uint64_t* s_off = BIGK ? a.offsets : s_off_sh;
   const unsigned lane = threadIdx.x & 31u;
   const unsigned lt = (1u << lane) - 1u;
-  const std::uint64_t stride = std::uint64_t(gridDim.x) * blockDim.x;
-  // rows [row_begin, row_end); whole warps iterate together
-  const std::uint64_t S_up = row_begin + ((row_end - row_begin + 31) & ~std::uint64_t(31));
+  // rows [row_begin, row_end); the whole CTA iterates over claimed chunks,
+  // with one chunk of lookahead for the id prefetch
+  __shared__ unsigned long long s_claim;
+  if (threadIdx.x == 0) s_claim = atomicAdd(cursor, 2ull * kPfChunk);
+  __syncthreads();
+  std::uint64_t base = row_begin + s_claim;
+  std::uint64_t next_base = base + kPfChunk;
+  const unsigned wofs = threadIdx.x & ~31u;  // this warp's slice of a 256-row step
+  unsigned it = 0;
   // binary32 cell-unit scale and margin (rounded up; the slacks cover the rest)
   // decode_row's coordinate unit: the fixed-point step in 3-D, 1 in 2-D
   const double unit = D == 3 ? og.qh : 1.0;
@@ -747,7 +763,7 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
     pos_ok = pos_ok && fabs(og.g.lo[d]) * og.inv_edge + static_cast<double>(og.ldims[0][d]) < 67108864.0;
   // software pipeline: the vertex ids of the next row are in flight while
   // this row's coordinates are gathered and tested
-  std::uint64_t s = row_begin + std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  std::uint64_t s = base + wofs + lane;
   std::uint32_t self = part_of(s_off, a.k, s < row_end ? s : row_end - 1);
   std::uint64_t next_off = self + 1 < a.k ? s_off[self + 1] : ~0ull;  // first row of the next part
   std::uint32_t vn[D + 1];
@@ -760,17 +776,19 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
   // atomic per chunk instead of one per iteration on the single counter);
   // the slots a warp leaves unused at exit are written as kNoRow holes
   unsigned qbase = 0, qleft = 0;
-  for (; s < S_up; s += stride) {
+  while (base < row_end) {
     const bool valid = s < row_end;
     std::uint32_t v[D + 1];
     std::uint64_t w[D + 1];
 #pragma unroll
     for (int j = 0; j <= D; ++j) v[j] = vn[j];
-    load_ids(s + stride, vn);
+    // the next row of this lane: the next 32 of the chunk, or the lookahead chunk
+    const std::uint64_t s_next = it + 1 < kPfIters ? s + kBThreads : next_base + wofs + lane;
+    load_ids(s_next, vn);
     const bool inf = valid && v[D] == kInfVertex;
     bool is_cand = false;
     float cU[D], creach = -1.f;  // recorded for the exact stage's neighbour test
-    // rows only grow along the grid-stride loop: advance the part cursor
+    // a warp's rows only grow (claims are monotonic): advance the part cursor
     {
       const std::uint64_t sc = valid ? s : row_end - 1;
       while (next_off <= sc) {
@@ -831,6 +849,15 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
         for (int d = 0; d < D; ++d) cand[std::uint64_t(D + 2 + d) * cap + q] = __float_as_uint(cU[d]);
     }
     if (inf) a.inf_queue[bi + __popc(mi & lt)] = static_cast<std::uint32_t>(s);
+    s = s_next;
+    if (++it == kPfIters) {  // CTA-uniform
+      it = 0;
+      __syncthreads();  // every thread has read s_claim
+      if (threadIdx.x == 0) s_claim = atomicAdd(cursor, static_cast<unsigned long long>(kPfChunk));
+      __syncthreads();
+      base = next_base;
+      next_base = row_begin + s_claim;
+    }
   }
   for (unsigned i = lane; i < qleft; i += 32) cand[qbase + i] = kNoRow;
   if (a.counters && lane == 0 && qleft) atomicAdd(&a.counters[11], static_cast<unsigned long long>(qleft));
@@ -1932,14 +1959,17 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
         else
           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_wide<D, false>, kWideWarps * 32, offs_sh);
         const unsigned resW = static_cast<unsigned>(sms * (per_sm > 0 ? per_sm : 1));
-        auto prefilter = [&](std::uint64_t r0, std::uint64_t r1) {
+        SBDT_WS(pfcur, unsigned long long, "border.pf_cursor", 1);
+        auto prefilter = [&](std::uint64_t r0, std::uint64_t r1) -> int {
           const std::uint64_t want = (r1 - r0 + kBThreads - 1) / kBThreads;
+          SBDT_CUDA_TRY(cudaMemsetAsync(pfcur, 0, sizeof(unsigned long long), st));
           if (bigk)
             k_border_prefilter<D, true><<<static_cast<unsigned>(want < resA ? want : resA), kBThreads, 0, st>>>(
-                a, og, cq, qcap, cn, r0, r1);
+                a, og, cq, qcap, cn, r0, r1, pfcur);
           else
             k_border_prefilter<D, false><<<static_cast<unsigned>(want < resA ? want : resA), kBThreads, offs_sh, st>>>(
-                a, og, cq, qcap, cn, r0, r1);
+                a, og, cq, qcap, cn, r0, r1, pfcur);
+          return kOk;
         };
         auto exact = [&]() {
           if (exact_policy)
@@ -1960,7 +1990,8 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
         if (ctx->chunks.empty()) {
           {
             StageTimer ta(ctx, "border.prefilter");
-            prefilter(0, in->S);
+            const int prc = prefilter(0, in->S);
+            if (prc != kOk) return prc;
           }
           // the hull queue is complete once the prefilter ran: its halfspace
           // kernel (few rows, latency-bound) overlaps exact + wide on the side
@@ -2001,7 +2032,8 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
             const std::uint64_t r1 = c.first < in->S ? c.first : in->S;
             SBDT_CUDA_TRY(cudaStreamWaitEvent(st, c.second, 0));
             if (r1 > r0) {
-              prefilter(r0, r1);
+              const int prc = prefilter(r0, r1);
+              if (prc != kOk) return prc;
               exact();
               wide();
               ctx->launches += 3;

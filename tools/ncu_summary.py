@@ -2,6 +2,7 @@
 
   python tools/ncu_summary.py launches <launch-list.csv>      per-kernel time shares
   python tools/ncu_summary.py full <report.ncu-rep> [...]      key --set full metrics
+  python tools/ncu_summary.py quick <metrics.csv>              tools/ncu_quick.sh output: per kernel, last launch
   python tools/ncu_summary.py traffic <report.ncu-rep> [...]   DRAM bytes per launch -> JSON
                                                                (profiles/ncu_traffic.json, read by bench.py)
 
@@ -49,6 +50,29 @@ KEYS = [
     ("launch__grid_size", "grid"),
     ("launch__block_size", "block"),
 ]
+
+
+def quick(path):
+    """Per kernel (the last launch of each name): the targeted metric set."""
+    rows = list(csv.reader(open(path)))
+    hdr = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    cols = rows[hdr]
+    ci = {c: i for i, c in enumerate(cols)}
+    per = collections.OrderedDict()
+    for r in rows[hdr + 1:]:
+        if len(r) != len(cols):
+            continue
+        name = r[ci["Kernel Name"]].split("(")[0].replace("void ", "").strip()
+        per.setdefault((name, int(r[ci["ID"]])), {})[r[ci["Metric Name"]]] = (r[ci["Metric Value"]], r[ci["Metric Unit"]])
+    last = collections.OrderedDict()
+    for (name, lid), m in per.items():
+        last[name] = m
+    for name, m in last.items():
+        print(f"### `{name}`\n")
+        print("| metric | value | unit |\n|---|---:|---|")
+        for k in sorted(m):
+            print(f"| `{k}` | {m[k][0]} | {m[k][1]} |")
+        print()
 
 
 def full(paths):
@@ -120,5 +144,7 @@ if __name__ == "__main__":
         launches(sys.argv[2])
     elif sys.argv[1] == "traffic":
         traffic(sys.argv[2:])
+    elif sys.argv[1] == "quick":
+        quick(sys.argv[2])
     else:
         full(sys.argv[2:])
