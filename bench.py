@@ -143,6 +143,34 @@ def algorithmic_bytes(dim, n, S, cells, n_vb):
     return b_assign, b_border
 
 
+def dropin_leg(exe, inst, part, steps):
+    """e2e through the C++ drop-in headers (the reference-facing C++ API):
+    the instance goes to a file, dropin_example times `steps` full steps."""
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        src = os.path.join(td, "instance.bin")
+        with open(src, "wb") as f:
+            f.write(np.array([inst.dim], np.uint32).tobytes() + np.array([inst.n], np.uint64).tobytes()
+                    + np.array([len(inst.sample_ids), part.k], np.uint32).tobytes()
+                    + np.array([part.S], np.uint64).tobytes())
+            for a in (inst.points, inst.sample_ids, inst.sample_labels, part.offsets, part.verts, part.nbrs,
+                      part.parity):
+                f.write(np.ascontiguousarray(a).tobytes())
+        try:
+            r = subprocess.run([exe, src, os.path.join(td, "out.bin"), "--bench", str(steps)], capture_output=True,
+                               text=True, timeout=600)
+        except subprocess.TimeoutExpired:
+            return {"error": "timeout"}
+    if r.returncode != 0:
+        return {"error": r.stderr.strip()[-300:]}
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    d.update(value=inst.n / (d["ms_per_step"] * 1e-3), unit="points/s",
+             path="sbdt::assign_points + sbdt::build_grid_index + sbdt::find_border(BorderOptions{no BFS, "
+                  "points resident}) on the reference's PointSet / Triangulation<D>, TaskPool(all threads), "
+                  "host buffers (tests/cpp/dropin_example.cpp --bench)")
+    return d
+
+
 def ceilings(ctx):
     """Binding ceilings measured on this device (diagnostic C-ABI microbenchmarks):
     the DFMA issue peak and random 8-byte gathers from an L2-sized table (the
@@ -551,6 +579,15 @@ def main():
                "path": "sbdt_gpu_assign_points + sbdt_gpu_find_border(RESIDENT_POINTS) (host buffers, pinned)"}
         ectx.close()
 
+    # ---- the C++ drop-in path (include/sbdt/*.hpp on the reference's own
+    # PointSet / Triangulation<D>, tests/cpp/dropin_example.cpp --bench):
+    # assign_points + build_grid_index + find_border(no BFS, points resident)
+    # on a TaskPool of all host threads, host buffers, wall clock per step
+    dropin = None
+    exe = os.path.join(ROOT, "paper_1902_07554_b200", "dropin_example")
+    if rank == 0 and world == 1 and not args.no_e2e and not args.profile and os.path.exists(exe):
+        dropin = dropin_leg(exe, inst, part, max(1, min(args.steps, 5)))
+
     cpu, par = None, None
     if rank == 0 and world == 1 and not args.no_parity and not args.profile:
         cores = os.cpu_count() or 1
@@ -580,7 +617,7 @@ def main():
             "border_vertices": n_vb, "positive_simplices": n_pos, "assign_table": table_stats, "border_pipeline": border_stats,
             "gpu_launches": int(launches), "gpu_launches_per_step": launches / args.steps,
             "clocks": clocks, "wall_timed_s": round(t_wall, 3), "setup_s": round(setup_s, 1),
-            "e2e": e2e, "cpu_baseline": cpu,
+            "e2e": e2e, "e2e_dropin": dropin, "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
     if dist:

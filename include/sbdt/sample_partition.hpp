@@ -7,13 +7,15 @@
 // SURVEY.md F1/F2). This header gives it the SPEC's signature with the
 // conventions of the shipped headers (proj/include/sbdt/*.hpp): namespace
 // sbdt, D in {2,3} as a template parameter, uint32 ids, std::span inputs,
-// return by value, an optional TaskPool* (unused: the work runs on the GPU),
+// return by value, an optional TaskPool* (host-side data movement only: the
+// work runs on the GPU),
 // errors as the reference's exception types (common.hpp:22-65).
 //
 // Drop into the reference tree next to proj/include/sbdt/geometry.hpp and
 // link libsbdt_gpu.so.
 #pragma once
 
+#include <chrono>
 #include <cstdint>
 #include <new>
 #include <span>
@@ -23,11 +25,10 @@
 
 #include "sbdt/common.hpp"
 #include "sbdt/geometry.hpp"
+#include "sbdt/task_pool.hpp"
 #include "sbdt_gpu.h"
 
 namespace sbdt {
-
-class TaskPool;
 
 // SPEC.md:307-312
 struct Partitioning {
@@ -38,6 +39,63 @@ struct Partitioning {
 };
 
 namespace gpu_detail {
+
+// Wall-clock phases of the last drop-in call on this thread (diagnostics for
+// the drop-in benchmark): host preparation, the C ABI call (H2D, kernels,
+// D2H), host post-processing.
+struct PhaseTimes {
+  double prepare_ms = 0, device_ms = 0, finish_ms = 0;
+};
+inline PhaseTimes& last_phases() {
+  thread_local PhaseTimes t;
+  return t;
+}
+inline double wall_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// Thread-local grow-only page-locked staging (sbdt_gpu_host_alloc): buffers
+// written / read here cross PCIe at full rate.
+struct PinnedSlot {
+  void* p = nullptr;
+  std::size_t bytes = 0;
+  PinnedSlot() = default;
+  PinnedSlot(const PinnedSlot&) = delete;
+  PinnedSlot& operator=(const PinnedSlot&) = delete;
+  ~PinnedSlot() {
+    if (p) sbdt_gpu_host_free(p);
+  }
+  template <class T>
+  T* get(std::size_t count) {
+    const std::size_t want = sizeof(T) * (count ? count : 1);
+    if (want > bytes) {
+      if (p) sbdt_gpu_host_free(p);
+      p = nullptr;
+      bytes = 0;
+      if (sbdt_gpu_host_alloc(want, &p) != SBDT_OK) throw std::bad_alloc();
+      bytes = want;
+    }
+    return static_cast<T*>(p);
+  }
+};
+inline PinnedSlot& pinned_slot(int which) {
+  thread_local PinnedSlot slots[16];
+  return slots[which];
+}
+
+// fn(p) for p in [0, k): on the caller's TaskPool (the reference's,
+// task_pool.hpp:63-80) when it has workers, else inline. Only used for pure
+// data movement, so results never depend on it.
+template <class Fn>
+void for_each_part(TaskPool* pool, std::size_t k, Fn&& fn) {
+  if (pool && pool->concurrency() > 1 && k > 1) {
+    pool->parallel_for(k, 1, [&](std::size_t b, std::size_t e) {
+      for (std::size_t p = b; p < e; ++p) fn(p);
+    });
+  } else {
+    for (std::size_t p = 0; p < k; ++p) fn(p);
+  }
+}
 
 // One device context per host thread (the C ABI contract).
 inline sbdt_gpu_ctx* thread_context() {
@@ -79,7 +137,6 @@ inline void check(sbdt_gpu_ctx* ctx, int rc, const char* what) {
 template <int D>
 Partitioning assign_points(const PointSet& points, std::span<const PointId> sample_ids,
                            std::span<const PartitionId> sample_labels, PartitionId k, TaskPool* pool = nullptr) {
-  (void)pool;
   static_assert(D == 2 || D == 3, "D must be 2 or 3");
   if (points.dim() != D) throw std::invalid_argument("assign_points: PointSet dimension mismatch");
   if (sample_ids.size() != sample_labels.size() || sample_ids.empty())
@@ -87,20 +144,28 @@ Partitioning assign_points(const PointSet& points, std::span<const PointId> samp
   for (PartitionId l : sample_labels)
     if (l >= k) throw std::invalid_argument("assign_points: sample label >= k");
   const std::uint64_t n = points.size();
+  gpu_detail::PhaseTimes& ph = gpu_detail::last_phases();
+  const double t0 = gpu_detail::wall_ms();
   Partitioning out;
   out.labels.resize(n);
   out.sample_point_ids.assign(sample_ids.begin(), sample_ids.end());
   out.sample_labels.assign(sample_labels.begin(), sample_labels.end());
-  std::vector<std::uint64_t> offsets(k + 1);
-  std::vector<std::uint32_t> ids(n);
+  // parts come back as CSR in page-locked staging (no zero-fill, full-rate D2H)
+  std::uint64_t* offsets = gpu_detail::pinned_slot(0).get<std::uint64_t>(k + 1);
+  std::uint32_t* ids = gpu_detail::pinned_slot(1).get<std::uint32_t>(n);
   sbdt_gpu_ctx* ctx = gpu_detail::thread_context();
+  const double t1 = gpu_detail::wall_ms();
   gpu_detail::check(ctx,
                     sbdt_gpu_assign_points(ctx, D, points.raw().data(), n, sample_ids.data(), sample_labels.data(),
                                            static_cast<std::uint32_t>(sample_ids.size()), k, out.labels.data(),
-                                           offsets.data(), ids.data(), nullptr),
+                                           offsets, ids, nullptr),
                     "assign_points");
+  const double t2 = gpu_detail::wall_ms();
   out.parts.resize(k);
-  for (PartitionId p = 0; p < k; ++p) out.parts[p].assign(ids.begin() + offsets[p], ids.begin() + offsets[p + 1]);
+  gpu_detail::for_each_part(pool, k, [&](std::size_t p) {
+    out.parts[p].assign(ids + offsets[p], ids + offsets[p + 1]);
+  });
+  ph.prepare_ms = t1 - t0, ph.device_ms = t2 - t1, ph.finish_ms = gpu_detail::wall_ms() - t2;
   return out;
 }
 

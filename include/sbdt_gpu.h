@@ -158,13 +158,22 @@ int sbdt_gpu_assign_points_dev(sbdt_gpu_ctx* ctx, int dim, const double* d_coord
  *   bfs_vertex_ids_out / n_bfs_vertices_out (optional): same for border_out;
  *   spheres_out      (optional) (dim+1) doubles per row: inflated centre, r^2
  *                    (zeros for infinite rows). */
+/* Recursion levels of delaunay_dc: the GridIndex of a
+ * level's partitions keeps the cell edge of the TOP level,
+ * c_G (vol(global bbox) / n_total)^(1/D) with origin global bbox lo
+ * (build_grid_index post). grid_bbox (2*dim doubles lo[], hi[],
+ * or NULL: the bbox of the n coords) and grid_n_total (0: n) give those
+ * values; points of `coords` outside the level carry the label
+ * SBDT_UNINDEXED (they occupy no cell and are nobody's points). */
+#define SBDT_UNINDEXED 0xFFFFFFFFu
+
 int sbdt_gpu_find_border(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint64_t n,
                          const uint32_t* labels, uint32_t k, const uint64_t* offsets,
                          const uint32_t* verts, const uint32_t* nbrs, const int8_t* parity,
                          int policy, double c_G, uint32_t flags, uint8_t* positive_out,
                          uint8_t* border_out, uint32_t* vertex_ids_out, uint64_t* n_vertices_out,
                          uint32_t* bfs_vertex_ids_out, uint64_t* n_bfs_vertices_out,
-                         double* spheres_out);
+                         double* spheres_out, const double* grid_bbox, uint64_t grid_n_total);
 
 typedef struct sbdt_border_args {
   int dim;
@@ -190,6 +199,8 @@ typedef struct sbdt_border_args {
   uint32_t* d_bfs_vertex_ids;     /* n, optional */
   uint64_t* d_bfs_vertex_count;   /* 1, optional */
   double* d_spheres;              /* S*(dim+1), optional */
+  const double* grid_bbox;        /* optional HOST array 2*dim (lo[], hi[]): the grid's global bbox (SBDT_UNINDEXED) */
+  uint64_t grid_n_total;          /* 0: n */
 } sbdt_border_args;
 
 int sbdt_gpu_find_border_dev(sbdt_gpu_ctx* ctx, const sbdt_border_args* args);

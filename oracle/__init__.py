@@ -44,7 +44,8 @@ def lib():
         L.oracle_grid_params.argtypes = [C.c_int, dp, u64, C.c_double, dp, dp, dp, C.POINTER(C.c_int64)]
         L.oracle_find_border.argtypes = [C.c_int, dp, u64, u32p, C.c_uint32, C.POINTER(C.c_uint64), u32p, u32p, i8p,
                                          C.c_int, C.c_double, C.c_int, C.c_uint32, C.c_uint32, u8p, u8p, u32p,
-                                         C.POINTER(C.c_uint64), u32p, C.POINTER(C.c_uint64), dp, dp, C.c_char_p, C.c_int]
+                                         C.POINTER(C.c_uint64), u32p, C.POINTER(C.c_uint64), dp, dp, dp, u64,
+                                         C.c_char_p, C.c_int]
         L.oracle_time_border.argtypes = [C.c_int, dp, u64, u32p, C.c_uint32, C.POINTER(C.c_uint64), u32p, u32p, i8p,
                                          C.c_int, C.c_double, C.c_int, C.c_uint32, C.c_uint32, C.c_int, dp, dp,
                                          C.POINTER(C.c_uint64)]
@@ -131,7 +132,8 @@ def grid_params(points, c_G=1.0):
     return lo, hi, float(edge[0]), dims
 
 
-def find_border(points, labels, partials, policy="grid", c_G=1.0, threads=8, parts=None, spheres=False):
+def find_border(points, labels, partials, policy="grid", c_G=1.0, threads=8, parts=None, spheres=False,
+                grid_bbox=None, grid_n_total=0):
     """Returns dict(positive, border, vertices_positive, vertices_border, times[, spheres]);
     times = (index build s, find_border s) measured inside the library."""
     pts = np.ascontiguousarray(points, np.float64)
@@ -148,12 +150,15 @@ def find_border(points, labels, partials, policy="grid", c_G=1.0, threads=8, par
     sph = np.empty((S, dim + 1), np.float64) if spheres else None
     err = C.create_string_buffer(256)
     times = np.zeros(2)
+    gbb = None if grid_bbox is None else np.ascontiguousarray(np.concatenate([np.asarray(grid_bbox[0], np.float64),
+                                                                              np.asarray(grid_bbox[1], np.float64)]))
     rc = lib().oracle_find_border(dim, _p(pts, C.c_double), len(pts), _p(lab, C.c_uint32), k,
                                   _p(partials.offsets, C.c_uint64), _p(partials.verts, C.c_uint32),
                                   _p(partials.nbrs, C.c_uint32), _p(partials.parity, C.c_int8), POLICY[policy], c_G,
                                   threads, p0, p1, _p(pos, C.c_uint8), _p(bor, C.c_uint8), _p(vpos, C.c_uint32),
                                   C.byref(npos), _p(vbfs, C.c_uint32), C.byref(nbfs),
-                                  _p(sph, C.c_double) if spheres else None, _p(times, C.c_double), err, 256)
+                                  _p(sph, C.c_double) if spheres else None, _p(times, C.c_double),
+                                  _p(gbb, C.c_double) if gbb is not None else None, int(grid_n_total), err, 256)
     if rc != 0:
         raise RuntimeError("oracle_find_border: " + err.value.decode())
     out = dict(positive=pos, border=bor, vertices_positive=vpos[:npos.value].copy(),

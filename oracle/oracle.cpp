@@ -103,7 +103,8 @@ int oracle_find_border(int dim, const double* xyz, std::uint64_t n, const std::u
                        const std::int8_t* parity, int policy, double c_G, int threads, std::uint32_t p0,
                        std::uint32_t p1, std::uint8_t* positive_out, std::uint8_t* border_out,
                        std::uint32_t* vpos_out, std::uint64_t* n_vpos, std::uint32_t* vbfs_out,
-                       std::uint64_t* n_vbfs, double* spheres_out, double* times_out, char* err, int errlen) {
+                       std::uint64_t* n_vbfs, double* spheres_out, double* times_out, const double* grid_bbox,
+                       std::uint64_t n_total, char* err, int errlen) {
   try {
     PartialsView pv{k, offsets, verts, nbrs, parity, offsets[k]};
     if (p1 == 0) p1 = k;
@@ -111,7 +112,7 @@ int oracle_find_border(int dim, const double* xyz, std::uint64_t n, const std::u
     auto go = [&](auto tag) {
       constexpr int D = decltype(tag)::value;
       const double t0 = now();
-      BorderOracle<D, OwnPrims<D>> bo(xyz, n, labels, pv, policy, c_G, threads);
+      BorderOracle<D, OwnPrims<D>> bo(xyz, n, labels, pv, policy, c_G, threads, grid_bbox, n_total);
       const double t1 = now();
       auto r = bo.run(p0, p1);
       const double t2 = now();

@@ -201,25 +201,51 @@ inline double cbrt_det(double x) {
   return std::ldexp(y, e / 3);
 }
 
-// edge = c_G * (vol(global bbox) / n_total)^(1/D)  (SPEC.md:403 / :450 convention)
+// edge = c_G * (vol(global bbox) / n_total)^(1/D)  (SPEC.md:403 / :410 / :450
+// convention), origin = global bbox lo, from a given global bbox and n_total
+// (recursion levels keep the top level's, build_grid_index post).
 template <int D>
-GridParams<D> grid_params(const double* xyz, std::size_t n, double c_G) {
+GridParams<D> grid_from_bbox(const double* lo, const double* hi, std::size_t n_total, double c_G) {
   GridParams<D> g;
-  for (int d = 0; d < D; ++d) {
-    g.lo[d] = INFINITY;
-    g.hi[d] = -INFINITY;
-  }
-  for (std::size_t i = 0; i < n; ++i)
-    for (int d = 0; d < D; ++d) {
-      g.lo[d] = std::min(g.lo[d], xyz[i * D + d]);
-      g.hi[d] = std::max(g.hi[d], xyz[i * D + d]);
-    }
+  for (int d = 0; d < D; ++d) g.lo[d] = lo[d], g.hi[d] = hi[d];
   double vol = 1.0;
   for (int d = 0; d < D; ++d) vol *= (g.hi[d] - g.lo[d]);
-  const double per = vol / static_cast<double>(n);
+  const double per = vol / static_cast<double>(n_total);
   g.edge = c_G * (D == 2 ? std::sqrt(per) : cbrt_det(per));
   for (int d = 0; d < D; ++d) g.dims[d] = static_cast<std::int64_t>(std::floor((g.hi[d] - g.lo[d]) / g.edge)) + 1;
   return g;
+}
+
+// ... from the bbox of all n points and n_total.
+template <int D>
+GridParams<D> grid_from_bbox_of(const double* xyz, std::size_t n, std::size_t n_total, double c_G) {
+  double lo[D], hi[D];
+  for (int d = 0; d < D; ++d) {
+    lo[d] = INFINITY;
+    hi[d] = -INFINITY;
+  }
+  for (std::size_t i = 0; i < n; ++i)
+    for (int d = 0; d < D; ++d) {
+      lo[d] = std::min(lo[d], xyz[i * D + d]);
+      hi[d] = std::max(hi[d], xyz[i * D + d]);
+    }
+  return grid_from_bbox<D>(lo, hi, n_total, c_G);
+}
+
+// ... from the bbox of all n points and n.
+template <int D>
+GridParams<D> grid_params(const double* xyz, std::size_t n, double c_G) {
+  double lo[D], hi[D];
+  for (int d = 0; d < D; ++d) {
+    lo[d] = INFINITY;
+    hi[d] = -INFINITY;
+  }
+  for (std::size_t i = 0; i < n; ++i)
+    for (int d = 0; d < D; ++d) {
+      lo[d] = std::min(lo[d], xyz[i * D + d]);
+      hi[d] = std::max(hi[d], xyz[i * D + d]);
+    }
+  return grid_from_bbox<D>(lo, hi, n, c_G);
 }
 
 // cell = floor((p - lo) / edge), clamped to the grid (SURVEY.md §7 grid decision).
@@ -393,12 +419,17 @@ struct BorderResult {
 template <int D, class Prims>
 class BorderOracle {
  public:
+  // grid_bbox (lo[D], hi[D]) / n_total: the top level's grid at a recursion
+  // level (nullptr / 0: the bbox and count of all n points); points labelled
+  // kInf belong to no index of this level.
   BorderOracle(const double* xyz, std::size_t n, const std::uint32_t* labels, const PartialsView& pv,
-               int policy, double c_G, unsigned threads)
+               int policy, double c_G, unsigned threads, const double* grid_bbox = nullptr, std::size_t n_total = 0)
       : xyz_(xyz), n_(n), pv_(pv), policy_(policy), threads_(threads) {
-    g_ = grid_params<D>(xyz, n, c_G);
+    g_ = grid_bbox ? grid_from_bbox<D>(grid_bbox, grid_bbox + D, n_total ? n_total : n, c_G)
+                   : (n_total ? grid_from_bbox_of<D>(xyz, n, n_total, c_G) : grid_params<D>(xyz, n, c_G));
     std::vector<std::vector<std::uint32_t>> parts(pv.k);
-    for (std::size_t i = 0; i < n; ++i) parts[labels[i]].push_back(static_cast<std::uint32_t>(i));
+    for (std::size_t i = 0; i < n; ++i)
+      if (labels[i] != kInf) parts[labels[i]].push_back(static_cast<std::uint32_t>(i));
     idx_.resize(pv.k);
     parallel_for(pv.k, 1, threads, [&](std::size_t b, std::size_t e) {
       for (std::size_t p = b; p < e; ++p) idx_[p] = build_grid_index<D>(g_, xyz, parts[p].data(), parts[p].size());

@@ -68,6 +68,19 @@ __global__ void k_bbox_points(const double* __restrict__ xyz, std::uint64_t n, u
   }
 }
 
+// The grid's bbox given by the caller (recursion levels), as ordered keys.
+struct GridBox {
+  double lo[3], hi[3];
+};
+template <int D>
+__global__ void k_set_bbox(GridBox gb, unsigned long long* bbox) {
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    bbox[d] = dbl_to_ordered(gb.lo[d]);
+    bbox[D + d] = dbl_to_ordered(gb.hi[d]);
+  }
+}
+
 __global__ void k_pbbox_init(unsigned long long* pbbox, std::uint32_t count, int dim) {
   for (std::uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < count; j += gridDim.x * blockDim.x)
     pbbox[j] = ((j % (2 * dim)) < static_cast<std::uint32_t>(dim)) ? 0xFFFFFFFFFFFFFFFFULL : 0ULL;
@@ -1590,13 +1603,14 @@ __global__ void k_compact_write(const std::uint8_t* __restrict__ flags, std::uin
 
 // ---- exact policy: per-cell point lists and the escalation pass --------------
 template <int D>
-__global__ void k_cell_count(const double* __restrict__ xyz, std::uint64_t n, const OwnerGrid<D>* __restrict__ ogp,
-                             std::uint32_t* __restrict__ cnt) {
+__global__ void k_cell_count(const double* __restrict__ xyz, const std::uint32_t* __restrict__ labels, std::uint64_t n,
+                             const OwnerGrid<D>* __restrict__ ogp, std::uint32_t* __restrict__ cnt) {
   __shared__ OwnerGrid<D> og;
   if (threadIdx.x == 0) og = *ogp;
   __syncthreads();
   for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += std::uint64_t(gridDim.x) * blockDim.x) {
+    if (labels[i] == SBDT_UNINDEXED) continue;
     int c[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) c[d] = static_cast<int>(cell_coord_fast<D>(og.g, og.inv_edge, xyz[i * D + d], d));
@@ -1614,6 +1628,7 @@ __global__ void k_cell_scatter(const double* __restrict__ xyz, const std::uint32
   __syncthreads();
   for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += std::uint64_t(gridDim.x) * blockDim.x) {
+    if (labels[i] == SBDT_UNINDEXED) continue;
     CellPt<D> q;
     int c[D];
 #pragma unroll
@@ -1713,7 +1728,7 @@ __global__ void k_part_present(const std::uint32_t* __restrict__ labels, std::ui
   for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += std::uint64_t(gridDim.x) * blockDim.x) {
     const std::uint32_t l = labels[i];
-    if (!present[l]) present[l] = 1;
+    if (l != SBDT_UNINDEXED && !present[l]) present[l] = 1;
   }
 }
 
@@ -1754,7 +1769,10 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   const double cg = in->c_G > 0 ? in->c_G : 1.0;
   double scale = 1.0;
   for (int d = 0; d < D; ++d) scale /= cg;
-  const unsigned long long cap = static_cast<unsigned long long>(4.0 * double(in->n) * scale) + 4096;
+  // recursion levels: the top level's grid (global bbox, n_total), SBDT_UNINDEXED points skipped
+  const std::uint64_t n_grid = in->grid_n_total ? in->grid_n_total : in->n;
+  const unsigned long long cap =
+      static_cast<unsigned long long>(4.0 * double(n_grid > in->n ? n_grid : in->n) * scale) + 4096;
   const unsigned long long owner_len = 2 * cap + 64 * kMaxLevels + 4096;
   SBDT_WS(og, OwnerGrid<D>, "border.og", 1);
   SBDT_WS(owner, std::uint16_t, "border.owner", owner_len);
@@ -1779,7 +1797,13 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   }
   StageTimer tgrid(ctx, "border.grid");
   const unsigned long long* bb = reinterpret_cast<const unsigned long long*>(in->d_bbox_ordered);
-  if (!bb) {
+  if (in->grid_bbox) {
+    GridBox gb{};
+    for (int d = 0; d < D; ++d) gb.lo[d] = in->grid_bbox[d], gb.hi[d] = in->grid_bbox[D + d];
+    k_set_bbox<D><<<1, 1, 0, st>>>(gb, bbox);
+    ++ctx->launches;
+    bb = bbox;
+  } else if (!bb) {
     k_bbox_points_init<<<1, 32, 0, st>>>(bbox, D);
     const std::uint64_t want = (in->n + 255) / 256;
     const unsigned blocks = static_cast<unsigned>(want < std::uint64_t(sms) * 8 ? want : std::uint64_t(sms) * 8);
@@ -1787,7 +1811,7 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
     ctx->launches += 2;
     bb = bbox;
   }
-  k_owner_params<D><<<1, 1, 0, st>>>(bb, in->n, cg, cap, owner_len, og, ctx->d_status);
+  k_owner_params<D><<<1, 1, 0, st>>>(bb, n_grid, cg, cap, owner_len, og, ctx->d_status);
   k_owner_clear<D><<<sms * 8, 256, 0, st>>>(og, owner);
   ++ctx->launches;
   if (pbbox) {
@@ -1820,7 +1844,7 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
     SBDT_CUDA_TRY(cudaMemsetAsync(ccnt, 0, sizeof(std::uint32_t) * (owner_len + 1), st));
     const std::uint64_t want = (in->n + 255) / 256;
     const unsigned blocks = static_cast<unsigned>(want < std::uint64_t(sms) * 16 ? want : std::uint64_t(sms) * 16);
-    k_cell_count<D><<<blocks > 0 ? blocks : 1, 256, 0, st>>>(in->d_xyz, in->n, og, ccnt);
+    k_cell_count<D><<<blocks > 0 ? blocks : 1, 256, 0, st>>>(in->d_xyz, in->d_labels, in->n, og, ccnt);
     exclusive_scan(ccnt, cstart, owner_len + 1, cbs, nullptr, st, &ctx->launches);
     SBDT_CUDA_TRY(cudaMemsetAsync(ccnt, 0, sizeof(std::uint32_t) * (owner_len + 1), st));
     k_cell_scatter<D><<<blocks > 0 ? blocks : 1, 256, 0, st>>>(in->d_xyz, in->d_labels, in->n, og, cstart, ccnt, cpts);

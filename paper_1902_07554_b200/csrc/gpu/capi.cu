@@ -363,7 +363,8 @@ int sbdt_gpu_find_border(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint6
                          uint32_t k, const uint64_t* offsets, const uint32_t* verts, const uint32_t* nbrs,
                          const int8_t* parity, int policy, double c_G, uint32_t flags, uint8_t* positive_out,
                          uint8_t* border_out, uint32_t* vertex_ids_out, uint64_t* n_vertices_out,
-                         uint32_t* bfs_vertex_ids_out, uint64_t* n_bfs_vertices_out, double* spheres_out) {
+                         uint32_t* bfs_vertex_ids_out, uint64_t* n_bfs_vertices_out, double* spheres_out,
+                         const double* grid_bbox, uint64_t grid_n_total) {
   if (!ctx || !coords || !labels || !offsets || !verts || !nbrs || (!parity && policy == SBDT_POLICY_EXACT) ||
       !positive_out || !vertex_ids_out || !n_vertices_out)
     return SBDT_ERR_INVALID;
@@ -378,6 +379,8 @@ int sbdt_gpu_find_border(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint6
   a.policy = policy;
   a.c_G = c_G;
   a.flags = flags;
+  a.grid_bbox = grid_bbox;
+  a.grid_n_total = grid_n_total;
   double* d_xyz;
   uint32_t *d_lab, *d_verts, *d_nbrs, *d_vids, *d_bvids = nullptr;
   uint64_t *d_off, *d_cnt, *d_bcnt = nullptr;

@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include "common.cuh"
+#include "sbdt_gpu.h"
 
 namespace sbdt_gpu {
 
@@ -167,6 +168,8 @@ __global__ void k_owner_mark(const double* __restrict__ xyz, const std::uint32_t
   const double inv_qh = 1.0 / og.qh;
   for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += std::uint64_t(gridDim.x) * blockDim.x) {
+    const std::uint32_t lab = labels[i];
+    if (lab == SBDT_UNINDEXED) continue;  // not in this level's indices (never a simplex vertex)
     double x[D];
     int c[D];
 #pragma unroll
@@ -192,7 +195,6 @@ __global__ void k_owner_mark(const double* __restrict__ xyz, const std::uint32_t
         xq[i] = static_cast<std::uint64_t>(__float_as_uint(fx)) | (static_cast<std::uint64_t>(__float_as_uint(fy)) << 32);
       }
     }
-    const std::uint32_t lab = labels[i];
     std::uint16_t* slot = owner + og_index<D>(og, 0, c);
     unsigned short old = *slot;
     while (old != lab && old != kOwnerMulti) {
@@ -421,6 +423,7 @@ __global__ void k_pbbox_global(const double* __restrict__ xyz, const std::uint32
   for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += std::uint64_t(gridDim.x) * blockDim.x) {
     const std::uint32_t lab = labels[i];
+    if (lab == SBDT_UNINDEXED) continue;
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       const unsigned long long o = dbl_to_ordered(xyz[i * D + d]);

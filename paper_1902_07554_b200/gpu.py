@@ -22,6 +22,7 @@ _lib = None
 
 SBDT_OK, SBDT_ERR_INVALID, SBDT_ERR_DEGENERATE, SBDT_ERR_CUDA, SBDT_ERR_OOM, SBDT_ERR_RANGE, SBDT_ERR_MERGE = range(7)
 MERGE_HULL = 1
+UNINDEXED = 0xFFFFFFFF  # label of a point outside this recursion level's indices (SBDT_UNINDEXED)
 POLICY = {"bbox": 0, "grid": 1, "exact": 2}
 RESIDENT_POINTS = 2
 HULL_BFS = 1
@@ -47,7 +48,7 @@ class BorderArgs(C.Structure):
         ("d_bbox_ordered", C.c_void_p), ("d_positive", C.c_void_p), ("d_border", C.c_void_p),
         ("d_vertex_flags", C.c_void_p), ("d_vertex_ids", C.c_void_p), ("d_vertex_count", C.c_void_p),
         ("d_bfs_vertex_flags", C.c_void_p), ("d_bfs_vertex_ids", C.c_void_p), ("d_bfs_vertex_count", C.c_void_p),
-        ("d_spheres", C.c_void_p),
+        ("d_spheres", C.c_void_p), ("grid_bbox", C.POINTER(C.c_double)), ("grid_n_total", C.c_uint64),
     ]
 
 
@@ -100,7 +101,7 @@ def lib():
         L.sbdt_gpu_assign_points.argtypes = [vp, C.c_int, dp, u64, u32p, u32p, u32, u32, u32p, u64p, u32p, dp]
         L.sbdt_gpu_assign_points_dev.argtypes = [vp, C.c_int, vp, u64, vp, vp, u32, u32, vp, vp, vp, vp]
         L.sbdt_gpu_find_border.argtypes = [vp, C.c_int, dp, u64, u32p, u32, u64p, u32p, u32p, i8p, C.c_int, C.c_double,
-                                           u32, u8p, u8p, u32p, u64p, u32p, u64p, dp]
+                                           u32, u8p, u8p, u32p, u64p, u32p, u64p, dp, dp, u64]
         L.sbdt_gpu_find_border_dev.argtypes = [vp, C.POINTER(BorderArgs)]
         L.sbdt_gpu_merge.argtypes = [vp, C.c_int, u32p, u64, u32, u64p, u32p, u32p, i8p, u8p, u32p, u32p, i8p, u64,
                                      u32, u64, u32p, u32p, i8p, u64p, u64p]
@@ -342,14 +343,18 @@ class BorderSet:
 
 def find_border(points: np.ndarray, labels: np.ndarray, partials, policy: IntersectionPolicy | None = None,
                 hull_bfs: bool = True, spheres: bool = False, ctx: Context | None = None,
-                out: BorderSet | None = None, resident: bool = False) -> BorderSet:
+                out: BorderSet | None = None, resident: bool = False, grid_bbox=None,
+                grid_n_total: int = 0) -> BorderSet:
     """find_border through the host-buffer C ABI entry point.
     `out` (optional): a BorderSet whose positive / border arrays (length S) and
     border_vertex_ids / positive_vertex_ids arrays (length n) are reused as
     output buffers; the result then holds views into them. resident=True:
     `points` and `labels` are the arrays of the last assign_points call on
     `ctx` (labels = its Partitioning.labels), unchanged: their device copies
-    are reused instead of uploaded (SBDT_BORDER_RESIDENT_POINTS)."""
+    are reused instead of uploaded (SBDT_BORDER_RESIDENT_POINTS).
+    Recursion levels: grid_bbox (lo, hi) and grid_n_total
+    give the top level's grid (GridIndex global bbox / n_total); points
+    outside the level carry the label UNINDEXED."""
     ctx = ctx or default_context()
     policy = policy or IntersectionPolicy()
     pts = np.ascontiguousarray(points, np.float64)
@@ -362,6 +367,8 @@ def find_border(points: np.ndarray, labels: np.ndarray, partials, policy: Inters
     bvids = _out(out.border_vertex_ids if out else None, n, np.uint32) if hull_bfs else None
     nv, nb = C.c_uint64(0), C.c_uint64(0)
     sph = np.empty((S, dim + 1), np.float64) if spheres else None
+    gbb = None if grid_bbox is None else np.ascontiguousarray(np.concatenate([np.asarray(grid_bbox[0], np.float64),
+                                                                              np.asarray(grid_bbox[1], np.float64)]))
     rc = lib().sbdt_gpu_find_border(
         ctx.handle, dim, _p(pts, C.c_double), n, _p(lab, C.c_uint32), k, _p(partials.offsets, C.c_uint64),
         _p(partials.verts, C.c_uint32), _p(partials.nbrs, C.c_uint32), _p(partials.parity, C.c_int8),
@@ -369,7 +376,8 @@ def find_border(points: np.ndarray, labels: np.ndarray, partials, policy: Inters
         _p(pos, C.c_uint8),
         _p(bor, C.c_uint8) if hull_bfs else None, _p(vids, C.c_uint32), C.byref(nv),
         _p(bvids, C.c_uint32) if hull_bfs else None, C.byref(nb) if hull_bfs else None,
-        _p(sph, C.c_double) if spheres else None)
+        _p(sph, C.c_double) if spheres else None,
+        _p(gbb, C.c_double) if gbb is not None else None, int(grid_n_total))
     ctx.check(rc, "find_border")
     if out is not None:  # views into the caller's buffers
         return BorderSet(pos, bor, bvids[:nb.value] if hull_bfs else vids[:nv.value], vids[:nv.value], sph)

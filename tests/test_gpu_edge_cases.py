@@ -261,3 +261,25 @@ def test_sample_label_out_of_range(ctx):
     slab[7] = 3
     part = gpu.assign_points(pts, sid, slab, 4, ctx=ctx)
     assert np.array_equal(part.labels, oracle.assign_brute(pts, sid, slab))
+
+
+@pytest.mark.parametrize("policy", ["grid", "exact", "bbox"])
+def test_recursion_level_grid(policy, ctx):
+    """find_border at a recursion level: the level's points
+    are a subset (the others labelled UNINDEXED: no cell, no foreign point)
+    and the grid is the top level's (global bbox + n_total)."""
+    inst = host.make_instance(2, n=60_000, k=8)
+    lab = oracle.assign_brute(inst.points, inst.sample_ids, inst.sample_labels)
+    P = host.attach_partials(inst, lab)
+    L = 5
+    SL = int(P.offsets[L])
+    lvl_lab = np.where(lab < L, lab, np.uint32(gpu.UNINDEXED)).astype(np.uint32)
+    lvl = host.Partials(P.offsets[:L + 1].copy(), np.ascontiguousarray(P.verts[:, :SL]),
+                        np.ascontiguousarray(P.nbrs[:, :SL]), P.parity[:SL].copy())
+    lo, hi = inst.points.min(axis=0), inst.points.max(axis=0)
+    g = gpu.find_border(inst.points, lvl_lab, lvl, gpu.IntersectionPolicy(policy, 1.0), hull_bfs=True, ctx=ctx,
+                        grid_bbox=(lo, hi), grid_n_total=inst.n)
+    o = oracle.find_border(inst.points, lvl_lab, lvl, policy, grid_bbox=(lo, hi), grid_n_total=inst.n)
+    assert np.array_equal(g.positive, o["positive"]) and np.array_equal(g.border, o["border"])
+    assert np.array_equal(g.positive_vertex_ids, o["vertices_positive"])
+    assert np.array_equal(g.border_vertex_ids, o["vertices_border"])
