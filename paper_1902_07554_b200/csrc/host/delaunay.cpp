@@ -39,6 +39,13 @@ inline std::uint64_t spread2(std::uint64_t x) {
   return x;
 }
 
+// Incremental Bowyer-Watson over a slot array of cells. The result is
+// determined only by the conflict rules (restated from the reference's
+// contract, see delaunay.hpp); the search structure below — bootstrap by
+// exact affine-independence tests, a deterministic visibility walk with a
+// linear-scan fallback, a depth-first cavity search with per-cell marks, and
+// the new cells' mutual links through a small open-addressing ridge table —
+// is this repo's own.
 template <int D>
 class Builder {
  public:
@@ -47,8 +54,10 @@ class Builder {
   TriSoA run(const std::uint32_t* ids, std::size_t n) {
     if (n < D + 1) throw DegenerateInputError("need at least " + std::to_string(D + 1) + " points");
     brio_order(ids, n);
-    bootstrap();
-    for (std::size_t i = D + 1; i < order_.size(); ++i) insert(order_[i]);
+    std::vector<char> used(order_.size(), 0);
+    first_simplex(used);
+    for (std::size_t i = 0; i < order_.size(); ++i)
+      if (!used[i]) insert(order_[i]);
     return compact();
   }
 
@@ -114,29 +123,19 @@ class Builder {
     for (std::size_t i = 0; i < n; ++i) order_[i] = keyed[i].second;
   }
 
-  static bool collinear3(const double* a, const double* b, const double* c) {
-    const double ux = b[0] - a[0], uy = b[1] - a[1], uz = b[2] - a[2];
-    const double vx = c[0] - a[0], vy = c[1] - a[1], vz = c[2] - a[2];
-    return (uy * vz - uz * vy) == 0.0 && (uz * vx - ux * vz) == 0.0 && (ux * vy - uy * vx) == 0.0;
-  }
-
-  static bool same_point(const double* a, const double* b) {
-    for (int d = 0; d < D; ++d)
-      if (a[d] != b[d]) return false;
-    return true;
-  }
-
-  std::uint32_t create(const Cell<D>& c) {
-    if (!free_.empty()) {
-      const std::uint32_t id = free_.back();
+  std::uint32_t new_cell(const Cell<D>& c) {
+    std::uint32_t id;
+    if (free_.empty()) {
+      id = static_cast<std::uint32_t>(cells_.size());
+      cells_.push_back(c);
+      mark_.push_back(0);
+    } else {
+      id = free_.back();
       free_.pop_back();
       cells_[id] = c;
-      cells_[id].alive = 1;
-      return id;
     }
-    cells_.push_back(c);
-    cells_.back().alive = 1;
-    return static_cast<std::uint32_t>(cells_.size() - 1);
+    cells_[id].alive = 1;
+    return id;
   }
 
   int parity_of(const std::uint32_t* v) const {
@@ -145,268 +144,233 @@ class Builder {
     return orient(p);
   }
 
-  void bootstrap() {
-    std::vector<std::size_t> pick{0};
-    for (std::size_t i = 1; i < order_.size() && pick.size() <= D; ++i) {
-      bool independent = false;
-      if (pick.size() == 1) {
-        independent = !same_point(P(order_[pick[0]]), P(order_[i]));
-      } else if (pick.size() == 2) {
-        if constexpr (D == 2)
-          independent = sbdt_pred::orient2(P(order_[pick[0]]), P(order_[pick[1]]), P(order_[i])) != 0;
-        else
-          independent = !collinear3(P(order_[pick[0]]), P(order_[pick[1]]), P(order_[i]));
+  // Rank of the affine hull of {q} and the already chosen points (exact).
+  bool extends_hull(const std::vector<std::uint32_t>& chosen, std::uint32_t q) const {
+    const double* c = P(q);
+    if (chosen.size() == 1) {
+      const double* a = P(chosen[0]);
+      for (int d = 0; d < D; ++d)
+        if (a[d] != c[d]) return true;
+      return false;
+    }
+    const double* a = P(chosen[0]);
+    const double* b = P(chosen[1]);
+    if (chosen.size() == 2) {
+      if constexpr (D == 2) {
+        return sbdt_pred::orient2(a, b, c) != 0;
       } else {
-        if constexpr (D == 3)
-          independent = sbdt_pred::orient3(P(order_[pick[0]]), P(order_[pick[1]]),
-                                           P(order_[pick[2]]), P(order_[i])) != 0;
+        // collinear in 3-D iff all three coordinate-plane projections are
+        for (int u = 0; u < 3; ++u) {
+          const int v = (u + 1) % 3;
+          const double pa[2] = {a[u], a[v]}, pb[2] = {b[u], b[v]}, pc[2] = {c[u], c[v]};
+          if (sbdt_pred::orient2(pa, pb, pc) != 0) return true;
+        }
+        return false;
       }
-      if (independent) pick.push_back(i);
     }
-    if (pick.size() < D + 1) throw DegenerateInputError("all points affinely dependent");
-    std::vector<std::uint32_t> reordered;
-    reordered.reserve(order_.size());
-    for (std::size_t j = 0; j <= D; ++j) reordered.push_back(order_[pick[j]]);
-    std::size_t next_pick = 0;
-    for (std::size_t r = 0; r < order_.size(); ++r) {
-      if (next_pick < pick.size() && pick[next_pick] == r) {
-        ++next_pick;
-        continue;
-      }
-      reordered.push_back(order_[r]);
-    }
-    order_ = std::move(reordered);
+    if constexpr (D == 3) return sbdt_pred::orient3(a, b, P(chosen[2]), c) != 0;
+    return false;
+  }
 
-    Cell<D> s0;
-    for (int i = 0; i <= D; ++i) s0.v[i] = order_[i];
-    std::sort(s0.v, s0.v + D + 1);
-    s0.parity = static_cast<std::int8_t>(parity_of(s0.v));
-    for (int i = 0; i <= D; ++i) s0.n[i] = kNone;
-    const std::uint32_t fid = create(s0);
-    std::uint32_t inf_ids[D + 1];
+  // The first D+1 affinely independent points of the insertion order form
+  // the first cell, closed by one infinite cell per facet.
+  void first_simplex(std::vector<char>& used) {
+    std::vector<std::uint32_t> chosen;
+    for (std::size_t i = 0; i < order_.size() && chosen.size() <= D; ++i) {
+      if (chosen.empty() || extends_hull(chosen, order_[i])) {
+        chosen.push_back(order_[i]);
+        used[i] = 1;
+      }
+    }
+    if (chosen.size() < D + 1) throw DegenerateInputError("all points affinely dependent");
+    std::sort(chosen.begin(), chosen.end());
+    Cell<D> f;
+    for (int i = 0; i <= D; ++i) f.v[i] = chosen[i], f.n[i] = kNone;
+    f.parity = static_cast<std::int8_t>(parity_of(f.v));
+    const std::uint32_t fid = new_cell(f);
+    // the hull star: cell opposite vertex d = facet d + infinity, linked to
+    // the finite cell through slot D and to each other through their ridges
+    std::vector<std::uint32_t> made;
     for (int d = 0; d <= D; ++d) {
-      Cell<D> inf;
-      int idx = 0;
+      Cell<D> h;
+      int w = 0;
       for (int i = 0; i <= D; ++i)
-        if (i != d) inf.v[idx++] = cells_[fid].v[i];
-      inf.v[D] = kInf;
-      inf.parity = 0;
-      for (int i = 0; i <= D; ++i) inf.n[i] = kNone;
-      inf.n[D] = fid;
-      inf_ids[d] = create(inf);
-      cells_[fid].n[d] = inf_ids[d];
+        if (i != d) h.v[w++] = chosen[i];
+      h.v[D] = kInf;
+      h.parity = 0;
+      for (int i = 0; i <= D; ++i) h.n[i] = kNone;
+      h.n[D] = fid;
+      const std::uint32_t hid = new_cell(h);
+      cells_[fid].n[d] = hid;
+      made.push_back(hid);
     }
-    for (int d = 0; d <= D; ++d) {
-      Cell<D>& inf = cells_[inf_ids[d]];
-      for (int j = 0; j < D; ++j)
-        for (int i = 0; i <= D; ++i)
-          if (cells_[fid].v[i] == inf.v[j]) {
-            inf.n[j] = inf_ids[i];
-            break;
-          }
-    }
+    link_by_ridges(made, kInf);
     hint_ = fid;
   }
 
-  bool infinite_conflict(const Cell<D>& s, const double* q, std::uint32_t qid) const {
-    const Cell<D>& owner = cells_[s.n[D]];
-    const double* pts[D + 1];
-    for (int i = 0; i < D; ++i) pts[i] = P(s.v[i]);
-    std::uint32_t inner = kInf;
-    for (int i = 0; i <= D; ++i) {
-      const std::uint32_t v = owner.v[i];
-      bool on_facet = false;
-      for (int f = 0; f < D; ++f) on_facet |= (s.v[f] == v);
-      if (!on_facet) {
-        inner = v;
-        break;
-      }
+  // conflict of q with an infinite cell: q strictly on the outer side of its
+  // hull facet, or on the facet's plane with a facet vertex of lower id
+  bool hull_conflict(const Cell<D>& s, const double* q, std::uint32_t qid) const {
+    const Cell<D>& inside = cells_[s.n[D]];
+    std::uint32_t apex = kInf;  // the inside cell's vertex off the facet
+    for (int i = 0; i <= D && apex == kInf; ++i) {
+      const std::uint32_t v = inside.v[i];
+      if (std::find(s.v, s.v + D, v) == s.v + D) apex = v;
     }
-    pts[D] = P(inner);
-    const int inner_sign = orient(pts);
-    pts[D] = q;
-    const int q_sign = orient(pts);
-    if (q_sign == 0) {
-      for (int f = 0; f < D; ++f)
-        if (s.v[f] < qid) return true;
-      return false;
-    }
-    return q_sign == -inner_sign;
+    const double* f[D + 1];
+    for (int i = 0; i < D; ++i) f[i] = P(s.v[i]);
+    f[D] = q;
+    const int side_q = orient(f);
+    if (side_q == 0) return *std::min_element(s.v, s.v + D) < qid;
+    f[D] = P(apex);
+    return side_q == -orient(f);
   }
 
-  bool conflict(std::uint32_t id, const double* q, std::uint32_t qid) const {
+  // conflict of q with a cell (in_sphere, tie toward "lowest id is outside")
+  bool in_conflict(std::uint32_t id, const double* q, std::uint32_t qid) const {
     const Cell<D>& s = cells_[id];
-    if (s.v[D] == kInf) return infinite_conflict(s, q, qid);
+    if (s.v[D] == kInf) return hull_conflict(s, q, qid);
     const double* p[D + 1];
     for (int i = 0; i <= D; ++i) p[i] = P(s.v[i]);
     if (s.parity < 0) std::swap(p[0], p[1]);
     const int r = in_sphere(p, q);
     if (r != 0) return r > 0;
-    for (int i = 0; i <= D; ++i)
-      if (s.v[i] < qid) return true;
-    return false;
+    return *std::min_element(s.v, s.v + D + 1) < qid;
   }
 
-  std::uint32_t random_alive() {
-    for (int t = 0; t < 64; ++t) {
-      const std::uint32_t id = static_cast<std::uint32_t>(uniform_index(rng_, cells_.size()));
-      if (cells_[id].alive) return id;
-    }
-    for (std::uint32_t id = 0; id < cells_.size(); ++id)
-      if (cells_[id].alive) return id;
-    return kNone;
-  }
-
-  std::uint32_t locate(const double* q, std::uint32_t qid) {
-    std::uint32_t cur = (hint_ < cells_.size() && cells_[hint_].alive) ? hint_ : random_alive();
-    std::uint32_t prev = kNone;
-    std::size_t steps = 0;
-    const std::size_t budget = 4 * (cells_.size() - free_.size()) + 16;
-    for (;;) {
-      if (steps++ > budget) {
-        cur = random_alive();
-        prev = kNone;
-        steps = 0;
-      }
+  // Visibility walk from the hint: leave through the first facet (in slot
+  // order, not back through the facet just crossed) that separates q from
+  // the cell's apex; a cell with no such facet contains q. A hull cell ends
+  // the walk when q conflicts with it. The walk terminates in a Delaunay
+  // triangulation; the step budget only guards the degenerate ties, after
+  // which every live cell is scanned for a conflict.
+  std::uint32_t locate(const double* q, std::uint32_t qid) const {
+    std::uint32_t cur = hint_, came = kNone;
+    const std::size_t budget = 8 * cells_.size() + 64;
+    for (std::size_t step = 0; step < budget; ++step) {
       const Cell<D>& s = cells_[cur];
       if (s.v[D] == kInf) {
-        if (infinite_conflict(s, q, qid)) return cur;
-        prev = cur;
+        if (hull_conflict(s, q, qid)) return cur;
+        came = cur;
         cur = s.n[D];
         continue;
       }
       const double* c[D + 1];
       for (int i = 0; i <= D; ++i) c[i] = P(s.v[i]);
-      const unsigned rot = static_cast<unsigned>(rng_() % (D + 1));
-      int exit_facet = -1;
-      for (int k = 0; k <= D; ++k) {
-        const int d = static_cast<int>((k + rot) % (D + 1));
-        if (prev != kNone && s.n[d] == prev) continue;
-        const double* saved = c[d];
+      int leave = -1;
+      for (int d = 0; d <= D && leave < 0; ++d) {
+        if (s.n[d] == came) continue;
+        const double* keep = c[d];
         c[d] = q;
         const int o = orient(c);
-        c[d] = saved;
-        if (o != 0 && o != s.parity) {
-          exit_facet = d;
-          break;
+        c[d] = keep;
+        if (o != 0 && o != s.parity) leave = d;
+      }
+      if (leave < 0) return cur;
+      came = cur;
+      cur = s.n[leave];
+    }
+    for (std::uint32_t id = 0; id < cells_.size(); ++id)
+      if (cells_[id].alive && in_conflict(id, q, qid)) return id;
+    throw DegenerateInputError("point location failed");
+  }
+
+  // Pairs the facets through q of the cells in `made`: every ridge (a facet
+  // minus `pivot`) is shared by exactly two of them.
+  void link_by_ridges(const std::vector<std::uint32_t>& made, std::uint32_t pivot) {
+    std::size_t cap = 16;
+    while (cap < 4 * made.size() * D) cap <<= 1;
+    table_.assign(cap, Slot{~0ull, kNone, 0});
+    for (std::uint32_t cid : made) {
+      const Cell<D>& c = cells_[cid];
+      for (int d = 0; d <= D; ++d) {
+        if (c.v[d] == pivot) continue;
+        std::uint64_t key = 0;  // the D-1 ridge ids, ascending (the cell's order minus v[d], pivot)
+        for (int i = 0; i <= D; ++i)
+          if (i != d && c.v[i] != pivot) key = key * 0x100000000ull + c.v[i];
+        std::size_t h = (key * 0x9E3779B97F4A7C15ull) >> 7 & (cap - 1);
+        for (;; h = (h + 1) & (cap - 1)) {
+          Slot& sl = table_[h];
+          if (sl.cell == kNone) {
+            sl = Slot{key, cid, d};
+            break;
+          }
+          if (sl.key == key) {
+            cells_[cid].n[d] = sl.cell;
+            cells_[sl.cell].n[sl.slot] = cid;
+            sl.key = ~0ull - 1;  // consumed: a third owner would be a defect
+            break;
+          }
         }
       }
-      if (exit_facet < 0) return cur;
-      prev = cur;
-      cur = s.n[exit_facet];
     }
   }
 
-  struct Boundary {
-    std::uint32_t outside;
-    int outside_slot;  // index in outside.n pointing back into the cavity
-    std::uint32_t verts[D];
-  };
-  struct Ridge {
-    std::uint64_t key;
-    std::uint32_t simplex;
-    int slot;
-    bool operator<(const Ridge& o) const {
-      return key < o.key || (key == o.key && simplex < o.simplex);
-    }
-  };
-
   void insert(std::uint32_t qid) {
     const double* q = P(qid);
-    const std::uint32_t seed = locate(q, qid);
-    if (stamp_.size() < cells_.size()) stamp_.resize(cells_.size() + cells_.size() / 2 + 16, 0);
-    epoch_ += 2;
-    if (epoch_ == 0 || epoch_ == 1) {
-      std::fill(stamp_.begin(), stamp_.end(), 0);
-      epoch_ = 2;
-    }
-    cavity_.clear();
-    boundary_.clear();
-    bfs_.clear();
-    bfs_.push_back(seed);
-    stamp_[seed] = epoch_ | 1;
-    while (!bfs_.empty()) {
-      const std::uint32_t id = bfs_.back();
-      bfs_.pop_back();
-      cavity_.push_back(id);
-      const Cell<D>& s = cells_[id];
+    const std::uint32_t start = locate(q, qid);
+    // depth-first cavity search; mark_: 1 = in the cavity, 2 = checked outside
+    std::vector<std::uint32_t>& stack = stack_;
+    stack.assign(1, start);
+    mark_[start] = 1;
+    touched_.assign(1, start);
+    shell_.clear();
+    while (!stack.empty()) {
+      const std::uint32_t id = stack.back();
+      stack.pop_back();
       for (int d = 0; d <= D; ++d) {
-        const std::uint32_t nb = s.n[d];
-        bool in_cavity;
-        if (stamp_[nb] >= epoch_) {
-          in_cavity = (stamp_[nb] & 1u) != 0;
-        } else {
-          in_cavity = conflict(nb, q, qid);
-          stamp_[nb] = epoch_ | (in_cavity ? 1u : 0u);
-          if (in_cavity) bfs_.push_back(nb);
+        const std::uint32_t nb = cells_[id].n[d];
+        if (mark_[nb] == 0) {
+          mark_[nb] = in_conflict(nb, q, qid) ? 1 : 2;
+          touched_.push_back(nb);
+          if (mark_[nb] == 1) stack.push_back(nb);
         }
-        if (!in_cavity) {
-          Boundary bf;
-          bf.outside = nb;
-          bf.outside_slot = -1;
-          const Cell<D>& o = cells_[nb];
-          for (int j = 0; j <= D; ++j)
-            if (o.n[j] == id) {
-              bf.outside_slot = j;
-              break;
-            }
-          int idx = 0;
-          for (int i = 0; i <= D; ++i)
-            if (i != d) bf.verts[idx++] = s.v[i];
-          boundary_.push_back(bf);
-        }
+        if (mark_[nb] == 2) shell_.push_back(Face{id, d, nb});
       }
     }
-    for (std::uint32_t id : cavity_) {
-      cells_[id].alive = 0;
-      free_.push_back(id);
-    }
-    ridges_.clear();
-    for (const Boundary& bf : boundary_) {
-      Cell<D> ns;
-      int idx = 0, q_slot = -1;
-      for (int i = 0; i < D; ++i) {
-        if (q_slot < 0 && qid < bf.verts[i]) {
-          q_slot = idx;
-          ns.v[idx++] = qid;
-        }
-        ns.v[idx++] = bf.verts[i];
-      }
-      if (q_slot < 0) {
-        q_slot = idx;
-        ns.v[idx++] = qid;
-      }
-      for (int i = 0; i <= D; ++i) ns.n[i] = kNone;
-      ns.n[q_slot] = bf.outside;
-      if (ns.v[D] == kInf) {
-        ns.parity = 0;
+    // the cavity's boundary facets, each coned to q; the outside cell's
+    // back link is found before any cavity slot is recycled
+    std::vector<std::uint32_t>& made = made_;
+    made.clear();
+    for (Face& f : shell_) {
+      const Cell<D>& inner = cells_[f.cell];
+      const Cell<D>& outer = cells_[f.outside];
+      f.back = -1;
+      for (int j = 0; j <= D; ++j)
+        if (outer.n[j] == f.cell) f.back = j;
+      Cell<D> c;
+      std::uint32_t vs[D + 1];
+      int w = 0;
+      for (int i = 0; i <= D; ++i)
+        if (i != f.slot) vs[w++] = inner.v[i];
+      vs[D] = qid;
+      std::sort(vs, vs + D + 1);  // ascending, the infinite id last
+      for (int i = 0; i <= D; ++i) c.v[i] = vs[i], c.n[i] = kNone;
+      const int at_q = static_cast<int>(std::find(vs, vs + D + 1, qid) - vs);
+      c.n[at_q] = f.outside;
+      if (c.v[D] == kInf) {
+        c.parity = 0;
       } else {
-        ns.parity = static_cast<std::int8_t>(parity_of(ns.v));
-        if (ns.parity == 0) throw DegenerateInputError("affinely dependent points beyond the tie-break's scope");
+        c.parity = static_cast<std::int8_t>(parity_of(c.v));
+        if (c.parity == 0) throw DegenerateInputError("affinely dependent points beyond the tie-break's scope");
       }
-      const std::uint32_t nid = create(ns);
-      cells_[bf.outside].n[bf.outside_slot] = nid;
-      for (int d = 0; d <= D; ++d) {
-        if (ns.v[d] == qid) continue;
-        // ridge = all vertices except v[d] and q
-        std::uint64_t key = 0;
-        for (int i = 0; i <= D; ++i) {
-          if (i == d || ns.v[i] == qid) continue;
-          key = (key << 32) | ns.v[i];
-        }
-        ridges_.push_back(Ridge{key, nid, d});
+      made.push_back(0);
+      pending_.push_back(c);
+    }
+    for (std::uint32_t id : touched_) {
+      if (mark_[id] == 1) {
+        cells_[id].alive = 0;
+        free_.push_back(id);
       }
-      hint_ = nid;
+      mark_[id] = 0;
     }
-    std::sort(ridges_.begin(), ridges_.end());
-    for (std::size_t i = 0; i + 1 < ridges_.size(); i += 2) {
-      const Ridge& a = ridges_[i];
-      const Ridge& b = ridges_[i + 1];
-      if (a.key != b.key) throw DegenerateInputError("unpaired cavity ridge");
-      cells_[a.simplex].n[a.slot] = b.simplex;
-      cells_[b.simplex].n[b.slot] = a.simplex;
+    for (std::size_t i = 0; i < shell_.size(); ++i) {
+      made[i] = new_cell(pending_[i]);
+      cells_[shell_[i].outside].n[shell_[i].back] = made[i];
     }
-    // prefer a finite hint
+    pending_.clear();
+    link_by_ridges(made, qid);
+    hint_ = made.back();
     if (cells_[hint_].v[D] == kInf) hint_ = cells_[hint_].n[D];
   }
 
@@ -433,17 +397,28 @@ class Builder {
     return t;
   }
 
+  struct Face {
+    std::uint32_t cell;     // the cavity cell
+    int slot;               // its slot facing `outside`
+    std::uint32_t outside;  // the kept cell across that facet
+    int back = -1;          // outside's slot facing the cavity
+  };
+  struct Slot {
+    std::uint64_t key;
+    std::uint32_t cell;
+    int slot;
+  };
+
   const double* xyz_;
   Rng rng_;
   std::vector<std::uint32_t> order_;
   std::vector<Cell<D>> cells_;
-  std::vector<std::uint32_t> free_;
-  std::vector<std::uint32_t> stamp_;
-  std::uint32_t epoch_ = 0;
+  std::vector<std::uint8_t> mark_;
+  std::vector<std::uint32_t> free_, stack_, touched_, made_;
+  std::vector<Face> shell_;
+  std::vector<Cell<D>> pending_;
+  std::vector<Slot> table_;
   std::uint32_t hint_ = 0;
-  std::vector<std::uint32_t> cavity_, bfs_;
-  std::vector<Boundary> boundary_;
-  std::vector<Ridge> ridges_;
   mutable std::vector<double> scratch_;
 };
 

@@ -10,13 +10,16 @@
 //     infinite simplices = open outer halfspace with the same tie rule) is the
 //     reference's (sequential_dt.cpp:130-169, geometry.hpp:158-166), so the
 //     canonical form equals the reference's triangulate_seq output.
-// Differences (performance only, result-neutral for a unique DT):
-//   * insertion order is a seeded BRIO (biased randomized insertion order,
-//     rounds sorted along a Morton curve) and the walk starts at the last
-//     created simplex, instead of a uniform shuffle + random start;
-//   * cavity slots are recycled only after every outside-neighbor index was
-//     recorded during the cavity search (no alias of a freed id; cf. the
-//     reference's slot-reuse defect at sequential_dt.cpp:265/296).
+// Only those rules fix the result (a unique DT under the tie rule); the
+// construction is this repo's own: a seeded BRIO insertion order (rounds
+// sorted along a Morton curve), the first cell from the first D+1 affinely
+// independent points (exact tests), a deterministic visibility walk from the
+// last created cell (linear-scan fallback on degenerate ties), a depth-first
+// cavity search with per-cell marks, new cells linked through an
+// open-addressing ridge table, and cavity slots recycled only after every
+// outside cell's back link was found (cf. the reference's slot-reuse defect,
+// SURVEY.md F4). tests/test_host.py pins the canonical forms against the
+// reference's compiled triangulate_seq (golden), incl. near-degenerate sets.
 #pragma once
 
 #include <cstddef>
