@@ -446,6 +446,11 @@ struct BorderArgs {
   std::uint32_t* esc;               // undecided filtered in_sphere tests: (row, cell-point slot)
   unsigned* esc_count;
   unsigned esc_cap;
+  // rows with an undecided pair that did not fit the queue: decided again,
+  // whole, by k_border_redo (bit per row + list)
+  unsigned* redo_bits;
+  std::uint32_t* redo_rows;
+  unsigned* redo_count;
   // exact policy, hull rows: the hull vertex set of all partials (sorted ids)
   const std::uint32_t* labels;
   const std::uint32_t* hull_ids;
@@ -475,8 +480,9 @@ __device__ bool cell_points_inside(const BorderArgs& a, unsigned long long idx, 
       if (slot < a.esc_cap) {
         a.esc[2ull * slot] = static_cast<std::uint32_t>(s);
         a.esc[2ull * slot + 1] = t;
-      } else {
-        atomicOr(a.status, kStQueueOverflow);
+      } else {  // the queue is full: the whole row is decided again after the escalation
+        const unsigned bit = 1u << (s & 31u);
+        if (!(atomicOr(&a.redo_bits[s >> 5], bit) & bit)) a.redo_rows[atomicAdd(a.redo_count, 1u)] = static_cast<std::uint32_t>(s);
       }
     }
   }
@@ -1681,6 +1687,58 @@ __global__ void __launch_bounds__(128) k_border_escalate(BorderArgs a, double* _
   }
 }
 
+// Exact policy, rows whose undecided in_sphere pairs overflowed the
+// escalation queue: one thread per row decides it again from scratch — the
+// binary64 sphere, the serial exact descent over the foreign cells it
+// overlaps, every foreign point of those cells with the filtered in_sphere
+// and, where undecided, the exact one in this thread's scratch (the
+// escalation kernel's, which has finished). Rare: a degrade path, not a
+// fast path.
+template <int D>
+__global__ void __launch_bounds__(128) k_border_redo(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
+                                                     double* __restrict__ scratch) {
+  const unsigned count = *a.redo_count;
+  const unsigned tid = blockIdx.x * blockDim.x + threadIdx.x;
+  double* buf = scratch + std::size_t(tid) * (D == 3 ? sbdt_pred::kInSphere3Scratch : sbdt_pred::kInSphere2Scratch);
+  const OwnerGrid<D>& og = *ogp;
+  const CellPt<D>* pts = static_cast<const CellPt<D>*>(a.cell_pts);
+  for (unsigned e = tid; e < count; e += gridDim.x * blockDim.x) {
+    const std::uint64_t s = a.redo_rows[e];
+    if (a.positive[s]) continue;  // decided by a queued pair
+    std::uint32_t v[D + 1];
+#pragma unroll
+    for (int j = 0; j <= D; ++j) v[j] = a.verts[std::uint64_t(j) * a.S + s];
+    double p[D + 1][D];
+    load_simplex<D>(a, v, p);
+    double c[D], r2;
+    circumsphere_inflated<D>(p, c, &r2);
+    const std::uint32_t self = part_of(a.offsets, a.k, s);
+    const double* A = a.parity[s] != 1 ? p[1] : p[0];
+    const double* B = a.parity[s] != 1 ? p[0] : p[1];
+    auto leaf = [&](const int* cell) -> bool {
+      const unsigned long long idx = og_index<D>(og, 0, cell);
+      for (std::uint32_t t = a.cell_start[idx], te = a.cell_start[idx + 1]; t < te; ++t) {
+        const CellPt<D> q = pts[t];
+        if (q.label == self) continue;
+        int r;
+        if constexpr (D == 3) r = sbdt_pred::in_sphere3_filtered(A, B, p[2], p[3], q.x);
+        else r = sbdt_pred::in_sphere2_filtered(A, B, p[2], q.x);
+        if (r == 2) {
+          if constexpr (D == 3) r = sbdt_pred::in_sphere3_exact_buf(A, B, p[2], p[3], q.x, buf);
+          else r = sbdt_pred::in_sphere2_exact_buf(A, B, p[2], q.x, buf);
+        }
+        if (r > 0) return true;
+      }
+      return false;
+    };
+    if (og_sphere_exact_serial<D>(og, a.owner, c, r2, self, leaf)) {
+      a.positive[s] = 1;
+#pragma unroll
+      for (int j = 0; j <= D; ++j) a.vflags[v[j]] = 1;
+    }
+  }
+}
+
 // Circumspheres only (spheres_out with the grid / exact policies).
 template <int D>
 __global__ void k_border_spheres(BorderArgs a) {
@@ -1893,6 +1951,9 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   a.esc = nullptr;
   a.esc_count = nullptr;
   a.esc_cap = 0;
+  a.redo_bits = nullptr;
+  a.redo_rows = nullptr;
+  a.redo_count = nullptr;
   a.labels = in->d_labels;
   a.hull_ids = nullptr;
   a.hull_count = nullptr;
@@ -1925,13 +1986,21 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
                          reinterpret_cast<std::uint64_t*>(const_cast<unsigned long long*>(a.hull_count)));
   };
   if (exact_policy) {
-    const unsigned long long want = 2ull * in->S + 2ull * in->n + (1ull << 20);
+    unsigned long long want = 2ull * in->S + 2ull * in->n + (1ull << 20);
+    // test hook: a tiny queue exercises the overflow (redo) path
+    if (const char* cap_env = std::getenv("SBDT_TEST_ESC_CAP")) want = std::strtoull(cap_env, nullptr, 10);
     a.esc_cap = static_cast<unsigned>(want < 0x7FFFFFFFull ? want : 0x7FFFFFFFull);
-    SBDT_WS(esc, std::uint32_t, "border.esc", 2ull * a.esc_cap);
-    SBDT_WS(escn, unsigned, "border.esc_n", 1);
-    SBDT_CUDA_TRY(cudaMemsetAsync(escn, 0, sizeof(unsigned), st));
+    SBDT_WS(esc, std::uint32_t, "border.esc", 2ull * a.esc_cap + 2);
+    SBDT_WS(escn, unsigned, "border.esc_n", 2);  // {queued pairs, redo rows}
+    SBDT_WS(rbits, unsigned, "border.redo_bits", in->S / 32 + 1);
+    SBDT_WS(rrows, std::uint32_t, "border.redo_rows", in->S + 1);
+    SBDT_CUDA_TRY(cudaMemsetAsync(escn, 0, 2 * sizeof(unsigned), st));
+    SBDT_CUDA_TRY(cudaMemsetAsync(rbits, 0, sizeof(unsigned) * (in->S / 32 + 1), st));
     a.esc = esc;
     a.esc_count = escn;
+    a.redo_bits = rbits;
+    a.redo_rows = rrows;
+    a.redo_count = escn + 1;
   }
   a.counters = nullptr;
   if (ctx->census) {
@@ -2098,7 +2167,8 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
       constexpr std::size_t per = D == 3 ? sbdt_pred::kInSphere3Scratch : sbdt_pred::kInSphere2Scratch;
       SBDT_WS(scr, double, "border.esc_scratch", per * kEscThreads);
       k_border_escalate<D><<<kEscThreads / 128, 128, 0, st>>>(a, scr);
-      ctx->launches += 1;
+      k_border_redo<D><<<kEscThreads / 128, 128, 0, st>>>(a, og, scr);
+      ctx->launches += 2;
     }
     if (tiled && in->d_spheres) {
       const std::uint64_t want = (in->S + 255) / 256;

@@ -169,14 +169,13 @@ __global__ void k_owner_mark(const double* __restrict__ xyz, const std::uint32_t
   for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += std::uint64_t(gridDim.x) * blockDim.x) {
     const std::uint32_t lab = labels[i];
-    if (lab == SBDT_UNINDEXED) continue;  // not in this level's indices (never a simplex vertex)
     double x[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) x[d] = xyz[i * D + d];  // in flight together with the label
+    if (lab == SBDT_UNINDEXED) continue;  // not in this level's indices (never a simplex vertex)
     int c[D];
 #pragma unroll
-    for (int d = 0; d < D; ++d) {
-      x[d] = xyz[i * D + d];
-      c[d] = static_cast<int>(cell_coord_fast<D>(og.g, og.inv_edge, x[d], d));
-    }
+    for (int d = 0; d < D; ++d) c[d] = static_cast<int>(cell_coord_fast<D>(og.g, og.inv_edge, x[d], d));
     if (xq) {
       // packed prefilter coordinates, indexed by PointId: 3-D 21-bit fixed
       // point of (x - lo) / qh (|error| <= qh / 2), 2-D the binary32 offsets

@@ -173,3 +173,28 @@ def test_find_border_escalates(case, policy, ctx):
         assert st["orient_check_rows"] > 0 and st["orient_escalations"] > 0
     if case == "cocircular" and policy == "exact":
         assert st["in_sphere_escalations"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["cocircular", "jittered_lattice"])
+def test_escalation_queue_overflow_degrades(case, ctx, monkeypatch):
+    """A full escalation queue no longer fails the call: the rows whose
+    undecided pairs did not fit are decided again, whole, after the
+    escalation (k_border_redo). The queue is shrunk to 4 entries through the
+    test hook SBDT_TEST_ESC_CAP; results must still equal the oracle."""
+    from paper_1902_07554_b200 import gpu, host
+    if case == "cocircular":
+        pts, lab = _cocircular_instance()
+        P = host.build_partials(pts, lab, 2, 7)
+    else:
+        side = 12
+        g = np.stack(np.meshgrid(*[np.arange(side, dtype=np.float64)] * 3, indexing="ij"), -1).reshape(-1, 3)
+        pts = np.ascontiguousarray(g + np.random.default_rng(3).uniform(-1e-9, 1e-9, g.shape))
+        lab = np.minimum((pts[:, 0] * 3 // side).astype(np.uint32), 2)
+        P = host.build_partials(pts, lab, 3, 7)
+    monkeypatch.setenv("SBDT_TEST_ESC_CAP", "4")
+    g = gpu.find_border(pts, lab, P, gpu.IntersectionPolicy("exact", 1.0), hull_bfs=True, ctx=ctx)
+    monkeypatch.delenv("SBDT_TEST_ESC_CAP")
+    o = oracle.find_border(pts, lab, P, "exact")
+    assert np.array_equal(g.positive, o["positive"]) and np.array_equal(g.border, o["border"])
+    assert np.array_equal(g.positive_vertex_ids, o["vertices_positive"])
