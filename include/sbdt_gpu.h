@@ -201,6 +201,10 @@ typedef struct sbdt_border_args {
   double* d_spheres;              /* S*(dim+1), optional */
   const double* grid_bbox;        /* optional HOST array 2*dim (lo[], hi[]): the grid's global bbox (SBDT_UNINDEXED) */
   uint64_t grid_n_total;          /* 0: n */
+  uint64_t grid_max_cells;        /* owner-grid capacity in cells; 0: 4 n / c_G^dim. A grid that needs more
+                                     (a bbox far from cubical) fails with SBDT_ERR_RANGE; the host-buffer
+                                     entry point then retries once with the capacity the grid needs
+                                     (up to 2^31 cells) */
 } sbdt_border_args;
 
 int sbdt_gpu_find_border_dev(sbdt_gpu_ctx* ctx, const sbdt_border_args* args);

@@ -1830,7 +1830,8 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   // recursion levels: the top level's grid (global bbox, n_total), SBDT_UNINDEXED points skipped
   const std::uint64_t n_grid = in->grid_n_total ? in->grid_n_total : in->n;
   const unsigned long long cap =
-      static_cast<unsigned long long>(4.0 * double(n_grid > in->n ? n_grid : in->n) * scale) + 4096;
+      in->grid_max_cells ? in->grid_max_cells
+                         : static_cast<unsigned long long>(4.0 * double(n_grid > in->n ? n_grid : in->n) * scale) + 4096;
   const unsigned long long owner_len = 2 * cap + 64 * kMaxLevels + 4096;
   SBDT_WS(og, OwnerGrid<D>, "border.og", 1);
   SBDT_WS(owner, std::uint16_t, "border.owner", owner_len);

@@ -5,12 +5,14 @@
 #include <thread>
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstring>
 #include <new>
 #include <string>
 
 #include "common.cuh"
 #include "context.cuh"
+#include "owner_grid.cuh"
 #include "sbdt_gpu.h"
 
 namespace sbdt_gpu {
@@ -359,12 +361,13 @@ int sbdt_gpu_find_border_dev(sbdt_gpu_ctx* ctx, const sbdt_border_args* a) {
   return kOk;
 }
 
-int sbdt_gpu_find_border(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint64_t n, const uint32_t* labels,
-                         uint32_t k, const uint64_t* offsets, const uint32_t* verts, const uint32_t* nbrs,
-                         const int8_t* parity, int policy, double c_G, uint32_t flags, uint8_t* positive_out,
-                         uint8_t* border_out, uint32_t* vertex_ids_out, uint64_t* n_vertices_out,
-                         uint32_t* bfs_vertex_ids_out, uint64_t* n_bfs_vertices_out, double* spheres_out,
-                         const double* grid_bbox, uint64_t grid_n_total) {
+namespace {
+int find_border_host(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint64_t n, const uint32_t* labels,
+                     uint32_t k, const uint64_t* offsets, const uint32_t* verts, const uint32_t* nbrs,
+                     const int8_t* parity, int policy, double c_G, uint32_t flags, uint8_t* positive_out,
+                     uint8_t* border_out, uint32_t* vertex_ids_out, uint64_t* n_vertices_out,
+                     uint32_t* bfs_vertex_ids_out, uint64_t* n_bfs_vertices_out, double* spheres_out,
+                     const double* grid_bbox, uint64_t grid_n_total, uint64_t grid_max_cells) {
   if (!ctx || !coords || !labels || !offsets || !verts || !nbrs || (!parity && policy == SBDT_POLICY_EXACT) ||
       !positive_out || !vertex_ids_out || !n_vertices_out)
     return SBDT_ERR_INVALID;
@@ -381,6 +384,7 @@ int sbdt_gpu_find_border(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint6
   a.flags = flags;
   a.grid_bbox = grid_bbox;
   a.grid_n_total = grid_n_total;
+  a.grid_max_cells = grid_max_cells;
   double* d_xyz;
   uint32_t *d_lab, *d_verts, *d_nbrs, *d_vids, *d_bvids = nullptr;
   uint64_t *d_off, *d_cnt, *d_bcnt = nullptr;
@@ -500,6 +504,33 @@ int sbdt_gpu_find_border(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint6
     if (n_bfs_vertices_out) *n_bfs_vertices_out = nb;
   }
   return SBDT_OK;
+}
+}  // namespace
+
+int sbdt_gpu_find_border(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint64_t n, const uint32_t* labels,
+                         uint32_t k, const uint64_t* offsets, const uint32_t* verts, const uint32_t* nbrs,
+                         const int8_t* parity, int policy, double c_G, uint32_t flags, uint8_t* positive_out,
+                         uint8_t* border_out, uint32_t* vertex_ids_out, uint64_t* n_vertices_out,
+                         uint32_t* bfs_vertex_ids_out, uint64_t* n_bfs_vertices_out, double* spheres_out,
+                         const double* grid_bbox, uint64_t grid_n_total) {
+  int rc = find_border_host(ctx, dim, coords, n, labels, k, offsets, verts, nbrs, parity, policy, c_G, flags,
+                            positive_out, border_out, vertex_ids_out, n_vertices_out, bfs_vertex_ids_out,
+                            n_bfs_vertices_out, spheres_out, grid_bbox, grid_n_total, 0);
+  if (rc != SBDT_ERR_RANGE || !ctx) return rc;
+  // A bbox far from cubical needs more cells than the default 4 n / c_G^dim
+  // capacity: retry once with what the grid needs (bounded), instead of
+  // rejecting an input the reference's sparse GridIndex accepts.
+  auto it = ctx->bufs.find("border.og");
+  if (it == ctx->bufs.end()) return rc;
+  unsigned long long need[2] = {0, 0};
+  const std::size_t off = dim == 2 ? offsetof(OwnerGrid<2>, need_cells) : offsetof(OwnerGrid<3>, need_cells);
+  if (cudaMemcpy(need, static_cast<char*>(it->second.ptr) + off, sizeof(need), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return rc;
+  const unsigned long long want = need[0] > need[1] ? need[0] : need[1];
+  if (need[0] == 0 || want > (1ull << 31)) return rc;
+  return find_border_host(ctx, dim, coords, n, labels, k, offsets, verts, nbrs, parity, policy, c_G, flags,
+                          positive_out, border_out, vertex_ids_out, n_vertices_out, bfs_vertex_ids_out,
+                          n_bfs_vertices_out, spheres_out, grid_bbox, grid_n_total, want + 4096);
 }
 
 namespace {

@@ -37,6 +37,7 @@ struct OwnerGrid {
   int shift;   // log2 per-axis fanout
   int ldims[kMaxLevels][D];
   unsigned long long loff[kMaxLevels + 1];
+  unsigned long long need_cells, need_entries;  // what the bbox needs (read back after a capacity failure)
 };
 
 template <int D>
@@ -107,6 +108,29 @@ __global__ void k_owner_params(const unsigned long long* bbox, std::uint64_t n, 
     og->g.dims[d] = bad ? 1 : static_cast<long long>(f) + 1;
     cells *= static_cast<unsigned long long>(og->g.dims[d]);
   }
+  og->need_cells = bad ? 0ull : cells;
+  og->need_entries = 0;
+  if (!bad) {  // the tiled layout's entries for these dims (as below)
+    int ld[kMaxLevels][D], nl = 0;
+    for (;;) {
+      bool top = true;
+      for (int d = 0; d < D; ++d) {
+        ld[nl][d] = static_cast<int>(((og->g.dims[d] - 1) >> (nl * og_shift<D>())) + 1);
+        top = top && ld[nl][d] == 1;
+      }
+      ++nl;
+      if (top || nl == kMaxLevels) break;
+    }
+    unsigned long long ent = 0;
+    for (int l = 0; l < nl; ++l) {
+      unsigned long long cnt = 64;
+      if (l == nl - 1) cnt = 1;
+      else
+        for (int d = 0; d < D; ++d) cnt *= static_cast<unsigned long long>(ld[l + 1][d]);
+      ent += cnt;
+    }
+    og->need_entries = ent;
+  }
   if (bad || cells > cap_cells) {
     atomicOr(status, kStGridCap);
     for (int d = 0; d < D; ++d) og->g.dims[d] = 1;
@@ -168,14 +192,13 @@ __global__ void k_owner_mark(const double* __restrict__ xyz, const std::uint32_t
   const double inv_qh = 1.0 / og.qh;
   for (std::uint64_t i = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += std::uint64_t(gridDim.x) * blockDim.x) {
-    const std::uint32_t lab = labels[i];
     double x[D];
-#pragma unroll
-    for (int d = 0; d < D; ++d) x[d] = xyz[i * D + d];  // in flight together with the label
-    if (lab == SBDT_UNINDEXED) continue;  // not in this level's indices (never a simplex vertex)
     int c[D];
 #pragma unroll
-    for (int d = 0; d < D; ++d) c[d] = static_cast<int>(cell_coord_fast<D>(og.g, og.inv_edge, x[d], d));
+    for (int d = 0; d < D; ++d) {
+      x[d] = xyz[i * D + d];
+      c[d] = static_cast<int>(cell_coord_fast<D>(og.g, og.inv_edge, x[d], d));
+    }
     if (xq) {
       // packed prefilter coordinates, indexed by PointId: 3-D 21-bit fixed
       // point of (x - lo) / qh (|error| <= qh / 2), 2-D the binary32 offsets
@@ -194,6 +217,8 @@ __global__ void k_owner_mark(const double* __restrict__ xyz, const std::uint32_t
         xq[i] = static_cast<std::uint64_t>(__float_as_uint(fx)) | (static_cast<std::uint64_t>(__float_as_uint(fy)) << 32);
       }
     }
+    const std::uint32_t lab = labels[i];
+    if (lab == SBDT_UNINDEXED) continue;  // not in this level's indices (never a simplex vertex)
     std::uint16_t* slot = owner + og_index<D>(og, 0, c);
     unsigned short old = *slot;
     while (old != lab && old != kOwnerMulti) {

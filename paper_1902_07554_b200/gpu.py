@@ -49,6 +49,7 @@ class BorderArgs(C.Structure):
         ("d_vertex_flags", C.c_void_p), ("d_vertex_ids", C.c_void_p), ("d_vertex_count", C.c_void_p),
         ("d_bfs_vertex_flags", C.c_void_p), ("d_bfs_vertex_ids", C.c_void_p), ("d_bfs_vertex_count", C.c_void_p),
         ("d_spheres", C.c_void_p), ("grid_bbox", C.POINTER(C.c_double)), ("grid_n_total", C.c_uint64),
+        ("grid_max_cells", C.c_uint64),
     ]
 
 

@@ -283,3 +283,25 @@ def test_recursion_level_grid(policy, ctx):
     assert np.array_equal(g.positive, o["positive"]) and np.array_equal(g.border, o["border"])
     assert np.array_equal(g.positive_vertex_ids, o["vertices_positive"])
     assert np.array_equal(g.border_vertex_ids, o["vertices_border"])
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_elongated_bbox_grid_capacity(dim, ctx):
+    """A bbox far from cubical (a thin needle / strip): c_G (V/n)^(1/D) cells
+    along the long axis far exceed the default 4 n capacity; the host entry
+    point retries with the capacity the grid needs instead of failing."""
+    rng = np.random.default_rng(17 + dim)
+    n = 20_000
+    pts = rng.random((n, dim))
+    pts[:, 1:] *= 1e-6 if dim == 3 else 1e-9
+    pts = np.ascontiguousarray(pts)
+    lab = np.minimum((pts[:, 0] * 4).astype(np.uint32), 3)
+    P = host.build_partials(pts, lab, 4, 7)
+    _, _, _, dims = oracle.grid_params(pts, 1.0)
+    assert np.prod(dims) > 4 * n  # beyond the default capacity
+    for policy in ("grid", "exact"):
+        g = gpu.find_border(pts, lab, P, gpu.IntersectionPolicy(policy, 1.0), hull_bfs=True, ctx=ctx)
+        o = oracle.find_border(pts, lab, P, policy)
+        assert np.array_equal(g.positive, o["positive"]), policy
+        assert np.array_equal(g.border, o["border"]), policy
+        assert np.array_equal(g.positive_vertex_ids, o["vertices_positive"]), policy
