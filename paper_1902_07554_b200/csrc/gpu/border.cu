@@ -317,41 +317,6 @@ __device__ __forceinline__ void decode_row(const std::uint64_t* w, float (*A)[D]
   }
 }
 
-// true iff every cell the sphere (c, R) can reach lies in one window (the
-// cell itself, its 3^D or its 5^D neighbourhood, the smallest that covers the
-// conservative cell range) whose combined code is EMPTY or `self`: then no
-// foreign occupied cell is reachable.
-template <int D>
-__device__ __forceinline__ bool window_clear(const OwnerGrid<D>& og, const std::uint16_t* __restrict__ owner,
-                                             const std::uint16_t* __restrict__ nbr3,
-                                             const std::uint16_t* __restrict__ nbr5, const double* c, double R,
-                                             std::uint32_t self) {
-  const double r = R * (1.0 + 1e-9) + og.margin;
-  int a[D];
-  int w = 0;
-  bool outside = false;
-#pragma unroll
-  for (int d = 0; d < D; ++d) {
-    const double fa = floor((c[d] - r - og.g.lo[d]) * og.inv_edge);
-    const double fb = floor((c[d] + r - og.g.lo[d]) * og.inv_edge);
-    const double top = static_cast<double>(og.ldims[0][d] - 1);
-    if (!(fa <= fb)) return false;  // NaN
-    outside = outside || fb < 0.0 || fa > top;
-    a[d] = fa < 0.0 ? 0 : (fa > top ? og.ldims[0][d] - 1 : static_cast<int>(fa));
-    const int b = fb > top ? og.ldims[0][d] - 1 : (fb < 0.0 ? 0 : static_cast<int>(fb));
-    w = max(w, b - a[d]);
-  }
-  if (outside) return true;  // the range misses the grid on some axis: no cell is reachable
-  if (w > 4) return false;
-  const int h = w == 0 ? 0 : (w <= 2 ? 1 : 2);
-  int cm[D];
-#pragma unroll
-  for (int d = 0; d < D; ++d) cm[d] = min(a[d] + h, og.ldims[0][d] - 1);
-  const std::uint16_t* src = h == 0 ? owner : (h == 1 ? nbr3 : nbr5);
-  const std::uint16_t code = __ldg(src + og_index<D>(og, 0, cm));
-  return code == kOwnerEmpty || code == self;
-}
-
 constexpr int kFlatSpan = 7;  // widest per-axis cell range of the flattened exact scan
 
 // Leaf-cell range of the (inflated binary64) sphere, as og_sphere_hits_foreign
@@ -429,8 +394,7 @@ struct BorderArgs {
   std::uint64_t S;
   int policy;
   const std::uint16_t* owner;
-  const std::uint16_t* nbr3;  // 3^D neighbourhood codes (grid policy prefilter)
-  const std::uint16_t* nbr5;  // 5^D neighbourhood codes
+  const std::uint32_t* field;  // window field of the prefilter (k_field_tiles), linear over ldims[0]
   const unsigned long long* pbbox;  // [k][2D] ordered (bbox policy)
   std::uint8_t* positive;
   std::uint8_t* vflags;
@@ -610,85 +574,104 @@ __device__ __forceinline__ void load_simplex(const BorderArgs& a, const std::uin
     for (int d = 0; d < D; ++d) p[j][d] = __ldg(a.xyz + std::size_t(v[j]) * D + d);
 }
 
+// Per-launch constants of the prefilter's decision (registers, not the
+// shared OwnerGrid: the hot loop reads them every row).
+template <int D>
+struct PfConst {
+  const std::uint32_t* field;  // window field (k_field_tiles), linear over ldims[0]
+  int ctop[D];                 // kFloorBias + ldims[0][d] - 1
+  unsigned dim0, dim1;         // ldims[0][0], ldims[0][1] (linear index)
+  float inv_e, margin_c, lo_mag;
+  bool pos_ok;                 // positive proofs allowed (grid policy, cell boxes within binary32 reach)
+};
+
+// floor_small(x) + kFloorBias: the bits of x + 1.5 * 2^23 rounded down
+constexpr int kFloorBias = 0x4B400000;
+
 // Prefilter decision for one finite row from its binary32 sphere:
-// 0 negative, 1 positive, 2 exact stage. Negative: the conservative cell range
-// of the enclosing ball (computed in binary32 cell units with explicit slack,
-// a superset of the exact stage's leaf range) sits in one window (the cell,
-// its 3^D or its 5^D neighbourhood) whose combined code is EMPTY or self.
-// Positive: the INNER ball (inside the binary64 sphere, checked in binary64)
-// reaches the cell of its centre and that cell holds another part.
+// 0 negative, 1 positive, 2 exact stage. One field word (k_field_tiles) at
+// the cell cc of the sphere's centre (clamped into the grid):
+//   negative: the conservative cell range of the enclosing ball (binary32
+//     cell units with explicit slack, a superset of the exact stage's leaf
+//     range, clipped to the grid) lies in the (2h+1)^D window around cc for
+//     some h < hs whose non-empty cells are all owned by `self`;
+//   positive: the INNER ball (inside the binary64 sphere, checked in
+//     binary64) reaches the cell of its centre, which holds another part.
 // For an undecided row (2) the cell-unit centre U and the inner ball's reach
 // are stored in out_U / out_reach (reach < 0: no positive proof possible) for
-// the exact stage's neighbour test (octant_proof), where every lane holds an
-// undecided row, so the extra lookups do not diverge the warp.
+// the exact stage's neighbour test (octant_proof).
 template <int D>
-__device__ __forceinline__ int prefilter_decide(const OwnerGrid<D>& og, const BorderArgs& a, const Sphere32<D>& sp,
-                                                std::uint32_t self, float inv_e, float margin_c, float lo_mag,
-                                                bool pos_ok, float* out_U, float* out_reach) {
-  if (out_reach) *out_reach = -1.f;
+__device__ __forceinline__ int prefilter_decide(const PfConst<D>& pc, const Sphere32<D>& sp, std::uint32_t self,
+                                                float* out_U, float* out_reach) {
+  *out_reach = -1.f;
   // R >= radius of the inflated binary64 sphere + distance between centres
   float slack = 0.f;
 #pragma unroll
   for (int d = 0; d < D; ++d) slack = fmaxf(slack, fabsf(sp.P0[d]) + fabsf(sp.rel[d]));
-  slack = (slack + lo_mag) * 1e-15f;
+  slack = (slack + pc.lo_mag) * 1e-15f;
   const float R = fmaf(fmaf(sp.r, 1.000004f, 2.01f * sp.e), 1.000001f, slack);
-  const float Rc = fmaf(R * inv_e, 1.000001f, margin_c);
-  int lo[D], w = 0;
-  int c0[D];
-  float Ucs[D];
-  bool outside = false, inside = true;
-  float sl_max = 0.f;
+  const float Rc = fmaf(R * pc.inv_e, 1.000001f, pc.margin_c);
+  float Uc[D], um = 0.f;
 #pragma unroll
   for (int d = 0; d < D; ++d) {
-    const float Uc = (sp.P0[d] + sp.rel[d]) * inv_e;
-    const float sl = fmaf(4e-7f, fabsf(Uc) + Rc, 1e-6f);
-    sl_max = fmaxf(sl_max, sl);
-    const float top = static_cast<float>(og.ldims[0][d] - 1);
-    const float fl = fminf(fmaxf(Uc - Rc - sl, -2.f), top + 2.f);
-    const float fh = fminf(fmaxf(Uc + Rc + sl, -2.f), top + 2.f);
-    const int ia = floor_small(fl), ib = floor_small(fh);
-    outside = outside || ib < 0 || ia > og.ldims[0][d] - 1;
-    lo[d] = max(ia, 0);
-    w = max(w, min(ib, og.ldims[0][d] - 1) - lo[d]);
-    Ucs[d] = Uc;
-    const int ic = floor_small(fminf(fmaxf(Uc, -2.f), top + 2.f));
-    inside = inside && ic >= 0 && ic <= og.ldims[0][d] - 1;
-    c0[d] = ic;
+    Uc[d] = (sp.P0[d] + sp.rel[d]) * pc.inv_e;
+    um = fmaxf(um, fabsf(Uc[d]));
   }
-  if (outside) return 0;  // the range misses the grid on some axis: no cell is reachable
-  // Both owner-code loads go out together (one latency instead of two in a
-  // row): the window's code for the negative proof and the centre cell's
-  // code for the positive proof below.
-  const bool cen = inside && pos_ok && !a.exact;  // exact policy: a foreign cell is not a foreign point
-  std::uint16_t wcode = kOwnerMulti, ccode = kOwnerEmpty;
-  if (w <= 4) {
-    const int h = w == 0 ? 0 : (w <= 2 ? 1 : 2);
-    int cm[D];
+  // rounding of Uc (three roundings of |Uc|) and of Uc -/+ Rp: below 4e-7 (|Uc| + Rc)
+  const float sl = fmaf(4e-7f, um + Rc, 1e-6f);
+  const float Rp = Rc + sl;
+  if (!(um + Rp < 4194304.f)) return 2;  // outside floor_small's range (or NaN)
+  int need = 0, cb[D];
+  bool inside = true;
 #pragma unroll
-    for (int d = 0; d < D; ++d) cm[d] = min(lo[d] + h, og.ldims[0][d] - 1);
-    const std::uint16_t* src = h == 0 ? a.owner : (h == 1 ? a.nbr3 : a.nbr5);
-    wcode = __ldg(src + og_index<D>(og, 0, cm));
+  for (int d = 0; d < D; ++d) {
+    const int a = max(__float_as_int(__fadd_rd(Uc[d] - Rp, 12582912.f)), kFloorBias);
+    const int b = min(__float_as_int(__fadd_rd(Uc[d] + Rp, 12582912.f)), pc.ctop[d]);
+    const int c0 = __float_as_int(__fadd_rd(Uc[d], 12582912.f));
+    const int cc = min(max(c0, kFloorBias), pc.ctop[d]);
+    inside = inside && c0 == cc;
+    need = max(need, max(cc - a, b - cc));
+    cb[d] = cc - kFloorBias;
   }
-  if (cen) ccode = __ldg(a.owner + og_index<D>(og, 0, c0));
-  if (wcode == kOwnerEmpty || wcode == self) return 0;
-  // Positive proof, in binary32 cell units: c0 = floor(Uc) holds Uc, the real
-  // centre lies within sqrt(D) sl of Uc, and the cell box in cell units is
-  // [c0, c0 + 1] up to the binary64 rounding of cell_lo (< 1e-7 cells while
-  // (|lo| / edge + dims) < 2^26, checked by the caller through pos_ok). If the
-  // inner ball, shrunk by the exact stage's margin, still reaches that box,
-  // the binary64 box test on the binary64 sphere accepts it.
-  // The same holds for a neighbour of c0 whose box (in cell units) is within
-  // the remaining reach of Uc.
-  if (!cen) return 2;
-  const float rin_c = ((sp.r * 0.999996f - 2.01f * sp.e * 1.000001f) * 0.999999f - slack) * inv_e * 0.999998f;
-  const float reach = rin_c - margin_c - 1.7321f * sl_max - 2e-7f;
+  unsigned long long li;
+  if constexpr (D == 3)
+    li = static_cast<unsigned long long>(static_cast<unsigned>(cb[1]) + pc.dim1 * static_cast<unsigned>(cb[2])) * pc.dim0 +
+         static_cast<unsigned>(cb[0]);
+  else
+    li = static_cast<unsigned long long>(static_cast<unsigned>(cb[1])) * pc.dim0 + static_cast<unsigned>(cb[0]);
+  const std::uint32_t fw = __ldg(pc.field + li);
+  const std::uint32_t code = fw & 0xFFFFu;
+  if (code == self && need < static_cast<int>(fw >> 24)) return 0;
+  // Positive proof, in binary32 cell units: cc = floor(Uc) holds Uc, the
+  // real centre lies within sqrt(D) sl of Uc, and the cell box in cell units
+  // is [cc, cc + 1] up to the binary64 rounding of cell_lo (< 1e-7 cells
+  // while (|lo| / edge + dims) < 2^26, checked by the caller through pos_ok).
+  // If the inner ball, shrunk by the exact stage's margin, still reaches that
+  // box, the binary64 box test on the binary64 sphere accepts it. The same
+  // holds for a neighbour of cc whose box is within the remaining reach of Uc
+  // (the exact stage's octant_proof).
+  if (!(inside && pc.pos_ok)) return 2;
+  const float rin_c = ((sp.r * 0.999996f - 2.01f * sp.e * 1.000001f) * 0.999999f - slack) * pc.inv_e * 0.999998f;
+  const float reach = rin_c - pc.margin_c - 1.7321f * sl - 2e-7f;
   if (!(reach > 0.f)) return 2;
-  if (ccode != kOwnerEmpty && ccode != self) return 1;
-  if (out_reach) {
-    *out_reach = reach;
+  if (!(fw & kFieldEmptyBit) && code != self) return 1;  // non-empty, another part or MULTI
+  // The window of radius hs (1 <= hs <= H) around cc is MULTI: it holds an
+  // occupied cell of another part. If the inner ball reaches even the far
+  // corner of the window's farthest cell, it overlaps that cell.
+  const int hs = static_cast<int>(fw >> 24);
+  if (hs >= 1 && hs <= field_h<D>()) {
+    float dd = 0.f;
 #pragma unroll
-    for (int d = 0; d < D; ++d) out_U[d] = Ucs[d];
+    for (int d = 0; d < D; ++d) {
+      const float f = Uc[d] - static_cast<float>(cb[d]);  // exact: cb = floor(Uc)
+      const float m = fmaxf(f, 1.f - f) + static_cast<float>(hs - 1);
+      dd = fmaf(m, m, dd);
+    }
+    if (dd * 1.000002f + 1e-6f < reach * reach) return 1;
   }
+  *out_reach = reach;
+#pragma unroll
+  for (int d = 0; d < D; ++d) out_U[d] = Uc[d];
   return 2;
 }
 
@@ -770,16 +753,23 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
   unsigned it = 0;
   // binary32 cell-unit scale and margin (rounded up; the slacks cover the rest)
   // decode_row's coordinate unit: the fixed-point step in 3-D, 1 in 2-D
-  const double unit = D == 3 ? og.qh : 1.0;
-  const float inv_e = static_cast<float>(og.inv_edge * unit);
-  const float margin_c = static_cast<float>(og.margin * og.inv_edge) * 1.0001f + 1e-30f;
-  float lo_mag = 0.f;
+  PfConst<D> pc;
+  {
+    const double unit = D == 3 ? og.qh : 1.0;
+    pc.field = a.field;
+    pc.inv_e = static_cast<float>(og.inv_edge * unit);
+    pc.margin_c = static_cast<float>(og.margin * og.inv_edge) * 1.0001f + 1e-30f;
+    pc.lo_mag = 0.f;
+    pc.pos_ok = !a.exact;  // exact policy: a foreign cell is not a foreign point
 #pragma unroll
-  for (int d = 0; d < D; ++d) lo_mag = fmaxf(lo_mag, static_cast<float>(fabs(og.g.lo[d]) / unit) * 1.0001f);
-  bool pos_ok = true;
-#pragma unroll
-  for (int d = 0; d < D; ++d)
-    pos_ok = pos_ok && fabs(og.g.lo[d]) * og.inv_edge + static_cast<double>(og.ldims[0][d]) < 67108864.0;
+    for (int d = 0; d < D; ++d) {
+      pc.lo_mag = fmaxf(pc.lo_mag, static_cast<float>(fabs(og.g.lo[d]) / unit) * 1.0001f);
+      pc.pos_ok = pc.pos_ok && fabs(og.g.lo[d]) * og.inv_edge + static_cast<double>(og.ldims[0][d]) < 67108864.0;
+      pc.ctop[d] = kFloorBias + og.ldims[0][d] - 1;
+    }
+    pc.dim0 = static_cast<unsigned>(og.ldims[0][0]);
+    pc.dim1 = static_cast<unsigned>(og.ldims[0][1]);
+  }
   // software pipeline: the vertex ids of the next row are in flight while
   // this row's coordinates are gathered and tested
   std::uint64_t s = base + wofs + lane;
@@ -825,7 +815,7 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
       // with the exact orientation in the exact stage (kReachCheckOrient)
       int res = 2;
       if (enclosing_sphere_f32<D>(A, eta, P0e, sp))
-        res = prefilter_decide<D>(og, a, sp, self, inv_e, margin_c, lo_mag, pos_ok, cU, &creach);
+        res = prefilter_decide<D>(pc, sp, self, cU, &creach);
       else
         creach = kReachCheckOrient;
       if (a.counters && res == 1) atomicAdd(&a.counters[8], 1ull);
@@ -860,12 +850,10 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
     }
     if (is_cand) {
       cand[q] = static_cast<std::uint32_t>(s);
-#pragma unroll
-      for (int j = 0; j <= D; ++j) cand[std::uint64_t(j + 1) * cap + q] = v[j];
-      cand[std::uint64_t(2 * D + 2) * cap + q] = __float_as_uint(creach);
+      cand[std::uint64_t(D + 1) * cap + q] = __float_as_uint(creach);
       if (creach > 0.f)
 #pragma unroll
-        for (int d = 0; d < D; ++d) cand[std::uint64_t(D + 2 + d) * cap + q] = __float_as_uint(cU[d]);
+        for (int d = 0; d < D; ++d) cand[std::uint64_t(1 + d) * cap + q] = __float_as_uint(cU[d]);
     }
     if (inf) a.inf_queue[bi + __popc(mi & lt)] = static_cast<std::uint32_t>(s);
     s = s_next;
@@ -963,17 +951,17 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
       s = crow;
       self = s_off.part(a.k, s);
 #pragma unroll
-      for (int j = 0; j <= D; ++j) v[j] = cand[std::uint64_t(j + 1) * cap + t];
+      for (int j = 0; j <= D; ++j) v[j] = __ldg(a.verts + std::uint64_t(j) * a.S + s);
       bool proven = false;
       if constexpr (!Ex) {
-        const float reach = __uint_as_float(cand[std::uint64_t(2 * D + 2) * cap + t]);
+        const float reach = __uint_as_float(cand[std::uint64_t(D + 1) * cap + t]);
         // binary32 positive proof over the centre cell's near-octant
         // neighbours (the prefilter tried the centre cell and recorded the
         // cell-unit centre and the inner ball's reach)
         if (reach > 0.f) {
           float U[D];
 #pragma unroll
-          for (int d = 0; d < D; ++d) U[d] = __uint_as_float(cand[std::uint64_t(D + 2 + d) * cap + t]);
+          for (int d = 0; d < D; ++d) U[d] = __uint_as_float(cand[std::uint64_t(1 + d) * cap + t]);
           proven = octant_proof<D>(og, a, U, reach, self);
         }
       }
@@ -1123,7 +1111,7 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
             if (!loaded) {
               std::uint32_t vv[D + 1];
 #pragma unroll
-              for (int j = 0; j <= D; ++j) vv[j] = cand[std::uint64_t(j + 1) * cap + r.qi];
+              for (int j = 0; j <= D; ++j) vv[j] = __ldg(a.verts + std::uint64_t(j) * a.S + r.row);
               load_simplex<D>(a, vv, pv);
               par = a.parity[r.row];
               loaded = true;
@@ -1159,10 +1147,10 @@ __global__ void __launch_bounds__(256) k_border_orient(BorderArgs a, const std::
   const unsigned ncand = *ncand_p;
   for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < ncand; t += gridDim.x * blockDim.x) {
     if (cand[t] == kNoRow) continue;
-    if (__uint_as_float(cand[std::uint64_t(2 * D + 2) * cap + t]) != kReachCheckOrient) continue;
+    if (__uint_as_float(cand[std::uint64_t(D + 1) * cap + t]) != kReachCheckOrient) continue;
     std::uint32_t v[D + 1];
 #pragma unroll
-    for (int j = 0; j <= D; ++j) v[j] = cand[std::uint64_t(j + 1) * cap + t];
+    for (int j = 0; j <= D; ++j) v[j] = __ldg(a.verts + std::uint64_t(j) * a.S + cand[t]);
     double p[D + 1][D];
     load_simplex<D>(a, v, p);
     if (a.counters) atomicAdd(a.counters + kCtrOrientRows, 1ull);
@@ -1911,13 +1899,17 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
     cell_start = cstart;
     cell_pts = cpts;
   }
-  std::uint16_t *nbr3 = nullptr, *nbr5 = nullptr;
+  std::uint32_t* field = nullptr;
   if (tiled) {
-    SBDT_WS(n3, std::uint16_t, "border.nbr3", owner_len);
-    SBDT_WS(n5, std::uint16_t, "border.nbr5", owner_len);
-    nbr3 = n3;
-    nbr5 = n5;
-    k_nbr_tiles<D><<<sms * 8, 256, 0, st>>>(og, owner, nbr3, nbr5);
+    SBDT_WS(fw, std::uint32_t, "border.field", cap + 1);  // level-0 cells <= cap
+    field = fw;
+    static bool attr_set[2] = {false, false};
+    if (!attr_set[D - 2]) {
+      SBDT_CUDA_TRY(cudaFuncSetAttribute(k_field_tiles<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(field_smem_bytes<D>())));
+      attr_set[D - 2] = true;
+    }
+    k_field_tiles<D><<<sms * 3, kFieldThreads, field_smem_bytes<D>(), st>>>(og, owner, field);
     ctx->launches += 1;
   }
   ctx->launches += 6;
@@ -1937,8 +1929,7 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   a.S = in->S;
   a.policy = in->policy;
   a.owner = owner;
-  a.nbr3 = nbr3;
-  a.nbr5 = nbr5;
+  a.field = field;
   a.pbbox = pbbox;
   a.positive = in->d_positive;
   a.vflags = in->d_vertex_flags;
@@ -2033,7 +2024,7 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
         // candidates <= rows, plus < kQChunk holes per prefilter warp and launch
         const std::uint64_t launches_A = ctx->chunks.empty() ? 1 : ctx->chunks.size();
         const std::uint64_t qcap = in->S + 32 + launches_A * resA * (kBThreads / 32) * kQChunk;
-        SBDT_WS(cq, std::uint32_t, "border.cand", qcap * (2 * D + 3));  // {row, vertices, U, reach}
+        SBDT_WS(cq, std::uint32_t, "border.cand", qcap * (D + 2));  // SoA {row, U[D], reach}
         // {candidates, cursor, wide rows, wide cursor, CTAs done (exact), CTAs done (wide)}
         // {candidates, cursor, wide rows, wide cursor, CTAs done (exact), CTAs done (wide), light wide rows}
         SBDT_WS(cn, unsigned, "border.cand_n", 8);

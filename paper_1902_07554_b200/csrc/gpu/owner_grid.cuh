@@ -304,21 +304,10 @@ __global__ void k_owner_levels_tail(const OwnerGrid<D>* __restrict__ ogp, std::u
   }
 }
 
-// ---- neighbourhood codes -----------------------------------------------------------
-// nbr3[c] / nbr5[c] = combine of the leaf codes in the 3^D / 5^D window
-// around c, clipped to the grid. The combine is a semilattice (EMPTY
-// identity, MULTI absorbing), so the box filter is separable (one 1-D pass of
-// half-width 1 per axis), and a 3-window of 3-windows is the 5-window.
-// Both neighbourhood code arrays in one pass. A CTA owns a block-aligned
-// tile (16^3 cells in 3-D, 64^2 in 2-D) and stages it with a 2-cell halo in
-// shared memory (EMPTY outside the grid). Three separable 3-window passes
-// give the 3^D codes (valid one cell into the halo), three more the 5^D
-// codes; each pass runs one thread per grid line with a sliding window.
-template <int D>
-constexpr int nbr_tile() {
-  return D == 3 ? 16 : 64;
-}
-
+// packed window word: (min code) << 16 | (0xFFFF - max code), EMPTY counting
+// as +inf for the min and 0 for the max; the window combine (EMPTY identity,
+// MULTI absorbing) is then a per-half-word min (VIMNMX.U16x2), and the code
+// is recovered from (min, max)
 __device__ __forceinline__ std::uint32_t nbr_pack(std::uint16_t code) {
   return (static_cast<std::uint32_t>(code) << 16) | (code == kOwnerEmpty ? 0xFFFFu : 0xFFFFu - code);
 }
@@ -327,47 +316,91 @@ __device__ __forceinline__ std::uint16_t nbr_unpack(std::uint32_t w) {
   return mn == kOwnerEmpty ? kOwnerEmpty : static_cast<std::uint16_t>(mn == mx ? mn : kOwnerMulti);
 }
 
+// ---- window field (grid-policy prefilter) ----------------------------------------
+// For every leaf cell c and h = 0..H let W_h(c) be the combined code of the
+// (2h+1)^D window of cells centred on c, clipped to the grid (cells outside
+// the grid do not exist: EMPTY). The combine is a semilattice (EMPTY
+// identity, MULTI absorbing), so W_{h+1} is the 3^D window combine of W_h and
+// the box filter is separable (one 1-D pass of half-width 1 per axis).
+// One u32 per cell, LINEAR layout (x fastest over ldims[0]):
+//   bits 24-31  hs = h* + 1, h* = the largest h <= H with W_h(c) not MULTI
+//               (0 when the cell itself is MULTI)
+//   bit  16     the cell itself is EMPTY
+//   bits 0-15   the cell's code, or W_{h*}(c) when the cell is EMPTY.
+// The prefilter then needs ONE load per row: a ball whose conservative cell
+// range lies in [c - h, c + h] (per axis) with h < hs and code == self
+// reaches no foreign occupied cell (every non-empty cell of the window is
+// owned by `self`), and a non-empty cell c with another code is foreign.
+// A CTA owns a T^D tile (16^3 cells in 3-D, 64^2 in 2-D) and stages it with
+// an H-cell halo in shared memory (row pitch RS + 1: the x-lines of the
+// in-place passes are bank-conflict free); H rounds of three separable
+// passes, one thread per grid line with a sliding window. After round h the
+// staged W is exact at least h cells inside the staged region, which covers
+// the tile (halo H).
+// H = 2 (windows up to 5^D): larger windows decide < 1.5% more rows on the
+// BASELINE configs (measured with H = 4) and cost a round of passes each.
 template <int D>
-__global__ void __launch_bounds__(256) k_nbr_tiles(const OwnerGrid<D>* __restrict__ ogp,
-                                                   const std::uint16_t* __restrict__ owner,
-                                                   std::uint16_t* __restrict__ nbr3, std::uint16_t* __restrict__ nbr5) {
+constexpr int field_h() {
+  return 2;
+}
+template <int D>
+constexpr int field_tile() {
+  return D == 3 ? 16 : 64;
+}
+constexpr std::uint32_t kFieldEmptyBit = 1u << 16;
+constexpr int kFieldThreads = 256;
+
+template <int D>
+constexpr int field_smem_words() {
+  constexpr int RS = field_tile<D>() + 2 * field_h<D>();
+  return D == 3 ? (RS + 1) * RS * RS : (RS + 1) * RS;
+}
+template <int D>
+constexpr std::size_t field_smem_bytes() {
+  constexpr int T = field_tile<D>();
+  return sizeof(std::uint32_t) * (field_smem_words<D>() + (D == 3 ? T * T * T : T * T));
+}
+
+template <int D>
+__global__ void __launch_bounds__(kFieldThreads) k_field_tiles(const OwnerGrid<D>* __restrict__ ogp,
+                                                               const std::uint16_t* __restrict__ owner,
+                                                               std::uint32_t* __restrict__ field) {
   constexpr int F = og_fan<D>();
   constexpr int SH = og_shift<D>();
-  constexpr int T = nbr_tile<D>();
-  constexpr int TB = T / F;     // tile blocks per axis
-  constexpr int RS = T + 4;     // staged cells per axis
+  constexpr int H = field_h<D>();
+  constexpr int T = field_tile<D>();
+  constexpr int RS = T + 2 * H;               // staged cells per axis
+  constexpr int P = RS + 1;                   // x pitch
   constexpr int RN = D == 3 ? RS * RS * RS : RS * RS;
   constexpr int LN = D == 3 ? RS * RS : RS;   // lines per pass
   constexpr int ON = D == 3 ? T * T * T : T * T;
   __shared__ OwnerGrid<D> og;
-  // one packed word per staged cell: (min code) << 16 | (0xFFFF - max code),
-  // EMPTY counting as +inf for the min and as 0 for the max; then the window
-  // combine (EMPTY identity, MULTI absorbing) is one 16x2 three-way min
-  // (VIMNMX3.U16x2), and the code is recovered from (min, max) at the end
-  __shared__ std::uint32_t buf[RN];
+  extern __shared__ std::uint32_t fsm[];
+  std::uint32_t* buf = fsm;                          // packed window words (nbr_pack)
+  std::uint32_t* outw = fsm + field_smem_words<D>();  // the tile's field words
   if (threadIdx.x == 0) og = *ogp;
   __syncthreads();
-  if (og.levels < 2) {  // a single cell
-    if (blockIdx.x == 0 && threadIdx.x == 0) nbr3[og.loff[0]] = nbr5[og.loff[0]] = owner[og.loff[0]];
-    return;
-  }
-  int nt[D], bd1[D], cd0[D];
+  int nt[D], cd0[D];
   unsigned long long ntiles = 1;
 #pragma unroll
   for (int d = 0; d < D; ++d) {
-    bd1[d] = og.ldims[1][d];
     cd0[d] = og.ldims[0][d];
-    nt[d] = (bd1[d] + TB - 1) / TB;
+    nt[d] = (cd0[d] + T - 1) / T;
     ntiles *= static_cast<unsigned long long>(nt[d]);
   }
   const std::uint16_t* own0 = owner + og.loff[0];
+  const bool single = og.levels < 2;  // one cell: no tiled level-0 layout
   auto gindex = [&](const int* c) -> unsigned long long {  // level-0 tiled index
+    if (single) return 0ull;
     unsigned b = static_cast<unsigned>(c[D - 1] >> SH), sub = 0;
 #pragma unroll
-    for (int d = D - 2; d >= 0; --d) b = b * static_cast<unsigned>(bd1[d]) + static_cast<unsigned>(c[d] >> SH);
+    for (int d = D - 2; d >= 0; --d) b = b * static_cast<unsigned>(og.ldims[1][d]) + static_cast<unsigned>(c[d] >> SH);
 #pragma unroll
     for (int d = 0; d < D; ++d) sub |= static_cast<unsigned>(c[d] & (F - 1)) << (SH * d);
     return static_cast<unsigned long long>(b) * 64u + sub;
+  };
+  auto sidx = [](const int* t) {  // staged coordinates -> buffer word
+    return D == 3 ? t[0] + P * (t[1] + RS * t[2]) : t[0] + P * t[1];
   };
   for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     int org[D];
@@ -378,59 +411,91 @@ __global__ void __launch_bounds__(256) k_nbr_tiles(const OwnerGrid<D>* __restric
       rem /= static_cast<unsigned>(nt[d]);
     }
     for (int r = threadIdx.x; r < RN; r += blockDim.x) {
-      int c[D], rr = r;
+      int c[D], t[D], rr = r;
       bool in = true;
 #pragma unroll
       for (int d = 0; d < D; ++d) {
-        c[d] = org[d] - 2 + rr % RS;
+        t[d] = rr % RS;
         rr /= RS;
+        c[d] = org[d] - H + t[d];
         in = in && c[d] >= 0 && c[d] < cd0[d];
       }
-      buf[r] = nbr_pack(in ? own0[gindex(c)] : kOwnerEmpty);
+      buf[sidx(t)] = nbr_pack(in ? own0[gindex(c)] : kOwnerEmpty);
     }
     __syncthreads();
-    for (int rep = 0; rep < 2; ++rep) {
+    // h = 0: the cell's own code
+    for (int o = threadIdx.x; o < ON; o += blockDim.x) {
+      int t[D], oo = o;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        t[d] = oo % T + H;
+        oo /= T;
+      }
+      const std::uint16_t code = nbr_unpack(buf[sidx(t)]);
+      outw[o] = code == kOwnerMulti ? static_cast<std::uint32_t>(kOwnerMulti)
+                                    : ((1u << 24) | (code == kOwnerEmpty ? kFieldEmptyBit : 0u) | code);
+    }
+    __syncthreads();  // the passes below overwrite buf in place
+    for (int h = 1; h <= H; ++h) {
 #pragma unroll
       for (int ax = 0; ax < D; ++ax) {
-        const int st = ax == 0 ? 1 : (ax == 1 ? RS : RS * RS);
+        const int st = ax == 0 ? 1 : (ax == 1 ? P : P * RS);
         for (int l = threadIdx.x; l < LN; l += blockDim.x) {
-          // line l: the other coordinates, in increasing axis order
           int base;
           if constexpr (D == 3) {
             const int u = l % RS, w = l / RS;
-            base = ax == 0 ? (u * RS + w * RS * RS) : (ax == 1 ? (u + w * RS * RS) : (u + w * RS));
+            base = ax == 0 ? (u * P + w * P * RS) : (ax == 1 ? (u + w * P * RS) : (u + w * P));
           } else {
-            base = ax == 0 ? l * RS : l;
+            base = ax == 0 ? l * P : l;
           }
-          // in place: a line belongs to one thread, and the registers hold
-          // the original values of the cells already overwritten
+          // in place: a line belongs to one thread, the registers hold the
+          // original values of the cells already overwritten; the end cells
+          // combine their in-range neighbours only (never read: see above)
           std::uint32_t prev = buf[base], cur = buf[base + st];
-#pragma unroll 6
+          buf[base] = __vminu2(prev, cur);
+#pragma unroll 4
           for (int i = 1; i < RS - 1; ++i) {
             const std::uint32_t next = buf[base + (i + 1) * st];
             buf[base + i * st] = __vminu2(__vminu2(prev, cur), next);
             prev = cur;
             cur = next;
           }
+          buf[base + (RS - 1) * st] = __vminu2(prev, cur);
         }
         __syncthreads();
       }
-      // store the tile in tiled order: output o = block-major, sub-cell minor
-      std::uint16_t* out = (rep == 0 ? nbr3 : nbr5) + og.loff[0];
       for (int o = threadIdx.x; o < ON; o += blockDim.x) {
-        const int b = o >> 6, sub = o & 63;
-        int c[D], r = 0, mul = 1, bb = b;
-        bool in = true;
+        const std::uint32_t w0 = outw[o];
+        if ((w0 >> 24) != static_cast<unsigned>(h)) continue;  // stopped growing earlier
+        int t[D], oo = o;
 #pragma unroll
         for (int d = 0; d < D; ++d) {
-          const int t = (bb % TB) * F + ((sub >> (SH * d)) & (F - 1));
-          bb /= TB;
-          c[d] = org[d] + t;
-          in = in && c[d] < cd0[d];
-          r += (t + 2) * mul;
-          mul *= RS;
+          t[d] = oo % T + H;
+          oo /= T;
         }
-        if (in) out[gindex(c)] = nbr_unpack(buf[r]);
+        const std::uint16_t code = nbr_unpack(buf[sidx(t)]);
+        if (code == kOwnerMulti) continue;
+        const std::uint32_t lo = (w0 & kFieldEmptyBit) ? (kFieldEmptyBit | code) : (w0 & 0xFFFFFu);
+        outw[o] = (static_cast<std::uint32_t>(h + 1) << 24) | lo;
+      }
+      __syncthreads();  // read before the next round's passes overwrite buf
+    }
+    __syncthreads();
+    // linear layout, x fastest: consecutive threads store consecutive cells
+    for (int o = threadIdx.x; o < ON; o += blockDim.x) {
+      int c[D], oo = o;
+      bool in = true;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        c[d] = org[d] + oo % T;
+        oo /= T;
+        in = in && c[d] < cd0[d];
+      }
+      if (in) {
+        unsigned long long li = static_cast<unsigned>(c[D - 1]);
+#pragma unroll
+        for (int d = D - 2; d >= 0; --d) li = li * static_cast<unsigned>(cd0[d]) + static_cast<unsigned>(c[d]);
+        field[li] = outw[o];
       }
     }
     __syncthreads();  // the buffers are reloaded for the next tile
