@@ -141,15 +141,20 @@ __device__ __forceinline__ void circumsphere_inflated(const double (*p)[D], doub
 }
 
 // MUFU approximations used only inside bounds that carry >= 1e-5 relative
-// slack (PTX: rcp.approx.f32 within 1 ulp, sqrt.approx.f32 within ~2^-22.)
+// slack (PTX: rcp.approx.f32 within 1 ulp, sqrt.approx.f32 within ~2^-22).
+// .ftz: one MUFU, no denormal fixup sequence. A subnormal input reads as 0:
+// enclosing_sphere_f32 then fails its L > 1e-24 (1e-18) range check (edge
+// lengths) or sees a non-finite centre (det), and its r, e arguments are
+// >= 0.25 in 3-D (integer edges, P0e); only reciprocals of |det| <= 1e24
+// (checked through L) are taken, far from a subnormal result.
 __device__ __forceinline__ float sqrt_apx(float x) {
   float y;
-  asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 __device__ __forceinline__ float rcp_apx(float x) {
   float y;
-  asm("rcp.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 // floor(x) for |x| < 2^22: x + 1.5 * 2^23 rounded toward -inf lands in
@@ -694,9 +699,9 @@ __device__ __forceinline__ bool octant_proof(const OwnerGrid<D>& og, const Borde
     side[d] = f < 0.5f ? -1 : 1;
     gap[d] = f < 0.5f ? f : 1.f - f;
   }
-  // all the neighbours' codes are loaded before any is tested (one memory
-  // latency instead of up to 2^D - 1 in a row)
-  std::uint16_t code[(1 << D) - 1];
+  // all the neighbours' field words are loaded before any is tested (one
+  // memory latency instead of up to 2^D - 1 in a row)
+  std::uint32_t fw[(1 << D) - 1];
 #pragma unroll
   for (int k = 1; k < (1 << D); ++k) {
     int cn[D];
@@ -709,11 +714,14 @@ __device__ __forceinline__ bool octant_proof(const OwnerGrid<D>& og, const Borde
       ok = ok && cn[d] >= 0 && cn[d] < og.ldims[0][d];
       d2 += move ? gap[d] * gap[d] : 0.f;
     }
-    code[k - 1] = (ok && d2 * 1.000002f + 1e-12f < reach2) ? __ldg(a.owner + og_index<D>(og, 0, cn)) : kOwnerEmpty;
+    unsigned long long li = static_cast<unsigned>(cn[D - 1]);
+#pragma unroll
+    for (int d = D - 2; d >= 0; --d) li = li * static_cast<unsigned>(og.ldims[0][d]) + static_cast<unsigned>(cn[d]);
+    fw[k - 1] = (ok && d2 * 1.000002f + 1e-12f < reach2) ? __ldg(a.field + li) : kFieldEmptyBit;
   }
   bool hit = false;
 #pragma unroll
-  for (int k = 0; k < (1 << D) - 1; ++k) hit = hit || (code[k] != kOwnerEmpty && code[k] != self);
+  for (int k = 0; k < (1 << D) - 1; ++k) hit = hit || (!(fw[k] & kFieldEmptyBit) && (fw[k] & 0xFFFFu) != self);
   return hit;
 }
 
@@ -929,6 +937,7 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
   bst[0] = 1;
 #pragma unroll
   for (int d = 1; d < D; ++d) bst[d] = bst[d - 1] * static_cast<unsigned long long>(multi_level ? og.ldims[1][d - 1] : 1);
+  const unsigned fd0 = static_cast<unsigned>(og.ldims[0][0]), fd1 = static_cast<unsigned>(og.ldims[0][1]);
   unsigned char* nz = nzl[wid];
   const unsigned full = 0xffffffffu;
   // the next batch is claimed while this one is processed (the atomic's
@@ -1066,42 +1075,63 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
         cl = nz[cur + __popc(smask & ((2u << lane) - 1u))];
         const CandSlot<D>& r = sl[cl];
         const unsigned rem = q - r.excl;
-        unsigned long long base = og.loff[0];
         double g12;  // g1^2 (+ g2^2 added after g0^2, box_sphere's order)
         double g2z = 0.0;
+        int c1, c2 = 0;  // the row's cell coordinates on axes 1 (and 2)
         if constexpr (D == 3) {
           const unsigned i2 = (rem * r.inv[1]) >> 16;  // rem / span1 (rem * span1 < 2^16)
           const unsigned i1 = rem - i2 * r.span[1];
-          base += cell_off<D>(r.lo[1] + static_cast<int>(i1), 1, bst, multi_level) +
-                  cell_off<D>(r.lo[2] + static_cast<int>(i2), 2, bst, multi_level);
+          c1 = r.lo[1] + static_cast<int>(i1);
+          c2 = r.lo[2] + static_cast<int>(i2);
           g12 = r.g2[1][i1];
           g2z = r.g2[2][i2];
         } else {
-          base += cell_off<D>(r.lo[1] + static_cast<int>(rem), 1, bst, multi_level);
+          c1 = r.lo[1] + static_cast<int>(rem);
           g12 = r.g2[1][rem];
         }
         const double rr = r.r2;
-        std::uint16_t code[kFlatSpan];
-        bool geo[kFlatSpan];
-        unsigned long long cidx[kFlatSpan];
-#pragma unroll
-        for (int i0 = 0; i0 < kFlatSpan; ++i0) {
-          geo[i0] = false;
-          code[i0] = kOwnerEmpty;
-          cidx[i0] = 0;
-          if (i0 < static_cast<int>(r.span[0])) {
-            double d2 = r.g2[0][i0] + g12;
-            if constexpr (D == 3) d2 += g2z;
-            geo[i0] = d2 <= rr;
-            cidx[i0] = base + cell_off<D>(r.lo[0] + i0, 0, bst, multi_level);
-            if (geo[i0]) code[i0] = __ldg(a.owner + cidx[i0]);
-          }
-        }
         const std::uint32_t sf = r.self;
         if constexpr (!Ex) {
+          // the row's cells are consecutive words of the linear window field
+          // (code of a non-empty cell in the low half-word)
+          const unsigned long long lb =
+              (D == 3 ? static_cast<unsigned long long>(static_cast<unsigned>(c1) + fd1 * static_cast<unsigned>(c2))
+                      : static_cast<unsigned long long>(static_cast<unsigned>(c1))) * fd0 +
+              static_cast<unsigned>(r.lo[0]);
+          std::uint32_t fw[kFlatSpan];
+          bool geo[kFlatSpan];
 #pragma unroll
-          for (int i0 = 0; i0 < kFlatSpan; ++i0) h = h || (geo[i0] && code[i0] != kOwnerEmpty && code[i0] != sf);
+          for (int i0 = 0; i0 < kFlatSpan; ++i0) {
+            geo[i0] = false;
+            fw[i0] = kFieldEmptyBit;
+            if (i0 < static_cast<int>(r.span[0])) {
+              double d2 = r.g2[0][i0] + g12;
+              if constexpr (D == 3) d2 += g2z;
+              geo[i0] = d2 <= rr;
+              if (geo[i0]) fw[i0] = __ldg(a.field + lb + i0);
+            }
+          }
+#pragma unroll
+          for (int i0 = 0; i0 < kFlatSpan; ++i0) h = h || (!(fw[i0] & kFieldEmptyBit) && (fw[i0] & 0xFFFFu) != sf);
         } else {
+          const unsigned long long base =
+              og.loff[0] + cell_off<D>(c1, 1, bst, multi_level) + (D == 3 ? cell_off<D>(c2, 2, bst, multi_level) : 0ull);
+          std::uint16_t code[kFlatSpan];
+          bool geo[kFlatSpan];
+          unsigned long long cidx[kFlatSpan];
+#pragma unroll
+          for (int i0 = 0; i0 < kFlatSpan; ++i0) {
+            geo[i0] = false;
+            code[i0] = kOwnerEmpty;
+            cidx[i0] = 0;
+            if (i0 < static_cast<int>(r.span[0])) {
+              double d2 = r.g2[0][i0] + g12;
+              if constexpr (D == 3) d2 += g2z;
+              geo[i0] = d2 <= rr;
+              cidx[i0] = base + cell_off<D>(r.lo[0] + i0, 0, bst, multi_level);
+              if (geo[i0]) code[i0] = __ldg(a.owner + cidx[i0]);
+            }
+          }
           // exact policy: the points of the foreign overlapping cells
           bool loaded = false;
           double pv[D + 1][D];

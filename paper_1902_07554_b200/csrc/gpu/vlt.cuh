@@ -66,10 +66,11 @@ __device__ __forceinline__ bool dominated_f(const float* rs, const float* rt, co
   }
   const float fmin_ = __fsub_rn(__fsub_rn(ds, dt), __fmul_rn(2.f, slope));
   // |c-s| + H and |c-t| + H only scale the safety margin: MUFU square roots
-  // (within 2^-22 relative) rounded up by 1e-6 can only raise it
+  // (within 2^-22 relative) rounded up by 1e-6 can only raise it (.ftz: a
+  // subnormal distance reads as 0, < 1e-19 below it, far inside the margin)
   float ra, rb;
-  asm("sqrt.approx.f32 %0, %1;" : "=f"(ra) : "f"(ds));
-  asm("sqrt.approx.f32 %0, %1;" : "=f"(rb) : "f"(dt));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(ra) : "f"(ds));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(rb) : "f"(dt));
   const float a = __fadd_ru(ra * 1.000001f, H), b = __fadd_ru(rb * 1.000001f, H);
   return fmin_ > 1e-5f * (a * a + b * b);
 }
