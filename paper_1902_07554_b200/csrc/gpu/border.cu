@@ -400,6 +400,7 @@ struct BorderArgs {
   int policy;
   const std::uint16_t* owner;
   const std::uint32_t* field;  // window field of the prefilter (k_field_tiles), linear over ldims[0]
+  const std::uint32_t* fmask;  // foreign masks of the 3^D windows (k_field_tiles), linear over ldims[0]
   const unsigned long long* pbbox;  // [k][2D] ordered (bbox policy)
   std::uint8_t* positive;
   std::uint8_t* vflags;
@@ -590,6 +591,11 @@ struct PfConst {
   bool pos_ok;                 // positive proofs allowed (grid policy, cell boxes within binary32 reach)
 };
 
+// candidate record's outer-ball slot: the foreign mask does not apply (the
+// centre cell's field code is not the row's part, or the centre is outside
+// the grid); -1: it applies for positive proofs only (range wider than 3^D)
+constexpr float kRoutNoMask = -2.f;
+
 // floor_small(x) + kFloorBias: the bits of x + 1.5 * 2^23 rounded down
 constexpr int kFloorBias = 0x4B400000;
 
@@ -607,8 +613,9 @@ constexpr int kFloorBias = 0x4B400000;
 // the exact stage's neighbour test (octant_proof).
 template <int D>
 __device__ __forceinline__ int prefilter_decide(const PfConst<D>& pc, const Sphere32<D>& sp, std::uint32_t self,
-                                                float* out_U, float* out_reach) {
+                                                float* out_U, float* out_reach, float* out_rout) {
   *out_reach = -1.f;
+  *out_rout = kRoutNoMask;
   // R >= radius of the inflated binary64 sphere + distance between centres
   float slack = 0.f;
 #pragma unroll
@@ -647,6 +654,12 @@ __device__ __forceinline__ int prefilter_decide(const PfConst<D>& pc, const Sphe
   const std::uint32_t fw = __ldg(pc.field + li);
   const std::uint32_t code = fw & 0xFFFFu;
   if (code == self && need < static_cast<int>(fw >> 24)) return 0;
+  if (!inside) return 2;
+  // the exact stage's foreign-mask test (exact_mask_test) needs U; its
+  // negative proof also needs the range inside the 3^D window around cc
+#pragma unroll
+  for (int d = 0; d < D; ++d) out_U[d] = Uc[d];
+  if (code == self) *out_rout = need <= 1 ? Rp : -1.f;
   // Positive proof, in binary32 cell units: cc = floor(Uc) holds Uc, the
   // real centre lies within sqrt(D) sl of Uc, and the cell box in cell units
   // is [cc, cc + 1] up to the binary64 rounding of cell_lo (< 1e-7 cells
@@ -655,7 +668,7 @@ __device__ __forceinline__ int prefilter_decide(const PfConst<D>& pc, const Sphe
   // box, the binary64 box test on the binary64 sphere accepts it. The same
   // holds for a neighbour of cc whose box is within the remaining reach of Uc
   // (the exact stage's octant_proof).
-  if (!(inside && pc.pos_ok)) return 2;
+  if (!pc.pos_ok) return 2;
   const float rin_c = ((sp.r * 0.999996f - 2.01f * sp.e * 1.000001f) * 0.999999f - slack) * pc.inv_e * 0.999998f;
   const float reach = rin_c - pc.margin_c - 1.7321f * sl - 2e-7f;
   if (!(reach > 0.f)) return 2;
@@ -675,8 +688,6 @@ __device__ __forceinline__ int prefilter_decide(const PfConst<D>& pc, const Sphe
     if (dd * 1.000002f + 1e-6f < reach * reach) return 1;
   }
   *out_reach = reach;
-#pragma unroll
-  for (int d = 0; d < D; ++d) out_U[d] = Uc[d];
   return 2;
 }
 
@@ -723,6 +734,56 @@ __device__ __forceinline__ bool octant_proof(const OwnerGrid<D>& og, const Borde
 #pragma unroll
   for (int k = 0; k < (1 << D) - 1; ++k) hit = hit || (!(fw[k] & kFieldEmptyBit) && (fw[k] & 0xFFFFu) != self);
   return hit;
+}
+
+// The centre cell's foreign mask (k_field_tiles; the row's part is the
+// cell's field code, checked by the prefilter): 1 if the inner ball (reach,
+// all error slack already subtracted) reaches the box of a foreign
+// neighbour, 0 if the outer ball (rout > 0: radius in cell units with every
+// slack, its cell range inside the 3^D window) stays strictly away from all
+// of them, -1 undecided. Box distances in cell units from U, whose cell is
+// c0 = floor(U): per axis the gap to the neighbour at offset -1, 0, +1 is
+// f, 0, 1 - f (f = U - c0).
+template <int D>
+__device__ __forceinline__ int exact_mask_test(const OwnerGrid<D>& og, const BorderArgs& a, const float* U, float reach,
+                                               float rout) {
+  int c0[D];
+  float g[D][3];
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    c0[d] = floor_small(U[d]);
+    const float f = U[d] - static_cast<float>(c0[d]);  // exact
+    g[d][0] = f * f;
+    g[d][1] = 0.f;
+    g[d][2] = (1.f - f) * (1.f - f);
+  }
+  unsigned long long li = static_cast<unsigned>(c0[D - 1]);
+#pragma unroll
+  for (int d = D - 2; d >= 0; --d) li = li * static_cast<unsigned>(og.ldims[0][d]) + static_cast<unsigned>(c0[d]);
+  const std::uint32_t m = __ldg(a.fmask + li);
+  if (!m) return rout > 0.f ? 0 : -1;
+  float mn = INFINITY;  // smallest squared box distance over the foreign neighbours
+  if constexpr (D == 3) {
+#pragma unroll
+    for (int o2 = 0; o2 < 3; ++o2)
+#pragma unroll
+      for (int o1 = 0; o1 < 3; ++o1) {
+        const float s12 = g[1][o1] + g[2][o2];
+#pragma unroll
+        for (int o0 = 0; o0 < 3; ++o0)
+          if ((m >> (o0 + 3 * o1 + 9 * o2)) & 1u) mn = fminf(mn, g[0][o0] + s12);
+      }
+  } else {
+#pragma unroll
+    for (int o1 = 0; o1 < 3; ++o1)
+#pragma unroll
+      for (int o0 = 0; o0 < 3; ++o0)
+        if ((m >> (o0 + 3 * o1)) & 1u) mn = fminf(mn, g[0][o0] + g[1][o1]);
+  }
+  // (a few binary32 roundings of the squared distance, far inside the margins)
+  if (reach > 0.f && mn * 1.000002f + 1e-12f < reach * reach) return 1;
+  if (rout > 0.f && mn * 0.99999f - 1e-6f > rout * rout) return 0;
+  return -1;
 }
 
 // Rows are claimed by CTAs in chunks of kPfChunk from a launch-wide cursor
@@ -804,7 +865,7 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
     load_ids(s_next, vn);
     const bool inf = valid && v[D] == kInfVertex;
     bool is_cand = false;
-    float cU[D], creach = -1.f;  // recorded for the exact stage's neighbour test
+    float cU[D], creach = -1.f, crout = kRoutNoMask;  // recorded for the exact stage's first tests
     // a warp's rows only grow (claims are monotonic): advance the part cursor
     {
       const std::uint64_t sc = valid ? s : row_end - 1;
@@ -823,7 +884,7 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
       // with the exact orientation in the exact stage (kReachCheckOrient)
       int res = 2;
       if (enclosing_sphere_f32<D>(A, eta, P0e, sp))
-        res = prefilter_decide<D>(pc, sp, self, cU, &creach);
+        res = prefilter_decide<D>(pc, sp, self, cU, &creach, &crout);
       else
         creach = kReachCheckOrient;
       if (a.counters && res == 1) atomicAdd(&a.counters[8], 1ull);
@@ -859,7 +920,8 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
     if (is_cand) {
       cand[q] = static_cast<std::uint32_t>(s);
       cand[std::uint64_t(D + 1) * cap + q] = __float_as_uint(creach);
-      if (creach > 0.f)
+      cand[std::uint64_t(D + 2) * cap + q] = __float_as_uint(crout);
+      if (creach > 0.f || crout >= -1.f)
 #pragma unroll
         for (int d = 0; d < D; ++d) cand[std::uint64_t(1 + d) * cap + q] = __float_as_uint(cU[d]);
     }
@@ -961,20 +1023,30 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
       self = s_off.part(a.k, s);
 #pragma unroll
       for (int j = 0; j <= D; ++j) v[j] = __ldg(a.verts + std::uint64_t(j) * a.S + s);
-      bool proven = false;
+      bool proven = false, refuted = false;
       if constexpr (!Ex) {
+        // binary32 proofs from the prefilter's record (cell-unit centre U,
+        // inner-ball reach, outer radius): the foreign mask of the centre
+        // cell when it applies, else the near-octant neighbours' codes
         const float reach = __uint_as_float(cand[std::uint64_t(D + 1) * cap + t]);
-        // binary32 positive proof over the centre cell's near-octant
-        // neighbours (the prefilter tried the centre cell and recorded the
-        // cell-unit centre and the inner ball's reach)
-        if (reach > 0.f) {
+        const float rout = __uint_as_float(cand[std::uint64_t(D + 2) * cap + t]);
+        if (reach > 0.f || rout >= -1.f) {
           float U[D];
 #pragma unroll
           for (int d = 0; d < D; ++d) U[d] = __uint_as_float(cand[std::uint64_t(1 + d) * cap + t]);
-          proven = octant_proof<D>(og, a, U, reach, self);
+          if (rout >= -1.f) {
+            const int m = exact_mask_test<D>(og, a, U, reach, rout);
+            proven = m == 1;
+            refuted = m == 0;
+          } else {
+            proven = octant_proof<D>(og, a, U, reach, self);
+          }
         }
       }
-      if (proven) {
+      if (refuted) {
+        mode = 0;
+        if (a.counters) atomicAdd(&a.counters[15], 1ull);
+      } else if (proven) {
         mode = 0;
         pre_pos = true;
       } else {
@@ -1930,16 +2002,19 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
     cell_pts = cpts;
   }
   std::uint32_t* field = nullptr;
+  std::uint32_t* fmask = nullptr;
   if (tiled) {
     SBDT_WS(fw, std::uint32_t, "border.field", cap + 1);  // level-0 cells <= cap
+    SBDT_WS(fm, std::uint32_t, "border.fmask", cap + 1);
     field = fw;
+    fmask = fm;
     static bool attr_set[2] = {false, false};
     if (!attr_set[D - 2]) {
       SBDT_CUDA_TRY(cudaFuncSetAttribute(k_field_tiles<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(field_smem_bytes<D>())));
       attr_set[D - 2] = true;
     }
-    k_field_tiles<D><<<sms * 3, kFieldThreads, field_smem_bytes<D>(), st>>>(og, owner, field);
+    k_field_tiles<D><<<sms * 3, kFieldThreads, field_smem_bytes<D>(), st>>>(og, owner, field, fmask);
     ctx->launches += 1;
   }
   ctx->launches += 6;
@@ -1960,6 +2035,7 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   a.policy = in->policy;
   a.owner = owner;
   a.field = field;
+  a.fmask = fmask;
   a.pbbox = pbbox;
   a.positive = in->d_positive;
   a.vflags = in->d_vertex_flags;
@@ -2054,7 +2130,7 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
         // candidates <= rows, plus < kQChunk holes per prefilter warp and launch
         const std::uint64_t launches_A = ctx->chunks.empty() ? 1 : ctx->chunks.size();
         const std::uint64_t qcap = in->S + 32 + launches_A * resA * (kBThreads / 32) * kQChunk;
-        SBDT_WS(cq, std::uint32_t, "border.cand", qcap * (D + 2));  // SoA {row, U[D], reach}
+        SBDT_WS(cq, std::uint32_t, "border.cand", qcap * (D + 3));  // SoA {row, U[D], reach, rout}
         // {candidates, cursor, wide rows, wide cursor, CTAs done (exact), CTAs done (wide)}
         // {candidates, cursor, wide rows, wide cursor, CTAs done (exact), CTAs done (wide), light wide rows}
         SBDT_WS(cn, unsigned, "border.cand_n", 8);

@@ -327,6 +327,10 @@ __device__ __forceinline__ std::uint16_t nbr_unpack(std::uint32_t w) {
 //               (0 when the cell itself is MULTI)
 //   bit  16     the cell itself is EMPTY
 //   bits 0-15   the cell's code, or W_{h*}(c) when the cell is EMPTY.
+// and a second u32 per cell, the FOREIGN MASK: bit (dx+1) + 3 (dy+1) [+ 9 (dz+1)]
+// set iff the neighbour c + (dx, dy[, dz]) is non-empty with a code other
+// than the word's code (for a row of that code: the foreign cells of the 3^D
+// window; the exact stage's first test, see exact_mask_test).
 // The prefilter then needs ONE load per row: a ball whose conservative cell
 // range lies in [c - h, c + h] (per axis) with h < hs and code == self
 // reaches no foreign occupied cell (every non-empty cell of the window is
@@ -356,15 +360,22 @@ constexpr int field_smem_words() {
   return D == 3 ? (RS + 1) * RS * RS : (RS + 1) * RS;
 }
 template <int D>
+constexpr int field_raw_cells() {
+  constexpr int RS = field_tile<D>() + 2 * field_h<D>();
+  return D == 3 ? RS * RS * RS : RS * RS;
+}
+template <int D>
 constexpr std::size_t field_smem_bytes() {
   constexpr int T = field_tile<D>();
-  return sizeof(std::uint32_t) * (field_smem_words<D>() + (D == 3 ? T * T * T : T * T));
+  return sizeof(std::uint32_t) * (field_smem_words<D>() + (D == 3 ? T * T * T : T * T)) +
+         sizeof(std::uint16_t) * field_raw_cells<D>();
 }
 
 template <int D>
 __global__ void __launch_bounds__(kFieldThreads) k_field_tiles(const OwnerGrid<D>* __restrict__ ogp,
                                                                const std::uint16_t* __restrict__ owner,
-                                                               std::uint32_t* __restrict__ field) {
+                                                               std::uint32_t* __restrict__ field,
+                                                               std::uint32_t* __restrict__ fmask) {
   constexpr int F = og_fan<D>();
   constexpr int SH = og_shift<D>();
   constexpr int H = field_h<D>();
@@ -378,6 +389,8 @@ __global__ void __launch_bounds__(kFieldThreads) k_field_tiles(const OwnerGrid<D
   extern __shared__ std::uint32_t fsm[];
   std::uint32_t* buf = fsm;                          // packed window words (nbr_pack)
   std::uint32_t* outw = fsm + field_smem_words<D>();  // the tile's field words
+  // the staged leaf codes, unchanged by the passes (foreign masks), x fastest
+  std::uint16_t* raw = reinterpret_cast<std::uint16_t*>(outw + ON);
   if (threadIdx.x == 0) og = *ogp;
   __syncthreads();
   int nt[D], cd0[D];
@@ -420,7 +433,9 @@ __global__ void __launch_bounds__(kFieldThreads) k_field_tiles(const OwnerGrid<D
         c[d] = org[d] - H + t[d];
         in = in && c[d] >= 0 && c[d] < cd0[d];
       }
-      buf[sidx(t)] = nbr_pack(in ? own0[gindex(c)] : kOwnerEmpty);
+      const std::uint16_t code = in ? own0[gindex(c)] : kOwnerEmpty;
+      buf[sidx(t)] = nbr_pack(code);
+      raw[r] = code;
     }
     __syncthreads();
     // h = 0: the cell's own code
@@ -495,7 +510,30 @@ __global__ void __launch_bounds__(kFieldThreads) k_field_tiles(const OwnerGrid<D
         unsigned long long li = static_cast<unsigned>(c[D - 1]);
 #pragma unroll
         for (int d = D - 2; d >= 0; --d) li = li * static_cast<unsigned>(cd0[d]) + static_cast<unsigned>(c[d]);
-        field[li] = outw[o];
+        const std::uint32_t w = outw[o];
+        const std::uint16_t own = static_cast<std::uint16_t>(w & 0xFFFFu);
+        int t[D], oo2 = o;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          t[d] = oo2 % T + H;
+          oo2 /= T;
+        }
+        std::uint32_t m = 0;
+        if constexpr (D == 3) {
+#pragma unroll
+          for (int j = 0; j < 27; ++j) {
+            const std::uint16_t nc = raw[(t[0] + j % 3 - 1) + RS * ((t[1] + (j / 3) % 3 - 1) + RS * (t[2] + j / 9 - 1))];
+            m |= (nc != kOwnerEmpty && nc != own) ? (1u << j) : 0u;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 9; ++j) {
+            const std::uint16_t nc = raw[(t[0] + j % 3 - 1) + RS * (t[1] + j / 3 - 1)];
+            m |= (nc != kOwnerEmpty && nc != own) ? (1u << j) : 0u;
+          }
+        }
+        field[li] = w;
+        fmask[li] = m;
       }
     }
     __syncthreads();  // the buffers are reloaded for the next tile

@@ -596,26 +596,6 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
   }
 }
 
-// Exact binary64 argmin over the candidates whose binary32 interval overlaps
-// the winner's (reference squared_distance, lowest pid on ties).
-template <int D>
-__device__ __forceinline__ std::uint32_t exact_among(const double* x, const VltEntry* ents, int cnt, const float* d32,
-                                                     const float* b32, float lim, const SampleRec* __restrict__ sorted) {
-  double best = INFINITY;
-  std::uint32_t best_pid = 0xFFFFFFFFu, label = 0;
-  for (int j = 0; j < cnt; ++j) {
-    if (d32[j] - b32[j] > lim) continue;
-    const SampleRec rec = sorted[ents[j].idx];
-    const double d2 = sqdist<D>(x, rec.x);
-    if (d2 < best || (d2 == best && rec.pid < best_pid)) {
-      best = d2;
-      best_pid = rec.pid;
-      label = rec.label;
-    }
-  }
-  return label;
-}
-
 // K2: table-driven point pass (coordinates streamed once; overflow points
 // are queued for k_assign_overflow so they do not diverge the warp).
 template <int D>
@@ -671,32 +651,64 @@ __global__ void __launch_bounds__(256) k_assign_vlt(const double* __restrict__ x
         p[d] = static_cast<float>(x[d] - fcen[d]);
         pp += p[d] * p[d];
       }
-      float d32[kSlots], b32[kSlots];
-      int best = 0;
-      float bval = INFINITY;
-      for (int j = 0; j < static_cast<int>(cnt); ++j) {
-        const VltEntry e = ents[j];
+      // binary32 distances with the rigorous bound 4e-6 (|p|^2 + |s|^2): one
+      // pass keeps the winner (smallest dd, first on ties) and the two
+      // smallest interval lower ends (no per-candidate arrays: registers only)
+      auto dist = [&](const float4& e, float* bnd) {
+        const float er[3] = {e.x, e.y, e.z};
         float dd = 0.f, ss = 0.f;
 #pragma unroll
         for (int d = 0; d < D; ++d) {
-          const float t = p[d] - e.r[d];
+          const float t = p[d] - er[d];
           dd += t * t;
-          ss += e.r[d] * e.r[d];
+          ss += er[d] * er[d];
         }
-        d32[j] = dd;
-        b32[j] = 4e-6f * (pp + ss) + 1e-30f;
-        if (dd < bval) {
-          bval = dd;
-          best = j;
+        *bnd = 4e-6f * (pp + ss) + 1e-30f;
+        return dd;
+      };
+      float bv = INFINITY, bb = 0.f, m1 = INFINITY, m2 = INFINITY;
+      int bj = 0, j1 = -1;
+      for (int j = 0; j < static_cast<int>(cnt); ++j) {
+        float bnd;
+        const float dd = dist(__ldg(reinterpret_cast<const float4*>(ents + j)), &bnd);
+        if (dd < bv) {
+          bv = dd;
+          bb = bnd;
+          bj = j;
+        }
+        const float lo_end = dd - bnd;
+        if (lo_end < m1) {
+          m2 = m1;
+          m1 = lo_end;
+          j1 = j;
+        } else if (lo_end < m2) {
+          m2 = lo_end;
         }
       }
       // decided iff every other candidate is provably farther
-      const float lim = d32[best] + b32[best];
-      bool decided = true;
-      for (int j = 0; j < static_cast<int>(cnt); ++j)
-        if (j != best && d32[j] - b32[j] <= lim) decided = false;
-      const std::uint32_t lab = decided ? __ldg(sorted_labels + ents[best].idx)
-                                        : exact_among<D>(x, ents, static_cast<int>(cnt), d32, b32, lim, sorted);
+      const float lim = bv + bb;
+      std::uint32_t lab;
+      if ((j1 == bj ? m2 : m1) > lim) {
+        lab = __ldg(sorted_labels + ents[bj].idx);
+      } else {
+        // exact binary64 argmin over the candidates whose interval overlaps
+        // the winner's (reference squared_distance, lowest pid on ties)
+        double best = INFINITY;
+        std::uint32_t bpid = 0xFFFFFFFFu;
+        lab = 0;
+        for (int j = 0; j < static_cast<int>(cnt); ++j) {
+          float bnd;
+          const float dd = dist(__ldg(reinterpret_cast<const float4*>(ents + j)), &bnd);
+          if (j != bj && dd - bnd > lim) continue;
+          const SampleRec rec = sorted[ents[j].idx];
+          const double d2 = sqdist<D>(x, rec.x);
+          if (d2 < best || (d2 == best && rec.pid < bpid)) {
+            best = d2;
+            bpid = rec.pid;
+            lab = rec.label;
+          }
+        }
+      }
       __stcs(labels + i, lab);
     }
   }
