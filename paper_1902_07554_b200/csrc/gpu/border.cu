@@ -793,6 +793,7 @@ __device__ __forceinline__ int exact_mask_test(const OwnerGrid<D>& og, const Bor
 // of CTAs that drifted apart, and the CTA's warps take consecutive 32-row
 // slices of its chunk (vertices shared by neighbouring rows hit in L1).
 constexpr unsigned kPfIters = 16;
+constexpr unsigned kPfBatch = 64;  // per-warp batch of undecided rows (< 32 waiting + 32 arriving)
 constexpr unsigned kPfChunk = kBThreads * kPfIters;
 
 template <int D, bool BIGK>
@@ -813,6 +814,7 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
   const unsigned lt = (1u << lane) - 1u;
   // rows [row_begin, row_end); the whole CTA iterates over claimed chunks,
   // with one chunk of lookahead for the id prefetch
+  __shared__ std::uint32_t s_bat[kBThreads / 32][D + 4][kPfBatch];
   __shared__ unsigned long long s_claim;
   if (threadIdx.x == 0) s_claim = atomicAdd(cursor, 2ull * kPfChunk);
   __syncthreads();
@@ -854,6 +856,66 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
   // atomic per chunk instead of one per iteration on the single counter);
   // the slots a warp leaves unused at exit are written as kNoRow holes
   unsigned qbase = 0, qleft = 0;
+  auto append = [&](bool want, std::uint32_t row, float reach) {
+    const unsigned mc = __ballot_sync(0xffffffffu, want);
+    const unsigned nc = __popc(mc);
+    if (!nc) return;
+    unsigned nbase = 0;
+    if (lane == 0 && nc > qleft) nbase = atomicAdd(ncand, kQChunk);
+    nbase = __shfl_sync(0xffffffffu, nbase, 0);
+    const unsigned rank = __popc(mc & lt);
+    const unsigned q = rank < qleft ? qbase + rank : nbase + (rank - qleft);
+    if (nc > qleft) {  // the current chunk is used up, the rest goes to the new one
+      qbase = nbase + (nc - qleft);
+      qleft = kQChunk - (nc - qleft);
+    } else {
+      qbase += nc;
+      qleft -= nc;
+    }
+    if (want) {
+      cand[q] = row;
+      cand[cap + q] = __float_as_uint(reach);
+    }
+  };
+  // Undecided rows wait in a per-warp batch (shared memory) until 32 have
+  // gathered; then every lane takes one and runs the binary32 neighbour
+  // proofs (foreign mask / near-octant codes) converged, and only the rows
+  // they leave open go to the exact stage's queue.
+  std::uint32_t(&B)[D + 4][kPfBatch] = s_bat[threadIdx.x >> 5];  // {row, self, reach, rout, U[D]}
+  unsigned bcount = 0;
+  auto flush_batch = [&](unsigned nproc) {
+    __syncwarp();
+    const unsigned e = bcount - nproc + lane;
+    bool to_q = false;
+    std::uint32_t row = 0;
+    float reach = -1.f;
+    if (lane < nproc) {
+      row = B[0][e];
+      reach = __uint_as_float(B[2][e]);
+      const float rout = __uint_as_float(B[3][e]);
+      int r = -1;
+      if (reach > 0.f || rout >= -1.f) {
+        float U[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) U[d] = __uint_as_float(B[4 + d][e]);
+        if (rout >= -1.f) r = exact_mask_test<D>(og, a, U, reach, rout);
+        else r = octant_proof<D>(og, a, U, reach, B[1][e]) ? 1 : -1;
+      }
+      if (r >= 0) {
+        __stcs(a.positive + row, static_cast<std::uint8_t>(r));
+        if (r == 1)
+#pragma unroll
+          for (int j = 0; j <= D; ++j) a.vflags[__ldg(a.verts + std::uint64_t(j) * a.S + row)] = 1;
+        if (a.counters) atomicAdd(&a.counters[r == 1 ? 10 : 15], 1ull);
+      } else {
+        to_q = true;
+        if (reach > 0.f) reach = -1.f;  // the exact stage only needs the kReachCheckOrient marker
+      }
+    }
+    bcount -= nproc;
+    __syncwarp();
+    append(to_q, row, reach);
+  };
   while (base < row_end) {
     const bool valid = s < row_end;
     std::uint32_t v[D + 1];
@@ -865,7 +927,7 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
     load_ids(s_next, vn);
     const bool inf = valid && v[D] == kInfVertex;
     bool is_cand = false;
-    float cU[D], creach = -1.f, crout = kRoutNoMask;  // recorded for the exact stage's first tests
+    float cU[D], creach = -1.f, crout = kRoutNoMask;  // recorded for the neighbour proofs
     // a warp's rows only grow (claims are monotonic): advance the part cursor
     {
       const std::uint64_t sc = valid ? s : row_end - 1;
@@ -897,35 +959,31 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
           for (int j = 0; j <= D; ++j) a.vflags[v[j]] = 1;
       }
     }
-    // warp-aggregated queue appends
-    const unsigned mc = __ballot_sync(0xffffffffu, is_cand);
-    const unsigned mi = __ballot_sync(0xffffffffu, inf);
-    const unsigned nc = __popc(mc);
-    unsigned nbase = 0, bi = 0;
-    if (lane == 0) {
-      if (nc > qleft) nbase = atomicAdd(ncand, kQChunk);
-      if (mi) bi = atomicAdd(a.inf_count, static_cast<unsigned>(__popc(mi)));
-    }
-    nbase = __shfl_sync(0xffffffffu, nbase, 0);
-    bi = __shfl_sync(0xffffffffu, bi, 0);
-    const unsigned rank = __popc(mc & lt);
-    const unsigned q = rank < qleft ? qbase + rank : nbase + (rank - qleft);
-    if (nc > qleft) {  // the current chunk is used up, the rest goes to the new one
-      qbase = nbase + (nc - qleft);
-      qleft = kQChunk - (nc - qleft);
-    } else {
-      qbase += nc;
-      qleft -= nc;
-    }
-    if (is_cand) {
-      cand[q] = static_cast<std::uint32_t>(s);
-      cand[std::uint64_t(D + 1) * cap + q] = __float_as_uint(creach);
-      cand[std::uint64_t(D + 2) * cap + q] = __float_as_uint(crout);
-      if (creach > 0.f || crout >= -1.f)
+    // undecided rows into the warp's batch
+    {
+      const unsigned mb = __ballot_sync(0xffffffffu, is_cand);
+      if (is_cand) {
+        const unsigned slot = bcount + __popc(mb & lt);
+        B[0][slot] = static_cast<std::uint32_t>(s);
+        B[1][slot] = self;
+        B[2][slot] = __float_as_uint(creach);
+        B[3][slot] = __float_as_uint(crout);
 #pragma unroll
-        for (int d = 0; d < D; ++d) cand[std::uint64_t(1 + d) * cap + q] = __float_as_uint(cU[d]);
+        for (int d = 0; d < D; ++d) B[4 + d][slot] = __float_as_uint(cU[d]);
+      }
+      bcount += __popc(mb);
+      if (bcount >= 32) flush_batch(32);
     }
-    if (inf) a.inf_queue[bi + __popc(mi & lt)] = static_cast<std::uint32_t>(s);
+    // hull rows
+    {
+      const unsigned mi = __ballot_sync(0xffffffffu, inf);
+      if (mi) {
+        unsigned bi = 0;
+        if (lane == 0) bi = atomicAdd(a.inf_count, static_cast<unsigned>(__popc(mi)));
+        bi = __shfl_sync(0xffffffffu, bi, 0);
+        if (inf) a.inf_queue[bi + __popc(mi & lt)] = static_cast<std::uint32_t>(s);
+      }
+    }
     s = s_next;
     if (++it == kPfIters) {  // CTA-uniform
       it = 0;
@@ -936,6 +994,7 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
       next_base = row_begin + s_claim;
     }
   }
+  if (bcount) flush_batch(bcount);
   for (unsigned i = lane; i < qleft; i += 32) cand[qbase + i] = kNoRow;
   if (a.counters && lane == 0 && qleft) atomicAdd(&a.counters[11], static_cast<unsigned long long>(qleft));
 }
@@ -1023,33 +1082,8 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
       self = s_off.part(a.k, s);
 #pragma unroll
       for (int j = 0; j <= D; ++j) v[j] = __ldg(a.verts + std::uint64_t(j) * a.S + s);
-      bool proven = false, refuted = false;
-      if constexpr (!Ex) {
-        // binary32 proofs from the prefilter's record (cell-unit centre U,
-        // inner-ball reach, outer radius): the foreign mask of the centre
-        // cell when it applies, else the near-octant neighbours' codes
-        const float reach = __uint_as_float(cand[std::uint64_t(D + 1) * cap + t]);
-        const float rout = __uint_as_float(cand[std::uint64_t(D + 2) * cap + t]);
-        if (reach > 0.f || rout >= -1.f) {
-          float U[D];
-#pragma unroll
-          for (int d = 0; d < D; ++d) U[d] = __uint_as_float(cand[std::uint64_t(1 + d) * cap + t]);
-          if (rout >= -1.f) {
-            const int m = exact_mask_test<D>(og, a, U, reach, rout);
-            proven = m == 1;
-            refuted = m == 0;
-          } else {
-            proven = octant_proof<D>(og, a, U, reach, self);
-          }
-        }
-      }
-      if (refuted) {
-        mode = 0;
-        if (a.counters) atomicAdd(&a.counters[15], 1ull);
-      } else if (proven) {
-        mode = 0;
-        pre_pos = true;
-      } else {
+      // (the binary32 neighbour proofs ran in the prefilter's batches)
+      {
         double p[D + 1][D];
         load_simplex<D>(a, v, p);
         circumsphere_inflated<D>(p, c, &r2);
@@ -1249,7 +1283,7 @@ __global__ void __launch_bounds__(256) k_border_orient(BorderArgs a, const std::
   const unsigned ncand = *ncand_p;
   for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < ncand; t += gridDim.x * blockDim.x) {
     if (cand[t] == kNoRow) continue;
-    if (__uint_as_float(cand[std::uint64_t(D + 1) * cap + t]) != kReachCheckOrient) continue;
+    if (__uint_as_float(cand[cap + t]) != kReachCheckOrient) continue;
     std::uint32_t v[D + 1];
 #pragma unroll
     for (int j = 0; j <= D; ++j) v[j] = __ldg(a.verts + std::uint64_t(j) * a.S + cand[t]);
@@ -2130,7 +2164,7 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
         // candidates <= rows, plus < kQChunk holes per prefilter warp and launch
         const std::uint64_t launches_A = ctx->chunks.empty() ? 1 : ctx->chunks.size();
         const std::uint64_t qcap = in->S + 32 + launches_A * resA * (kBThreads / 32) * kQChunk;
-        SBDT_WS(cq, std::uint32_t, "border.cand", qcap * (D + 3));  // SoA {row, U[D], reach, rout}
+        SBDT_WS(cq, std::uint32_t, "border.cand", qcap * 2);  // SoA {row, reach (kReachCheckOrient marker)}
         // {candidates, cursor, wide rows, wide cursor, CTAs done (exact), CTAs done (wide)}
         // {candidates, cursor, wide rows, wide cursor, CTAs done (exact), CTAs done (wide), light wide rows}
         SBDT_WS(cn, unsigned, "border.cand_n", 8);

@@ -518,8 +518,11 @@ __global__ void __launch_bounds__(kFieldThreads) k_field_tiles(const OwnerGrid<D
           t[d] = oo2 % T + H;
           oo2 /= T;
         }
+        // hs >= 2: the 3^D window holds at most one code (the word's), so no
+        // neighbour is foreign to it
         std::uint32_t m = 0;
-        if constexpr (D == 3) {
+        if ((w >> 24) >= 2u) {
+        } else if constexpr (D == 3) {
 #pragma unroll
           for (int j = 0; j < 27; ++j) {
             const std::uint16_t nc = raw[(t[0] + j % 3 - 1) + RS * ((t[1] + (j / 3) % 3 - 1) + RS * (t[2] + j / 9 - 1))];

@@ -184,8 +184,8 @@ class Context:
             return {}
         keys = {0: "rows", 1: "exact_stage_rows", 2: "exact_flat_scan", 3: "wide_two_level", 4: "wide_pyramid",
                 5: "row_pairs", 6: "wide_expansions", 7: "exact_flat_positive", 8: "prefilter_positive",
-                9: "wide_positive", 12: "orient_check_rows", 13: "orient_escalations", 14: "in_sphere_escalations",
-                15: "exact_mask_negative"}
+                9: "wide_positive", 10: "mask_positive", 12: "orient_check_rows", 13: "orient_escalations",
+                14: "in_sphere_escalations", 15: "mask_negative"}
         return {kk: int(out[i]) for i, kk in keys.items()}
 
     # ---- diagnostics (tests / bench): device predicates, binding ceilings
