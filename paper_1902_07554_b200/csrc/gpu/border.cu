@@ -25,6 +25,7 @@
 #include "common.cuh"
 #include "context.cuh"
 #include "owner_grid.cuh"
+#include "../common/plane_filter.hpp"
 #include "scan.cuh"
 #include "sbdt_gpu.h"
 
@@ -399,8 +400,7 @@ struct BorderArgs {
   std::uint64_t S;
   int policy;
   const std::uint16_t* owner;
-  const std::uint32_t* field;  // window field of the prefilter (k_field_tiles), linear over ldims[0]
-  const std::uint32_t* fmask;  // foreign masks of the 3^D windows (k_field_tiles), linear over ldims[0]
+  const std::uint64_t* field;  // window field + foreign mask per cell (k_field_tiles), linear over ldims[0]
   const unsigned long long* pbbox;  // [k][2D] ordered (bbox policy)
   std::uint8_t* positive;
   std::uint8_t* vflags;
@@ -584,7 +584,7 @@ __device__ __forceinline__ void load_simplex(const BorderArgs& a, const std::uin
 // shared OwnerGrid: the hot loop reads them every row).
 template <int D>
 struct PfConst {
-  const std::uint32_t* field;  // window field (k_field_tiles), linear over ldims[0]
+  const std::uint64_t* field;  // window field + foreign mask (k_field_tiles), linear over ldims[0]
   int ctop[D];                 // kFloorBias + ldims[0][d] - 1
   unsigned dim0, dim1;         // ldims[0][0], ldims[0][1] (linear index)
   float inv_e, margin_c, lo_mag;
@@ -595,6 +595,12 @@ struct PfConst {
 // centre cell's field code is not the row's part, or the centre is outside
 // the grid); -1: it applies for positive proofs only (range wider than 3^D)
 constexpr float kRoutNoMask = -2.f;
+// prefilter's half-width of the conservative cell range around its centre
+// cell, unknown (range beyond binary32 floor reach): such rows and those
+// with need > kFlatHalf go straight to the wide queue
+constexpr int kNeedUnknown = 1 << 20;
+constexpr int kFlatHalf = 3;      // need <= 3: every axis spans <= 7 cells (the flattened scan)
+constexpr int kWideHeavyNeed = 8;  // need > 8: spans > 17 cells, the pyramid rows (queued first)
 
 // floor_small(x) + kFloorBias: the bits of x + 1.5 * 2^23 rounded down
 constexpr int kFloorBias = 0x4B400000;
@@ -613,9 +619,11 @@ constexpr int kFloorBias = 0x4B400000;
 // the exact stage's neighbour test (octant_proof).
 template <int D>
 __device__ __forceinline__ int prefilter_decide(const PfConst<D>& pc, const Sphere32<D>& sp, std::uint32_t self,
-                                                float* out_U, float* out_reach, float* out_rout) {
+                                                float* out_U, float* out_reach, float* out_rout,
+                                                std::uint32_t* out_mask, int* out_need) {
   *out_reach = -1.f;
   *out_rout = kRoutNoMask;
+  *out_need = kNeedUnknown;
   // R >= radius of the inflated binary64 sphere + distance between centres
   float slack = 0.f;
 #pragma unroll
@@ -645,13 +653,16 @@ __device__ __forceinline__ int prefilter_decide(const PfConst<D>& pc, const Sphe
     need = max(need, max(cc - a, b - cc));
     cb[d] = cc - kFloorBias;
   }
+  *out_need = need;
   unsigned long long li;
   if constexpr (D == 3)
     li = static_cast<unsigned long long>(static_cast<unsigned>(cb[1]) + pc.dim1 * static_cast<unsigned>(cb[2])) * pc.dim0 +
          static_cast<unsigned>(cb[0]);
   else
     li = static_cast<unsigned long long>(static_cast<unsigned>(cb[1])) * pc.dim0 + static_cast<unsigned>(cb[0]);
-  const std::uint32_t fw = __ldg(pc.field + li);
+  const std::uint64_t f64 = __ldg(pc.field + li);
+  const std::uint32_t fw = static_cast<std::uint32_t>(f64);
+  *out_mask = static_cast<std::uint32_t>(f64 >> 32);
   const std::uint32_t code = fw & 0xFFFFu;
   if (code == self && need < static_cast<int>(fw >> 24)) return 0;
   if (!inside) return 2;
@@ -728,7 +739,7 @@ __device__ __forceinline__ bool octant_proof(const OwnerGrid<D>& og, const Borde
     unsigned long long li = static_cast<unsigned>(cn[D - 1]);
 #pragma unroll
     for (int d = D - 2; d >= 0; --d) li = li * static_cast<unsigned>(og.ldims[0][d]) + static_cast<unsigned>(cn[d]);
-    fw[k - 1] = (ok && d2 * 1.000002f + 1e-12f < reach2) ? __ldg(a.field + li) : kFieldEmptyBit;
+    fw[k - 1] = (ok && d2 * 1.000002f + 1e-12f < reach2) ? static_cast<std::uint32_t>(__ldg(a.field + li)) : kFieldEmptyBit;
   }
   bool hit = false;
 #pragma unroll
@@ -736,7 +747,7 @@ __device__ __forceinline__ bool octant_proof(const OwnerGrid<D>& og, const Borde
   return hit;
 }
 
-// The centre cell's foreign mask (k_field_tiles; the row's part is the
+// The centre cell's foreign mask m (k_field_tiles; the row's part is the
 // cell's field code, checked by the prefilter): 1 if the inner ball (reach,
 // all error slack already subtracted) reaches the box of a foreign
 // neighbour, 0 if the outer ball (rout > 0: radius in cell units with every
@@ -745,22 +756,15 @@ __device__ __forceinline__ bool octant_proof(const OwnerGrid<D>& og, const Borde
 // c0 = floor(U): per axis the gap to the neighbour at offset -1, 0, +1 is
 // f, 0, 1 - f (f = U - c0).
 template <int D>
-__device__ __forceinline__ int exact_mask_test(const OwnerGrid<D>& og, const BorderArgs& a, const float* U, float reach,
-                                               float rout) {
-  int c0[D];
+__device__ __forceinline__ int exact_mask_test(const std::uint32_t m, const float* U, float reach, float rout) {
   float g[D][3];
 #pragma unroll
   for (int d = 0; d < D; ++d) {
-    c0[d] = floor_small(U[d]);
-    const float f = U[d] - static_cast<float>(c0[d]);  // exact
+    const float f = U[d] - static_cast<float>(floor_small(U[d]));  // exact
     g[d][0] = f * f;
     g[d][1] = 0.f;
     g[d][2] = (1.f - f) * (1.f - f);
   }
-  unsigned long long li = static_cast<unsigned>(c0[D - 1]);
-#pragma unroll
-  for (int d = D - 2; d >= 0; --d) li = li * static_cast<unsigned>(og.ldims[0][d]) + static_cast<unsigned>(c0[d]);
-  const std::uint32_t m = __ldg(a.fmask + li);
   if (!m) return rout > 0.f ? 0 : -1;
   float mn = INFINITY;  // smallest squared box distance over the foreign neighbours
   if constexpr (D == 3) {
@@ -786,22 +790,27 @@ __device__ __forceinline__ int exact_mask_test(const OwnerGrid<D>& og, const Bor
   return -1;
 }
 
-// Rows are claimed by CTAs in chunks of kPfChunk from a launch-wide cursor
-// (instead of a static grid-stride split): every CTA works on the same
-// sliding window of rows, so the packed-coordinate lines and owner codes of
+// Rows are claimed by warps in chunks of kPfChunk from a launch-wide cursor
+// (instead of a static grid-stride split): every warp works on the same
+// sliding window of rows, so the packed-coordinate lines and field words of
 // the 1-2 partitions in flight stay in L2 instead of spreading over the rows
-// of CTAs that drifted apart, and the CTA's warps take consecutive 32-row
-// slices of its chunk (vertices shared by neighbouring rows hit in L1).
+// of warps that drifted apart, and a lane's consecutive rows are 32 apart
+// (vertices shared by neighbouring rows hit in L1).
 constexpr unsigned kPfIters = 16;
 constexpr unsigned kPfBatch = 64;  // per-warp batch of undecided rows (< 32 waiting + 32 arriving)
-constexpr unsigned kPfChunk = kBThreads * kPfIters;
+template <int D>
+constexpr int kPfBatchWords = 2 * D + 7;
+constexpr unsigned kPfChunk = 32 * kPfIters;
 
 template <int D, bool BIGK>
 __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
                                                                 std::uint32_t* __restrict__ cand, std::uint64_t cap,
                                                                 unsigned* __restrict__ ncand, std::uint64_t row_begin,
                                                                 std::uint64_t row_end,
-                                                                unsigned long long* __restrict__ cursor) {
+                                                                unsigned long long* __restrict__ cursor,
+                                                                std::uint32_t* __restrict__ wq, std::uint64_t wcap,
+                                                                unsigned* __restrict__ nwide,
+                                                                unsigned* __restrict__ nwlight) {
   __shared__ OwnerGrid<D> og;
   extern __shared__ std::uint64_t s_off_sh[];
   if (threadIdx.x == 0) og = *ogp;
@@ -812,15 +821,16 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
   const std::uint64_t* s_off = BIGK ? a.offsets : s_off_sh;
   const unsigned lane = threadIdx.x & 31u;
   const unsigned lt = (1u << lane) - 1u;
-  // rows [row_begin, row_end); the whole CTA iterates over claimed chunks,
-  // with one chunk of lookahead for the id prefetch
-  __shared__ std::uint32_t s_bat[kBThreads / 32][D + 4][kPfBatch];
-  __shared__ unsigned long long s_claim;
-  if (threadIdx.x == 0) s_claim = atomicAdd(cursor, 2ull * kPfChunk);
-  __syncthreads();
-  std::uint64_t base = row_begin + s_claim;
+  // rows [row_begin, row_end); every warp iterates over its own claimed
+  // chunks (no CTA barrier: the batch flushes make warps uneven), with one
+  // chunk of lookahead for the id prefetch
+  __shared__ std::uint32_t s_bat[kBThreads / 32][kPfBatchWords<D>][kPfBatch];
+  unsigned long long claim = 0;
+  if (lane == 0) claim = atomicAdd(cursor, 2ull * kPfChunk);
+  claim = __shfl_sync(0xffffffffu, claim, 0);
+  std::uint64_t base = row_begin + claim;
   std::uint64_t next_base = base + kPfChunk;
-  const unsigned wofs = threadIdx.x & ~31u;  // this warp's slice of a 256-row step
+  constexpr unsigned wofs = 0;
   unsigned it = 0;
   // binary32 cell-unit scale and margin (rounded up; the slacks cover the rest)
   // decode_row's coordinate unit: the fixed-point step in 3-D, 1 in 2-D
@@ -881,12 +891,13 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
   // gathered; then every lane takes one and runs the binary32 neighbour
   // proofs (foreign mask / near-octant codes) converged, and only the rows
   // they leave open go to the exact stage's queue.
-  std::uint32_t(&B)[D + 4][kPfBatch] = s_bat[threadIdx.x >> 5];  // {row, self, reach, rout, U[D]}
+  // {row, self, reach, rout, mask, U[D], vertex ids[D + 1], need}
+  std::uint32_t(&B)[kPfBatchWords<D>][kPfBatch] = s_bat[threadIdx.x >> 5];
   unsigned bcount = 0;
   auto flush_batch = [&](unsigned nproc) {
     __syncwarp();
     const unsigned e = bcount - nproc + lane;
-    bool to_q = false;
+    bool to_q = false, to_w = false;
     std::uint32_t row = 0;
     float reach = -1.f;
     if (lane < nproc) {
@@ -897,19 +908,43 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
       if (reach > 0.f || rout >= -1.f) {
         float U[D];
 #pragma unroll
-        for (int d = 0; d < D; ++d) U[d] = __uint_as_float(B[4 + d][e]);
-        if (rout >= -1.f) r = exact_mask_test<D>(og, a, U, reach, rout);
+        for (int d = 0; d < D; ++d) U[d] = __uint_as_float(B[5 + d][e]);
+        if (rout >= -1.f) r = exact_mask_test<D>(B[4][e], U, reach, rout);
         else r = octant_proof<D>(og, a, U, reach, B[1][e]) ? 1 : -1;
       }
       if (r >= 0) {
         __stcs(a.positive + row, static_cast<std::uint8_t>(r));
         if (r == 1)
 #pragma unroll
-          for (int j = 0; j <= D; ++j) a.vflags[__ldg(a.verts + std::uint64_t(j) * a.S + row)] = 1;
+          for (int j = 0; j <= D; ++j) a.vflags[B[5 + D + j][e]] = 1;
         if (a.counters) atomicAdd(&a.counters[r == 1 ? 10 : 15], 1ull);
+      } else if (reach != kReachCheckOrient && static_cast<int>(B[6 + 2 * D][e]) > kFlatHalf) {
+        to_w = true;  // wide cell range: the pyramid descent (k_border_wide), next to the exact stage
       } else {
         to_q = true;
         if (reach > 0.f) reach = -1.f;  // the exact stage only needs the kReachCheckOrient marker
+      }
+    }
+    // wide rows: {row, vertex ids}, heavy ones from the front of the queue,
+    // the others from the back when the queue is split (device path)
+    {
+      const bool heavy = to_w && (!nwlight || static_cast<int>(B[6 + 2 * D][e]) > kWideHeavyNeed);
+      const bool light = to_w && !heavy;
+      const unsigned mh = __ballot_sync(0xffffffffu, heavy), ml = __ballot_sync(0xffffffffu, light);
+      if (mh | ml) {
+        unsigned hb = 0, lb = 0;
+        if (lane == 0) {
+          if (mh) hb = atomicAdd(nwide, static_cast<unsigned>(__popc(mh)));
+          if (ml) lb = atomicAdd(nwlight, static_cast<unsigned>(__popc(ml)));
+        }
+        hb = __shfl_sync(0xffffffffu, hb, 0);
+        lb = __shfl_sync(0xffffffffu, lb, 0);
+        if (to_w) {
+          const std::uint64_t q = heavy ? hb + __popc(mh & lt) : wcap - 1 - (lb + __popc(ml & lt));
+          wq[q] = row;
+#pragma unroll
+          for (int j = 0; j <= D; ++j) wq[std::uint64_t(j + 1) * wcap + q] = B[5 + D + j][e];
+        }
       }
     }
     bcount -= nproc;
@@ -923,11 +958,13 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
 #pragma unroll
     for (int j = 0; j <= D; ++j) v[j] = vn[j];
     // the next row of this lane: the next 32 of the chunk, or the lookahead chunk
-    const std::uint64_t s_next = it + 1 < kPfIters ? s + kBThreads : next_base + wofs + lane;
+    const std::uint64_t s_next = it + 1 < kPfIters ? s + 32 : next_base + wofs + lane;
     load_ids(s_next, vn);
     const bool inf = valid && v[D] == kInfVertex;
     bool is_cand = false;
     float cU[D], creach = -1.f, crout = kRoutNoMask;  // recorded for the neighbour proofs
+    std::uint32_t cmask = 0;
+    int cneed = kNeedUnknown;
     // a warp's rows only grow (claims are monotonic): advance the part cursor
     {
       const std::uint64_t sc = valid ? s : row_end - 1;
@@ -946,7 +983,7 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
       // with the exact orientation in the exact stage (kReachCheckOrient)
       int res = 2;
       if (enclosing_sphere_f32<D>(A, eta, P0e, sp))
-        res = prefilter_decide<D>(pc, sp, self, cU, &creach, &crout);
+        res = prefilter_decide<D>(pc, sp, self, cU, &creach, &crout, &cmask, &cneed);
       else
         creach = kReachCheckOrient;
       if (a.counters && res == 1) atomicAdd(&a.counters[8], 1ull);
@@ -968,8 +1005,12 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
         B[1][slot] = self;
         B[2][slot] = __float_as_uint(creach);
         B[3][slot] = __float_as_uint(crout);
+        B[4][slot] = cmask;
+        B[6 + 2 * D][slot] = static_cast<std::uint32_t>(cneed);
 #pragma unroll
-        for (int d = 0; d < D; ++d) B[4 + d][slot] = __float_as_uint(cU[d]);
+        for (int d = 0; d < D; ++d) B[5 + d][slot] = __float_as_uint(cU[d]);
+#pragma unroll
+        for (int j = 0; j <= D; ++j) B[5 + D + j][slot] = v[j];
       }
       bcount += __popc(mb);
       if (bcount >= 32) flush_batch(32);
@@ -985,13 +1026,12 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
       }
     }
     s = s_next;
-    if (++it == kPfIters) {  // CTA-uniform
+    if (++it == kPfIters) {  // warp-uniform
       it = 0;
-      __syncthreads();  // every thread has read s_claim
-      if (threadIdx.x == 0) s_claim = atomicAdd(cursor, static_cast<unsigned long long>(kPfChunk));
-      __syncthreads();
+      unsigned long long c2 = 0;
+      if (lane == 0) c2 = atomicAdd(cursor, static_cast<unsigned long long>(kPfChunk));
       base = next_base;
-      next_base = row_begin + s_claim;
+      next_base = row_begin + __shfl_sync(0xffffffffu, c2, 0);
     }
   }
   if (bcount) flush_batch(bcount);
@@ -1092,13 +1132,8 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
     }
     bool pos = pre_pos;
     if (a.counters) {
-      const unsigned m1 = __ballot_sync(full, mode == 1), m2 = __ballot_sync(full, mode == 2),
-                     m3 = __ballot_sync(full, mode == 3);
-      if (lane == 0) {
-        if (m1) atomicAdd(&a.counters[2], static_cast<unsigned long long>(__popc(m1)));
-        if (m2) atomicAdd(&a.counters[3], static_cast<unsigned long long>(__popc(m2)));
-        if (m3) atomicAdd(&a.counters[4], static_cast<unsigned long long>(__popc(m3)));
-      }
+      const unsigned m1 = __ballot_sync(full, mode == 1);
+      if (lane == 0 && m1) atomicAdd(&a.counters[2], static_cast<unsigned long long>(__popc(m1)));
     }
     {
       // forward wide ranges. With nlight, the pyramid rows (mode 3: the
@@ -1214,7 +1249,7 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
               double d2 = r.g2[0][i0] + g12;
               if constexpr (D == 3) d2 += g2z;
               geo[i0] = d2 <= rr;
-              if (geo[i0]) fw[i0] = __ldg(a.field + lb + i0);
+              if (geo[i0]) fw[i0] = static_cast<std::uint32_t>(__ldg(a.field + lb + i0));
             }
           }
 #pragma unroll
@@ -1623,10 +1658,15 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_border_infinite(BorderArgs 
         auto leaf = [&](const int* cell) -> bool {
           return cell_points_outside<D>(a, og_index<D>(og, 0, cell), facet, sl_sign, sl_self);
         };
+        sbdt_pred::PlaneFilter<D> pf;
+        sbdt_pred::plane_filter_init<D>(pf, facet, sl_sign);
         auto test = [&](int L, const int* cc) -> int {
           double blo[D], bhi[D];
           og_block_box<D>(og, L, cc, blo, bhi);
-          const int out = corners_outside<D>(facet, sl_sign, blo, bhi, pesc);
+          // all corners at once through the facet's plane with its error
+          // bound; the exact per-corner orient only when that is undecided
+          const int f = sbdt_pred::plane_filter_box<D>(pf, blo, bhi);
+          const int out = f >= 0 ? (f == 0 ? 0 : (f == 2 ? (1 << D) : 1)) : corners_outside<D>(facet, sl_sign, blo, bhi, pesc);
           if (out == 0) return 0;
           if (out == (1 << D)) return 2;  // the whole box is strictly outside
           if (L > 0) return 1;
@@ -1881,10 +1921,12 @@ __global__ void k_border_spheres(BorderArgs a) {
   }
 }
 
-__global__ void k_cand_count(const unsigned* ncand, std::uint64_t S, unsigned long long* counters,
-                             const unsigned* esc_count, unsigned esc_cap) {
+__global__ void k_cand_count(const unsigned* ncand, const unsigned* npf_wide, std::uint64_t S,
+                             unsigned long long* counters, const unsigned* esc_count, unsigned esc_cap) {
   counters[0] = S;  // rows scanned by the prefilter (finite + infinite)
-  counters[1] = *ncand - counters[11];  // queue slots minus the holes
+  counters[1] = ncand[0] - counters[11];  // queue slots minus the holes
+  counters[3] = ncand[2] + ncand[6];      // wide rows forwarded by the exact stage
+  counters[4] = npf_wide[0] + npf_wide[3];  // wide rows routed by the prefilter
   // exact policy: (row, point) in_sphere tests the filter left undecided
   counters[kCtrInSphereExact] = esc_count ? min(*esc_count, esc_cap) : 0u;
 }
@@ -2035,20 +2077,17 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
     cell_start = cstart;
     cell_pts = cpts;
   }
-  std::uint32_t* field = nullptr;
-  std::uint32_t* fmask = nullptr;
+  std::uint64_t* field = nullptr;
   if (tiled) {
-    SBDT_WS(fw, std::uint32_t, "border.field", cap + 1);  // level-0 cells <= cap
-    SBDT_WS(fm, std::uint32_t, "border.fmask", cap + 1);
+    SBDT_WS(fw, std::uint64_t, "border.field", cap + 1);  // level-0 cells <= cap
     field = fw;
-    fmask = fm;
     static bool attr_set[2] = {false, false};
     if (!attr_set[D - 2]) {
       SBDT_CUDA_TRY(cudaFuncSetAttribute(k_field_tiles<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(field_smem_bytes<D>())));
       attr_set[D - 2] = true;
     }
-    k_field_tiles<D><<<sms * 3, kFieldThreads, field_smem_bytes<D>(), st>>>(og, owner, field, fmask);
+    k_field_tiles<D><<<sms * 3, kFieldThreads, field_smem_bytes<D>(), st>>>(og, owner, field);
     ctx->launches += 1;
   }
   ctx->launches += 6;
@@ -2069,7 +2108,6 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   a.policy = in->policy;
   a.owner = owner;
   a.field = field;
-  a.fmask = fmask;
   a.pbbox = pbbox;
   a.positive = in->d_positive;
   a.vflags = in->d_vertex_flags;
@@ -2174,6 +2212,14 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
         unsigned* nlight = ctx->chunks.empty() ? cn + 6 : nullptr;
         const std::uint64_t wcap = qcap;  // wide rows <= candidates
         SBDT_WS(wq, std::uint32_t, "border.wide", wcap * (D + 2));
+        // rows the prefilter routes to the pyramid descent directly (range
+        // wider than the flattened scan's): {row, vertex ids}, counters
+        // {heavy rows, cursor, CTAs done, light rows}
+        const std::uint64_t pcap = in->S + 64;
+        SBDT_WS(pq, std::uint32_t, "border.pf_wide", pcap * (D + 2));
+        SBDT_WS(pn, unsigned, "border.pf_wide_n", 4);
+        SBDT_CUDA_TRY(cudaMemsetAsync(pn, 0, 4 * sizeof(unsigned), st));
+        unsigned* pnlight = ctx->chunks.empty() ? pn + 3 : nullptr;
         if (exact_policy)
           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_exact<D, true>, kExactWarps * 32, offs_sh);
         else
@@ -2190,10 +2236,10 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
           SBDT_CUDA_TRY(cudaMemsetAsync(pfcur, 0, sizeof(unsigned long long), st));
           if (bigk)
             k_border_prefilter<D, true><<<static_cast<unsigned>(want < resA ? want : resA), kBThreads, 0, st>>>(
-                a, og, cq, qcap, cn, r0, r1, pfcur);
+                a, og, cq, qcap, cn, r0, r1, pfcur, pq, pcap, pn, pnlight);
           else
             k_border_prefilter<D, false><<<static_cast<unsigned>(want < resA ? want : resA), kBThreads, offs_sh, st>>>(
-                a, og, cq, qcap, cn, r0, r1, pfcur);
+                a, og, cq, qcap, cn, r0, r1, pfcur, pq, pcap, pn, pnlight);
           return kOk;
         };
         auto exact = [&]() {
@@ -2204,13 +2250,18 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
             k_border_exact<D, false><<<resX, kExactWarps * 32, offs_sh, st>>>(a, og, cq, qcap, cn, cn + 1, wq, cn + 2,
                                                                              cn + 4, nlight);
         };
-        auto wide = [&]() {
+        // the exact stage's forwarded rows (wq), or the prefilter's (pq)
+        auto wide = [&](bool from_pf, cudaStream_t on) {
+          std::uint32_t* q = from_pf ? pq : wq;
+          const std::uint64_t qc = from_pf ? pcap : wcap;
+          unsigned* nh = from_pf ? pn : cn + 2;
+          unsigned* cur = from_pf ? pn + 1 : cn + 3;
+          unsigned* fin = from_pf ? pn + 2 : cn + 5;
+          unsigned* nl = from_pf ? pnlight : nlight;
           if (exact_policy)
-            k_border_wide<D, true><<<resW, kWideWarps * 32, offs_sh, st>>>(a, og, wq, wcap, cn + 2, cn + 3, cn + 5,
-                                                                          nlight);
+            k_border_wide<D, true><<<resW, kWideWarps * 32, offs_sh, on>>>(a, og, q, qc, nh, cur, fin, nl);
           else
-            k_border_wide<D, false><<<resW, kWideWarps * 32, offs_sh, st>>>(a, og, wq, wcap, cn + 2, cn + 3, cn + 5,
-                                                                           nlight);
+            k_border_wide<D, false><<<resW, kWideWarps * 32, offs_sh, on>>>(a, og, q, qc, nh, cur, fin, nl);
         };
         if (ctx->chunks.empty()) {
           {
@@ -2225,7 +2276,14 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
             const int hrc = build_hull_set();
             if (hrc != kOk) return hrc;
           }
-          if (!ctx->side_stream) SBDT_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
+          // the hull-row and wide-row descents are the longest latency-bound
+          // chains after the prefilter: their streams get the highest
+          // priority, so their CTAs are placed first and the exact stage
+          // fills the remaining slots
+          int prio_lo = 0, prio_hi = 0;
+          cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+          if (!ctx->side_stream)
+            SBDT_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->side_stream, cudaStreamNonBlocking, prio_hi));
           if (!ctx->fork_ev) SBDT_CUDA_TRY(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
           if (!ctx->join_ev) SBDT_CUDA_TRY(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
           SBDT_CUDA_TRY(cudaEventRecord(ctx->fork_ev, st));
@@ -2238,16 +2296,27 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
           ++ctx->launches;
           SBDT_CUDA_TRY(cudaEventRecord(ctx->join_ev, ctx->side_stream));
           inf_forked = true;
+          // the prefilter's wide rows on a second side stream, next to the exact stage
+          if (!ctx->wide_stream)
+            SBDT_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->wide_stream, cudaStreamNonBlocking, prio_hi));
+          if (!ctx->wide_join_ev) SBDT_CUDA_TRY(cudaEventCreateWithFlags(&ctx->wide_join_ev, cudaEventDisableTiming));
+          SBDT_CUDA_TRY(cudaStreamWaitEvent(ctx->wide_stream, ctx->fork_ev, 0));
+          {
+            StageTimer tw(ctx, "border.wide", ctx->wide_stream);
+            wide(true, ctx->wide_stream);
+          }
+          SBDT_CUDA_TRY(cudaEventRecord(ctx->wide_join_ev, ctx->wide_stream));
           {
             StageTimer tx(ctx, "border.exact");
             exact();
           }
           {
             StageTimer tw(ctx, "border.exact_wide");
-            wide();
+            wide(false, st);
           }
           SBDT_CUDA_TRY(cudaStreamWaitEvent(st, ctx->join_ev, 0));
-          ctx->launches += 4;
+          SBDT_CUDA_TRY(cudaStreamWaitEvent(st, ctx->wide_join_ev, 0));
+          ctx->launches += 5;
         } else {
           // host path: every chunk of rows as soon as its upload has landed;
           // the exact and wide kernels drain the queues grown so far (their
@@ -2259,9 +2328,10 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
             if (r1 > r0) {
               const int prc = prefilter(r0, r1);
               if (prc != kOk) return prc;
+              wide(true, st);
               exact();
-              wide();
-              ctx->launches += 3;
+              wide(false, st);
+              ctx->launches += 4;
               if (stream_out) {
                 infinite(st);
                 ++ctx->launches;
@@ -2278,7 +2348,7 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
           ++ctx->launches;
         }
         if (a.counters) {
-          k_cand_count<<<1, 1, 0, st>>>(cn, in->S, a.counters, a.esc_count, a.esc_cap);
+          k_cand_count<<<1, 1, 0, st>>>(cn, pn, in->S, a.counters, a.esc_count, a.esc_cap);
           ctx->launches += 1;
         }
       } else if (blocks > 0) {

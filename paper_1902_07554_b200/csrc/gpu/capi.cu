@@ -105,6 +105,8 @@ void sbdt_gpu_destroy(sbdt_gpu_ctx* ctx) {
   if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
   if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
   if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
+  if (ctx->wide_stream) cudaStreamDestroy(ctx->wide_stream);
+  if (ctx->wide_join_ev) cudaEventDestroy(ctx->wide_join_ev);
   for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);

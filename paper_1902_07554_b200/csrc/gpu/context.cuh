@@ -55,6 +55,9 @@ struct sbdt_gpu_ctx {
   // runs on side_stream between fork/join events
   cudaStream_t side_stream = nullptr;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  // the prefilter-routed wide rows (k_border_wide) next to the exact stage
+  cudaStream_t wide_stream = nullptr;
+  cudaEvent_t wide_join_ev = nullptr;
   std::vector<cudaEvent_t> chunk_done;
   // host buffers whose device copies ("h.xyz", "h.lab", "h.bbox") are current
   // (SBDT_BORDER_RESIDENT_POINTS)

@@ -327,7 +327,7 @@ __device__ __forceinline__ std::uint16_t nbr_unpack(std::uint32_t w) {
 //               (0 when the cell itself is MULTI)
 //   bit  16     the cell itself is EMPTY
 //   bits 0-15   the cell's code, or W_{h*}(c) when the cell is EMPTY.
-// and a second u32 per cell, the FOREIGN MASK: bit (dx+1) + 3 (dy+1) [+ 9 (dz+1)]
+// and in the high half of the same u64 the FOREIGN MASK: bit (dx+1) + 3 (dy+1) [+ 9 (dz+1)]
 // set iff the neighbour c + (dx, dy[, dz]) is non-empty with a code other
 // than the word's code (for a row of that code: the foreign cells of the 3^D
 // window; the exact stage's first test, see exact_mask_test).
@@ -374,8 +374,7 @@ constexpr std::size_t field_smem_bytes() {
 template <int D>
 __global__ void __launch_bounds__(kFieldThreads) k_field_tiles(const OwnerGrid<D>* __restrict__ ogp,
                                                                const std::uint16_t* __restrict__ owner,
-                                                               std::uint32_t* __restrict__ field,
-                                                               std::uint32_t* __restrict__ fmask) {
+                                                               std::uint64_t* __restrict__ field) {
   constexpr int F = og_fan<D>();
   constexpr int SH = og_shift<D>();
   constexpr int H = field_h<D>();
@@ -535,8 +534,7 @@ __global__ void __launch_bounds__(kFieldThreads) k_field_tiles(const OwnerGrid<D
             m |= (nc != kOwnerEmpty && nc != own) ? (1u << j) : 0u;
           }
         }
-        field[li] = w;
-        fmask[li] = m;
+        field[li] = static_cast<std::uint64_t>(m) << 32 | w;
       }
     }
     __syncthreads();  // the buffers are reloaded for the next tile

@@ -182,7 +182,7 @@ class Context:
         out = (C.c_ulonglong * 16)()
         if lib().sbdt_gpu_border_stats(self._h, out, 16) != SBDT_OK:
             return {}
-        keys = {0: "rows", 1: "exact_stage_rows", 2: "exact_flat_scan", 3: "wide_two_level", 4: "wide_pyramid",
+        keys = {0: "rows", 1: "exact_stage_rows", 2: "exact_flat_scan", 3: "wide_from_exact", 4: "wide_rows",
                 5: "row_pairs", 6: "wide_expansions", 7: "exact_flat_positive", 8: "prefilter_positive",
                 9: "wide_positive", 10: "mask_positive", 12: "orient_check_rows", 13: "orient_escalations",
                 14: "in_sphere_escalations", 15: "mask_negative"}

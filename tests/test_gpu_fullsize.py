@@ -56,7 +56,7 @@ def _run(cfg, policy, ctx):
                                    bs.border_vertex_ids, policy, THREADS))
     rec = {"config": inst.config["name"], "policy": policy, "n": inst.n, "k": k, "m": len(inst.sample_ids),
            "S": P.S, "threads": THREADS, "parity": res, "assign_table": table,
-           "census": {kk: census.get(kk) for kk in ("rows", "exact_stage_rows", "wide_pyramid", "orient_check_rows",
+           "census": {kk: census.get(kk) for kk in ("rows", "exact_stage_rows", "wide_rows", "orient_check_rows",
                                                     "orient_escalations", "in_sphere_escalations")}}
     print("FULLSIZE " + json.dumps(rec))
     for key in ("positive", "border", "positive_vertices", "border_vertices"):
