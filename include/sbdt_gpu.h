@@ -90,15 +90,20 @@ int sbdt_gpu_stage_times(sbdt_gpu_ctx* ctx, char* names, int names_len, float* m
  * built by the dense pass}. */
 int sbdt_gpu_assign_table_stats(sbdt_gpu_ctx* ctx, unsigned* out6);
 /* Border pipeline census of the last find_border with the census enabled:
- * the first `count` (<= 16) of {rows scanned by the prefilter, rows that
- * reached the exact stage, exact rows by scan kind: flattened cell scan,
- * two-level range (wide), pyramid range (wide), (candidate, cell row) pairs
- * of the flattened scan, wide-stage block expansions, positives of the
- * flattened scan, positives proven by the prefilter, positives of the wide
- * stage, 0, candidate-queue slots left unused (holes of the per-warp chunks),
- * rows whose binary32 sphere failed (exact orientation checked), orientation
- * predicates escalated to expansion arithmetic, in_sphere predicates
- * escalated to expansion arithmetic (exact policy), 0}. */
+ * the first `count` (<= 20) of {0 rows scanned by the prefilter, 1 rows that
+ * reached the binary64 exact stage, 2 of those through its flattened cell
+ * scan, 3 wide rows forwarded by the exact stage, 4 wide rows routed by the
+ * prefilter, 5 (candidate, cell row) pairs of the binary64 flattened scan,
+ * 6 wide-stage block expansions, 7 positives of the binary64 flattened scan,
+ * 8 positives proven by the prefilter's own sphere test, 9 positives of the
+ * wide stage, 10 positives proven by the prefilter's neighbour proofs
+ * (foreign mask / near octant), 11 candidate-queue slots left unused (holes
+ * of the per-warp chunks), 12 rows whose binary32 sphere failed (exact
+ * orientation checked), 13 orientation predicates escalated to expansion
+ * arithmetic, 14 in_sphere predicates escalated to expansion arithmetic
+ * (exact policy), 15 negatives proven by the foreign mask, 16 rows of the
+ * binary32 cell scan, 17 positives of the binary32 cell scan, 18 rows it
+ * left to the binary64 exact stage, 19 0}. */
 int sbdt_gpu_border_stats(sbdt_gpu_ctx* ctx, unsigned long long* out, int count);
 
 /* Page-locked host memory for the host-buffer entry points' inputs and

@@ -620,9 +620,10 @@ constexpr int kFloorBias = 0x4B400000;
 template <int D>
 __device__ __forceinline__ int prefilter_decide(const PfConst<D>& pc, const Sphere32<D>& sp, std::uint32_t self,
                                                 float* out_U, float* out_reach, float* out_rout,
-                                                std::uint32_t* out_mask, int* out_need) {
+                                                std::uint32_t* out_mask, int* out_need, float* out_rp) {
   *out_reach = -1.f;
   *out_rout = kRoutNoMask;
+  *out_rp = -1.f;
   *out_need = kNeedUnknown;
   // R >= radius of the inflated binary64 sphere + distance between centres
   float slack = 0.f;
@@ -670,6 +671,7 @@ __device__ __forceinline__ int prefilter_decide(const PfConst<D>& pc, const Sphe
   // negative proof also needs the range inside the 3^D window around cc
 #pragma unroll
   for (int d = 0; d < D; ++d) out_U[d] = Uc[d];
+  *out_rp = Rp;
   if (code == self) *out_rout = need <= 1 ? Rp : -1.f;
   // Positive proof, in binary32 cell units: cc = floor(Uc) holds Uc, the
   // real centre lies within sqrt(D) sl of Uc, and the cell box in cell units
@@ -799,7 +801,7 @@ __device__ __forceinline__ int exact_mask_test(const std::uint32_t m, const floa
 constexpr unsigned kPfIters = 16;
 constexpr unsigned kPfBatch = 64;  // per-warp batch of undecided rows (< 32 waiting + 32 arriving)
 template <int D>
-constexpr int kPfBatchWords = 2 * D + 7;
+constexpr int kPfBatchWords = 2 * D + 8;
 constexpr unsigned kPfChunk = 32 * kPfIters;
 
 template <int D, bool BIGK>
@@ -810,7 +812,9 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
                                                                 unsigned long long* __restrict__ cursor,
                                                                 std::uint32_t* __restrict__ wq, std::uint64_t wcap,
                                                                 unsigned* __restrict__ nwide,
-                                                                unsigned* __restrict__ nwlight) {
+                                                                unsigned* __restrict__ nwlight,
+                                                                std::uint32_t* __restrict__ sq, std::uint64_t scap,
+                                                                unsigned* __restrict__ nsq) {
   __shared__ OwnerGrid<D> og;
   extern __shared__ std::uint64_t s_off_sh[];
   if (threadIdx.x == 0) og = *ogp;
@@ -891,13 +895,13 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
   // gathered; then every lane takes one and runs the binary32 neighbour
   // proofs (foreign mask / near-octant codes) converged, and only the rows
   // they leave open go to the exact stage's queue.
-  // {row, self, reach, rout, mask, U[D], vertex ids[D + 1], need}
+  // {row, self, reach, rout, mask, U[D], vertex ids[D + 1], need, Rp}
   std::uint32_t(&B)[kPfBatchWords<D>][kPfBatch] = s_bat[threadIdx.x >> 5];
   unsigned bcount = 0;
   auto flush_batch = [&](unsigned nproc) {
     __syncwarp();
     const unsigned e = bcount - nproc + lane;
-    bool to_q = false, to_w = false;
+    bool to_q = false, to_w = false, to_s = false;
     std::uint32_t row = 0;
     float reach = -1.f;
     if (lane < nproc) {
@@ -920,9 +924,27 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
         if (a.counters) atomicAdd(&a.counters[r == 1 ? 10 : 15], 1ull);
       } else if (reach != kReachCheckOrient && static_cast<int>(B[6 + 2 * D][e]) > kFlatHalf) {
         to_w = true;  // wide cell range: the pyramid descent (k_border_wide), next to the exact stage
+      } else if (sq && reach != kReachCheckOrient && __uint_as_float(B[7 + 2 * D][e]) > 0.f) {
+        to_s = true;  // the binary32 cell scan (k_border_scan32)
       } else {
         to_q = true;
         if (reach > 0.f) reach = -1.f;  // the exact stage only needs the kReachCheckOrient marker
+      }
+    }
+    {
+      const unsigned ms = __ballot_sync(0xffffffffu, to_s);
+      if (ms) {
+        unsigned sb = 0;
+        if (lane == 0) sb = atomicAdd(nsq, static_cast<unsigned>(__popc(ms)));
+        sb = __shfl_sync(0xffffffffu, sb, 0);
+        if (to_s) {
+          const std::uint64_t qs = sb + __popc(ms & lt);
+          sq[qs] = row;
+#pragma unroll
+          for (int d = 0; d < D; ++d) sq[std::uint64_t(1 + d) * scap + qs] = B[5 + d][e];
+          sq[std::uint64_t(D + 1) * scap + qs] = B[7 + 2 * D][e];
+          sq[std::uint64_t(D + 2) * scap + qs] = __float_as_uint(reach);
+        }
       }
     }
     // wide rows: {row, vertex ids}, heavy ones from the front of the queue,
@@ -965,6 +987,7 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
     float cU[D], creach = -1.f, crout = kRoutNoMask;  // recorded for the neighbour proofs
     std::uint32_t cmask = 0;
     int cneed = kNeedUnknown;
+    float crp = -1.f;
     // a warp's rows only grow (claims are monotonic): advance the part cursor
     {
       const std::uint64_t sc = valid ? s : row_end - 1;
@@ -983,7 +1006,7 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
       // with the exact orientation in the exact stage (kReachCheckOrient)
       int res = 2;
       if (enclosing_sphere_f32<D>(A, eta, P0e, sp))
-        res = prefilter_decide<D>(pc, sp, self, cU, &creach, &crout, &cmask, &cneed);
+        res = prefilter_decide<D>(pc, sp, self, cU, &creach, &crout, &cmask, &cneed, &crp);
       else
         creach = kReachCheckOrient;
       if (a.counters && res == 1) atomicAdd(&a.counters[8], 1ull);
@@ -1007,6 +1030,7 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
         B[3][slot] = __float_as_uint(crout);
         B[4][slot] = cmask;
         B[6 + 2 * D][slot] = static_cast<std::uint32_t>(cneed);
+        B[7 + 2 * D][slot] = __float_as_uint(crp);
 #pragma unroll
         for (int d = 0; d < D; ++d) B[5 + d][slot] = __float_as_uint(cU[d]);
 #pragma unroll
@@ -1307,6 +1331,201 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
     base = __shfl_sync(full, nclaim, 0);
   }
   rewind_cursor(next, fin, ncand);
+}
+
+// Grid policy, flattened cell scan in binary32 (the rows the prefilter's
+// neighbour proofs left open, cell range <= kFlatSpan per axis): the
+// prefilter's cell-unit centre U, outer radius Rp (every slack included) and
+// inner reach (every slack subtracted) decide each cell of the range from
+// its box distance to U (box [i, i + 1] per axis in cell units, see
+// prefilter_decide): a foreign cell with distance < reach overlaps the
+// binary64 sphere (positive), a cell with distance > Rp cannot; a foreign
+// cell in between (a shell of relative width ~1e-5) sends the row to the
+// binary64 exact stage (k_border_exact). No vertex or coordinate loads for
+// the rows decided here, except the vertex ids of the positive ones.
+// Queue: SoA {row, U[D], Rp, reach}.
+constexpr int kScanWarps = 4;
+
+template <int D>
+struct ScanSlot {
+  float g2[D][kFlatSpan];  // squared box gaps to U per axis and cell of the range
+  float rin2, rout2;       // reach^2 (shrunk) and Rp^2 (grown), cell units
+  int lo[D];
+  unsigned span[D];
+  unsigned inv[D];  // ceil(2^16 / span)
+  unsigned self;
+  unsigned excl;    // first position of this candidate in the flattened stream
+};
+
+template <int D>
+__global__ void __launch_bounds__(kScanWarps * 32) k_border_scan32(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
+                                                                  const std::uint32_t* __restrict__ sq,
+                                                                  std::uint64_t scap,
+                                                                  const unsigned* __restrict__ nsq_p,
+                                                                  unsigned* __restrict__ next,
+                                                                  unsigned* __restrict__ fin,
+                                                                  std::uint32_t* __restrict__ cand,
+                                                                  std::uint64_t cap,
+                                                                  unsigned* __restrict__ ncand) {
+  __shared__ OwnerGrid<D> og;
+  __shared__ ScanSlot<D> slots[kScanWarps][32];
+  __shared__ unsigned char nzl[kScanWarps][32];
+  extern __shared__ std::uint64_t s_off_sh[];
+  if (threadIdx.x == 0) og = *ogp;
+  if (a.k + 1 <= kSmemOffsMax)
+    for (std::uint32_t j = threadIdx.x; j <= a.k; j += blockDim.x) s_off_sh[j] = a.offsets[j];
+  __syncthreads();
+  const PartOffs s_off{s_off_sh, a.offsets, a.k + 1 <= kSmemOffsMax};
+  const unsigned nsq = *nsq_p;
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned lt = (1u << lane) - 1u;
+  const unsigned wid = threadIdx.x >> 5;
+  ScanSlot<D>* sl = slots[wid];
+  unsigned char* nz = nzl[wid];
+  const unsigned full = 0xffffffffu;
+  const unsigned fd0 = static_cast<unsigned>(og.ldims[0][0]), fd1 = static_cast<unsigned>(og.ldims[0][1]);
+  int top[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) top[d] = og.ldims[0][d] - 1;
+  unsigned base = claim_batch(next);
+  for (;;) {
+    if (base >= nsq) break;
+    unsigned nclaim = 0;
+    if (lane == 0) nclaim = atomicAdd(next, 32u);
+    const unsigned t = base + lane;
+    const bool has = t < nsq;
+    std::uint32_t row = 0, self = 0;
+    unsigned cnt = 0;
+    bool wide_row = false;
+    if (has) {
+      row = sq[t];
+      float U[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) U[d] = __uint_as_float(sq[std::uint64_t(1 + d) * scap + t]);
+      const float rp = __uint_as_float(sq[std::uint64_t(D + 1) * scap + t]);
+      const float reach = __uint_as_float(sq[std::uint64_t(D + 2) * scap + t]);
+      self = s_off.part(a.k, row);
+      ScanSlot<D>& r = sl[lane];
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const int lo = max(floor_small(U[d] - rp), 0);
+        const int hi = min(floor_small(U[d] + rp), top[d]);
+        const int span = hi - lo + 1;
+        wide_row = wide_row || span > kFlatSpan || span < 1;
+        r.lo[d] = lo;
+        r.span[d] = static_cast<unsigned>(span);
+#pragma unroll
+        for (int i = 0; i < kFlatSpan; ++i) {
+          const float c = static_cast<float>(lo + i);
+          const float g = fmaxf(fmaxf(c - U[d], U[d] - (c + 1.f)), 0.f);
+          r.g2[d][i] = g * g;
+        }
+        r.inv[d] = static_cast<unsigned>(ceilf(__fdiv_rn(65536.f, static_cast<float>(max(span, 1)))));
+      }
+      // (a few binary32 roundings of the squared distances, far inside the margins)
+      r.rin2 = reach > 0.f ? reach * reach * 0.999998f - 1e-12f : -1.f;
+      r.rout2 = (rp * rp + 1e-6f) * 1.00001f;
+      r.self = self;
+      if (!wide_row) cnt = D == 3 ? r.span[1] * r.span[2] : r.span[1];
+    }
+    unsigned incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(full, incl, o);
+      if (lane >= static_cast<unsigned>(o)) incl += y;
+    }
+    const unsigned total = __shfl_sync(full, incl, 31);
+    const unsigned excl = incl - cnt;
+    const unsigned nzmask = __ballot_sync(full, cnt > 0);
+    if (cnt) {
+      sl[lane].excl = excl;
+      nz[__popc(nzmask & lt)] = static_cast<unsigned char>(lane);
+    }
+    __syncwarp();
+    unsigned hitm = 0, ambm = 0;
+    int cur = -1;
+    for (unsigned b0 = 0; b0 < total; b0 += 32) {
+      const bool st = cnt && excl >= b0 && excl < b0 + 32;
+      const unsigned smask = __reduce_or_sync(full, st ? 1u << (excl - b0) : 0u);
+      const unsigned q = b0 + lane;
+      bool hit = false, amb = false;
+      unsigned cl = 0;
+      if (q < total) {
+        cl = nz[cur + __popc(smask & ((2u << lane) - 1u))];
+        const ScanSlot<D>& r = sl[cl];
+        const unsigned rem = q - r.excl;
+        float g12, g2z = 0.f;
+        int c1, c2 = 0;
+        if constexpr (D == 3) {
+          const unsigned i2 = (rem * r.inv[1]) >> 16;  // rem / span1 (rem * span1 < 2^16)
+          const unsigned i1 = rem - i2 * r.span[1];
+          c1 = r.lo[1] + static_cast<int>(i1);
+          c2 = r.lo[2] + static_cast<int>(i2);
+          g12 = r.g2[1][i1];
+          g2z = r.g2[2][i2];
+        } else {
+          c1 = r.lo[1] + static_cast<int>(rem);
+          g12 = r.g2[1][rem];
+        }
+        const unsigned long long lb =
+            (D == 3 ? static_cast<unsigned long long>(static_cast<unsigned>(c1) + fd1 * static_cast<unsigned>(c2))
+                    : static_cast<unsigned long long>(static_cast<unsigned>(c1))) * fd0 +
+            static_cast<unsigned>(r.lo[0]);
+        std::uint32_t fw[kFlatSpan];
+        float d2[kFlatSpan];
+#pragma unroll
+        for (int i0 = 0; i0 < kFlatSpan; ++i0) {
+          d2[i0] = r.g2[0][i0] + g12 + g2z;
+          fw[i0] = kFieldEmptyBit;
+          if (i0 < static_cast<int>(r.span[0]) && d2[i0] * 0.99999f - 1e-6f <= r.rout2)
+            fw[i0] = static_cast<std::uint32_t>(__ldg(a.field + lb + i0));
+        }
+        const std::uint32_t sf = r.self;
+#pragma unroll
+        for (int i0 = 0; i0 < kFlatSpan; ++i0) {
+          const bool foreign = !(fw[i0] & kFieldEmptyBit) && (fw[i0] & 0xFFFFu) != sf;
+          const bool in = d2[i0] * 1.000002f + 1e-12f < r.rin2;
+          hit = hit || (foreign && in);
+          amb = amb || (foreign && !in);
+        }
+      }
+      hitm |= __reduce_or_sync(full, hit ? 1u << cl : 0u);
+      ambm |= __reduce_or_sync(full, amb ? 1u << cl : 0u);
+      cur += __popc(smask);
+    }
+    __syncwarp();
+    const bool pos = has && !wide_row && ((hitm >> lane) & 1u);
+    const bool open = has && !pos && (wide_row || ((ambm >> lane) & 1u));
+    if (has && !open) {
+      __stcs(a.positive + row, static_cast<std::uint8_t>(pos ? 1 : 0));
+      if (pos)
+#pragma unroll
+        for (int j = 0; j <= D; ++j) a.vflags[__ldg(a.verts + std::uint64_t(j) * a.S + row)] = 1;
+    }
+    if (a.counters) {
+      const unsigned mh = __ballot_sync(full, has), mp = __ballot_sync(full, pos), mo = __ballot_sync(full, open);
+      if (lane == 0) {
+        atomicAdd(&a.counters[16], static_cast<unsigned long long>(__popc(mh)));
+        if (mp) atomicAdd(&a.counters[17], static_cast<unsigned long long>(__popc(mp)));
+        if (mo) atomicAdd(&a.counters[18], static_cast<unsigned long long>(__popc(mo)));
+      }
+    }
+    // the undecided rows: the binary64 exact stage
+    {
+      const unsigned mo = __ballot_sync(full, open);
+      if (mo) {
+        unsigned ob = 0;
+        if (lane == 0) ob = atomicAdd(ncand, static_cast<unsigned>(__popc(mo)));
+        ob = __shfl_sync(full, ob, 0);
+        if (open) {
+          cand[ob + __popc(mo & lt)] = row;
+          cand[cap + ob + __popc(mo & lt)] = __float_as_uint(-1.f);
+        }
+      }
+    }
+    base = __shfl_sync(full, nclaim, 0);
+  }
+  rewind_cursor(next, fin, nsq);
 }
 
 // Candidates whose binary32 sphere failed (reach == kReachCheckOrient): the
@@ -2220,6 +2439,28 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
         SBDT_WS(pn, unsigned, "border.pf_wide_n", 4);
         SBDT_CUDA_TRY(cudaMemsetAsync(pn, 0, 4 * sizeof(unsigned), st));
         unsigned* pnlight = ctx->chunks.empty() ? pn + 3 : nullptr;
+        // grid policy: the prefilter's open rows with a narrow range go to the
+        // binary32 cell scan first: SoA {row, U[D], Rp, reach}, counters
+        // {rows, cursor, CTAs done}
+        std::uint32_t* sq = nullptr;
+        unsigned* sn = nullptr;
+        const std::uint64_t scap = in->S + 64;
+        if (!exact_policy) {
+          SBDT_WS(sqw, std::uint32_t, "border.scan_q", scap * (D + 3));
+          SBDT_WS(snw, unsigned, "border.scan_n", 4);
+          SBDT_CUDA_TRY(cudaMemsetAsync(snw, 0, 4 * sizeof(unsigned), st));
+          sq = sqw;
+          sn = snw;
+        }
+        int per_sm_s = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_s, k_border_scan32<D>, kScanWarps * 32, offs_sh);
+        const unsigned resS = static_cast<unsigned>(sms * (per_sm_s > 0 ? per_sm_s : 1));
+        auto scan32 = [&]() {
+          if (sq) {
+            k_border_scan32<D><<<resS, kScanWarps * 32, offs_sh, st>>>(a, og, sq, scap, sn, sn + 1, sn + 2, cq, qcap, cn);
+            ++ctx->launches;
+          }
+        };
         if (exact_policy)
           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_exact<D, true>, kExactWarps * 32, offs_sh);
         else
@@ -2236,10 +2477,10 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
           SBDT_CUDA_TRY(cudaMemsetAsync(pfcur, 0, sizeof(unsigned long long), st));
           if (bigk)
             k_border_prefilter<D, true><<<static_cast<unsigned>(want < resA ? want : resA), kBThreads, 0, st>>>(
-                a, og, cq, qcap, cn, r0, r1, pfcur, pq, pcap, pn, pnlight);
+                a, og, cq, qcap, cn, r0, r1, pfcur, pq, pcap, pn, pnlight, sq, scap, sn);
           else
             k_border_prefilter<D, false><<<static_cast<unsigned>(want < resA ? want : resA), kBThreads, offs_sh, st>>>(
-                a, og, cq, qcap, cn, r0, r1, pfcur, pq, pcap, pn, pnlight);
+                a, og, cq, qcap, cn, r0, r1, pfcur, pq, pcap, pn, pnlight, sq, scap, sn);
           return kOk;
         };
         auto exact = [&]() {
@@ -2307,6 +2548,10 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
           }
           SBDT_CUDA_TRY(cudaEventRecord(ctx->wide_join_ev, ctx->wide_stream));
           {
+            StageTimer ts(ctx, "border.scan32");
+            scan32();
+          }
+          {
             StageTimer tx(ctx, "border.exact");
             exact();
           }
@@ -2329,6 +2574,7 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
               const int prc = prefilter(r0, r1);
               if (prc != kOk) return prc;
               wide(true, st);
+              scan32();
               exact();
               wide(false, st);
               ctx->launches += 4;

@@ -96,7 +96,7 @@ enum BorderCounter : int {
   kCtrOrientRows = 12,     // rows whose binary32 sphere failed: exact orientation checked
   kCtrOrientExact = 13,    // orient evaluations escalated to expansion arithmetic
   kCtrInSphereExact = 14,  // in_sphere tests escalated (exact policy, k_border_escalate)
-  kBorderCounters = 16,
+  kBorderCounters = 20,
 };
 
 inline int fail(sbdt_gpu_ctx* ctx, int code, const std::string& msg) {

@@ -179,13 +179,14 @@ class Context:
                 "queued_points": int(out[4]), "dense_cells": int(out[5])}
 
     def border_stats(self) -> dict:
-        out = (C.c_ulonglong * 16)()
-        if lib().sbdt_gpu_border_stats(self._h, out, 16) != SBDT_OK:
+        out = (C.c_ulonglong * 20)()
+        if lib().sbdt_gpu_border_stats(self._h, out, 20) != SBDT_OK:
             return {}
         keys = {0: "rows", 1: "exact_stage_rows", 2: "exact_flat_scan", 3: "wide_from_exact", 4: "wide_rows",
                 5: "row_pairs", 6: "wide_expansions", 7: "exact_flat_positive", 8: "prefilter_positive",
                 9: "wide_positive", 10: "mask_positive", 12: "orient_check_rows", 13: "orient_escalations",
-                14: "in_sphere_escalations", 15: "mask_negative"}
+                14: "in_sphere_escalations", 15: "mask_negative", 16: "scan32_rows", 17: "scan32_positive",
+                18: "scan32_open"}
         return {kk: int(out[i]) for i, kk in keys.items()}
 
     # ---- diagnostics (tests / bench): device predicates, binding ceilings
