@@ -621,10 +621,8 @@ template <int D>
 __device__ __forceinline__ int prefilter_decide(const PfConst<D>& pc, const Sphere32<D>& sp, std::uint32_t self,
                                                 float* out_U, float* out_reach, float* out_rout,
                                                 std::uint32_t* out_mask, int* out_need, float* out_rp) {
-  *out_reach = -1.f;
-  *out_rout = kRoutNoMask;
-  *out_rp = -1.f;
-  *out_need = kNeedUnknown;
+  // (straight-line: every test is evaluated and the outcome selected at the
+  // end; the row's field word is the only load)
   // R >= radius of the inflated binary64 sphere + distance between centres
   float slack = 0.f;
 #pragma unroll
@@ -641,20 +639,20 @@ __device__ __forceinline__ int prefilter_decide(const PfConst<D>& pc, const Sphe
   // rounding of Uc (three roundings of |Uc|) and of Uc -/+ Rp: below 4e-7 (|Uc| + Rc)
   const float sl = fmaf(4e-7f, um + Rc, 1e-6f);
   const float Rp = Rc + sl;
-  if (!(um + Rp < 4194304.f)) return 2;  // outside floor_small's range (or NaN)
+  const bool ok = um + Rp < 4194304.f;  // within floor_small's range (false for NaN)
   int need = 0, cb[D];
-  bool inside = true;
+  bool inside = ok;
 #pragma unroll
   for (int d = 0; d < D; ++d) {
-    const int a = max(__float_as_int(__fadd_rd(Uc[d] - Rp, 12582912.f)), kFloorBias);
-    const int b = min(__float_as_int(__fadd_rd(Uc[d] + Rp, 12582912.f)), pc.ctop[d]);
-    const int c0 = __float_as_int(__fadd_rd(Uc[d], 12582912.f));
+    const float u = ok ? Uc[d] : 0.f;
+    const int a = max(__float_as_int(__fadd_rd(u - Rp, 12582912.f)), kFloorBias);
+    const int b = min(__float_as_int(__fadd_rd(u + Rp, 12582912.f)), pc.ctop[d]);
+    const int c0 = __float_as_int(__fadd_rd(u, 12582912.f));
     const int cc = min(max(c0, kFloorBias), pc.ctop[d]);
     inside = inside && c0 == cc;
     need = max(need, max(cc - a, b - cc));
     cb[d] = cc - kFloorBias;
   }
-  *out_need = need;
   unsigned long long li;
   if constexpr (D == 3)
     li = static_cast<unsigned long long>(static_cast<unsigned>(cb[1]) + pc.dim1 * static_cast<unsigned>(cb[2])) * pc.dim0 +
@@ -663,45 +661,42 @@ __device__ __forceinline__ int prefilter_decide(const PfConst<D>& pc, const Sphe
     li = static_cast<unsigned long long>(static_cast<unsigned>(cb[1])) * pc.dim0 + static_cast<unsigned>(cb[0]);
   const std::uint64_t f64 = __ldg(pc.field + li);
   const std::uint32_t fw = static_cast<std::uint32_t>(f64);
-  *out_mask = static_cast<std::uint32_t>(f64 >> 32);
   const std::uint32_t code = fw & 0xFFFFu;
-  if (code == self && need < static_cast<int>(fw >> 24)) return 0;
-  if (!inside) return 2;
-  // the exact stage's foreign-mask test (exact_mask_test) needs U; its
-  // negative proof also needs the range inside the 3^D window around cc
-#pragma unroll
-  for (int d = 0; d < D; ++d) out_U[d] = Uc[d];
-  *out_rp = Rp;
-  if (code == self) *out_rout = need <= 1 ? Rp : -1.f;
+  const int hs = static_cast<int>(fw >> 24);
+  *out_mask = static_cast<std::uint32_t>(f64 >> 32);
+  *out_need = ok ? need : kNeedUnknown;
+  const bool neg = ok && code == self && need < hs;
   // Positive proof, in binary32 cell units: cc = floor(Uc) holds Uc, the
   // real centre lies within sqrt(D) sl of Uc, and the cell box in cell units
   // is [cc, cc + 1] up to the binary64 rounding of cell_lo (< 1e-7 cells
   // while (|lo| / edge + dims) < 2^26, checked by the caller through pos_ok).
   // If the inner ball, shrunk by the exact stage's margin, still reaches that
   // box, the binary64 box test on the binary64 sphere accepts it. The same
-  // holds for a neighbour of cc whose box is within the remaining reach of Uc
-  // (the exact stage's octant_proof).
-  if (!pc.pos_ok) return 2;
+  // holds for every other cell whose box is within the remaining reach of Uc
+  // (the foreign-mask test and the binary32 cell scan).
   const float rin_c = ((sp.r * 0.999996f - 2.01f * sp.e * 1.000001f) * 0.999999f - slack) * pc.inv_e * 0.999998f;
   const float reach = rin_c - pc.margin_c - 1.7321f * sl - 2e-7f;
-  if (!(reach > 0.f)) return 2;
-  if (!(fw & kFieldEmptyBit) && code != self) return 1;  // non-empty, another part or MULTI
+  const bool can_pos = inside && pc.pos_ok && reach > 0.f;
+  const bool pos_centre = !(fw & kFieldEmptyBit) && code != self;  // non-empty, another part or MULTI
   // The window of radius hs (1 <= hs <= H) around cc is MULTI: it holds an
   // occupied cell of another part. If the inner ball reaches even the far
   // corner of the window's farthest cell, it overlaps that cell.
-  const int hs = static_cast<int>(fw >> 24);
-  if (hs >= 1 && hs <= field_h<D>()) {
-    float dd = 0.f;
+  float dd = 0.f;
 #pragma unroll
-    for (int d = 0; d < D; ++d) {
-      const float f = Uc[d] - static_cast<float>(cb[d]);  // exact: cb = floor(Uc)
-      const float m = fmaxf(f, 1.f - f) + static_cast<float>(hs - 1);
-      dd = fmaf(m, m, dd);
-    }
-    if (dd * 1.000002f + 1e-6f < reach * reach) return 1;
+  for (int d = 0; d < D; ++d) {
+    const float f = Uc[d] - static_cast<float>(cb[d]);  // exact when inside: cb = floor(Uc)
+    const float m = fmaxf(f, 1.f - f) + static_cast<float>(hs - 1);
+    dd = fmaf(m, m, dd);
   }
-  *out_reach = reach;
-  return 2;
+  const bool pos_window = hs >= 1 && hs <= field_h<D>() && dd * 1.000002f + 1e-6f < reach * reach;
+  const bool pos = !neg && can_pos && (pos_centre || pos_window);
+  // the record for the neighbour proofs and the cell scans (centre inside the grid)
+#pragma unroll
+  for (int d = 0; d < D; ++d) out_U[d] = Uc[d];
+  *out_rp = inside ? Rp : -1.f;
+  *out_rout = (inside && code == self) ? (need <= 1 ? Rp : -1.f) : kRoutNoMask;
+  *out_reach = can_pos ? reach : -1.f;
+  return neg ? 0 : (pos ? 1 : 2);
 }
 
 // The neighbours of the centre cell c0 = floor(U) on the near side of U in
@@ -805,7 +800,7 @@ constexpr int kPfBatchWords = 2 * D + 8;
 constexpr unsigned kPfChunk = 32 * kPfIters;
 
 template <int D, bool BIGK>
-__global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
+__global__ void __launch_bounds__(kBThreads, 4) k_border_prefilter(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
                                                                 std::uint32_t* __restrict__ cand, std::uint64_t cap,
                                                                 unsigned* __restrict__ ncand, std::uint64_t row_begin,
                                                                 std::uint64_t row_end,
@@ -908,13 +903,20 @@ __global__ void __launch_bounds__(kBThreads) k_border_prefilter(BorderArgs a, co
       row = B[0][e];
       reach = __uint_as_float(B[2][e]);
       const float rout = __uint_as_float(B[3][e]);
+      // the centre cell's foreign mask (no loads: it came with the field
+      // word), else (the centre's field code is not the row's part) the
+      // near-octant neighbours' codes
       int r = -1;
-      if (reach > 0.f || rout >= -1.f) {
+      if (rout >= -1.f) {
         float U[D];
 #pragma unroll
         for (int d = 0; d < D; ++d) U[d] = __uint_as_float(B[5 + d][e]);
-        if (rout >= -1.f) r = exact_mask_test<D>(B[4][e], U, reach, rout);
-        else r = octant_proof<D>(og, a, U, reach, B[1][e]) ? 1 : -1;
+        r = exact_mask_test<D>(B[4][e], U, reach, rout);
+      } else if (reach > 0.f) {
+        float U[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) U[d] = __uint_as_float(B[5 + d][e]);
+        r = octant_proof<D>(og, a, U, reach, B[1][e]) ? 1 : -1;
       }
       if (r >= 0) {
         __stcs(a.positive + row, static_cast<std::uint8_t>(r));
