@@ -305,3 +305,26 @@ def test_elongated_bbox_grid_capacity(dim, ctx):
         assert np.array_equal(g.positive, o["positive"]), policy
         assert np.array_equal(g.border, o["border"]), policy
         assert np.array_equal(g.positive_vertex_ids, o["vertices_positive"]), policy
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_enclosed_island_bfs(dim, ctx):
+    """Part 1 is an island (the samples within 0.15 of the centre) inside
+    part 0: part 0's simplices around the hole are positive but their
+    component holds no hull simplex, so the SPEC BFS border (find_border,
+    SPEC.md:491) is a strict subset of the full-scan positive set and the
+    hull-BFS takes its general path (per-row root marks, not the all-reached
+    copy)."""
+    inst = host.make_instance(1 if dim == 2 else 2, n=30_000, k=2)
+    sp = inst.points[inst.sample_ids]
+    sl = (np.linalg.norm(sp - 0.5, axis=1) < 0.15).astype(np.uint32)
+    lab = oracle.assign_brute(inst.points, inst.sample_ids, sl)
+    P = host.build_partials(inst.points, lab, 2, 7)
+    for policy in ("grid", "exact"):
+        g = gpu.find_border(inst.points, lab, P, gpu.IntersectionPolicy(policy, 1.0), hull_bfs=True, ctx=ctx)
+        o = oracle.find_border(inst.points, lab, P, policy)
+        assert o["border"].sum() < o["positive"].sum()
+        assert np.array_equal(g.positive, o["positive"])
+        assert np.array_equal(g.border, o["border"])
+        assert np.array_equal(g.positive_vertex_ids, o["vertices_positive"])
+        assert np.array_equal(g.border_vertex_ids, o["vertices_border"])
