@@ -492,34 +492,53 @@ def main():
 
     # DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) from
     # the committed ncu --set full capture of the same command (config 2)
-    traffic_by_stage = {}
+    traffic_by_stage, inst_by_stage = {}, {}
     tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
     if os.path.exists(tpath) and args.config == 2 and args.n is None and args.policy == "grid":
         with open(tpath) as f:
-            traffic_by_stage = json.load(f).get("stages", {})
+            tj = json.load(f)
+            traffic_by_stage, inst_by_stage = tj.get("stages", {}), tj.get("inst", {})
+    issue_peak = torch.cuda.get_device_properties(dev).multi_processor_count * 4 * 1965e6  # warp inst/s
 
     def roof(bytes_, ms_, stage=None):
         a = bytes_ / (ms_ * 1e-3) / 1e9
         t = traffic_by_stage.get(stage)
-        return {"bound": "hbm", "achieved": round(a, 1), "peak": peak, "unit": "GB/s", "frac": round(a / peak, 4),
-                "traffic": int(t) if t else None, "algorithmic_bytes": int(bytes_), "ms": round(ms_, 4),
-                "peak_kind": peak_kind}
+        r = {"bound": "hbm", "achieved": round(a, 1), "peak": peak, "unit": "GB/s", "frac": round(a / peak, 4),
+             "traffic": int(t) if t else None, "algorithmic_bytes": int(bytes_), "ms": round(ms_, 4),
+             "peak_kind": peak_kind}
+        ins = inst_by_stage.get(stage)
+        if ins:
+            # the binding ceiling of these gather/latency-bound kernels: the
+            # issue rate (one warp instruction per SMSP per clock; ncu's
+            # instruction count of the same kernel per launch)
+            r["issue_frac"] = round(ins / (ms_ * 1e-3) / issue_peak, 4)
+        return r
 
     # stages timed on the side stream overlap the launch stream's kernels
     # (find_border runs the hull rows' halfspace kernel next to exact + wide):
     # they count neither in the serial stage sums nor as the dominant kernel
-    overlapped = {"border.infinite"} if args.policy in ("grid", "exact") and S > 0 else set()
+    overlapped = {"border.infinite", "border.wide"} if args.policy in ("grid", "exact") and S > 0 else set()
     t_assign = sum(v for kk, v in stages.items() if kk.startswith("assign."))
     t_border = sum(v for kk, v in stages.items() if kk.startswith("border.") and kk not in overlapped)
-    n_cand = int(border_stats.get("exact_stage_rows", 0))
+    n_cand = int(border_stats.get("exact_stage_rows", 0))   # binary64 exact stage
+    n_scan = int(border_stats.get("scan32_rows", 0))        # binary32 cell scan
+    n_wide = int(border_stats.get("wide_rows", 0))          # pyramid descents routed by the prefilter
+    # algorithmic bytes per launch (SURVEY.md 8d per unit x the units of one launch):
     kernel_bytes = {
         "assign.points": n * (8 * dim + 4),
         "border.finite": S * (4 * (dim + 1) + 1) + n * (8 * dim + 4 + 1) + cells * 2,
-        # prefilter: vertex ids + flag per row, coords once, 3 code arrays (parity is not read)
-        "border.prefilter": S * (4 * (dim + 1) + 1) + n * (8 * dim + 4) + cells * 2 * 3,
-        # exact stage: queue entry + ids per candidate + result, coords once
-        "border.exact": n_cand * (4 + 4 * (dim + 1) + 1) + n * (8 * dim + 4) + cells * 2,
-        "border.grid": n * (8 * dim + 4) + cells * 2,
+        # prefilter: vertex ids + flag per row, the 8-byte packed coordinate of
+        # every point once, one 8-byte field word per cell once, and its queue
+        # records (binary32 scan {row, U, Rp, reach}, wide {row, ids})
+        "border.prefilter": S * (4 * (dim + 1) + 1) + n * 8 + cells * 8 + n_scan * 4 * (dim + 3)
+        + n_wide * 4 * (dim + 2),
+        # binary32 scan: its queue record and flag per row, field words once
+        "border.scan32": n_scan * (4 * (dim + 3) + 1) + cells * 8,
+        # binary64 exact stage: queue entry + ids + flag per row, coordinates once
+        "border.exact": n_cand * (8 + 4 * (dim + 1) + 1) + n * 8 * dim + cells * 8,
+        # owner grid: coordinates + labels in, packed coordinates out; owner
+        # codes (2 B) and field words (8 B) per cell
+        "border.grid": n * (8 * dim + 4 + 8) + cells * 10,
         "assign.bucket": n * 12,
         "border.compact": n + n_vb * 4,
     }

@@ -9,5 +9,5 @@ l1tex__t_sector_hit_rate.pct,smsp__inst_executed.sum,smsp__issue_active.avg.pct_
 sm__warps_active.avg.pct_of_peak_sustained_active,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,\
 sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active,smsp__inst_executed_pipe_fp64.sum,\
 gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed,lts__t_sectors_srcunit_tex.sum,launch__registers_per_thread
-KERN='regex:k_border_(prefilter|exact|wide|infinite)|k_assign_vlt|k_vlt_build|k_owner_mark|k_nbr_tiles|k_bucket|k_reach'
+KERN='regex:k_border_(prefilter|scan32|exact|wide|infinite)|k_assign_vlt|k_assign_overflow|k_vlt_build|k_owner_mark|k_field_tiles|k_bucket|k_reach'
 ncu --metrics $METRICS --clock-control none -k "$KERN" --csv --log-file "$out" python bench.py --profile "$@"

@@ -106,13 +106,42 @@ def full(paths):
 # bench.py stage -> kernels whose DRAM traffic makes up the stage
 STAGE_KERNELS = {
     "border.prefilter": ["k_border_prefilter"],
+    "border.scan32": ["k_border_scan32"],
     "border.exact": ["k_border_exact"],
-    "border.exact_wide": ["k_border_wide"],
+    "border.wide": ["k_border_wide"],
     "border.infinite": ["k_border_infinite"],
-    "border.grid": ["k_owner_mark", "k_nbr_tiles"],
+    "border.grid": ["k_owner_mark", "k_field_tiles"],
     "assign.table": ["k_vlt_build"],
     "assign.points": ["k_assign_vlt", "k_assign_overflow"],
 }
+
+
+def traffic_quick(path):
+    """tools/ncu_quick.sh output -> per kernel (largest launch, the step's main
+    one) DRAM bytes and warp instructions, per bench stage: the JSON bench.py
+    reads (profiles/ncu_traffic.json)."""
+    import json
+    rows = [r for r in csv.reader(open(path)) if len(r) > 10]
+    h = {k: i for i, k in enumerate(rows[0])}
+    per = {}
+    for r in rows[1:]:
+        if r[0] == "ID":
+            continue
+        name = r[h["Kernel Name"]].split("(")[0].replace("void ", "").split("::")[-1].split("<")[0]
+        key = (name, r[h["ID"]])
+        per.setdefault(key, {})[r[h["Metric Name"]]] = float(r[h["Metric Value"]].replace(",", ""))
+    best = {}
+    for (name, _), m in per.items():
+        b = m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
+        t = m.get("gpu__time_duration.sum", 0.0)
+        if name not in best or t > best[name]["ns"]:
+            best[name] = {"dram_bytes": b, "inst": m.get("smsp__inst_executed.sum", 0.0), "ns": t}
+    res = {"source": [path], "kernels": best, "stages": {}, "inst": {}}
+    for st, ks in STAGE_KERNELS.items():
+        if all(k in best for k in ks):
+            res["stages"][st] = sum(best[k]["dram_bytes"] for k in ks)
+            res["inst"][st] = sum(best[k]["inst"] for k in ks)
+    print(json.dumps(res, indent=1))
 
 
 def traffic(paths):
@@ -146,5 +175,7 @@ if __name__ == "__main__":
         traffic(sys.argv[2:])
     elif sys.argv[1] == "quick":
         quick(sys.argv[2])
+    elif sys.argv[1] == "traffic_quick":
+        traffic_quick(sys.argv[2])
     else:
         full(sys.argv[2:])
