@@ -211,28 +211,48 @@ BorderSet find_border(std::span<const Triangulation<D>> partials, std::span<cons
       }
     }
   });
-  constexpr std::size_t kRowGrain = 1u << 16;
+  // The compact partials' rows are converted chunk by chunk from inside the
+  // call (sbdt_gpu_set_fill): the C ABI asks for rows [r0, r1) right before
+  // it uploads them, so this conversion overlaps the previous chunk's
+  // transfer (the non-compact partials were converted above).
+  constexpr std::size_t kRowGrain = 1u << 15;
   const bool exact = policy.kind == IntersectionPolicy::Exact;
-  parallel_chunks(pool, S, kRowGrain, [&](std::size_t b, std::size_t e) {
-    std::uint32_t p = static_cast<std::uint32_t>(std::upper_bound(offsets.begin(), offsets.end(), b) - offsets.begin()) - 1;
-    for (std::size_t row = b; row < e;) {
-      while (offsets[p + 1] <= row) ++p;
-      const std::size_t end = std::min<std::size_t>(e, offsets[p + 1]);
-      if (compact[p]) {
-        // only what the device reads: all vertex rows; the neighbour rows for
-        // the BFS, else only row D (the hull rows' owner, read in place from
-        // this page-locked buffer); parity for the exact policy
-        const Simplex<D>* raw = partials[p].raw_simplices().data() + (row - offsets[p]);
-        for (std::size_t r = row; r < end; ++r)
-          for (int j = 0; j <= D; ++j) verts[std::uint64_t(j) * S + r] = raw[r - row].vertices[j];
-        for (int j = opts.hull_bfs ? 0 : D; j <= D; ++j)
-          for (std::size_t r = row; r < end; ++r) nbrs[std::uint64_t(j) * S + r] = raw[r - row].neighbors[j];
-        if (exact)
-          for (std::size_t r = row; r < end; ++r) parity[r] = raw[r - row].parity;
+  auto convert = [&](std::uint64_t r0, std::uint64_t r1) {
+    parallel_chunks(pool, r1 - r0, kRowGrain, [&](std::size_t b0, std::size_t e0) {
+      const std::size_t b = r0 + b0, e = r0 + e0;
+      std::uint32_t p =
+          static_cast<std::uint32_t>(std::upper_bound(offsets.begin(), offsets.end(), b) - offsets.begin()) - 1;
+      for (std::size_t row = b; row < e;) {
+        while (offsets[p + 1] <= row) ++p;
+        const std::size_t end = std::min<std::size_t>(e, offsets[p + 1]);
+        if (compact[p]) {
+          // only what the device reads: all vertex rows; the neighbour rows
+          // for the BFS, else only row D (the hull rows' owner, read in place
+          // from this page-locked buffer); parity for the exact policy
+          const Simplex<D>* raw = partials[p].raw_simplices().data() + (row - offsets[p]);
+          for (std::size_t r = row; r < end; ++r)
+            for (int j = 0; j <= D; ++j) verts[std::uint64_t(j) * S + r] = raw[r - row].vertices[j];
+          for (int j = opts.hull_bfs ? 0 : D; j <= D; ++j)
+            for (std::size_t r = row; r < end; ++r) nbrs[std::uint64_t(j) * S + r] = raw[r - row].neighbors[j];
+          if (exact)
+            for (std::size_t r = row; r < end; ++r) parity[r] = raw[r - row].parity;
+        }
+        row = end;
       }
-      row = end;
+    });
+  };
+  struct FillState {
+    decltype(convert)* fn;
+    static int call(void* user, int what, std::uint64_t r0, std::uint64_t r1) {
+      if (what != SBDT_FILL_ROWS) return 0;
+      try {
+        (*static_cast<FillState*>(user)->fn)(r0, r1);
+        return 0;
+      } catch (...) {
+        return 1;
+      }
     }
-  });
+  } fill_state{&convert};
   std::uint8_t* positive = gpu_detail::pinned(4).get<std::uint8_t>(S);
   std::uint8_t* border = opts.hull_bfs ? gpu_detail::pinned(5).get<std::uint8_t>(S) : nullptr;
   std::uint32_t* vids = gpu_detail::pinned(6).get<std::uint32_t>(n);
@@ -242,10 +262,26 @@ BorderSet find_border(std::span<const Triangulation<D>> partials, std::span<cons
   for (int d = 0; d < D; ++d) gbb[d] = g0.global_bbox.lo[d], gbb[D + d] = g0.global_bbox.hi[d];
   const std::uint32_t flags = (opts.hull_bfs ? SBDT_BORDER_HULL_BFS : 0u) |
                               (opts.points_resident ? SBDT_BORDER_RESIDENT_POINTS : 0u);
+  // points_resident: the device keeps the points and labels of the last
+  // assign_points call, which handed the C ABI its page-locked copies
+  const double* coords_arg = ps.raw().data();
+  const std::uint32_t* labels_arg = labels;
+  if (opts.points_resident) {
+    const gpu_detail::ResidentRecord& rr = gpu_detail::resident();
+    if (rr.coords != ps.raw().data() || rr.n != n || rr.labels != opts.labels.data())
+      throw std::invalid_argument("find_border: points_resident needs the points and labels of the last assign_points");
+    coords_arg = rr.staged_coords;
+    labels_arg = rr.staged_labels;
+  }
   sbdt_gpu_ctx* ctx = gpu_detail::thread_context();
   const double t1 = gpu_detail::wall_ms();
+  struct FillGuard {
+    sbdt_gpu_ctx* c;
+    ~FillGuard() { sbdt_gpu_set_fill(c, nullptr, nullptr); }
+  } fill_guard{ctx};
+  sbdt_gpu_set_fill(ctx, &FillState::call, &fill_state);
   gpu_detail::check(ctx,
-                    sbdt_gpu_find_border(ctx, D, ps.raw().data(), n, labels, k, offsets.data(), verts, nbrs, parity,
+                    sbdt_gpu_find_border(ctx, D, coords_arg, n, labels_arg, k, offsets.data(), verts, nbrs, parity,
                                          static_cast<int>(policy.kind), policy.c_G, flags, positive, border, vids, &nv,
                                          bvids, opts.hull_bfs ? &nb : nullptr, nullptr, gbb, g0.n_total),
                     "find_border");

@@ -16,6 +16,8 @@
 #pragma once
 
 #include <chrono>
+#include <cstring>
+#include <thread>
 #include <cstdint>
 #include <new>
 #include <span>
@@ -97,6 +99,31 @@ void for_each_part(TaskPool* pool, std::size_t k, Fn&& fn) {
   }
 }
 
+// fn(b, e) over [0, n) in chunks of `grain`, on the caller's TaskPool when it
+// has workers (pure data movement).
+template <class Fn>
+void for_each_chunk(TaskPool* pool, std::size_t n, std::size_t grain, Fn&& fn) {
+  if (pool && pool->concurrency() > 1 && n > grain) {
+    pool->parallel_for(n, grain, [&](std::size_t b, std::size_t e) { fn(b, e); });
+  } else if (n) {
+    fn(0, n);
+  }
+}
+
+// The points and labels of the last assign_points call on this thread and
+// the page-locked copies the C ABI saw (find_border with points_resident).
+struct ResidentRecord {
+  const double* coords = nullptr;
+  std::uint64_t n = 0;
+  const PartitionId* labels = nullptr;
+  const double* staged_coords = nullptr;
+  const std::uint32_t* staged_labels = nullptr;
+};
+inline ResidentRecord& resident() {
+  thread_local ResidentRecord r;
+  return r;
+}
+
 // One device context per host thread (the C ABI contract).
 inline sbdt_gpu_ctx* thread_context() {
   struct Holder {
@@ -147,24 +174,47 @@ Partitioning assign_points(const PointSet& points, std::span<const PointId> samp
   gpu_detail::PhaseTimes& ph = gpu_detail::last_phases();
   const double t0 = gpu_detail::wall_ms();
   Partitioning out;
-  out.labels.resize(n);
+  // the labels vector is value-initialised by resize: done by a helper thread
+  // while the coordinates are staged and the device works
+  std::thread labels_init([&] { out.labels.resize(n); });
+  struct Join {
+    std::thread& t;
+    ~Join() {
+      if (t.joinable()) t.join();
+    }
+  } join{labels_init};
   out.sample_point_ids.assign(sample_ids.begin(), sample_ids.end());
   out.sample_labels.assign(sample_labels.begin(), sample_labels.end());
-  // parts come back as CSR in page-locked staging (no zero-fill, full-rate D2H)
+  // the coordinates go through page-locked staging (copied by the pool's
+  // threads; a pageable source would be staged by the driver at a fraction of
+  // the link rate), the labels and parts come back into page-locked staging
+  double* xyz = gpu_detail::pinned_slot(2).get<double>(n * D);
+  std::uint32_t* lab = gpu_detail::pinned_slot(3).get<std::uint32_t>(n);
   std::uint64_t* offsets = gpu_detail::pinned_slot(0).get<std::uint64_t>(k + 1);
   std::uint32_t* ids = gpu_detail::pinned_slot(1).get<std::uint32_t>(n);
+  const double* src = points.raw().data();
+  gpu_detail::for_each_chunk(pool, n * D, std::size_t(1) << 19, [&](std::size_t b, std::size_t e) {
+    std::memcpy(xyz + b, src + b, sizeof(double) * (e - b));
+  });
   sbdt_gpu_ctx* ctx = gpu_detail::thread_context();
   const double t1 = gpu_detail::wall_ms();
   gpu_detail::check(ctx,
-                    sbdt_gpu_assign_points(ctx, D, points.raw().data(), n, sample_ids.data(), sample_labels.data(),
-                                           static_cast<std::uint32_t>(sample_ids.size()), k, out.labels.data(),
-                                           offsets, ids, nullptr),
+                    sbdt_gpu_assign_points(ctx, D, xyz, n, sample_ids.data(), sample_labels.data(),
+                                           static_cast<std::uint32_t>(sample_ids.size()), k, lab, offsets, ids,
+                                           nullptr),
                     "assign_points");
   const double t2 = gpu_detail::wall_ms();
+  labels_init.join();
+  gpu_detail::for_each_chunk(pool, n, std::size_t(1) << 20, [&](std::size_t b, std::size_t e) {
+    std::memcpy(out.labels.data() + b, lab + b, sizeof(std::uint32_t) * (e - b));
+  });
   out.parts.resize(k);
   gpu_detail::for_each_part(pool, k, [&](std::size_t p) {
     out.parts[p].assign(ids + offsets[p], ids + offsets[p + 1]);
   });
+  // find_border(points_resident) on these points and labels reuses the
+  // device copies: it is handed the staging pointers this call used
+  gpu_detail::resident() = {src, n, out.labels.data(), xyz, lab};
   ph.prepare_ms = t1 - t0, ph.device_ms = t2 - t1, ph.finish_ms = gpu_detail::wall_ms() - t2;
   return out;
 }

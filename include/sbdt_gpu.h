@@ -112,6 +112,18 @@ int sbdt_gpu_border_stats(sbdt_gpu_ctx* ctx, unsigned long long* out, int count)
 int sbdt_gpu_host_alloc(uint64_t bytes, void** out);
 void sbdt_gpu_host_free(void* p);
 
+/* Producer hook of sbdt_gpu_find_border (host buffers): when set, the call
+ * invokes fill(user, SBDT_FILL_ROWS, r0, r1) right before it uploads the
+ * simplex rows [r0, r1) of verts / nbrs / parity, in increasing order, so
+ * the caller can write those rows into the (page-locked) buffers it passed
+ * while the previous chunk is in flight (e.g. converting the reference's
+ * Triangulation<D> records). A non-zero return aborts the call with
+ * SBDT_ERR_INVALID. fill == NULL removes the hook. The hook applies to the
+ * context's host-buffer find_border calls until removed. */
+#define SBDT_FILL_ROWS 1
+typedef int (*sbdt_fill_fn)(void* user, int what, uint64_t begin, uint64_t end);
+int sbdt_gpu_set_fill(sbdt_gpu_ctx* ctx, sbdt_fill_fn fill, void* user);
+
 /* ---- assign_points -------------------------------------
  * coords: n points, AoS binary64 (PointSet::raw(), geometry.hpp:94-95).
  * sample_ids: m global PointIds; sample_labels: m labels < k.

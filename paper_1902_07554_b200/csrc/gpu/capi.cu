@@ -172,6 +172,13 @@ int sbdt_gpu_assign_table_stats(sbdt_gpu_ctx* ctx, unsigned* out6) {
   return assign_stats(ctx, out6) == kOk ? SBDT_OK : SBDT_ERR_INVALID;
 }
 
+int sbdt_gpu_set_fill(sbdt_gpu_ctx* ctx, sbdt_fill_fn fill, void* user) {
+  if (!ctx) return SBDT_ERR_INVALID;
+  ctx->fill = fill;
+  ctx->fill_user = user;
+  return SBDT_OK;
+}
+
 int sbdt_gpu_border_stats(sbdt_gpu_ctx* ctx, unsigned long long* out, int count) {
   if (!ctx || !out || count < 0) return SBDT_ERR_INVALID;
   auto it = ctx->bufs.find("border.counters");
@@ -450,6 +457,8 @@ int find_border_host(sbdt_gpu_ctx* ctx, int dim, const double* coords, uint64_t 
   }
   for (int c = 0; c < kUploadChunks; ++c) {
     const uint64_t r0 = row_chunk_end(S, c - 1), r1 = row_chunk_end(S, c);
+    if (r1 > r0 && ctx->fill && ctx->fill(ctx->fill_user, SBDT_FILL_ROWS, r0, r1) != 0)
+      return fail(ctx, SBDT_ERR_INVALID, "fill hook failed");
     if (r1 > r0) {
       for (int j = 0; j <= dim; ++j)
         SBDT_CUDA_TRY(cudaMemcpyAsync(d_verts + j * S + r0, verts + j * S + r0, sizeof(uint32_t) * (r1 - r0),

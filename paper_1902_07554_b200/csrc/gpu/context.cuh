@@ -10,11 +10,14 @@
 #include <vector>
 
 #include "common.cuh"
+#include "sbdt_gpu.h"
 
 struct sbdt_gpu_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  sbdt_fill_fn fill = nullptr;  // find_border's row producer (sbdt_gpu_set_fill)
+  void* fill_user = nullptr;
   std::string last_error;
   unsigned long long launches = 0;
   struct Buf {
