@@ -1703,7 +1703,7 @@ __device__ bool warp_sphere_descent(const OwnerGrid<D>& og, const std::uint16_t*
 }
 
 template <int D, bool Ex>
-__global__ void __launch_bounds__(kWideWarps * 32, 6) k_border_wide(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
+__global__ void __launch_bounds__(kWideWarps * 32, Ex ? 6 : 8) k_border_wide(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
                                                                  const std::uint32_t* __restrict__ wide,
                                                                  std::uint64_t cap,
                                                                  const unsigned* __restrict__ nwide_p,
@@ -2241,6 +2241,8 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
     SBDT_WS(q, std::uint64_t, "border.xq", in->n + 1);
     xq = q;
   }
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   StageTimer tgrid(ctx, "border.grid");
   const unsigned long long* bb = reinterpret_cast<const unsigned long long*>(in->d_bbox_ordered);
   if (in->grid_bbox) {
@@ -2512,19 +2514,20 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
             const int prc = prefilter(0, in->S);
             if (prc != kOk) return prc;
           }
+          // the prefilter's queue length: the orientation checks read only
+          // its entries (k_border_scan32 appends to the same queue meanwhile)
+          SBDT_CUDA_TRY(cudaMemcpyAsync(cn + 7, cn, sizeof(unsigned), cudaMemcpyDeviceToDevice, st));
           // the hull queue is complete once the prefilter ran: its halfspace
-          // kernel (few rows, latency-bound) overlaps exact + wide on the side
-          // stream and joins before the escalation / compaction
+          // kernel (few rows, latency-bound) overlaps the exact stages on the
+          // side stream and joins before the escalation / compaction
           {
             const int hrc = build_hull_set();
             if (hrc != kOk) return hrc;
           }
           // the hull-row and wide-row descents are the longest latency-bound
           // chains after the prefilter: their streams get the highest
-          // priority, so their CTAs are placed first and the exact stage
-          // fills the remaining slots
-          int prio_lo = 0, prio_hi = 0;
-          cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+          // priority, so their CTAs are placed first and the binary32 scan
+          // and the exact stage fill the remaining slots
           if (!ctx->side_stream)
             SBDT_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->side_stream, cudaStreamNonBlocking, prio_hi));
           if (!ctx->fork_ev) SBDT_CUDA_TRY(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
@@ -2535,7 +2538,7 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
             StageTimer ti(ctx, "border.infinite", ctx->side_stream);
             infinite(ctx->side_stream);
           }
-          k_border_orient<D><<<sms * 4, 256, 0, ctx->side_stream>>>(a, cq, qcap, cn);
+          k_border_orient<D><<<sms * 4, 256, 0, ctx->side_stream>>>(a, cq, qcap, cn + 7);
           ++ctx->launches;
           SBDT_CUDA_TRY(cudaEventRecord(ctx->join_ev, ctx->side_stream));
           inf_forked = true;
