@@ -23,6 +23,8 @@
 // K3  stable counting sort by label -> Partitioning.parts (ascending ids).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "context.cuh"
 #include "scan.cuh"
@@ -54,6 +56,7 @@ struct SampleGrid {
   double delta_f;        // fine-box inflation
   double delta_c;        // coarse-box inflation (> fine inflation)
   unsigned long long cells;
+  int refined;            // cells shrunk for clustered samples: only cells with samples nearby get a table record
 };
 
 constexpr int kBlock = 256;
@@ -120,22 +123,17 @@ __global__ void k_sample_gather(const double* __restrict__ xyz, const std::uint3
   bbox_flush<D>(lo, hi, bbox);
 }
 
-// Sample-grid parameters: ~2 samples per cell plus one cell of padding on
-// every side; cell count capped at cap.
+// Sample-grid parameters for cell edge e over the bbox: one cell of padding
+// on every side; the edge doubled until the cell count fits cap.
 template <int D>
-__global__ void k_sample_grid_params(const unsigned long long* bbox, std::uint32_t m, unsigned long long cap,
-                                     SampleGrid<D>* sg) {
-  double lo[D], hi[D], vol = 1.0, ext_max = 0.0, mag = 0.0;
+__device__ void sample_grid_set(const unsigned long long* bbox, double e, unsigned long long cap, SampleGrid<D>* sg) {
+  double lo[D], hi[D], ext_max = 0.0, mag = 0.0;
   for (int d = 0; d < D; ++d) {
     lo[d] = ordered_to_dbl(bbox[d]);
     hi[d] = ordered_to_dbl(bbox[D + d]);
-    const double ext = hi[d] - lo[d];
-    vol *= ext;
-    ext_max = fmax(ext_max, ext);
+    ext_max = fmax(ext_max, hi[d] - lo[d]);
     mag = fmax(mag, fmax(fabs(lo[d]), fabs(hi[d])));
   }
-  const double per = 2.0 * vol / static_cast<double>(m > 0 ? m : 1);
-  double e = (D == 2) ? sqrt(per) : cbrt_det(per);
   if (!(e > 0.0)) e = ext_max > 0.0 ? ext_max / 64.0 : 1.0;
   unsigned long long cells;
   long long dims[D];
@@ -146,7 +144,9 @@ __global__ void k_sample_grid_params(const unsigned long long* bbox, std::uint32
       cells *= static_cast<unsigned long long>(dims[d]);
     }
     if (cells <= cap) break;
-    e *= 2.0;
+    // grow the edge to about the cap (with a 2% margin; at least by 1%)
+    const double g = (D == 2 ? sqrt(static_cast<double>(cells) / cap) : cbrt_det(static_cast<double>(cells) / cap));
+    e *= fmax(1.01, g * 1.02);
   }
   for (int d = 0; d < D; ++d) {
     sg->g.lo[d] = lo[d] - e;
@@ -163,6 +163,53 @@ __global__ void k_sample_grid_params(const unsigned long long* bbox, std::uint32
   sg->delta_c = 2.0 * sg->delta_f + 1e-9 * e;
 }
 
+// ~2 samples per cell of the bbox volume
+template <int D>
+__global__ void k_sample_grid_params(const unsigned long long* bbox, std::uint32_t m, unsigned long long cap,
+                                     SampleGrid<D>* sg) {
+  double vol = 1.0;
+  for (int d = 0; d < D; ++d) vol *= ordered_to_dbl(bbox[D + d]) - ordered_to_dbl(bbox[d]);
+  const double per = 2.0 * vol / static_cast<double>(m > 0 ? m : 1);
+  sample_grid_set<D>(bbox, (D == 2) ? sqrt(per) : cbrt_det(per), cap, sg);
+  sg->refined = 0;
+}
+
+// Clustered samples (surfaces, lines, dense cores): q = samples per occupied
+// cell of that grid. Above 4 the edge shrinks by (q / 2)^(1 / D) (the volume
+// estimate: a dense core gets ~2 samples per cell; a lower-dimensional
+// structure keeps more, which the table's adaptive sub-boxes absorb, while a
+// finer grid would leave the sparse regions' points to long ring searches),
+// within cap cells; the table is
+// then built only for cells with samples in their 3^D neighbourhood (the
+// others send their points to the exact ring search), so the extra empty
+// cells cost one head each.
+// Occupied cells holding a single sample (the first grid's sparse regions).
+template <int D>
+__global__ void k_sample_singletons(const std::uint32_t* __restrict__ counts, const SampleGrid<D>* __restrict__ sg,
+                                    unsigned* __restrict__ singles) {
+  const unsigned long long cells = sg->cells;
+  unsigned c = 0;
+  for (unsigned long long i = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < cells;
+       i += static_cast<unsigned long long>(gridDim.x) * blockDim.x)
+    c += counts[i] == 1u ? 1u : 0u;
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31u) == 0 && c) atomicAdd(singles, c);
+}
+
+template <int D>
+__global__ void k_sample_grid_refine(const unsigned long long* bbox, std::uint32_t m, unsigned long long cap,
+                                     const unsigned* __restrict__ occupied, SampleGrid<D>* sg) {
+  const unsigned occ = occupied[0] > 0 ? occupied[0] : 1u;
+  const double q = static_cast<double>(m) / static_cast<double>(occ);
+  // many single-sample cells: a wide density range (a dense core with sparse
+  // tails), where the refined grid's sparse regions would send their points
+  // to long ring searches; refine only structures without them
+  if (!(q > 4.0) || !(static_cast<double>(occupied[1]) < 0.15 * static_cast<double>(occ))) return;
+  const double r = D == 2 ? sqrt(0.5 * q) : cbrt_det(0.5 * q);
+  sample_grid_set<D>(bbox, sg->g.edge / r, cap, sg);
+  sg->refined = 1;
+}
+
 template <int D>
 __device__ __forceinline__ long long linear(const Grid<D>& g, const long long* c) {
   long long id = c[D - 1];
@@ -173,7 +220,8 @@ __device__ __forceinline__ long long linear(const Grid<D>& g, const long long* c
 
 template <int D>
 __global__ void k_sample_count(const SampleRec* __restrict__ recs, std::uint32_t m, const SampleGrid<D>* sgp,
-                               std::uint32_t* __restrict__ counts, std::uint32_t* __restrict__ cell_of) {
+                               std::uint32_t* __restrict__ counts, std::uint32_t* __restrict__ cell_of,
+                               unsigned* __restrict__ occupied = nullptr) {
   const Grid<D> g = sgp->g;
   for (std::uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < m; s += gridDim.x * blockDim.x) {
     long long c[D];
@@ -181,7 +229,7 @@ __global__ void k_sample_count(const SampleRec* __restrict__ recs, std::uint32_t
     for (int d = 0; d < D; ++d) c[d] = cell_coord<D>(g, recs[s].x[d], d);
     const std::uint32_t cell = static_cast<std::uint32_t>(linear<D>(g, c));
     cell_of[s] = cell;
-    atomicAdd(&counts[cell], 1u);
+    if (atomicAdd(&counts[cell], 1u) == 0u && occupied) atomicAdd(occupied, 1u);
   }
 }
 
@@ -392,7 +440,8 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
                 const std::uint32_t* d_sample_labels, std::uint32_t m, std::uint32_t* d_labels,
                 unsigned long long* d_bbox) {
   cudaStream_t st = ctx->stream;
-  const unsigned long long cap = 2ULL * m + 1024;
+  const unsigned long long cap0 = 2ULL * m + 1024;  // pools sized from the bbox grid
+  const unsigned long long cap = std::min(16ULL * m + 1024, 1ULL << 31);  // cells of a refined grid (clustered samples)
   SBDT_WS(recs, SampleRec, "assign.recs", m);
   SBDT_WS(sorted, SampleRec, "assign.sorted", m);
   SBDT_WS(sbbox, unsigned long long, "assign.sbbox", 2 * D);
@@ -404,11 +453,11 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
   const unsigned long long fine = cap * fine_per_cell<D>();
   SBDT_WS(heads, std::uint32_t, "assign.heads", fine);
   SBDT_WS(slab, VltEntry, "assign.slab", fine * kSlots);
-  const unsigned long long lcap_ll = fine * 24 + 4096;  // long lists (dense cells: ~100 per fine cell); full -> ring search
+  const unsigned long long lcap_ll = cap0 * fine_per_cell<D>() * 24 + 4096;  // long lists (dense cells: ~100 per fine cell); full -> ring search
   const unsigned lcap = lcap_ll < (1ull << 28) ? static_cast<unsigned>(lcap_ll) : (1u << 28);
   SBDT_WS(lslab, VltEntry, "assign.lslab", lcap);
   SBDT_WS(lcount, unsigned, "assign.lcount", 1);
-  const unsigned long long subcap_ll = fine * 8 + 4096;  // sub-box heads; full -> long lists
+  const unsigned long long subcap_ll = cap0 * fine_per_cell<D>() * 8 + 4096;  // sub-box heads; full -> long lists
   const unsigned subcap = subcap_ll < (1ull << 28) ? static_cast<unsigned>(subcap_ll) : (1u << 28);
   SBDT_WS(subheads, std::uint32_t, "assign.subheads", subcap);
   SBDT_WS(subcount, unsigned, "assign.subcount", 1);
@@ -430,9 +479,18 @@ int assign_impl(sbdt_gpu_ctx* ctx, const double* d_xyz, std::uint64_t n, const s
     k_bbox_init<<<1, 32, 0, st>>>(d_bbox, D);
     k_sample_gather<D><<<sblocks, kBlock, 0, st>>>(d_xyz, d_sample_ids, d_sample_labels, m, recs, sbbox,
                                                    ctx->sample_xyz);
-    k_sample_grid_params<D><<<1, 1, 0, st>>>(sbbox, m, cap, sg);
+    SBDT_WS(occ, unsigned, "assign.occupied", 2);  // {occupied cells, single-sample cells}
+    k_sample_grid_params<D><<<1, 1, 0, st>>>(sbbox, m, cap0, sg);
+    SBDT_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(std::uint32_t) * (cap0 + 1), st));
+    SBDT_CUDA_TRY(cudaMemsetAsync(occ, 0, 2 * sizeof(unsigned), st));
+    k_sample_count<D><<<sblocks, kBlock, 0, st>>>(recs, m, sg, counts, cell_of, occ);
+    k_sample_singletons<D><<<static_cast<unsigned>(std::min<unsigned long long>((cap0 + 255) / 256, 1024)), 256, 0, st>>>(
+        counts, sg, occ + 1);
+    k_sample_grid_refine<D><<<1, 1, 0, st>>>(sbbox, m, cap, occ, sg);
+    ++ctx->launches;
     SBDT_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(std::uint32_t) * (cap + 1), st));
     k_sample_count<D><<<sblocks, kBlock, 0, st>>>(recs, m, sg, counts, cell_of);
+    ctx->launches += 2;
     exclusive_scan(counts, starts, cap + 1, blocksums, nullptr, st, &ctx->launches);
     SBDT_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(std::uint32_t) * (cap + 1), st));
     k_sample_scatter<<<sblocks, kBlock, 0, st>>>(recs, m, cell_of, starts, counts, sorted);

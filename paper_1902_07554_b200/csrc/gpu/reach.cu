@@ -200,20 +200,23 @@ __global__ void k_reach_hook(ReachArgs a, const std::uint32_t* __restrict__ ptot
     }
 }
 
-// roots of the seeds marked; then every row's root (full compression) and a
-// count of the rows whose component holds no seed
+// roots of the seeds marked; then every row's root and a count of the rows
+// whose component holds no seed
 __global__ void k_reach_mark(ReachArgs a, const std::uint32_t* __restrict__ ptotal) {
   const std::uint32_t P = *ptotal;
   for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x)
     if (a.mark[i] & 2u) a.mark[find_root(a.parent, i)] |= 1u;
 }
 
-__global__ void k_reach_roots(ReachArgs a, const std::uint32_t* __restrict__ ptotal, unsigned* __restrict__ unreached) {
+// (the roots go to a separate array: the parent array may still receive
+// path-shortening writes of other threads, which store ancestors, not roots)
+__global__ void k_reach_roots(ReachArgs a, const std::uint32_t* __restrict__ ptotal, unsigned* __restrict__ unreached,
+                              std::uint32_t* __restrict__ rootof) {
   const std::uint32_t P = *ptotal;
   unsigned c = 0;
   for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
     const std::uint32_t r = find_root(a.parent, i);
-    a.parent[i] = r;
+    rootof[i] = r;
     c += (a.mark[r] & 1u) ? 0u : 1u;
   }
   for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
@@ -225,7 +228,7 @@ __global__ void k_reach_roots(ReachArgs a, const std::uint32_t* __restrict__ pto
 // copy of the flags; else per positive row from its root's mark.
 __global__ void k_reach_final(ReachArgs a, const std::uint32_t* __restrict__ ptotal,
                               const unsigned* __restrict__ unreached, const std::uint8_t* __restrict__ pos_vflags,
-                              std::uint64_t n) {
+                              std::uint64_t n, const std::uint32_t* __restrict__ rootof) {
   const int D = a.dim;
   if (*unreached == 0) {
     const std::uint64_t t0 = std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -246,7 +249,7 @@ __global__ void k_reach_final(ReachArgs a, const std::uint32_t* __restrict__ pto
   const std::uint32_t P = *ptotal;
   for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
     const std::uint64_t s = a.pos_ids[i];
-    const bool b = (a.mark[a.parent[i]] & 1u) != 0;
+    const bool b = (a.mark[rootof[i]] & 1u) != 0;
     a.border[s] = b ? 1 : 0;
     if (b && a.vflags)
       for (int j = 0; j <= D; ++j) {
@@ -290,8 +293,9 @@ int reach_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   k_reach_hook<<<blocks, 256, 0, st>>>(a, ptot, nrank);
   k_reach_mark<<<blocks, 256, 0, st>>>(a, ptot);
   SBDT_CUDA_TRY(cudaMemsetAsync(unreached, 0, sizeof(unsigned), st));
-  k_reach_roots<<<blocks, 256, 0, st>>>(a, ptot, unreached);
-  k_reach_final<<<blocks, 256, 0, st>>>(a, ptot, unreached, in->d_vertex_flags, in->n);
+  // nrank is free after the hooking: its first P words take the roots
+  k_reach_roots<<<blocks, 256, 0, st>>>(a, ptot, unreached, nrank);
+  k_reach_final<<<blocks, 256, 0, st>>>(a, ptot, unreached, in->d_vertex_flags, in->n, nrank);
   ctx->launches += 8;
   if (in->d_bfs_vertex_flags && in->d_bfs_vertex_ids && in->d_bfs_vertex_count) {
     const int rc = compact_flags(ctx, in->d_bfs_vertex_flags, in->n, in->d_bfs_vertex_ids, in->d_bfs_vertex_count);

@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
     const long long cell = DENSE ? static_cast<long long>(dq[item]) : item;
     int cc[D];
     {
-      // 32-bit: the sample grid has at most 2 m + 1024 cells
+      // 32-bit: the sample grid has at most min(16 m + 1024, 2^31) cells
       unsigned rem = static_cast<unsigned>(cell);
 #pragma unroll
       for (int d = 0; d < D; ++d) {
@@ -266,6 +266,30 @@ __global__ void __launch_bounds__(32 * kVltWarps) k_vlt_build(const SampleGrid<D
         const unsigned qd = rem / dd;
         cc[d] = static_cast<int>(rem - qd * dd);
         rem = qd;
+      }
+    }
+    if (!DENSE && sg.refined) {
+      // refined grid (clustered samples): a record only where samples are
+      // within the 3^D neighbourhood; elsewhere (no point expected: points
+      // follow the samples) the heads send points to the exact ring search
+      bool near = false;
+      if (lane < static_cast<unsigned>(D == 3 ? 27 : 9)) {
+        long long nid = 0, mul = 1;
+        bool in = true;
+        unsigned rem = lane;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const int nc = cc[d] + static_cast<int>(rem % 3u) - 1;
+          rem /= 3u;
+          in = in && nc >= 0 && nc < static_cast<int>(g.dims[d]);
+          nid += static_cast<long long>(nc) * mul;
+          mul *= g.dims[d];
+        }
+        near = in && starts[nid + 1] > starts[nid];
+      }
+      if (!__any_sync(0xffffffffu, near)) {
+        for (int f = static_cast<int>(lane); f < FC; f += 32) heads[cell * FC + f] = kHeadOverflow;
+        continue;
       }
     }
     double c[D];

@@ -321,10 +321,11 @@ def test_enclosed_island_bfs(dim, ctx):
     lab = oracle.assign_brute(inst.points, inst.sample_ids, sl)
     P = host.build_partials(inst.points, lab, 2, 7)
     for policy in ("grid", "exact"):
-        g = gpu.find_border(inst.points, lab, P, gpu.IntersectionPolicy(policy, 1.0), hull_bfs=True, ctx=ctx)
         o = oracle.find_border(inst.points, lab, P, policy)
         assert o["border"].sum() < o["positive"].sum()
-        assert np.array_equal(g.positive, o["positive"])
-        assert np.array_equal(g.border, o["border"])
-        assert np.array_equal(g.positive_vertex_ids, o["vertices_positive"])
-        assert np.array_equal(g.border_vertex_ids, o["vertices_border"])
+        for _ in range(4):  # the union-find runs with concurrent hooks: repeat
+            g = gpu.find_border(inst.points, lab, P, gpu.IntersectionPolicy(policy, 1.0), hull_bfs=True, ctx=ctx)
+            assert np.array_equal(g.positive, o["positive"])
+            assert np.array_equal(g.border, o["border"])
+            assert np.array_equal(g.positive_vertex_ids, o["vertices_positive"])
+            assert np.array_equal(g.border_vertex_ids, o["vertices_border"])
