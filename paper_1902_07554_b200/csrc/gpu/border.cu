@@ -588,7 +588,9 @@ struct PfConst {
   int ctop[D];                 // kFloorBias + ldims[0][d] - 1
   unsigned dim0, dim1;         // ldims[0][0], ldims[0][1] (linear index)
   float inv_e, margin_c, lo_mag;
-  bool pos_ok;                 // positive proofs allowed (grid policy, cell boxes within binary32 reach)
+  bool pos_ok;                 // positive proofs allowed (cell boxes within binary32 reach)
+  bool contain;                // exact policy: a proof needs a foreign cell INSIDE the inner ball (its points
+                               // then lie strictly inside the circumsphere), not only overlapping it
 };
 
 // candidate record's outer-ball slot: the foreign mask does not apply (the
@@ -677,18 +679,26 @@ __device__ __forceinline__ int prefilter_decide(const PfConst<D>& pc, const Sphe
   const float rin_c = ((sp.r * 0.999996f - 2.01f * sp.e * 1.000001f) * 0.999999f - slack) * pc.inv_e * 0.999998f;
   const float reach = rin_c - pc.margin_c - 1.7321f * sl - 2e-7f;
   const bool can_pos = inside && pc.pos_ok && reach > 0.f;
-  const bool pos_centre = !(fw & kFieldEmptyBit) && code != self;  // non-empty, another part or MULTI
   // The window of radius hs (1 <= hs <= H) around cc is MULTI: it holds an
-  // occupied cell of another part. If the inner ball reaches even the far
-  // corner of the window's farthest cell, it overlaps that cell.
-  float dd = 0.f;
+  // occupied cell of another part. Grid policy: if the inner ball reaches
+  // even the nearest point of the window's farthest cell (per axis
+  // hs - 1 + max(f, 1 - f)), it overlaps that cell. Exact policy: the inner
+  // ball must contain the whole window (far corners: hs + max(f, 1 - f)), so
+  // that cell's points lie strictly inside the circumsphere; likewise the
+  // centre cell (far corner: max(f, 1 - f)).
+  float dd = 0.f, dc = 0.f;
 #pragma unroll
   for (int d = 0; d < D; ++d) {
     const float f = Uc[d] - static_cast<float>(cb[d]);  // exact when inside: cb = floor(Uc)
-    const float m = fmaxf(f, 1.f - f) + static_cast<float>(hs - 1);
+    const float mf = fmaxf(f, 1.f - f);
+    const float m = mf + static_cast<float>(pc.contain ? hs : hs - 1);
     dd = fmaf(m, m, dd);
+    dc = fmaf(mf, mf, dc);
   }
-  const bool pos_window = hs >= 1 && hs <= field_h<D>() && dd * 1.000002f + 1e-6f < reach * reach;
+  const float reach2 = reach * reach;
+  const bool pos_centre = !(fw & kFieldEmptyBit) && code != self &&  // non-empty, another part or MULTI
+                          (!pc.contain || dc * 1.000002f + 1e-6f < reach2);
+  const bool pos_window = hs >= 1 && hs <= field_h<D>() && dd * 1.000002f + 1e-6f < reach2;
   const bool pos = !neg && can_pos && (pos_centre || pos_window);
   // the record for the neighbour proofs and the cell scans (centre inside the grid)
 #pragma unroll
@@ -747,42 +757,58 @@ __device__ __forceinline__ bool octant_proof(const OwnerGrid<D>& og, const Borde
 // The centre cell's foreign mask m (k_field_tiles; the row's part is the
 // cell's field code, checked by the prefilter): 1 if the inner ball (reach,
 // all error slack already subtracted) reaches the box of a foreign
-// neighbour, 0 if the outer ball (rout > 0: radius in cell units with every
+// neighbour (exact policy: contains it, so that its points lie strictly
+// inside the circumsphere), 0 if the outer ball (rout > 0: radius in cell units with every
 // slack, its cell range inside the 3^D window) stays strictly away from all
 // of them, -1 undecided. Box distances in cell units from U, whose cell is
 // c0 = floor(U): per axis the gap to the neighbour at offset -1, 0, +1 is
 // f, 0, 1 - f (f = U - c0).
 template <int D>
-__device__ __forceinline__ int exact_mask_test(const std::uint32_t m, const float* U, float reach, float rout) {
-  float g[D][3];
+__device__ __forceinline__ int exact_mask_test(const std::uint32_t m, const float* U, float reach, float rout,
+                                               bool contain) {
+  // per axis, for the neighbour offsets -1, 0, +1: the squared box gap to U
+  // (f, 0, 1 - f) and, for the exact policy's containment proof, the squared
+  // far-corner distance (1 + f, max(f, 1 - f), 2 - f)
+  float g[D][3], h[D][3];
 #pragma unroll
   for (int d = 0; d < D; ++d) {
     const float f = U[d] - static_cast<float>(floor_small(U[d]));  // exact
     g[d][0] = f * f;
     g[d][1] = 0.f;
     g[d][2] = (1.f - f) * (1.f - f);
+    const float mf = fmaxf(f, 1.f - f);
+    h[d][0] = (1.f + f) * (1.f + f);
+    h[d][1] = mf * mf;
+    h[d][2] = (2.f - f) * (2.f - f);
   }
   if (!m) return rout > 0.f ? 0 : -1;
-  float mn = INFINITY;  // smallest squared box distance over the foreign neighbours
+  float mn = INFINITY, mx = INFINITY;  // smallest squared box gap / far-corner distance over the foreign neighbours
   if constexpr (D == 3) {
 #pragma unroll
     for (int o2 = 0; o2 < 3; ++o2)
 #pragma unroll
       for (int o1 = 0; o1 < 3; ++o1) {
-        const float s12 = g[1][o1] + g[2][o2];
+        const float s12 = g[1][o1] + g[2][o2], t12 = h[1][o1] + h[2][o2];
 #pragma unroll
         for (int o0 = 0; o0 < 3; ++o0)
-          if ((m >> (o0 + 3 * o1 + 9 * o2)) & 1u) mn = fminf(mn, g[0][o0] + s12);
+          if ((m >> (o0 + 3 * o1 + 9 * o2)) & 1u) {
+            mn = fminf(mn, g[0][o0] + s12);
+            mx = fminf(mx, h[0][o0] + t12);
+          }
       }
   } else {
 #pragma unroll
     for (int o1 = 0; o1 < 3; ++o1)
 #pragma unroll
       for (int o0 = 0; o0 < 3; ++o0)
-        if ((m >> (o0 + 3 * o1)) & 1u) mn = fminf(mn, g[0][o0] + g[1][o1]);
+        if ((m >> (o0 + 3 * o1)) & 1u) {
+          mn = fminf(mn, g[0][o0] + g[1][o1]);
+          mx = fminf(mx, h[0][o0] + h[1][o1]);
+        }
   }
-  // (a few binary32 roundings of the squared distance, far inside the margins)
-  if (reach > 0.f && mn * 1.000002f + 1e-12f < reach * reach) return 1;
+  // (a few binary32 roundings of the squared distances, far inside the margins)
+  const float prove = contain ? mx : mn;
+  if (reach > 0.f && prove * 1.000002f + 1e-12f < reach * reach) return 1;
   if (rout > 0.f && mn * 0.99999f - 1e-6f > rout * rout) return 0;
   return -1;
 }
@@ -840,7 +866,8 @@ __global__ void __launch_bounds__(kBThreads, 4) k_border_prefilter(BorderArgs a,
     pc.inv_e = static_cast<float>(og.inv_edge * unit);
     pc.margin_c = static_cast<float>(og.margin * og.inv_edge) * 1.0001f + 1e-30f;
     pc.lo_mag = 0.f;
-    pc.pos_ok = !a.exact;  // exact policy: a foreign cell is not a foreign point
+    pc.pos_ok = true;
+    pc.contain = a.exact != 0;
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       pc.lo_mag = fmaxf(pc.lo_mag, static_cast<float>(fabs(og.g.lo[d]) / unit) * 1.0001f);
@@ -911,8 +938,8 @@ __global__ void __launch_bounds__(kBThreads, 4) k_border_prefilter(BorderArgs a,
         float U[D];
 #pragma unroll
         for (int d = 0; d < D; ++d) U[d] = __uint_as_float(B[5 + d][e]);
-        r = exact_mask_test<D>(B[4][e], U, reach, rout);
-      } else if (reach > 0.f) {
+        r = exact_mask_test<D>(B[4][e], U, reach, rout, a.exact != 0);
+      } else if (reach > 0.f && !a.exact) {  // (overlap-based: grid policy only)
         float U[D];
 #pragma unroll
         for (int d = 0; d < D; ++d) U[d] = __uint_as_float(B[5 + d][e]);
