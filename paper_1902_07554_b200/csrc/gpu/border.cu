@@ -995,6 +995,10 @@ __global__ void __launch_bounds__(kBThreads, 4) k_border_prefilter(BorderArgs a,
           wq[q] = row;
 #pragma unroll
           for (int j = 0; j <= D; ++j) wq[std::uint64_t(j + 1) * wcap + q] = B[5 + D + j][e];
+          // the recorded cell-unit centre and inner reach (exact policy: blocks inside it are accepted)
+#pragma unroll
+          for (int d = 0; d < D; ++d) wq[std::uint64_t(D + 2 + d) * wcap + q] = B[5 + d][e];
+          wq[std::uint64_t(2 * D + 2) * wcap + q] = __float_as_uint(reach);
         }
       }
     }
@@ -1208,6 +1212,7 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
           wide[q] = static_cast<std::uint32_t>(s);
 #pragma unroll
           for (int j = 0; j <= D; ++j) wide[std::uint64_t(j + 1) * cap + q] = v[j];
+          wide[std::uint64_t(2 * D + 2) * cap + q] = __float_as_uint(-1.f);  // no recorded ball
         }
       }
     }
@@ -1375,8 +1380,16 @@ __global__ void __launch_bounds__(kExactWarps * 32, 6) k_border_exact(BorderArgs
 // Queue: SoA {row, U[D], Rp, reach}.
 constexpr int kScanWarps = 4;
 
+template <int D, bool Ex>
+struct ScanBalls {};  // grid policy: the cell-unit balls only
 template <int D>
-struct ScanSlot {
+struct ScanBalls<D, true> {
+  double c64[D];  // exact policy: U in coordinates, and the two radii squared in coordinate units
+  double pin2, pout2;
+};
+
+template <int D, bool Ex>
+struct ScanSlot : ScanBalls<D, Ex> {
   float g2[D][kFlatSpan];  // squared box gaps to U per axis and cell of the range
   float rin2, rout2;       // reach^2 (shrunk) and Rp^2 (grown), cell units
   int lo[D];
@@ -1386,7 +1399,7 @@ struct ScanSlot {
   unsigned excl;    // first position of this candidate in the flattened stream
 };
 
-template <int D>
+template <int D, bool Ex>
 __global__ void __launch_bounds__(kScanWarps * 32) k_border_scan32(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
                                                                   const std::uint32_t* __restrict__ sq,
                                                                   std::uint64_t scap,
@@ -1397,7 +1410,7 @@ __global__ void __launch_bounds__(kScanWarps * 32) k_border_scan32(BorderArgs a,
                                                                   std::uint64_t cap,
                                                                   unsigned* __restrict__ ncand) {
   __shared__ OwnerGrid<D> og;
-  __shared__ ScanSlot<D> slots[kScanWarps][32];
+  __shared__ ScanSlot<D, Ex> slots[kScanWarps][32];
   __shared__ unsigned char nzl[kScanWarps][32];
   extern __shared__ std::uint64_t s_off_sh[];
   if (threadIdx.x == 0) og = *ogp;
@@ -1409,13 +1422,20 @@ __global__ void __launch_bounds__(kScanWarps * 32) k_border_scan32(BorderArgs a,
   const unsigned lane = threadIdx.x & 31u;
   const unsigned lt = (1u << lane) - 1u;
   const unsigned wid = threadIdx.x >> 5;
-  ScanSlot<D>* sl = slots[wid];
+  ScanSlot<D, Ex>* sl = slots[wid];
   unsigned char* nz = nzl[wid];
   const unsigned full = 0xffffffffu;
   const unsigned fd0 = static_cast<unsigned>(og.ldims[0][0]), fd1 = static_cast<unsigned>(og.ldims[0][1]);
   int top[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) top[d] = og.ldims[0][d] - 1;
+  // exact policy: the level-0 tiled index of a cell (the per-cell point lists)
+  const bool multi_level = og.levels > 1;
+  unsigned long long bst[D];
+  bst[0] = 1;
+#pragma unroll
+  for (int d = 1; d < D; ++d) bst[d] = bst[d - 1] * static_cast<unsigned long long>(multi_level ? og.ldims[1][d - 1] : 1);
+  const CellPt<D>* cpts = static_cast<const CellPt<D>*>(a.cell_pts);
   unsigned base = claim_batch(next);
   for (;;) {
     if (base >= nsq) break;
@@ -1434,7 +1454,7 @@ __global__ void __launch_bounds__(kScanWarps * 32) k_border_scan32(BorderArgs a,
       const float rp = __uint_as_float(sq[std::uint64_t(D + 1) * scap + t]);
       const float reach = __uint_as_float(sq[std::uint64_t(D + 2) * scap + t]);
       self = s_off.part(a.k, row);
-      ScanSlot<D>& r = sl[lane];
+      ScanSlot<D, Ex>& r = sl[lane];
 #pragma unroll
       for (int d = 0; d < D; ++d) {
         const int lo = max(floor_small(U[d] - rp), 0);
@@ -1455,6 +1475,17 @@ __global__ void __launch_bounds__(kScanWarps * 32) k_border_scan32(BorderArgs a,
       r.rin2 = reach > 0.f ? reach * reach * 0.999998f - 1e-12f : -1.f;
       r.rout2 = (rp * rp + 1e-6f) * 1.00001f;
       r.self = self;
+      if constexpr (Ex) {
+        // the balls in coordinates: centre lo + U edge (binary64, ~1e-16
+        // relative), radii scaled by the edge, 1e-9 relative margins (the
+        // binary64 distances below round ~1e-15 relative)
+#pragma unroll
+        for (int d = 0; d < D; ++d) r.c64[d] = og.g.lo[d] + static_cast<double>(U[d]) * og.g.edge;
+        const double ri = reach > 0.f ? static_cast<double>(reach) * og.g.edge : 0.0;
+        const double ro = static_cast<double>(rp) * og.g.edge;
+        r.pin2 = reach > 0.f ? ri * ri * (1.0 - 1e-9) : -1.0;
+        r.pout2 = ro * ro * (1.0 + 1e-9) + 1e-300;
+      }
       if (!wide_row) cnt = D == 3 ? r.span[1] * r.span[2] : r.span[1];
     }
     unsigned incl = cnt;
@@ -1481,7 +1512,7 @@ __global__ void __launch_bounds__(kScanWarps * 32) k_border_scan32(BorderArgs a,
       unsigned cl = 0;
       if (q < total) {
         cl = nz[cur + __popc(smask & ((2u << lane) - 1u))];
-        const ScanSlot<D>& r = sl[cl];
+        const ScanSlot<D, Ex>& r = sl[cl];
         const unsigned rem = q - r.excl;
         float g12, g2z = 0.f;
         int c1, c2 = 0;
@@ -1510,12 +1541,40 @@ __global__ void __launch_bounds__(kScanWarps * 32) k_border_scan32(BorderArgs a,
             fw[i0] = static_cast<std::uint32_t>(__ldg(a.field + lb + i0));
         }
         const std::uint32_t sf = r.self;
+        if constexpr (!Ex) {
 #pragma unroll
-        for (int i0 = 0; i0 < kFlatSpan; ++i0) {
-          const bool foreign = !(fw[i0] & kFieldEmptyBit) && (fw[i0] & 0xFFFFu) != sf;
-          const bool in = d2[i0] * 1.000002f + 1e-12f < r.rin2;
-          hit = hit || (foreign && in);
-          amb = amb || (foreign && !in);
+          for (int i0 = 0; i0 < kFlatSpan; ++i0) {
+            const bool foreign = !(fw[i0] & kFieldEmptyBit) && (fw[i0] & 0xFFFFu) != sf;
+            const bool in = d2[i0] * 1.000002f + 1e-12f < r.rin2;
+            hit = hit || (foreign && in);
+            amb = amb || (foreign && !in);
+          }
+        } else {
+          // exact policy: the other parts' points of the foreign cells, by
+          // their binary64 distance to the ball centre: strictly inside the
+          // inner ball -> strictly inside the circumsphere (positive); beyond
+          // the outer ball -> not inside; in between -> the binary64 stage
+          const unsigned long long tb =
+              og.loff[0] + cell_off<D>(c1, 1, bst, multi_level) + (D == 3 ? cell_off<D>(c2, 2, bst, multi_level) : 0ull);
+          for (int i0 = 0; i0 < static_cast<int>(r.span[0]) && !hit; ++i0) {
+            if ((fw[i0] & kFieldEmptyBit) || (fw[i0] & 0xFFFFu) == sf) continue;
+            const unsigned long long idx = tb + cell_off<D>(r.lo[0] + i0, 0, bst, multi_level);
+            for (std::uint32_t t = a.cell_start[idx], te = a.cell_start[idx + 1]; t < te; ++t) {
+              const CellPt<D> q = cpts[t];
+              if (q.label == sf) continue;
+              double dq = 0.0;
+#pragma unroll
+              for (int d = 0; d < D; ++d) {
+                const double x = q.x[d] - r.c64[d];
+                dq = fma(x, x, dq);
+              }
+              if (dq < r.pin2) {
+                hit = true;
+                break;
+              }
+              amb = amb || dq <= r.pout2;
+            }
+          }
         }
       }
       hitm |= __reduce_or_sync(full, hit ? 1u << cl : 0u);
@@ -1690,7 +1749,8 @@ __device__ bool warp_descent(const OwnerGrid<D>& og, const std::uint16_t* __rest
 template <int D, bool Ex, class Leaf>
 __device__ bool warp_sphere_descent(const OwnerGrid<D>& og, const std::uint16_t* __restrict__ owner, const double* c,
                                     double r2, std::uint32_t self, WideEntry<D>* stk, const Leaf& leaf,
-                                    unsigned long long* counters = nullptr) {
+                                    unsigned long long* counters = nullptr, const float* U = nullptr,
+                                    float reach = -1.f) {
   if (isnan(r2)) return false;
   bool fin = isfinite(r2);
 #pragma unroll
@@ -1716,6 +1776,22 @@ __device__ bool warp_sphere_descent(const OwnerGrid<D>& og, const std::uint16_t*
     og_block_box<D>(og, L, cc, blo, bhi);
     if (!box_sphere<D>(blo, bhi, c, r2)) return 0;
     if constexpr (Ex) {
+      // a block (foreign code: it holds another part's point) entirely
+      // inside the prefilter's inner ball has that point strictly inside the
+      // circumsphere: accepted without its leaves (cell units: the block's
+      // cell range, far corner from U, the prefilter's margins)
+      if (reach > 0.f) {
+        const int sh = L * og.shift;
+        float dd = 0.f;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const float b0 = static_cast<float>(cc[d] << sh);
+          const float b1 = static_cast<float>(min((cc[d] + 1) << sh, og.ldims[0][d]));
+          const float far = fmaxf(U[d] - b0, b1 - U[d]);
+          dd = fmaf(far, far, dd);
+        }
+        if (dd * 1.000002f + 1e-6f < reach * reach) return 2;
+      }
       return L > 0 ? 1 : (leaf(cc) ? 2 : 0);
     } else {
       if (L == 0 || box_inside_sphere<D>(blo, bhi, c, r2)) return 2;
@@ -1763,12 +1839,18 @@ __global__ void __launch_bounds__(kWideWarps * 32, Ex ? 6 : 8) k_border_wide(Bor
     std::uint64_t s = 0;
     std::uint32_t self = 0, v[D + 1];
     double c[D], r2 = 0.0;
+    float U[D], reach = -1.f;
     if (has) {
       const std::uint64_t slot = t < nheavy ? t : cap - 1 - (t - nheavy);
       s = wide[slot];
       self = s_off.part(a.k, s);
 #pragma unroll
       for (int j = 0; j <= D; ++j) v[j] = wide[std::uint64_t(j + 1) * cap + slot];
+      if constexpr (Ex) {
+        reach = __uint_as_float(wide[std::uint64_t(2 * D + 2) * cap + slot]);
+#pragma unroll
+        for (int d = 0; d < D; ++d) U[d] = reach > 0.f ? __uint_as_float(wide[std::uint64_t(D + 2 + d) * cap + slot]) : 0.f;
+      }
       double p[D + 1][D];
       load_simplex<D>(a, v, p);
       circumsphere_inflated<D>(p, c, &r2);
@@ -1799,7 +1881,11 @@ __global__ void __launch_bounds__(kWideWarps * 32, Ex ? 6 : 8) k_border_wide(Bor
         }
         return cell_points_inside<D>(a, og_index<D>(og, 0, cell), pv, par, sl, srow);
       };
-      const bool hit = warp_sphere_descent<D, Ex>(og, a.owner, cl, rl, sl, stk, leaf, a.counters);
+      float Ul[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) Ul[d] = __shfl_sync(full, Ex ? U[d] : 0.f, l);
+      const float reach_l = __shfl_sync(full, reach, l);
+      const bool hit = warp_sphere_descent<D, Ex>(og, a.owner, cl, rl, sl, stk, leaf, a.counters, Ul, reach_l);
       if (static_cast<int>(lane) == l) pos = hit;
       if (a.counters && hit && lane == 0) atomicAdd(&a.counters[9], 1ull);
       __syncwarp();
@@ -2461,22 +2547,23 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
         // by cost class (host path: the launches per chunk share one cursor)
         unsigned* nlight = ctx->chunks.empty() ? cn + 6 : nullptr;
         const std::uint64_t wcap = qcap;  // wide rows <= candidates
-        SBDT_WS(wq, std::uint32_t, "border.wide", wcap * (D + 2));
+        SBDT_WS(wq, std::uint32_t, "border.wide", wcap * (2 * D + 3));  // SoA {row, ids, U[D], reach}
         // rows the prefilter routes to the pyramid descent directly (range
         // wider than the flattened scan's): {row, vertex ids}, counters
         // {heavy rows, cursor, CTAs done, light rows}
         const std::uint64_t pcap = in->S + 64;
-        SBDT_WS(pq, std::uint32_t, "border.pf_wide", pcap * (D + 2));
+        SBDT_WS(pq, std::uint32_t, "border.pf_wide", pcap * (2 * D + 3));
         SBDT_WS(pn, unsigned, "border.pf_wide_n", 4);
         SBDT_CUDA_TRY(cudaMemsetAsync(pn, 0, 4 * sizeof(unsigned), st));
         unsigned* pnlight = ctx->chunks.empty() ? pn + 3 : nullptr;
-        // grid policy: the prefilter's open rows with a narrow range go to the
-        // binary32 cell scan first: SoA {row, U[D], Rp, reach}, counters
-        // {rows, cursor, CTAs done}
+        // the prefilter's open rows with a narrow range go to the cell scan
+        // first (grid policy: cell boxes in binary32; exact policy: the
+        // foreign cells' points in binary64 against the recorded balls): SoA
+        // {row, U[D], Rp, reach}, counters {rows, cursor, CTAs done}
         std::uint32_t* sq = nullptr;
         unsigned* sn = nullptr;
         const std::uint64_t scap = in->S + 64;
-        if (!exact_policy) {
+        {
           SBDT_WS(sqw, std::uint32_t, "border.scan_q", scap * (D + 3));
           SBDT_WS(snw, unsigned, "border.scan_n", 4);
           SBDT_CUDA_TRY(cudaMemsetAsync(snw, 0, 4 * sizeof(unsigned), st));
@@ -2484,13 +2571,19 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
           sn = snw;
         }
         int per_sm_s = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_s, k_border_scan32<D>, kScanWarps * 32, offs_sh);
+        if (exact_policy)
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_s, k_border_scan32<D, true>, kScanWarps * 32, offs_sh);
+        else
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_s, k_border_scan32<D, false>, kScanWarps * 32, offs_sh);
         const unsigned resS = static_cast<unsigned>(sms * (per_sm_s > 0 ? per_sm_s : 1));
         auto scan32 = [&]() {
-          if (sq) {
-            k_border_scan32<D><<<resS, kScanWarps * 32, offs_sh, st>>>(a, og, sq, scap, sn, sn + 1, sn + 2, cq, qcap, cn);
-            ++ctx->launches;
-          }
+          if (exact_policy)
+            k_border_scan32<D, true><<<resS, kScanWarps * 32, offs_sh, st>>>(a, og, sq, scap, sn, sn + 1, sn + 2, cq, qcap,
+                                                                            cn);
+          else
+            k_border_scan32<D, false><<<resS, kScanWarps * 32, offs_sh, st>>>(a, og, sq, scap, sn, sn + 1, sn + 2, cq, qcap,
+                                                                             cn);
+          ++ctx->launches;
         };
         if (exact_policy)
           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_exact<D, true>, kExactWarps * 32, offs_sh);
