@@ -2417,11 +2417,11 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   if (tiled) {
     SBDT_WS(fw, std::uint64_t, "border.field", cap + 1);  // level-0 cells <= cap
     field = fw;
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[D - 2]) {
+    // the dynamic shared-memory opt-in, once per context (= per device)
+    if (!(ctx->attr_set & (1u << D))) {
       SBDT_CUDA_TRY(cudaFuncSetAttribute(k_field_tiles<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(field_smem_bytes<D>())));
-      attr_set[D - 2] = true;
+      ctx->attr_set |= 1u << D;
     }
     k_field_tiles<D><<<sms * 3, kFieldThreads, field_smem_bytes<D>(), st>>>(og, owner, field);
     ctx->launches += 1;

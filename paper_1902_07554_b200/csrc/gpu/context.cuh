@@ -17,6 +17,7 @@ struct sbdt_gpu_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   sbdt_fill_fn fill = nullptr;  // find_border's row producer (sbdt_gpu_set_fill)
+  unsigned attr_set = 0;        // kernels whose shared-memory opt-in was set on this device (bit D: k_field_tiles<D>)
   void* fill_user = nullptr;
   std::string last_error;
   unsigned long long launches = 0;
