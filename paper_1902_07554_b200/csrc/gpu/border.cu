@@ -819,7 +819,10 @@ __device__ __forceinline__ int exact_mask_test(const std::uint32_t m, const floa
 // the 1-2 partitions in flight stay in L2 instead of spreading over the rows
 // of warps that drifted apart, and a lane's consecutive rows are 32 apart
 // (vertices shared by neighbouring rows hit in L1).
-constexpr unsigned kPfIters = 16;
+#ifndef PF_ITERS
+#define PF_ITERS 8
+#endif
+constexpr unsigned kPfIters = PF_ITERS;
 constexpr unsigned kPfBatch = 64;  // per-warp batch of undecided rows (< 32 waiting + 32 arriving)
 template <int D>
 constexpr int kPfBatchWords = 2 * D + 8;

@@ -2,7 +2,9 @@
 
 #include <algorithm>
 #include <array>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 #include <numeric>
 
 #include "../common/predicates.hpp"
@@ -94,6 +96,7 @@ class Builder {
         lo[d] = std::min(lo[d], P(order_[i])[d]);
         hi[d] = std::max(hi[d], P(order_[i])[d]);
       }
+    for (int d = 0; d < D; ++d) blo_[d] = lo[d], bhi_[d] = hi[d];
     const double bits = (D == 3) ? 2097151.0 : 4294967295.0;
     std::vector<std::pair<std::uint64_t, std::uint32_t>> keyed(n);
     for (std::size_t i = 0; i < n; ++i) {
@@ -374,11 +377,47 @@ class Builder {
     if (cells_[hint_].v[D] == kInf) hint_ = cells_[hint_].n[D];
   }
 
+  // Morton key of a cell's position (centroid of its finite vertices) in the
+  // bounding box of the inserted points.
+  std::uint64_t cell_key(const Cell<D>& c) const {
+    const double bits = (D == 3) ? 2097151.0 : 4294967295.0;
+    double ctr[D] = {};
+    int nf = 0;
+    for (int j = 0; j <= D; ++j)
+      if (c.v[j] != kInf) {
+        for (int d = 0; d < D; ++d) ctr[d] += P(c.v[j])[d];
+        ++nf;
+      }
+    std::uint64_t key = 0;
+    for (int d = 0; d < D; ++d) {
+      const double ext = bhi_[d] - blo_[d];
+      const double t = ext > 0 ? (ctr[d] / nf - blo_[d]) / ext : 0.0;
+      const std::uint64_t q = static_cast<std::uint64_t>(std::min(bits, std::max(0.0, t * bits)));
+      key |= (D == 3 ? spread3(q) : spread2(q)) << d;
+    }
+    return key;
+  }
+
+  // Output rows in the order of a Morton curve through the cells' positions
+  // (ties by slot): consecutive rows of the SoA are neighbours in space, which
+  // is the layout the device kernels' coordinate gathers want.
+  // Any row order is a valid Triangulation; SBDT_HOST_ROW_ORDER=slot keeps the
+  // slot order of the construction (what the bench's row-order leg compares).
   TriSoA compact() {
     std::vector<std::uint32_t> remap(cells_.size(), kNone);
     std::size_t cnt = 0;
-    for (std::size_t i = 0; i < cells_.size(); ++i)
-      if (cells_[i].alive) remap[i] = static_cast<std::uint32_t>(cnt++);
+    const char* ord = std::getenv("SBDT_HOST_ROW_ORDER");
+    if (ord && std::string(ord) == "slot") {
+      for (std::size_t i = 0; i < cells_.size(); ++i)
+        if (cells_[i].alive) remap[i] = static_cast<std::uint32_t>(cnt++);
+    } else {
+      std::vector<std::pair<std::uint64_t, std::uint32_t>> keyed;
+      keyed.reserve(cells_.size());
+      for (std::size_t i = 0; i < cells_.size(); ++i)
+        if (cells_[i].alive) keyed.emplace_back(cell_key(cells_[i]), static_cast<std::uint32_t>(i));
+      std::sort(keyed.begin(), keyed.end());
+      for (const auto& kv : keyed) remap[kv.second] = static_cast<std::uint32_t>(cnt++);
+    }
     TriSoA t;
     t.dim = D;
     t.count = cnt;
@@ -419,6 +458,7 @@ class Builder {
   std::vector<Cell<D>> pending_;
   std::vector<Slot> table_;
   std::uint32_t hint_ = 0;
+  double blo_[D] = {}, bhi_[D] = {};
   mutable std::vector<double> scratch_;
 };
 
