@@ -621,10 +621,11 @@ constexpr int kFloorBias = 0x4B400000;
 // the exact stage's neighbour test (octant_proof).
 template <int D>
 __device__ __forceinline__ int prefilter_decide(const PfConst<D>& pc, const Sphere32<D>& sp, std::uint32_t self,
-                                                float* out_U, float* out_reach, float* out_rout,
-                                                std::uint32_t* out_mask, int* out_need, float* out_rp) {
+                                                const std::uint64_t f64, float* out_U, float* out_reach,
+                                                float* out_rout, std::uint32_t* out_mask, int* out_need,
+                                                float* out_rp) {
   // (straight-line: every test is evaluated and the outcome selected at the
-  // end; the row's field word is the only load)
+  // end; the row's field word f64 = field[cc] was loaded by prefilter_fast_negative)
   // R >= radius of the inflated binary64 sphere + distance between centres
   float slack = 0.f;
 #pragma unroll
@@ -655,13 +656,6 @@ __device__ __forceinline__ int prefilter_decide(const PfConst<D>& pc, const Sphe
     need = max(need, max(cc - a, b - cc));
     cb[d] = cc - kFloorBias;
   }
-  unsigned long long li;
-  if constexpr (D == 3)
-    li = static_cast<unsigned long long>(static_cast<unsigned>(cb[1]) + pc.dim1 * static_cast<unsigned>(cb[2])) * pc.dim0 +
-         static_cast<unsigned>(cb[0]);
-  else
-    li = static_cast<unsigned long long>(static_cast<unsigned>(cb[1])) * pc.dim0 + static_cast<unsigned>(cb[0]);
-  const std::uint64_t f64 = __ldg(pc.field + li);
   const std::uint32_t fw = static_cast<std::uint32_t>(f64);
   const std::uint32_t code = fw & 0xFFFFu;
   const int hs = static_cast<int>(fw >> 24);
@@ -707,6 +701,66 @@ __device__ __forceinline__ int prefilter_decide(const PfConst<D>& pc, const Sphe
   *out_rout = (inside && code == self) ? (need <= 1 ? Rp : -1.f) : kRoutNoMask;
   *out_reach = can_pos ? reach : -1.f;
   return neg ? 0 : (pos ? 1 : 2);
+}
+
+// The prefilter's pass over EVERY row: only the negative proof of
+// prefilter_decide, with an upper bound of its `need` that costs one floor
+// instead of two per axis; loads the field word *out_f64 = field[cc]. A row it
+// does not prove negative is deferred to the warp's batch, where
+// prefilter_decide runs in full on the recorded sphere (so the outcome of
+// every row is the one prefilter_decide gives: this pass only accepts rows
+// that prefilter_decide would also call negative).
+//   With the centre inside the grid (cc = floor(u), f = u - cc exact) and
+//   d = 6e-8 (|u| + Rp) >= the rounding of u -/+ Rp:
+//     floor(fl(u + Rp)) - cc <= floor(f + Rp + d),
+//     cc - floor(fl(u - Rp))  = ceil(Rp - f + d) <= floor(Rp + (1 - f) + d),
+//   and clipping the range to the grid only shrinks it, so
+//     need <= floor(Rp + max_d max(f_d, 1 - f_d) + d) =: need_u
+//   (evaluated with 3e-7 (um + Rp) + 1e-6 for d and the roundings of the sum).
+template <int D>
+__device__ __forceinline__ bool prefilter_fast_negative(const PfConst<D>& pc, const Sphere32<D>& sp,
+                                                        std::uint32_t self, std::uint64_t* out_f64) {
+  // (the same expressions as prefilter_decide up to Rp and cc)
+  float slack = 0.f;
+#pragma unroll
+  for (int d = 0; d < D; ++d) slack = fmaxf(slack, fabsf(sp.P0[d]) + fabsf(sp.rel[d]));
+  slack = (slack + pc.lo_mag) * 1e-15f;
+  const float R = fmaf(fmaf(sp.r, 1.000004f, 2.01f * sp.e), 1.000001f, slack);
+  const float Rc = fmaf(R * pc.inv_e, 1.000001f, pc.margin_c);
+  float Uc[D], um = 0.f;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    Uc[d] = (sp.P0[d] + sp.rel[d]) * pc.inv_e;
+    um = fmaxf(um, fabsf(Uc[d]));
+  }
+  const float sl = fmaf(4e-7f, um + Rc, 1e-6f);
+  const float Rp = Rc + sl;
+  const bool ok = um + Rp < 4194304.f;  // within floor_small's range (false for NaN)
+  int cb[D];
+  bool inside = ok;
+  float mfm = 0.f;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const float u = ok ? Uc[d] : 0.f;
+    const int c0 = __float_as_int(__fadd_rd(u, 12582912.f));
+    const int cc = min(max(c0, kFloorBias), pc.ctop[d]);
+    inside = inside && c0 == cc;
+    cb[d] = cc - kFloorBias;
+    const float f = u - static_cast<float>(cb[d]);  // exact when inside
+    mfm = fmaxf(mfm, fmaxf(f, 1.f - f));
+  }
+  unsigned long long li;
+  if constexpr (D == 3)
+    li = static_cast<unsigned long long>(static_cast<unsigned>(cb[1]) + pc.dim1 * static_cast<unsigned>(cb[2])) * pc.dim0 +
+         static_cast<unsigned>(cb[0]);
+  else
+    li = static_cast<unsigned long long>(static_cast<unsigned>(cb[1])) * pc.dim0 + static_cast<unsigned>(cb[0]);
+  const std::uint64_t f64 = __ldg(pc.field + li);
+  *out_f64 = f64;
+  const std::uint32_t fw = static_cast<std::uint32_t>(f64);
+  // (hs <= H + 1: any bound >= 8 reads as "too wide")
+  const int need_u = floor_small(fminf(fmaf(um + Rp, 3e-7f, mfm + Rp) + 1e-6f, 8.f));
+  return inside && (fw & 0xFFFFu) == self && need_u < static_cast<int>(fw >> 24);
 }
 
 // The neighbours of the centre cell c0 = floor(U) on the near side of U in
@@ -825,7 +879,7 @@ __device__ __forceinline__ int exact_mask_test(const std::uint32_t m, const floa
 constexpr unsigned kPfIters = PF_ITERS;
 constexpr unsigned kPfBatch = 64;  // per-warp batch of undecided rows (< 32 waiting + 32 arriving)
 template <int D>
-constexpr int kPfBatchWords = 2 * D + 8;
+constexpr int kPfBatchWords = 3 * D + 7;
 constexpr unsigned kPfChunk = 32 * kPfIters;
 
 template <int D, bool BIGK>
@@ -856,9 +910,8 @@ __global__ void __launch_bounds__(kBThreads, 4) k_border_prefilter(BorderArgs a,
   unsigned long long claim = 0;
   if (lane == 0) claim = atomicAdd(cursor, 2ull * kPfChunk);
   claim = __shfl_sync(0xffffffffu, claim, 0);
-  std::uint64_t base = row_begin + claim;
-  std::uint64_t next_base = base + kPfChunk;
-  constexpr unsigned wofs = 0;
+  const std::uint64_t base = row_begin + claim;
+  const std::uint64_t next_base = base + kPfChunk;
   unsigned it = 0;
   // binary32 cell-unit scale and margin (rounded up; the slacks cover the rest)
   // decode_row's coordinate unit: the fixed-point step in 3-D, 1 in 2-D
@@ -880,17 +933,32 @@ __global__ void __launch_bounds__(kBThreads, 4) k_border_prefilter(BorderArgs a,
     pc.dim0 = static_cast<unsigned>(og.ldims[0][0]);
     pc.dim1 = static_cast<unsigned>(og.ldims[0][1]);
   }
+  // Row bookkeeping in 32 bits (S < 2^32, capi.cu): a chunk is its first row
+  // and its number of rows inside [row_begin, row_end) (0: past the end).
+  auto span = [&](std::uint64_t b, std::uint32_t& first, std::uint32_t& count) {
+    const std::uint64_t left = b < row_end ? row_end - b : 0ull;
+    count = static_cast<std::uint32_t>(left < kPfChunk ? left : kPfChunk);
+    first = static_cast<std::uint32_t>(b);
+  };
+  std::uint32_t c_first, c_count, n_first, n_count;
+  span(base, c_first, c_count);
+  span(next_base, n_first, n_count);
+  const std::uint32_t last_row = static_cast<std::uint32_t>(row_end ? row_end - 1 : 0);
   // software pipeline: the vertex ids of the next row are in flight while
   // this row's coordinates are gathered and tested
-  std::uint64_t s = base + wofs + lane;
-  std::uint32_t self = part_of(s_off, a.k, s < row_end ? s : row_end - 1);
-  std::uint64_t next_off = self + 1 < a.k ? s_off[self + 1] : ~0ull;  // first row of the next part
-  std::uint32_t vn[D + 1];
-  auto load_ids = [&](std::uint64_t r, std::uint32_t* ids) {
-#pragma unroll
-    for (int j = 0; j <= D; ++j) ids[j] = r < row_end ? __ldcs(a.verts + std::uint64_t(j) * a.S + r) : kInfVertex;
+  std::uint32_t s = c_first + lane;  // this lane's row
+  bool valid = lane < c_count;
+  std::uint32_t self = part_of(s_off, a.k, valid ? s : last_row);
+  auto part_end = [&](std::uint32_t p) -> std::uint32_t {  // first row of the next part
+    return p + 1 < a.k ? static_cast<std::uint32_t>(s_off[p + 1]) : 0xFFFFFFFFu;
   };
-  load_ids(s, vn);
+  std::uint32_t next_off = part_end(self);
+  std::uint32_t vn[D + 1];
+  auto load_ids = [&](std::uint32_t r, bool ok, std::uint32_t* ids) {
+#pragma unroll
+    for (int j = 0; j <= D; ++j) ids[j] = ok ? __ldcs(a.verts + r + std::uint64_t(j) * a.S) : kInfVertex;
+  };
+  load_ids(s, valid, vn);
   // candidate-queue slots are claimed per warp in chunks of kQChunk (one
   // atomic per chunk instead of one per iteration on the single counter);
   // the slots a warp leaves unused at exit are written as kNoRow holes
@@ -916,47 +984,68 @@ __global__ void __launch_bounds__(kBThreads, 4) k_border_prefilter(BorderArgs a,
       cand[cap + q] = __float_as_uint(reach);
     }
   };
-  // Undecided rows wait in a per-warp batch (shared memory) until 32 have
-  // gathered; then every lane takes one and runs the binary32 neighbour
-  // proofs (foreign mask / near-octant codes) converged, and only the rows
-  // they leave open go to the exact stage's queue.
-  // {row, self, reach, rout, mask, U[D], vertex ids[D + 1], need, Rp}
+  // Rows the fast pass does not prove negative wait in a per-warp batch
+  // (shared memory) until 32 have gathered; then every lane takes one and
+  // runs, converged, the full decision (prefilter_decide on the recorded
+  // sphere and field word) and, for the rows it leaves open, the binary32
+  // neighbour proofs (foreign mask / near-octant codes); only the rows those
+  // leave open go to the queues of the later stages.
+  // {row, self, r, e (< 0: no binary32 sphere), field word lo/hi, P0[D], rel[D], vertex ids[D + 1]}
   std::uint32_t(&B)[kPfBatchWords<D>][kPfBatch] = s_bat[threadIdx.x >> 5];
   unsigned bcount = 0;
   auto flush_batch = [&](unsigned nproc) {
     __syncwarp();
     const unsigned e = bcount - nproc + lane;
     bool to_q = false, to_w = false, to_s = false;
-    std::uint32_t row = 0;
-    float reach = -1.f;
+    std::uint32_t row = 0, ids[D + 1];
+    float reach = -1.f, crp = -1.f, cU[D];
+    int cneed = kNeedUnknown;
+#pragma unroll
+    for (int d = 0; d < D; ++d) cU[d] = 0.f;
+#pragma unroll
+    for (int j = 0; j <= D; ++j) ids[j] = 0;
     if (lane < nproc) {
       row = B[0][e];
-      reach = __uint_as_float(B[2][e]);
-      const float rout = __uint_as_float(B[3][e]);
+      const std::uint32_t bself = B[1][e];
+#pragma unroll
+      for (int j = 0; j <= D; ++j) ids[j] = B[6 + 2 * D + j][e];
+      Sphere32<D> sp;
+      sp.r = __uint_as_float(B[2][e]);
+      sp.e = __uint_as_float(B[3][e]);
+      float rout = kRoutNoMask;
+      std::uint32_t cmask = 0;
+      int res = 2;
+      if (sp.e >= 0.f) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          sp.P0[d] = __uint_as_float(B[6 + d][e]);
+          sp.rel[d] = __uint_as_float(B[6 + D + d][e]);
+        }
+        const std::uint64_t f64 = static_cast<std::uint64_t>(B[4][e]) | (static_cast<std::uint64_t>(B[5][e]) << 32);
+        res = prefilter_decide<D>(pc, sp, bself, f64, cU, &reach, &rout, &cmask, &cneed, &crp);
+      } else {
+        reach = kReachCheckOrient;  // no binary32 sphere: the exact orientation decides degeneracy
+      }
+      if (a.counters && res == 1) atomicAdd(&a.counters[8], 1ull);
       // the centre cell's foreign mask (no loads: it came with the field
       // word), else (the centre's field code is not the row's part) the
       // near-octant neighbours' codes
-      int r = -1;
-      if (rout >= -1.f) {
-        float U[D];
-#pragma unroll
-        for (int d = 0; d < D; ++d) U[d] = __uint_as_float(B[5 + d][e]);
-        r = exact_mask_test<D>(B[4][e], U, reach, rout, a.exact != 0);
-      } else if (reach > 0.f && !a.exact) {  // (overlap-based: grid policy only)
-        float U[D];
-#pragma unroll
-        for (int d = 0; d < D; ++d) U[d] = __uint_as_float(B[5 + d][e]);
-        r = octant_proof<D>(og, a, U, reach, B[1][e]) ? 1 : -1;
+      int r = res == 2 ? -1 : res;
+      if (res == 2) {
+        if (rout >= -1.f)
+          r = exact_mask_test<D>(cmask, cU, reach, rout, a.exact != 0);
+        else if (reach > 0.f && !a.exact)  // (overlap-based: grid policy only)
+          r = octant_proof<D>(og, a, cU, reach, bself) ? 1 : -1;
+        if (a.counters && r >= 0) atomicAdd(&a.counters[r == 1 ? 10 : 15], 1ull);
       }
       if (r >= 0) {
         __stcs(a.positive + row, static_cast<std::uint8_t>(r));
         if (r == 1)
 #pragma unroll
-          for (int j = 0; j <= D; ++j) a.vflags[B[5 + D + j][e]] = 1;
-        if (a.counters) atomicAdd(&a.counters[r == 1 ? 10 : 15], 1ull);
-      } else if (reach != kReachCheckOrient && static_cast<int>(B[6 + 2 * D][e]) > kFlatHalf) {
+          for (int j = 0; j <= D; ++j) a.vflags[ids[j]] = 1;
+      } else if (reach != kReachCheckOrient && cneed > kFlatHalf) {
         to_w = true;  // wide cell range: the pyramid descent (k_border_wide), next to the exact stage
-      } else if (sq && reach != kReachCheckOrient && __uint_as_float(B[7 + 2 * D][e]) > 0.f) {
+      } else if (sq && reach != kReachCheckOrient && crp > 0.f) {
         to_s = true;  // the binary32 cell scan (k_border_scan32)
       } else {
         to_q = true;
@@ -973,8 +1062,8 @@ __global__ void __launch_bounds__(kBThreads, 4) k_border_prefilter(BorderArgs a,
           const std::uint64_t qs = sb + __popc(ms & lt);
           sq[qs] = row;
 #pragma unroll
-          for (int d = 0; d < D; ++d) sq[std::uint64_t(1 + d) * scap + qs] = B[5 + d][e];
-          sq[std::uint64_t(D + 1) * scap + qs] = B[7 + 2 * D][e];
+          for (int d = 0; d < D; ++d) sq[std::uint64_t(1 + d) * scap + qs] = __float_as_uint(cU[d]);
+          sq[std::uint64_t(D + 1) * scap + qs] = __float_as_uint(crp);
           sq[std::uint64_t(D + 2) * scap + qs] = __float_as_uint(reach);
         }
       }
@@ -982,7 +1071,7 @@ __global__ void __launch_bounds__(kBThreads, 4) k_border_prefilter(BorderArgs a,
     // wide rows: {row, vertex ids}, heavy ones from the front of the queue,
     // the others from the back when the queue is split (device path)
     {
-      const bool heavy = to_w && (!nwlight || static_cast<int>(B[6 + 2 * D][e]) > kWideHeavyNeed);
+      const bool heavy = to_w && (!nwlight || cneed > kWideHeavyNeed);
       const bool light = to_w && !heavy;
       const unsigned mh = __ballot_sync(0xffffffffu, heavy), ml = __ballot_sync(0xffffffffu, light);
       if (mh | ml) {
@@ -997,10 +1086,10 @@ __global__ void __launch_bounds__(kBThreads, 4) k_border_prefilter(BorderArgs a,
           const std::uint64_t q = heavy ? hb + __popc(mh & lt) : wcap - 1 - (lb + __popc(ml & lt));
           wq[q] = row;
 #pragma unroll
-          for (int j = 0; j <= D; ++j) wq[std::uint64_t(j + 1) * wcap + q] = B[5 + D + j][e];
+          for (int j = 0; j <= D; ++j) wq[std::uint64_t(j + 1) * wcap + q] = ids[j];
           // the recorded cell-unit centre and inner reach (exact policy: blocks inside it are accepted)
 #pragma unroll
-          for (int d = 0; d < D; ++d) wq[std::uint64_t(D + 2 + d) * wcap + q] = B[5 + d][e];
+          for (int d = 0; d < D; ++d) wq[std::uint64_t(D + 2 + d) * wcap + q] = __float_as_uint(cU[d]);
           wq[std::uint64_t(2 * D + 2) * wcap + q] = __float_as_uint(reach);
         }
       }
@@ -1009,68 +1098,64 @@ __global__ void __launch_bounds__(kBThreads, 4) k_border_prefilter(BorderArgs a,
     __syncwarp();
     append(to_q, row, reach);
   };
-  while (base < row_end) {
-    const bool valid = s < row_end;
+  while (c_count) {
     std::uint32_t v[D + 1];
     std::uint64_t w[D + 1];
 #pragma unroll
     for (int j = 0; j <= D; ++j) v[j] = vn[j];
     // the next row of this lane: the next 32 of the chunk, or the lookahead chunk
-    const std::uint64_t s_next = it + 1 < kPfIters ? s + 32 : next_base + wofs + lane;
-    load_ids(s_next, vn);
+    const bool same = it + 1 < kPfIters;
+    const std::uint32_t li_next = same ? (it + 1) * 32u + lane : lane;  // its index inside that chunk
+    const std::uint32_t s_next = (same ? c_first : n_first) + li_next;
+    const bool valid_next = li_next < (same ? c_count : n_count);
+    load_ids(s_next, valid_next, vn);
     const bool inf = valid && v[D] == kInfVertex;
-    bool is_cand = false;
-    float cU[D], creach = -1.f, crout = kRoutNoMask;  // recorded for the neighbour proofs
-    std::uint32_t cmask = 0;
-    int cneed = kNeedUnknown;
-    float crp = -1.f;
     // a warp's rows only grow (claims are monotonic): advance the part cursor
     {
-      const std::uint64_t sc = valid ? s : row_end - 1;
+      const std::uint32_t sc = valid ? s : last_row;
       while (next_off <= sc) {
         ++self;
-        next_off = self + 1 < a.k ? s_off[self + 1] : ~0ull;
+        next_off = part_end(self);
       }
     }
+    bool is_cand = false;
+    Sphere32<D> sp;
+    std::uint64_t f64 = 0;
     if (valid && !inf) {
       float A[D][D], P0e[D], eta;
-      Sphere32<D> sp;
       gather_row<D>(a.xq, v, a.n, w);
       decode_row<D>(w, A, sp.P0, P0e, &eta);
       // a binary32 sphere with its bound proves |det| > 0 (the orientation
       // of the binary64 vertices is nonzero); rows without one are checked
       // with the exact orientation in the exact stage (kReachCheckOrient)
-      int res = 2;
+      bool neg = false;
       if (enclosing_sphere_f32<D>(A, eta, P0e, sp))
-        res = prefilter_decide<D>(pc, sp, self, cU, &creach, &crout, &cmask, &cneed, &crp);
+        neg = prefilter_fast_negative<D>(pc, sp, self, &f64);
       else
-        creach = kReachCheckOrient;
-      if (a.counters && res == 1) atomicAdd(&a.counters[8], 1ull);
-      if (res == 2) {
+        sp.e = -1.f;
+      if (neg)
+        __stcs(a.positive + s, static_cast<std::uint8_t>(0));
+      else
         is_cand = true;
-      } else {
-        __stcs(a.positive + s, static_cast<std::uint8_t>(res));
-        if (res == 1)
-#pragma unroll
-          for (int j = 0; j <= D; ++j) a.vflags[v[j]] = 1;
-      }
     }
-    // undecided rows into the warp's batch
+    // deferred rows into the warp's batch
     {
       const unsigned mb = __ballot_sync(0xffffffffu, is_cand);
       if (is_cand) {
         const unsigned slot = bcount + __popc(mb & lt);
-        B[0][slot] = static_cast<std::uint32_t>(s);
+        B[0][slot] = s;
         B[1][slot] = self;
-        B[2][slot] = __float_as_uint(creach);
-        B[3][slot] = __float_as_uint(crout);
-        B[4][slot] = cmask;
-        B[6 + 2 * D][slot] = static_cast<std::uint32_t>(cneed);
-        B[7 + 2 * D][slot] = __float_as_uint(crp);
+        B[2][slot] = __float_as_uint(sp.r);
+        B[3][slot] = __float_as_uint(sp.e);
+        B[4][slot] = static_cast<std::uint32_t>(f64);
+        B[5][slot] = static_cast<std::uint32_t>(f64 >> 32);
 #pragma unroll
-        for (int d = 0; d < D; ++d) B[5 + d][slot] = __float_as_uint(cU[d]);
+        for (int d = 0; d < D; ++d) {
+          B[6 + d][slot] = __float_as_uint(sp.P0[d]);
+          B[6 + D + d][slot] = __float_as_uint(sp.rel[d]);
+        }
 #pragma unroll
-        for (int j = 0; j <= D; ++j) B[5 + D + j][slot] = v[j];
+        for (int j = 0; j <= D; ++j) B[6 + 2 * D + j][slot] = v[j];
       }
       bcount += __popc(mb);
       if (bcount >= 32) flush_batch(32);
@@ -1082,16 +1167,18 @@ __global__ void __launch_bounds__(kBThreads, 4) k_border_prefilter(BorderArgs a,
         unsigned bi = 0;
         if (lane == 0) bi = atomicAdd(a.inf_count, static_cast<unsigned>(__popc(mi)));
         bi = __shfl_sync(0xffffffffu, bi, 0);
-        if (inf) a.inf_queue[bi + __popc(mi & lt)] = static_cast<std::uint32_t>(s);
+        if (inf) a.inf_queue[bi + __popc(mi & lt)] = s;
       }
     }
     s = s_next;
+    valid = valid_next;
     if (++it == kPfIters) {  // warp-uniform
       it = 0;
       unsigned long long c2 = 0;
       if (lane == 0) c2 = atomicAdd(cursor, static_cast<unsigned long long>(kPfChunk));
-      base = next_base;
-      next_base = row_begin + __shfl_sync(0xffffffffu, c2, 0);
+      c_first = n_first;
+      c_count = n_count;
+      span(row_begin + __shfl_sync(0xffffffffu, c2, 0), n_first, n_count);
     }
   }
   if (bcount) flush_batch(bcount);
