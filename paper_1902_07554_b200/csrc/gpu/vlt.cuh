@@ -643,111 +643,167 @@ __global__ void __launch_bounds__(256) k_assign_vlt(const double* __restrict__ x
   double blo[D], bhi[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) blo[d] = INFINITY, bhi[d] = -INFINITY;
-  for (std::uint64_t i = i_begin + std::uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += std::uint64_t(gridDim.x) * blockDim.x) {
-    double x[D];
+  // Points whose record is a candidate list wait in a per-warp batch (shared
+  // memory) until 32 have gathered; then every lane takes one and the list
+  // decision runs with all lanes busy. PointIds are spatially random, so a
+  // warp's 32 points mix UNIFORM records (most of them: one lookup) with
+  // lists: deciding the lists in place ran the list code for every warp with
+  // a quarter of its lanes.
+  // {point id, entries pointer lo/hi, count, p[D] (offset from the box centre, binary32)}
+  constexpr int BW = 4 + D;
+  __shared__ std::uint32_t s_bat[8][BW][64];
+  std::uint32_t(&B)[BW][64] = s_bat[threadIdx.x >> 5];
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned lt = (1u << lane) - 1u;
+  unsigned bcount = 0;
+  auto decide_list = [&](std::uint64_t i, const VltEntry* ents, std::uint32_t cnt, const float* p) {
+    float pp = 0.f;
 #pragma unroll
-    for (int d = 0; d < D; ++d) {
-      x[d] = __ldcs(xyz + i * D + d);
-      blo[d] = fmin(blo[d], x[d]);
-      bhi[d] = fmax(bhi[d], x[d]);
-    }
-    double fcen[D];
-    std::uint32_t head = kHeadOverflow;
-    long long fid = 0;
-    vlt_locate<D>(x, sg, heads, subheads, &head, &fid, fcen);
-    std::uint32_t cnt = head & 15u;
-    if (cnt == 0) {
-      __stcs(labels + i, head >> 8);
-    } else if (cnt >= kHeadLong) {
-      const unsigned slot = atomicAdd(oq_count, 1u);
-      oq[slot] = static_cast<std::uint32_t>(i);
-    } else {
-      const VltEntry* ents = slab + fid * kSlots;
-      if (cnt == kHeadPool) {  // sub-box list in the long slab
-        ents = lslab + (head >> 4);
-        cnt = ents[0].idx;
-        ++ents;
-      }
-      float p[D], pp = 0.f;
+    for (int d = 0; d < D; ++d) pp += p[d] * p[d];
+    // binary32 distances with the rigorous bound 4e-6 (|p|^2 + |s|^2): one
+    // pass keeps the winner (smallest dd, first on ties) and the two
+    // smallest interval lower ends (no per-candidate arrays: registers only)
+    auto dist = [&](const float4& e, float* bnd) {
+      const float er[3] = {e.x, e.y, e.z};
+      float dd = 0.f, ss = 0.f;
 #pragma unroll
       for (int d = 0; d < D; ++d) {
-        p[d] = static_cast<float>(x[d] - fcen[d]);
-        pp += p[d] * p[d];
+        const float t = p[d] - er[d];
+        dd += t * t;
+        ss += er[d] * er[d];
       }
-      // binary32 distances with the rigorous bound 4e-6 (|p|^2 + |s|^2): one
-      // pass keeps the winner (smallest dd, first on ties) and the two
-      // smallest interval lower ends (no per-candidate arrays: registers only)
-      auto dist = [&](const float4& e, float* bnd) {
-        const float er[3] = {e.x, e.y, e.z};
-        float dd = 0.f, ss = 0.f;
+      *bnd = 4e-6f * (pp + ss) + 1e-30f;
+      return dd;
+    };
+    float bv = INFINITY, bb = 0.f, m1 = INFINITY, m2 = INFINITY;
+    int bj = 0, j1 = -1;
+    // entries in groups of 4 whose loads are in flight together (one L2
+    // latency per group instead of one per entry)
+    for (int j0 = 0; j0 < static_cast<int>(cnt); j0 += 4) {
+      float4 eg[4];
 #pragma unroll
-        for (int d = 0; d < D; ++d) {
-          const float t = p[d] - er[d];
-          dd += t * t;
-          ss += er[d] * er[d];
+      for (int u = 0; u < 4; ++u)
+        eg[u] = j0 + u < static_cast<int>(cnt) ? __ldg(reinterpret_cast<const float4*>(ents + j0 + u))
+                                                : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (j0 + u >= static_cast<int>(cnt)) break;
+        const int j = j0 + u;
+        float bnd;
+        const float dd = dist(eg[u], &bnd);
+        if (dd < bv) {
+          bv = dd;
+          bb = bnd;
+          bj = j;
         }
-        *bnd = 4e-6f * (pp + ss) + 1e-30f;
-        return dd;
-      };
-      float bv = INFINITY, bb = 0.f, m1 = INFINITY, m2 = INFINITY;
-      int bj = 0, j1 = -1;
-      // entries in groups of 4 whose loads are in flight together (one L2
-      // latency per group instead of one per entry)
-      for (int j0 = 0; j0 < static_cast<int>(cnt); j0 += 4) {
-        float4 eg[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          eg[u] = j0 + u < static_cast<int>(cnt) ? __ldg(reinterpret_cast<const float4*>(ents + j0 + u))
-                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (j0 + u >= static_cast<int>(cnt)) break;
-          const int j = j0 + u;
-          float bnd;
-          const float dd = dist(eg[u], &bnd);
-          if (dd < bv) {
-            bv = dd;
-            bb = bnd;
-            bj = j;
-          }
-          const float lo_end = dd - bnd;
-          if (lo_end < m1) {
-            m2 = m1;
-            m1 = lo_end;
-            j1 = j;
-          } else if (lo_end < m2) {
-            m2 = lo_end;
-          }
+        const float lo_end = dd - bnd;
+        if (lo_end < m1) {
+          m2 = m1;
+          m1 = lo_end;
+          j1 = j;
+        } else if (lo_end < m2) {
+          m2 = lo_end;
         }
       }
-      // decided iff every other candidate is provably farther
-      const float lim = bv + bb;
-      std::uint32_t lab;
-      if ((j1 == bj ? m2 : m1) > lim) {
-        lab = __ldg(sorted_labels + ents[bj].idx);
-      } else {
-        // exact binary64 argmin over the candidates whose interval overlaps
-        // the winner's (reference squared_distance, lowest pid on ties)
-        double best = INFINITY;
-        std::uint32_t bpid = 0xFFFFFFFFu;
-        lab = 0;
-        for (int j = 0; j < static_cast<int>(cnt); ++j) {
-          float bnd;
-          const float dd = dist(__ldg(reinterpret_cast<const float4*>(ents + j)), &bnd);
-          if (j != bj && dd - bnd > lim) continue;
-          const SampleRec rec = sorted[ents[j].idx];
-          const double d2 = sqdist<D>(x, rec.x);
-          if (d2 < best || (d2 == best && rec.pid < bpid)) {
-            best = d2;
-            bpid = rec.pid;
-            lab = rec.label;
-          }
-        }
-      }
-      __stcs(labels + i, lab);
     }
+    // decided iff every other candidate is provably farther
+    const float lim = bv + bb;
+    std::uint32_t lab;
+    if ((j1 == bj ? m2 : m1) > lim) {
+      lab = __ldg(sorted_labels + ents[bj].idx);
+    } else {
+      // exact binary64 argmin over the candidates whose interval overlaps
+      // the winner's (reference squared_distance, lowest pid on ties)
+      double x[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) x[d] = xyz[i * D + d];
+      double best = INFINITY;
+      std::uint32_t bpid = 0xFFFFFFFFu;
+      lab = 0;
+      for (int j = 0; j < static_cast<int>(cnt); ++j) {
+        float bnd;
+        const float dd = dist(__ldg(reinterpret_cast<const float4*>(ents + j)), &bnd);
+        if (j != bj && dd - bnd > lim) continue;
+        const SampleRec rec = sorted[ents[j].idx];
+        const double d2 = sqdist<D>(x, rec.x);
+        if (d2 < best || (d2 == best && rec.pid < bpid)) {
+          best = d2;
+          bpid = rec.pid;
+          lab = rec.label;
+        }
+      }
+    }
+    __stcs(labels + i, lab);
+  };
+  auto flush_batch = [&](unsigned nproc) {
+    __syncwarp();
+    if (lane < nproc) {
+      const unsigned e = bcount - nproc + lane;
+      float p[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) p[d] = __uint_as_float(B[4 + d][e]);
+      const VltEntry* ents = reinterpret_cast<const VltEntry*>(
+          static_cast<std::uintptr_t>(B[1][e]) | (static_cast<std::uintptr_t>(B[2][e]) << 32));
+      decide_list(B[0][e], ents, B[3][e], p);
+    }
+    bcount -= nproc;
+    __syncwarp();
+  };
+  const std::uint64_t stride = std::uint64_t(gridDim.x) * blockDim.x;
+  // (warp-uniform trip count: the lanes of a warp hold consecutive points)
+  for (std::uint64_t i0 = i_begin + std::uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u); i0 < n; i0 += stride) {
+    const std::uint64_t i = i0 + lane;
+    bool is_list = false;
+    const VltEntry* ents = nullptr;
+    std::uint32_t cnt = 0;
+    float p[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) p[d] = 0.f;
+    if (i < n) {
+      double x[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        x[d] = __ldcs(xyz + i * D + d);
+        blo[d] = fmin(blo[d], x[d]);
+        bhi[d] = fmax(bhi[d], x[d]);
+      }
+      double fcen[D];
+      std::uint32_t head = kHeadOverflow;
+      long long fid = 0;
+      vlt_locate<D>(x, sg, heads, subheads, &head, &fid, fcen);
+      cnt = head & 15u;
+      if (cnt == 0) {
+        __stcs(labels + i, head >> 8);
+      } else if (cnt >= kHeadLong) {
+        const unsigned slot = atomicAdd(oq_count, 1u);
+        oq[slot] = static_cast<std::uint32_t>(i);
+      } else {
+        is_list = true;
+        ents = slab + fid * kSlots;
+        if (cnt == kHeadPool) {  // sub-box list in the long slab
+          ents = lslab + (head >> 4);
+          cnt = ents[0].idx;
+          ++ents;
+        }
+#pragma unroll
+        for (int d = 0; d < D; ++d) p[d] = static_cast<float>(x[d] - fcen[d]);
+      }
+    }
+    const unsigned mb = __ballot_sync(0xffffffffu, is_list);
+    if (is_list) {
+      const unsigned slot = bcount + __popc(mb & lt);
+      const std::uintptr_t ep = reinterpret_cast<std::uintptr_t>(ents);
+      B[0][slot] = static_cast<std::uint32_t>(i);
+      B[1][slot] = static_cast<std::uint32_t>(ep);
+      B[2][slot] = static_cast<std::uint32_t>(ep >> 32);
+      B[3][slot] = cnt;
+#pragma unroll
+      for (int d = 0; d < D; ++d) B[4 + d][slot] = __float_as_uint(p[d]);
+    }
+    bcount += __popc(mb);
+    if (bcount >= 32) flush_batch(32);
   }
+  if (bcount) flush_batch(bcount);
   bbox_flush<D>(blo, bhi, bbox);
 }
 
