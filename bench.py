@@ -199,6 +199,8 @@ def config_dict(inst, policy, world, cells):
             "m": len(inst.sample_ids), "S": part.S, "policy": f"{policy}(c_G=1)", "cells": cells,
             "l2": "inputs > L2 (coords %d MB, simplices %d MB); the GPU arm also writes a 256 MB buffer (> L2) "
                   "between steps" % (inst.points.nbytes >> 20, (part.verts.nbytes + part.nbrs.nbytes) >> 20),
+            "row_order": "slot (construction order)" if os.environ.get("SBDT_HOST_ROW_ORDER") == "slot"
+                         else "morton (the host DT builder's compacted row order)",
             "parallelism": f"{world} independent instance(s), one per rank"}
 
 

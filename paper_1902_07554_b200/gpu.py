@@ -73,7 +73,7 @@ EXPORTS = [
 
 
 def lib_path() -> str:
-    return os.environ.get("SBDT_GPU_LIB_EXPERIMENT") or os.path.join(_HERE, "libsbdt_gpu.so")
+    return os.path.join(_HERE, "libsbdt_gpu.so")
 
 
 def lib():

@@ -28,4 +28,4 @@ def test_reference_arm_json_line():
     assert d["steps"] >= 1 and "full steps, measured" in d["cpu_baseline"]["sample"]
     assert d["cpu_baseline"]["single_core"]["cores"] == 1 and d["cpu_baseline"]["cpu_model"]
     # the same config keys as the product arm (bench.config_dict)
-    assert set(d["config"]) == {"workload", "n", "dim", "k", "m", "S", "policy", "cells", "l2", "parallelism"}
+    assert set(d["config"]) == {"workload", "n", "dim", "k", "m", "S", "policy", "cells", "l2", "row_order", "parallelism"}
