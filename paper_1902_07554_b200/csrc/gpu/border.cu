@@ -836,30 +836,33 @@ __device__ __forceinline__ int exact_mask_test(const std::uint32_t m, const floa
     h[d][2] = (2.f - f) * (2.f - f);
   }
   if (!m) return rout > 0.f ? 0 : -1;
-  float mn = INFINITY, mx = INFINITY;  // smallest squared box gap / far-corner distance over the foreign neighbours
-  if constexpr (D == 3) {
+  // smallest squared box gap (mn) and, under the exact policy only
+  // (`contain` is uniform over the launch), far-corner distance (mx) over
+  // the foreign neighbours
+  auto smallest = [&](const float (*t)[3]) {
+    float r = INFINITY;
+    if constexpr (D == 3) {
 #pragma unroll
-    for (int o2 = 0; o2 < 3; ++o2)
+      for (int o2 = 0; o2 < 3; ++o2)
 #pragma unroll
-      for (int o1 = 0; o1 < 3; ++o1) {
-        const float s12 = g[1][o1] + g[2][o2], t12 = h[1][o1] + h[2][o2];
+        for (int o1 = 0; o1 < 3; ++o1) {
+          const float s12 = t[1][o1] + t[2][o2];
+#pragma unroll
+          for (int o0 = 0; o0 < 3; ++o0)
+            if ((m >> (o0 + 3 * o1 + 9 * o2)) & 1u) r = fminf(r, t[0][o0] + s12);
+        }
+    } else {
+#pragma unroll
+      for (int o1 = 0; o1 < 3; ++o1)
 #pragma unroll
         for (int o0 = 0; o0 < 3; ++o0)
-          if ((m >> (o0 + 3 * o1 + 9 * o2)) & 1u) {
-            mn = fminf(mn, g[0][o0] + s12);
-            mx = fminf(mx, h[0][o0] + t12);
-          }
-      }
-  } else {
-#pragma unroll
-    for (int o1 = 0; o1 < 3; ++o1)
-#pragma unroll
-      for (int o0 = 0; o0 < 3; ++o0)
-        if ((m >> (o0 + 3 * o1)) & 1u) {
-          mn = fminf(mn, g[0][o0] + g[1][o1]);
-          mx = fminf(mx, h[0][o0] + h[1][o1]);
-        }
-  }
+          if ((m >> (o0 + 3 * o1)) & 1u) r = fminf(r, t[0][o0] + t[1][o1]);
+    }
+    return r;
+  };
+  const float mn = smallest(g);
+  float mx = INFINITY;
+  if (contain) mx = smallest(h);
   // (a few binary32 roundings of the squared distances, far inside the margins)
   const float prove = contain ? mx : mn;
   if (reach > 0.f && prove * 1.000002f + 1e-12f < reach * reach) return 1;
@@ -907,6 +910,7 @@ __global__ void __launch_bounds__(kBThreads, 4) k_border_prefilter(BorderArgs a,
   // chunks (no CTA barrier: the batch flushes make warps uneven), with one
   // chunk of lookahead for the id prefetch
   __shared__ std::uint32_t s_bat[kBThreads / 32][kPfBatchWords<D>][kPfBatch];
+  __shared__ std::uint32_t s_ids[kBThreads / 32][D + 1][32];  // the next row's vertex ids, per lane
   unsigned long long claim = 0;
   if (lane == 0) claim = atomicAdd(cursor, 2ull * kPfChunk);
   claim = __shfl_sync(0xffffffffu, claim, 0);
@@ -953,12 +957,22 @@ __global__ void __launch_bounds__(kBThreads, 4) k_border_prefilter(BorderArgs a,
     return p + 1 < a.k ? static_cast<std::uint32_t>(s_off[p + 1]) : 0xFFFFFFFFu;
   };
   std::uint32_t next_off = part_end(self);
-  std::uint32_t vn[D + 1];
-  auto load_ids = [&](std::uint32_t r, bool ok, std::uint32_t* ids) {
+  // (asynchronous copies into a per-warp staging area: LDGSTS, no destination
+  // registers held across the row's work; each lane stages and reads its own
+  // row, so cp.async.wait_group is the only synchronisation)
+  std::uint32_t(&I)[D + 1][32] = s_ids[threadIdx.x >> 5];
+  auto stage_ids = [&](std::uint32_t r, bool ok) {
+    if (ok) {
 #pragma unroll
-    for (int j = 0; j <= D; ++j) ids[j] = ok ? __ldcs(a.verts + r + std::uint64_t(j) * a.S) : kInfVertex;
+      for (int j = 0; j <= D; ++j) {
+        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(&I[j][lane]));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(a.verts + r + std::uint64_t(j) * a.S)
+                     : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  load_ids(s, valid, vn);
+  stage_ids(s, valid);
   // candidate-queue slots are claimed per warp in chunks of kQChunk (one
   // atomic per chunk instead of one per iteration on the single counter);
   // the slots a warp leaves unused at exit are written as kNoRow holes
@@ -1101,14 +1115,15 @@ __global__ void __launch_bounds__(kBThreads, 4) k_border_prefilter(BorderArgs a,
   while (c_count) {
     std::uint32_t v[D + 1];
     std::uint64_t w[D + 1];
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
 #pragma unroll
-    for (int j = 0; j <= D; ++j) v[j] = vn[j];
+    for (int j = 0; j <= D; ++j) v[j] = valid ? I[j][lane] : kInfVertex;
     // the next row of this lane: the next 32 of the chunk, or the lookahead chunk
     const bool same = it + 1 < kPfIters;
     const std::uint32_t li_next = same ? (it + 1) * 32u + lane : lane;  // its index inside that chunk
     const std::uint32_t s_next = (same ? c_first : n_first) + li_next;
     const bool valid_next = li_next < (same ? c_count : n_count);
-    load_ids(s_next, valid_next, vn);
+    stage_ids(s_next, valid_next);
     const bool inf = valid && v[D] == kInfVertex;
     // a warp's rows only grow (claims are monotonic): advance the part cursor
     {
