@@ -187,17 +187,92 @@ __global__ void k_reach_link(ReachArgs a, const std::uint32_t* __restrict__ ptot
   }
 }
 
-// every positive-positive link once (from the larger row): union-find with
-// path halving, the larger root hooked under the smaller one
+// The hooking runs in two phases. The rows come in a spatially coherent order
+// (the host builder's Morton order), so most links join ranks that are close:
+// phase 1 (k_reach_hook_tiles) takes a tile of kReachTile consecutive ranks
+// per CTA, runs the union-find over the links INSIDE the tile in shared
+// memory (same hooking rule: the larger root under the smaller one) and
+// writes every rank's tile root as its global parent; phase 2 (k_reach_hook)
+// unites over the links that leave a tile, on trees that are one hop deep.
+constexpr std::uint32_t kReachTile = 4096;
+constexpr unsigned kReachTileThreads = 512;
+
+__device__ __forceinline__ std::uint32_t find_root_sh(volatile std::uint32_t* sp, std::uint32_t v) {
+  std::uint32_t curr = sp[v];
+  if (curr != v) {
+    std::uint32_t next, prev = v;
+    while (curr > (next = sp[curr])) {
+      sp[prev] = next;
+      prev = curr;
+      curr = next;
+    }
+  }
+  return curr;
+}
+
+__global__ void __launch_bounds__(kReachTileThreads) k_reach_hook_tiles(ReachArgs a,
+                                                                        const std::uint32_t* __restrict__ ptotal,
+                                                                        const std::uint32_t* __restrict__ nrank) {
+  __shared__ std::uint32_t sp[kReachTile];
+  const std::uint32_t P = *ptotal;
+  const int D = a.dim;
+  const std::uint32_t ntiles = (P + kReachTile - 1) / kReachTile;
+  for (std::uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const std::uint32_t base = tile * kReachTile;
+    const std::uint32_t cnt = min(kReachTile, P - base);
+    // initial parents: the smallest in-tile smaller neighbour (no atomics)
+    for (std::uint32_t e = threadIdx.x; e < cnt; e += blockDim.x) {
+      std::uint32_t m = e;
+      for (int d = 0; d <= D; ++d) {
+        const std::uint32_t r = __ldg(nrank + std::uint64_t(d) * P + base + e);
+        if (r != kNoRank && r >= base) m = min(m, r - base);
+      }
+      sp[e] = m;
+    }
+    __syncthreads();
+    for (std::uint32_t e = threadIdx.x; e < cnt; e += blockDim.x)
+      for (int d = 0; d <= D; ++d) {
+        const std::uint32_t r = __ldg(nrank + std::uint64_t(d) * P + base + e);
+        if (r == kNoRank || r < base) continue;
+        std::uint32_t ra = find_root_sh(sp, e), rb = find_root_sh(sp, r - base);
+        while (ra != rb) {
+          if (ra < rb) {
+            const std::uint32_t ret = atomicCAS(&sp[rb], rb, ra);
+            if (ret == rb) break;
+            rb = ret;
+          } else {
+            const std::uint32_t ret = atomicCAS(&sp[ra], ra, rb);
+            if (ret == ra) break;
+            ra = ret;
+          }
+        }
+      }
+    __syncthreads();
+    // (no more hooks: the walks below only shorten paths, every stored value
+    // is an ancestor, and a root is recognised by sp[x] == x)
+    for (std::uint32_t e = threadIdx.x; e < cnt; e += blockDim.x) {
+      std::uint32_t x = sp[e];
+      while (x != sp[x]) x = sp[x];
+      a.parent[base + e] = base + x;
+    }
+    __syncthreads();
+  }
+}
+
+// every positive-positive link that leaves its tile, once (from the larger
+// row): union-find with path halving, the larger root hooked under the
+// smaller one
 __global__ void k_reach_hook(ReachArgs a, const std::uint32_t* __restrict__ ptotal,
                              const std::uint32_t* __restrict__ nrank) {
   const std::uint32_t P = *ptotal;
   const int D = a.dim;
-  for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x)
+  for (std::uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
+    const std::uint32_t base = i - i % kReachTile;
     for (int d = 0; d <= D; ++d) {
       const std::uint32_t r = nrank[std::uint64_t(d) * P + i];
-      if (r != kNoRank) unite(a.parent, i, r);
+      if (r != kNoRank && r < base) unite(a.parent, i, r);
     }
+  }
 }
 
 // roots of the seeds marked; then every row's root and a count of the rows
@@ -290,13 +365,14 @@ int reach_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
   exclusive_scan(wcnt, wpre, W, wbs, ptot, st, &ctx->launches);
   k_reach_init<<<blocks, 256, 0, st>>>(a);
   k_reach_link<<<blocks, 256, sh, st>>>(a, ptot, nrank);
+  k_reach_hook_tiles<<<static_cast<unsigned>(sms) * 4, kReachTileThreads, 0, st>>>(a, ptot, nrank);
   k_reach_hook<<<blocks, 256, 0, st>>>(a, ptot, nrank);
   k_reach_mark<<<blocks, 256, 0, st>>>(a, ptot);
   SBDT_CUDA_TRY(cudaMemsetAsync(unreached, 0, sizeof(unsigned), st));
   // nrank is free after the hooking: its first P words take the roots
   k_reach_roots<<<blocks, 256, 0, st>>>(a, ptot, unreached, nrank);
   k_reach_final<<<blocks, 256, 0, st>>>(a, ptot, unreached, in->d_vertex_flags, in->n, nrank);
-  ctx->launches += 8;
+  ctx->launches += 9;
   if (in->d_bfs_vertex_flags && in->d_bfs_vertex_ids && in->d_bfs_vertex_count) {
     const int rc = compact_flags(ctx, in->d_bfs_vertex_flags, in->n, in->d_bfs_vertex_ids, in->d_bfs_vertex_count);
     if (rc != kOk) return rc;
