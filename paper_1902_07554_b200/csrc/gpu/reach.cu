@@ -194,7 +194,7 @@ __global__ void k_reach_link(ReachArgs a, const std::uint32_t* __restrict__ ptot
 // memory (same hooking rule: the larger root under the smaller one) and
 // writes every rank's tile root as its global parent; phase 2 (k_reach_hook)
 // unites over the links that leave a tile, on trees that are one hop deep.
-constexpr std::uint32_t kReachTile = 4096;
+constexpr std::uint32_t kReachTile = 8192;
 constexpr unsigned kReachTileThreads = 1024;
 constexpr int kReachEpt = kReachTile / kReachTileThreads;  // ranks per thread
 
