@@ -583,11 +583,20 @@ __device__ __forceinline__ void og_block_box(const OwnerGrid<D>& og, int L, cons
   const int s = L * og_shift<D>();
 #pragma unroll
   for (int d = 0; d < D; ++d) {
-    const long long first = static_cast<long long>(c[d]) << s;
-    long long last1 = static_cast<long long>(c[d] + 1) << s;
-    if (last1 > og.g.dims[d]) last1 = og.g.dims[d];
-    blo[d] = cell_lo<D>(og.g, first, d);
-    bhi[d] = cell_lo<D>(og.g, last1, d);
+    if (og.ldims[0][d] <= (1 << 26)) {  // ((c + 1) << s stays below 2^30 at every level)
+      // 32-bit cell indices (the conversion to binary64 is exact either way:
+      // the same values as the 64-bit path, one I2F instead of a sequence)
+      const int first = c[d] << s;
+      const int last1 = min((c[d] + 1) << s, og.ldims[0][d]);
+      blo[d] = og.g.lo[d] + static_cast<double>(first) * og.g.edge;
+      bhi[d] = og.g.lo[d] + static_cast<double>(last1) * og.g.edge;
+    } else {
+      const long long first = static_cast<long long>(c[d]) << s;
+      long long last1 = static_cast<long long>(c[d] + 1) << s;
+      if (last1 > og.g.dims[d]) last1 = og.g.dims[d];
+      blo[d] = cell_lo<D>(og.g, first, d);
+      bhi[d] = cell_lo<D>(og.g, last1, d);
+    }
   }
 }
 
