@@ -746,7 +746,8 @@ __device__ __forceinline__ bool prefilter_fast_negative(const PfConst<D>& pc, co
     const int cc = min(max(c0, kFloorBias), pc.ctop[d]);
     inside = inside && c0 == cc;
     cb[d] = cc - kFloorBias;
-    const float f = u - static_cast<float>(cb[d]);  // exact when inside
+    // (cc carries the bits of 1.5 * 2^23 + cb: cb as a float without an I2F)
+    const float f = u - (__int_as_float(cc) - 12582912.f);  // exact when inside
     mfm = fmaxf(mfm, fmaxf(f, 1.f - f));
   }
   unsigned long long li;
