@@ -216,3 +216,43 @@ def test_zero_copy_hull_neighbours(ctx):
     assert np.array_equal(zc.positive_vertex_ids, ref.positive_vertex_ids)
     o = oracle.find_border(inst.points, part.labels, pt, "grid")
     assert np.array_equal(zc.positive, o["positive"])
+
+
+def _permuted(part, rng):
+    """The same partial DTs with each part's rows in a random order
+    (neighbour links are part-local row ids: remapped with the permutation)."""
+    v, nb, par = part.verts.copy(), part.nbrs.copy(), part.parity.copy()
+    for p in range(part.k):
+        a, b = int(part.offsets[p]), int(part.offsets[p + 1])
+        perm = rng.permutation(b - a)          # new row i holds old row perm[i]
+        inv = np.empty_like(perm)
+        inv[perm] = np.arange(b - a)
+        v[:, a:b] = part.verts[:, a:b][:, perm]
+        par[a:b] = part.parity[a:b][perm]
+        old_nb = part.nbrs[:, a:b][:, perm]
+        nb[:, a:b] = inv[old_nb].astype(np.uint32)
+    return host.Partials(part.offsets.copy(), v, nb, par), None
+
+
+@pytest.mark.parametrize("cfg,n,k", [(2, 200_000, 8), (5, 300_000, 16)])
+@pytest.mark.parametrize("order", ["slot", "shuffled"])
+def test_find_border_row_order_independent(cfg, n, k, order, ctx, monkeypatch):
+    """The host builder emits rows along a Morton curve (a layout decision for
+    the device kernels' gathers); find_border must give the same answer for
+    any row order: the builder's slot order and a random order per part, each
+    against the oracle on the same rows (positive and BFS flags, vertex sets)."""
+    inst = host.make_instance(cfg, n=n, k=k)
+    lab = oracle.assign_kdtree(inst.points, inst.sample_ids, inst.sample_labels)
+    if order == "slot":
+        monkeypatch.setenv("SBDT_HOST_ROW_ORDER", "slot")
+        part = host.attach_partials(inst, lab)
+    else:
+        monkeypatch.delenv("SBDT_HOST_ROW_ORDER", raising=False)
+        part, _ = _permuted(host.attach_partials(inst, lab), np.random.default_rng(5))
+    for policy in ("grid", "exact"):
+        g = gpu.find_border(inst.points, lab, part, gpu.IntersectionPolicy(policy, 1.0), hull_bfs=True, ctx=ctx)
+        o = oracle.find_border(inst.points, lab, part, policy)
+        assert np.array_equal(g.positive, o["positive"])
+        assert np.array_equal(g.border, o["border"])
+        assert np.array_equal(g.positive_vertex_ids, o["vertices_positive"])
+        assert np.array_equal(g.border_vertex_ids, o["vertices_border"])

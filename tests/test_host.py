@@ -122,3 +122,34 @@ def test_partials_cover_every_point_once():
         v = part.verts[:, lo:hi]
         ids = np.unique(v[v != 0xFFFFFFFF])
         assert np.array_equal(ids, np.nonzero(lab == p)[0])
+
+
+def _rows(tri):
+    """Row set with each row's neighbours as vertex tuples (order-independent form)."""
+    v, nb = tri.verts, tri.nbrs
+    key = [tuple(v[:, s]) for s in range(v.shape[1])]
+    return {key[s]: (tri.parity[s], frozenset(key[nb[d, s]] for d in range(v.shape[0]))) for s in range(v.shape[1])}
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_row_order_morton_vs_slot(dim, monkeypatch):
+    """compact() emits rows along a Morton curve (default) or in slot order
+    (SBDT_HOST_ROW_ORDER=slot): the same triangulation either way (rows,
+    parities, neighbour links), and the Morton order is the spatially coherent
+    one (fewer distinct vertices per 32 consecutive rows)."""
+    pts = host.generate("uniform", dim, 20000, 11)
+    ids = np.arange(20000, dtype=np.uint32)
+    monkeypatch.delenv("SBDT_HOST_ROW_ORDER", raising=False)
+    tm = host.triangulate(pts, ids, 7)
+    monkeypatch.setenv("SBDT_HOST_ROW_ORDER", "slot")
+    ts = host.triangulate(pts, ids, 7)
+    assert tm.verts.shape == ts.verts.shape
+    assert _rows(tm) == _rows(ts)
+    assert not np.array_equal(tm.verts, ts.verts)
+
+    def distinct(t):
+        g = t.verts.shape[1] // 32
+        blocks = t.verts[:, :g * 32].reshape(dim + 1, g, 32)
+        return np.mean([len(np.unique(blocks[:, i, :])) for i in range(0, g, 5)])
+
+    assert distinct(tm) < 0.7 * distinct(ts)
