@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-row-order", action="store_true", help="skip the slot-row-order leg")
     ap.add_argument("--ref-budget-s", type=float, default=180.0,
                     help="--impl reference: wall budget for the timed full CPU steps (at least 3 run)")
     ap.add_argument("--no-parity", action="store_true", help="skip the full-size parity leg (and the CPU baseline)")
@@ -385,10 +386,11 @@ def main():
     d_bvids = torch.empty(n, dtype=torch.int32, device=dev)
     d_bcnt = torch.zeros(1, dtype=torch.int64, device=dev)
 
-    def border_args(bfs: bool):
+    def border_args(bfs: bool, rows=None):
         a = gpu.BorderArgs()
         a.dim, a.d_xyz, a.n, a.d_labels, a.k = dim, P(d_xyz), n, P(d_lab), k
-        a.d_offsets, a.d_verts, a.d_nbrs, a.d_parity, a.S = P(d_off), P(d_verts), P(d_nbrs), P(d_par), S
+        r_off, r_verts, r_nbrs, r_par = rows or (d_off, d_verts, d_nbrs, d_par)
+        a.d_offsets, a.d_verts, a.d_nbrs, a.d_parity, a.S = P(r_off), P(r_verts), P(r_nbrs), P(r_par), S
         a.policy, a.c_G, a.flags = gpu.POLICY[args.policy], 1.0, gpu.HULL_BFS if bfs else 0
         a.d_bbox_ordered = P(d_bbox)
         a.d_positive, a.d_border = P(d_pos), P(d_bor) if bfs else None
@@ -480,6 +482,41 @@ def main():
     ms_bfs, stages_bfs, _ = timed(max(1, min(args.steps, 5)), bfs=True)
     n_vb_bfs = int(d_bcnt.item())
     n_pos = int(d_pos.sum().item())
+
+    # Row-order leg: the bench's partial DTs come from this repo's host builder,
+    # which emits rows along a Morton curve. The same
+    # step on the builder's slot order (the order of its construction, what a
+    # caller with spatially unordered rows sees), launched, a few steps.
+    row_order = None
+    if rank == 0 and world == 1 and not args.profile and not args.no_row_order \
+            and os.environ.get("SBDT_HOST_ROW_ORDER") != "slot":
+        os.environ["SBDT_HOST_ROW_ORDER"] = "slot"
+        try:
+            part_s = host.build_partials(inst.points, labels, k, inst.config["seed"], threads)
+        finally:
+            del os.environ["SBDT_HOST_ROW_ORDER"]
+        assert part_s.S == S and np.array_equal(part_s.offsets, part.offsets)
+        rows_s = (d_off, torch.from_numpy(part_s.verts.view(np.int32)).to(dev),
+                  torch.from_numpy(part_s.nbrs.view(np.int32)).to(dev), torch.from_numpy(part_s.parity).to(dev))
+        args_slot = border_args(False, rows_s)
+        keep = args_full
+        args_full = args_slot
+        try:
+            for _ in range(2):
+                step()
+            torch.cuda.synchronize()
+            ms_s, stages_s, _ = timed(max(1, min(args.steps, 5)))
+            ctx.synchronize()
+            assert int(d_pos.sum().item()) == n_pos and int(d_cnt.item()) == n_vb  # the same border, other row ids
+        finally:
+            args_full = keep
+        row_order = {"bench": "morton", "morton_launched_ms": round(sum(ms) / len(ms), 4),
+                     "slot_launched_ms": round(sum(ms_s) / len(ms_s), 4),
+                     "slot_prefilter_ms": round(stages_s.get("border.prefilter", 0.0), 4),
+                     "morton_prefilter_ms": round(stages.get("border.prefilter", 0.0), 4)}
+        del rows_s, part_s, args_slot
+        step()  # the device outputs of the bench's own rows again (parity leg below)
+        torch.cuda.synchronize()
     # this run's device outputs, for the full-size parity leg
     u32 = lambda t: t.cpu().numpy().view(np.uint32)  # noqa: E731
     g_out = {"labels": u32(d_lab), "parts_offsets": d_poff.cpu().numpy().view(np.uint64),
@@ -638,6 +675,7 @@ def main():
             "hull_bfs": {"ms_per_step": round(sum(ms_bfs) / len(ms_bfs), 4),
                          "stages_ms": {kk: round(v, 4) for kk, v in stages_bfs.items()},
                          "border_vertices": n_vb_bfs},
+            "row_order": row_order,
             "border_vertices": n_vb, "positive_simplices": n_pos, "assign_table": table_stats, "border_pipeline": border_stats,
             "gpu_launches": int(launches), "gpu_launches_per_step": launches / args.steps,
             "clocks": clocks, "wall_timed_s": round(t_wall, 3), "setup_s": round(setup_s, 1),
