@@ -32,6 +32,11 @@
 namespace sbdt_gpu {
 
 constexpr int kBThreads = 256;
+#ifndef PF_THREADS
+#define PF_THREADS 256
+#define PF_CTAS 4
+#endif
+constexpr int kPfThreads = PF_THREADS;  // prefilter CTA size / CTAs per SM (launch bound)
 constexpr std::uint32_t kSmemOffsMax = 1024;  // part offsets staged in shared memory up to this many (k + 1)
 
 __global__ void k_bbox_points_init(unsigned long long* bbox, int dim) {
@@ -887,7 +892,7 @@ constexpr int kPfBatchWords = 3 * D + 7;
 constexpr unsigned kPfChunk = 32 * kPfIters;
 
 template <int D, bool BIGK>
-__global__ void __launch_bounds__(kBThreads, 4) k_border_prefilter(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
+__global__ void __launch_bounds__(kPfThreads, PF_CTAS) k_border_prefilter(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
                                                                 std::uint32_t* __restrict__ cand, std::uint64_t cap,
                                                                 unsigned* __restrict__ ncand, std::uint64_t row_begin,
                                                                 std::uint64_t row_end,
@@ -910,8 +915,8 @@ __global__ void __launch_bounds__(kBThreads, 4) k_border_prefilter(BorderArgs a,
   // rows [row_begin, row_end); every warp iterates over its own claimed
   // chunks (no CTA barrier: the batch flushes make warps uneven), with one
   // chunk of lookahead for the id prefetch
-  __shared__ std::uint32_t s_bat[kBThreads / 32][kPfBatchWords<D>][kPfBatch];
-  __shared__ std::uint32_t s_ids[kBThreads / 32][D + 1][32];  // the next row's vertex ids, per lane
+  __shared__ std::uint32_t s_bat[kPfThreads / 32][kPfBatchWords<D>][kPfBatch];
+  __shared__ std::uint32_t s_ids[kPfThreads / 32][D + 1][32];  // the next row's vertex ids, per lane
   unsigned long long claim = 0;
   if (lane == 0) claim = atomicAdd(cursor, 2ull * kPfChunk);
   claim = __shfl_sync(0xffffffffu, claim, 0);
@@ -2638,12 +2643,12 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
       if (tiled && in->S > 0) {
         int per_sm = 1;
         const bool bigk = in->k + 1 > kSmemOffsMax;
-        if (bigk) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_prefilter<D, true>, kBThreads, 0);
-        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_prefilter<D, false>, kBThreads, offs_sh);
+        if (bigk) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_prefilter<D, true>, kPfThreads, 0);
+        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_border_prefilter<D, false>, kPfThreads, offs_sh);
         const std::uint64_t resA = std::uint64_t(sms) * std::uint64_t(per_sm > 0 ? per_sm : 1);
         // candidates <= rows, plus < kQChunk holes per prefilter warp and launch
         const std::uint64_t launches_A = ctx->chunks.empty() ? 1 : ctx->chunks.size();
-        const std::uint64_t qcap = in->S + 32 + launches_A * resA * (kBThreads / 32) * kQChunk;
+        const std::uint64_t qcap = in->S + 32 + launches_A * resA * (kPfThreads / 32) * kQChunk;
         SBDT_WS(cq, std::uint32_t, "border.cand", qcap * 2);  // SoA {row, reach (kReachCheckOrient marker)}
         // {candidates, cursor, wide rows, wide cursor, CTAs done (exact), CTAs done (wide)}
         // {candidates, cursor, wide rows, wide cursor, CTAs done (exact), CTAs done (wide), light wide rows}
@@ -2703,13 +2708,13 @@ int border_impl(sbdt_gpu_ctx* ctx, const sbdt_border_args* in) {
         const unsigned resW = static_cast<unsigned>(sms * (per_sm > 0 ? per_sm : 1));
         SBDT_WS(pfcur, unsigned long long, "border.pf_cursor", 1);
         auto prefilter = [&](std::uint64_t r0, std::uint64_t r1) -> int {
-          const std::uint64_t want = (r1 - r0 + kBThreads - 1) / kBThreads;
+          const std::uint64_t want = (r1 - r0 + kPfThreads - 1) / kPfThreads;
           SBDT_CUDA_TRY(cudaMemsetAsync(pfcur, 0, sizeof(unsigned long long), st));
           if (bigk)
-            k_border_prefilter<D, true><<<static_cast<unsigned>(want < resA ? want : resA), kBThreads, 0, st>>>(
+            k_border_prefilter<D, true><<<static_cast<unsigned>(want < resA ? want : resA), kPfThreads, 0, st>>>(
                 a, og, cq, qcap, cn, r0, r1, pfcur, pq, pcap, pn, pnlight, sq, scap, sn);
           else
-            k_border_prefilter<D, false><<<static_cast<unsigned>(want < resA ? want : resA), kBThreads, offs_sh, st>>>(
+            k_border_prefilter<D, false><<<static_cast<unsigned>(want < resA ? want : resA), kPfThreads, offs_sh, st>>>(
                 a, og, cq, qcap, cn, r0, r1, pfcur, pq, pcap, pn, pnlight, sq, scap, sn);
           return kOk;
         };
