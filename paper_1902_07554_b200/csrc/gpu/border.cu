@@ -1583,8 +1583,11 @@ __global__ void __launch_bounds__(kScanWarps * 32) k_border_scan32(BorderArgs a,
         r.inv[d] = static_cast<unsigned>(ceilf(__fdiv_rn(65536.f, static_cast<float>(max(span, 1)))));
       }
       // (a few binary32 roundings of the squared distances, far inside the margins)
-      r.rin2 = reach > 0.f ? reach * reach * 0.999998f - 1e-12f : -1.f;
-      r.rout2 = (rp * rp + 1e-6f) * 1.00001f;
+      // (the per-cell comparisons' own slack, d2 * 1.000002 + 1e-12 < rin2 and
+      // d2 * 0.99999 - 1e-6 <= rout2, folded into the thresholds with the
+      // rounding directed to the conservative side)
+      r.rin2 = reach > 0.f ? __fmul_rd((reach * reach * 0.999998f - 1e-12f) - 1e-12f, 0.999998f) : -1.f;
+      r.rout2 = __fmul_ru((rp * rp + 1e-6f) * 1.00001f + 1e-6f, 1.0000101f);
       r.self = self;
       if constexpr (Ex) {
         // the balls in coordinates: centre lo + U edge (binary64, ~1e-16
@@ -1648,7 +1651,7 @@ __global__ void __launch_bounds__(kScanWarps * 32) k_border_scan32(BorderArgs a,
         for (int i0 = 0; i0 < kFlatSpan; ++i0) {
           d2[i0] = r.g2[0][i0] + g12 + g2z;
           fw[i0] = kFieldEmptyBit;
-          if (i0 < static_cast<int>(r.span[0]) && d2[i0] * 0.99999f - 1e-6f <= r.rout2)
+          if (i0 < static_cast<int>(r.span[0]) && d2[i0] <= r.rout2)
             fw[i0] = static_cast<std::uint32_t>(__ldg(a.field + lb + i0));
         }
         const std::uint32_t sf = r.self;
@@ -1656,7 +1659,7 @@ __global__ void __launch_bounds__(kScanWarps * 32) k_border_scan32(BorderArgs a,
 #pragma unroll
           for (int i0 = 0; i0 < kFlatSpan; ++i0) {
             const bool foreign = !(fw[i0] & kFieldEmptyBit) && (fw[i0] & 0xFFFFu) != sf;
-            const bool in = d2[i0] * 1.000002f + 1e-12f < r.rin2;
+            const bool in = d2[i0] < r.rin2;
             hit = hit || (foreign && in);
             amb = amb || (foreign && !in);
           }
