@@ -1759,7 +1759,13 @@ __global__ void __launch_bounds__(256) k_border_orient(BorderArgs a, const std::
 // shared memory. Same decisions as og_sphere_hits_foreign (exact pruning),
 // without serialising a whole descent on one lane.
 constexpr int kWideWarps = 4;
-constexpr unsigned kWideClaim = 4;  // rows a warp claims at a time in the wide / hull kernels
+#ifndef WIDE_CLAIM
+#define WIDE_CLAIM 4
+#endif
+#ifndef WIDE_CTAS
+#define WIDE_CTAS 8
+#endif
+constexpr unsigned kWideClaim = WIDE_CLAIM;  // rows a warp claims at a time in the wide / hull kernels
 constexpr int kWideStack = 256;  // deeper stacks (> 4 levels of dense partial blocks) take the serial fallback
 
 template <int D>
@@ -1920,7 +1926,7 @@ __device__ bool warp_sphere_descent(const OwnerGrid<D>& og, const std::uint16_t*
 }
 
 template <int D, bool Ex>
-__global__ void __launch_bounds__(kWideWarps * 32, Ex ? 6 : 8) k_border_wide(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
+__global__ void __launch_bounds__(kWideWarps * 32, Ex ? 6 : WIDE_CTAS) k_border_wide(BorderArgs a, const OwnerGrid<D>* __restrict__ ogp,
                                                                  const std::uint32_t* __restrict__ wide,
                                                                  std::uint64_t cap,
                                                                  const unsigned* __restrict__ nwide_p,
