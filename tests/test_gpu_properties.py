@@ -256,3 +256,22 @@ def test_find_border_row_order_independent(cfg, n, k, order, ctx, monkeypatch):
         assert np.array_equal(g.border, o["border"])
         assert np.array_equal(g.positive_vertex_ids, o["vertices_positive"])
         assert np.array_equal(g.border_vertex_ids, o["vertices_border"])
+
+
+@pytest.mark.parametrize("seed", [101, 202])
+@pytest.mark.parametrize("cfg,n,k", [(1, 300_000, 16), (2, 400_000, 16), (3, 400_000, 16), (4, 500_000, 32),
+                                     (5, 600_000, 32)])
+def test_other_seeds_bit_exact(cfg, n, k, seed, ctx):
+    """The BASELINE configs' distributions under other seeds than the configs'
+    own (labels; positive and BFS flags and both vertex sets, grid + exact)."""
+    inst = host.make_instance(cfg, n=n, k=k, seed=seed)
+    lab = gpu.assign_points(inst.points, inst.sample_ids, inst.sample_labels, k, ctx=ctx).labels
+    assert np.array_equal(lab, oracle.assign_kdtree(inst.points, inst.sample_ids, inst.sample_labels))
+    part = host.attach_partials(inst, lab)
+    for policy in ("grid", "exact"):
+        g = gpu.find_border(inst.points, lab, part, gpu.IntersectionPolicy(policy, 1.0), hull_bfs=True, ctx=ctx)
+        o = oracle.find_border(inst.points, lab, part, policy)
+        assert np.array_equal(g.positive, o["positive"])
+        assert np.array_equal(g.border, o["border"])
+        assert np.array_equal(g.positive_vertex_ids, o["vertices_positive"])
+        assert np.array_equal(g.border_vertex_ids, o["vertices_border"])
